@@ -1,0 +1,226 @@
+/* sk_api.h -- C-ABI of the B200-native sparse-DNN engine (libsk_b200.so).
+ *
+ * Drop-in boundary for the hot path of the reference library `semikern`
+ * (/root/reference/proj).  The reference exposes a C++ value-type API in
+ * namespace semikern; this header is the plain-C surface a binding (ctypes,
+ * cgo, JNI, or the header-only C++ shim include/semikern_b200/semikern.hpp)
+ * links against.  Every entry point cites the reference interface it replaces.
+ *
+ * Conventions
+ *  - Orientation is the reference's: a weight matrix W_ref is m-by-m CSR whose
+ *    row i lists the in-edges of output neuron i; activations Y are m-by-n
+ *    neuron-major (neurons x samples), row-major (dnn.hpp:24-25).
+ *  - Storage is the reference's: u32 row_ptr[rows+1], u32 col_idx[nnz] strictly
+ *    increasing per row, f32 values[nnz] (matrix.hpp:29,74-116).
+ *  - Handles (sk_csr, sk_dense, sk_model) own device memory and are immutable
+ *    after creation, like the reference's value types; the caller frees every
+ *    handle it receives.  Operations allocate new output handles.
+ *  - Work is stream-ordered on the context's CUDA stream.  Calls that return
+ *    host data (downloads, counts, error checks) synchronise that stream.
+ *  - Errors: every call returns sk_status; sk_last_error() gives a
+ *    thread-local message.  The codes map 1:1 onto the reference's exception
+ *    classes (error.hpp:24-58): DIMENSION -> DimensionError, DOMAIN ->
+ *    DomainError (raised from inside a kernel via a device error word),
+ *    INVALID_ARGUMENT -> InvalidArgument, ERROR -> Error.
+ *  - There is no CPU fallback: without a usable CUDA device every call that
+ *    needs one returns SK_ERR_CUDA.
+ */
+#ifndef SK_API_H
+#define SK_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sk_status {
+  SK_OK = 0,
+  SK_ERR = 1,                  /* semikern::Error */
+  SK_ERR_DIMENSION = 2,        /* semikern::DimensionError */
+  SK_ERR_DOMAIN = 3,           /* semikern::DomainError */
+  SK_ERR_INVALID_ARGUMENT = 4, /* semikern::InvalidArgument */
+  SK_ERR_PARSE = 5,            /* semikern::ParseError (not used on this path) */
+  SK_ERR_OOM = 6,              /* device allocation failed (cf. SkippedRun, bench.hpp:64-79) */
+  SK_ERR_CUDA = 7              /* CUDA runtime failure / no device */
+} sk_status;
+
+/* Order of semikern::SemiringKind (semiring.hpp:34). */
+typedef enum sk_semiring {
+  SK_ARITHMETIC = 0,
+  SK_MAX_PLUS = 1,
+  SK_MIN_MAX = 2,
+  SK_GF2 = 3
+} sk_semiring;
+
+typedef struct sk_ctx sk_ctx;
+typedef struct sk_csr sk_csr;
+typedef struct sk_dense sk_dense;
+typedef struct sk_model sk_model;
+
+/* Options of a forward pass; mirrors semikern::ForwardOptions (dnn.hpp:49-56)
+ * plus the BASELINE clip.  `workers` is accepted and ignored: the GPU result is
+ * bitwise independent of it, as the reference guarantees (dnn.hpp:75-76).
+ * `clip` > 0 clamps activations from above after the ReLU (Graph-Challenge
+ * style, BASELINE cfg3-5); 0 disables it (the reference has no clip). */
+typedef struct sk_fwd_opts {
+  int workers;
+  int materialize_bias;
+  float clip;
+} sk_fwd_opts;
+
+/* ---- library / context ------------------------------------------------- */
+const char* sk_last_error(void);
+const char* sk_version(void);
+/* Number of kernel launches this process has issued through the library. */
+uint64_t sk_kernel_launch_count(void);
+
+sk_status sk_ctx_create(int device, sk_ctx** out);
+sk_status sk_ctx_destroy(sk_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL = own. */
+sk_status sk_ctx_set_stream(sk_ctx* ctx, void* cuda_stream);
+void* sk_ctx_stream(const sk_ctx* ctx);
+sk_status sk_ctx_synchronize(sk_ctx* ctx);
+/* Measurement hook (no reference counterpart): when enabled, the library
+ * records a CUDA-event pair on the context stream around every launch of the
+ * dominant kernel (the per-layer SpGEMM / SpMM); sk_ctx_kernel_times returns
+ * their durations in ms (synchronising) and resets the list. */
+sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable);
+sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count);
+/* Page-lock / unlock a caller host buffer for async copies. */
+sk_status sk_host_register(void* p, size_t bytes);
+sk_status sk_host_unregister(void* p);
+
+/* ---- dense matrices (semikern::DenseMatrix, matrix.hpp:39-72) ----------- */
+sk_status sk_dense_create(sk_ctx* ctx, uint32_t rows, uint32_t cols, float fill,
+                          sk_dense** out);
+sk_status sk_dense_upload(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                          const float* host, sk_dense** out);
+/* Copy into an existing handle of the same shape (stream-ordered). */
+sk_status sk_dense_write(sk_ctx* ctx, sk_dense* d, const float* host);
+sk_status sk_dense_download(sk_ctx* ctx, const sk_dense* d, float* host);
+/* Stream-ordered download; the caller synchronises. */
+sk_status sk_dense_download_async(sk_ctx* ctx, const sk_dense* d, float* host);
+sk_status sk_dense_shape(const sk_dense* d, uint32_t* rows, uint32_t* cols);
+float* sk_dense_device_ptr(const sk_dense* d);
+sk_status sk_dense_identity(sk_ctx* ctx, uint32_t n, sk_dense** out);
+sk_status sk_dense_free(sk_dense* d);
+
+/* ---- CSR matrices (semikern::CsrMatrix, matrix.hpp:74-116) ------------ */
+/* csr_from_triples (matrix.hpp:144-150, matrix.cpp:145-189): any order; exact
+ * 0.0 values dropped; out-of-range index or duplicate coordinate ->
+ * SK_ERR_INVALID_ARGUMENT with the reference's message. Host triples. */
+sk_status sk_csr_from_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                              const uint32_t* row, const uint32_t* col,
+                              const float* val, size_t n, sk_csr** out);
+/* Validating (validate=1, matrix.cpp:89-119) or trusted (validate=0,
+ * from_parts_unchecked, matrix.cpp:76-87) construction from host arrays. */
+sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                            const uint32_t* row_ptr, const uint32_t* col_idx,
+                            const float* values, int validate, sk_csr** out);
+sk_status sk_csr_shape(const sk_csr* a, uint32_t* rows, uint32_t* cols,
+                       size_t* nnz);
+/* extractTuples / span accessors (matrix.hpp:99-108): D2H copy of the three
+ * arrays; any pointer may be NULL. */
+sk_status sk_csr_extract(sk_ctx* ctx, const sk_csr* a, uint32_t* row_ptr,
+                         uint32_t* col_idx, float* values);
+sk_status sk_csr_free(sk_csr* a);
+
+/* to_dense (matrix.hpp:154-155), from_dense = select(!= 0) (matrix.hpp:158),
+ * nnz (matrix.hpp:161). */
+sk_status sk_to_dense(sk_ctx* ctx, const sk_csr* a, float ambient_zero,
+                      sk_dense** out);
+sk_status sk_from_dense(sk_ctx* ctx, const sk_dense* d, sk_csr** out);
+sk_status sk_dense_nnz(sk_ctx* ctx, const sk_dense* d, size_t* out);
+
+/* ---- element-wise (matrix.hpp:181-191; union semantics matrix.cpp:253-312) */
+sk_status sk_ewise_dense(sk_ctx* ctx, int mul, const sk_dense* a,
+                         const sk_dense* b, sk_semiring s, sk_dense** out);
+sk_status sk_ewise_csr(sk_ctx* ctx, int mul, const sk_csr* a, const sk_csr* b,
+                       sk_semiring s, sk_csr** out);
+/* sparse (op) dense -> dense; sparse_is_left selects operand order. */
+sk_status sk_ewise_mixed(sk_ctx* ctx, int mul, const sk_csr* sp,
+                         const sk_dense* dn, int sparse_is_left, sk_semiring s,
+                         sk_dense** out);
+
+/* ---- mxm (matrix.hpp:202-218) ----------------------------------------- */
+sk_status sk_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const sk_dense* b,
+                           sk_semiring s, sk_dense** out);
+sk_status sk_mxm_dense_dense(sk_ctx* ctx, const sk_dense* a, const sk_dense* b,
+                             sk_semiring s, sk_dense** out);
+sk_status sk_mxm_csr_csr(sk_ctx* ctx, const sk_csr* a, const sk_csr* b,
+                         sk_semiring s, sk_csr** out);
+/* dense_mxm_baseline (matrix.hpp:217-218): tcgen05 tensor-core GEMM
+ * (3xTF32, fp32-class accuracy; within kRelTol of the scalar product). */
+sk_status sk_dense_mxm_baseline(sk_ctx* ctx, const sk_dense* a,
+                                const sk_dense* b, sk_dense** out);
+
+/* ---- DNN (dnn.hpp:31-89) ----------------------------------------------- */
+/* DnnModel (dnn.hpp:31-47, dnn.cpp:23-51): L square CSR layers of one width
+ * plus host bias vectors (copied).  Handles are borrowed, not consumed. */
+sk_status sk_model_create(sk_ctx* ctx, uint32_t layers,
+                          const sk_csr* const* weights,
+                          const float* const* biases, sk_model** out);
+sk_status sk_model_shape(const sk_model* m, uint32_t* layers, uint32_t* neurons);
+sk_status sk_model_free(sk_model* m);
+
+/* layer_step (dnn.hpp:66-72, dnn.cpp:86-103) as ONE fused kernel:
+ * Z = W.Y (ascending-k fold) ; Z + b ; ReLU ; optional clip. Host bias. */
+sk_status sk_layer_step(sk_ctx* ctx, const sk_csr* w, const float* bias,
+                        const sk_dense* y, const sk_fwd_opts* opt,
+                        sk_dense** out);
+/* relu_forward (dnn.hpp:77-78, dnn.cpp:111-121) on dense activations. */
+sk_status sk_relu_forward(sk_ctx* ctx, const sk_model* m, const sk_dense* y0,
+                          const sk_fwd_opts* opt, sk_dense** out);
+/* Host-to-host convenience: H2D(y0) -> relu_forward -> D2H(yL). */
+sk_status sk_relu_forward_host(sk_ctx* ctx, const sk_model* m, uint32_t n,
+                               const float* y0, const sk_fwd_opts* opt,
+                               float* yL);
+/* Sparse-activation forward (BASELINE cfg3-5): Y0 is an m-by-n CSR; every
+ * layer is SpGEMM + bias + ReLU (+clip) + prune of exact zeros; result is the
+ * CSR Y_L.  Values/pattern bitwise equal to the reference's
+ * mxm(CsrMatrix,CsrMatrix) (matrix.cpp:452-521) followed by the layer
+ * epilogue of dnn.cpp:65-103.  nnz_trace (optional, L+1 entries) receives
+ * nnz(Y_k).  */
+sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m,
+                                 const sk_csr* y0, const sk_fwd_opts* opt,
+                                 sk_csr** out, uint64_t* nnz_trace);
+/* Category set of a result: sorted indices of samples (columns) holding any
+ * nonzero; returns the count; idx may be NULL to size. */
+sk_status sk_categories_csr(sk_ctx* ctx, const sk_csr* y, uint32_t* idx,
+                            size_t cap, size_t* count);
+sk_status sk_categories_dense(sk_ctx* ctx, const sk_dense* y, uint32_t* idx,
+                              size_t cap, size_t* count);
+
+/* dense_layer_step / dense_relu_forward (dnn.hpp:85-89, dnn.cpp:123-149):
+ * the dense comparator on tcgen05 tensor cores (3xTF32, fused bias+ReLU). */
+sk_status sk_dense_layer_step(sk_ctx* ctx, const sk_dense* w, const float* bias,
+                              const sk_dense* y, sk_dense** out);
+sk_status sk_dense_relu_forward(sk_ctx* ctx, const sk_model* m,
+                                const sk_dense* y0, sk_dense** out);
+
+/* ---- BASELINE workload generators (device-side, bitwise equal to
+ * oracle/sk_oracle.c) ----------------- */
+/* Weight layer with exactly k nonzeros per row of W (Y.W orientation), in
+ * reference orientation W_ref = W^T.  value NaN -> U[-1,1) values. */
+sk_status sk_gen_layer_fixed(sk_ctx* ctx, uint32_t m, uint32_t k,
+                             uint64_t layer_seed, float value, sk_csr** out);
+/* Bernoulli(density) layer with U[-1,1) values (cfg2). */
+sk_status sk_gen_layer_density(sk_ctx* ctx, uint32_t m, double density,
+                               uint64_t layer_seed, sk_csr** out);
+/* Dense U[0,1) neuron-major input = the reference gen_input formula. */
+sk_status sk_gen_input_dense(sk_ctx* ctx, uint32_t m, uint32_t n,
+                             uint64_t seed, sk_dense** out);
+/* Binary input: every sample has exactly k active neurons (value 1.0);
+ * neuron-major CSR m x n.  sample_offset shifts the sample counter (batch-row
+ * shards generate their own slice of one global batch). */
+sk_status sk_gen_input_binary(sk_ctx* ctx, uint32_t m, uint32_t n, uint32_t k,
+                              uint64_t seed, uint64_t sample_offset,
+                              sk_csr** out);
+uint64_t sk_layer_seed(uint64_t seed, uint32_t layer);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SK_API_H */

@@ -1,0 +1,297 @@
+// TEST INFRASTRUCTURE ONLY -- never linked into the product library.
+//
+// extern "C" shim over the UNMODIFIED reference library (semikern, compiled
+// from /root/reference/proj/src by oracle/Makefile into oracle/_ref/).  It
+// exists so that Python tests, the golden-fixture generator and bench.py's
+// reference arm can call the reference's own hot-path functions through
+// ctypes.  Every function below forwards to the reference API named in its
+// comment; nothing here re-implements arithmetic.
+//
+// Reference interfaces wrapped (paths relative to /root/reference):
+//   csr_from_triples            proj/include/semikern/matrix.hpp:144-150
+//   CsrMatrix validating ctor   proj/include/semikern/matrix.hpp:84-89
+//   from_dense / to_dense       proj/include/semikern/matrix.hpp:154-159
+//   mxm (4 overloads)           proj/include/semikern/matrix.hpp:202-211
+//   ewise_add / ewise_mul       proj/include/semikern/matrix.hpp:186-191
+//   dense_mxm_baseline          proj/include/semikern/matrix.hpp:217-218
+//   layer_step / relu_forward   proj/include/semikern/dnn.hpp:66-78
+//   dense_layer_step / dense_relu_forward  proj/include/semikern/dnn.hpp:85-89
+//   gen_weight / gen_input / gen_bias      proj/include/semikern/matgen.hpp:46-52
+//   SplitMix64::at              proj/include/semikern/rng.hpp:43-46
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "semikern/dnn.hpp"
+#include "semikern/error.hpp"
+#include "semikern/matgen.hpp"
+#include "semikern/matrix.hpp"
+#include "semikern/rng.hpp"
+#include "semikern/semiring.hpp"
+
+using namespace semikern;
+
+namespace {
+
+thread_local std::string g_msg;
+
+// Status codes shared with include/sk_api.h (SK_OK ... SK_ERR_PARSE).
+enum : int {
+  kOk = 0,
+  kErr = 1,
+  kDim = 2,
+  kDomain = 3,
+  kInvalid = 4,
+  kParse = 5,
+};
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const DimensionError& e) {
+    g_msg = e.what();
+    return kDim;
+  } catch (const DomainError& e) {
+    g_msg = e.what();
+    return kDomain;
+  } catch (const InvalidArgument& e) {
+    g_msg = e.what();
+    return kInvalid;
+  } catch (const ParseError& e) {
+    g_msg = e.what();
+    return kParse;
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    return kErr;
+  }
+}
+
+Semiring semiring_of(int kind) {
+  switch (kind) {
+    case 0: return arithmetic_semiring();
+    case 1: return max_plus_semiring();
+    case 2: return min_max_semiring();
+    case 3: return gf2_semiring();
+  }
+  throw InvalidArgument("unknown semiring kind " + std::to_string(kind));
+}
+
+CsrMatrix csr_of(uint32_t rows, uint32_t cols, const uint32_t* rp,
+                 const uint32_t* ci, const float* v) {
+  const std::size_t nnz = rp[rows];
+  return CsrMatrix(rows, cols, std::vector<index_t>(rp, rp + rows + 1),
+                   std::vector<index_t>(ci, ci + nnz),
+                   std::vector<Scalar>(v, v + nnz));
+}
+
+DenseMatrix dense_of(uint32_t rows, uint32_t cols, const float* d) {
+  return DenseMatrix(rows, cols,
+                     std::vector<Scalar>(d, d + std::size_t(rows) * cols));
+}
+
+void copy_out(const DenseMatrix& m, float* out) {
+  std::memcpy(out, m.data().data(), m.data().size_bytes());
+}
+
+}  // namespace
+
+/// Opaque owner of a reference CsrMatrix result.
+struct skref_csr {
+  CsrMatrix m;
+};
+
+extern "C" {
+
+const char* skref_last_error(void) { return g_msg.c_str(); }
+
+// --- rng -------------------------------------------------------------------
+uint64_t skref_splitmix_at(uint64_t seed, uint64_t idx) {
+  return SplitMix64::at(seed, idx);
+}
+
+// --- CSR handles --------------------------------------------------------------
+int skref_csr_from_triples(uint32_t rows, uint32_t cols, const uint32_t* r,
+                           const uint32_t* c, const float* v, size_t n,
+                           skref_csr** out) {
+  return guarded([&] {
+    std::vector<Triple> t(n);
+    for (size_t i = 0; i < n; ++i) t[i] = Triple{r[i], c[i], v[i]};
+    *out = new skref_csr{csr_from_triples(rows, cols, t)};
+  });
+}
+
+int skref_csr_from_parts(uint32_t rows, uint32_t cols, const uint32_t* rp,
+                         const uint32_t* ci, const float* v, skref_csr** out) {
+  return guarded([&] { *out = new skref_csr{csr_of(rows, cols, rp, ci, v)}; });
+}
+
+int skref_csr_from_dense(uint32_t rows, uint32_t cols, const float* d,
+                         skref_csr** out) {
+  return guarded(
+      [&] { *out = new skref_csr{from_dense(dense_of(rows, cols, d))}; });
+}
+
+size_t skref_csr_nnz(const skref_csr* a) { return a->m.nnz(); }
+uint32_t skref_csr_rows(const skref_csr* a) { return a->m.rows(); }
+uint32_t skref_csr_cols(const skref_csr* a) { return a->m.cols(); }
+
+void skref_csr_extract(const skref_csr* a, uint32_t* rp, uint32_t* ci,
+                       float* v) {
+  const auto r = a->m.row_ptr();
+  const auto c = a->m.col_idx();
+  const auto x = a->m.values();
+  if (rp) std::memcpy(rp, r.data(), r.size_bytes());
+  if (ci) std::memcpy(ci, c.data(), c.size_bytes());
+  if (v) std::memcpy(v, x.data(), x.size_bytes());
+}
+
+void skref_csr_free(skref_csr* a) { delete a; }
+
+int skref_to_dense(const skref_csr* a, float ambient_zero, float* out) {
+  return guarded([&] { copy_out(to_dense(a->m, ambient_zero), out); });
+}
+
+// --- mxm ------------------------------------------------------------------------
+int skref_mxm_csr_dense(const skref_csr* a, uint32_t brows, uint32_t bcols,
+                        const float* b, int semiring, int workers, float* out) {
+  return guarded([&] {
+    copy_out(mxm(a->m, dense_of(brows, bcols, b), semiring_of(semiring), workers),
+             out);
+  });
+}
+
+int skref_mxm_dense_dense(uint32_t arows, uint32_t acols, const float* a,
+                          uint32_t brows, uint32_t bcols, const float* b,
+                          int semiring, int workers, float* out) {
+  return guarded([&] {
+    copy_out(mxm(dense_of(arows, acols, a), dense_of(brows, bcols, b),
+                 semiring_of(semiring), workers),
+             out);
+  });
+}
+
+int skref_mxm_csr_csr(const skref_csr* a, const skref_csr* b, int semiring,
+                      int workers, skref_csr** out) {
+  return guarded([&] {
+    *out = new skref_csr{mxm(a->m, b->m, semiring_of(semiring), workers)};
+  });
+}
+
+int skref_dense_mxm_baseline(uint32_t arows, uint32_t acols, const float* a,
+                             uint32_t brows, uint32_t bcols, const float* b,
+                             int workers, float* out) {
+  return guarded([&] {
+    copy_out(dense_mxm_baseline(dense_of(arows, acols, a),
+                                dense_of(brows, bcols, b), workers),
+             out);
+  });
+}
+
+// --- element-wise -------------------------------------------------------------
+int skref_ewise_dense(int mul, uint32_t rows, uint32_t cols, const float* a,
+                      const float* b, int semiring, float* out) {
+  return guarded([&] {
+    const DenseMatrix da = dense_of(rows, cols, a);
+    const DenseMatrix db = dense_of(rows, cols, b);
+    const Semiring s = semiring_of(semiring);
+    copy_out(mul ? ewise_mul(da, db, s) : ewise_add(da, db, s), out);
+  });
+}
+
+// Sparse (+) sparse keeps union semantics (matrix.cpp:253-290).
+int skref_ewise_csr(int mul, const skref_csr* a, const skref_csr* b,
+                    int semiring, skref_csr** out) {
+  return guarded([&] {
+    const Semiring s = semiring_of(semiring);
+    Matrix r = mul ? ewise_mul(Matrix(a->m), Matrix(b->m), s)
+                   : ewise_add(Matrix(a->m), Matrix(b->m), s);
+    *out = new skref_csr{r.csr()};
+  });
+}
+
+// --- DNN ----------------------------------------------------------------------------
+// Layers are given in the reference orientation: W_ref[k] is m-by-m CSR with
+// row i = in-edges of output neuron i; Y is m-by-n neuron-major.
+static DnnModel model_of(uint32_t m, uint32_t layers, const skref_csr* const* w,
+                         const float* const* bias, int dense_weights) {
+  std::vector<Matrix> ws;
+  std::vector<std::vector<Scalar>> bs;
+  for (uint32_t k = 0; k < layers; ++k) {
+    if (dense_weights)
+      ws.emplace_back(to_dense(w[k]->m, 0.0f));
+    else
+      ws.emplace_back(w[k]->m);
+    bs.emplace_back(bias[k], bias[k] + m);
+  }
+  return DnnModel(std::move(ws), std::move(bs));
+}
+
+int skref_relu_forward(uint32_t m, uint32_t layers, const skref_csr* const* w,
+                       const float* const* bias, uint32_t n, const float* y0,
+                       int workers, int materialize_bias, float* out) {
+  return guarded([&] {
+    const DnnModel model = model_of(m, layers, w, bias, 0);
+    ForwardOptions opt;
+    opt.workers = workers;
+    opt.materialize_bias = materialize_bias != 0;
+    copy_out(relu_forward(model, dense_of(m, n, y0), opt), out);
+  });
+}
+
+int skref_dense_relu_forward(uint32_t m, uint32_t layers,
+                             const skref_csr* const* w, const float* const* bias,
+                             uint32_t n, const float* y0, float* out) {
+  return guarded([&] {
+    const DnnModel model = model_of(m, layers, w, bias, 0);
+    copy_out(dense_relu_forward(model, dense_of(m, n, y0)), out);
+  });
+}
+
+int skref_layer_step(const skref_csr* w, const float* bias, uint32_t n,
+                     const float* y, int workers, float* out) {
+  return guarded([&] {
+    const uint32_t m = w->m.rows();
+    ForwardOptions opt;
+    opt.workers = workers;
+    copy_out(layer_step(Matrix(w->m), std::span<const Scalar>(bias, m),
+                        dense_of(w->m.cols(), n, y), opt),
+             out);
+  });
+}
+
+int skref_dense_layer_step(uint32_t m, uint32_t l, const float* wd,
+                           const float* bias, uint32_t n, const float* y,
+                           int workers, float* out) {
+  return guarded([&] {
+    copy_out(dense_layer_step(dense_of(m, l, wd), std::span<const Scalar>(bias, m),
+                              dense_of(l, n, y), workers),
+             out);
+  });
+}
+
+// --- generators (matgen.cpp) --------------------------------------------------------
+int skref_gen_weight(uint32_t m, double inverse_sparsity, uint64_t seed,
+                     skref_csr** out) {
+  return guarded([&] {
+    *out = new skref_csr{gen_weight(GenSpec{m, inverse_sparsity, 1, seed})};
+  });
+}
+
+int skref_gen_input(uint32_t m, uint32_t batch, uint64_t seed, float* out) {
+  return guarded([&] { copy_out(gen_input(GenSpec{m, 1.0, batch, seed}), out); });
+}
+
+int skref_gen_bias(uint32_t m, uint64_t seed, int uniform01, float* out) {
+  return guarded([&] {
+    const auto b = gen_bias(GenSpec{m, 1.0, 1, seed},
+                            uniform01 ? BiasMode::uniform01 : BiasMode::zero);
+    std::memcpy(out, b.data(), b.size() * sizeof(float));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,850 @@
+// Construction, conversion, element-wise and generator kernels.
+//
+//  csr_from_triples  (proj/src/matrix.cpp:145-189): device range check ->
+//      radix sort on (row<<32|col) (stable) -> adjacent-duplicate check ->
+//      exact-zero elision -> row_ptr by lower_bound.  Errors carry the
+//      reference's messages; the first offending triple is found with atomicMin
+//      so the reported one is the one the reference's sequential loop reports.
+//  CsrMatrix validating ctor (matrix.cpp:89-119): per-row device check.
+//  to_dense / from_dense (matrix.cpp:191-227): warp per row; from_dense is
+//      the ballot/popc ordered compaction ("select != 0").
+//  ewise_add / ewise_mul (matrix.cpp:245-392): union semantics.
+//  Generators: counter-addressed SplitMix64, bitwise equal to oracle/sk_oracle.c.
+#include <cub/cub.cuh>
+
+#include <cstring>
+
+#include "sk_common.cuh"
+
+namespace sk {
+
+// ---- helpers ------------------------------------------------------------------
+
+__global__ void k_range_check(const uint32_t* r, const uint32_t* c, size_t n,
+                              uint32_t rows, uint32_t cols,
+                              unsigned long long* first_bad) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    if (r[i] >= rows || c[i] >= cols) atomicMin(first_bad, (unsigned long long)i);
+}
+
+__global__ void k_make_keys(const uint32_t* r, const uint32_t* c, size_t n,
+                            uint64_t* keys, uint32_t* idx) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    keys[i] = (uint64_t(r[i]) << 32) | c[i];
+    idx[i] = uint32_t(i);
+  }
+}
+
+__global__ void k_dup_check(const uint64_t* keys, size_t n,
+                            unsigned long long* first_dup) {
+  for (size_t i = 1 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    if (keys[i] == keys[i - 1]) atomicMin(first_dup, (unsigned long long)i);
+}
+
+__global__ void k_keep_flags(const uint32_t* idx, const float* v, size_t n,
+                             uint32_t* flags) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    flags[i] = (v ? v[idx[i]] : 1.0f) != 0.0f ? 1u : 0u;
+}
+
+__global__ void k_scatter_kept(const uint64_t* keys, const uint32_t* idx,
+                               const float* v, const uint32_t* flags,
+                               const uint32_t* pos, size_t n, uint32_t* out_row,
+                               uint32_t* out_col, float* out_v) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    if (!flags[i]) continue;
+    const uint32_t p = pos[i];
+    out_row[p] = uint32_t(keys[i] >> 32);
+    out_col[p] = uint32_t(keys[i]);
+    out_v[p] = v[idx[i]];
+  }
+}
+
+// rp[i] = lower_bound(rows_sorted, i) for i in [0, nrows]
+__global__ void k_row_ptr_from_sorted(const uint32_t* rows_sorted, size_t nnz,
+                                      uint32_t nrows, uint32_t* rp) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i <= nrows;
+       i += size_t(gridDim.x) * blockDim.x) {
+    size_t lo = 0, hi = nnz;
+    while (lo < hi) {
+      size_t mid = (lo + hi) >> 1;
+      if (rows_sorted[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    rp[i] = uint32_t(lo);
+  }
+}
+
+static unsigned grid_for(sk_ctx* ctx, size_t n, unsigned block = 256) {
+  return std::max(1u, std::min<unsigned>(ceil_div(n, block), ctx->num_sms * 16));
+}
+
+static uint64_t read_u64(sk_ctx* ctx, const void* d) {
+  uint64_t h = 0;
+  SK_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  return h;
+}
+
+static void set_u64(sk_ctx* ctx, void* d, uint64_t v) {
+  SK_CUDA(cudaMemcpyAsync(d, &v, 8, cudaMemcpyHostToDevice, ctx->stream));
+}
+
+static int end_bit_for(uint32_t rows) {
+  int b = 0;
+  while (b < 32 && (uint64_t(1) << b) < uint64_t(rows)) ++b;
+  return 32 + b;
+}
+
+// Sorted (row,col)-keyed triples -> CSR with exact-zero elision.
+static sk_csr* csr_from_sorted(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                               const uint64_t* keys, const uint32_t* idx,
+                               const float* v, size_t n, bool drop_zeros) {
+  uint32_t* flags = dalloc<uint32_t>(ctx, n + 1);
+  uint32_t* pos = dalloc<uint32_t>(ctx, n + 1);
+  SK_CUDA(cudaMemsetAsync(flags + n, 0, 4, ctx->stream));
+  if (n) SK_LAUNCH(k_keep_flags, grid_for(ctx, n), 256, 0, ctx->stream, idx,
+                   drop_zeros ? v : nullptr, n, flags);
+  exclusive_scan_u32(ctx, flags, pos, n + 1);
+  uint32_t nnz32 = 0;
+  SK_CUDA(cudaMemcpyAsync(&nnz32, pos + n, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  const size_t nnz = nnz32;
+  sk_csr* a = new_csr(ctx, rows, cols, nnz);
+  uint32_t* srow = dalloc<uint32_t>(ctx, nnz);
+  if (n) SK_LAUNCH(k_scatter_kept, grid_for(ctx, n), 256, 0, ctx->stream, keys, idx, v,
+                   flags, pos, n, srow, a->ci, a->v);
+  SK_LAUNCH(k_row_ptr_from_sorted, grid_for(ctx, size_t(rows) + 1), 256, 0, ctx->stream,
+            srow, nnz, rows, a->rp);
+  dfree(ctx, srow);
+  dfree(ctx, flags);
+  dfree(ctx, pos);
+  return a;
+}
+
+static void sort_pairs(sk_ctx* ctx, uint64_t* kin, uint64_t* kout, uint32_t* vin,
+                       uint32_t* vout, size_t n, int end_bit) {
+  size_t tmp = 0;
+  SK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, n, 0, end_bit,
+                                          ctx->stream));
+  void* t = dalloc<char>(ctx, tmp);
+  SK_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, vout, n, 0, end_bit,
+                                          ctx->stream));
+  g_launches.fetch_add(1);
+  dfree(ctx, t);
+}
+
+sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                const uint32_t* d_r, const uint32_t* d_c,
+                                const float* d_v, size_t n, const uint32_t* h_r,
+                                const uint32_t* h_c) {
+  unsigned long long* first_bad = reinterpret_cast<unsigned long long*>(ctx->d_u64);
+  // 1. range (matrix.cpp:147-153)
+  set_u64(ctx, first_bad, ~0ull);
+  if (n) SK_LAUNCH(k_range_check, grid_for(ctx, n), 256, 0, ctx->stream, d_r, d_c, n,
+                   rows, cols, first_bad);
+  uint64_t bad = read_u64(ctx, first_bad);
+  if (bad != ~0ull) {
+    uint32_t br = 0, bc = 0;
+    if (h_r) {
+      br = h_r[bad];
+      bc = h_c[bad];
+    } else {
+      SK_CUDA(cudaMemcpy(&br, d_r + bad, 4, cudaMemcpyDeviceToHost));
+      SK_CUDA(cudaMemcpy(&bc, d_c + bad, 4, cudaMemcpyDeviceToHost));
+    }
+    fail(SK_ERR_INVALID_ARGUMENT, "triple (" + std::to_string(br) + ", " + std::to_string(bc) +
+                                      ") outside " + dim_string(rows, cols));
+  }
+  // 2. sort by (row, col) (matrix.cpp:154-157)
+  uint64_t* k0 = dalloc<uint64_t>(ctx, n);
+  uint64_t* k1 = dalloc<uint64_t>(ctx, n);
+  uint32_t* i0 = dalloc<uint32_t>(ctx, n);
+  uint32_t* i1 = dalloc<uint32_t>(ctx, n);
+  if (n) {
+    SK_LAUNCH(k_make_keys, grid_for(ctx, n), 256, 0, ctx->stream, d_r, d_c, n, k0, i0);
+    sort_pairs(ctx, k0, k1, i0, i1, n, end_bit_for(rows));
+  }
+  // 3. duplicates (matrix.cpp:158-165)
+  set_u64(ctx, first_bad, ~0ull);
+  if (n > 1) SK_LAUNCH(k_dup_check, grid_for(ctx, n), 256, 0, ctx->stream, k1, n, first_bad);
+  bad = read_u64(ctx, first_bad);
+  if (bad != ~0ull) {
+    const uint64_t key = read_u64(ctx, k1 + bad);
+    for (void* p : {(void*)k0, (void*)k1, (void*)i0, (void*)i1}) dfree(ctx, p);
+    fail(SK_ERR_INVALID_ARGUMENT, "duplicate coordinate (" + std::to_string(key >> 32) + ", " +
+                                      std::to_string(uint32_t(key)) + ")");
+  }
+  // 4. nnz limit (matrix.cpp:166-168)
+  if (n > 0xFFFFFFFFull) {
+    for (void* p : {(void*)k0, (void*)k1, (void*)i0, (void*)i1}) dfree(ctx, p);
+    fail(SK_ERR_INVALID_ARGUMENT, "nnz exceeds the 32-bit index range");
+  }
+  // 5. zero elision + row_ptr (matrix.cpp:170-188)
+  sk_csr* a = csr_from_sorted(ctx, rows, cols, k1, i1, d_v, n, true);
+  for (void* p : {(void*)k0, (void*)k1, (void*)i0, (void*)i1}) dfree(ctx, p);
+  return a;
+}
+
+// ---- transpose (used by the generators and the column-major views) -------------
+
+__global__ void k_expand_keys_t(const uint32_t* rp, const uint32_t* ci, uint32_t rows,
+                                uint64_t* keys, uint32_t* idx) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += (gridDim.x * blockDim.x) >> 5) {
+    for (uint32_t e = rp[r] + lane; e < rp[r + 1]; e += 32) {
+      keys[e] = (uint64_t(ci[e]) << 32) | r;
+      idx[e] = e;
+    }
+  }
+}
+
+sk_csr* csr_transpose(sk_ctx* ctx, const sk_csr* a) {
+  const size_t n = a->nnz;
+  uint64_t* k0 = dalloc<uint64_t>(ctx, n);
+  uint64_t* k1 = dalloc<uint64_t>(ctx, n);
+  uint32_t* i0 = dalloc<uint32_t>(ctx, n);
+  uint32_t* i1 = dalloc<uint32_t>(ctx, n);
+  SK_LAUNCH(k_expand_keys_t, grid_for(ctx, size_t(a->rows) * 32), 256, 0, ctx->stream,
+            a->rp, a->ci, a->rows, k0, i0);
+  if (n) sort_pairs(ctx, k0, k1, i0, i1, n, end_bit_for(a->cols));
+  sk_csr* t = csr_from_sorted(ctx, a->cols, a->rows, k1, i1, a->v, n, false);
+  for (void* p : {(void*)k0, (void*)k1, (void*)i0, (void*)i1}) dfree(ctx, p);
+  return t;
+}
+
+// ---- validating constructor (matrix.cpp:89-119) ---------------------------------
+
+__global__ void k_validate_rows(const uint32_t* rp, const uint32_t* ci, uint32_t rows,
+                                uint32_t cols, size_t nnz, unsigned long long* bad_row) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += gridDim.x * blockDim.x) {
+    const uint32_t b = rp[i], e = rp[i + 1];
+    bool bad = b > e || e > nnz;
+    for (uint32_t k = b; !bad && k < e; ++k) {
+      if (ci[k] >= cols) bad = true;
+      else if (k > b && ci[k - 1] >= ci[k]) bad = true;
+    }
+    if (bad) atomicMin(bad_row, (unsigned long long)i);
+  }
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" sk_status sk_csr_from_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                         const uint32_t* row, const uint32_t* col,
+                                         const float* val, size_t n, sk_csr** out) {
+  return guarded([&] {
+    if (!ctx) fail(SK_ERR_INVALID_ARGUMENT, "null context");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    uint32_t* dr = dalloc<uint32_t>(ctx, n);
+    uint32_t* dc = dalloc<uint32_t>(ctx, n);
+    float* dv = dalloc<float>(ctx, n);
+    if (n) {
+      SK_CUDA(cudaMemcpyAsync(dr, row, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+      SK_CUDA(cudaMemcpyAsync(dc, col, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+      SK_CUDA(cudaMemcpyAsync(dv, val, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    try {
+      *out = csr_from_device_triples(ctx, rows, cols, dr, dc, dv, n, row, col);
+    } catch (...) {
+      dfree(ctx, dr);
+      dfree(ctx, dc);
+      dfree(ctx, dv);
+      throw;
+    }
+    dfree(ctx, dr);
+    dfree(ctx, dc);
+    dfree(ctx, dv);
+  });
+}
+
+extern "C" sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                       const uint32_t* rp, const uint32_t* ci,
+                                       const float* v, int validate, sk_csr** out) {
+  return guarded([&] {
+    if (!ctx) fail(SK_ERR_INVALID_ARGUMENT, "null context");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    if (validate && rp[0] != 0) fail(SK_ERR_INVALID_ARGUMENT, "row_ptr[0] must be 0");
+    const size_t nnz = rp[rows];
+    sk_csr* a = new_csr(ctx, rows, cols, nnz);
+    SK_CUDA(cudaMemcpyAsync(a->rp, rp, (size_t(rows) + 1) * 4, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    if (nnz) {
+      SK_CUDA(cudaMemcpyAsync(a->ci, ci, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+      SK_CUDA(cudaMemcpyAsync(a->v, v, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if (validate && rows) {
+      unsigned long long* bad = reinterpret_cast<unsigned long long*>(ctx->d_u64);
+      set_u64(ctx, bad, ~0ull);
+      SK_LAUNCH(k_validate_rows, grid_for(ctx, rows), 256, 0, ctx->stream, a->rp, a->ci, rows,
+                cols, nnz, bad);
+      const uint64_t r = read_u64(ctx, bad);
+      if (r != ~0ull) {
+        csr_release(a);
+        // Reproduce the reference's message for the first offending row.
+        const uint32_t i = uint32_t(r);
+        if (rp[i] > rp[i + 1] || rp[i + 1] > nnz)
+          fail(SK_ERR_INVALID_ARGUMENT, "row_ptr must be non-decreasing");
+        for (uint32_t k = rp[i]; k < rp[i + 1]; ++k) {
+          if (ci[k] >= cols)
+            fail(SK_ERR_INVALID_ARGUMENT, "column index " + std::to_string(ci[k]) +
+                                              " out of range in row " + std::to_string(i));
+          if (k > rp[i] && ci[k - 1] >= ci[k])
+            fail(SK_ERR_INVALID_ARGUMENT,
+                 "column indices must be strictly increasing within row " + std::to_string(i));
+        }
+        fail(SK_ERR_INVALID_ARGUMENT, "invalid CSR row " + std::to_string(i));
+      }
+    }
+    sync(ctx);  // host arrays are borrowed only for the call
+    *out = a;
+  });
+}
+
+// ==== to_dense / from_dense / nnz ====================================================
+
+namespace sk {
+
+__global__ void k_scatter_rows(const uint32_t* rp, const uint32_t* ci, const float* v,
+                               uint32_t rows, uint32_t cols, float* out) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += (gridDim.x * blockDim.x) >> 5)
+    for (uint32_t e = rp[r] + lane; e < rp[r + 1]; e += 32)
+      out[size_t(r) * cols + ci[e]] = v[e];
+}
+
+__global__ void k_count_nonzero_rows(const float* d, uint32_t rows, uint32_t cols,
+                                     unsigned long long* cnt) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += (gridDim.x * blockDim.x) >> 5) {
+    uint32_t c = 0;
+    const float* row = d + size_t(r) * cols;
+    for (uint32_t j = lane; j < cols; j += 32) c += row[j] != 0.0f;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[r] = c;
+  }
+}
+
+__global__ void k_compact_rows(const float* d, uint32_t rows, uint32_t cols,
+                               const unsigned long long* off, uint32_t* rp, uint32_t* ci,
+                               float* v) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += (gridDim.x * blockDim.x) >> 5) {
+    uint64_t o = off[r];
+    if (lane == 0) rp[r] = uint32_t(o);
+    if (r == rows - 1 && lane == 0) rp[rows] = uint32_t(off[rows]);
+    const float* row = d + size_t(r) * cols;
+    for (uint32_t j0 = 0; j0 < cols; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const float x = j < cols ? row[j] : 0.0f;
+      const bool keep = x != 0.0f;
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const uint32_t p = uint32_t(o) + __popc(m & ((1u << lane) - 1));
+        ci[p] = j;
+        v[p] = x;
+      }
+      o += __popc(m);
+    }
+  }
+}
+
+}  // namespace sk
+
+extern "C" sk_status sk_to_dense(sk_ctx* ctx, const sk_csr* a, float ambient, sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    sk_dense* d = new_dense(ctx, a->rows, a->cols);
+    fill(ctx, d->d, d->elems(), ambient);
+    if (a->rows)
+      SK_LAUNCH(k_scatter_rows, grid_for(ctx, size_t(a->rows) * 32), 256, 0, ctx->stream,
+                a->rp, a->ci, a->v, a->rows, a->cols, d->d);
+    *out = d;
+  });
+}
+
+namespace sk {
+
+sk_csr* from_dense_impl(sk_ctx* ctx, const float* d, uint32_t rows, uint32_t cols) {
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(
+      dalloc<uint64_t>(ctx, size_t(rows) + 1));
+  unsigned long long* off = reinterpret_cast<unsigned long long*>(
+      dalloc<uint64_t>(ctx, size_t(rows) + 1));
+  SK_CUDA(cudaMemsetAsync(cnt + rows, 0, 8, ctx->stream));
+  if (rows)
+    SK_LAUNCH(k_count_nonzero_rows, grid_for(ctx, size_t(rows) * 32), 256, 0, ctx->stream, d,
+              rows, cols, cnt);
+  exclusive_scan_u64(ctx, reinterpret_cast<uint64_t*>(cnt), reinterpret_cast<uint64_t*>(off),
+                     size_t(rows) + 1);
+  const uint64_t nnz = read_u64(ctx, off + rows);
+  if (nnz > 0xFFFFFFFFull) {
+    dfree(ctx, cnt);
+    dfree(ctx, off);
+    fail(SK_ERR_INVALID_ARGUMENT, "nnz exceeds the 32-bit index range");
+  }
+  sk_csr* a = new_csr(ctx, rows, cols, nnz);
+  if (rows)
+    SK_LAUNCH(k_compact_rows, grid_for(ctx, size_t(rows) * 32), 256, 0, ctx->stream, d, rows,
+              cols, off, a->rp, a->ci, a->v);
+  else
+    SK_CUDA(cudaMemsetAsync(a->rp, 0, 4, ctx->stream));
+  dfree(ctx, cnt);
+  dfree(ctx, off);
+  return a;
+}
+}  // namespace sk
+
+extern "C" sk_status sk_from_dense(sk_ctx* ctx, const sk_dense* d, sk_csr** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    *out = from_dense_impl(ctx, d->d, d->rows, d->cols);
+  });
+}
+
+namespace sk {
+__global__ void k_count_nz(const float* d, size_t n, unsigned long long* total) {
+  unsigned long long c = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    c += d[i] != 0.0f;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
+}
+}  // namespace sk
+
+extern "C" sk_status sk_dense_nnz(sk_ctx* ctx, const sk_dense* d, size_t* out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    unsigned long long* t = reinterpret_cast<unsigned long long*>(ctx->d_u64);
+    set_u64(ctx, t, 0);
+    if (d->elems())
+      SK_LAUNCH(k_count_nz, grid_for(ctx, d->elems()), 256, 0, ctx->stream, d->d, d->elems(), t);
+    *out = read_u64(ctx, t);
+  });
+}
+
+// ==== element-wise ===================================================================
+
+namespace sk {
+
+template <typename Ops, bool kMul>
+__device__ __forceinline__ float combine(float a, float b, int* err) {
+  return kMul ? Ops::mul(a, b, err) : Ops::add(a, b, err);
+}
+
+template <typename Ops, bool kMul>
+__global__ void k_ewise_dense(const float* a, const float* b, size_t n, float* out, int* err) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    out[i] = combine<Ops, kMul>(a[i], b[i], err);
+}
+
+// sparse (op) dense: every position first gets the "absent" combination...
+template <typename Ops, bool kMul>
+__global__ void k_ewise_mixed_base(const float* dn, size_t n, bool sparse_left, float* out,
+                                   int* err) {
+  const float z = Ops::zero();
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    out[i] = sparse_left ? combine<Ops, kMul>(z, dn[i], err) : combine<Ops, kMul>(dn[i], z, err);
+}
+// ...then stored positions overwrite it (matrix.cpp:294-312).
+template <typename Ops, bool kMul>
+__global__ void k_ewise_mixed_stored(const uint32_t* rp, const uint32_t* ci, const float* v,
+                                     uint32_t rows, uint32_t cols, const float* dn,
+                                     bool sparse_left, float* out, int* err) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += (gridDim.x * blockDim.x) >> 5)
+    for (uint32_t e = rp[r] + lane; e < rp[r + 1]; e += 32) {
+      const size_t p = size_t(r) * cols + ci[e];
+      out[p] = sparse_left ? combine<Ops, kMul>(v[e], dn[p], err)
+                           : combine<Ops, kMul>(dn[p], v[e], err);
+    }
+}
+
+// Union merge of two CSR rows (matrix.cpp:253-290): pass 0 counts, pass 1 writes.
+template <typename Ops, bool kMul>
+__global__ void k_merge_rows(const uint32_t* arp, const uint32_t* aci, const float* av,
+                             const uint32_t* brp, const uint32_t* bci, const float* bv,
+                             uint32_t rows, uint32_t* cnt, const uint32_t* orp,
+                             uint32_t* oci, float* ov, int* err) {
+  const float z = Ops::zero();
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += gridDim.x * blockDim.x) {
+    uint32_t p = arp[r], pe = arp[r + 1], q = brp[r], qe = brp[r + 1];
+    uint32_t o = orp ? orp[r] : 0, c = 0;
+    while (p < pe || q < qe) {
+      uint32_t col;
+      float val = 0.0f;
+      if (q == qe || (p < pe && aci[p] < bci[q])) {
+        col = aci[p];
+        if (orp) val = combine<Ops, kMul>(av[p], z, err);
+        ++p;
+      } else if (p == pe || bci[q] < aci[p]) {
+        col = bci[q];
+        if (orp) val = combine<Ops, kMul>(z, bv[q], err);
+        ++q;
+      } else {
+        col = aci[p];
+        if (orp) val = combine<Ops, kMul>(av[p], bv[q], err);
+        ++p;
+        ++q;
+      }
+      if (orp) {
+        oci[o + c] = col;
+        ov[o + c] = val;
+      }
+      ++c;
+    }
+    if (!orp) cnt[r] = c;
+  }
+}
+
+}  // namespace sk
+
+static void require_same_shape(const char* op, uint32_t ar, uint32_t ac, uint32_t br,
+                               uint32_t bc) {
+  // matrix.cpp:32-38
+  if (ar != br || ac != bc)
+    fail(SK_ERR_DIMENSION, std::string(op) + ": operands " + dim_string(ar, ac) + " and " +
+                               dim_string(br, bc) + " differ in shape");
+}
+
+extern "C" sk_status sk_ewise_dense(sk_ctx* ctx, int mul, const sk_dense* a,
+                                    const sk_dense* b, sk_semiring s, sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    require_same_shape(mul ? "ewise_mul" : "ewise_add", a->rows, a->cols, b->rows, b->cols);
+    sk_dense* o = new_dense(ctx, a->rows, a->cols);
+    const size_t n = a->elems();
+    dispatch_semiring(s, [&](auto ops) {
+      using Ops = decltype(ops);
+      if (n == 0) return;
+      if (mul)
+        SK_LAUNCH((k_ewise_dense<Ops, true>), grid_for(ctx, n), 256, 0, ctx->stream, a->d, b->d,
+                  n, o->d, ctx->d_err);
+      else
+        SK_LAUNCH((k_ewise_dense<Ops, false>), grid_for(ctx, n), 256, 0, ctx->stream, a->d,
+                  b->d, n, o->d, ctx->d_err);
+    });
+    if (s == SK_GF2) {
+      try {
+        check_device_error(ctx, mul ? "ewise_mul" : "ewise_add");
+      } catch (...) {
+        sk_dense_free(o);
+        throw;
+      }
+    }
+    *out = o;
+  });
+}
+
+extern "C" sk_status sk_ewise_mixed(sk_ctx* ctx, int mul, const sk_csr* sp, const sk_dense* dn,
+                                    int sparse_left, sk_semiring s, sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    const char* op = mul ? "ewise_mul" : "ewise_add";
+    if (sparse_left)
+      require_same_shape(op, sp->rows, sp->cols, dn->rows, dn->cols);
+    else
+      require_same_shape(op, dn->rows, dn->cols, sp->rows, sp->cols);
+    sk_dense* o = new_dense(ctx, dn->rows, dn->cols);
+    const size_t n = dn->elems();
+    dispatch_semiring(s, [&](auto ops) {
+      using Ops = decltype(ops);
+      if (n == 0) return;
+      if (mul) {
+        SK_LAUNCH((k_ewise_mixed_base<Ops, true>), grid_for(ctx, n), 256, 0, ctx->stream, dn->d,
+                  n, sparse_left != 0, o->d, ctx->d_err);
+        SK_LAUNCH((k_ewise_mixed_stored<Ops, true>), grid_for(ctx, size_t(sp->rows) * 32), 256,
+                  0, ctx->stream, sp->rp, sp->ci, sp->v, sp->rows, sp->cols, dn->d,
+                  sparse_left != 0, o->d, ctx->d_err);
+      } else {
+        SK_LAUNCH((k_ewise_mixed_base<Ops, false>), grid_for(ctx, n), 256, 0, ctx->stream,
+                  dn->d, n, sparse_left != 0, o->d, ctx->d_err);
+        SK_LAUNCH((k_ewise_mixed_stored<Ops, false>), grid_for(ctx, size_t(sp->rows) * 32), 256,
+                  0, ctx->stream, sp->rp, sp->ci, sp->v, sp->rows, sp->cols, dn->d,
+                  sparse_left != 0, o->d, ctx->d_err);
+      }
+    });
+    if (s == SK_GF2) {
+      try {
+        check_device_error(ctx, op);
+      } catch (...) {
+        sk_dense_free(o);
+        throw;
+      }
+    }
+    *out = o;
+  });
+}
+
+extern "C" sk_status sk_ewise_csr(sk_ctx* ctx, int mul, const sk_csr* a, const sk_csr* b,
+                                  sk_semiring s, sk_csr** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    require_same_shape(mul ? "ewise_mul" : "ewise_add", a->rows, a->cols, b->rows, b->cols);
+    const uint32_t rows = a->rows;
+    uint32_t* cnt = dalloc<uint32_t>(ctx, size_t(rows) + 1);
+    uint32_t* rp = dalloc<uint32_t>(ctx, size_t(rows) + 1);
+    SK_CUDA(cudaMemsetAsync(cnt + rows, 0, 4, ctx->stream));
+    sk_csr* o = nullptr;
+    dispatch_semiring(s, [&](auto ops) {
+      using Ops = decltype(ops);
+      auto kern = mul ? k_merge_rows<Ops, true> : k_merge_rows<Ops, false>;
+      if (rows)
+        SK_LAUNCH(kern, grid_for(ctx, rows), 256, 0, ctx->stream, a->rp, a->ci, a->v, b->rp,
+                  b->ci, b->v, rows, cnt, nullptr, nullptr, nullptr, ctx->d_err);
+      exclusive_scan_u32(ctx, cnt, rp, size_t(rows) + 1);
+      uint32_t nnz = 0;
+      SK_CUDA(cudaMemcpyAsync(&nnz, rp + rows, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+      o = new_csr(ctx, rows, a->cols, nnz);
+      SK_CUDA(cudaMemcpyAsync(o->rp, rp, (size_t(rows) + 1) * 4, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+      if (rows)
+        SK_LAUNCH(kern, grid_for(ctx, rows), 256, 0, ctx->stream, a->rp, a->ci, a->v, b->rp,
+                  b->ci, b->v, rows, nullptr, o->rp, o->ci, o->v, ctx->d_err);
+    });
+    dfree(ctx, cnt);
+    dfree(ctx, rp);
+    if (s == SK_GF2) {
+      try {
+        check_device_error(ctx, mul ? "ewise_mul" : "ewise_add");
+      } catch (...) {
+        csr_release(o);
+        throw;
+      }
+    }
+    *out = o;
+  });
+}
+
+// ==== category set =====================================================================
+
+namespace sk {
+__global__ void k_flag_cols_csr(const uint32_t* ci, const float* v, size_t nnz,
+                                uint8_t* flags) {
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < nnz;
+       e += size_t(gridDim.x) * blockDim.x)
+    if (v[e] != 0.0f) flags[ci[e]] = 1;  // benign race: every writer stores 1
+}
+__global__ void k_flag_cols_dense(const float* d, uint32_t rows, uint32_t cols,
+                                  uint8_t* flags) {
+  const size_t n = size_t(rows) * cols;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    if (d[i] != 0.0f) flags[i % cols] = 1;
+}
+
+void categories_from_flags(sk_ctx* ctx, uint8_t* flags, uint32_t n, uint32_t* idx,
+                           size_t cap, size_t* count) {
+  uint32_t* out = dalloc<uint32_t>(ctx, n);
+  int* nsel = reinterpret_cast<int*>(ctx->d_u64);
+  size_t tmp = 0;
+  cub::CountingInputIterator<uint32_t> it(0);
+  SK_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flags, out, nsel, n, ctx->stream));
+  void* t = dalloc<char>(ctx, tmp);
+  SK_CUDA(cub::DeviceSelect::Flagged(t, tmp, it, flags, out, nsel, n, ctx->stream));
+  g_launches.fetch_add(1);
+  int h = 0;
+  SK_CUDA(cudaMemcpyAsync(&h, nsel, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  *count = size_t(h);
+  if (idx && h)
+    SK_CUDA(cudaMemcpyAsync(idx, out, std::min<size_t>(cap, h) * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  sync(ctx);
+  dfree(ctx, t);
+  dfree(ctx, out);
+}
+}  // namespace sk
+
+extern "C" sk_status sk_categories_csr(sk_ctx* ctx, const sk_csr* y, uint32_t* idx, size_t cap,
+                                       size_t* count) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    uint8_t* flags = dalloc<uint8_t>(ctx, y->cols);
+    SK_CUDA(cudaMemsetAsync(flags, 0, y->cols, ctx->stream));
+    if (y->nnz)
+      SK_LAUNCH(k_flag_cols_csr, grid_for(ctx, y->nnz), 256, 0, ctx->stream, y->ci, y->v, y->nnz,
+                flags);
+    categories_from_flags(ctx, flags, y->cols, idx, cap, count);
+    dfree(ctx, flags);
+  });
+}
+
+extern "C" sk_status sk_categories_dense(sk_ctx* ctx, const sk_dense* y, uint32_t* idx,
+                                         size_t cap, size_t* count) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    uint8_t* flags = dalloc<uint8_t>(ctx, y->cols);
+    SK_CUDA(cudaMemsetAsync(flags, 0, y->cols, ctx->stream));
+    if (y->elems())
+      SK_LAUNCH(k_flag_cols_dense, grid_for(ctx, y->elems()), 256, 0, ctx->stream, y->d, y->rows,
+                y->cols, flags);
+    categories_from_flags(ctx, flags, y->cols, idx, cap, count);
+    dfree(ctx, flags);
+  });
+}
+
+// ==== generators (bitwise equal to oracle/sk_oracle.c) ===============================
+
+namespace sk {
+
+__device__ __forceinline__ uint32_t bounded(uint64_t bits, uint32_t range) {
+  return uint32_t(__umul64hi(bits, uint64_t(range)));
+}
+
+// Row i (global index i + row_offset) draws distinct sorted columns in place.
+__global__ void k_gen_fixed_rows(uint32_t rows, uint32_t cols, uint32_t k, uint64_t seed,
+                                 uint64_t row_offset, uint32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += gridDim.x * blockDim.x) {
+    const uint64_t rs = splitmix_at(seed, uint64_t(i) + row_offset);
+    uint32_t* row = out + size_t(i) * k;
+    uint32_t have = 0;
+    for (uint64_t t = 0; have < k; ++t) {
+      const uint32_t c = bounded(splitmix_at(rs, t), cols);
+      uint32_t lo = 0, hi = have;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (row[mid] < c) lo = mid + 1; else hi = mid;
+      }
+      if (lo < have && row[lo] == c) continue;
+      for (uint32_t q = have; q > lo; --q) row[q] = row[q - 1];
+      row[lo] = c;
+      ++have;
+    }
+  }
+}
+
+__device__ __forceinline__ float uniform_pm1(uint64_t seed, uint64_t idx) {
+  const float v = float(__dadd_rn(-1.0, __dmul_rn(2.0, to_unit(splitmix_at(seed, idx)))));
+  return v == 0.0f ? 1.0f : v;
+}
+
+__global__ void k_gen_values(float* v, size_t n, uint64_t seed, float value, int uniform) {
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < n;
+       e += size_t(gridDim.x) * blockDim.x)
+    v[e] = uniform ? uniform_pm1(seed, e) : value;
+}
+
+__global__ void k_iota_rp(uint32_t* rp, uint32_t rows, uint32_t k) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= rows;
+       i += gridDim.x * blockDim.x)
+    rp[i] = i * k;
+}
+
+// cfg2: W_ref row j, column i present iff U(at(sel, i*m+j)) < density.
+__global__ void k_gen_density(uint32_t m, double density, uint64_t sel, uint64_t val,
+                              const uint32_t* rp, uint32_t* cnt, uint32_t* ci, float* v) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    const uint32_t o = rp ? rp[j] : 0;
+    for (uint32_t i = 0; i < m; ++i) {
+      const uint64_t idx = uint64_t(i) * m + j;
+      if (to_unit(splitmix_at(sel, idx)) < density) {
+        if (rp) {
+          ci[o + c] = i;
+          v[o + c] = uniform_pm1(val, idx);
+        }
+        ++c;
+      }
+    }
+    if (!rp) cnt[j] = c;
+  }
+}
+
+__global__ void k_gen_input_dense(float* y, size_t n, uint64_t stream) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    y[i] = float(to_unit(splitmix_at(stream, i)));
+}
+
+sk_csr* gen_fixed_csr(sk_ctx* ctx, uint32_t rows, uint32_t cols, uint32_t k, uint64_t sel_seed,
+                      uint64_t row_offset, uint64_t val_seed, float value, int uniform) {
+  if (k > cols) fail(SK_ERR_INVALID_ARGUMENT, "k exceeds the number of columns");
+  sk_csr* a = new_csr(ctx, rows, cols, size_t(rows) * k);
+  SK_LAUNCH(k_gen_fixed_rows, grid_for(ctx, rows, 128), 128, 0, ctx->stream, rows, cols, k,
+            sel_seed, row_offset, a->ci);
+  SK_LAUNCH(k_gen_values, grid_for(ctx, a->nnz), 256, 0, ctx->stream, a->v, a->nnz, val_seed,
+            value, uniform);
+  SK_LAUNCH(k_iota_rp, grid_for(ctx, size_t(rows) + 1), 256, 0, ctx->stream, a->rp, rows, k);
+  return a;
+}
+
+}  // namespace sk
+
+extern "C" sk_status sk_gen_layer_fixed(sk_ctx* ctx, uint32_t m, uint32_t k, uint64_t layer_seed,
+                                        float value, sk_csr** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    const int uniform = value != value;
+    sk_csr* w = gen_fixed_csr(ctx, m, m, k, splitmix_at(layer_seed, 0), 0,
+                              splitmix_at(layer_seed, 1), value, uniform);
+    sk_csr* t = csr_transpose(ctx, w);
+    csr_release(w);
+    *out = t;
+  });
+}
+
+extern "C" sk_status sk_gen_layer_density(sk_ctx* ctx, uint32_t m, double density,
+                                          uint64_t layer_seed, sk_csr** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t sel = splitmix_at(layer_seed, 0), val = splitmix_at(layer_seed, 1);
+    uint32_t* cnt = dalloc<uint32_t>(ctx, size_t(m) + 1);
+    uint32_t* rp = dalloc<uint32_t>(ctx, size_t(m) + 1);
+    SK_CUDA(cudaMemsetAsync(cnt + m, 0, 4, ctx->stream));
+    SK_LAUNCH(k_gen_density, grid_for(ctx, m, 128), 128, 0, ctx->stream, m, density, sel, val,
+              nullptr, cnt, nullptr, nullptr);
+    exclusive_scan_u32(ctx, cnt, rp, size_t(m) + 1);
+    uint32_t nnz = 0;
+    SK_CUDA(cudaMemcpyAsync(&nnz, rp + m, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    sk_csr* a = new_csr(ctx, m, m, nnz);
+    SK_CUDA(cudaMemcpyAsync(a->rp, rp, (size_t(m) + 1) * 4, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    SK_LAUNCH(k_gen_density, grid_for(ctx, m, 128), 128, 0, ctx->stream, m, density, sel, val,
+              a->rp, nullptr, a->ci, a->v);
+    dfree(ctx, cnt);
+    dfree(ctx, rp);
+    *out = a;
+  });
+}
+
+extern "C" sk_status sk_gen_input_dense(sk_ctx* ctx, uint32_t m, uint32_t n, uint64_t seed,
+                                        sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    sk_dense* d = new_dense(ctx, m, n);
+    if (d->elems())
+      SK_LAUNCH(k_gen_input_dense, grid_for(ctx, d->elems()), 256, 0, ctx->stream, d->d,
+                d->elems(), splitmix_at(seed, 2));
+    *out = d;
+  });
+}
+
+extern "C" sk_status sk_gen_input_binary(sk_ctx* ctx, uint32_t m, uint32_t n, uint32_t k,
+                                         uint64_t seed, uint64_t sample_offset, sk_csr** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    sk_csr* b = gen_fixed_csr(ctx, n, m, k, splitmix_at(seed, 4), sample_offset, 0, 1.0f, 0);
+    sk_csr* t = csr_transpose(ctx, b);
+    csr_release(b);
+    *out = t;
+  });
+}

@@ -1,0 +1,76 @@
+// Dense comparator leg: dense_mxm_baseline / dense_layer_step /
+// dense_relu_forward (proj/src/matrix.cpp:564-585, proj/src/dnn.cpp:123-149).
+//
+// launch_dense_gemm_tc() is the entry used by the C-ABI; the tensor-core
+// implementation lives in k_dense_tc.cu.
+#include "sk_common.cuh"
+
+namespace sk {
+
+void launch_mxm_dense_dense(sk_ctx* ctx, const float* a, const float* b, uint32_t M, uint32_t K,
+                            uint32_t N, sk_semiring s, float* c);
+sk_csr* csr_transpose(sk_ctx* ctx, const sk_csr* a);
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" sk_status sk_dense_mxm_baseline(sk_ctx* ctx, const sk_dense* a, const sk_dense* b,
+                                           sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    if (a->cols != b->rows)
+      fail(SK_ERR_DIMENSION, "dense_mxm_baseline: inner dimensions " + std::to_string(a->cols) +
+                                 " and " + std::to_string(b->rows) + " do not match");
+    sk_dense* o = new_dense(ctx, a->rows, b->cols);
+    launch_dense_gemm_tc(ctx, a->d, b->d, a->rows, a->cols, b->cols, nullptr, 0, o->d);
+    *out = o;
+  });
+}
+
+extern "C" sk_status sk_dense_layer_step(sk_ctx* ctx, const sk_dense* w, const float* bias,
+                                         const sk_dense* y, sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    if (!bias)
+      fail(SK_ERR_DIMENSION, "bias length 0 does not match " + std::to_string(w->rows) +
+                                 " output rows");
+    if (w->cols != y->rows)
+      fail(SK_ERR_DIMENSION, "dense_mxm_baseline: inner dimensions " + std::to_string(w->cols) +
+                                 " and " + std::to_string(y->rows) + " do not match");
+    float* db = dalloc<float>(ctx, w->rows);
+    SK_CUDA(cudaMemcpyAsync(db, bias, size_t(w->rows) * 4, cudaMemcpyHostToDevice, ctx->stream));
+    sk_dense* o = new_dense(ctx, w->rows, y->cols);
+    launch_dense_gemm_tc(ctx, w->d, y->d, w->rows, w->cols, y->cols, db, 1, o->d);
+    dfree(ctx, db);
+    sync(ctx);
+    *out = o;
+  });
+}
+
+extern "C" sk_status sk_dense_relu_forward(sk_ctx* ctx, const sk_model* m, const sk_dense* y0,
+                                           sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    if (y0->rows != m->neurons || y0->cols < 1)
+      fail(SK_ERR_DIMENSION, "input batch is " + dim_string(y0->rows, y0->cols) + ", expected " +
+                                 std::to_string(m->neurons) + " rows and n >= 1 columns");
+    const uint32_t nn = m->neurons, n = y0->cols;
+    sk_dense* wd = nullptr;
+    SK_CUDA(cudaSuccess);
+    // dnn.cpp:141-149: re-densify each layer's weights, then the dense step.
+    sk_dense* bufs[2] = {new_dense(ctx, nn, n), new_dense(ctx, nn, n)};
+    const float* src = y0->d;
+    int cur = 0;
+    for (uint32_t k = 0; k < m->layers; ++k) {
+      sk_status st = sk_to_dense(ctx, m->w[k], 0.0f, &wd);
+      if (st != SK_OK) fail(st, sk_last_error());
+      launch_dense_gemm_tc(ctx, wd->d, src, nn, nn, n, m->bias + size_t(k) * nn, 1, bufs[cur]->d);
+      sk_dense_free(wd);
+      src = bufs[cur]->d;
+      cur ^= 1;
+    }
+    sk_dense_free(bufs[cur]);
+    *out = bufs[cur ^ 1];
+  });
+}

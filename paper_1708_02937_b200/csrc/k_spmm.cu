@@ -1,0 +1,227 @@
+// K1: CSR x dense SpMM on neuron-major activations, with the layer epilogue
+// fused (proj/src/matrix.cpp:403-424 + proj/src/dnn.cpp:65-103).
+//
+// Bitwise contract (SURVEY §8a "Op order"): every output (i, j) is a LEFT FOLD
+// over the stored entries of W_ref row i in ascending column order, starting
+// from the semiring zero, with separately rounded multiply and add
+// (__fmul_rn/__fadd_rn -- never contracted to FMA).  Each output element has
+// exactly one owner lane, so there is no split-K and no atomic anywhere.
+//
+// Mapping: one warp owns (row i, 128-column chunk c); each lane owns 4
+// consecutive columns and streams float4 rows of Y.  The warp loads 32 (k, w)
+// pairs of W row i cooperatively and broadcasts them with shuffles, so the
+// inner loop issues only the Y loads.  Tasks are ordered chunk-major so the
+// live Y panel (m x 128 floats) stays L2-resident while every row that
+// touches it runs.
+#include "sk_common.cuh"
+
+namespace sk {
+
+enum EpiMode { kEpiNone = 0, kEpiLayer = 1 };
+
+template <typename Ops, int kEpi, bool kVec4>
+__global__ void __launch_bounds__(256)
+    k_spmm_rows(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                const float* __restrict__ wv, const float* __restrict__ bias,
+                const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
+                float* __restrict__ out, int* err) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t chunks = (n + 127) / 128;
+  const uint64_t tasks = uint64_t(chunks) * m;
+  for (uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; task < tasks;
+       task += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+    const uint32_t c = uint32_t(task / m);
+    const uint32_t i = uint32_t(task % m);
+    const uint32_t col0 = c * 128 + lane * 4;
+    float acc0 = Ops::zero(), acc1 = Ops::zero(), acc2 = Ops::zero(), acc3 = Ops::zero();
+    const uint32_t eb = rp[i], ee = rp[i + 1];
+    for (uint32_t e0 = eb; e0 < ee; e0 += 32) {
+      const uint32_t cnt = min(32u, ee - e0);
+      uint32_t kk = 0;
+      float aa = 0.0f;
+      if (uint32_t(lane) < cnt) {
+        kk = ci[e0 + lane];
+        aa = wv[e0 + lane];
+      }
+#pragma unroll 4
+      for (uint32_t t = 0; t < cnt; ++t) {
+        const uint32_t k = __shfl_sync(0xffffffffu, kk, t);
+        const float a = __shfl_sync(0xffffffffu, aa, t);
+        const float* yr = y + size_t(k) * n;
+        if (kVec4) {
+          if (col0 < n) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(yr + col0));
+            acc0 = Ops::add(acc0, Ops::mul(a, v.x, err), err);
+            acc1 = Ops::add(acc1, Ops::mul(a, v.y, err), err);
+            acc2 = Ops::add(acc2, Ops::mul(a, v.z, err), err);
+            acc3 = Ops::add(acc3, Ops::mul(a, v.w, err), err);
+          }
+        } else {
+          if (col0 + 0 < n) acc0 = Ops::add(acc0, Ops::mul(a, __ldg(yr + col0 + 0), err), err);
+          if (col0 + 1 < n) acc1 = Ops::add(acc1, Ops::mul(a, __ldg(yr + col0 + 1), err), err);
+          if (col0 + 2 < n) acc2 = Ops::add(acc2, Ops::mul(a, __ldg(yr + col0 + 2), err), err);
+          if (col0 + 3 < n) acc3 = Ops::add(acc3, Ops::mul(a, __ldg(yr + col0 + 3), err), err);
+        }
+      }
+    }
+    if (kEpi == kEpiLayer) {
+      const float b = bias[i];
+      acc0 = layer_epilogue(acc0, b, clip);
+      acc1 = layer_epilogue(acc1, b, clip);
+      acc2 = layer_epilogue(acc2, b, clip);
+      acc3 = layer_epilogue(acc3, b, clip);
+    }
+    float* orow = out + size_t(i) * n;
+    if (kVec4) {
+      if (col0 < n) *reinterpret_cast<float4*>(orow + col0) = make_float4(acc0, acc1, acc2, acc3);
+    } else {
+      if (col0 + 0 < n) orow[col0 + 0] = acc0;
+      if (col0 + 1 < n) orow[col0 + 1] = acc1;
+      if (col0 + 2 < n) orow[col0 + 2] = acc2;
+      if (col0 + 3 < n) orow[col0 + 3] = acc3;
+    }
+  }
+}
+
+static unsigned spmm_grid(sk_ctx* ctx, uint32_t m, uint32_t n) {
+  const uint64_t warps = uint64_t((n + 127) / 128) * m;
+  const uint64_t blocks = (warps + 7) / 8;
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(blocks, uint64_t(ctx->num_sms) * 16)));
+}
+
+void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const float* y,
+                        uint32_t n, float clip, float* out) {
+  if (w->rows == 0 || n == 0) return;
+  const bool vec = (n % 4 == 0);
+  if (vec)
+    SK_LAUNCH((k_spmm_rows<OpArith, kEpiLayer, true>), spmm_grid(ctx, w->rows, n), 256, 0,
+              ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n, clip, out, ctx->d_err);
+  else
+    SK_LAUNCH((k_spmm_rows<OpArith, kEpiLayer, false>), spmm_grid(ctx, w->rows, n), 256, 0,
+              ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n, clip, out, ctx->d_err);
+}
+
+void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b, uint32_t n,
+                          sk_semiring s, float* out) {
+  if (a->rows == 0 || n == 0) return;
+  dispatch_semiring(s, [&](auto ops) {
+    using Ops = decltype(ops);
+    if (n % 4 == 0)
+      SK_LAUNCH((k_spmm_rows<Ops, kEpiNone, true>), spmm_grid(ctx, a->rows, n), 256, 0,
+                ctx->stream, a->rp, a->ci, a->v, nullptr, b, a->rows, n, 0.0f, out, ctx->d_err);
+    else
+      SK_LAUNCH((k_spmm_rows<Ops, kEpiNone, false>), spmm_grid(ctx, a->rows, n), 256, 0,
+                ctx->stream, a->rp, a->ci, a->v, nullptr, b, a->rows, n, 0.0f, out, ctx->d_err);
+  });
+}
+
+// ---- dense x dense over a semiring (matrix.cpp:426-447), exact ascending-k fold ----
+// 32x32 output tile per block; K staged through shared memory in 32-wide slabs.
+template <typename Ops>
+__global__ void __launch_bounds__(256)
+    k_mxm_dense_dense(const float* __restrict__ a, const float* __restrict__ b, uint32_t M,
+                      uint32_t K, uint32_t N, float* __restrict__ c, int* err) {
+  __shared__ float As[32][33];
+  __shared__ float Bs[32][33];
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const uint32_t row0 = blockIdx.y * 32, col = blockIdx.x * 32 + tx;
+  float acc[4] = {Ops::zero(), Ops::zero(), Ops::zero(), Ops::zero()};
+  for (uint32_t k0 = 0; k0 < K; k0 += 32) {
+    for (uint32_t r = ty; r < 32; r += 8) {
+      const uint32_t gi = row0 + r, gk = k0 + tx;
+      As[r][tx] = (gi < M && gk < K) ? a[size_t(gi) * K + gk] : 0.0f;
+      const uint32_t bk = k0 + r;
+      Bs[r][tx] = (bk < K && col < N) ? b[size_t(bk) * N + col] : 0.0f;
+    }
+    __syncthreads();
+    const uint32_t kmax = min(32u, K - k0);
+    for (uint32_t kk = 0; kk < kmax; ++kk) {
+      const float bv = Bs[kk][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = Ops::add(acc[q], Ops::mul(As[ty + 8 * q][kk], bv, err), err);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t gi = row0 + ty + 8 * q;
+    if (gi < M && col < N) c[size_t(gi) * N + col] = acc[q];
+  }
+}
+
+void launch_mxm_dense_dense(sk_ctx* ctx, const float* a, const float* b, uint32_t M, uint32_t K,
+                            uint32_t N, sk_semiring s, float* c) {
+  if (M == 0 || N == 0) return;
+  dim3 grid(ceil_div(N, 32), ceil_div(M, 32));
+  dispatch_semiring(s, [&](auto ops) {
+    using Ops = decltype(ops);
+    SK_LAUNCH(k_mxm_dense_dense<Ops>, grid, 256, 0, ctx->stream, a, b, M, K, N, c, ctx->d_err);
+  });
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+static void require_inner(const char* op, uint32_t ac, uint32_t br) {
+  // matrix.cpp:40-46
+  if (ac != br)
+    fail(SK_ERR_DIMENSION, std::string(op) + ": inner dimensions " + std::to_string(ac) +
+                               " and " + std::to_string(br) + " do not match");
+}
+
+extern "C" sk_status sk_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const sk_dense* b,
+                                      sk_semiring s, sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    require_inner("mxm", a->cols, b->rows);
+    sk_dense* o = new_dense(ctx, a->rows, b->cols);
+    launch_mxm_csr_dense(ctx, a, b->d, b->cols, s, o->d);
+    if (s == SK_GF2) {
+      try {
+        check_device_error(ctx, "mxm");
+      } catch (...) {
+        sk_dense_free(o);
+        throw;
+      }
+    }
+    *out = o;
+  });
+}
+
+extern "C" sk_status sk_mxm_dense_dense(sk_ctx* ctx, const sk_dense* a, const sk_dense* b,
+                                        sk_semiring s, sk_dense** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    require_inner("mxm", a->cols, b->rows);
+    sk_dense* o = new_dense(ctx, a->rows, b->cols);
+    launch_mxm_dense_dense(ctx, a->d, b->d, a->rows, a->cols, b->cols, s, o->d);
+    if (s == SK_GF2) {
+      try {
+        check_device_error(ctx, "mxm");
+      } catch (...) {
+        sk_dense_free(o);
+        throw;
+      }
+    }
+    *out = o;
+  });
+}
+
+extern "C" sk_status sk_mxm_csr_csr(sk_ctx* ctx, const sk_csr* a, const sk_csr* b,
+                                    sk_semiring s, sk_csr** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    require_inner("mxm", a->cols, b->rows);
+    sk_csr* o = mxm_csr_csr_impl(ctx, a, b, s);
+    if (s == SK_GF2) {
+      try {
+        check_device_error(ctx, "mxm");
+      } catch (...) {
+        csr_release(o);
+        throw;
+      }
+    }
+    *out = o;
+  });
+}

@@ -1,0 +1,494 @@
+// C-ABI entry points of libsk_b200 (include/sk_api.h): contexts, handles,
+// transfers, model construction and argument/shape checking.  Shape checks
+// and their messages follow the reference (proj/src/matrix.cpp:28-46,
+// proj/src/dnn.cpp:23-61,86-98); the compute lives in k_*.cu.
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <mutex>
+
+#include "sk_common.cuh"
+
+namespace sk {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_last_error;
+
+void set_last_error(const std::string& msg) { t_last_error = msg; }
+
+void dfree(sk_ctx* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+sk_dense* new_dense(sk_ctx* ctx, uint32_t rows, uint32_t cols) {
+  auto* d = new sk_dense;
+  d->ctx = ctx;
+  d->rows = rows;
+  d->cols = cols;
+  d->d = dalloc<float>(ctx, d->elems());
+  return d;
+}
+
+sk_csr* new_csr(sk_ctx* ctx, uint32_t rows, uint32_t cols, size_t nnz) {
+  auto* a = new sk_csr;
+  a->ctx = ctx;
+  a->rows = rows;
+  a->cols = cols;
+  a->nnz = nnz;
+  a->rp = dalloc<uint32_t>(ctx, size_t(rows) + 1);
+  a->ci = dalloc<uint32_t>(ctx, nnz);
+  a->v = dalloc<float>(ctx, nnz);
+  return a;
+}
+
+void csr_release(sk_csr* a) {
+  if (!a) return;
+  if (a->refs.fetch_sub(1) == 1) {
+    dfree(a->ctx, a->rp);
+    dfree(a->ctx, a->ci);
+    dfree(a->ctx, a->v);
+    delete a;
+  }
+}
+
+void sync(sk_ctx* ctx) { SK_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+void timing_mark(sk_ctx* ctx) {
+  if (!ctx->timing) return;
+  if (ctx->ev_used == ctx->ev.size()) {
+    cudaEvent_t e;
+    SK_CUDA(cudaEventCreate(&e));
+    ctx->ev.push_back(e);
+  }
+  SK_CUDA(cudaEventRecord(ctx->ev[ctx->ev_used++], ctx->stream));
+}
+
+void check_device_error(sk_ctx* ctx, const char* op) {
+  int err = 0;
+  SK_CUDA(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  sync(ctx);
+  if (err != 0) {
+    SK_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+    if (err == kErrGf2Domain)
+      fail(SK_ERR_DOMAIN, std::string(op) + ": GF(2) scalar must be 0 or 1");
+    fail(SK_ERR, std::string(op) + ": device error " + std::to_string(err));
+  }
+}
+
+void exclusive_scan_u32(sk_ctx* ctx, const uint32_t* in, uint32_t* out, size_t n) {
+  size_t tmp = 0;
+  SK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, ctx->stream));
+  void* t = dalloc<char>(ctx, tmp);
+  SK_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, ctx->stream));
+  g_launches.fetch_add(1);
+  dfree(ctx, t);
+}
+
+void exclusive_scan_u64(sk_ctx* ctx, const uint64_t* in, uint64_t* out, size_t n) {
+  size_t tmp = 0;
+  SK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, ctx->stream));
+  void* t = dalloc<char>(ctx, tmp);
+  SK_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, ctx->stream));
+  g_launches.fetch_add(1);
+  dfree(ctx, t);
+}
+
+float semiring_zero_host(sk_semiring s) {
+  switch (s) {
+    case SK_MAX_PLUS: return -INFINITY;
+    case SK_MIN_MAX: return INFINITY;
+    default: return 0.0f;
+  }
+}
+
+static void require_ctx(sk_ctx* ctx) {
+  if (!ctx) fail(SK_ERR_INVALID_ARGUMENT, "null context");
+  SK_CUDA(cudaSetDevice(ctx->device));
+}
+
+// ---- small kernels used by the API layer ---------------------------------------
+
+__global__ void k_fill(float* p, size_t n, float v) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_identity(float* p, uint32_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < size_t(n);
+       i += size_t(gridDim.x) * blockDim.x)
+    p[i * n + i] = 1.0f;
+}
+
+void fill(sk_ctx* ctx, float* p, size_t n, float v) {
+  if (n == 0) return;
+  unsigned grid = std::min<unsigned>(ceil_div(n, 256), ctx->num_sms * 8);
+  SK_LAUNCH(k_fill, grid, 256, 0, ctx->stream, p, n, v);
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+// ==== library / context ==========================================================
+
+extern "C" const char* sk_last_error(void) { return sk::t_last_error.c_str(); }
+extern "C" const char* sk_version(void) { return "sk_b200 0.1 (sm_100a)"; }
+extern "C" uint64_t sk_kernel_launch_count(void) { return g_launches.load(); }
+
+extern "C" sk_status sk_ctx_create(int device, sk_ctx** out) {
+  return guarded([&] {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+      fail(SK_ERR_CUDA, std::string("no CUDA device available: ") +
+                            (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+    if (device < 0 || device >= count)
+      fail(SK_ERR_INVALID_ARGUMENT, "device " + std::to_string(device) + " out of range");
+    SK_CUDA(cudaSetDevice(device));
+    auto* c = new sk_ctx;
+    c->device = device;
+    SK_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    SK_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    cudaMemPool_t pool;
+    SK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thresh = UINT64_MAX;
+    SK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    SK_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
+    SK_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+    SK_CUDA(cudaMalloc(&c->d_u64, 64 * sizeof(uint64_t)));
+    SK_CUDA(cudaMemset(c->d_u64, 0, 64 * sizeof(uint64_t)));
+    SK_CUDA(cudaMallocHost(&c->h_u64, 64 * sizeof(uint64_t)));
+    *out = c;
+  });
+}
+
+extern "C" sk_status sk_ctx_destroy(sk_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->d_err);
+    cudaFree(ctx->d_u64);
+    cudaFreeHost(ctx->h_u64);
+    for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+  });
+}
+
+extern "C" sk_status sk_ctx_set_stream(sk_ctx* ctx, void* s) {
+  return guarded([&] {
+    require_ctx(ctx);
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+  });
+}
+
+extern "C" void* sk_ctx_stream(const sk_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+extern "C" sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable) {
+  return guarded([&] {
+    require_ctx(ctx);
+    ctx->timing = enable != 0;
+    ctx->ev_used = 0;
+  });
+}
+
+extern "C" sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count) {
+  return guarded([&] {
+    require_ctx(ctx);
+    sync(ctx);
+    const size_t pairs = ctx->ev_used / 2;
+    *count = pairs;
+    for (size_t i = 0; i < pairs && i < cap; ++i)
+      SK_CUDA(cudaEventElapsedTime(&ms[i], ctx->ev[2 * i], ctx->ev[2 * i + 1]));
+    ctx->ev_used = 0;
+  });
+}
+
+extern "C" sk_status sk_ctx_synchronize(sk_ctx* ctx) {
+  return guarded([&] {
+    require_ctx(ctx);
+    sync(ctx);
+  });
+}
+
+extern "C" sk_status sk_host_register(void* p, size_t bytes) {
+  return guarded([&] { SK_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault)); });
+}
+
+extern "C" sk_status sk_host_unregister(void* p) {
+  return guarded([&] { SK_CUDA(cudaHostUnregister(p)); });
+}
+
+// ==== dense =======================================================================
+
+extern "C" sk_status sk_dense_create(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                     float fillv, sk_dense** out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    sk_dense* d = new_dense(ctx, rows, cols);
+    fill(ctx, d->d, d->elems(), fillv);
+    *out = d;
+  });
+}
+
+extern "C" sk_status sk_dense_upload(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                     const float* host, sk_dense** out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    sk_dense* d = new_dense(ctx, rows, cols);
+    if (d->elems())
+      SK_CUDA(cudaMemcpyAsync(d->d, host, d->elems() * sizeof(float),
+                              cudaMemcpyHostToDevice, ctx->stream));
+    *out = d;
+  });
+}
+
+extern "C" sk_status sk_dense_write(sk_ctx* ctx, sk_dense* d, const float* host) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (d->elems())
+      SK_CUDA(cudaMemcpyAsync(d->d, host, d->elems() * sizeof(float),
+                              cudaMemcpyHostToDevice, ctx->stream));
+  });
+}
+
+extern "C" sk_status sk_dense_download(sk_ctx* ctx, const sk_dense* d, float* host) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (d->elems())
+      SK_CUDA(cudaMemcpyAsync(host, d->d, d->elems() * sizeof(float),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+  });
+}
+
+extern "C" sk_status sk_dense_download_async(sk_ctx* ctx, const sk_dense* d, float* host) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (d->elems())
+      SK_CUDA(cudaMemcpyAsync(host, d->d, d->elems() * sizeof(float),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  });
+}
+
+extern "C" sk_status sk_dense_shape(const sk_dense* d, uint32_t* rows, uint32_t* cols) {
+  return guarded([&] {
+    if (rows) *rows = d->rows;
+    if (cols) *cols = d->cols;
+  });
+}
+
+extern "C" float* sk_dense_device_ptr(const sk_dense* d) { return d ? d->d : nullptr; }
+
+extern "C" sk_status sk_dense_identity(sk_ctx* ctx, uint32_t n, sk_dense** out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    sk_dense* d = new_dense(ctx, n, n);
+    fill(ctx, d->d, d->elems(), 0.0f);
+    if (n) SK_LAUNCH(k_identity, ceil_div(n, 256), 256, 0, ctx->stream, d->d, n);
+    *out = d;
+  });
+}
+
+extern "C" sk_status sk_dense_free(sk_dense* d) {
+  return guarded([&] {
+    if (!d) return;
+    dfree(d->ctx, d->d);
+    delete d;
+  });
+}
+
+// ==== CSR =========================================================================
+
+extern "C" sk_status sk_csr_shape(const sk_csr* a, uint32_t* rows, uint32_t* cols,
+                                  size_t* nnz) {
+  return guarded([&] {
+    if (rows) *rows = a->rows;
+    if (cols) *cols = a->cols;
+    if (nnz) *nnz = a->nnz;
+  });
+}
+
+extern "C" sk_status sk_csr_extract(sk_ctx* ctx, const sk_csr* a, uint32_t* rp,
+                                    uint32_t* ci, float* v) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (rp)
+      SK_CUDA(cudaMemcpyAsync(rp, a->rp, (size_t(a->rows) + 1) * 4,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    if (ci && a->nnz)
+      SK_CUDA(cudaMemcpyAsync(ci, a->ci, a->nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (v && a->nnz)
+      SK_CUDA(cudaMemcpyAsync(v, a->v, a->nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+  });
+}
+
+extern "C" sk_status sk_csr_free(sk_csr* a) {
+  return guarded([&] { csr_release(a); });
+}
+
+// ==== model ===========================================================================
+
+extern "C" sk_status sk_model_create(sk_ctx* ctx, uint32_t layers,
+                                     const sk_csr* const* weights,
+                                     const float* const* biases, sk_model** out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    // dnn.cpp:23-51
+    if (layers == 0) fail(SK_ERR_INVALID_ARGUMENT, "model must have at least one layer");
+    if (!biases)
+      fail(SK_ERR_INVALID_ARGUMENT, "model has " + std::to_string(layers) +
+                                        " weight matrices but 0 bias vectors");
+    const uint32_t m = weights[0]->rows;
+    for (uint32_t k = 0; k < layers; ++k) {
+      const sk_csr* w = weights[k];
+      if (w->rows != m || w->cols != m)
+        fail(SK_ERR_DIMENSION, "layer " + std::to_string(k) + " weight is " +
+                                   dim_string(w->rows, w->cols) + "; all layers must be " +
+                                   dim_string(m, m));
+      if (!biases[k])
+        fail(SK_ERR_DIMENSION, "layer " + std::to_string(k) + " bias length 0 does not match " +
+                                   std::to_string(m) + " neurons");
+    }
+    auto* md = new sk_model;
+    md->ctx = ctx;
+    md->layers = layers;
+    md->neurons = m;
+    md->bias_host.resize(size_t(layers) * m);
+    md->bias_nonpos.resize(layers);
+    for (uint32_t k = 0; k < layers; ++k) {
+      auto* w = const_cast<sk_csr*>(weights[k]);
+      w->refs.fetch_add(1);
+      md->w.push_back(w);
+      std::memcpy(md->bias_host.data() + size_t(k) * m, biases[k], size_t(m) * 4);
+      bool nonpos = true;
+      for (uint32_t i = 0; i < m; ++i) nonpos &= (biases[k][i] <= 0.0f);
+      md->bias_nonpos[k] = nonpos;
+    }
+    md->bias = dalloc<float>(ctx, md->bias_host.size());
+    SK_CUDA(cudaMemcpyAsync(md->bias, md->bias_host.data(), md->bias_host.size() * 4,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    sync(ctx);  // host bias copy may be released by the caller
+    *out = md;
+  });
+}
+
+extern "C" sk_status sk_model_shape(const sk_model* m, uint32_t* layers, uint32_t* neurons) {
+  return guarded([&] {
+    if (layers) *layers = m->layers;
+    if (neurons) *neurons = m->neurons;
+  });
+}
+
+extern "C" sk_status sk_model_free(sk_model* m) {
+  return guarded([&] {
+    if (!m) return;
+    for (sk_csr* w : m->w) csr_release(w);
+    dfree(m->ctx, m->bias);
+    delete m;
+  });
+}
+
+// ==== DNN: dense activations ===========================================================
+
+static float opt_clip(const sk_fwd_opts* o) { return o ? o->clip : 0.0f; }
+
+static void require_input(uint32_t neurons, const sk_dense* y) {
+  // dnn.cpp:55-61
+  if (y->rows != neurons || y->cols < 1)
+    fail(SK_ERR_DIMENSION, "input batch is " + dim_string(y->rows, y->cols) + ", expected " +
+                               std::to_string(neurons) + " rows and n >= 1 columns");
+}
+
+extern "C" sk_status sk_layer_step(sk_ctx* ctx, const sk_csr* w, const float* bias,
+                                   const sk_dense* y, const sk_fwd_opts* opt,
+                                   sk_dense** out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    // dnn.cpp:89-98
+    if (w->cols != y->rows)
+      fail(SK_ERR_DIMENSION, "weight is " + dim_string(w->rows, w->cols) + " but input has " +
+                                 std::to_string(y->rows) + " rows");
+    if (!bias)
+      fail(SK_ERR_DIMENSION, "bias length 0 does not match " + std::to_string(w->rows) +
+                                 " output rows");
+    float* db = dalloc<float>(ctx, w->rows);
+    SK_CUDA(cudaMemcpyAsync(db, bias, size_t(w->rows) * 4, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    sk_dense* o = new_dense(ctx, w->rows, y->cols);
+    launch_layer_dense(ctx, w, db, y->d, y->cols, opt_clip(opt), o->d);
+    dfree(ctx, db);
+    sync(ctx);  // the host bias buffer is borrowed only for this call
+    *out = o;
+  });
+}
+
+static sk_dense* forward_dense(sk_ctx* ctx, const sk_model* m, const sk_dense* y0,
+                               float clip) {
+  require_input(m->neurons, y0);
+  const uint32_t n = y0->cols;
+  sk_dense* a = new_dense(ctx, m->neurons, n);
+  sk_dense* b = m->layers > 1 ? new_dense(ctx, m->neurons, n) : nullptr;
+  const float* src = y0->d;
+  sk_dense* dst = a;
+  for (uint32_t k = 0; k < m->layers; ++k) {
+    timing_mark(ctx);
+    launch_layer_dense(ctx, m->w[k], m->bias + size_t(k) * m->neurons, src, n, clip, dst->d);
+    timing_mark(ctx);
+    src = dst->d;
+    dst = (dst == a) ? b : a;
+  }
+  sk_dense* result = (m->layers % 2 == 1) ? a : b;
+  sk_dense* spare = (result == a) ? b : a;
+  if (spare) sk_dense_free(spare);
+  return result;
+}
+
+extern "C" sk_status sk_relu_forward(sk_ctx* ctx, const sk_model* m, const sk_dense* y0,
+                                     const sk_fwd_opts* opt, sk_dense** out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    *out = forward_dense(ctx, m, y0, opt_clip(opt));
+  });
+}
+
+extern "C" sk_status sk_relu_forward_host(sk_ctx* ctx, const sk_model* m, uint32_t n,
+                                          const float* y0, const sk_fwd_opts* opt,
+                                          float* yL) {
+  return guarded([&] {
+    require_ctx(ctx);
+    sk_dense in;
+    in.ctx = ctx;
+    in.rows = m->neurons;
+    in.cols = n;
+    in.d = dalloc<float>(ctx, in.elems());
+    SK_CUDA(cudaMemcpyAsync(in.d, y0, in.elems() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    sk_dense* r = forward_dense(ctx, m, &in, opt_clip(opt));
+    SK_CUDA(cudaMemcpyAsync(yL, r->d, r->elems() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    dfree(ctx, in.d);
+    sk_dense_free(r);
+    sync(ctx);
+  });
+}
+
+extern "C" sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m, const sk_csr* y0,
+                                            const sk_fwd_opts* opt, sk_csr** out,
+                                            uint64_t* nnz_trace) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (y0->rows != m->neurons || y0->cols < 1)
+      fail(SK_ERR_DIMENSION, "input batch is " + dim_string(y0->rows, y0->cols) +
+                                 ", expected " + std::to_string(m->neurons) +
+                                 " rows and n >= 1 columns");
+    *out = sparse_forward_impl(ctx, m, y0, opt_clip(opt), nnz_trace);
+  });
+}
+
+extern "C" uint64_t sk_layer_seed(uint64_t seed, uint32_t layer) {
+  return splitmix_at(seed, 1000ull + layer);
+}

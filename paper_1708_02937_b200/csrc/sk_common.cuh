@@ -1,0 +1,248 @@
+// Internals shared by the libsk_b200 translation units.
+//
+// Design notes (see DESIGN.md for the full picture):
+//  * Every handle remembers the context whose stream allocated it; memory is
+//    stream-ordered (cudaMallocAsync / cudaFreeAsync) from the device's default
+//    memory pool with an unlimited release threshold, so per-call allocations
+//    are pool hits, not driver calls.
+//  * Errors are reported as sk_status plus a thread-local message.  Errors a
+//    kernel discovers (GF(2) domain violations) are written to a device error
+//    word owned by the context and read back after the kernel, mirroring the
+//    reference's exceptions thrown from inside worker threads
+//    (proj/src/detail/parallel.hpp:55-70).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sk_api.h"
+
+namespace sk {
+
+// ---- status plumbing ----------------------------------------------------------
+
+struct Failure {
+  sk_status code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(sk_status code, const std::string& msg) {
+  throw Failure{code, msg};
+}
+
+void set_last_error(const std::string& msg);
+
+#define SK_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess) {                                                 \
+      if (e_ == cudaErrorMemoryAllocation)                                   \
+        ::sk::fail(SK_ERR_OOM, std::string("device allocation failed: ") +   \
+                                   cudaGetErrorString(e_));                  \
+      ::sk::fail(SK_ERR_CUDA, std::string(#call) + ": " +                    \
+                                  cudaGetErrorString(e_));                   \
+    }                                                                        \
+  } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+
+// Every kernel launch goes through this so the count is exact.
+#define SK_LAUNCH(kernel, grid, block, smem, stream, ...)                    \
+  do {                                                                       \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
+    ::sk::g_launches.fetch_add(1, std::memory_order_relaxed);                \
+    SK_CUDA(cudaGetLastError());                                             \
+  } while (0)
+
+template <typename F>
+sk_status guarded(F&& f) {
+  try {
+    f();
+    return SK_OK;
+  } catch (const Failure& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return SK_ERR_OOM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return SK_ERR;
+  }
+}
+
+inline std::string dim_string(uint32_t r, uint32_t c) {
+  return std::to_string(r) + "x" + std::to_string(c);
+}
+
+inline unsigned ceil_div(uint64_t a, uint64_t b) { return unsigned((a + b - 1) / b); }
+
+}  // namespace sk
+
+// ---- handles ------------------------------------------------------------------
+
+struct sk_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int num_sms = 148;
+  int* d_err = nullptr;      // device error word (0 = ok)
+  uint64_t* d_u64 = nullptr; // small device scratch for counters/flags (64 slots)
+  uint64_t* h_u64 = nullptr; // pinned mirror of d_u64
+  // Optional per-layer timing of the dominant kernel (CUDA events recorded on
+  // this stream around each layer's SpGEMM launch); see sk_ctx_set_timing.
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // 2 per layer
+  size_t ev_used = 0;
+};
+
+struct sk_dense {
+  sk_ctx* ctx = nullptr;
+  uint32_t rows = 0, cols = 0;
+  float* d = nullptr;
+  size_t elems() const { return size_t(rows) * cols; }
+};
+
+struct sk_csr {
+  sk_ctx* ctx = nullptr;
+  uint32_t rows = 0, cols = 0;
+  size_t nnz = 0;
+  uint32_t* rp = nullptr;  // rows+1
+  uint32_t* ci = nullptr;  // nnz
+  float* v = nullptr;      // nnz
+  std::atomic<int> refs{1};
+};
+
+struct sk_model {
+  sk_ctx* ctx = nullptr;
+  uint32_t layers = 0, neurons = 0;
+  std::vector<sk_csr*> w;       // shared (ref-counted) layer weights
+  float* bias = nullptr;        // device, layers*neurons
+  std::vector<float> bias_host; // layers*neurons
+  std::vector<uint8_t> bias_nonpos;  // per layer: every b <= 0 (no NaN)
+};
+
+namespace sk {
+
+// device memory (stream-ordered)
+template <typename T>
+T* dalloc(sk_ctx* ctx, size_t n) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  SK_CUDA(cudaMallocAsync(&p, n * sizeof(T), ctx->stream));
+  return static_cast<T*>(p);
+}
+void dfree(sk_ctx* ctx, void* p);
+
+sk_dense* new_dense(sk_ctx* ctx, uint32_t rows, uint32_t cols);
+sk_csr* new_csr(sk_ctx* ctx, uint32_t rows, uint32_t cols, size_t nnz);
+void csr_release(sk_csr* a);
+
+// Reads and clears the context's device error word (synchronising).
+void check_device_error(sk_ctx* ctx, const char* op);
+void sync(sk_ctx* ctx);
+// Record a timing event pair slot (no-op unless ctx->timing).
+void timing_mark(sk_ctx* ctx);
+void fill(sk_ctx* ctx, float* p, size_t n, float v);
+
+// device scan helpers (CUB, stream-ordered temp storage)
+void exclusive_scan_u32(sk_ctx* ctx, const uint32_t* in, uint32_t* out, size_t n);
+void exclusive_scan_u64(sk_ctx* ctx, const uint64_t* in, uint64_t* out, size_t n);
+
+// ---- semiring op tables (semiring.hpp:63-110), device side --------------------
+
+enum DevErr : int { kErrNone = 0, kErrGf2Domain = 1 };
+
+struct OpArith {
+  static constexpr int kind = SK_ARITHMETIC;
+  __device__ static float zero() { return 0.0f; }
+  __device__ static float add(float a, float b, int*) { return __fadd_rn(a, b); }
+  __device__ static float mul(float a, float b, int*) { return __fmul_rn(a, b); }
+};
+struct OpMaxPlus {
+  static constexpr int kind = SK_MAX_PLUS;
+  __device__ static float zero() { return -__int_as_float(0x7f800000); }
+  __device__ static float add(float a, float b, int*) { return a < b ? b : a; }
+  __device__ static float mul(float a, float b, int*) { return __fadd_rn(a, b); }
+};
+struct OpMinMax {
+  static constexpr int kind = SK_MIN_MAX;
+  __device__ static float zero() { return __int_as_float(0x7f800000); }
+  __device__ static float add(float a, float b, int*) { return b < a ? b : a; }
+  __device__ static float mul(float a, float b, int*) { return a < b ? b : a; }
+};
+struct OpGf2 {
+  static constexpr int kind = SK_GF2;
+  __device__ static float zero() { return 0.0f; }
+  __device__ static bool ok(float v) { return v == 0.0f || v == 1.0f; }
+  __device__ static float add(float a, float b, int* err) {
+    if (!ok(a) || !ok(b)) atomicCAS(err, 0, kErrGf2Domain);
+    return a == b ? 0.0f : 1.0f;
+  }
+  __device__ static float mul(float a, float b, int* err) {
+    if (!ok(a) || !ok(b)) atomicCAS(err, 0, kErrGf2Domain);
+    return (a == 1.0f && b == 1.0f) ? 1.0f : 0.0f;
+  }
+};
+
+template <typename F>
+void dispatch_semiring(sk_semiring s, F&& f) {
+  switch (s) {
+    case SK_ARITHMETIC: f(OpArith{}); return;
+    case SK_MAX_PLUS: f(OpMaxPlus{}); return;
+    case SK_MIN_MAX: f(OpMinMax{}); return;
+    case SK_GF2: f(OpGf2{}); return;
+  }
+  fail(SK_ERR_INVALID_ARGUMENT, "unknown semiring kind " + std::to_string(int(s)));
+}
+
+float semiring_zero_host(sk_semiring s);
+
+// ---- the layer epilogue (dnn.cpp:65-103 + optional clip) -----------------------
+// z = acc + b (max-plus "times"); z = z<0 ? 0 : z (max-plus "plus" with 0,
+// semiring.hpp:75 -- a select, so -0.0 and NaN pass through); clip by select.
+__device__ __forceinline__ float layer_epilogue(float acc, float b, float clip) {
+  float z = __fadd_rn(acc, b);
+  z = (z < 0.0f) ? 0.0f : z;
+  if (clip > 0.0f) z = (z > clip) ? clip : z;
+  return z;
+}
+
+// ---- SplitMix64 (rng.hpp:29-62), device side ------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t idx) {
+  return mix64(seed + (idx + 1) * 0x9E3779B97F4A7C15ull);
+}
+__device__ __forceinline__ double to_unit(uint64_t bits) {
+  return __dmul_rn((double)(bits >> 11), 0x1.0p-53);
+}
+
+// ---- internal entry points implemented in the .cu files ------------------------
+sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                const uint32_t* d_r, const uint32_t* d_c,
+                                const float* d_v, size_t n,
+                                const uint32_t* h_r, const uint32_t* h_c);
+sk_csr* csr_transpose(sk_ctx* ctx, const sk_csr* a);
+void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias,
+                        const float* y, uint32_t n, float clip, float* out);
+void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b,
+                          uint32_t n, sk_semiring s, float* out);
+sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b,
+                         sk_semiring s);
+sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* m, const sk_csr* y0,
+                            float clip, uint64_t* nnz_trace);
+void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b,
+                          uint32_t M, uint32_t K, uint32_t N, const float* bias,
+                          int relu, float* c);
+
+}  // namespace sk

@@ -1,0 +1,381 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference
+library (oracle/_ref), the C restatement (oracle/_build) and the committed
+golden fixtures.  Bitwise for the sparse path; the tensor-core dense leg is
+checked with the reference's magnitude-scaled tolerance
+(approx_equal_scaled, semiring.hpp:50-55, kRelTol = 1e-5)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle.oracle import csr as hcsr
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def same_bits_nan(a, b):
+    """Bitwise equal except NaN payloads: the GPU emits the canonical NaN
+    (0x7fffffff) where x86 propagates the input payload, so NaN positions must
+    match and every other value must be bit-identical."""
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    na, nb = np.isnan(a), np.isnan(b)
+    return np.array_equal(na, nb) and np.array_equal(bits(a)[~na], bits(b)[~nb])
+
+
+def dev_csr(sk, a):
+    return sk.CsrMatrix(a.rows, a.cols, a.row_ptr, a.col_idx, a.values)
+
+
+def host_csr(a):
+    rp, ci, v = a.extract()
+    return hcsr(a.rows(), a.cols(), rp, ci, v)
+
+
+def assert_csr_bitwise(got, want):
+    g = host_csr(got)
+    assert g.rows == want.rows and g.cols == want.cols
+    assert np.array_equal(g.row_ptr, want.row_ptr)
+    assert np.array_equal(g.col_idx, want.col_idx)
+    assert np.array_equal(bits(g.values), bits(want.values))
+
+
+# ---- known answers (proj/tests/test_dnn.cpp, test_matrix.cpp) ---------------------------
+
+def test_known_answers(sk):
+    kat = json.load(open(os.path.join(GOLDEN, "kat.json")))
+    I2 = sk.DnnModel([sk.Matrix(sk.DenseMatrix.identity(2))], [[0.0, 0.0]])
+    x = sk.DenseMatrix(2, 1, [3.0, -2.0])
+    assert sk.relu_forward(I2, x).numpy().tolist() == kat["identity_clamp"]
+    assert sk.dense_relu_forward(I2, x).numpy().tolist() == kat["identity_clamp"]
+    W = sk.DenseMatrix(2, 2, [1, 2, 3, 4])
+    model = sk.DnnModel([sk.Matrix(W)], [[1.0, -100.0]])
+    assert sk.relu_forward(model, sk.DenseMatrix(2, 1, 1.0)).numpy().tolist() == kat["hand_layer"]
+    assert sk.dense_relu_forward(model, sk.DenseMatrix(2, 1, 1.0)).numpy().tolist() == kat["hand_layer"]
+    B = sk.DenseMatrix(2, 1, [5, 6])
+    assert sk.mxm(W, B, sk.arithmetic_semiring()).numpy().tolist() == kat["mxm_arith"]
+    assert sk.mxm(W, B, sk.max_plus_semiring()).numpy().tolist() == kat["mxm_maxplus"]
+    neg = sk.DnnModel([sk.Matrix(sk.DenseMatrix(2, 2, [-1, -2, -3, -4]))], [[-1.0, -1.0]])
+    assert sk.dense_relu_forward(neg, sk.DenseMatrix(2, 2, [1, 2, 1, 2])).numpy().tolist() == \
+        kat["all_negative"]
+    empty = sk.csr_from_triples(3, 3, [])
+    assert sk.layer_step(sk.Matrix(empty), [0.0] * 3, sk.DenseMatrix(3, 2, 1.0)).numpy().tolist() \
+        == kat["empty_w"]
+    I4 = sk.Matrix(sk.DenseMatrix.identity(4))
+    assert sk.layer_step(I4, [-1.0] * 4, sk.DenseMatrix(4, 3, 1.0)).numpy().tolist() == \
+        kat["identity_minus1"]
+
+
+def test_csr_from_triples_matches_reference(sk, ref):
+    kat = json.load(open(os.path.join(GOLDEN, "kat.json")))
+    t = sk.csr_from_triples(1, 3, [(0, 2, 3.0), (0, 0, 1.0), (0, 1, 2.0)])
+    assert t.row_ptr().tolist() == kat["triples_sorted"]["rp"]
+    assert t.col_idx().tolist() == kat["triples_sorted"]["ci"]
+    assert t.values().tolist() == kat["triples_sorted"]["v"]
+    t = sk.csr_from_triples(2, 2, [(0, 0, 0.0), (1, 1, 2.0)])
+    assert t.nnz() == 1 and t.row_ptr().tolist() == kat["triples_zero_elided"]["rp"]
+    cases = {"out_of_range": (2, 2, [2], [0], [1.0]),
+             "duplicate": (2, 2, [0, 0], [1, 1], [1.0, 2.0]),
+             "dup_after_sort": (3, 3, [2, 0, 2, 1], [1, 0, 1, 2], [1.0, 1.0, 5.0, 0.0]),
+             "first_bad_in_input_order": (4, 4, [0, 9, 5], [0, 1, 0], [1., 1., 1.])}
+    for name, (rows, cols, r, c, v) in cases.items():
+        with pytest.raises(sk.InvalidArgument) as e:
+            sk.csr_from_triples(rows, cols, (r, c, v))
+        assert str(e.value) == kat["triple_errors"][name]["msg"], name
+    # random triples, shuffled, with zeros: same CSR as the reference
+    rng = np.random.default_rng(3)
+    flat = rng.choice(300 * 200, size=5000, replace=False)
+    r, c = (flat // 200).astype(np.uint32), (flat % 200).astype(np.uint32)
+    v = rng.uniform(-1, 1, 5000).astype(np.float32)
+    v[::7] = 0.0
+    assert_csr_bitwise(sk.csr_from_triples(300, 200, (r, c, v)),
+                       ref.csr_from_triples(300, 200, r, c, v))
+    e = sk.csr_from_triples(2, 2, [])
+    assert e.nnz() == 0 and e.row_ptr().tolist() == [0, 0, 0]
+
+
+def test_validating_constructor_messages(sk):
+    kat = json.load(open(os.path.join(GOLDEN, "kat.json")))["validate_errors"]
+    cases = {"not_monotone": (3, 2, [0, 1, 0, 1], [0], [1.0]),
+             "cols_not_increasing": (1, 2, [0, 2], [1, 0], [1.0, 2.0]),
+             "col_out_of_range": (1, 2, [0, 1], [5], [1.0])}
+    for name, (rows, cols, rp, ci, v) in cases.items():
+        with pytest.raises(sk.InvalidArgument) as e:
+            sk.CsrMatrix(rows, cols, rp, ci, v)
+        assert str(e.value) == kat[name]["msg"]
+    assert sk.CsrMatrix(1, 2, [0, 2], [0, 1], [0.0, 2.0]).nnz() == 2  # stored zero allowed
+    with pytest.raises(sk.InvalidArgument):
+        sk.CsrMatrix(2, 2, [0, 1], [0], [1.0])  # row_ptr length != rows+1
+
+
+# ---- generators are bitwise the oracle's ------------------------------------------------
+
+def test_device_generators_match_oracle(sk, port):
+    a = sk.gen_layer_fixed(2048, 32, 77, 1.0 / 16)
+    assert_csr_bitwise(a, port.gen_layer_fixed(2048, 32, 77, 1.0 / 16))
+    a = sk.gen_layer_fixed(1024, 16, 78)
+    assert_csr_bitwise(a, port.gen_layer_fixed(1024, 16, 78))
+    a = sk.gen_layer_density(512, 0.05, 79)
+    assert_csr_bitwise(a, port.gen_layer_density(512, 0.05, 79))
+    y = sk.gen_input_dense(300, 70, 80)
+    assert np.array_equal(bits(y.numpy()), bits(port.gen_input_dense(300, 70, 80)))
+    b = sk.gen_input_binary(4096, 500, 60, 81, sample_offset=1234)
+    assert_csr_bitwise(b, port.gen_input_binary(4096, 500, 60, 81, 1234))
+
+
+# ---- the dense-activation path (K1) ---------------------------------------------------------
+
+def test_cfg1_full_bitwise_vs_reference_golden(sk):
+    g = np.load(os.path.join(GOLDEN, "cfg1.npz"))
+    m, n, L, k, seed = (int(g[x]) for x in ("m", "n", "L", "k", "seed"))
+    Ws = [sk.gen_layer_fixed(m, k, sk.layer_seed(seed, i)) for i in range(L)]
+    model = sk.DnnModel(Ws, [np.full(m, g["bias"], np.float32)] * L)
+    y0 = sk.gen_input_dense(m, n, seed)
+    out = sk.relu_forward(model, y0)
+    assert np.array_equal(bits(out.numpy()), bits(g["yL"]))
+    assert np.array_equal(sk.categories(out), g["categories"])
+    # the reference-facing host path (H2D -> forward -> D2H)
+    host = sk.relu_forward_host(model, y0.numpy())
+    assert np.array_equal(bits(host), bits(g["yL"]))
+    # determinism / worker independence (dnn.hpp:75-76)
+    for w in (1, 2, 7):
+        again = sk.relu_forward(model, y0, sk.ForwardOptions(workers=w)).numpy()
+        assert np.array_equal(bits(again), bits(g["yL"]))
+
+
+def test_random_models_bitwise_vs_reference(sk):
+    g = np.load(os.path.join(GOLDEN, "random_models.npz"))
+    for t in range(12):
+        mm, layers, nn = (int(x) for x in g[f"t{t}_meta"])
+        Ws = [sk.CsrMatrix(mm, mm, g[f"t{t}_w{k}_rp"], g[f"t{t}_w{k}_ci"], g[f"t{t}_w{k}_v"])
+              for k in range(layers)]
+        model = sk.DnnModel(Ws, [g[f"t{t}_b{k}"] for k in range(layers)])
+        y0 = sk.DenseMatrix.from_numpy(g[f"t{t}_y0"])
+        out = sk.relu_forward(model, y0).numpy()
+        assert np.array_equal(bits(out), bits(g[f"t{t}_out"])), t
+        assert (out >= 0).all()
+        dout = sk.dense_relu_forward(model, y0).numpy()
+        want = g[f"t{t}_dense_out"]
+        scale = np.maximum(np.abs(want), 1.0)
+        assert (np.abs(dout - want) <= np.maximum(1e-6, 1e-5 * scale * mm)).all(), t
+
+
+def test_cfg2_small_bitwise_vs_reference_golden(sk):
+    g = np.load(os.path.join(GOLDEN, "cfg2_small.npz"))
+    m, n, seed = int(g["m"]), int(g["n"]), int(g["seed"])
+    y = sk.gen_input_dense(m, n, seed)
+    for d in (0.01, 0.001):
+        key = f"d{d:g}".replace(".", "p")
+        W = sk.gen_layer_density(m, d, sk.layer_seed(seed, 0))
+        assert W.nnz() == int(g[f"{key}_nnz"])
+        out = sk.layer_step(sk.Matrix(W), np.full(m, -0.05, np.float32), y)
+        assert np.array_equal(bits(out.numpy()), bits(g[f"{key}_out"]))
+
+
+def test_layer_step_matches_reference_on_odd_shapes(sk, ref, port):
+    rng = np.random.default_rng(11)
+    for m, n in [(1, 1), (5, 3), (33, 1), (64, 130), (257, 257), (1000, 5)]:
+        W = port.gen_layer_fixed(m, min(m, 7), int(rng.integers(1 << 30)))
+        y = rng.uniform(-1, 1, (m, n)).astype(np.float32)
+        y[rng.random((m, n)) < 0.2] = 0.0
+        b = rng.uniform(-0.5, 0.5, m).astype(np.float32)
+        got = sk.layer_step(sk.Matrix(dev_csr(sk, W)), b, sk.DenseMatrix.from_numpy(y)).numpy()
+        assert np.array_equal(bits(got), bits(ref.layer_step(W, b, y))), (m, n)
+        got = sk.layer_step(sk.Matrix(dev_csr(sk, W)), b, sk.DenseMatrix.from_numpy(y),
+                            sk.ForwardOptions(clip=0.75)).numpy()
+        assert np.array_equal(bits(got), bits(port.layer_dense(W, b, y, 0.75))), (m, n)
+
+
+def test_special_values_follow_reference_select(sk, ref):
+    # NaN propagates, -0.0 survives the ReLU select, inf saturates (F4)
+    m, n = 4, 6
+    W = hcsr(4, 4, [0, 1, 2, 3, 4], [0, 1, 2, 3], [1.0, 1.0, 1.0, 1.0])
+    y = np.array([[np.nan, 1, -1, 0, np.inf, -np.inf]] * 4, np.float32)
+    y[1] = -0.0
+    b = np.zeros(4, np.float32)
+    got = sk.layer_step(sk.Matrix(dev_csr(sk, W)), b, sk.DenseMatrix.from_numpy(y)).numpy()
+    want = ref.layer_step(W, b, y)
+    assert same_bits_nan(got, want)
+    assert np.isnan(got[0, 0]) and bits(got)[1, 0] == bits(np.float32(-0.0))
+
+
+def test_dimension_errors(sk):
+    model = sk.DnnModel([sk.csr_from_triples(3, 3, [(0, 0, 1.0)])], [[0.0] * 3])
+    with pytest.raises(sk.DimensionError):
+        sk.relu_forward(model, sk.DenseMatrix(4, 2, 0.0))
+    with pytest.raises(sk.DimensionError):
+        sk.layer_step(sk.Matrix(sk.DenseMatrix.identity(3)), [0.0] * 3, sk.DenseMatrix(2, 2, 1.0))
+    with pytest.raises(sk.DimensionError):
+        sk.layer_step(sk.Matrix(sk.DenseMatrix.identity(3)), [0.0] * 2, sk.DenseMatrix(3, 2, 1.0))
+    with pytest.raises(sk.InvalidArgument):
+        sk.DnnModel([], [])
+    with pytest.raises(sk.DimensionError):
+        sk.DnnModel([sk.csr_from_triples(2, 3, [])], [[0.0, 0.0]])
+    with pytest.raises(sk.DimensionError):
+        sk.mxm(sk.DenseMatrix(2, 3), sk.DenseMatrix(2, 2), sk.arithmetic_semiring())
+    with pytest.raises(sk.Error):
+        sk.mxm(sk.Matrix(sk.DenseMatrix(2, 2)), sk.Matrix(sk.csr_from_triples(2, 2, [])),
+               sk.arithmetic_semiring())
+
+
+# ---- semiring kernels against the reference -----------------------------------------
+
+SEMIRINGS = ["arithmetic", "max_plus", "min_max", "gf2"]
+
+
+def sample(kind, rng, shape):
+    if kind == "arithmetic":
+        v = rng.uniform(-2, 2, shape).astype(np.float32)
+        v[v == 0] = 1
+    elif kind == "max_plus":
+        v = ((rng.integers(0, 1024, shape) - 512) / 64.0).astype(np.float32)
+    elif kind == "min_max":
+        v = rng.uniform(0, 10, shape).astype(np.float32)
+    else:
+        v = np.ones(shape, np.float32)
+    return v
+
+
+def rand_csr(rng, rows, cols, density, kind):
+    mask = rng.random((rows, cols)) < density
+    vals = sample(kind, rng, (rows, cols))
+    rp = np.concatenate([[0], np.cumsum(mask.sum(1))]).astype(np.uint32)
+    ci = np.nonzero(mask)[1].astype(np.uint32)
+    return hcsr(rows, cols, rp, ci, vals[mask])
+
+
+def test_mxm_all_semirings_match_reference(sk, ref):
+    rng = np.random.default_rng(13)
+    for kind in SEMIRINGS:
+        s = getattr(sk, {"arithmetic": "arithmetic_semiring", "max_plus": "max_plus_semiring",
+                         "min_max": "min_max_semiring", "gf2": "gf2_semiring"}[kind])()
+        for trial in range(8):
+            m, l, n = (int(x) for x in rng.integers(1, 40, 3))
+            a = rand_csr(rng, m, l, 0.2 + 0.6 * rng.random(), kind)
+            b = rand_csr(rng, l, n, 0.2 + 0.6 * rng.random(), kind)
+            bd = ref.to_dense(b, s.zero)
+            ad = ref.to_dense(a, s.zero)
+            got = sk.mxm(dev_csr(sk, a), sk.DenseMatrix.from_numpy(bd), s).numpy()
+            assert np.array_equal(bits(got), bits(ref.mxm_csr_dense(a, bd, kind))), (kind, trial)
+            got = sk.mxm(sk.DenseMatrix.from_numpy(ad), sk.DenseMatrix.from_numpy(bd), s).numpy()
+            assert np.array_equal(bits(got), bits(ref.mxm_dense_dense(ad, bd, kind))), (kind, trial)
+            got = sk.mxm(dev_csr(sk, a), dev_csr(sk, b), s)
+            assert_csr_bitwise(got, ref.mxm_csr_csr(a, b, kind))
+
+
+def test_ewise_all_semirings_match_reference(sk, ref):
+    rng = np.random.default_rng(31)
+    for kind in SEMIRINGS:
+        s = getattr(sk, {"arithmetic": "arithmetic_semiring", "max_plus": "max_plus_semiring",
+                         "min_max": "min_max_semiring", "gf2": "gf2_semiring"}[kind])()
+        for trial in range(6):
+            rows, cols = (int(x) for x in rng.integers(1, 10, 2))
+            a = rand_csr(rng, rows, cols, 0.4, kind)
+            b = rand_csr(rng, rows, cols, 0.4, kind)
+            da, db = ref.to_dense(a, s.zero), ref.to_dense(b, s.zero)
+            for mul in (0, 1):
+                fn = sk.ewise_mul if mul else sk.ewise_add
+                got = fn(sk.DenseMatrix.from_numpy(da), sk.DenseMatrix.from_numpy(db), s).numpy()
+                assert np.array_equal(bits(got), bits(ref.ewise_dense(mul, da, db, kind)))
+                got = fn(sk.Matrix(dev_csr(sk, a)), sk.Matrix(dev_csr(sk, b)), s)
+                assert got.is_sparse()
+                assert_csr_bitwise(got.csr(), ref.ewise_csr(mul, a, b, kind))
+                got = fn(sk.Matrix(dev_csr(sk, a)), sk.Matrix(sk.DenseMatrix.from_numpy(db)), s)
+                assert not got.is_sparse()
+                want = ref.ewise_dense(mul, da, db, kind)
+                assert np.array_equal(bits(got.dense().numpy()), bits(want))
+
+
+def test_gf2_domain_error_surfaces_from_kernel(sk):
+    a = sk.csr_from_triples(1, 1, [(0, 0, 2.0)])
+    b = sk.DenseMatrix(1, 1, 1.0)
+    with pytest.raises(sk.DomainError):
+        sk.mxm(a, b, sk.gf2_semiring())
+    with pytest.raises(sk.DomainError):
+        sk.mxm(a, b, sk.gf2_semiring(), 4)
+    # the context is usable afterwards
+    assert sk.mxm(sk.csr_from_triples(1, 1, [(0, 0, 1.0)]), b, sk.gf2_semiring()).numpy()[0, 0] == 1
+
+
+def test_conversions_and_counts(sk, ref):
+    rng = np.random.default_rng(5)
+    d = rng.uniform(-1, 1, (37, 91)).astype(np.float32)
+    d[rng.random(d.shape) < 0.7] = 0.0
+    dd = sk.DenseMatrix.from_numpy(d)
+    assert_csr_bitwise(sk.from_dense(dd), ref.from_dense(d))
+    assert sk.nnz(dd) == int((d != 0).sum())
+    back = sk.to_dense(sk.from_dense(dd), 0.0).numpy()
+    assert np.array_equal(bits(back), bits(d))
+    e = sk.to_dense(sk.csr_from_triples(3, 3, []), float("-inf")).numpy()
+    assert (e == -np.inf).all()
+
+
+# ---- the sparse-activation path (K3) ---------------------------------------------------------
+
+def test_cfg3_small_sparse_forward_bitwise_vs_golden(sk):
+    g = np.load(os.path.join(GOLDEN, "cfg3_small.npz"))
+    m, n, L, kY, seed = (int(g[x]) for x in ("m", "n", "L", "kY", "seed"))
+    Ws = [sk.gen_layer_fixed(m, 32, sk.layer_seed(seed, k), 1.0 / 16) for k in range(L)]
+    model = sk.DnnModel(Ws, [np.full(m, -0.3, np.float32)] * L)
+    Y0 = sk.gen_input_binary(m, n, kY, seed)
+    out, trace = sk.relu_forward_sparse(model, Y0, sk.ForwardOptions(clip=32.0))
+    assert list(trace) == list(g["trace"])
+    want = hcsr(m, n, g["yL_rp"], g["yL_ci"], g["yL_v"])
+    assert_csr_bitwise(out, want)
+    assert np.array_equal(sk.categories(out), np.unique(want.col_idx))
+
+
+@pytest.mark.parametrize("m,n,kY,kW,value,bias,clip,L", [
+    (16384, 2500, 246, 32, 1.0 / 16, -0.3, 32.0, 2),      # cfg3 construction, several windows
+    (65536, 700, 262, 32, 1.0 / 16, -0.35, 32.0, 2),      # cfg4 construction
+    (4096, 3000, 400, 32, 1.0 / 16, -0.05, 32.0, 3),      # live network (slow decay)
+    (2048, 600, 1200, 24, float("nan"), -0.02, 0.0, 3),   # random weights, dense-ish Y: conflicts
+    (1024, 257, 100, 16, float("nan"), 0.05, 0.0, 2),     # positive bias: rows densify
+])
+def test_sparse_forward_bitwise_vs_oracle(sk, port, m, n, kY, kW, value, bias, clip, L):
+    seed = 17
+    hW = [port.gen_layer_fixed(m, kW, port.layer_seed(seed, k), value) for k in range(L)]
+    b = np.full(m, bias, np.float32)
+    hY = port.gen_input_binary(m, n, kY, seed)
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], [b] * L)
+    out, trace = sk.relu_forward_sparse(model, dev_csr(sk, hY), sk.ForwardOptions(clip=clip))
+    y = hY
+    want_trace = [y.nnz]
+    for k in range(L):
+        y = port.layer_sparse(hW[k], b, y, clip)
+        want_trace.append(y.nnz)
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, y)
+
+
+def test_sparse_forward_empty_and_tiny_inputs(sk, port):
+    m = 512
+    W = sk.gen_layer_fixed(m, 8, 3, 0.5)
+    model = sk.DnnModel([W, W], [np.full(m, -0.1, np.float32)] * 2)
+    empty = sk.CsrMatrix(m, 10, [0] * (m + 1), [], [])
+    out, trace = sk.relu_forward_sparse(model, empty)
+    assert out.nnz() == 0 and list(trace) == [0, 0, 0]
+    one = sk.csr_from_triples(m, 1, [(5, 0, 3.0)])
+    out, _ = sk.relu_forward_sparse(model, one)
+    hW = host_csr(W)
+    y = host_csr(one)
+    for _ in range(2):
+        y = port.layer_sparse(hW, np.full(m, -0.1, np.float32), y, 0.0)
+    assert_csr_bitwise(out, y)
+
+
+def test_sparse_route_equals_dense_route(sk):
+    # the same network through K1 (dense Y) and K3 (sparse Y) agrees bitwise
+    m, n = 2048, 300
+    Ws = [sk.gen_layer_fixed(m, 32, sk.layer_seed(5, k)) for k in range(3)]
+    model = sk.DnnModel(Ws, [np.full(m, -0.05, np.float32)] * 3)
+    y0 = sk.gen_input_dense(m, n, 5)
+    dense = sk.relu_forward(model, y0).numpy()
+    sparse, _ = sk.relu_forward_sparse(model, sk.from_dense(y0))
+    assert np.array_equal(bits(sk.to_dense(sparse).numpy()), bits(dense))
