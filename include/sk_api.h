@@ -88,6 +88,9 @@ sk_status sk_ctx_synchronize(sk_ctx* ctx);
  * their durations in ms (synchronising) and resets the list. */
 sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable);
 sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count);
+/* With timing enabled, the sparse engine writes %globaltimer (ns) at the start
+ * (entry 0) and at the end of every layer (entry k+1) of the last forward. */
+sk_status sk_ctx_layer_stamps(sk_ctx* ctx, long long* ns, size_t n);
 /* Page-lock / unlock a caller host buffer for async copies. */
 sk_status sk_host_register(void* p, size_t bytes);
 sk_status sk_host_unregister(void* p);

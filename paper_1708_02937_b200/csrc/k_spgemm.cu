@@ -5,42 +5,51 @@
 //
 // Layout.  B carries a "window table" wp[k*nW + w] = offset of the first entry
 // of row k whose column (sample) is >= w*S, for S = 2^sh samples per window;
-// wp[l*nW] = nnz.  A window of row k is then the contiguous slice
-// [wp[k*nW+w], wp[k*nW+w+1]).  The output of one layer is produced directly in
-// this layout (its window table is the scan of per-(row,window) counts), so
-// layers chain with no re-indexing.  Row pointers are wp[k*nW].
+// wp[l*nW] = nnz.  A window of row k is the contiguous slice
+// [wp[k*nW+w], wp[k*nW+w+1]).  Each layer's output is produced directly in this
+// layout (its window table is the scan of per-(row,window) counts), so layers
+// chain with no re-indexing.  Row pointers are wp[k*nW].
 //
-// Work item = (output row i, window w), one warp.  The warp owns a dense
-// S-float accumulator in shared memory (initialised to a sentinel bit pattern
-// that no FADD can produce, so "touched" is tracked without extra state) and
-// per-128-sample dirty bytes.  The in-edges of row i are taken 32 at a time in
-// ascending k; their window slices are flattened (warp scan + shuffle binary
-// search) so all 32 lanes stay busy.  Within one step two lanes can hit the
-// same sample only if they come from different in-edges; __match_any_sync
-// detects that and the step is then applied lane by lane in lane order, i.e.
-// ascending k.  Hence every output is a left fold in ascending k, exactly the
-// reference's order -- bitwise, with no atomics on values.
+// Per output row, one warp walks the windows.  It owns an S-float accumulator
+// in shared memory initialised to a sentinel bit pattern no FADD produces, a
+// touched-sample list and a survivor bitmap.  The in-edges of the row (ascending
+// k, 32 per chunk) have their window slices flattened by a warp scan and a
+// shuffle binary search, so every lane does one product per step.  Two lanes of
+// a step can hit the same sample only if they come from different in-edges:
+// __match_any_sync groups them and the group applies its updates in rounds by
+// rank, i.e. in lane order = ascending k.  Every output is therefore a left fold
+// in ascending k, the reference's order: bitwise equal, no value atomics.
 //
-// Epilogue (layer mode): z = acc + b_i; ReLU select; optional clip; keep z!=0.
-// Untouched positions see z = epilogue(0 + b_i); a row whose value is nonzero
-// there (b_i > 0 or NaN) is emitted densely, as the dense reference would.
-// Generic mode keeps every touched position (the reference never prunes mxm
-// results, matrix.cpp:449-451).
+// Epilogue (layer mode): z = acc + b_i; ReLU select; optional clip; keep z != 0.
+// Sparse windows (touched <= S/4) run the epilogue over the touched list only,
+// mark survivors in a bitmap and emit them in sample order from it; denser
+// windows (or rows with epilogue(0 + b_i) != 0, which come out dense exactly as
+// the dense reference) scan the whole window.  Generic mode keeps every touched
+// position (the reference never prunes mxm results, matrix.cpp:449-451).
 //
-// Output placement: each item bump-allocates its span in a scratch buffer
-// (one atomic per item with output), records (count, offset); a scan of the
-// counts gives the output window table and a gather writes the final CSR
-// order.  Capacity overflow is flagged on device and handled by the host.
+// Placement: each (row, window) item bump-allocates its span in a scratch
+// buffer and records (count, offset); a scan of the counts is the output window
+// table and a gather writes final CSR order.
+//
+// The forward pass runs ALL layers in one persistent cooperative kernel
+// (k_sparse_engine): phase A (rows) / grid sync / phase B (two-level scan) /
+// grid sync / phase C (gather) / grid sync per layer.  A layer whose input has
+// no entries and whose biases are all <= 0 produces no entries (untouched
+// positions give ReLU(0 + b) = 0); every block sees the same count, so such a
+// layer costs no memory traffic and no grid sync.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
 
 #include "sk_common.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace sk {
 
 constexpr uint32_t kSent = 0xFFFFFFFFu;  // never produced by FADD (canonical NaN is 0x7fffffff)
-constexpr int kWarpsPerBlock = 8;
+constexpr int kWarps = 8;                // warps per block
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
@@ -51,14 +60,42 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
   return v;
 }
 
-struct WinArgs {
+__host__ __device__ constexpr uint32_t list_cap(uint32_t S) { return S / 4; }
+__host__ __device__ constexpr size_t warp_smem_bytes(uint32_t S) {
+  // rounded to 16 B: every warp's accumulator is read/written as uint4
+  return (size_t(S) * 4 + size_t(list_cap(S)) * 2 + size_t(S / 32) * 4 + 15) & ~size_t(15);
+}
+
+struct WarpSmem {
+  uint32_t* acc;   // S
+  uint32_t* surv;  // S/32
+  uint16_t* list;  // S/4
+};
+
+__device__ __forceinline__ WarpSmem warp_smem(uint32_t* base, int wid, uint32_t S) {
+  uint8_t* p = reinterpret_cast<uint8_t*>(base) + size_t(wid) * warp_smem_bytes(S);
+  WarpSmem w;
+  w.acc = reinterpret_cast<uint32_t*>(p);
+  w.surv = reinterpret_cast<uint32_t*>(p + size_t(S) * 4);
+  w.list = reinterpret_cast<uint16_t*>(p + size_t(S) * 4 + size_t(S / 32) * 4);
+  return w;
+}
+
+__device__ __forceinline__ void warp_smem_init(const WarpSmem& ws, uint32_t S, int lane) {
+  for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = kSent;
+  for (uint32_t t = lane; t < S / 32; t += 32) ws.surv[t] = 0;
+  __syncwarp();
+}
+
+struct RowArgs {
   const uint32_t* arp;
   const uint32_t* aci;
   const float* av;
   const uint32_t* bci;
   const float* bv;
-  const uint32_t* wp;  // B window table, l*nW+1
-  uint32_t m, l, n, nW;
+  const uint32_t* wp;  // B window table
+  bool b_empty;        // B has no entries (table may be absent)
+  uint32_t n, nW;
   int sh;
   const float* bias;
   float clip;
@@ -70,121 +107,180 @@ struct WinArgs {
   unsigned long long cap;
   int* overflow;
   int* err;
-  int skip_if_empty;  // layer mode with all biases <= 0: empty input -> empty output
 };
 
-template <typename Ops, bool kLayer>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_spgemm_win(WinArgs p) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t S = 1u << p.sh;
-  uint32_t* acc = sm + size_t(wid) * S;
-  uint8_t* dirty = reinterpret_cast<uint8_t*>(sm + size_t(kWarpsPerBlock) * S) + wid * (S >> 7);
-  const uint64_t items = uint64_t(p.m) * p.nW;
-  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+__device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
-  if (kLayer && p.skip_if_empty && p.wp[size_t(p.l) * p.nW] == 0) {
-    for (uint64_t it = gw * 32 + lane; it < items; it += nwarps * 32) p.item_cnt[it] = 0;
-    return;
+// Reserve `tot` scratch entries for item `it`; returns the offset.
+__device__ __forceinline__ unsigned long long reserve(const RowArgs& p, uint64_t it, uint32_t tot,
+                                                      int lane, bool& can_write) {
+  unsigned long long off = 0;
+  if (lane == 0) {
+    if (tot) {
+      off = atomicAdd(p.bump, (unsigned long long)tot);
+      if (off + tot > p.cap) atomicExch(p.overflow, 1);
+    }
+    p.item_cnt[it] = tot;
+    p.item_off[it] = off;
   }
-  for (uint32_t t = lane; t < S; t += 32) acc[t] = kSent;
-  for (uint32_t t = lane; t < (S >> 7); t += 32) dirty[t] = 0;
-  __syncwarp();
+  off = __shfl_sync(0xffffffffu, off, 0);
+  can_write = tot && (off + tot <= p.cap);
+  return off;
+}
 
-  for (uint64_t it = gw; it < items; it += nwarps) {
-    const uint32_t i = uint32_t(it / p.nW), w = uint32_t(it % p.nW);
+template <typename Ops, bool kLayer>
+__device__ void process_row(const RowArgs& p, uint32_t i, const WarpSmem& ws, int lane) {
+  const uint32_t S = 1u << p.sh;
+  const uint32_t cap = list_cap(S);
+  const uint32_t eb = p.arp[i], ee = p.arp[i + 1];
+  float b = 0.0f, zu = 0.0f;
+  bool dense_row = false;
+  if (kLayer) {
+    b = p.bias[i];
+    zu = layer_epilogue(0.0f, b, p.clip);
+    dense_row = zu != 0.0f;
+  }
+  const bool one_chunk = (ee - eb) <= 32;
+  uint32_t k1 = 0;
+  float a1 = 0.0f;
+  const bool v1 = one_chunk && uint32_t(lane) < ee - eb;
+  if (v1) {
+    k1 = p.aci[eb + lane];
+    a1 = p.av[eb + lane];
+  }
+  for (uint32_t w = 0; w < p.nW; ++w) {
+    const uint64_t it = uint64_t(i) * p.nW + w;
     const uint32_t wbase = w << p.sh;
     const uint32_t wlen = min(S, p.n - wbase);
-    const uint32_t eb = p.arp[i], ee = p.arp[i + 1];
+    uint32_t T = 0;
     bool any = false;
-    for (uint32_t e0 = eb; e0 < ee; e0 += 32) {
-      const uint32_t e = e0 + lane;
-      const bool valid = e < ee;
-      uint32_t beg = 0, cnt = 0;
-      float a = 0.0f;
-      if (valid) {
-        const uint32_t k = p.aci[e];
-        a = p.av[e];
-        const uint32_t* wk = p.wp + size_t(k) * p.nW + w;
-        beg = wk[0];
-        cnt = wk[1] - beg;
-      }
-      const uint32_t incl = warp_incl_scan(cnt, lane);
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      if (total == 0) continue;
-      any = true;
-      const uint32_t excl = incl - cnt;
-      for (uint32_t base = 0; base < total; base += 32) {
-        const uint32_t idx = base + lane;
-        const bool act = idx < total;
-        int L = 0;
+    if (!p.b_empty) {
+      for (uint32_t e0 = eb; e0 < ee; e0 += 32) {
+        uint32_t k = k1;
+        float a = a1;
+        bool valid = v1;
+        if (!one_chunk) {
+          valid = e0 + lane < ee;
+          k = valid ? p.aci[e0 + lane] : 0;
+          a = valid ? p.av[e0 + lane] : 0.0f;
+        }
+        uint32_t beg = 0, cnt = 0;
+        if (valid) {
+          const uint32_t* wk = p.wp + size_t(k) * p.nW + w;
+          beg = wk[0];
+          cnt = wk[1] - beg;
+        }
+        const uint32_t incl = warp_incl_scan(cnt, lane);
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) continue;
+        any = true;
+        const uint32_t excl = incl - cnt;
+        for (uint32_t base = 0; base < total; base += 32) {
+          const uint32_t idx = base + lane;
+          const bool act = idx < total;
+          int L = 0;
 #pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
-          const uint32_t v = __shfl_sync(0xffffffffu, incl, L + s - 1);
-          if (v <= idx) L += s;
-        }
-        const uint32_t begL = __shfl_sync(0xffffffffu, beg, L);
-        const uint32_t exclL = __shfl_sync(0xffffffffu, excl, L);
-        const float aL = __shfl_sync(0xffffffffu, a, L);
-        uint32_t s_loc = 0;
-        float prod = 0.0f;
-        if (act) {
-          const uint32_t q = begL + (idx - exclL);
-          s_loc = p.bci[q] - wbase;
-          prod = Ops::mul(aL, p.bv[q], p.err);
-        }
-        const uint32_t key = act ? s_loc : (0x80000000u | uint32_t(lane));
-        const uint32_t mm = __match_any_sync(0xffffffffu, key);
-        const bool conflict = __any_sync(0xffffffffu, act && __popc(mm) > 1);
-        if (!conflict) {
-          if (act) {
-            const uint32_t x = acc[s_loc];
-            const float xf = (x == kSent) ? Ops::zero() : __uint_as_float(x);
-            acc[s_loc] = __float_as_uint(Ops::add(xf, prod, p.err));
-            dirty[s_loc >> 7] = 1;
+          for (int s = 16; s >= 1; s >>= 1) {
+            const uint32_t v = __shfl_sync(0xffffffffu, incl, L + s - 1);
+            if (v <= idx) L += s;
           }
-        } else {
-          // Serialise in lane order (= ascending k within this step).
-          for (int b = 0; b < 32; ++b) {
-            const uint32_t sb = __shfl_sync(0xffffffffu, s_loc, b);
-            const float pb = __shfl_sync(0xffffffffu, prod, b);
-            const bool ab = __shfl_sync(0xffffffffu, act ? 1 : 0, b) != 0;
-            if (lane == 0 && ab) {
-              const uint32_t x = acc[sb];
-              const float xf = (x == kSent) ? Ops::zero() : __uint_as_float(x);
-              acc[sb] = __float_as_uint(Ops::add(xf, pb, p.err));
-              dirty[sb >> 7] = 1;
+          const uint32_t begL = __shfl_sync(0xffffffffu, beg, L);
+          const uint32_t exclL = __shfl_sync(0xffffffffu, excl, L);
+          const float aL = __shfl_sync(0xffffffffu, a, L);
+          uint32_t s_loc = 0;
+          float prod = 0.0f;
+          if (act) {
+            const uint32_t q = begL + (idx - exclL);
+            s_loc = p.bci[q] - wbase;
+            prod = Ops::mul(aL, p.bv[q], p.err);
+          }
+          const uint32_t key = act ? s_loc : (0x80000000u | uint32_t(lane));
+          const uint32_t mm = __match_any_sync(0xffffffffu, key);
+          const uint32_t rank = __popc(mm & lanemask_lt(lane));
+          const uint32_t rounds = __reduce_max_sync(0xffffffffu, act ? __popc(mm) : 1u);
+          for (uint32_t r = 0; r < rounds; ++r) {
+            bool first = false;
+            if (act && rank == r) {
+              const uint32_t x = ws.acc[s_loc];
+              first = x == kSent;
+              const float xf = first ? Ops::zero() : __uint_as_float(x);
+              uint32_t nx = __float_as_uint(Ops::add(xf, prod, p.err));
+              if (Ops::kind != SK_ARITHMETIC && nx == kSent) nx = 0x7fffffffu;
+              ws.acc[s_loc] = nx;
             }
+            const uint32_t fm = __ballot_sync(0xffffffffu, first);
+            if (first) {
+              const uint32_t pos = T + __popc(fm & lanemask_lt(lane));
+              if (pos < cap) ws.list[pos] = uint16_t(s_loc);
+            }
+            T += __popc(fm);
             __syncwarp();
           }
         }
-        __syncwarp();
       }
     }
 
-    // ---- epilogue --------------------------------------------------------------
-    float b = 0.0f, zu = 0.0f;
-    bool dense_row = false;
-    if (kLayer) {
-      b = p.bias[i];
-      zu = layer_epilogue(0.0f, b, p.clip);
-      dense_row = zu != 0.0f;
-    }
     if (!any && !dense_row) {
       if (lane == 0) p.item_cnt[it] = 0;
       continue;
     }
+
+    if (!dense_row && T <= cap) {
+      // ---- sparse epilogue over the touched list -----------------------------------
+      for (uint32_t t = lane; t < T; t += 32) {
+        const uint32_t s = ws.list[t];
+        const uint32_t x = ws.acc[s];
+        float z;
+        bool keep;
+        if (kLayer) {
+          z = layer_epilogue(__uint_as_float(x), b, p.clip);
+          keep = z != 0.0f;
+        } else {
+          z = __uint_as_float(x);
+          keep = true;
+        }
+        ws.acc[s] = keep ? __float_as_uint(z) : kSent;
+        if (keep) atomicOr(&ws.surv[s >> 5], 1u << (s & 31));
+      }
+      __syncwarp();
+      const uint32_t nwords = (wlen + 31) >> 5;
+      const uint32_t per = (nwords + 31) >> 5;
+      const uint32_t w0 = min(nwords, lane * per), w1 = min(nwords, w0 + per);
+      uint32_t mine = 0;
+      for (uint32_t q = w0; q < w1; ++q) mine += __popc(ws.surv[q]);
+      const uint32_t incl = warp_incl_scan(mine, lane);
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      bool can_write;
+      const unsigned long long off = reserve(p, it, tot, lane, can_write);
+      unsigned long long pos = off + (incl - mine);
+      for (uint32_t q = w0; q < w1; ++q) {
+        uint32_t bitsw = ws.surv[q];
+        ws.surv[q] = 0;
+        while (bitsw) {
+          const uint32_t bt = __ffs(bitsw) - 1;
+          bitsw &= bitsw - 1;
+          const uint32_t s = q * 32 + bt;
+          if (can_write) {
+            p.sc_c[pos] = wbase + s;
+            p.sc_v[pos] = __uint_as_float(ws.acc[s]);
+          }
+          ws.acc[s] = kSent;
+          ++pos;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+
+    // ---- dense epilogue: two sweeps over the window ----------------------------------
     const uint32_t nch = (wlen + 127) >> 7;
     uint32_t mine = 0;
     for (uint32_t c = 0; c < nch; ++c) {
-      if (!dirty[c] && !dense_row) continue;
       const uint32_t s0 = c * 128 + lane * 4;
-      const uint4 x4 = *reinterpret_cast<const uint4*>(acc + s0);
+      const uint4 x4 = *reinterpret_cast<const uint4*>(ws.acc + s0);
       const uint32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const uint32_t s = s0 + t;
         const bool touched = xs[t] != kSent;
         bool keep;
         if (kLayer) {
@@ -193,35 +289,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_spgemm_win(WinArgs p) {
         } else {
           keep = touched;
         }
-        mine += (s < wlen && keep) ? 1u : 0u;
+        mine += (s0 + t < wlen && keep) ? 1u : 0u;
       }
     }
     uint32_t tot = mine;
 #pragma unroll
     for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    unsigned long long off = 0;
-    if (lane == 0) {
-      if (tot) {
-        off = atomicAdd(p.bump, (unsigned long long)tot);
-        if (off + tot > p.cap) atomicExch(p.overflow, 1);
-      }
-      p.item_cnt[it] = tot;
-      p.item_off[it] = off;
-    }
-    off = __shfl_sync(0xffffffffu, off, 0);
-    const bool can_write = tot && (off + tot <= p.cap);
-    unsigned long long pos = off;
+    bool can_write;
+    unsigned long long pos = reserve(p, it, tot, lane, can_write);
     for (uint32_t c = 0; c < nch; ++c) {
-      if (!dirty[c] && !dense_row) continue;
       const uint32_t s0 = c * 128 + lane * 4;
-      uint4* slot = reinterpret_cast<uint4*>(acc + s0);
+      uint4* slot = reinterpret_cast<uint4*>(ws.acc + s0);
       const uint4 x4 = *slot;
       const uint32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
       float zs[4];
       uint32_t keepm = 0;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const uint32_t s = s0 + t;
         const bool touched = xs[t] != kSent;
         bool keep;
         if (kLayer) {
@@ -231,7 +315,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_spgemm_win(WinArgs p) {
           zs[t] = __uint_as_float(xs[t]);
           keep = touched;
         }
-        if (s < wlen && keep) keepm |= 1u << t;
+        if (s0 + t < wlen && keep) keepm |= 1u << t;
       }
       const uint32_t kc = __popc(keepm);
       const uint32_t incl = warp_incl_scan(kc, lane);
@@ -248,14 +332,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_spgemm_win(WinArgs p) {
       }
       pos += ctot;
       *slot = make_uint4(kSent, kSent, kSent, kSent);
-      __syncwarp();
-      if (lane == 0) dirty[c] = 0;
-      __syncwarp();
     }
+    __syncwarp();
   }
 }
 
-// Copy each item's span from scratch to its final CSR position.
+// ---- generic SpGEMM (mxm over any semiring): separate kernels -------------------------
+
+template <typename Ops>
+__global__ void __launch_bounds__(kWarps * 32) k_spgemm_rows(RowArgs p, uint32_t m) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t S = 1u << p.sh;
+  const WarpSmem ws = warp_smem(sm, wid, S);
+  warp_smem_init(ws, S, lane);
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = gw; i < m; i += nw) process_row<Ops, false>(p, i, ws, lane);
+}
+
 __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
                                const unsigned long long* __restrict__ item_off,
                                const uint32_t* __restrict__ wp_out, uint64_t items,
@@ -304,7 +399,6 @@ __global__ void k_rp_from_wp(const uint32_t* wp, uint32_t rows, uint32_t nW, uin
     rp[i] = wp[size_t(i) * nW];
 }
 
-// Upper bound on the products of A.B restricted by rows: sum_i sum_{k in A_i} nnz(B_k).
 __global__ void k_count_products(const uint32_t* arp, const uint32_t* aci, uint32_t m,
                                  const uint32_t* brp, unsigned long long* total) {
   unsigned long long c = 0;
@@ -315,7 +409,188 @@ __global__ void k_count_products(const uint32_t* arp, const uint32_t* aci, uint3
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
 }
 
-// ---- host side -------------------------------------------------------------------
+// ---- the persistent forward engine --------------------------------------------------
+
+struct EngineArgs {
+  const uint32_t* const* w_rp;
+  const uint32_t* const* w_ci;
+  const float* const* w_v;
+  const float* bias;
+  const uint8_t* bias_nonpos;
+  uint32_t m, n, L, nW;
+  int sh;
+  float clip;
+  const uint32_t* y0_ci;
+  const float* y0_v;
+  const uint32_t* y0_wp;
+  unsigned long long nnz0;
+  uint32_t* ci[2];
+  float* v[2];
+  uint32_t* wp[2];
+  uint32_t* item_cnt;
+  unsigned long long* item_off;
+  uint32_t* sc_c;
+  float* sc_v;
+  unsigned long long cap;
+  unsigned long long* bump;        // L counters, zeroed
+  unsigned long long* block_sums;  // gridDim.x
+  unsigned long long* trace;       // L+1
+  int* result;                     // buffer of Y_L: 0/1, -1 no entries, -2 Y_L is Y0
+  int* overflow;
+  int* err;
+  long long* stamps;               // optional %globaltimer per layer end (L+1)
+};
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+  for (int q = 0; q < int(blockDim.x >> 5); ++q) t += red[q];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_sparse_engine(EngineArgs p) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ unsigned long long red[kWarps];
+  __shared__ unsigned long long tile_carry;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t S = 1u << p.sh;
+  const WarpSmem ws = warp_smem(sm, wid, S);
+  warp_smem_init(ws, S, lane);
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t items = uint64_t(p.m) * p.nW;
+
+  unsigned long long total_in = p.nnz0;
+  const uint32_t* in_ci = p.y0_ci;
+  const float* in_v = p.y0_v;
+  const uint32_t* in_wp = p.y0_wp;
+  int cur = 0, last = -2;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.trace[0] = p.nnz0;
+    if (p.stamps) p.stamps[0] = globaltimer();
+  }
+
+  for (uint32_t layer = 0; layer < p.L; ++layer) {
+    if (total_in == 0 && p.bias_nonpos[layer]) {
+      // Empty input and every bias <= 0: the output is empty.  Every block makes
+      // the same decision from the same count, so no synchronisation is needed.
+      last = -1;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.trace[layer + 1] = 0;
+        if (p.stamps) p.stamps[layer + 1] = globaltimer();
+      }
+      continue;
+    }
+    RowArgs ra;
+    ra.arp = p.w_rp[layer];
+    ra.aci = p.w_ci[layer];
+    ra.av = p.w_v[layer];
+    ra.bci = in_ci;
+    ra.bv = in_v;
+    ra.wp = in_wp;
+    ra.b_empty = total_in == 0;
+    ra.n = p.n;
+    ra.nW = p.nW;
+    ra.sh = p.sh;
+    ra.bias = p.bias + size_t(layer) * p.m;
+    ra.clip = p.clip;
+    ra.item_cnt = p.item_cnt;
+    ra.item_off = p.item_off;
+    ra.sc_c = p.sc_c;
+    ra.sc_v = p.sc_v;
+    ra.bump = p.bump + layer;
+    ra.cap = p.cap;
+    ra.overflow = p.overflow;
+    ra.err = p.err;
+
+    // ---- phase A: rows ---------------------------------------------------------------
+    for (uint32_t i = gw; i < p.m; i += nwarps) process_row<OpArith, true>(ra, i, ws, lane);
+    grid.sync();
+
+    // ---- phase B: exclusive scan of item counts -> output window table ---------------
+    uint32_t* out_wp = p.wp[cur];
+    const uint64_t per = (items + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = min(items, uint64_t(blockIdx.x) * per), hi = min(items, lo + per);
+    unsigned long long mine = 0;
+    for (uint64_t t = lo + threadIdx.x; t < hi; t += blockDim.x) mine += p.item_cnt[t];
+    const unsigned long long bsum = block_sum_u64(mine, red);
+    if (threadIdx.x == 0) p.block_sums[blockIdx.x] = bsum;
+    grid.sync();
+    unsigned long long pre = 0, grand = 0;
+    for (uint32_t q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
+      const unsigned long long v = p.block_sums[q];
+      grand += v;
+      if (q < blockIdx.x) pre += v;
+    }
+    pre = block_sum_u64(pre, red);
+    grand = block_sum_u64(grand, red);
+    if (threadIdx.x == 0) tile_carry = pre;
+    __syncthreads();
+    for (uint64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
+      const uint64_t t = t0 + threadIdx.x;
+      const uint32_t c = t < hi ? p.item_cnt[t] : 0u;
+      const uint32_t incl = warp_incl_scan(c, lane);
+      if (lane == 31) red[wid] = incl;
+      __syncthreads();
+      unsigned long long base = tile_carry;
+      for (int q = 0; q < wid; ++q) base += red[q];
+      unsigned long long tile_total = 0;
+      for (int q = 0; q < kWarps; ++q) tile_total += red[q];
+      if (t < hi) out_wp[t] = uint32_t(base + incl - c);
+      __syncthreads();
+      if (threadIdx.x == 0) tile_carry += tile_total;
+      __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      out_wp[items] = uint32_t(grand);
+      if (grand > p.cap) atomicExch(p.overflow, 1);
+    }
+    grid.sync();
+
+    // ---- phase C: gather scratch spans into CSR order -------------------------------
+    if (grand <= p.cap) {
+      for (uint64_t it = gw; it < items; it += nwarps) {
+        const uint32_t c = p.item_cnt[it];
+        if (!c) continue;
+        const unsigned long long src = p.item_off[it];
+        if (src + c > p.cap) continue;
+        const uint32_t dst = out_wp[it];
+        for (uint32_t t = lane; t < c; t += 32) {
+          p.ci[cur][size_t(dst) + t] = p.sc_c[src + t];
+          p.v[cur][size_t(dst) + t] = p.sc_v[src + t];
+        }
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.trace[layer + 1] = grand;
+      if (p.stamps) p.stamps[layer + 1] = globaltimer();
+    }
+    grid.sync();
+
+    total_in = grand;
+    in_ci = p.ci[cur];
+    in_v = p.v[cur];
+    in_wp = out_wp;
+    last = cur;
+    cur ^= 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.result = (total_in == 0 && last != -2) ? -1 : last;
+}
+
+// ---- host side ------------------------------------------------------------------------
 
 struct WinGeom {
   int sh;
@@ -323,8 +598,7 @@ struct WinGeom {
 };
 
 static WinGeom geometry(uint32_t n) {
-  // 2048-sample windows (8 KB per warp) by default; small batches use one window.
-  int sh = 11;
+  int sh = 11;  // 2048-sample windows; small batches use one smaller window
   while (sh > 7 && (1u << (sh - 1)) >= n) --sh;
   WinGeom g;
   g.sh = sh;
@@ -333,28 +607,7 @@ static WinGeom geometry(uint32_t n) {
   return g;
 }
 
-static size_t win_smem(const WinGeom& g) {
-  return size_t(kWarpsPerBlock) * g.S * 4 + size_t(kWarpsPerBlock) * (g.S >> 7);
-}
-
-template <typename Ops, bool kLayer>
-static void launch_win(sk_ctx* ctx, const WinArgs& a, const WinGeom& g) {
-  const size_t smem = win_smem(g);
-  static bool configured = false;  // per template instance
-  if (!configured) {
-    SK_CUDA(cudaFuncSetAttribute(k_spgemm_win<Ops, kLayer>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured = true;
-  }
-  int per_sm = 0;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_win<Ops, kLayer>,
-                                                        kWarpsPerBlock * 32, smem));
-  const uint64_t items = uint64_t(a.m) * a.nW;
-  const uint64_t want = (items + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const unsigned grid =
-      unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(ctx->num_sms) * std::max(per_sm, 1))));
-  SK_LAUNCH((k_spgemm_win<Ops, kLayer>), grid, kWarpsPerBlock * 32, smem, ctx->stream, a);
-}
+static size_t block_smem(const WinGeom& g) { return size_t(kWarps) * warp_smem_bytes(g.S); }
 
 static unsigned grid_warps(sk_ctx* ctx, uint64_t warps) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, uint64_t(ctx->num_sms) * 16)));
@@ -368,56 +621,9 @@ static uint32_t* build_wp(sk_ctx* ctx, const sk_csr* b, const WinGeom& g) {
   return wp;
 }
 
-// One SpGEMM pass.  Returns false on scratch overflow (needed size in *need).
-struct PassBuffers {
-  uint32_t* item_cnt = nullptr;           // items+1
-  unsigned long long* item_off = nullptr; // items
-  uint32_t* sc_c = nullptr;
-  float* sc_v = nullptr;
-  unsigned long long cap = 0;
-};
-
-static void run_pass(sk_ctx* ctx, sk_semiring s, bool layer, const sk_csr* a,
-                     const uint32_t* bci, const float* bv, const uint32_t* wp_b, uint32_t l,
-                     uint32_t n, const WinGeom& g, const float* bias, float clip,
-                     bool skip_if_empty, PassBuffers& pb, uint32_t* wp_out, uint32_t* oc,
-                     float* ov, unsigned long long* bump, int* overflow) {
-  WinArgs p;
-  p.arp = a->rp;
-  p.aci = a->ci;
-  p.av = a->v;
-  p.bci = bci;
-  p.bv = bv;
-  p.wp = wp_b;
-  p.m = a->rows;
-  p.l = l;
-  p.n = n;
-  p.nW = g.nW;
-  p.sh = g.sh;
-  p.bias = bias;
-  p.clip = clip;
-  p.item_cnt = pb.item_cnt;
-  p.item_off = pb.item_off;
-  p.sc_c = pb.sc_c;
-  p.sc_v = pb.sc_v;
-  p.bump = bump;
-  p.cap = pb.cap;
-  p.overflow = overflow;
-  p.err = ctx->d_err;
-  p.skip_if_empty = skip_if_empty ? 1 : 0;
-  const uint64_t items = uint64_t(a->rows) * g.nW;
-  SK_CUDA(cudaMemsetAsync(bump, 0, sizeof(unsigned long long), ctx->stream));
-  timing_mark(ctx);
-  if (layer) {
-    launch_win<OpArith, true>(ctx, p, g);
-  } else {
-    dispatch_semiring(s, [&](auto ops) { launch_win<decltype(ops), false>(ctx, p, g); });
-  }
-  timing_mark(ctx);
-  SK_CUDA(cudaMemsetAsync(pb.item_cnt + items, 0, 4, ctx->stream));
-  exclusive_scan_u32(ctx, pb.item_cnt, wp_out, items + 1);
-  SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, pb.item_cnt,
-            pb.item_off, wp_out, items, pb.sc_c, pb.sc_v, oc, ov, overflow);
+template <typename K>
+static void set_smem_attr(K kernel) {
+  SK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 }
 
 sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semiring s) {
@@ -435,21 +641,62 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
   unsigned long long prods = 0;
   SK_CUDA(cudaMemcpyAsync(&prods, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
-  const unsigned long long cap = std::min<unsigned long long>(prods, uint64_t(m) * n);
-  if (cap > 0xFFFFFFFFull) fail(SK_ERR_INVALID_ARGUMENT, "mxm result nnz exceeds the 32-bit index range");
+  SK_CUDA(cudaMemsetAsync(d, 0, 16, ctx->stream));  // d[0] becomes the bump counter
+  const unsigned long long cap =
+      std::max<unsigned long long>(1, std::min<unsigned long long>(prods, uint64_t(m) * n));
+  if (cap > 0xFFFFFFFFull)
+    fail(SK_ERR_INVALID_ARGUMENT, "mxm result nnz exceeds the 32-bit index range");
   const uint64_t items = uint64_t(m) * g.nW;
-  PassBuffers pb;
-  pb.cap = cap;
-  pb.item_cnt = dalloc<uint32_t>(ctx, items + 1);
-  pb.item_off = reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, items));
-  pb.sc_c = dalloc<uint32_t>(ctx, cap);
-  pb.sc_v = dalloc<float>(ctx, cap);
+  uint32_t* item_cnt = dalloc<uint32_t>(ctx, items + 1);
+  unsigned long long* item_off =
+      reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, items));
+  uint32_t* sc_c = dalloc<uint32_t>(ctx, cap);
+  float* sc_v = dalloc<float>(ctx, cap);
   uint32_t* wp_out = dalloc<uint32_t>(ctx, items + 1);
   uint32_t* oc = dalloc<uint32_t>(ctx, cap);
   float* ov = dalloc<float>(ctx, cap);
   int* overflow = reinterpret_cast<int*>(d + 1);
-  run_pass(ctx, s, false, a, b->ci, b->v, wp_b, b->rows, n, g, nullptr, 0.0f, false, pb, wp_out,
-           oc, ov, d, overflow);
+
+  RowArgs p;
+  p.arp = a->rp;
+  p.aci = a->ci;
+  p.av = a->v;
+  p.bci = b->ci;
+  p.bv = b->v;
+  p.wp = wp_b;
+  p.b_empty = false;
+  p.n = n;
+  p.nW = g.nW;
+  p.sh = g.sh;
+  p.bias = nullptr;
+  p.clip = 0.0f;
+  p.item_cnt = item_cnt;
+  p.item_off = item_off;
+  p.sc_c = sc_c;
+  p.sc_v = sc_v;
+  p.bump = d;
+  p.cap = cap;
+  p.overflow = overflow;
+  p.err = ctx->d_err;
+  const size_t smem = block_smem(g);
+  dispatch_semiring(s, [&](auto ops) {
+    using Ops = decltype(ops);
+    static bool attr = false;
+    if (!attr) {
+      set_smem_attr(k_spgemm_rows<Ops>);
+      attr = true;
+    }
+    int per_sm = 1;
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_rows<Ops>,
+                                                          kWarps * 32, smem));
+    const unsigned grid = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>((m + kWarps - 1) / kWarps, uint64_t(ctx->num_sms) * std::max(1, per_sm))));
+    SK_LAUNCH(k_spgemm_rows<Ops>, grid, kWarps * 32, smem, ctx->stream, p, m);
+  });
+  SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
+  exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
+  SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, item_cnt, item_off,
+            wp_out, items, sc_c, sc_v, oc, ov, overflow);
   uint32_t nnz = 0;
   SK_CUDA(cudaMemcpyAsync(&nnz, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
@@ -462,12 +709,9 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
   o->ci = oc;
   o->v = ov;
   SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, g.nW, o->rp);
-  dfree(ctx, wp_b);
-  dfree(ctx, wp_out);
-  dfree(ctx, pb.item_cnt);
-  dfree(ctx, pb.item_off);
-  dfree(ctx, pb.sc_c);
-  dfree(ctx, pb.sc_v);
+  for (void* q : {(void*)wp_b, (void*)wp_out, (void*)item_cnt, (void*)item_off, (void*)sc_c,
+                  (void*)sc_v})
+    dfree(ctx, q);
   return o;
 }
 
@@ -480,9 +724,26 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   const uint64_t items = uint64_t(m) * g.nW;
   const uint64_t full = uint64_t(m) * n;
 
+  // Device arrays of per-layer weight pointers (cached on the model).
+  auto* mm = const_cast<sk_model*>(md);
+  if (!mm->d_wptr) {
+    std::vector<const void*> h(size_t(3) * L);
+    for (uint32_t k = 0; k < L; ++k) {
+      h[k] = md->w[k]->rp;
+      h[L + k] = md->w[k]->ci;
+      h[2 * L + k] = md->w[k]->v;
+    }
+    mm->d_wptr = dalloc<const void*>(ctx, h.size());
+    mm->d_bias_nonpos = dalloc<uint8_t>(ctx, L);
+    SK_CUDA(cudaMemcpyAsync(mm->d_wptr, h.data(), h.size() * sizeof(void*),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    SK_CUDA(cudaMemcpyAsync(mm->d_bias_nonpos, md->bias_nonpos.data(), L,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    sync(ctx);
+  }
+
   size_t free_b = 0, total_b = 0;
   SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  // three entry buffers (two ping-pong activations + scratch), 8 B per entry
   const unsigned long long mem_cap = (unsigned long long)(free_b * 0.6 / 24.0);
   auto clamp_cap = [&](unsigned long long c) {
     c = std::min<unsigned long long>(c, full);
@@ -492,48 +753,89 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   };
   unsigned long long cap = clamp_cap(std::max<unsigned long long>(4ull * y0->nnz, 1ull << 24));
 
+  static bool attr = false;
+  if (!attr) {
+    set_smem_attr(k_sparse_engine);
+    attr = true;
+  }
+  const size_t smem = block_smem(g);
+  int per_sm = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sparse_engine, kWarps * 32,
+                                                        smem));
+  if (per_sm < 1) fail(SK_ERR_CUDA, "sparse engine does not fit on an SM");
+  const unsigned grid = unsigned(ctx->num_sms * per_sm);
+
   uint32_t* wp0 = build_wp(ctx, y0, g);
-  unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
-  int* overflow = reinterpret_cast<int*>(d + 1);
-  uint32_t* trace_d = dalloc<uint32_t>(ctx, size_t(L) + 1);
-  SK_CUDA(cudaMemcpyAsync(trace_d, wp0 + items, 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  const size_t nsmall = size_t(L) + 1 + L + grid + 4;
+  unsigned long long* small =
+      reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, nsmall));
+  unsigned long long* trace_d = small;
+  unsigned long long* bump = small + L + 1;
+  unsigned long long* block_sums = bump + L;
+  int* flags = reinterpret_cast<int*>(block_sums + grid);  // [0] overflow, [1] result
 
   for (int attempt = 0; attempt < 2; ++attempt) {
-    SK_CUDA(cudaMemsetAsync(overflow, 0, 4, ctx->stream));
-    PassBuffers pb;
-    pb.cap = cap;
-    pb.item_cnt = dalloc<uint32_t>(ctx, items + 1);
-    pb.item_off = reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, items));
-    pb.sc_c = dalloc<uint32_t>(ctx, cap);
-    pb.sc_v = dalloc<float>(ctx, cap);
-    uint32_t* wp_buf[2] = {dalloc<uint32_t>(ctx, items + 1), dalloc<uint32_t>(ctx, items + 1)};
-    uint32_t* c_buf[2] = {dalloc<uint32_t>(ctx, cap), dalloc<uint32_t>(ctx, cap)};
-    float* v_buf[2] = {dalloc<float>(ctx, cap), dalloc<float>(ctx, cap)};
-
-    const uint32_t* in_c = y0->ci;
-    const float* in_v = y0->v;
-    const uint32_t* in_wp = wp0;
-    int cur = 0;
-    for (uint32_t k = 0; k < L; ++k) {
-      run_pass(ctx, SK_ARITHMETIC, true, md->w[k], in_c, in_v, in_wp, m, n, g,
-               md->bias + size_t(k) * m, clip, md->bias_nonpos[k] != 0, pb, wp_buf[cur],
-               c_buf[cur], v_buf[cur], d, overflow);
-      SK_CUDA(cudaMemcpyAsync(trace_d + k + 1, wp_buf[cur] + items, 4, cudaMemcpyDeviceToDevice,
-                              ctx->stream));
-      in_c = c_buf[cur];
-      in_v = v_buf[cur];
-      in_wp = wp_buf[cur];
-      cur ^= 1;
+    SK_CUDA(cudaMemsetAsync(small, 0, nsmall * 8, ctx->stream));
+    EngineArgs p;
+    p.w_rp = reinterpret_cast<const uint32_t* const*>(mm->d_wptr);
+    p.w_ci = reinterpret_cast<const uint32_t* const*>(mm->d_wptr + L);
+    p.w_v = reinterpret_cast<const float* const*>(mm->d_wptr + 2 * L);
+    p.bias = md->bias;
+    p.bias_nonpos = mm->d_bias_nonpos;
+    p.m = m;
+    p.n = n;
+    p.L = L;
+    p.nW = g.nW;
+    p.sh = g.sh;
+    p.clip = clip;
+    p.y0_ci = y0->ci;
+    p.y0_v = y0->v;
+    p.y0_wp = wp0;
+    p.nnz0 = y0->nnz;
+    for (int q = 0; q < 2; ++q) {
+      p.ci[q] = dalloc<uint32_t>(ctx, cap);
+      p.v[q] = dalloc<float>(ctx, cap);
+      p.wp[q] = dalloc<uint32_t>(ctx, items + 1);
     }
-    int ov = 0;
-    std::vector<uint32_t> trace(size_t(L) + 1);
-    SK_CUDA(cudaMemcpyAsync(&ov, overflow, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    SK_CUDA(cudaMemcpyAsync(trace.data(), trace_d, trace.size() * 4, cudaMemcpyDeviceToHost,
+    p.item_cnt = dalloc<uint32_t>(ctx, items + 1);
+    p.item_off = reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, items));
+    p.sc_c = dalloc<uint32_t>(ctx, cap);
+    p.sc_v = dalloc<float>(ctx, cap);
+    p.cap = cap;
+    p.bump = bump;
+    p.block_sums = block_sums;
+    p.trace = trace_d;
+    p.result = flags + 1;
+    p.overflow = flags;
+    p.err = ctx->d_err;
+    p.stamps = ctx->stamps;
+    void* args[] = {&p};
+    timing_mark(ctx);
+    SK_CUDA(cudaLaunchCooperativeKernel((void*)k_sparse_engine, dim3(grid), dim3(kWarps * 32),
+                                        args, smem, ctx->stream));
+    g_launches.fetch_add(1);
+    timing_mark(ctx);
+
+    std::vector<unsigned long long> trace(size_t(L) + 1);
+    int hflags[2] = {0, 0};
+    SK_CUDA(cudaMemcpyAsync(hflags, flags, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    SK_CUDA(cudaMemcpyAsync(trace.data(), trace_d, trace.size() * 8, cudaMemcpyDeviceToHost,
                             ctx->stream));
     sync(ctx);
-    const int last = cur ^ 1;
-    if (!ov) {
-      const uint32_t nnz = trace[L];
+    auto release = [&] {
+      for (int q = 0; q < 2; ++q) {
+        dfree(ctx, p.ci[q]);
+        dfree(ctx, p.v[q]);
+        dfree(ctx, p.wp[q]);
+      }
+      dfree(ctx, p.item_cnt);
+      dfree(ctx, p.item_off);
+      dfree(ctx, p.sc_c);
+      dfree(ctx, p.sc_v);
+    };
+    if (!hflags[0]) {
+      const int res = hflags[1];
+      const unsigned long long nnz = trace[L];
       sk_csr* o = new sk_csr;
       o->ctx = ctx;
       o->rows = m;
@@ -542,45 +844,33 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
       o->rp = dalloc<uint32_t>(ctx, size_t(m) + 1);
       o->ci = dalloc<uint32_t>(ctx, nnz);
       o->v = dalloc<float>(ctx, nnz);
-      SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_buf[last], m, g.nW,
-                o->rp);
-      if (nnz) {
-        SK_CUDA(cudaMemcpyAsync(o->ci, c_buf[last], size_t(nnz) * 4, cudaMemcpyDeviceToDevice,
+      if (res == -1 || nnz == 0) {
+        SK_CUDA(cudaMemsetAsync(o->rp, 0, (size_t(m) + 1) * 4, ctx->stream));
+      } else {
+        const uint32_t* src_wp = res == -2 ? wp0 : p.wp[res];
+        const uint32_t* src_c = res == -2 ? y0->ci : p.ci[res];
+        const float* src_v = res == -2 ? y0->v : p.v[res];
+        SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, src_wp, m, g.nW,
+                  o->rp);
+        SK_CUDA(cudaMemcpyAsync(o->ci, src_c, size_t(nnz) * 4, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
-        SK_CUDA(cudaMemcpyAsync(o->v, v_buf[last], size_t(nnz) * 4, cudaMemcpyDeviceToDevice,
+        SK_CUDA(cudaMemcpyAsync(o->v, src_v, size_t(nnz) * 4, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
       }
       if (nnz_trace)
         for (uint32_t k = 0; k <= L; ++k) nnz_trace[k] = trace[k];
-      for (int q = 0; q < 2; ++q) {
-        dfree(ctx, wp_buf[q]);
-        dfree(ctx, c_buf[q]);
-        dfree(ctx, v_buf[q]);
-      }
-      dfree(ctx, pb.item_cnt);
-      dfree(ctx, pb.item_off);
-      dfree(ctx, pb.sc_c);
-      dfree(ctx, pb.sc_v);
+      release();
       dfree(ctx, wp0);
-      dfree(ctx, trace_d);
+      dfree(ctx, small);
       return o;
     }
-    for (int q = 0; q < 2; ++q) {
-      dfree(ctx, wp_buf[q]);
-      dfree(ctx, c_buf[q]);
-      dfree(ctx, v_buf[q]);
-    }
-    dfree(ctx, pb.item_cnt);
-    dfree(ctx, pb.item_off);
-    dfree(ctx, pb.sc_c);
-    dfree(ctx, pb.sc_v);
-    // Retry once with the largest capacity memory allows.
+    release();
     const unsigned long long bigger = clamp_cap(full);
     if (bigger <= cap) break;
-    cap = bigger;
+    cap = bigger;  // retry once with the largest capacity memory allows
   }
   dfree(ctx, wp0);
-  dfree(ctx, trace_d);
+  dfree(ctx, small);
   fail(SK_ERR_OOM, "sparse forward: activation nnz exceeds the device capacity");
 }
 

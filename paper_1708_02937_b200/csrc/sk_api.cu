@@ -174,6 +174,7 @@ extern "C" sk_status sk_ctx_destroy(sk_ctx* ctx) {
     cudaFree(ctx->d_u64);
     cudaFreeHost(ctx->h_u64);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+    if (ctx->stamps) cudaFree(ctx->stamps);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -193,6 +194,27 @@ extern "C" sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable) {
     require_ctx(ctx);
     ctx->timing = enable != 0;
     ctx->ev_used = 0;
+    if (enable && !ctx->stamps) {
+      ctx->stamps_cap = 1 << 16;
+      SK_CUDA(cudaMalloc(&ctx->stamps, size_t(ctx->stamps_cap) * sizeof(long long)));
+    }
+    if (!enable && ctx->stamps) {
+      sync(ctx);
+      cudaFree(ctx->stamps);
+      ctx->stamps = nullptr;
+      ctx->stamps_cap = 0;
+    }
+  });
+}
+
+extern "C" sk_status sk_ctx_layer_stamps(sk_ctx* ctx, long long* ns, size_t n) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!ctx->stamps) fail(SK_ERR_INVALID_ARGUMENT, "timing is not enabled");
+    if (n > ctx->stamps_cap) n = ctx->stamps_cap;
+    SK_CUDA(cudaMemcpyAsync(ns, ctx->stamps, n * sizeof(long long), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    sync(ctx);
   });
 }
 
@@ -390,6 +412,8 @@ extern "C" sk_status sk_model_free(sk_model* m) {
     if (!m) return;
     for (sk_csr* w : m->w) csr_release(w);
     dfree(m->ctx, m->bias);
+    dfree(m->ctx, m->d_wptr);
+    dfree(m->ctx, m->d_bias_nonpos);
     delete m;
   });
 }

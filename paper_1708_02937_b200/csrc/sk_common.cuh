@@ -100,6 +100,9 @@ struct sk_ctx {
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // 2 per layer
   size_t ev_used = 0;
+  // Optional per-layer %globaltimer stamps written by the sparse engine.
+  long long* stamps = nullptr;
+  uint32_t stamps_cap = 0;
 };
 
 struct sk_dense {
@@ -126,6 +129,8 @@ struct sk_model {
   float* bias = nullptr;        // device, layers*neurons
   std::vector<float> bias_host; // layers*neurons
   std::vector<uint8_t> bias_nonpos;  // per layer: every b <= 0 (no NaN)
+  const void** d_wptr = nullptr;     // device [rp[L], ci[L], v[L]] for the engine
+  uint8_t* d_bias_nonpos = nullptr;
 };
 
 namespace sk {

@@ -161,6 +161,12 @@ class Context:
                                            C.byref(n)))
         return buf[: min(n.value, cap)].copy()
 
+    def layer_stamps_ns(self, n: int) -> np.ndarray:
+        """%globaltimer stamps of the last sparse forward: start + end of each layer."""
+        buf = np.zeros(n, np.int64)
+        _check(self._L.sk_ctx_layer_stamps(self.h, buf.ctypes.data_as(C.POINTER(C.c_longlong)), n))
+        return buf
+
     def set_stream(self, stream_ptr: int | None):
         _check(self._L.sk_ctx_set_stream(self.h, vp(stream_ptr) if stream_ptr else None))
 
