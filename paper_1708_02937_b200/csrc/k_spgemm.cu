@@ -41,6 +41,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "sk_common.cuh"
 
@@ -61,23 +62,35 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 }
 
 __host__ __device__ constexpr uint32_t list_cap(uint32_t S) { return S / 4; }
+constexpr uint32_t kStage = 512;  // staged products per warp (expansion buffer)
+constexpr uint32_t kGroup = 4;    // windows per work item
 __host__ __device__ constexpr size_t warp_smem_bytes(uint32_t S) {
-  // rounded to 16 B: every warp's accumulator is read/written as uint4
-  return (size_t(S) * 4 + size_t(list_cap(S)) * 2 + size_t(S / 32) * 4 + 15) & ~size_t(15);
+  // acc | surv | staged prod | list | staged sample; rounded to 16 B (acc is
+  // read and written as uint4)
+  return (size_t(S) * 4 + size_t(S / 32) * 4 + size_t(kStage) * 4 + size_t(list_cap(S)) * 2 +
+          size_t(kStage) * 2 + 15) & ~size_t(15);
 }
 
 struct WarpSmem {
-  uint32_t* acc;   // S
-  uint32_t* surv;  // S/32
-  uint16_t* list;  // S/4
+  uint32_t* acc;     // S       accumulator bits, kSent = untouched
+  uint32_t* surv;    // S/32    survivor bitmap
+  float* st_p;       // kStage  staged products
+  uint16_t* list;    // S/4     touched samples
+  uint16_t* st_s;    // kStage  staged samples (window-local)
 };
 
 __device__ __forceinline__ WarpSmem warp_smem(uint32_t* base, int wid, uint32_t S) {
   uint8_t* p = reinterpret_cast<uint8_t*>(base) + size_t(wid) * warp_smem_bytes(S);
   WarpSmem w;
   w.acc = reinterpret_cast<uint32_t*>(p);
-  w.surv = reinterpret_cast<uint32_t*>(p + size_t(S) * 4);
-  w.list = reinterpret_cast<uint16_t*>(p + size_t(S) * 4 + size_t(S / 32) * 4);
+  p += size_t(S) * 4;
+  w.surv = reinterpret_cast<uint32_t*>(p);
+  p += size_t(S / 32) * 4;
+  w.st_p = reinterpret_cast<float*>(p);
+  p += size_t(kStage) * 4;
+  w.list = reinterpret_cast<uint16_t*>(p);
+  p += size_t(list_cap(S)) * 2;
+  w.st_s = reinterpret_cast<uint16_t*>(p);
   return w;
 }
 
@@ -95,11 +108,11 @@ struct RowArgs {
   const float* bv;
   const uint32_t* wp;  // B window table
   bool b_empty;        // B has no entries (table may be absent)
-  uint32_t n, nW;
+  uint32_t m, n, nW;
   int sh;
   const float* bias;
   float clip;
-  uint32_t* item_cnt;
+  uint32_t* item_cnt;  // indexed (row, window) row-major: the output window table order
   unsigned long long* item_off;
   uint32_t* sc_c;
   float* sc_v;
@@ -111,7 +124,7 @@ struct RowArgs {
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
-// Reserve `tot` scratch entries for item `it`; returns the offset.
+// Reserve `tot` scratch entries for output item `it`; returns the offset.
 __device__ __forceinline__ unsigned long long reserve(const RowArgs& p, uint64_t it, uint32_t tot,
                                                       int lane, bool& can_write) {
   unsigned long long off = 0;
@@ -128,133 +141,122 @@ __device__ __forceinline__ unsigned long long reserve(const RowArgs& p, uint64_t
   return off;
 }
 
-template <typename Ops, bool kLayer>
-__device__ void process_row(const RowArgs& p, uint32_t i, const WarpSmem& ws, int lane) {
-  const uint32_t S = 1u << p.sh;
-  const uint32_t cap = list_cap(S);
-  const uint32_t eb = p.arp[i], ee = p.arp[i + 1];
-  float b = 0.0f, zu = 0.0f;
-  bool dense_row = false;
-  if (kLayer) {
-    b = p.bias[i];
-    zu = layer_epilogue(0.0f, b, p.clip);
-    dense_row = zu != 0.0f;
-  }
-  const bool one_chunk = (ee - eb) <= 32;
-  uint32_t k1 = 0;
-  float a1 = 0.0f;
-  const bool v1 = one_chunk && uint32_t(lane) < ee - eb;
-  if (v1) {
-    k1 = p.aci[eb + lane];
-    a1 = p.av[eb + lane];
-  }
-  for (uint32_t w = 0; w < p.nW; ++w) {
-    const uint64_t it = uint64_t(i) * p.nW + w;
-    const uint32_t wbase = w << p.sh;
-    const uint32_t wlen = min(S, p.n - wbase);
-    uint32_t T = 0;
-    bool any = false;
-    if (!p.b_empty) {
-      for (uint32_t e0 = eb; e0 < ee; e0 += 32) {
-        uint32_t k = k1;
-        float a = a1;
-        bool valid = v1;
-        if (!one_chunk) {
-          valid = e0 + lane < ee;
-          k = valid ? p.aci[e0 + lane] : 0;
-          a = valid ? p.av[e0 + lane] : 0.0f;
-        }
-        uint32_t beg = 0, cnt = 0;
-        if (valid) {
-          const uint32_t* wk = p.wp + size_t(k) * p.nW + w;
-          beg = wk[0];
-          cnt = wk[1] - beg;
-        }
-        const uint32_t incl = warp_incl_scan(cnt, lane);
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        if (total == 0) continue;
-        any = true;
-        const uint32_t excl = incl - cnt;
-        for (uint32_t base = 0; base < total; base += 32) {
-          const uint32_t idx = base + lane;
-          const bool act = idx < total;
-          int L = 0;
+// Fold one in-edge chunk's window slices into the accumulator, in ascending k.
+// Lane l owns in-edge l of the chunk (weight a, slice [beg, beg+cnt)).  The
+// slices are expanded lane-parallel into the warp's staging buffer in
+// flattened (ascending k, ascending sample) order, then applied 32 at a time;
+// products of one step that hit the same sample are applied in rounds by rank,
+// i.e. lane order = ascending k.
+template <typename Ops>
+__device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws, int lane,
+                                           uint32_t wbase, float a, uint32_t beg, uint32_t cnt,
+                                           uint32_t& T, bool& any) {
+  const uint32_t cap = list_cap(1u << p.sh);
+  const uint32_t incl = warp_incl_scan(cnt, lane);
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  any = true;
+  const uint32_t excl = incl - cnt;
+  for (uint32_t base = 0; base < total; base += kStage) {
+    // ---- expansion: this lane's entries whose flattened index is in the batch
+    const uint32_t lo = max(excl, base), hi = min(excl + cnt, base + kStage);
+    uint32_t idx = lo;
+    for (; idx + 4 <= hi; idx += 4) {
+      const uint32_t q = beg + (idx - excl);
+      uint32_t c[4];
+      float y[4];
 #pragma unroll
-          for (int s = 16; s >= 1; s >>= 1) {
-            const uint32_t v = __shfl_sync(0xffffffffu, incl, L + s - 1);
-            if (v <= idx) L += s;
-          }
-          const uint32_t begL = __shfl_sync(0xffffffffu, beg, L);
-          const uint32_t exclL = __shfl_sync(0xffffffffu, excl, L);
-          const float aL = __shfl_sync(0xffffffffu, a, L);
-          uint32_t s_loc = 0;
-          float prod = 0.0f;
-          if (act) {
-            const uint32_t q = begL + (idx - exclL);
-            s_loc = p.bci[q] - wbase;
-            prod = Ops::mul(aL, p.bv[q], p.err);
-          }
-          const uint32_t key = act ? s_loc : (0x80000000u | uint32_t(lane));
-          const uint32_t mm = __match_any_sync(0xffffffffu, key);
-          const uint32_t rank = __popc(mm & lanemask_lt(lane));
-          const uint32_t rounds = __reduce_max_sync(0xffffffffu, act ? __popc(mm) : 1u);
-          for (uint32_t r = 0; r < rounds; ++r) {
-            bool first = false;
-            if (act && rank == r) {
-              const uint32_t x = ws.acc[s_loc];
-              first = x == kSent;
-              const float xf = first ? Ops::zero() : __uint_as_float(x);
-              uint32_t nx = __float_as_uint(Ops::add(xf, prod, p.err));
-              if (Ops::kind != SK_ARITHMETIC && nx == kSent) nx = 0x7fffffffu;
-              ws.acc[s_loc] = nx;
-            }
-            const uint32_t fm = __ballot_sync(0xffffffffu, first);
-            if (first) {
-              const uint32_t pos = T + __popc(fm & lanemask_lt(lane));
-              if (pos < cap) ws.list[pos] = uint16_t(s_loc);
-            }
-            T += __popc(fm);
-            __syncwarp();
-          }
-        }
+      for (int u = 0; u < 4; ++u) {
+        c[u] = __ldg(p.bci + q + u);
+        y[u] = __ldg(p.bv + q + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ws.st_s[idx + u - base] = uint16_t(c[u] - wbase);
+        ws.st_p[idx + u - base] = Ops::mul(a, y[u], p.err);
       }
     }
-
-    if (!any && !dense_row) {
-      if (lane == 0) p.item_cnt[it] = 0;
-      continue;
+    for (; idx < hi; ++idx) {
+      const uint32_t q = beg + (idx - excl);
+      ws.st_s[idx - base] = uint16_t(__ldg(p.bci + q) - wbase);
+      ws.st_p[idx - base] = Ops::mul(a, __ldg(p.bv + q), p.err);
     }
-
-    if (!dense_row && T <= cap) {
-      // ---- sparse epilogue over the touched list -----------------------------------
-      for (uint32_t t = lane; t < T; t += 32) {
-        const uint32_t s = ws.list[t];
-        const uint32_t x = ws.acc[s];
-        float z;
-        bool keep;
-        if (kLayer) {
-          z = layer_epilogue(__uint_as_float(x), b, p.clip);
-          keep = z != 0.0f;
-        } else {
-          z = __uint_as_float(x);
-          keep = true;
+    __syncwarp();
+    // ---- application, 32 staged products per step
+    const uint32_t nb = min(kStage, total - base);
+    for (uint32_t t = 0; t < nb; t += 32) {
+      const uint32_t j = t + lane;
+      const bool act = j < nb;
+      const uint32_t s_loc = act ? uint32_t(ws.st_s[j]) : 0u;
+      const float prod = act ? ws.st_p[j] : 0.0f;
+      const uint32_t key = act ? s_loc : (0x80000000u | uint32_t(lane));
+      const uint32_t mm = __match_any_sync(0xffffffffu, key);
+      const uint32_t rank = __popc(mm & lanemask_lt(lane));
+      const uint32_t rounds = __reduce_max_sync(0xffffffffu, act ? __popc(mm) : 1u);
+      for (uint32_t r = 0; r < rounds; ++r) {
+        bool first = false;
+        if (act && rank == r) {
+          const uint32_t x = ws.acc[s_loc];
+          first = x == kSent;
+          const float xf = first ? Ops::zero() : __uint_as_float(x);
+          uint32_t nx = __float_as_uint(Ops::add(xf, prod, p.err));
+          if (Ops::kind != SK_ARITHMETIC && nx == kSent) nx = 0x7fffffffu;
+          ws.acc[s_loc] = nx;
         }
-        ws.acc[s] = keep ? __float_as_uint(z) : kSent;
-        if (keep) atomicOr(&ws.surv[s >> 5], 1u << (s & 31));
+        const uint32_t fm = __ballot_sync(0xffffffffu, first);
+        if (first) {
+          const uint32_t pos = T + __popc(fm & lanemask_lt(lane));
+          if (pos < cap) ws.list[pos] = uint16_t(s_loc);
+        }
+        T += __popc(fm);
+        __syncwarp();
       }
-      __syncwarp();
-      const uint32_t nwords = (wlen + 31) >> 5;
-      const uint32_t per = (nwords + 31) >> 5;
-      const uint32_t w0 = min(nwords, lane * per), w1 = min(nwords, w0 + per);
-      uint32_t mine = 0;
-      for (uint32_t q = w0; q < w1; ++q) mine += __popc(ws.surv[q]);
-      const uint32_t incl = warp_incl_scan(mine, lane);
-      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-      bool can_write;
-      const unsigned long long off = reserve(p, it, tot, lane, can_write);
+    }
+  }
+}
+
+// Epilogue of one (row, window): emit the row's window slice of the output.
+template <bool kLayer>
+__device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws, int lane,
+                                            uint64_t it, uint32_t wbase, uint32_t wlen, bool any,
+                                            uint32_t T, float b, float zu, bool dense_row) {
+  const uint32_t cap = list_cap(1u << p.sh);
+  if (!any && !dense_row) {
+    if (lane == 0) p.item_cnt[it] = 0;
+    return;
+  }
+  if (!dense_row && T <= cap) {
+    // sparse epilogue over the touched list; survivors -> bitmap -> ordered emit
+    for (uint32_t t = lane; t < T; t += 32) {
+      const uint32_t s = ws.list[t];
+      const uint32_t x = ws.acc[s];
+      float z;
+      bool keep;
+      if (kLayer) {
+        z = layer_epilogue(__uint_as_float(x), b, p.clip);
+        keep = z != 0.0f;
+      } else {
+        z = __uint_as_float(x);
+        keep = true;
+      }
+      ws.acc[s] = keep ? __float_as_uint(z) : kSent;
+      if (keep) atomicOr(&ws.surv[s >> 5], 1u << (s & 31));
+    }
+    __syncwarp();
+    const uint32_t nwords = (wlen + 31) >> 5;
+    const uint32_t per = (nwords + 31) >> 5;
+    const uint32_t w0 = min(nwords, lane * per), w1 = min(nwords, w0 + per);
+    uint32_t mine = 0;
+    for (uint32_t q = w0; q < w1; ++q) mine += __popc(ws.surv[q]);
+    const uint32_t incl = warp_incl_scan(mine, lane);
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    bool can_write;
+    const unsigned long long off = reserve(p, it, tot, lane, can_write);
+    if (tot) {
       unsigned long long pos = off + (incl - mine);
       for (uint32_t q = w0; q < w1; ++q) {
         uint32_t bitsw = ws.surv[q];
+        if (!bitsw) continue;
         ws.surv[q] = 0;
         while (bitsw) {
           const uint32_t bt = __ffs(bitsw) - 1;
@@ -268,73 +270,147 @@ __device__ void process_row(const RowArgs& p, uint32_t i, const WarpSmem& ws, in
           ++pos;
         }
       }
-      __syncwarp();
-      continue;
-    }
-
-    // ---- dense epilogue: two sweeps over the window ----------------------------------
-    const uint32_t nch = (wlen + 127) >> 7;
-    uint32_t mine = 0;
-    for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t s0 = c * 128 + lane * 4;
-      const uint4 x4 = *reinterpret_cast<const uint4*>(ws.acc + s0);
-      const uint32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const bool touched = xs[t] != kSent;
-        bool keep;
-        if (kLayer) {
-          const float z = touched ? layer_epilogue(__uint_as_float(xs[t]), b, p.clip) : zu;
-          keep = (touched || dense_row) && z != 0.0f;
-        } else {
-          keep = touched;
-        }
-        mine += (s0 + t < wlen && keep) ? 1u : 0u;
-      }
-    }
-    uint32_t tot = mine;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    bool can_write;
-    unsigned long long pos = reserve(p, it, tot, lane, can_write);
-    for (uint32_t c = 0; c < nch; ++c) {
-      const uint32_t s0 = c * 128 + lane * 4;
-      uint4* slot = reinterpret_cast<uint4*>(ws.acc + s0);
-      const uint4 x4 = *slot;
-      const uint32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
-      float zs[4];
-      uint32_t keepm = 0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const bool touched = xs[t] != kSent;
-        bool keep;
-        if (kLayer) {
-          zs[t] = touched ? layer_epilogue(__uint_as_float(xs[t]), b, p.clip) : zu;
-          keep = (touched || dense_row) && zs[t] != 0.0f;
-        } else {
-          zs[t] = __uint_as_float(xs[t]);
-          keep = touched;
-        }
-        if (s0 + t < wlen && keep) keepm |= 1u << t;
-      }
-      const uint32_t kc = __popc(keepm);
-      const uint32_t incl = warp_incl_scan(kc, lane);
-      const uint32_t ctot = __shfl_sync(0xffffffffu, incl, 31);
-      if (can_write) {
-        unsigned long long q = pos + (incl - kc);
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (keepm & (1u << t)) {
-            p.sc_c[q] = wbase + s0 + t;
-            p.sc_v[q] = zs[t];
-            ++q;
-          }
-      }
-      pos += ctot;
-      *slot = make_uint4(kSent, kSent, kSent, kSent);
     }
     __syncwarp();
+    return;
   }
+  // dense epilogue: two sweeps over the window
+  const uint32_t nch = (wlen + 127) >> 7;
+  uint32_t mine = 0;
+  for (uint32_t c = 0; c < nch; ++c) {
+    const uint32_t s0 = c * 128 + lane * 4;
+    const uint4 x4 = *reinterpret_cast<const uint4*>(ws.acc + s0);
+    const uint32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool touched = xs[t] != kSent;
+      bool keep;
+      if (kLayer) {
+        const float z = touched ? layer_epilogue(__uint_as_float(xs[t]), b, p.clip) : zu;
+        keep = (touched || dense_row) && z != 0.0f;
+      } else {
+        keep = touched;
+      }
+      mine += (s0 + t < wlen && keep) ? 1u : 0u;
+    }
+  }
+  uint32_t tot = mine;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  bool can_write;
+  unsigned long long pos = reserve(p, it, tot, lane, can_write);
+  for (uint32_t c = 0; c < nch; ++c) {
+    const uint32_t s0 = c * 128 + lane * 4;
+    uint4* slot = reinterpret_cast<uint4*>(ws.acc + s0);
+    const uint4 x4 = *slot;
+    const uint32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
+    float zs[4];
+    uint32_t keepm = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool touched = xs[t] != kSent;
+      bool keep;
+      if (kLayer) {
+        zs[t] = touched ? layer_epilogue(__uint_as_float(xs[t]), b, p.clip) : zu;
+        keep = (touched || dense_row) && zs[t] != 0.0f;
+      } else {
+        zs[t] = __uint_as_float(xs[t]);
+        keep = touched;
+      }
+      if (s0 + t < wlen && keep) keepm |= 1u << t;
+    }
+    const uint32_t kc = __popc(keepm);
+    const uint32_t incl = warp_incl_scan(kc, lane);
+    const uint32_t ctot = __shfl_sync(0xffffffffu, incl, 31);
+    if (can_write) {
+      unsigned long long q = pos + (incl - kc);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (keepm & (1u << t)) {
+          p.sc_c[q] = wbase + s0 + t;
+          p.sc_v[q] = zs[t];
+          ++q;
+        }
+    }
+    pos += ctot;
+    *slot = make_uint4(kSent, kSent, kSent, kSent);
+  }
+  __syncwarp();
+}
+
+// One work item: output row i, windows [g*kGroup, g*kGroup + kGroup).  The
+// first 64 in-edges of the row are loaded once for the group and kept in
+// registers.  Loops are deliberately not unrolled: one inlined copy each of
+// fold_chunk and emit_window keeps the kernel inside the instruction cache.
+template <typename Ops, bool kLayer>
+__device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
+                             int lane) {
+  const uint32_t S = 1u << p.sh;
+  const uint32_t w0 = g * kGroup;
+  const uint32_t wn = min(kGroup, p.nW - w0);
+  const uint32_t eb = p.arp[i], ee = p.arp[i + 1];
+  const uint32_t deg = ee - eb;
+  float b = 0.0f, zu = 0.0f;
+  bool dense_row = false;
+  if (kLayer) {
+    b = p.bias[i];
+    zu = layer_epilogue(0.0f, b, p.clip);
+    dense_row = zu != 0.0f;
+  }
+  uint32_t k0 = 0, k1 = 0;
+  float a0 = 0.0f, a1 = 0.0f;
+  if (uint32_t(lane) < deg) {
+    k0 = p.aci[eb + lane];
+    a0 = p.av[eb + lane];
+  }
+  if (uint32_t(lane) + 32 < deg) {
+    k1 = p.aci[eb + 32 + lane];
+    a1 = p.av[eb + 32 + lane];
+  }
+  const uint32_t nchunks = p.b_empty ? 0u : (deg + 31) / 32;
+#pragma unroll 1
+  for (uint32_t gw = 0; gw < wn; ++gw) {
+    const uint32_t w = w0 + gw;
+    const uint32_t wbase = w << p.sh;
+    uint32_t T = 0;
+    bool any = false;
+#pragma unroll 1
+    for (uint32_t c = 0; c < nchunks; ++c) {
+      const uint32_t e = eb + 32 * c + lane;
+      const bool valid = e < ee;
+      uint32_t kk;
+      float aa;
+      if (c == 0) {
+        kk = k0;
+        aa = a0;
+      } else if (c == 1) {
+        kk = k1;
+        aa = a1;
+      } else {
+        kk = valid ? p.aci[e] : 0u;
+        aa = valid ? p.av[e] : 0.0f;
+      }
+      uint32_t beg = 0, cnt = 0;
+      if (valid) {
+        const uint32_t* wk = p.wp + size_t(kk) * p.nW + w;
+        beg = wk[0];
+        cnt = wk[1] - beg;
+      }
+      fold_chunk<Ops>(p, ws, lane, wbase, aa, beg, cnt, T, any);
+    }
+    emit_window<kLayer>(p, ws, lane, uint64_t(i) * p.nW + w, wbase, min(S, p.n - wbase), any, T,
+                        b, zu, dense_row);
+  }
+}
+
+// Phase A over all items, window-group-major so the live slice of B stays in L2.
+template <typename Ops, bool kLayer>
+__device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
+                                        uint64_t gw, uint64_t nwarps) {
+  const uint32_t ng = (p.nW + kGroup - 1) / kGroup;
+  const uint64_t items = uint64_t(ng) * p.m;
+  for (uint64_t it = gw; it < items; it += nwarps)
+    process_item<Ops, kLayer>(p, uint32_t(it % p.m), uint32_t(it / p.m), ws, lane);
 }
 
 // ---- generic SpGEMM (mxm over any semiring): separate kernels -------------------------
@@ -348,7 +424,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_spgemm_rows(RowArgs p, uint32_t
   warp_smem_init(ws, S, lane);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t i = gw; i < m; i += nw) process_row<Ops, false>(p, i, ws, lane);
+  phase_a<Ops, false>(p, ws, lane, gw, nw);
 }
 
 __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
@@ -502,6 +578,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_sparse_engine(EngineArgs p) {
     ra.bv = in_v;
     ra.wp = in_wp;
     ra.b_empty = total_in == 0;
+    ra.m = p.m;
     ra.n = p.n;
     ra.nW = p.nW;
     ra.sh = p.sh;
@@ -517,11 +594,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_sparse_engine(EngineArgs p) {
     ra.err = p.err;
 
     // ---- phase A: rows ---------------------------------------------------------------
-    for (uint32_t i = gw; i < p.m; i += nwarps) process_row<OpArith, true>(ra, i, ws, lane);
+    phase_a<OpArith, true>(ra, ws, lane, gw, nwarps);
     grid.sync();
 
     // ---- phase B: exclusive scan of item counts -> output window table ---------------
-    uint32_t* out_wp = p.wp[cur];
+    uint32_t* const out_wp = cur ? p.wp[1] : p.wp[0];
     const uint64_t per = (items + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = min(items, uint64_t(blockIdx.x) * per), hi = min(items, lo + per);
     unsigned long long mine = 0;
@@ -561,7 +638,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_sparse_engine(EngineArgs p) {
     grid.sync();
 
     // ---- phase C: gather scratch spans into CSR order -------------------------------
-    if (grand <= p.cap) {
+    uint32_t* const oc = cur ? p.ci[1] : p.ci[0];
+    float* const ov = cur ? p.v[1] : p.v[0];
+    if (grand <= p.cap && grand > 0) {
       for (uint64_t it = gw; it < items; it += nwarps) {
         const uint32_t c = p.item_cnt[it];
         if (!c) continue;
@@ -569,8 +648,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_sparse_engine(EngineArgs p) {
         if (src + c > p.cap) continue;
         const uint32_t dst = out_wp[it];
         for (uint32_t t = lane; t < c; t += 32) {
-          p.ci[cur][size_t(dst) + t] = p.sc_c[src + t];
-          p.v[cur][size_t(dst) + t] = p.sc_v[src + t];
+          oc[size_t(dst) + t] = p.sc_c[src + t];
+          ov[size_t(dst) + t] = p.sc_v[src + t];
         }
       }
     }
@@ -581,8 +660,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_sparse_engine(EngineArgs p) {
     grid.sync();
 
     total_in = grand;
-    in_ci = p.ci[cur];
-    in_v = p.v[cur];
+    in_ci = oc;
+    in_v = ov;
     in_wp = out_wp;
     last = cur;
     cur ^= 1;
@@ -598,7 +677,14 @@ struct WinGeom {
 };
 
 static WinGeom geometry(uint32_t n) {
-  int sh = 11;  // 2048-sample windows; small batches use one smaller window
+  // 1024-sample windows by default (SK_WINDOW_LOG2 overrides, 8..12, for tuning);
+  // small batches use one smaller window
+  static const int env_sh = [] {
+    const char* e = getenv("SK_WINDOW_LOG2");
+    const int v = e ? atoi(e) : 10;
+    return (v >= 8 && v <= 12) ? v : 10;
+  }();
+  int sh = env_sh;
   while (sh > 7 && (1u << (sh - 1)) >= n) --sh;
   WinGeom g;
   g.sh = sh;
@@ -665,6 +751,7 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
   p.bv = b->v;
   p.wp = wp_b;
   p.b_empty = false;
+  p.m = m;
   p.n = n;
   p.nW = g.nW;
   p.sh = g.sh;
