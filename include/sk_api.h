@@ -189,6 +189,21 @@ sk_status sk_relu_forward_host(sk_ctx* ctx, const sk_model* m, uint32_t n,
 sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m,
                                  const sk_csr* y0, const sk_fwd_opts* opt,
                                  sk_csr** out, uint64_t* nnz_trace);
+/* One sparse-activation layer with a RECTANGULAR weight block: W_ref rows are
+ * a block of output neurons (m_blk x m), Y is m x n, the result m_blk x n.
+ * Used by the column-sharded forward (each GPU owns a block of output
+ * neurons, BASELINE cfg5); bias is host memory of length m_blk. */
+sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* bias,
+                          const sk_csr* y, float clip, sk_csr** out);
+/* Zero-copy view of a handle's device arrays (valid while the handle lives). */
+sk_status sk_csr_device_arrays(const sk_csr* a, uint32_t** row_ptr,
+                               uint32_t** col_idx, float** values);
+/* New handle from device arrays (copied; e.g. buffers owned by torch/NCCL). */
+sk_status sk_csr_from_device(sk_ctx* ctx, uint32_t rows, uint32_t cols, size_t nnz,
+                             const uint32_t* row_ptr, const uint32_t* col_idx,
+                             const float* values, sk_csr** out);
+/* Stream-ordered device-to-device copy on the context stream. */
+sk_status sk_memcpy_d2d(sk_ctx* ctx, void* dst, const void* src, size_t bytes);
 /* Category set of a result: sorted indices of samples (columns) holding any
  * nonzero; returns the count; idx may be NULL to size. */
 sk_status sk_categories_csr(sk_ctx* ctx, const sk_csr* y, uint32_t* idx,

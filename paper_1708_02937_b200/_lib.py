@@ -36,6 +36,7 @@ EXPORTS = [
     "sk_model_create", "sk_model_shape", "sk_model_free",
     "sk_layer_step", "sk_relu_forward", "sk_relu_forward_host", "sk_relu_forward_sparse",
     "sk_categories_csr", "sk_categories_dense",
+    "sk_sparse_layer", "sk_csr_device_arrays", "sk_csr_from_device", "sk_memcpy_d2d",
     "sk_dense_layer_step", "sk_dense_relu_forward",
     "sk_gen_layer_fixed", "sk_gen_layer_density", "sk_gen_input_dense",
     "sk_gen_input_binary", "sk_layer_seed",
@@ -107,6 +108,11 @@ def load() -> C.CDLL:
     L.sk_relu_forward.argtypes = [vp, vp, vp, C.POINTER(FwdOpts), C.POINTER(vp)]
     L.sk_relu_forward_host.argtypes = [vp, vp, C.c_uint32, vp, C.POINTER(FwdOpts), vp]
     L.sk_relu_forward_sparse.argtypes = [vp, vp, vp, C.POINTER(FwdOpts), C.POINTER(vp), vp]
+    L.sk_sparse_layer.argtypes = [vp, vp, vp, vp, C.c_float, C.POINTER(vp)]
+    L.sk_csr_device_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
+    L.sk_csr_from_device.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_size_t, vp, vp, vp,
+                                     C.POINTER(vp)]
+    L.sk_memcpy_d2d.argtypes = [vp, vp, vp, C.c_size_t]
     L.sk_categories_csr.argtypes = [vp, vp, vp, C.c_size_t, C.POINTER(C.c_size_t)]
     L.sk_categories_dense.argtypes = [vp, vp, vp, C.c_size_t, C.POINTER(C.c_size_t)]
     L.sk_dense_layer_step.argtypes = [vp, vp, vp, vp, C.POINTER(vp)]

@@ -415,7 +415,7 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
 
 // ---- generic SpGEMM (mxm over any semiring): separate kernels -------------------------
 
-template <typename Ops>
+template <typename Ops, bool kLayer>
 __global__ void __launch_bounds__(kWarps * 32) k_spgemm_rows(RowArgs p, uint32_t m) {
   extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_spgemm_rows(RowArgs p, uint32_t
   warp_smem_init(ws, S, lane);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  phase_a<Ops, false>(p, ws, lane, gw, nw);
+  phase_a<Ops, kLayer>(p, ws, lane, gw, nw);
 }
 
 __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
@@ -712,9 +712,27 @@ static void set_smem_attr(K kernel) {
   SK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 }
 
-sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semiring s) {
+template <typename Ops, bool kLayer>
+static void launch_rows(sk_ctx* ctx, const RowArgs& p, uint32_t m, size_t smem) {
+  static bool attr = false;
+  if (!attr) {
+    set_smem_attr(k_spgemm_rows<Ops, kLayer>);
+    attr = true;
+  }
+  int per_sm = 1;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_rows<Ops, kLayer>,
+                                                        kWarps * 32, smem));
+  const unsigned grid = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((m + kWarps - 1) / kWarps, uint64_t(ctx->num_sms) * std::max(1, per_sm))));
+  SK_LAUNCH((k_spgemm_rows<Ops, kLayer>), grid, kWarps * 32, smem, ctx->stream, p, m);
+}
+
+// C = A.B over a semiring (generic mode), or one layer's SpGEMM + epilogue
+// (layer mode: bias != nullptr).  A may be rectangular.
+static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semiring s,
+                           const float* d_bias, float clip, uint64_t dense_rows) {
   const uint32_t m = a->rows, n = b->cols;
-  if (m == 0 || n == 0 || a->nnz == 0 || b->nnz == 0) {
+  if (m == 0 || n == 0 || ((a->nnz == 0 || b->nnz == 0) && !d_bias)) {
     sk_csr* o = new_csr(ctx, m, n, 0);
     SK_CUDA(cudaMemsetAsync(o->rp, 0, (size_t(m) + 1) * 4, ctx->stream));
     return o;
@@ -728,8 +746,9 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
   SK_CUDA(cudaMemcpyAsync(&prods, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
   SK_CUDA(cudaMemsetAsync(d, 0, 16, ctx->stream));  // d[0] becomes the bump counter
-  const unsigned long long cap =
-      std::max<unsigned long long>(1, std::min<unsigned long long>(prods, uint64_t(m) * n));
+  // outputs <= products, plus full rows for rows whose bias survives the ReLU
+  const unsigned long long cap = std::max<unsigned long long>(
+      1, std::min<unsigned long long>(prods + dense_rows * n, uint64_t(m) * n));
   if (cap > 0xFFFFFFFFull)
     fail(SK_ERR_INVALID_ARGUMENT, "mxm result nnz exceeds the 32-bit index range");
   const uint64_t items = uint64_t(m) * g.nW;
@@ -755,8 +774,9 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
   p.n = n;
   p.nW = g.nW;
   p.sh = g.sh;
-  p.bias = nullptr;
-  p.clip = 0.0f;
+  p.b_empty = b->nnz == 0;
+  p.bias = d_bias;
+  p.clip = clip;
   p.item_cnt = item_cnt;
   p.item_off = item_off;
   p.sc_c = sc_c;
@@ -766,20 +786,11 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
   p.overflow = overflow;
   p.err = ctx->d_err;
   const size_t smem = block_smem(g);
-  dispatch_semiring(s, [&](auto ops) {
-    using Ops = decltype(ops);
-    static bool attr = false;
-    if (!attr) {
-      set_smem_attr(k_spgemm_rows<Ops>);
-      attr = true;
-    }
-    int per_sm = 1;
-    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_rows<Ops>,
-                                                          kWarps * 32, smem));
-    const unsigned grid = unsigned(std::max<uint64_t>(
-        1, std::min<uint64_t>((m + kWarps - 1) / kWarps, uint64_t(ctx->num_sms) * std::max(1, per_sm))));
-    SK_LAUNCH(k_spgemm_rows<Ops>, grid, kWarps * 32, smem, ctx->stream, p, m);
-  });
+  if (d_bias) {
+    launch_rows<OpArith, true>(ctx, p, m, smem);
+  } else {
+    dispatch_semiring(s, [&](auto ops) { launch_rows<decltype(ops), false>(ctx, p, m, smem); });
+  }
   SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
   exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
   SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, item_cnt, item_off,
@@ -800,6 +811,15 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
                   (void*)sc_v})
     dfree(ctx, q);
   return o;
+}
+
+sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semiring s) {
+  return spgemm_impl(ctx, a, b, s, nullptr, 0.0f, 0);
+}
+
+sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const sk_csr* y,
+                          float clip, uint64_t dense_rows) {
+  return spgemm_impl(ctx, w, y, SK_ARITHMETIC, d_bias, clip, dense_rows);
 }
 
 // ---- the sparse-activation forward pass -----------------------------------------

@@ -516,3 +516,56 @@ extern "C" sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m, cons
 extern "C" uint64_t sk_layer_seed(uint64_t seed, uint32_t layer) {
   return splitmix_at(seed, 1000ull + layer);
 }
+
+extern "C" sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* bias,
+                                     const sk_csr* y, float clip, sk_csr** out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (w->cols != y->rows)
+      fail(SK_ERR_DIMENSION, "weight is " + dim_string(w->rows, w->cols) + " but input has " +
+                                 std::to_string(y->rows) + " rows");
+    if (!bias)
+      fail(SK_ERR_DIMENSION, "bias length 0 does not match " + std::to_string(w->rows) +
+                                 " output rows");
+    float* db = dalloc<float>(ctx, w->rows);
+    SK_CUDA(cudaMemcpyAsync(db, bias, size_t(w->rows) * 4, cudaMemcpyHostToDevice, ctx->stream));
+    uint64_t dense_rows = 0;  // rows whose untouched positions survive: 0 + b_i > 0 or NaN
+    for (uint32_t i = 0; i < w->rows; ++i) dense_rows += !(bias[i] <= 0.0f);
+    sk_csr* o = sparse_layer_impl(ctx, w, db, y, clip, dense_rows);
+    dfree(ctx, db);
+    sync(ctx);
+    *out = o;
+  });
+}
+
+extern "C" sk_status sk_csr_device_arrays(const sk_csr* a, uint32_t** rp, uint32_t** ci,
+                                          float** v) {
+  return guarded([&] {
+    if (rp) *rp = a->rp;
+    if (ci) *ci = a->ci;
+    if (v) *v = a->v;
+  });
+}
+
+extern "C" sk_status sk_csr_from_device(sk_ctx* ctx, uint32_t rows, uint32_t cols, size_t nnz,
+                                        const uint32_t* rp, const uint32_t* ci, const float* v,
+                                        sk_csr** out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    sk_csr* a = new_csr(ctx, rows, cols, nnz);
+    SK_CUDA(cudaMemcpyAsync(a->rp, rp, (size_t(rows) + 1) * 4, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    if (nnz) {
+      SK_CUDA(cudaMemcpyAsync(a->ci, ci, nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+      SK_CUDA(cudaMemcpyAsync(a->v, v, nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    *out = a;
+  });
+}
+
+extern "C" sk_status sk_memcpy_d2d(sk_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (bytes) SK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  });
+}

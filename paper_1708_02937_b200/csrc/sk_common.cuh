@@ -244,6 +244,8 @@ void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b,
                           uint32_t n, sk_semiring s, float* out);
 sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b,
                          sk_semiring s);
+sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const sk_csr* y,
+                          float clip, uint64_t dense_rows);
 sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* m, const sk_csr* y0,
                             float clip, uint64_t* nnz_trace);
 void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b,

@@ -717,3 +717,36 @@ def gen_input_binary(m: int, n: int, k: int, seed: int, sample_offset: int = 0,
     h = vp()
     _check(c._L.sk_gen_input_binary(c.h, m, n, k, seed, sample_offset, C.byref(h)))
     return CsrMatrix(m, n, ctx=c, _handle=h)
+
+
+def sparse_layer(w: CsrMatrix, bias, y: CsrMatrix, clip: float = 0.0) -> CsrMatrix:
+    """One sparse-activation layer with a (possibly rectangular) weight block:
+    W_ref rows = a block of output neurons.  The unit of the column-sharded
+    forward pass (each GPU owns a block of output neurons)."""
+    b = _f32(bias)
+    if b.size != w.rows():
+        raise DimensionError(f"bias length {b.size} does not match {w.rows()} output rows")
+    h = vp()
+    _check(y.ctx._L.sk_sparse_layer(y.ctx.h, w.h, b.ctypes.data, y.h, float(clip), C.byref(h)))
+    return CsrMatrix(w.rows(), y.cols(), ctx=y.ctx, _handle=h)
+
+
+def csr_device_arrays(a: CsrMatrix):
+    """(row_ptr, col_idx, values) device pointers of a handle (zero-copy)."""
+    rp, ci, v = vp(), vp(), vp()
+    _check(a.ctx._L.sk_csr_device_arrays(a.h, C.byref(rp), C.byref(ci), C.byref(v)))
+    return rp.value or 0, ci.value or 0, v.value or 0
+
+
+def csr_from_device(rows: int, cols: int, nnz: int, rp_ptr: int, ci_ptr: int, v_ptr: int,
+                    ctx: Context | None = None) -> CsrMatrix:
+    c = _ctx(ctx)
+    h = vp()
+    _check(c._L.sk_csr_from_device(c.h, rows, cols, nnz, vp(rp_ptr), vp(ci_ptr), vp(v_ptr),
+                                   C.byref(h)))
+    return CsrMatrix(rows, cols, ctx=c, _handle=h)
+
+
+def memcpy_d2d(dst_ptr: int, src_ptr: int, nbytes: int, ctx: Context | None = None):
+    c = _ctx(ctx)
+    _check(c._L.sk_memcpy_d2d(c.h, vp(dst_ptr), vp(src_ptr), nbytes))

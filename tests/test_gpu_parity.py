@@ -379,3 +379,45 @@ def test_sparse_route_equals_dense_route(sk):
     dense = sk.relu_forward(model, y0).numpy()
     sparse, _ = sk.relu_forward_sparse(model, sk.from_dense(y0))
     assert np.array_equal(bits(sk.to_dense(sparse).numpy()), bits(dense))
+
+
+# ---- multi-GPU building blocks on one GPU ----------------------------------------------
+
+def test_sparse_layer_on_a_row_block_matches_oracle(sk, port):
+    from oracle.oracle import Csr
+    m, n = 4096, 700
+    W = port.gen_layer_fixed(m, 32, 5, 1.0 / 16)
+    Y = port.gen_input_binary(m, n, 300, 5)
+    r0, r1 = 1000, 2500
+    blk = Csr(r1 - r0, m, (W.row_ptr[r0:r1 + 1] - W.row_ptr[r0]).astype(np.uint32),
+              W.col_idx[W.row_ptr[r0]:W.row_ptr[r1]], W.values[W.row_ptr[r0]:W.row_ptr[r1]])
+    b = np.where(np.arange(r1 - r0) % 7 == 0, 0.01, -0.05).astype(np.float32)
+    got = sk.sparse_layer(dev_csr(sk, blk), b, dev_csr(sk, Y), 32.0)
+    assert_csr_bitwise(got, port.layer_sparse(blk, b, Y, 32.0))
+
+
+def test_column_sharded_forward_single_rank_nccl(sk, port):
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1708_02937_b200.shard import relu_forward_sparse_colsharded
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port_no = s.getsockname()[1]
+        s.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port_no}", rank=0,
+                                world_size=1)
+    m, n, L = 4096, 500, 3
+    hW = [port.gen_layer_fixed(m, 32, port.layer_seed(8, k), 1.0 / 16) for k in range(L)]
+    hY = port.gen_input_binary(m, n, 400, 8)
+    b = np.full(m, -0.05, np.float32)
+    y, trace = relu_forward_sparse_colsharded([dev_csr(sk, w) for w in hW], [b] * L,
+                                              dev_csr(sk, hY), clip=32.0,
+                                              device=torch.device("cuda", 0))
+    want = hY
+    for w in hW:
+        want = port.layer_sparse(w, b, want, 32.0)
+    assert_csr_bitwise(y, want)
+    assert trace[-1] == want.nnz
+    dist.destroy_process_group()
