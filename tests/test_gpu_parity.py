@@ -421,3 +421,44 @@ def test_column_sharded_forward_single_rank_nccl(sk, port):
     assert_csr_bitwise(y, want)
     assert trace[-1] == want.nnz
     dist.destroy_process_group()
+
+
+# ---- the dense comparator leg on tcgen05 (K4) ----------------------------------------
+
+def scaled_ok(got, want, scale):
+    """approx_equal_scaled (semiring.hpp:50-55): |x-y| <= max(kAbsTol, kRelTol*scale)."""
+    return np.abs(got.astype(np.float64) - want.astype(np.float64)) <= np.maximum(1e-6, 1e-5 * scale)
+
+
+@pytest.mark.parametrize("M,K,N", [(128, 32, 128), (130, 33, 7), (1000, 600, 257),
+                                   (4096, 4096, 256), (1, 5, 1)])
+def test_dense_mxm_baseline_tcgen05_within_scaled_tolerance(sk, ref, M, K, N):
+    rng = np.random.default_rng(M + K + N)
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(0, 1, (K, N)).astype(np.float32)
+    a[rng.random(a.shape) < 0.3] = 0.0
+    got = sk.dense_mxm_baseline(sk.DenseMatrix.from_numpy(a), sk.DenseMatrix.from_numpy(b)).numpy()
+    exact = a.astype(np.float64) @ b.astype(np.float64)
+    want = ref.dense_mxm_baseline(a, b, workers=8) if M * K * N < 2e9 else exact.astype(np.float32)
+    scale = np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64)
+    assert scaled_ok(got, want, scale).all()
+    # an fp32-class result (3xTF32): a single-pass tf32 product carries ~2^-11
+    # relative error per term (median |err|/scale ~1e-4); 3xTF32 is ~1e-7
+    rel = np.abs(got - exact) / np.maximum(scale, 1e-30)
+    assert np.median(rel) < 1e-6 and rel.max() < 1e-5
+
+
+def test_dense_layer_step_cfg2_density_matches_reference(sk, ref, port):
+    m, n = 4096, 256
+    W = port.gen_layer_density(m, 0.1, port.layer_seed(7, 0))
+    wd = W.to_dense()
+    y = port.gen_input_dense(m, n, 7)
+    b = np.full(m, -0.05, np.float32)
+    got = sk.dense_layer_step(sk.DenseMatrix.from_numpy(wd), b, sk.DenseMatrix.from_numpy(y)).numpy()
+    want = ref.dense_layer_step(wd, b, y, workers=8)
+    scale = np.abs(wd).astype(np.float64) @ np.abs(y).astype(np.float64)
+    assert scaled_ok(got, want, scale).all()
+    # ReLU pattern equal except where the pre-activation is within tolerance of 0
+    pre = (wd.astype(np.float64) @ y.astype(np.float64)) + b[:, None]
+    near = np.abs(pre) <= 1e-5 * scale + 1e-6
+    assert ((got != 0) == (want != 0))[~near].all()
