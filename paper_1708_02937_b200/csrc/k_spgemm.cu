@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <climits>
 
 #include "sk_common.cuh"
 
@@ -147,7 +148,7 @@ __device__ __forceinline__ unsigned long long reserve(const RowArgs& p, uint64_t
 // flattened (ascending k, ascending sample) order, then applied 32 at a time;
 // products of one step that hit the same sample are applied in rounds by rank,
 // i.e. lane order = ascending k.
-template <typename Ops>
+template <typename Ops, bool kExact>
 __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws, int lane,
                                            uint32_t wbase, float a, uint32_t beg, uint32_t cnt,
                                            uint32_t& T, bool& any) {
@@ -184,6 +185,15 @@ __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws,
     __syncwarp();
     // ---- application, 32 staged products per step
     const uint32_t nb = min(kStage, total - base);
+    if (kExact) {
+      // Every partial sum of this layer is exactly representable (proved from
+      // the operands' granularity and magnitude), so the order of the adds
+      // cannot change a single bit: shared-memory atomics, no ordering rounds.
+      for (uint32_t j = lane; j < nb; j += 32)
+        atomicAdd(reinterpret_cast<float*>(ws.acc) + ws.st_s[j], ws.st_p[j]);
+      __syncwarp();
+      continue;
+    }
     for (uint32_t t = 0; t < nb; t += 32) {
       const uint32_t j = t + lane;
       const bool act = j < nb;
@@ -216,7 +226,7 @@ __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws,
 }
 
 // Epilogue of one (row, window): emit the row's window slice of the output.
-template <bool kLayer>
+template <bool kLayer, bool kExact>
 __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws, int lane,
                                             uint64_t it, uint32_t wbase, uint32_t wlen, bool any,
                                             uint32_t T, float b, float zu, bool dense_row) {
@@ -225,7 +235,7 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
     if (lane == 0) p.item_cnt[it] = 0;
     return;
   }
-  if (!dense_row && T <= cap) {
+  if (!kExact && !dense_row && T <= cap) {
     // sparse epilogue over the touched list; survivors -> bitmap -> ordered emit
     for (uint32_t t = lane; t < T; t += 32) {
       const uint32_t s = ws.list[t];
@@ -274,8 +284,11 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
     __syncwarp();
     return;
   }
-  // dense epilogue: two sweeps over the window
+  // dense epilogue: two sweeps over the window.  In exact mode the accumulator
+  // starts at +0.0 instead of the sentinel: an untouched position then gives
+  // epilogue(0 + b) = zu, which is exactly what "untouched" means.
   const uint32_t nch = (wlen + 127) >> 7;
+  const uint32_t reset = kExact ? 0u : kSent;
   uint32_t mine = 0;
   for (uint32_t c = 0; c < nch; ++c) {
     const uint32_t s0 = c * 128 + lane * 4;
@@ -283,7 +296,7 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
     const uint32_t xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const bool touched = xs[t] != kSent;
+      const bool touched = kExact || xs[t] != kSent;
       bool keep;
       if (kLayer) {
         const float z = touched ? layer_epilogue(__uint_as_float(xs[t]), b, p.clip) : zu;
@@ -308,7 +321,7 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
     uint32_t keepm = 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const bool touched = xs[t] != kSent;
+      const bool touched = kExact || xs[t] != kSent;
       bool keep;
       if (kLayer) {
         zs[t] = touched ? layer_epilogue(__uint_as_float(xs[t]), b, p.clip) : zu;
@@ -333,7 +346,7 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
         }
     }
     pos += ctot;
-    *slot = make_uint4(kSent, kSent, kSent, kSent);
+    *slot = make_uint4(reset, reset, reset, reset);
   }
   __syncwarp();
 }
@@ -342,7 +355,7 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
 // first 64 in-edges of the row are loaded once for the group and kept in
 // registers.  Loops are deliberately not unrolled: one inlined copy each of
 // fold_chunk and emit_window keeps the kernel inside the instruction cache.
-template <typename Ops, bool kLayer>
+template <typename Ops, bool kLayer, bool kExact>
 __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
                              int lane) {
   const uint32_t S = 1u << p.sh;
@@ -396,21 +409,92 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
         beg = wk[0];
         cnt = wk[1] - beg;
       }
-      fold_chunk<Ops>(p, ws, lane, wbase, aa, beg, cnt, T, any);
+      fold_chunk<Ops, kExact>(p, ws, lane, wbase, aa, beg, cnt, T, any);
     }
-    emit_window<kLayer>(p, ws, lane, uint64_t(i) * p.nW + w, wbase, min(S, p.n - wbase), any, T,
+    emit_window<kLayer, kExact>(p, ws, lane, uint64_t(i) * p.nW + w, wbase, min(S, p.n - wbase), any, T,
                         b, zu, dense_row);
   }
 }
 
 // Phase A over all items, window-group-major so the live slice of B stays in L2.
-template <typename Ops, bool kLayer>
+template <typename Ops, bool kLayer, bool kExact>
 __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
                                         uint64_t gw, uint64_t nwarps) {
   const uint32_t ng = (p.nW + kGroup - 1) / kGroup;
   const uint64_t items = uint64_t(ng) * p.m;
   for (uint64_t it = gw; it < items; it += nwarps)
-    process_item<Ops, kLayer>(p, uint32_t(it % p.m), uint32_t(it / p.m), ws, lane);
+    process_item<Ops, kLayer, kExact>(p, uint32_t(it % p.m), uint32_t(it / p.m), ws, lane);
+}
+
+// Per-matrix value statistics for the exactness test: the smallest power of
+// two every nonzero value is a multiple of ("granularity", lowbit exponent),
+// the smallest e with |v| < 2^e, and whether any value is not finite.
+struct ValueStats {
+  int lowbit;     // min over nonzero values
+  int ehi;        // max over nonzero values
+  int nonfinite;  // any Inf/NaN
+  int maxdeg;     // max stored entries per row (weights only)
+};
+
+__device__ __forceinline__ void value_bits(float v, int& lowbit, int& ehi) {
+  const uint32_t b = __float_as_uint(v) & 0x7fffffffu;
+  const int E = int(b >> 23);
+  uint32_t M = b & 0x7fffffu;
+  int e0;
+  if (E == 0) {
+    e0 = -149;
+  } else {
+    M |= 0x800000u;
+    e0 = E - 150;
+  }
+  lowbit = e0 + __ffs(M) - 1;
+  ehi = e0 + (32 - __clz(M));
+}
+
+__global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
+  int lo = INT_MAX, hi = INT_MIN, nf = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const float x = v[i];
+    if (!isfinite(x)) {
+      nf = 1;
+    } else if (x != 0.0f) {
+      int l, h;
+      value_bits(x, l, h);
+      lo = min(lo, l);
+      hi = max(hi, h);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    nf |= __shfl_xor_sync(0xffffffffu, nf, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&out->lowbit, lo);
+    atomicMax(&out->ehi, hi);
+    if (nf) atomicOr(&out->nonfinite, 1);
+  }
+}
+
+__global__ void k_max_row_len(const uint32_t* rp, uint32_t rows, ValueStats* out) {
+  int mx = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
+    mx = max(mx, int(rp[i + 1] - rp[i]));
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&out->maxdeg, mx);
+}
+
+// True when every partial sum of W.Y is exactly representable in fp32, so the
+// accumulation order cannot change any bit of the result.
+__device__ __forceinline__ bool products_exact(const ValueStats& w, const ValueStats& y) {
+  if (w.nonfinite || y.nonfinite) return false;
+  if (w.lowbit == INT_MAX || y.lowbit == INT_MAX) return true;  // an operand is all zero
+  int lg = 0;
+  while ((1 << lg) < max(w.maxdeg, 1)) ++lg;
+  const int top = lg + w.ehi + y.ehi;     // |partial sum| < 2^top
+  const int gran = w.lowbit + y.lowbit;   // every partial sum is a multiple of 2^gran
+  return gran >= -126 && top <= 127 && top - gran <= 24;
 }
 
 // ---- generic SpGEMM (mxm over any semiring): separate kernels -------------------------
@@ -424,7 +508,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_spgemm_rows(RowArgs p, uint32_t
   warp_smem_init(ws, S, lane);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  phase_a<Ops, kLayer>(p, ws, lane, gw, nw);
+  phase_a<Ops, kLayer, false>(p, ws, lane, gw, nw);
 }
 
 __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
@@ -515,6 +599,9 @@ struct EngineArgs {
   int* overflow;
   int* err;
   long long* stamps;               // optional %globaltimer per layer end (L+1)
+  const ValueStats* wstats;        // per layer
+  const ValueStats* y0stats;       // of Y0's values
+  int exact_ok;                    // layer 0 windows are dense enough for the order-free path
 };
 
 __device__ __forceinline__ long long globaltimer() {
@@ -536,7 +623,7 @@ __device__ unsigned long long block_sum_u64(unsigned long long v, unsigned long 
   return t;
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_sparse_engine(EngineArgs p) {
+__global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ unsigned long long red[kWarps];
   __shared__ unsigned long long tile_carry;
@@ -594,7 +681,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_sparse_engine(EngineArgs p) {
     ra.err = p.err;
 
     // ---- phase A: rows ---------------------------------------------------------------
-    phase_a<OpArith, true>(ra, ws, lane, gw, nwarps);
+    // Layer 0's operand statistics are known: if every partial sum is exact, the
+    // order-free path (shared atomics, zero-initialised windows) is bitwise the
+    // ascending fold.  Decided identically by every warp.
+    const bool exact = layer == 0 && p.exact_ok && products_exact(p.wstats[0], *p.y0stats);
+    if (exact) {
+      for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = 0u;
+      __syncwarp();
+      phase_a<OpArith, true, true>(ra, ws, lane, gw, nwarps);
+      for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = kSent;
+      __syncwarp();
+    } else {
+      phase_a<OpArith, true, false>(ra, ws, lane, gw, nwarps);
+    }
     grid.sync();
 
     // ---- phase B: exclusive scan of item counts -> output window table ---------------
@@ -849,6 +948,43 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
     sync(ctx);
   }
 
+  if (!mm->d_wstats) {  // per-layer weight statistics for the exactness test (cached)
+    mm->d_wstats = dalloc<ValueStats>(ctx, L);
+    std::vector<ValueStats> init(L, ValueStats{INT_MAX, INT_MIN, 0, 0});
+    SK_CUDA(cudaMemcpyAsync(mm->d_wstats, init.data(), L * sizeof(ValueStats),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    for (uint32_t k = 0; k < L; ++k) {
+      const sk_csr* w = md->w[k];
+      ValueStats* o = static_cast<ValueStats*>(mm->d_wstats) + k;
+      if (w->nnz)
+        SK_LAUNCH(k_value_stats, grid_warps(ctx, w->nnz / 32 + 1), 256, 0, ctx->stream, w->v,
+                  w->nnz, o);
+      SK_LAUNCH(k_max_row_len, grid_warps(ctx, w->rows / 32 + 1), 256, 0, ctx->stream, w->rp,
+                w->rows, o);
+    }
+  }
+  // Layer-0 product count: the order-free path pays a shared-memory atomic per
+  // product plus a full window sweep, which only wins when windows are dense.
+  int exact_ok = 0;
+  if (y0->nnz && L > 0) {
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
+    SK_CUDA(cudaMemsetAsync(d, 0, 8, ctx->stream));
+    SK_LAUNCH(k_count_products, grid_warps(ctx, m), 256, 0, ctx->stream, md->w[0]->rp,
+              md->w[0]->ci, m, y0->rp, d);
+    unsigned long long prods = 0;
+    SK_CUDA(cudaMemcpyAsync(&prods, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    exact_ok = prods >= uint64_t(m) * g.nW * (g.S / 4);
+  }
+  ValueStats* y0stats = dalloc<ValueStats>(ctx, 1);
+  {
+    const ValueStats init{INT_MAX, INT_MIN, 0, 0};
+    SK_CUDA(cudaMemcpyAsync(y0stats, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+    if (y0->nnz)
+      SK_LAUNCH(k_value_stats, grid_warps(ctx, y0->nnz / 32 + 1), 256, 0, ctx->stream, y0->v,
+                y0->nnz, y0stats);
+  }
+
   size_t free_b = 0, total_b = 0;
   SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const unsigned long long mem_cap = (unsigned long long)(free_b * 0.6 / 24.0);
@@ -916,6 +1052,9 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
     p.overflow = flags;
     p.err = ctx->d_err;
     p.stamps = ctx->stamps;
+    p.wstats = static_cast<const ValueStats*>(mm->d_wstats);
+    p.y0stats = y0stats;
+    p.exact_ok = exact_ok;
     void* args[] = {&p};
     timing_mark(ctx);
     SK_CUDA(cudaLaunchCooperativeKernel((void*)k_sparse_engine, dim3(grid), dim3(kWarps * 32),
@@ -969,6 +1108,7 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
       release();
       dfree(ctx, wp0);
       dfree(ctx, small);
+      dfree(ctx, y0stats);
       return o;
     }
     release();
@@ -978,6 +1118,7 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   }
   dfree(ctx, wp0);
   dfree(ctx, small);
+  dfree(ctx, y0stats);
   fail(SK_ERR_OOM, "sparse forward: activation nnz exceeds the device capacity");
 }
 

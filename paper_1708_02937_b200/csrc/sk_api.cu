@@ -413,6 +413,7 @@ extern "C" sk_status sk_model_free(sk_model* m) {
     for (sk_csr* w : m->w) csr_release(w);
     dfree(m->ctx, m->bias);
     dfree(m->ctx, m->d_wptr);
+    dfree(m->ctx, m->d_wstats);
     dfree(m->ctx, m->d_bias_nonpos);
     delete m;
   });

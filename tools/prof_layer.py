@@ -22,7 +22,11 @@ m, dens, bias = {"cfg3": (16384, 0.015, -0.3), "cfg4": (65536, 0.004, -0.35)}[a.
 Ws = [sk.gen_layer_fixed(m, 32, sk.layer_seed(42, k), 1.0 / 16) for k in range(a.layers)]
 model = sk.DnnModel(Ws, [np.full(m, bias, np.float32)] * a.layers)
 Y0 = sk.gen_input_binary(m, a.batch, int(round(dens * m)), 42)
+ctx = sk.default_context()
+ctx.set_timing(True)
 for r in range(a.reps):
     t = time.perf_counter()
     out, trace = sk.relu_forward_sparse(model, Y0, sk.ForwardOptions(clip=32.0))
-    print(f"rep {r}: {1e3 * (time.perf_counter() - t):.2f} ms trace {list(trace)}", flush=True)
+    kt = ctx.kernel_times_ms()
+    print(f"rep {r}: wall {1e3 * (time.perf_counter() - t):.2f} ms engine {kt[-1]:.3f} ms "
+          f"trace {[int(x) for x in trace]}", flush=True)
