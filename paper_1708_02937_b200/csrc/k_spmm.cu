@@ -13,18 +13,23 @@
 // inner loop issues only the Y loads.  Tasks are ordered chunk-major so the
 // live Y panel (m x 128 floats) stays L2-resident while every row that
 // touches it runs.
+#include <cooperative_groups.h>
+
 #include "sk_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sk {
 
 enum EpiMode { kEpiNone = 0, kEpiLayer = 1 };
 
 template <typename Ops, int kEpi, bool kVec4>
-__global__ void __launch_bounds__(256)
-    k_spmm_rows(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
-                const float* __restrict__ wv, const float* __restrict__ bias,
-                const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
-                float* __restrict__ out, int* err) {
+__device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
+                                           const uint32_t* __restrict__ ci,
+                                           const float* __restrict__ wv,
+                                           const float* __restrict__ bias,
+                                           const float* __restrict__ y, uint32_t m, uint32_t n,
+                                           float clip, float* __restrict__ out, int* err) {
   const int lane = threadIdx.x & 31;
   const uint32_t chunks = (n + 127) / 128;
   const uint64_t tasks = uint64_t(chunks) * m;
@@ -50,17 +55,17 @@ __global__ void __launch_bounds__(256)
         const float* yr = y + size_t(k) * n;
         if (kVec4) {
           if (col0 < n) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(yr + col0));
+            const float4 v = *reinterpret_cast<const float4*>(yr + col0);
             acc0 = Ops::add(acc0, Ops::mul(a, v.x, err), err);
             acc1 = Ops::add(acc1, Ops::mul(a, v.y, err), err);
             acc2 = Ops::add(acc2, Ops::mul(a, v.z, err), err);
             acc3 = Ops::add(acc3, Ops::mul(a, v.w, err), err);
           }
         } else {
-          if (col0 + 0 < n) acc0 = Ops::add(acc0, Ops::mul(a, __ldg(yr + col0 + 0), err), err);
-          if (col0 + 1 < n) acc1 = Ops::add(acc1, Ops::mul(a, __ldg(yr + col0 + 1), err), err);
-          if (col0 + 2 < n) acc2 = Ops::add(acc2, Ops::mul(a, __ldg(yr + col0 + 2), err), err);
-          if (col0 + 3 < n) acc3 = Ops::add(acc3, Ops::mul(a, __ldg(yr + col0 + 3), err), err);
+          if (col0 + 0 < n) acc0 = Ops::add(acc0, Ops::mul(a, yr[col0 + 0], err), err);
+          if (col0 + 1 < n) acc1 = Ops::add(acc1, Ops::mul(a, yr[col0 + 1], err), err);
+          if (col0 + 2 < n) acc2 = Ops::add(acc2, Ops::mul(a, yr[col0 + 2], err), err);
+          if (col0 + 3 < n) acc3 = Ops::add(acc3, Ops::mul(a, yr[col0 + 3], err), err);
         }
       }
     }
@@ -83,10 +88,91 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+template <typename Ops, int kEpi, bool kVec4>
+__global__ void __launch_bounds__(256)
+    k_spmm_rows(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                const float* __restrict__ wv, const float* __restrict__ bias,
+                const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
+                float* __restrict__ out, int* err) {
+  spmm_tasks<Ops, kEpi, kVec4>(rp, ci, wv, bias, y, m, n, clip, out, err);
+}
+
+// The whole dense-activation forward in ONE persistent cooperative launch: each
+// layer is the K1 task loop, layers are separated by a grid barrier (every
+// output column of layer k+1 needs the whole of Y_k).  Removes the per-layer
+// launch latency that dominates small models (BASELINE cfg1).
+struct DenseEngineArgs {
+  const uint32_t* const* w_rp;
+  const uint32_t* const* w_ci;
+  const float* const* w_v;
+  const float* bias;
+  uint32_t m, n, L;
+  float clip;
+  const float* y0;
+  float* buf[2];
+  int* err;
+};
+
+template <bool kVec4>
+__global__ void __launch_bounds__(256) k_dense_engine(DenseEngineArgs p) {
+  cg::grid_group grid = cg::this_grid();
+  for (uint32_t k = 0; k < p.L; ++k) {
+    const float* src = k == 0 ? p.y0 : p.buf[(k - 1) & 1];
+    float* dst = p.buf[k & 1];
+    spmm_tasks<OpArith, kEpiLayer, kVec4>(p.w_rp[k], p.w_ci[k], p.w_v[k], p.bias + size_t(k) * p.m,
+                                          src, p.m, p.n, p.clip, dst, p.err);
+    if (k + 1 < p.L) grid.sync();
+  }
+}
+
 static unsigned spmm_grid(sk_ctx* ctx, uint32_t m, uint32_t n) {
   const uint64_t warps = uint64_t((n + 127) / 128) * m;
   const uint64_t blocks = (warps + 7) / 8;
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(blocks, uint64_t(ctx->num_sms) * 16)));
+}
+
+// Dense forward over all layers of a model: returns the buffer holding Y_L.
+void dense_forward_engine(sk_ctx* ctx, const sk_model* md, const float* y0, uint32_t n,
+                          float clip, float* buf0, float* buf1) {
+  auto* mm = const_cast<sk_model*>(md);
+  const uint32_t L = md->layers, m = md->neurons;
+  if (!mm->d_wptr) {
+    std::vector<const void*> h(size_t(3) * L);
+    for (uint32_t k = 0; k < L; ++k) {
+      h[k] = md->w[k]->rp;
+      h[L + k] = md->w[k]->ci;
+      h[2 * L + k] = md->w[k]->v;
+    }
+    mm->d_wptr = dalloc<const void*>(ctx, h.size());
+    SK_CUDA(cudaMemcpyAsync(mm->d_wptr, h.data(), h.size() * sizeof(void*),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    sync(ctx);
+  }
+  DenseEngineArgs p;
+  p.w_rp = reinterpret_cast<const uint32_t* const*>(mm->d_wptr);
+  p.w_ci = reinterpret_cast<const uint32_t* const*>(mm->d_wptr + L);
+  p.w_v = reinterpret_cast<const float* const*>(mm->d_wptr + 2 * L);
+  p.bias = md->bias;
+  p.m = m;
+  p.n = n;
+  p.L = L;
+  p.clip = clip;
+  p.y0 = y0;
+  p.buf[0] = buf0;
+  p.buf[1] = buf1;
+  p.err = ctx->d_err;
+  const bool vec = (n % 4) == 0;
+  const void* fn = vec ? (const void*)k_dense_engine<true> : (const void*)k_dense_engine<false>;
+  int per_sm = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+  const uint64_t warps = uint64_t((n + 127) / 128) * m;
+  const unsigned grid = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((warps + 7) / 8, uint64_t(ctx->num_sms) * std::max(per_sm, 1))));
+  void* args[] = {&p};
+  timing_mark(ctx);
+  SK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, ctx->stream));
+  g_launches.fetch_add(1);
+  timing_mark(ctx);
 }
 
 void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const float* y,

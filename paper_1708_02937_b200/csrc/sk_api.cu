@@ -459,16 +459,9 @@ static sk_dense* forward_dense(sk_ctx* ctx, const sk_model* m, const sk_dense* y
   const uint32_t n = y0->cols;
   sk_dense* a = new_dense(ctx, m->neurons, n);
   sk_dense* b = m->layers > 1 ? new_dense(ctx, m->neurons, n) : nullptr;
-  const float* src = y0->d;
-  sk_dense* dst = a;
-  for (uint32_t k = 0; k < m->layers; ++k) {
-    timing_mark(ctx);
-    launch_layer_dense(ctx, m->w[k], m->bias + size_t(k) * m->neurons, src, n, clip, dst->d);
-    timing_mark(ctx);
-    src = dst->d;
-    dst = (dst == a) ? b : a;
-  }
-  sk_dense* result = (m->layers % 2 == 1) ? a : b;
+  // one persistent launch for all layers; layer k writes buffer k & 1
+  dense_forward_engine(ctx, m, y0->d, n, clip, a->d, b ? b->d : nullptr);
+  sk_dense* result = ((m->layers - 1) & 1) ? b : a;
   sk_dense* spare = (result == a) ? b : a;
   if (spare) sk_dense_free(spare);
   return result;

@@ -239,6 +239,8 @@ sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                                 const float* d_v, size_t n,
                                 const uint32_t* h_r, const uint32_t* h_c);
 sk_csr* csr_transpose(sk_ctx* ctx, const sk_csr* a);
+void dense_forward_engine(sk_ctx* ctx, const sk_model* md, const float* y0, uint32_t n,
+                          float clip, float* buf0, float* buf1);
 void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias,
                         const float* y, uint32_t n, float clip, float* out);
 void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b,
