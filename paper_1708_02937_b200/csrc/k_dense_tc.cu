@@ -32,17 +32,21 @@
 namespace sk {
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 128;
-constexpr uint32_t kTileBytes = BM * BK * 4;  // 16 KB, same for A (128x32) and B (32x128)
-constexpr uint32_t kStageBytes = 4 * kTileBytes;  // A_hi, A_lo, B_hi, B_lo
-constexpr uint32_t kSmemBytes = 2 * kStageBytes + 64;
-
-// A (K-major): core (kc, mg) = 8 rows x 4 k, at mg*SBO + kc*LBO; 8 k-chunks/row group
-constexpr uint32_t kA_LBO = 128, kA_SBO = (BK / 4) * 128;       // 128 B, 1024 B
-// B is staged K-major as well (B^T tile, n rows x k): the same core layout as A.
-// (An MN-major fp32/tf32 operand would need the 128B_BASE32B swizzle.)
-constexpr uint32_t kB_LBO = 128, kB_SBO = (BK / 4) * 128;       // 128 B, 1024 B
+template <int BK>
+struct Cfg {
+  static constexpr uint32_t kTileBytes = BM * BK * 4;      // A (128 x BK) and B (BK x 128)
+  static constexpr uint32_t kStageBytes = 4 * kTileBytes;  // A_hi, A_lo, B_hi, B_lo
+  static constexpr uint32_t kSmemBytes = 2 * kStageBytes + 64;
+  static constexpr uint32_t KC = BK / 4;                   // 16-byte k-chunks per row
+  static constexpr uint32_t KC_LOG = KC == 8 ? 3 : (KC == 4 ? 2 : 1);
+  // core matrix (kc, row group) = 8 rows x 4 k at group*SBO + kc*LBO; B is staged
+  // K-major as well (B^T tile: n rows x k).  An MN-major fp32/tf32 operand would
+  // need the 128B_BASE32B swizzle.
+  static constexpr uint32_t LBO = 128, SBO = KC * 128;
+};
+constexpr uint32_t kA_LBO = 128, kA_SBO = 1024, kB_LBO = 128, kB_SBO = 1024;  // BK = 32
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -121,10 +125,14 @@ struct TcParams {  // descriptor fields, overridable for bring-up (SK_TC_DBG)
   uint32_t mode;  // 0 normal; 1 TMEM st/ld self-test (no MMA); 2 delay after wait
 };
 
+template <int BK>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tf32x3(const float* __restrict__ A, const float* __restrict__ B, uint32_t M,
                   uint32_t K, uint32_t N, const float* __restrict__ bias, int relu,
                   float* __restrict__ C, TcParams tp) {
+  using G = Cfg<BK>;
+  constexpr uint32_t kTileBytes = G::kTileBytes, kStageBytes = G::kStageBytes;
+  constexpr uint32_t KC = G::KC, KC_LOG = G::KC_LOG;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[2];
   __shared__ uint32_t tmem_base_slot;
@@ -169,17 +177,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           : "memory");
     }
   }
-  for (uint32_t t = 0; t < nk; ++t) {
-    const uint32_t s = t & 1;
-    if (t >= 2) mbar_wait(smem_u32(&mbar[s]), ((t - 2) >> 1) & 1);
-    const uint32_t st = sbase + s * kStageBytes;
+  // Register double buffering: the global loads of slab t+1 are issued before
+  // slab t is split/stored and its MMAs run, so their latency overlaps the
+  // tensor-core work instead of being exposed once per slab.
+  constexpr int NJ = int(KC);  // 16-byte chunks per thread per operand (128*KC/128)
+  float4 ra[NJ];
+  float rb[NJ][4];
+  auto load_slab = [&](uint32_t t) {
     const uint32_t k0 = t * BK;
-    // ---- A slab: 128 rows x 32 k = 1024 16-byte chunks, 8 per thread.  A warp
-    // covers 8 rows x 4 k-chunks: 8 distinct 16-byte bank groups per store.
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const uint32_t c = uint32_t(j) * kThreads + tid;
-      const uint32_t kc = (c >> 3) & 7, r = (c >> 6) * 8 + (c & 7);
+      const uint32_t kc = (c >> 3) & (KC - 1), r = (c >> (3 + KC_LOG)) * 8 + (c & 7);
       const uint32_t gr = m0 + r, gk = k0 + kc * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (gr < M) {
@@ -193,37 +202,53 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (gk + 3 < K) v.w = __ldg(src + 3);
         }
       }
+      ra[j] = v;
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const uint32_t c = uint32_t(j) * kThreads + tid;
+      const uint32_t nr = (c & 31) + 32 * ((c >> 5) & 3);
+      const uint32_t kc = c >> 7;
+      const uint32_t gn = n0 + nr, gk = k0 + kc * 4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        rb[j][q] = (gn < N && gk + q < K) ? __ldg(B + size_t(gk + q) * N + gn) : 0.0f;
+    }
+  };
+  auto store_slab = [&](uint32_t st) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const uint32_t c = uint32_t(j) * kThreads + tid;
+      const uint32_t kc = (c >> 3) & (KC - 1), r = (c >> (3 + KC_LOG)) * 8 + (c & 7);
       float h[4], l[4];
-      split(v.x, h[0], l[0]);
-      split(v.y, h[1], l[1]);
-      split(v.z, h[2], l[2]);
-      split(v.w, h[3], l[3]);
-      const uint32_t off = (r >> 3) * kA_SBO + kc * kA_LBO + (r & 7) * 16;
+      split(ra[j].x, h[0], l[0]);
+      split(ra[j].y, h[1], l[1]);
+      split(ra[j].z, h[2], l[2]);
+      split(ra[j].w, h[3], l[3]);
+      const uint32_t off = (r >> 3) * G::SBO + kc * G::LBO + (r & 7) * 16;
       st_shared_v4(st + off, h[0], h[1], h[2], h[3]);
       st_shared_v4(st + kTileBytes + off, l[0], l[1], l[2], l[3]);
     }
-    // ---- B slab, staged transposed (K-major): 128 n x 32 k = 1024 chunks of
-    // 4 k, 8 per thread.  Lanes walk 32 consecutive n, so each of the 4 loads
-    // of a chunk is a coalesced 128-byte row segment of B.
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const uint32_t c = uint32_t(j) * kThreads + tid;
-      const uint32_t nr = (c & 31) + 32 * ((c >> 5) & 3);  // n row 0..127
-      const uint32_t kc = c >> 7;                          // k chunk 0..7
-      const uint32_t gn = n0 + nr, gk = k0 + kc * 4;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (gn < N) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (gk + q < K) v[q] = __ldg(B + size_t(gk + q) * N + gn);
-      }
+      const uint32_t nr = (c & 31) + 32 * ((c >> 5) & 3);
+      const uint32_t kc = c >> 7;
       float h[4], l[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) split(v[q], h[q], l[q]);
-      const uint32_t off = (nr >> 3) * kB_SBO + kc * kB_LBO + (nr & 7) * 16;
+      for (int q = 0; q < 4; ++q) split(rb[j][q], h[q], l[q]);
+      const uint32_t off = (nr >> 3) * G::SBO + kc * G::LBO + (nr & 7) * 16;
       st_shared_v4(st + 2 * kTileBytes + off, h[0], h[1], h[2], h[3]);
       st_shared_v4(st + 3 * kTileBytes + off, l[0], l[1], l[2], l[3]);
     }
+  };
+  if (nk > 0) load_slab(0);
+  for (uint32_t t = 0; t < nk; ++t) {
+    const uint32_t s = t & 1;
+    if (t >= 2) mbar_wait(smem_u32(&mbar[s]), ((t - 2) >> 1) & 1);
+    const uint32_t st = sbase + s * kStageBytes;
+    store_slab(st);
+    if (t + 1 < nk) load_slab(t + 1);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
@@ -235,12 +260,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // K=8 is two 4-wide k-chunks (LBO apart) for both operands.
         const uint32_t ao = kk * 2 * kA_LBO, bo = kk * 2 * kB_LBO;
         const uint32_t acc0 = (t | kk) ? 1u : 0u;
-        mma_tf32(tmem, umma_desc(a_hi + ao, tp.a_lbo, tp.a_sbo),
-                 umma_desc(b_hi + bo, tp.b_lbo, tp.b_sbo), idesc, acc0);
-        mma_tf32(tmem, umma_desc(a_hi + ao, tp.a_lbo, tp.a_sbo),
-                 umma_desc(b_lo + bo, tp.b_lbo, tp.b_sbo), idesc, 1u);
-        mma_tf32(tmem, umma_desc(a_lo + ao, tp.a_lbo, tp.a_sbo),
-                 umma_desc(b_hi + bo, tp.b_lbo, tp.b_sbo), idesc, 1u);
+        const uint32_t asbo = BK == 32 ? tp.a_sbo : G::SBO, bsbo = BK == 32 ? tp.b_sbo : G::SBO;
+        mma_tf32(tmem, umma_desc(a_hi + ao, tp.a_lbo, asbo),
+                 umma_desc(b_hi + bo, tp.b_lbo, bsbo), idesc, acc0);
+        mma_tf32(tmem, umma_desc(a_hi + ao, tp.a_lbo, asbo),
+                 umma_desc(b_lo + bo, tp.b_lbo, bsbo), idesc, 1u);
+        mma_tf32(tmem, umma_desc(a_lo + ao, tp.a_lbo, asbo),
+                 umma_desc(b_hi + bo, tp.b_lbo, bsbo), idesc, 1u);
       }
       mma_commit(smem_u32(&mbar[s]));
     }
@@ -306,10 +332,16 @@ void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t 
   if (M == 0 || N == 0) return;
   static bool attr = false;
   if (!attr) {
-    SK_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::kSmemBytes));
+    SK_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32x3<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::Cfg<32>::kSmemBytes));
+    SK_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32x3<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::Cfg<16>::kSmemBytes));
     attr = true;
   }
+  static const int bk = [] {
+    const char* e = getenv("SK_TC_BK");
+    return (e && atoi(e) == 32) ? 32 : 16;
+  }();
   dim3 grid(ceil_div(N, tc::BN), ceil_div(M, tc::BM));
   tc::TcParams tp{tc::kA_LBO, tc::kA_SBO, tc::kB_LBO, tc::kB_SBO,
                   tc::idesc_tf32(tc::BM, tc::BN), 0};
@@ -319,8 +351,12 @@ void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t 
       tp = tc::TcParams{v[0], v[1], v[2], v[3], v[4], v[5]};
   }
   timing_mark(ctx);
-  SK_LAUNCH(tc::k_gemm_tf32x3, grid, tc::kThreads, tc::kSmemBytes, ctx->stream, a, b, M, K, N,
-            bias, relu, c, tp);
+  if (bk == 32)
+    SK_LAUNCH(tc::k_gemm_tf32x3<32>, grid, tc::kThreads, tc::Cfg<32>::kSmemBytes, ctx->stream, a,
+              b, M, K, N, bias, relu, c, tp);
+  else
+    SK_LAUNCH(tc::k_gemm_tf32x3<16>, grid, tc::kThreads, tc::Cfg<16>::kSmemBytes, ctx->stream, a,
+              b, M, K, N, bias, relu, c, tp);
   timing_mark(ctx);
 }
 
