@@ -133,6 +133,16 @@ def dense_layer_bytes(batch, m, nnzW):
     return 8 * batch * m + 4 * (m + 1) + 8 * nnzW + 4 * m
 
 
+def measured_traffic(workload):
+    """Per-launch DRAM traffic of the dominant kernel from the committed ncu
+    capture (profiles/r01/traffic.json), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
+        return t[workload]["bytes"], t[workload]["report"]
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
@@ -420,6 +430,10 @@ def run_ours(args, w):
             cpu = {"value": None, "unit": "edges/s", "cores": cpu_cores(), "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
 
+    if roof is not None:
+        tb, trep = measured_traffic(args.workload)
+        roof["traffic"] = tb
+        roof["traffic_source"] = trep
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
