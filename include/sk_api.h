@@ -91,6 +91,14 @@ sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count)
 /* With timing enabled, the sparse engine writes %globaltimer (ns) at the start
  * (entry 0) and at the end of every layer (entry k+1) of the last forward. */
 sk_status sk_ctx_layer_stamps(sk_ctx* ctx, long long* ns, size_t n);
+/* Density-adaptive sparse forward (sk_relu_forward_sparse): the activations
+ * move to the dense engine when a layer's output holds more than
+ * dense_above * m * n entries and back to the sparse engine below
+ * sparse_below * m * n.  Results are bitwise identical either way (the switch
+ * is only taken when every weight is finite).  dense_above <= 0 disables it.
+ * Defaults 1/32 and 1/128.  No reference counterpart (the reference's
+ * activation type is fixed by the caller, dnn.hpp:77-78). */
+sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double sparse_below);
 /* Page-lock / unlock a caller host buffer for async copies. */
 sk_status sk_host_register(void* p, size_t bytes);
 sk_status sk_host_unregister(void* p);

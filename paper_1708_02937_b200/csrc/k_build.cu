@@ -376,6 +376,14 @@ extern "C" sk_status sk_to_dense(sk_ctx* ctx, const sk_csr* a, float ambient, sk
 
 namespace sk {
 
+// Zero-filled dense copy of a CSR matrix into caller-owned device memory.
+void csr_scatter_dense(sk_ctx* ctx, const sk_csr* a, float* out) {
+  SK_CUDA(cudaMemsetAsync(out, 0, size_t(a->rows) * a->cols * 4, ctx->stream));
+  if (a->rows && a->nnz)
+    SK_LAUNCH(k_scatter_rows, grid_for(ctx, size_t(a->rows) * 32), 256, 0, ctx->stream, a->rp,
+              a->ci, a->v, a->rows, a->cols, out);
+}
+
 sk_csr* from_dense_impl(sk_ctx* ctx, const float* d, uint32_t rows, uint32_t cols) {
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(
       dalloc<uint64_t>(ctx, size_t(rows) + 1));

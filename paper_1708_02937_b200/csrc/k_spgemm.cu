@@ -602,6 +602,8 @@ struct EngineArgs {
   const ValueStats* wstats;        // per layer
   const ValueStats* y0stats;       // of Y0's values
   int exact_ok;                    // layer 0 windows are dense enough for the order-free path
+  unsigned long long stop_above;   // stop after a layer with more entries (0 = never)
+  int* layers_done;                // written when stopping early
 };
 
 __device__ __forceinline__ long long globaltimer() {
@@ -764,6 +766,12 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     in_wp = out_wp;
     last = cur;
     cur ^= 1;
+    // Density-adaptive hand-off: the activations became dense enough that the
+    // dense engine is faster; uniform decision (same grand in every block).
+    if (p.stop_above && grand > p.stop_above && grand <= p.cap && layer + 1 < p.L) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *p.layers_done = int(layer + 1);
+      break;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *p.result = (total_in == 0 && last != -2) ? -1 : last;
 }
@@ -923,54 +931,68 @@ sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, con
 
 // ---- the sparse-activation forward pass -----------------------------------------
 
-sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, float clip,
-                            uint64_t* nnz_trace) {
-  const uint32_t m = md->neurons, n = y0->cols, L = md->layers;
-  const WinGeom g = geometry(n);
-  const uint64_t items = uint64_t(m) * g.nW;
-  const uint64_t full = uint64_t(m) * n;
-
-  // Device arrays of per-layer weight pointers (cached on the model).
-  auto* mm = const_cast<sk_model*>(md);
-  if (!mm->d_wptr) {
-    std::vector<const void*> h(size_t(3) * L);
-    for (uint32_t k = 0; k < L; ++k) {
-      h[k] = md->w[k]->rp;
-      h[L + k] = md->w[k]->ci;
-      h[2 * L + k] = md->w[k]->v;
-    }
-    mm->d_wptr = dalloc<const void*>(ctx, h.size());
-    mm->d_bias_nonpos = dalloc<uint8_t>(ctx, L);
+// Device tables the persistent engines read (cached on the model): per-layer
+// weight pointers, "every bias <= 0" flags and weight value statistics.
+void ensure_model_tables(sk_ctx* ctx, sk_model* mm) {
+  const uint32_t L = mm->layers;
+  if (mm->d_wptr && mm->d_bias_nonpos && mm->d_wstats) return;
+  std::vector<const void*> h(size_t(3) * L);
+  for (uint32_t k = 0; k < L; ++k) {
+    h[k] = mm->w[k]->rp;
+    h[L + k] = mm->w[k]->ci;
+    h[2 * L + k] = mm->w[k]->v;
+  }
+  if (!mm->d_wptr) mm->d_wptr = dalloc<const void*>(ctx, std::max<size_t>(1, h.size()));
+  if (!mm->d_bias_nonpos) mm->d_bias_nonpos = dalloc<uint8_t>(ctx, std::max<uint32_t>(1, L));
+  if (!mm->d_wstats) mm->d_wstats = dalloc<ValueStats>(ctx, std::max<uint32_t>(1, L));
+  if (L) {
     SK_CUDA(cudaMemcpyAsync(mm->d_wptr, h.data(), h.size() * sizeof(void*),
                             cudaMemcpyHostToDevice, ctx->stream));
-    SK_CUDA(cudaMemcpyAsync(mm->d_bias_nonpos, md->bias_nonpos.data(), L,
+    SK_CUDA(cudaMemcpyAsync(mm->d_bias_nonpos, mm->bias_nonpos.data(), L,
                             cudaMemcpyHostToDevice, ctx->stream));
-    sync(ctx);
-  }
-
-  if (!mm->d_wstats) {  // per-layer weight statistics for the exactness test (cached)
-    mm->d_wstats = dalloc<ValueStats>(ctx, L);
     std::vector<ValueStats> init(L, ValueStats{INT_MAX, INT_MIN, 0, 0});
     SK_CUDA(cudaMemcpyAsync(mm->d_wstats, init.data(), L * sizeof(ValueStats),
                             cudaMemcpyHostToDevice, ctx->stream));
-    for (uint32_t k = 0; k < L; ++k) {
-      const sk_csr* w = md->w[k];
-      ValueStats* o = static_cast<ValueStats*>(mm->d_wstats) + k;
-      if (w->nnz)
-        SK_LAUNCH(k_value_stats, grid_warps(ctx, w->nnz / 32 + 1), 256, 0, ctx->stream, w->v,
-                  w->nnz, o);
-      SK_LAUNCH(k_max_row_len, grid_warps(ctx, w->rows / 32 + 1), 256, 0, ctx->stream, w->rp,
-                w->rows, o);
-    }
   }
+  for (uint32_t k = 0; k < L; ++k) {
+    const sk_csr* w = mm->w[k];
+    ValueStats* o = static_cast<ValueStats*>(mm->d_wstats) + k;
+    if (w->nnz)
+      SK_LAUNCH(k_value_stats, grid_warps(ctx, w->nnz / 32 + 1), 256, 0, ctx->stream, w->v,
+                w->nnz, o);
+    SK_LAUNCH(k_max_row_len, grid_warps(ctx, w->rows / 32 + 1), 256, 0, ctx->stream, w->rp,
+              w->rows, o);
+  }
+  std::vector<ValueStats> hs(L);
+  if (L)
+    SK_CUDA(cudaMemcpyAsync(hs.data(), mm->d_wstats, L * sizeof(ValueStats),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  mm->weights_finite = 1;
+  for (const ValueStats& v : hs)
+    if (v.nonfinite) mm->weights_finite = 0;
+}
+
+// One launch of the sparse engine over layers [k0, L): returns Y after the last
+// layer it ran (*done layers) and writes trace[0..*done] (trace[0] = y0->nnz).
+// With stop_above > 0 it stops after the first layer with more output entries.
+static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, uint32_t k0,
+                              float clip, unsigned long long stop_above,
+                              unsigned long long* trace_out, uint32_t* done) {
+  const uint32_t m = md->neurons, n = y0->cols, Lm = md->layers, L = Lm - k0;
+  const WinGeom g = geometry(n);
+  const uint64_t items = uint64_t(m) * g.nW;
+  const uint64_t full = uint64_t(m) * n;
+  auto* mm = const_cast<sk_model*>(md);
+
   // Layer-0 product count: the order-free path pays a shared-memory atomic per
   // product plus a full window sweep, which only wins when windows are dense.
   int exact_ok = 0;
   if (y0->nnz && L > 0) {
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
     SK_CUDA(cudaMemsetAsync(d, 0, 8, ctx->stream));
-    SK_LAUNCH(k_count_products, grid_warps(ctx, m), 256, 0, ctx->stream, md->w[0]->rp,
-              md->w[0]->ci, m, y0->rp, d);
+    SK_LAUNCH(k_count_products, grid_warps(ctx, m), 256, 0, ctx->stream, md->w[k0]->rp,
+              md->w[k0]->ci, m, y0->rp, d);
     unsigned long long prods = 0;
     SK_CUDA(cudaMemcpyAsync(&prods, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
@@ -995,6 +1017,8 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
     return std::max<unsigned long long>(c, 1);
   };
   unsigned long long cap = clamp_cap(std::max<unsigned long long>(4ull * y0->nnz, 1ull << 24));
+  // An early stop must leave a complete CSR, so the capacity covers the threshold.
+  if (stop_above) cap = clamp_cap(std::max<unsigned long long>(cap, 2 * stop_above));
 
   static bool attr = false;
   if (!attr) {
@@ -1015,16 +1039,16 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   unsigned long long* trace_d = small;
   unsigned long long* bump = small + L + 1;
   unsigned long long* block_sums = bump + L;
-  int* flags = reinterpret_cast<int*>(block_sums + grid);  // [0] overflow, [1] result
+  int* flags = reinterpret_cast<int*>(block_sums + grid);  // [0] overflow, [1] result, [2] done
 
   for (int attempt = 0; attempt < 2; ++attempt) {
     SK_CUDA(cudaMemsetAsync(small, 0, nsmall * 8, ctx->stream));
     EngineArgs p;
-    p.w_rp = reinterpret_cast<const uint32_t* const*>(mm->d_wptr);
-    p.w_ci = reinterpret_cast<const uint32_t* const*>(mm->d_wptr + L);
-    p.w_v = reinterpret_cast<const float* const*>(mm->d_wptr + 2 * L);
-    p.bias = md->bias;
-    p.bias_nonpos = mm->d_bias_nonpos;
+    p.w_rp = reinterpret_cast<const uint32_t* const*>(mm->d_wptr) + k0;
+    p.w_ci = reinterpret_cast<const uint32_t* const*>(mm->d_wptr + Lm) + k0;
+    p.w_v = reinterpret_cast<const float* const*>(mm->d_wptr + 2 * Lm) + k0;
+    p.bias = md->bias + size_t(k0) * m;
+    p.bias_nonpos = mm->d_bias_nonpos + k0;
     p.m = m;
     p.n = n;
     p.L = L;
@@ -1051,10 +1075,12 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
     p.result = flags + 1;
     p.overflow = flags;
     p.err = ctx->d_err;
-    p.stamps = ctx->stamps;
-    p.wstats = static_cast<const ValueStats*>(mm->d_wstats);
+    p.stamps = (ctx->stamps && k0 + L < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
+    p.wstats = static_cast<const ValueStats*>(mm->d_wstats) + k0;
     p.y0stats = y0stats;
     p.exact_ok = exact_ok;
+    p.stop_above = stop_above;
+    p.layers_done = flags + 2;
     void* args[] = {&p};
     timing_mark(ctx);
     SK_CUDA(cudaLaunchCooperativeKernel((void*)k_sparse_engine, dim3(grid), dim3(kWarps * 32),
@@ -1063,8 +1089,8 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
     timing_mark(ctx);
 
     std::vector<unsigned long long> trace(size_t(L) + 1);
-    int hflags[2] = {0, 0};
-    SK_CUDA(cudaMemcpyAsync(hflags, flags, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    int hflags[3] = {0, 0, 0};
+    SK_CUDA(cudaMemcpyAsync(hflags, flags, 12, cudaMemcpyDeviceToHost, ctx->stream));
     SK_CUDA(cudaMemcpyAsync(trace.data(), trace_d, trace.size() * 8, cudaMemcpyDeviceToHost,
                             ctx->stream));
     sync(ctx);
@@ -1079,9 +1105,10 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
       dfree(ctx, p.sc_c);
       dfree(ctx, p.sc_v);
     };
+    const uint32_t ran = hflags[2] ? uint32_t(hflags[2]) : L;
     if (!hflags[0]) {
       const int res = hflags[1];
-      const unsigned long long nnz = trace[L];
+      const unsigned long long nnz = trace[ran];
       sk_csr* o = new sk_csr;
       o->ctx = ctx;
       o->rows = m;
@@ -1103,8 +1130,8 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
         SK_CUDA(cudaMemcpyAsync(o->v, src_v, size_t(nnz) * 4, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
       }
-      if (nnz_trace)
-        for (uint32_t k = 0; k <= L; ++k) nnz_trace[k] = trace[k];
+      for (uint32_t k = 0; k <= ran; ++k) trace_out[k] = trace[k];
+      *done = ran;
       release();
       dfree(ctx, wp0);
       dfree(ctx, small);
@@ -1120,6 +1147,96 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   dfree(ctx, small);
   dfree(ctx, y0stats);
   fail(SK_ERR_OOM, "sparse forward: activation nnz exceeds the device capacity");
+}
+
+// The sparse-activation forward pass, density-adaptive.  Both engines compute
+// every output as the same ascending fold; the dense one also folds the w * 0
+// terms of absent activations, which leave the sum unchanged bit for bit when
+// every weight is finite (acc is never -0: it starts at +0 and x + y = -0 in
+// round-to-nearest only when both are -0).  So with finite weights the
+// representation can follow the activation density: sparse engine while
+// nnz <= dense_above * m * n, dense engine (K1) above it, back to sparse below
+// sparse_below * m * n.  Non-finite weights, tiny batches or too little memory
+// for two dense buffers keep the whole pass on the sparse engine.
+sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, float clip,
+                            uint64_t* nnz_trace) {
+  const uint32_t m = md->neurons, n = y0->cols, L = md->layers;
+  const uint64_t full = uint64_t(m) * n;
+  auto* mm = const_cast<sk_model*>(md);
+  ensure_model_tables(ctx, mm);
+
+  unsigned long long hi = 0, lo = 0;
+  if (ctx->dense_above > 0 && mm->weights_finite == 1 && L > 0) {
+    size_t free_b = 0, total_b = 0;
+    SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    // two dense buffers + a worst-case CSR of the dense result
+    if (double(full) * 16.0 < 0.7 * double(free_b) && full <= 0xFFFFFFFFull) {
+      hi = std::max<unsigned long long>(1, (unsigned long long)(ctx->dense_above * double(full)));
+      lo = (unsigned long long)(ctx->sparse_below * double(full));
+      lo = std::min(lo, hi);
+    }
+  }
+
+  std::vector<unsigned long long> trace(size_t(L) + 1, 0);
+  trace[0] = y0->nnz;
+  const sk_csr* cur = y0;
+  sk_csr* owned = nullptr;
+  float* dbuf[2] = {nullptr, nullptr};
+  unsigned long long* counts = nullptr;
+  uint32_t k = 0;
+  auto cleanup = [&] {
+    for (float* b : dbuf)
+      if (b) dfree(ctx, b);
+    if (counts) dfree(ctx, counts);
+  };
+  try {
+    for (;;) {
+      if (!(hi && k < L && cur->nnz > hi)) {
+        uint32_t done = 0;
+        sk_csr* r = sparse_segment(ctx, md, cur, k, clip, hi, trace.data() + k, &done);
+        if (owned) csr_release(owned);
+        owned = r;
+        cur = r;
+        k += done;
+        if (k >= L) break;
+      }
+      // dense segment from layer k: Y_k is scattered into buffer 1, layer k
+      // writes buffer 0, and the engine ping-pongs from there
+      if (!dbuf[0]) {
+        dbuf[0] = dalloc<float>(ctx, full);
+        dbuf[1] = dalloc<float>(ctx, full);
+        counts = reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, size_t(L) + 1));
+      }
+      csr_scatter_dense(ctx, cur, dbuf[1]);
+      if (owned) {
+        csr_release(owned);
+        owned = nullptr;
+      }
+      cur = nullptr;
+      int* d_done = reinterpret_cast<int*>(counts + L);
+      SK_CUDA(cudaMemsetAsync(counts, 0, (size_t(L) + 1) * 8, ctx->stream));
+      dense_forward_engine(ctx, md, k, dbuf[1], n, clip, dbuf[0], dbuf[1], counts, lo, d_done);
+      std::vector<unsigned long long> hc(size_t(L) + 1);
+      SK_CUDA(cudaMemcpyAsync(hc.data(), counts, hc.size() * 8, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      sync(ctx);
+      const int dflag = int(hc[L] & 0xFFFFFFFFull);
+      const uint32_t done = dflag ? uint32_t(dflag) : L - k;
+      for (uint32_t j = 0; j < done; ++j) trace[k + 1 + j] = hc[j];
+      owned = from_dense_impl(ctx, dbuf[(done - 1) & 1], m, n);
+      cur = owned;
+      k += done;
+      if (k >= L) break;
+    }
+  } catch (...) {
+    cleanup();
+    if (owned) csr_release(owned);
+    throw;
+  }
+  cleanup();
+  if (nnz_trace)
+    for (uint32_t q = 0; q <= L; ++q) nnz_trace[q] = trace[q];
+  return owned;
 }
 
 }  // namespace sk

@@ -29,8 +29,10 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
                                            const float* __restrict__ wv,
                                            const float* __restrict__ bias,
                                            const float* __restrict__ y, uint32_t m, uint32_t n,
-                                           float clip, float* __restrict__ out, int* err) {
+                                           float clip, float* __restrict__ out, int* err,
+                                           unsigned long long* nz_count = nullptr) {
   const int lane = threadIdx.x & 31;
+  uint32_t nz = 0;  // nonzero outputs written by this lane (only when nz_count)
   const uint32_t chunks = (n + 127) / 128;
   const uint64_t tasks = uint64_t(chunks) * m;
   for (uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; task < tasks;
@@ -76,6 +78,12 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
       acc2 = layer_epilogue(acc2, b, clip);
       acc3 = layer_epilogue(acc3, b, clip);
     }
+    if (nz_count) {
+      if (col0 + 0 < n) nz += acc0 != 0.0f;
+      if (col0 + 1 < n) nz += acc1 != 0.0f;
+      if (col0 + 2 < n) nz += acc2 != 0.0f;
+      if (col0 + 3 < n) nz += acc3 != 0.0f;
+    }
     float* orow = out + size_t(i) * n;
     if (kVec4) {
       if (col0 < n) *reinterpret_cast<float4*>(orow + col0) = make_float4(acc0, acc1, acc2, acc3);
@@ -85,6 +93,11 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
       if (col0 + 2 < n) orow[col0 + 2] = acc2;
       if (col0 + 3 < n) orow[col0 + 3] = acc3;
     }
+  }
+  if (nz_count) {  // warp-uniform: nz_count is a kernel argument
+#pragma unroll
+    for (int o = 16; o; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    if (lane == 0 && nz) atomicAdd(nz_count, (unsigned long long)nz);
   }
 }
 
@@ -101,6 +114,11 @@ __global__ void __launch_bounds__(256)
 // layer is the K1 task loop, layers are separated by a grid barrier (every
 // output column of layer k+1 needs the whole of Y_k).  Removes the per-layer
 // launch latency that dominates small models (BASELINE cfg1).
+//
+// Density-adaptive mode (nnz != nullptr): every layer also counts its nonzero
+// outputs; when a layer's count drops below stop_below the engine stops after
+// that layer (every block reads the same count after the barrier, so the
+// decision is uniform) and the host continues on the sparse engine.
 struct DenseEngineArgs {
   const uint32_t* const* w_rp;
   const uint32_t* const* w_ci;
@@ -111,6 +129,9 @@ struct DenseEngineArgs {
   const float* y0;
   float* buf[2];
   int* err;
+  unsigned long long* nnz;         // L counters, zeroed (optional)
+  unsigned long long stop_below;   // 0 = never stop early
+  int* layers_done;                // written when stopping early
 };
 
 template <bool kVec4>
@@ -120,8 +141,15 @@ __global__ void __launch_bounds__(256) k_dense_engine(DenseEngineArgs p) {
     const float* src = k == 0 ? p.y0 : p.buf[(k - 1) & 1];
     float* dst = p.buf[k & 1];
     spmm_tasks<OpArith, kEpiLayer, kVec4>(p.w_rp[k], p.w_ci[k], p.w_v[k], p.bias + size_t(k) * p.m,
-                                          src, p.m, p.n, p.clip, dst, p.err);
-    if (k + 1 < p.L) grid.sync();
+                                          src, p.m, p.n, p.clip, dst, p.err,
+                                          p.nnz ? p.nnz + k : nullptr);
+    if (k + 1 < p.L) {
+      grid.sync();
+      if (p.stop_below && *(volatile unsigned long long*)(p.nnz + k) < p.stop_below) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *p.layers_done = int(k + 1);
+        return;
+      }
+    }
   }
 }
 
@@ -131,36 +159,32 @@ static unsigned spmm_grid(sk_ctx* ctx, uint32_t m, uint32_t n) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(blocks, uint64_t(ctx->num_sms) * 16)));
 }
 
-// Dense forward over all layers of a model: returns the buffer holding Y_L.
-void dense_forward_engine(sk_ctx* ctx, const sk_model* md, const float* y0, uint32_t n,
-                          float clip, float* buf0, float* buf1) {
+// Dense forward over layers [k0, L) of a model (layer k0 + j writes buffer j & 1).
+// With nnz != nullptr (L - k0 zeroed device counters) each layer's nonzero count
+// is recorded and the engine stops after the first layer whose count is below
+// stop_below (> 0); *d_done (device) then holds the number of layers run.
+void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const float* y0,
+                          uint32_t n, float clip, float* buf0, float* buf1,
+                          unsigned long long* nnz, unsigned long long stop_below, int* d_done) {
   auto* mm = const_cast<sk_model*>(md);
   const uint32_t L = md->layers, m = md->neurons;
-  if (!mm->d_wptr) {
-    std::vector<const void*> h(size_t(3) * L);
-    for (uint32_t k = 0; k < L; ++k) {
-      h[k] = md->w[k]->rp;
-      h[L + k] = md->w[k]->ci;
-      h[2 * L + k] = md->w[k]->v;
-    }
-    mm->d_wptr = dalloc<const void*>(ctx, h.size());
-    SK_CUDA(cudaMemcpyAsync(mm->d_wptr, h.data(), h.size() * sizeof(void*),
-                            cudaMemcpyHostToDevice, ctx->stream));
-    sync(ctx);
-  }
+  ensure_model_tables(ctx, mm);
   DenseEngineArgs p;
-  p.w_rp = reinterpret_cast<const uint32_t* const*>(mm->d_wptr);
-  p.w_ci = reinterpret_cast<const uint32_t* const*>(mm->d_wptr + L);
-  p.w_v = reinterpret_cast<const float* const*>(mm->d_wptr + 2 * L);
-  p.bias = md->bias;
+  p.w_rp = reinterpret_cast<const uint32_t* const*>(mm->d_wptr) + k0;
+  p.w_ci = reinterpret_cast<const uint32_t* const*>(mm->d_wptr + L) + k0;
+  p.w_v = reinterpret_cast<const float* const*>(mm->d_wptr + 2 * L) + k0;
+  p.bias = md->bias + size_t(k0) * m;
   p.m = m;
   p.n = n;
-  p.L = L;
+  p.L = L - k0;
   p.clip = clip;
   p.y0 = y0;
   p.buf[0] = buf0;
   p.buf[1] = buf1;
   p.err = ctx->d_err;
+  p.nnz = nnz;
+  p.stop_below = nnz ? stop_below : 0;
+  p.layers_done = d_done;
   const bool vec = (n % 4) == 0;
   const void* fn = vec ? (const void*)k_dense_engine<true> : (const void*)k_dense_engine<false>;
   int per_sm = 0;

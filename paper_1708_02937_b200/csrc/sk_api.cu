@@ -189,6 +189,17 @@ extern "C" sk_status sk_ctx_set_stream(sk_ctx* ctx, void* s) {
 
 extern "C" void* sk_ctx_stream(const sk_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 
+extern "C" sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above,
+                                               double sparse_below) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!(sparse_below >= 0.0) || (dense_above > 0 && sparse_below > dense_above))
+      fail(SK_ERR_INVALID_ARGUMENT, "density switch needs 0 <= sparse_below <= dense_above");
+    ctx->dense_above = dense_above > 0 ? dense_above : 0.0;
+    ctx->sparse_below = sparse_below;
+  });
+}
+
 extern "C" sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable) {
   return guarded([&] {
     require_ctx(ctx);
@@ -460,7 +471,7 @@ static sk_dense* forward_dense(sk_ctx* ctx, const sk_model* m, const sk_dense* y
   sk_dense* a = new_dense(ctx, m->neurons, n);
   sk_dense* b = m->layers > 1 ? new_dense(ctx, m->neurons, n) : nullptr;
   // one persistent launch for all layers; layer k writes buffer k & 1
-  dense_forward_engine(ctx, m, y0->d, n, clip, a->d, b ? b->d : nullptr);
+  dense_forward_engine(ctx, m, 0, y0->d, n, clip, a->d, b ? b->d : nullptr);
   sk_dense* result = ((m->layers - 1) & 1) ? b : a;
   sk_dense* spare = (result == a) ? b : a;
   if (spare) sk_dense_free(spare);

@@ -103,6 +103,11 @@ struct sk_ctx {
   // Optional per-layer %globaltimer stamps written by the sparse engine.
   long long* stamps = nullptr;
   uint32_t stamps_cap = 0;
+  // Density-adaptive sparse forward: switch to the dense engine when a layer's
+  // output has more than dense_above * m * n entries, back to the sparse engine
+  // below sparse_below * m * n (sk_ctx_set_density_switch; dense_above <= 0 = off).
+  double dense_above = 1.0 / 32;
+  double sparse_below = 1.0 / 128;
 };
 
 struct sk_dense {
@@ -132,6 +137,7 @@ struct sk_model {
   const void** d_wptr = nullptr;     // device [rp[L], ci[L], v[L]] for the engine
   void* d_wstats = nullptr;          // device per-layer value statistics (exactness test)
   uint8_t* d_bias_nonpos = nullptr;
+  int weights_finite = -1;           // every weight finite (-1 = not computed yet)
 };
 
 namespace sk {
@@ -239,8 +245,13 @@ sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                                 const float* d_v, size_t n,
                                 const uint32_t* h_r, const uint32_t* h_c);
 sk_csr* csr_transpose(sk_ctx* ctx, const sk_csr* a);
-void dense_forward_engine(sk_ctx* ctx, const sk_model* md, const float* y0, uint32_t n,
-                          float clip, float* buf0, float* buf1);
+void ensure_model_tables(sk_ctx* ctx, sk_model* md);
+void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const float* y0,
+                          uint32_t n, float clip, float* buf0, float* buf1,
+                          unsigned long long* nnz = nullptr, unsigned long long stop_below = 0,
+                          int* d_done = nullptr);
+sk_csr* from_dense_impl(sk_ctx* ctx, const float* d, uint32_t rows, uint32_t cols);
+void csr_scatter_dense(sk_ctx* ctx, const sk_csr* a, float* out);
 void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias,
                         const float* y, uint32_t n, float clip, float* out);
 void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b,

@@ -167,6 +167,12 @@ class Context:
         _check(self._L.sk_ctx_layer_stamps(self.h, buf.ctypes.data_as(C.POINTER(C.c_longlong)), n))
         return buf
 
+    def set_density_switch(self, dense_above: float = 1.0 / 32, sparse_below: float = 1.0 / 128):
+        """Activation density (fraction of m*n) above which relu_forward_sparse
+        continues on the dense engine, and below which it returns to the sparse
+        one.  dense_above <= 0 keeps the whole pass sparse.  Bitwise neutral."""
+        _check(self._L.sk_ctx_set_density_switch(self.h, float(dense_above), float(sparse_below)))
+
     def set_stream(self, stream_ptr: int | None):
         _check(self._L.sk_ctx_set_stream(self.h, vp(stream_ptr) if stream_ptr else None))
 

@@ -354,6 +354,86 @@ def test_sparse_forward_bitwise_vs_oracle(sk, port, m, n, kY, kW, value, bias, c
     assert_csr_bitwise(out, y)
 
 
+def _rise_and_fall(port, sk):
+    """A network whose activation density rises (positive bias) then decays
+    (negative bias), so the density-adaptive forward switches both ways."""
+    m, n, seed = 2048, 520, 23
+    hW = [port.gen_layer_fixed(m, 16, port.layer_seed(seed, k), float("nan")) for k in range(6)]
+    bs = [np.full(m, b, np.float32) for b in (0.01, -0.2, -0.6, -0.9, -0.9, -0.9)]
+    hY = port.gen_input_binary(m, n, 20, seed)
+    want, trace = hY, [hY.nnz]
+    for k in range(6):
+        want = port.layer_sparse(hW[k], bs[k], want, 0.0)
+        trace.append(want.nnz)
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], bs)
+    return model, dev_csr(sk, hY), want, trace, m * n
+
+
+@pytest.mark.parametrize("mode", ["sparse_only", "default", "all_dense", "dense_after_first",
+                                  "pingpong"])
+def test_density_switch_is_bitwise_neutral(sk, port, mode):
+    model, y0, want, want_trace, full = _rise_and_fall(port, sk)
+    dens = np.array(want_trace[1:-1], np.float64) / full
+    ctx = sk.default_context()
+    try:
+        if mode == "sparse_only":
+            ctx.set_density_switch(0.0, 0.0)
+        elif mode == "all_dense":  # Y0 itself is above the threshold
+            ctx.set_density_switch(1e-9, 0.0)
+        elif mode == "dense_after_first":  # Y0 (1%) sparse, layer 0 output dense
+            ctx.set_density_switch(want_trace[0] / full * 2, 0.0)
+        elif mode == "pingpong":
+            t = float(np.sqrt(dens.max() * max(dens.min(), 1e-9)))
+            ctx.set_density_switch(t, t)
+        ctx.set_timing(True)
+        ctx.kernel_times_ms()
+        out, trace = sk.relu_forward_sparse(model, y0)
+        segments = len(ctx.kernel_times_ms())
+    finally:
+        ctx.set_timing(False)
+        ctx.set_density_switch()
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, want)
+    if mode in ("sparse_only", "all_dense"):
+        assert segments == 1
+    if mode == "dense_after_first":
+        assert segments == 2
+    if mode == "pingpong":
+        assert segments >= 3  # sparse -> dense -> sparse
+
+
+def test_density_switch_not_taken_with_nonfinite_weights(sk, port):
+    # w * 0 = NaN for w = inf: the dense engine would differ, so the pass stays sparse
+    m, n = 1024, 300
+    W = port.gen_layer_fixed(m, 16, 9, 0.25)
+    W.values[::97] = np.inf
+    b = np.full(m, 0.01, np.float32)  # positive bias densifies
+    Y = port.gen_input_binary(m, n, 300, 9)
+    model = sk.DnnModel([dev_csr(sk, W)] * 3, [b] * 3)
+    ctx = sk.default_context()
+    ctx.set_density_switch(1e-9, 0.0)
+    try:
+        out, _ = sk.relu_forward_sparse(model, dev_csr(sk, Y))
+    finally:
+        ctx.set_density_switch()
+    want = Y
+    for _ in range(3):
+        want = port.layer_sparse(W, b, want, 0.0)
+    g = host_csr(out)
+    assert np.array_equal(g.row_ptr, want.row_ptr) and np.array_equal(g.col_idx, want.col_idx)
+    assert same_bits_nan(g.values, want.values)
+
+
+def test_density_switch_argument_checks(sk):
+    from paper_1708_02937_b200.semikern import InvalidArgument
+    ctx = sk.default_context()
+    with pytest.raises(InvalidArgument):
+        ctx.set_density_switch(0.01, 0.5)
+    with pytest.raises(InvalidArgument):
+        ctx.set_density_switch(0.01, -1.0)
+    ctx.set_density_switch()
+
+
 def test_sparse_forward_empty_and_tiny_inputs(sk, port):
     m = 512
     W = sk.gen_layer_fixed(m, 8, 3, 0.5)
