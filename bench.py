@@ -83,7 +83,18 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
-        time.sleep(0.25)
+        # nvidia-smi's start-up (NVML init) takes driver locks that stall CUDA
+        # API calls: wait for its first sample so that never lands in the timed
+        # region.
+        t0 = time.time()
+        while self.proc and time.time() - t0 < 10:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                pass
+            time.sleep(0.05)
+        time.sleep(0.1)
         return self
 
     def __exit__(self, *a):

@@ -148,7 +148,7 @@ __device__ __forceinline__ unsigned long long reserve(const RowArgs& p, uint64_t
 // flattened (ascending k, ascending sample) order, then applied 32 at a time;
 // products of one step that hit the same sample are applied in rounds by rank,
 // i.e. lane order = ascending k.
-template <typename Ops, bool kExact>
+template <typename Ops>
 __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws, int lane,
                                            uint32_t wbase, float a, uint32_t beg, uint32_t cnt,
                                            uint32_t& T, bool& any) {
@@ -185,15 +185,6 @@ __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws,
     __syncwarp();
     // ---- application, 32 staged products per step
     const uint32_t nb = min(kStage, total - base);
-    if (kExact) {
-      // Every partial sum of this layer is exactly representable (proved from
-      // the operands' granularity and magnitude), so the order of the adds
-      // cannot change a single bit: shared-memory atomics, no ordering rounds.
-      for (uint32_t j = lane; j < nb; j += 32)
-        atomicAdd(reinterpret_cast<float*>(ws.acc) + ws.st_s[j], ws.st_p[j]);
-      __syncwarp();
-      continue;
-    }
     for (uint32_t t = 0; t < nb; t += 32) {
       const uint32_t j = t + lane;
       const bool act = j < nb;
@@ -225,6 +216,99 @@ __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws,
   }
 }
 
+// Exact mode: every partial sum of the layer is exactly representable (proved
+// from the operands' granularity and magnitude), so the order of the adds
+// cannot change a single bit.  Each lane applies its own slice directly:
+// shared-memory float atomics into the zero-initialised accumulator plus a
+// touched bitmap (ws.surv) that the epilogue walks instead of the whole window.
+__device__ __forceinline__ void fold_chunk_exact(const RowArgs& p, const WarpSmem& ws,
+                                                 uint32_t wbase, float a, uint32_t beg,
+                                                 uint32_t cnt, bool& any) {
+  if (!__any_sync(0xffffffffu, cnt != 0)) return;
+  any = true;
+  float* acc = reinterpret_cast<float*>(ws.acc);
+  const uint32_t end = beg + cnt;
+  uint32_t e = beg;
+  for (; e + 4 <= end; e += 4) {
+    uint32_t c[4];
+    float y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[u] = __ldg(p.bci + e + u);
+      y[u] = __ldg(p.bv + e + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t sl = c[u] - wbase;
+      atomicAdd(acc + sl, __fmul_rn(a, y[u]));
+      atomicOr(ws.surv + (sl >> 5), 1u << (sl & 31));
+    }
+  }
+  for (; e < end; ++e) {
+    const uint32_t sl = __ldg(p.bci + e) - wbase;
+    atomicAdd(acc + sl, __fmul_rn(a, __ldg(p.bv + e)));
+    atomicOr(ws.surv + (sl >> 5), 1u << (sl & 31));
+  }
+  // lanes finish their slices at different times: every update must land before
+  // any lane reads the bitmap in the epilogue
+  __syncwarp();
+}
+
+// Exact-mode epilogue over the touched bitmap.  An untouched position and a
+// touched one whose exact sum is +0 give the same z = epilogue(0 + b) (the
+// accumulator is never -0: it starts at +0 and x + y = -0 only for -0 + -0), so
+// only touched positions can survive when epilogue(0 + b) == 0.  Lanes own
+// contiguous word ranges, so survivors are emitted in sample order.
+template <bool kLayer>
+__device__ __forceinline__ void emit_window_exact(const RowArgs& p, const WarpSmem& ws, int lane,
+                                                  uint64_t it, uint32_t wlen, uint32_t wbase,
+                                                  float b) {
+  const uint32_t nwords = (wlen + 31) >> 5;
+  const uint32_t per = (nwords + 31) >> 5;
+  const uint32_t w0 = min(nwords, lane * per), w1 = min(nwords, w0 + per);
+  uint32_t mine = 0;
+  for (uint32_t q = w0; q < w1; ++q) {
+    uint32_t t = ws.surv[q], keepw = 0;
+    while (t) {
+      const uint32_t bt = __ffs(t) - 1;
+      t &= t - 1;
+      const uint32_t sl = q * 32 + bt;
+      const float x = __uint_as_float(ws.acc[sl]);
+      const float z = kLayer ? layer_epilogue(x, b, p.clip) : x;
+      if (!kLayer || z != 0.0f) {
+        keepw |= 1u << bt;
+        ws.acc[sl] = __float_as_uint(z);
+      } else {
+        ws.acc[sl] = 0u;
+      }
+    }
+    ws.surv[q] = keepw;
+    mine += __popc(keepw);
+  }
+  const uint32_t incl = warp_incl_scan(mine, lane);
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  bool can_write;
+  const unsigned long long off = reserve(p, it, tot, lane, can_write);
+  unsigned long long pos = off + (incl - mine);
+  for (uint32_t q = w0; q < w1; ++q) {
+    uint32_t t = ws.surv[q];
+    if (!t) continue;
+    ws.surv[q] = 0;
+    while (t) {
+      const uint32_t bt = __ffs(t) - 1;
+      t &= t - 1;
+      const uint32_t sl = q * 32 + bt;
+      if (can_write) {
+        p.sc_c[pos] = wbase + sl;
+        p.sc_v[pos] = __uint_as_float(ws.acc[sl]);
+      }
+      ws.acc[sl] = 0u;
+      ++pos;
+    }
+  }
+  __syncwarp();
+}
+
 // Epilogue of one (row, window): emit the row's window slice of the output.
 template <bool kLayer, bool kExact>
 __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws, int lane,
@@ -233,6 +317,10 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
   const uint32_t cap = list_cap(1u << p.sh);
   if (!any && !dense_row) {
     if (lane == 0) p.item_cnt[it] = 0;
+    return;
+  }
+  if (kExact && !dense_row) {
+    emit_window_exact<kLayer>(p, ws, lane, it, wlen, wbase, b);
     return;
   }
   if (!kExact && !dense_row && T <= cap) {
@@ -348,6 +436,8 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
     pos += ctot;
     *slot = make_uint4(reset, reset, reset, reset);
   }
+  if (kExact)
+    for (uint32_t q = lane; q < ((wlen + 31) >> 5); q += 32) ws.surv[q] = 0;
   __syncwarp();
 }
 
@@ -409,7 +499,10 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
         beg = wk[0];
         cnt = wk[1] - beg;
       }
-      fold_chunk<Ops, kExact>(p, ws, lane, wbase, aa, beg, cnt, T, any);
+      if (kExact)
+        fold_chunk_exact(p, ws, wbase, aa, beg, cnt, any);
+      else
+        fold_chunk<Ops>(p, ws, lane, wbase, aa, beg, cnt, T, any);
     }
     emit_window<kLayer, kExact>(p, ws, lane, uint64_t(i) * p.nW + w, wbase, min(S, p.n - wbase), any, T,
                         b, zu, dense_row);
@@ -601,7 +694,7 @@ struct EngineArgs {
   long long* stamps;               // optional %globaltimer per layer end (L+1)
   const ValueStats* wstats;        // per layer
   const ValueStats* y0stats;       // of Y0's values
-  int exact_ok;                    // layer 0 windows are dense enough for the order-free path
+  int exact_ok;                    // layer 0 may use the order-free path (SK_NO_EXACT unset)
   unsigned long long stop_above;   // stop after a layer with more entries (0 = never)
   int* layers_done;                // written when stopping early
 };
@@ -985,19 +1078,11 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
   const uint64_t full = uint64_t(m) * n;
   auto* mm = const_cast<sk_model*>(md);
 
-  // Layer-0 product count: the order-free path pays a shared-memory atomic per
-  // product plus a full window sweep, which only wins when windows are dense.
-  int exact_ok = 0;
-  if (y0->nnz && L > 0) {
-    unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
-    SK_CUDA(cudaMemsetAsync(d, 0, 8, ctx->stream));
-    SK_LAUNCH(k_count_products, grid_warps(ctx, m), 256, 0, ctx->stream, md->w[k0]->rp,
-              md->w[k0]->ci, m, y0->rp, d);
-    unsigned long long prods = 0;
-    SK_CUDA(cudaMemcpyAsync(&prods, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    sync(ctx);
-    exact_ok = prods >= uint64_t(m) * g.nW * (g.S / 4);
-  }
+  // Layer 0 may take the order-free path when its products are provably exact
+  // (decided on the device from the value statistics); SK_NO_EXACT=1 disables
+  // it for A/B measurements.
+  static const int exact_env = getenv("SK_NO_EXACT") ? 0 : 1;
+  const int exact_ok = exact_env;
   ValueStats* y0stats = dalloc<ValueStats>(ctx, 1);
   {
     const ValueStats init{INT_MAX, INT_MIN, 0, 0};
@@ -1007,9 +1092,9 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
                 y0->nnz, y0stats);
   }
 
-  size_t free_b = 0, total_b = 0;
-  SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const unsigned long long mem_cap = (unsigned long long)(free_b * 0.6 / 24.0);
+  // Scratch capacity: the first attempt is bounded by the device size; only the
+  // overflow retry asks the driver for the free memory.
+  unsigned long long mem_cap = (unsigned long long)(ctx->total_mem * 0.3 / 24.0);
   auto clamp_cap = [&](unsigned long long c) {
     c = std::min<unsigned long long>(c, full);
     c = std::min<unsigned long long>(c, mem_cap);
@@ -1139,6 +1224,11 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
       return o;
     }
     release();
+    {
+      size_t free_b = 0, total_b = 0;
+      SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      mem_cap = (unsigned long long)(free_b * 0.6 / 24.0);
+    }
     const unsigned long long bigger = clamp_cap(full);
     if (bigger <= cap) break;
     cap = bigger;  // retry once with the largest capacity memory allows
@@ -1166,16 +1256,20 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   ensure_model_tables(ctx, mm);
 
   unsigned long long hi = 0, lo = 0;
-  if (ctx->dense_above > 0 && mm->weights_finite == 1 && L > 0) {
+  if (ctx->dense_above > 0 && mm->weights_finite == 1 && L > 0 && full <= 0xFFFFFFFFull &&
+      double(full) * 16.0 < 0.7 * double(ctx->total_mem)) {
+    hi = std::max<unsigned long long>(1, (unsigned long long)(ctx->dense_above * double(full)));
+    lo = (unsigned long long)(ctx->sparse_below * double(full));
+    lo = std::min(lo, hi);
+  }
+  // The free memory is checked when a switch is actually about to happen: two
+  // dense buffers + a worst-case CSR of the dense result.  Without it the pass
+  // simply stays sparse.
+  auto dense_fits = [&] {
     size_t free_b = 0, total_b = 0;
     SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    // two dense buffers + a worst-case CSR of the dense result
-    if (double(full) * 16.0 < 0.7 * double(free_b) && full <= 0xFFFFFFFFull) {
-      hi = std::max<unsigned long long>(1, (unsigned long long)(ctx->dense_above * double(full)));
-      lo = (unsigned long long)(ctx->sparse_below * double(full));
-      lo = std::min(lo, hi);
-    }
-  }
+    return double(full) * 16.0 < 0.7 * double(free_b);
+  };
 
   std::vector<unsigned long long> trace(size_t(L) + 1, 0);
   trace[0] = y0->nnz;
@@ -1202,6 +1296,10 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
       }
       // dense segment from layer k: Y_k is scattered into buffer 1, layer k
       // writes buffer 0, and the engine ping-pongs from there
+      if (!dbuf[0] && !dense_fits()) {
+        hi = 0;  // stay sparse for the rest of the pass
+        continue;
+      }
       if (!dbuf[0]) {
         dbuf[0] = dalloc<float>(ctx, full);
         dbuf[1] = dalloc<float>(ctx, full);

@@ -152,6 +152,11 @@ extern "C" sk_status sk_ctx_create(int device, sk_ctx** out) {
     SK_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     SK_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    {
+      size_t fr = 0, tot = 0;
+      SK_CUDA(cudaMemGetInfo(&fr, &tot));
+      c->total_mem = tot;
+    }
     cudaMemPool_t pool;
     SK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thresh = UINT64_MAX;

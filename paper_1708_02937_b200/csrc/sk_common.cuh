@@ -92,6 +92,8 @@ struct sk_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   int num_sms = 148;
+  size_t total_mem = 0;      // device memory size (queried once: cudaMemGetInfo takes a
+                             // driver lock, so hot paths only call it when they must)
   int* d_err = nullptr;      // device error word (0 = ok)
   uint64_t* d_u64 = nullptr; // small device scratch for counters/flags (64 slots)
   uint64_t* h_u64 = nullptr; // pinned mirror of d_u64
