@@ -121,6 +121,7 @@ struct RowArgs {
   unsigned long long cap;
   int* overflow;
   int* err;
+  float fx_scale, fx_unscale;  // exact mode: 2^-gran and 2^gran (fixed-point accumulation)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
@@ -509,14 +510,185 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
   }
 }
 
+// Exact mode, fixed point.  Every product and partial sum is a multiple of
+// 2^gran below 2^24 * 2^gran in magnitude (products_exact), so q = p * 2^-gran
+// is an exact int32 and any order of integer adds gives the exact sum; the float
+// ascending fold of the reference equals it bit for bit (acc * 2^gran, +0 for
+// 0).  Integer shared atomics are native (float ones are a CAS loop).  The
+// products of one (row, window) are distributed flat over the warp: product j
+// belongs to the last lane whose exclusive scan offset is <= j.
+template <bool kLayer>
+__device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
+                                   int lane) {
+  const uint32_t S = 1u << p.sh;
+  const uint32_t w0 = g * kGroup;
+  const uint32_t wn = min(kGroup, p.nW - w0);
+  const uint32_t eb = p.arp[i], ee = p.arp[i + 1];
+  const uint32_t deg = ee - eb;
+  float b = 0.0f;
+  if (kLayer) b = p.bias[i];
+  int* const acc = reinterpret_cast<int*>(ws.acc);
+  const uint32_t nchunks = p.b_empty ? 0u : (deg + 31) / 32;
+  // first chunk's in-edges and their window-table entries for the whole group
+  uint32_t k0 = 0;
+  float a0 = 0.0f;
+  uint32_t wq[kGroup + 1] = {0, 0, 0, 0, 0};
+  if (nchunks && uint32_t(lane) < deg) {
+    k0 = p.aci[eb + lane];
+    a0 = p.av[eb + lane];
+    const uint32_t* wk = p.wp + size_t(k0) * p.nW + w0;
+#pragma unroll
+    for (uint32_t q = 0; q <= kGroup; ++q)
+      if (q <= wn) wq[q] = wk[q];
+  }
+#pragma unroll 1
+  for (uint32_t gw = 0; gw < wn; ++gw) {
+    const uint32_t w = w0 + gw;
+    const uint32_t wbase = w << p.sh;
+    bool any = false;
+#pragma unroll 1
+    for (uint32_t c = 0; c < nchunks; ++c) {
+      uint32_t beg = 0, cnt = 0;
+      float aa = 0.0f;
+      if (c == 0) {
+        aa = a0;
+#pragma unroll
+        for (uint32_t q = 0; q < kGroup; ++q)
+          if (q == gw) {
+            beg = wq[q];
+            cnt = wq[q + 1] - wq[q];
+          }
+      } else {
+        const uint32_t e = eb + 32 * c + lane;
+        if (e < ee) {
+          const uint32_t kk = p.aci[e];
+          aa = p.av[e];
+          const uint32_t* wk = p.wp + size_t(kk) * p.nW + w;
+          beg = wk[0];
+          cnt = wk[1] - beg;
+        }
+      }
+      const uint32_t incl = warp_incl_scan(cnt, lane);
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total == 0) continue;
+      any = true;
+      const uint32_t excl = incl - cnt;
+      const uint32_t base_off = beg - excl;  // entry index = j + base_off[owner]
+#pragma unroll 1
+      for (uint32_t j0 = 0; j0 < total; j0 += 64) {
+        // two products per lane per step, loads issued before any update
+        uint32_t jj[2], own[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          jj[u] = j0 + 32 * u + lane;
+          uint32_t o = 0;
+#pragma unroll
+          for (uint32_t st = 16; st; st >>= 1) {
+            const uint32_t ex = __shfl_sync(0xffffffffu, excl, o + st);
+            if (ex <= jj[u]) o += st;
+          }
+          own[u] = o;
+        }
+        uint32_t cc[2];
+        float yy[2], ao[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t off = __shfl_sync(0xffffffffu, base_off, own[u]);
+          ao[u] = __shfl_sync(0xffffffffu, aa, own[u]);
+          if (jj[u] < total) {
+            cc[u] = __ldg(p.bci + jj[u] + off);
+            yy[u] = __ldg(p.bv + jj[u] + off);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (jj[u] < total) {
+            const uint32_t sl = cc[u] - wbase;
+            atomicAdd(acc + sl, __float2int_rn(__fmul_rn(__fmul_rn(ao[u], yy[u]), p.fx_scale)));
+            atomicOr(ws.surv + (sl >> 5), 1u << (sl & 31));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    const uint64_t it = uint64_t(i) * p.nW + w;
+    if (!any) {
+      if (lane == 0) p.item_cnt[it] = 0;
+      continue;
+    }
+    // epilogue over the touched bitmap (see emit_window_exact); fixed point -> float
+    const uint32_t wlen = min(S, p.n - wbase);
+    const uint32_t nwords = (wlen + 31) >> 5;
+    const uint32_t per = (nwords + 31) >> 5;
+    const uint32_t q0 = min(nwords, lane * per), q1 = min(nwords, q0 + per);
+    uint32_t mine = 0;
+    for (uint32_t q = q0; q < q1; ++q) {
+      uint32_t t = ws.surv[q], keepw = 0;
+      while (t) {
+        const uint32_t bt = __ffs(t) - 1;
+        t &= t - 1;
+        const uint32_t sl = q * 32 + bt;
+        const float x = __fmul_rn(__int2float_rn(acc[sl]), p.fx_unscale);
+        const float z = kLayer ? layer_epilogue(x, b, p.clip) : x;
+        if (!kLayer || z != 0.0f) {
+          keepw |= 1u << bt;
+          ws.acc[sl] = __float_as_uint(z);
+        } else {
+          ws.acc[sl] = 0u;
+        }
+      }
+      ws.surv[q] = keepw;
+      mine += __popc(keepw);
+    }
+    const uint32_t incl = warp_incl_scan(mine, lane);
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    bool can_write;
+    const unsigned long long off = reserve(p, it, tot, lane, can_write);
+    unsigned long long pos = off + (incl - mine);
+    for (uint32_t q = q0; q < q1; ++q) {
+      uint32_t t = ws.surv[q];
+      if (!t) continue;
+      ws.surv[q] = 0;
+      while (t) {
+        const uint32_t bt = __ffs(t) - 1;
+        t &= t - 1;
+        const uint32_t sl = q * 32 + bt;
+        if (can_write) {
+          p.sc_c[pos] = wbase + sl;
+          p.sc_v[pos] = __uint_as_float(ws.acc[sl]);
+        }
+        ws.acc[sl] = 0u;
+        ++pos;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Phase A over all items, window-group-major so the live slice of B stays in L2.
+// With a frontier (rows != nullptr) only the nrows listed output rows are
+// processed; every other row's items were zeroed by the caller.
 template <typename Ops, bool kLayer, bool kExact>
 __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
-                                        uint64_t gw, uint64_t nwarps) {
+                                        uint64_t gw, uint64_t nwarps,
+                                        const uint32_t* rows = nullptr, uint32_t nrows = 0) {
   const uint32_t ng = (p.nW + kGroup - 1) / kGroup;
-  const uint64_t items = uint64_t(ng) * p.m;
-  for (uint64_t it = gw; it < items; it += nwarps)
-    process_item<Ops, kLayer, kExact>(p, uint32_t(it % p.m), uint32_t(it / p.m), ws, lane);
+  const uint32_t nr = rows ? nrows : p.m;
+  const uint64_t items = uint64_t(ng) * nr;
+  for (uint64_t it = gw; it < items; it += nwarps) {
+    const uint32_t r = uint32_t(it % nr);
+    const uint32_t i = rows ? rows[r] : r;
+    if (kExact) {
+      // rows whose untouched positions survive (epilogue(0 + b) != 0) need the
+      // dense sweep of the float exact path
+      if (kLayer && layer_epilogue(0.0f, p.bias[i], p.clip) != 0.0f)
+        process_item<Ops, kLayer, true>(p, i, uint32_t(it / nr), ws, lane);
+      else
+        process_item_exact<kLayer>(p, i, uint32_t(it / nr), ws, lane);
+    } else {
+      process_item<Ops, kLayer, false>(p, i, uint32_t(it / nr), ws, lane);
+    }
+  }
 }
 
 // Per-matrix value statistics for the exactness test: the smallest power of
@@ -576,6 +748,10 @@ __global__ void k_max_row_len(const uint32_t* rp, uint32_t rows, ValueStats* out
     mx = max(mx, int(rp[i + 1] - rp[i]));
   for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) atomicMax(&out->maxdeg, mx);
+}
+
+__device__ __forceinline__ float pow2f(int e) {
+  return (e >= -126 && e <= 127) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e);
 }
 
 // True when every partial sum of W.Y is exactly representable in fp32, so the
@@ -697,6 +873,13 @@ struct EngineArgs {
   int exact_ok;                    // layer 0 may use the order-free path (SK_NO_EXACT unset)
   unsigned long long stop_above;   // stop after a layer with more entries (0 = never)
   int* layers_done;                // written when stopping early
+  // Frontier path for near-empty inputs (bias_nonpos layers): bitmap of input
+  // rows holding entries (two buffers, alternating), list of output rows with an
+  // in-edge from one of them, and its per-layer length.
+  uint32_t* kbits;                 // 2 * kbits_words, zeroed
+  uint32_t kbits_words;
+  uint32_t* frontier;              // m
+  unsigned int* nfront;            // L counters, zeroed
 };
 
 __device__ __forceinline__ long long globaltimer() {
@@ -736,6 +919,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
   const float* in_v = p.y0_v;
   const uint32_t* in_wp = p.y0_wp;
   int cur = 0, last = -2;
+  uint32_t nfilt = 0;  // frontier layers so far (selects the kbits buffer)
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.trace[0] = p.nnz0;
     if (p.stamps) p.stamps[0] = globaltimer();
@@ -774,6 +958,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     ra.cap = p.cap;
     ra.overflow = p.overflow;
     ra.err = p.err;
+    ra.fx_scale = 1.0f;
+    ra.fx_unscale = 1.0f;
 
     // ---- phase A: rows ---------------------------------------------------------------
     // Layer 0's operand statistics are known: if every partial sum is exact, the
@@ -781,6 +967,43 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     // ascending fold.  Decided identically by every warp.
     const bool exact = layer == 0 && p.exact_ok && products_exact(p.wstats[0], *p.y0stats);
     if (exact) {
+      const int wl = p.wstats[0].lowbit, yl = p.y0stats->lowbit;
+      const int gran = (wl == INT_MAX || yl == INT_MAX) ? 0 : wl + yl;
+      ra.fx_scale = pow2f(-gran);
+      ra.fx_unscale = pow2f(gran);
+    }
+    // Near-empty input with every bias <= 0: an output row with no in-edge from
+    // an input row holding entries has no entries, so only the frontier rows are
+    // processed (and the others' item counts zeroed).  Uniform decision.
+    const bool frontier = !exact && p.bias_nonpos[layer] && total_in * 64 < p.m;
+    if (frontier) {
+      uint32_t* const kb = p.kbits + (nfilt & 1) * p.kbits_words;
+      uint32_t* const kb_next = p.kbits + ((nfilt + 1) & 1) * p.kbits_words;
+      ++nfilt;
+      const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+      const uint32_t nt = gridDim.x * blockDim.x;
+      for (uint32_t k = gt; k < p.m; k += nt)
+        if (in_wp[size_t(k + 1) * p.nW] > in_wp[size_t(k) * p.nW])
+          atomicOr(kb + (k >> 5), 1u << (k & 31));
+      grid.sync();
+      for (uint32_t q = gt; q < p.kbits_words; q += nt) kb_next[q] = 0u;
+      for (uint32_t i = gw; i < p.m; i += nwarps) {
+        const uint32_t eb = ra.arp[i], ee = ra.arp[i + 1];
+        bool hit = false;
+        for (uint32_t e = eb + lane; e < ee && !hit; e += 32) {
+          const uint32_t k = ra.aci[e];
+          hit = (__ldcg(kb + (k >> 5)) >> (k & 31)) & 1u;
+        }
+        if (__any_sync(0xffffffffu, hit)) {
+          if (lane == 0) p.frontier[atomicAdd(p.nfront + layer, 1u)] = i;
+        } else {
+          for (uint32_t w = lane; w < p.nW; w += 32) p.item_cnt[size_t(i) * p.nW + w] = 0u;
+        }
+      }
+      grid.sync();
+      const uint32_t nrows = __ldcg(p.nfront + layer);
+      phase_a<OpArith, true, false>(ra, ws, lane, gw, nwarps, p.frontier, nrows);
+    } else if (exact) {
       for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = 0u;
       __syncwarp();
       phase_a<OpArith, true, true>(ra, ws, lane, gw, nwarps);
@@ -985,6 +1208,8 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   p.cap = cap;
   p.overflow = overflow;
   p.err = ctx->d_err;
+  p.fx_scale = 1.0f;
+  p.fx_unscale = 1.0f;
   const size_t smem = block_smem(g);
   if (d_bias) {
     launch_rows<OpArith, true>(ctx, p, m, smem);
@@ -1118,13 +1343,17 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
   const unsigned grid = unsigned(ctx->num_sms * per_sm);
 
   uint32_t* wp0 = build_wp(ctx, y0, g);
-  const size_t nsmall = size_t(L) + 1 + L + grid + 4;
+  const uint32_t kbw = m / 32 + 1;
+  const size_t nsmall = size_t(L) + 1 + L + grid + 4 + (size_t(L) + 1) / 2 + kbw;
   unsigned long long* small =
       reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, nsmall));
   unsigned long long* trace_d = small;
   unsigned long long* bump = small + L + 1;
   unsigned long long* block_sums = bump + L;
   int* flags = reinterpret_cast<int*>(block_sums + grid);  // [0] overflow, [1] result, [2] done
+  unsigned int* nfront = reinterpret_cast<unsigned int*>(block_sums + grid + 4);
+  uint32_t* kbits = reinterpret_cast<uint32_t*>(block_sums + grid + 4 + (size_t(L) + 1) / 2);
+  uint32_t* frontier = dalloc<uint32_t>(ctx, m);
 
   for (int attempt = 0; attempt < 2; ++attempt) {
     SK_CUDA(cudaMemsetAsync(small, 0, nsmall * 8, ctx->stream));
@@ -1166,6 +1395,10 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     p.exact_ok = exact_ok;
     p.stop_above = stop_above;
     p.layers_done = flags + 2;
+    p.kbits = kbits;
+    p.kbits_words = kbw;
+    p.frontier = frontier;
+    p.nfront = nfront;
     void* args[] = {&p};
     timing_mark(ctx);
     SK_CUDA(cudaLaunchCooperativeKernel((void*)k_sparse_engine, dim3(grid), dim3(kWarps * 32),
@@ -1221,6 +1454,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
       dfree(ctx, wp0);
       dfree(ctx, small);
       dfree(ctx, y0stats);
+      dfree(ctx, frontier);
       return o;
     }
     release();
@@ -1236,6 +1470,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
   dfree(ctx, wp0);
   dfree(ctx, small);
   dfree(ctx, y0stats);
+  dfree(ctx, frontier);
   fail(SK_ERR_OOM, "sparse forward: activation nnz exceeds the device capacity");
 }
 

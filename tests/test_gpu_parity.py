@@ -434,6 +434,31 @@ def test_density_switch_argument_checks(sk):
     ctx.set_density_switch()
 
 
+@pytest.mark.parametrize("entries,bias", [(1, -0.01), (40, -0.01), (40, -0.2), (900, 0.0)])
+def test_sparse_forward_frontier_layers(sk, port, entries, bias):
+    # near-empty inputs take the frontier path (only rows with an in-edge from an
+    # active input row are processed); it must be invisible in the results
+    m, n, L, seed = 8192, 3000, 5, 31
+    rng = np.random.default_rng(seed)
+    flat = rng.choice(m * n, size=entries, replace=False)
+    r, c = (flat // n).astype(np.uint32), (flat % n).astype(np.uint32)
+    v = rng.uniform(0.5, 2.0, entries).astype(np.float32)
+    hY = port.csr_from_triples(m, n, r, c, v) if hasattr(port, "csr_from_triples") else None
+    Y = sk.csr_from_triples(m, n, (r, c, v))
+    if hY is None:
+        hY = host_csr(Y)
+    hW = [port.gen_layer_fixed(m, 32, port.layer_seed(seed, k), float("nan")) for k in range(L)]
+    b = np.full(m, bias, np.float32)
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], [b] * L)
+    out, trace = sk.relu_forward_sparse(model, Y)
+    y, want_trace = hY, [hY.nnz]
+    for k in range(L):
+        y = port.layer_sparse(hW[k], b, y, 0.0)
+        want_trace.append(y.nnz)
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, y)
+
+
 def test_sparse_forward_empty_and_tiny_inputs(sk, port):
     m = 512
     W = sk.gen_layer_fixed(m, 8, 3, 0.5)

@@ -28,5 +28,7 @@ for r in range(a.reps):
     t = time.perf_counter()
     out, trace = sk.relu_forward_sparse(model, Y0, sk.ForwardOptions(clip=32.0))
     kt = ctx.kernel_times_ms()
+    st = ctx.layer_stamps_ns(a.layers + 1).astype(np.float64)
+    per = np.round(np.diff(st) / 1e3, 1).tolist()
     print(f"rep {r}: wall {1e3 * (time.perf_counter() - t):.2f} ms engine {kt[-1]:.3f} ms "
-          f"trace {[int(x) for x in trace]}", flush=True)
+          f"trace {[int(x) for x in trace][:8]} layer_us {per[:8]}", flush=True)
