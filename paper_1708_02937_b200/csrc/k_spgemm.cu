@@ -527,6 +527,11 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
   const uint32_t deg = ee - eb;
   float b = 0.0f;
   if (kLayer) b = p.bias[i];
+  // x + b <= 0 (ReLU -> 0) exactly when acc <= -b * 2^-gran: the rounded sum has
+  // the sign of the exact one, and that scaling of -b is exact.  A position can
+  // only survive if its final partial sum is above thr, so the accumulation
+  // marks a candidate bit whenever an update leaves the sum above thr.
+  const float thr = kLayer ? __fmul_rn(-b, p.fx_scale) : -INFINITY;
   int* const acc = reinterpret_cast<int*>(ws.acc);
   const uint32_t nchunks = p.b_empty ? 0u : (deg + 31) / 32;
   // first chunk's in-edges and their window-table entries for the whole group
@@ -604,8 +609,9 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
         for (int u = 0; u < 2; ++u) {
           if (jj[u] < total) {
             const uint32_t sl = cc[u] - wbase;
-            atomicAdd(acc + sl, __float2int_rn(__fmul_rn(__fmul_rn(ao[u], yy[u]), p.fx_scale)));
-            atomicOr(ws.surv + (sl >> 5), 1u << (sl & 31));
+            const int q = __float2int_rn(__fmul_rn(__fmul_rn(ao[u], yy[u]), p.fx_scale));
+            const int nv = atomicAdd(acc + sl, q) + q;
+            if (__int2float_rn(nv) > thr) atomicOr(ws.surv + (sl >> 5), 1u << (sl & 31));
           }
         }
       }
@@ -628,13 +634,14 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
         const uint32_t bt = __ffs(t) - 1;
         t &= t - 1;
         const uint32_t sl = q * 32 + bt;
-        const float x = __fmul_rn(__int2float_rn(acc[sl]), p.fx_unscale);
-        const float z = kLayer ? layer_epilogue(x, b, p.clip) : x;
-        if (!kLayer || z != 0.0f) {
-          keepw |= 1u << bt;
-          ws.acc[sl] = __float_as_uint(z);
-        } else {
-          ws.acc[sl] = 0u;
+        const int ai = acc[sl];
+        if (!kLayer || __int2float_rn(ai) > thr) {
+          const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
+          const float z = kLayer ? layer_epilogue(x, b, p.clip) : x;
+          if (!kLayer || z != 0.0f) {
+            keepw |= 1u << bt;
+            ws.acc[sl] = __float_as_uint(z);
+          }
         }
       }
       ws.surv[q] = keepw;
@@ -657,10 +664,13 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
           p.sc_c[pos] = wbase + sl;
           p.sc_v[pos] = __uint_as_float(ws.acc[sl]);
         }
-        ws.acc[sl] = 0u;
         ++pos;
       }
     }
+    __syncwarp();
+    // touched positions are not tracked: clear the window with vector stores
+    for (uint32_t t = lane * 4; t < wlen; t += 128)
+      *reinterpret_cast<uint4*>(ws.acc + t) = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
   }
 }
@@ -788,15 +798,21 @@ __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
                                const int* overflow) {
   if (*overflow || wp_out[items] == 0) return;
   const int lane = threadIdx.x & 31;
-  for (uint64_t it = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < items;
-       it += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-    const uint32_t c = item_cnt[it];
-    if (!c) continue;
-    const unsigned long long src = item_off[it];
-    const uint32_t dst = wp_out[it];
-    for (uint32_t t = lane; t < c; t += 32) {
-      oc[size_t(dst) + t] = sc_c[src + t];
-      ov[size_t(dst) + t] = sc_v[src + t];
+  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t it0 = gw * 32; it0 < items; it0 += nw * 32) {
+    const uint32_t c = it0 + lane < items ? item_cnt[it0 + lane] : 0u;
+    uint32_t nz = __ballot_sync(0xffffffffu, c != 0);
+    while (nz) {
+      const int l = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t cl = __shfl_sync(0xffffffffu, c, l);
+      const unsigned long long src = item_off[it0 + l];
+      const uint32_t dst = wp_out[it0 + l];
+      for (uint32_t t = lane; t < cl; t += 32) {
+        oc[size_t(dst) + t] = sc_c[src + t];
+        ov[size_t(dst) + t] = sc_v[src + t];
+      }
     }
   }
 }
@@ -1058,15 +1074,23 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     uint32_t* const oc = cur ? p.ci[1] : p.ci[0];
     float* const ov = cur ? p.v[1] : p.v[0];
     if (grand <= p.cap && grand > 0) {
-      for (uint64_t it = gw; it < items; it += nwarps) {
-        const uint32_t c = p.item_cnt[it];
-        if (!c) continue;
-        const unsigned long long src = p.item_off[it];
-        if (src + c > p.cap) continue;
-        const uint32_t dst = out_wp[it];
-        for (uint32_t t = lane; t < c; t += 32) {
-          oc[size_t(dst) + t] = p.sc_c[src + t];
-          ov[size_t(dst) + t] = p.sc_v[src + t];
+      // 32 items per warp step (coalesced count reads); only non-empty spans move
+      for (uint64_t it0 = uint64_t(gw) * 32; it0 < items; it0 += uint64_t(nwarps) * 32) {
+        const uint64_t mine_it = it0 + lane;
+        const uint32_t c = mine_it < items ? p.item_cnt[mine_it] : 0u;
+        uint32_t nz = __ballot_sync(0xffffffffu, c != 0);
+        while (nz) {
+          const int l = __ffs(nz) - 1;
+          nz &= nz - 1;
+          const uint64_t it = it0 + l;
+          const uint32_t cl = __shfl_sync(0xffffffffu, c, l);
+          const unsigned long long src = p.item_off[it];
+          if (src + cl > p.cap) continue;
+          const uint32_t dst = out_wp[it];
+          for (uint32_t t = lane; t < cl; t += 32) {
+            oc[size_t(dst) + t] = p.sc_c[src + t];
+            ov[size_t(dst) + t] = p.sc_v[src + t];
+          }
         }
       }
     }
