@@ -122,6 +122,7 @@ struct RowArgs {
   int* overflow;
   int* err;
   float fx_scale, fx_unscale;  // exact mode: 2^-gran and 2^gran (fixed-point accumulation)
+  uint32_t fx_pack;            // exact mode: windows per accumulator word (1, 2, 4)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
@@ -511,28 +512,50 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
 }
 
 // Exact mode, fixed point.  Every product and partial sum is a multiple of
-// 2^gran below 2^24 * 2^gran in magnitude (products_exact), so q = p * 2^-gran
-// is an exact int32 and any order of integer adds gives the exact sum; the float
-// ascending fold of the reference equals it bit for bit (acc * 2^gran, +0 for
-// 0).  Integer shared atomics are native (float ones are a CAS loop).  The
-// products of one (row, window) are distributed flat over the warp: product j
-// belongs to the last lane whose exclusive scan offset is <= j.
+// 2^gran below 2^R * 2^gran in magnitude, R = top - gran <= 24
+// (products_exact), so q = p * 2^-gran is an exact integer and any order of
+// integer adds gives the exact sum; the float ascending fold of the reference
+// equals it bit for bit (acc * 2^gran, +0 for 0).  Integer shared atomics are
+// native (float ones are a CAS loop).
+//
+// Packing: when R <= 15 (or <= 7) every partial sum fits a biased 16-bit (8-bit)
+// field, so one 32-bit accumulator word holds P = 2 (4) fields: field `sub` of
+// word s is window (first + sub), sample s.  Adding q << (B*sub) to the word
+// never carries across fields (the biased field stays in [0, 2^B)), so one
+// S-word accumulator serves P consecutive windows and the per-window overhead
+// is paid once per P windows.
+//
+// The accumulator's products are spread flat over the warp, four consecutive
+// ones per lane with all loads in flight before any update (the path is load
+// latency bound); owners come from a compacted table of non-empty slices.  A
+// position can only survive if its final sum is above thr = -b * 2^-gran, so
+// updates that leave the sum above thr mark a candidate bit; the epilogue walks
+// candidates only and the accumulator is reset with vector stores.
+__device__ __forceinline__ uint32_t fx_clear_word(uint32_t P) {
+  return P == 1 ? 0u : (P == 2 ? 0x80008000u : 0x80808080u);
+}
+
 template <bool kLayer>
 __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
                                    int lane) {
-  const uint32_t S = 1u << p.sh;
+  const uint32_t S = 1u << p.sh, SW = S / 32;
+  const uint32_t P = p.fx_pack;
+  const uint32_t B = 32 / P;
+  const uint32_t fmask = P == 1 ? 0xFFFFFFFFu : ((1u << B) - 1u);
+  const uint32_t fbias = P == 1 ? 0u : (1u << (B - 1));
+  const uint32_t clearw = fx_clear_word(P);
   const uint32_t w0 = g * kGroup;
   const uint32_t wn = min(kGroup, p.nW - w0);
   const uint32_t eb = p.arp[i], ee = p.arp[i + 1];
   const uint32_t deg = ee - eb;
-  float b = 0.0f;
-  if (kLayer) b = p.bias[i];
-  // x + b <= 0 (ReLU -> 0) exactly when acc <= -b * 2^-gran: the rounded sum has
-  // the sign of the exact one, and that scaling of -b is exact.  A position can
-  // only survive if its final partial sum is above thr, so the accumulation
-  // marks a candidate bit whenever an update leaves the sum above thr.
+  const float b = kLayer ? p.bias[i] : 0.0f;
   const float thr = kLayer ? __fmul_rn(-b, p.fx_scale) : -INFINITY;
-  int* const acc = reinterpret_cast<int*>(ws.acc);
+  uint32_t* const acc = ws.acc;
+  // staging area (unused in exact mode): compacted in-edge table + candidates
+  uint32_t* const tab_ex = reinterpret_cast<uint32_t*>(ws.st_p);
+  uint32_t* const tab_off = tab_ex + 32;
+  float* const tab_a = reinterpret_cast<float*>(tab_ex + 64);
+  uint32_t* const cand = tab_ex + 128;  // P * SW words
   const uint32_t nchunks = p.b_empty ? 0u : (deg + 31) / 32;
   // first chunk's in-edges and their window-table entries for the whole group
   uint32_t k0 = 0;
@@ -547,9 +570,9 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
       if (q <= wn) wq[q] = wk[q];
   }
 #pragma unroll 1
-  for (uint32_t gw = 0; gw < wn; ++gw) {
-    const uint32_t w = w0 + gw;
-    const uint32_t wbase = w << p.sh;
+  for (uint32_t gw = 0; gw < wn; gw += P) {
+    const uint32_t np = min(P, wn - gw);  // windows sharing this accumulator
+    const uint32_t wbase = (w0 + gw) << p.sh;
     bool any = false;
 #pragma unroll 1
     for (uint32_t c = 0; c < nchunks; ++c) {
@@ -559,118 +582,140 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
         aa = a0;
 #pragma unroll
         for (uint32_t q = 0; q < kGroup; ++q)
-          if (q == gw) {
-            beg = wq[q];
-            cnt = wq[q + 1] - wq[q];
-          }
+          if (q == gw) beg = wq[q];
+#pragma unroll
+        for (uint32_t q = 1; q <= kGroup; ++q)
+          if (q == gw + np) cnt = wq[q] - beg;
       } else {
         const uint32_t e = eb + 32 * c + lane;
         if (e < ee) {
           const uint32_t kk = p.aci[e];
           aa = p.av[e];
-          const uint32_t* wk = p.wp + size_t(kk) * p.nW + w;
+          const uint32_t* wk = p.wp + size_t(kk) * p.nW + w0 + gw;
           beg = wk[0];
-          cnt = wk[1] - beg;
+          cnt = wk[np] - beg;
         }
       }
+      const uint32_t nzm = __ballot_sync(0xffffffffu, cnt != 0);
+      if (!nzm) continue;
+      any = true;
       const uint32_t incl = warp_incl_scan(cnt, lane);
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      if (total == 0) continue;
-      any = true;
-      const uint32_t excl = incl - cnt;
-      const uint32_t base_off = beg - excl;  // entry index = j + base_off[owner]
+      const uint32_t nnzl = __popc(nzm);
+      if (cnt) {
+        const uint32_t r = __popc(nzm & lanemask_lt(lane));
+        tab_ex[r] = incl - cnt;
+        tab_off[r] = beg - (incl - cnt);
+        tab_a[r] = aa;
+      }
+      __syncwarp();
+      const uint32_t cex = uint32_t(lane) < nnzl ? tab_ex[lane] : 0xFFFFFFFFu;
+      const uint32_t coff = tab_off[lane];
+      const float ca = tab_a[lane];
+      __syncwarp();
 #pragma unroll 1
-      for (uint32_t j0 = 0; j0 < total; j0 += 64) {
-        // two products per lane per step, loads issued before any update
-        uint32_t jj[2], own[2];
+      for (uint32_t j0 = 4 * lane; j0 < total + 4 * lane; j0 += 128) {
+        // lane owns products j0 .. j0+3: one search, then step-wise advance
+        uint32_t o = 0;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          jj[u] = j0 + 32 * u + lane;
-          uint32_t o = 0;
+        for (uint32_t st = 16; st; st >>= 1)
+          if (__shfl_sync(0xffffffffu, cex, o + st) <= j0) o += st;
+        uint32_t cc[4];
+        float yy[4], ao[4];
 #pragma unroll
-          for (uint32_t st = 16; st; st >>= 1) {
-            const uint32_t ex = __shfl_sync(0xffffffffu, excl, o + st);
-            if (ex <= jj[u]) o += st;
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t j = j0 + u;
+          if (u) {
+            const uint32_t nx = __shfl_sync(0xffffffffu, cex, min(o + 1, 31u));
+            if (o < 31 && nx <= j) ++o;
           }
-          own[u] = o;
-        }
-        uint32_t cc[2];
-        float yy[2], ao[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const uint32_t off = __shfl_sync(0xffffffffu, base_off, own[u]);
-          ao[u] = __shfl_sync(0xffffffffu, aa, own[u]);
-          if (jj[u] < total) {
-            cc[u] = __ldg(p.bci + jj[u] + off);
-            yy[u] = __ldg(p.bv + jj[u] + off);
+          const uint32_t off = __shfl_sync(0xffffffffu, coff, o);
+          ao[u] = __shfl_sync(0xffffffffu, ca, o);
+          if (j < total) {
+            cc[u] = __ldg(p.bci + j + off);
+            yy[u] = __ldg(p.bv + j + off);
           }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (jj[u] < total) {
+        for (int u = 0; u < 4; ++u) {
+          if (j0 + u < total) {
             const uint32_t sl = cc[u] - wbase;
-            const int q = __float2int_rn(__fmul_rn(__fmul_rn(ao[u], yy[u]), p.fx_scale));
-            const int nv = atomicAdd(acc + sl, q) + q;
-            if (__int2float_rn(nv) > thr) atomicOr(ws.surv + (sl >> 5), 1u << (sl & 31));
+            const uint32_t sub = sl >> p.sh, wl = sl & (S - 1);
+            const uint32_t fs = B * sub;
+            const uint32_t delta =
+                uint32_t(__float2int_rn(__fmul_rn(__fmul_rn(ao[u], yy[u]), p.fx_scale))) << fs;
+            const uint32_t old = atomicAdd(acc + wl, delta);
+            const int nv = int(((old + delta) >> fs) & fmask) - int(fbias);
+            if (__int2float_rn(nv) > thr) atomicOr(cand + sub * SW + (wl >> 5), 1u << (wl & 31));
           }
         }
       }
     }
     __syncwarp();
-    const uint64_t it = uint64_t(i) * p.nW + w;
-    if (!any) {
-      if (lane == 0) p.item_cnt[it] = 0;
-      continue;
-    }
-    // epilogue over the touched bitmap (see emit_window_exact); fixed point -> float
-    const uint32_t wlen = min(S, p.n - wbase);
-    const uint32_t nwords = (wlen + 31) >> 5;
-    const uint32_t per = (nwords + 31) >> 5;
-    const uint32_t q0 = min(nwords, lane * per), q1 = min(nwords, q0 + per);
-    uint32_t mine = 0;
-    for (uint32_t q = q0; q < q1; ++q) {
-      uint32_t t = ws.surv[q], keepw = 0;
-      while (t) {
-        const uint32_t bt = __ffs(t) - 1;
-        t &= t - 1;
-        const uint32_t sl = q * 32 + bt;
-        const int ai = acc[sl];
-        if (!kLayer || __int2float_rn(ai) > thr) {
-          const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
-          const float z = kLayer ? layer_epilogue(x, b, p.clip) : x;
-          if (!kLayer || z != 0.0f) {
-            keepw |= 1u << bt;
-            ws.acc[sl] = __float_as_uint(z);
+    // ---- emit each window of the accumulator ---------------------------------------
+#pragma unroll 1
+    for (uint32_t sub = 0; sub < np; ++sub) {
+      const uint32_t w = w0 + gw + sub;
+      const uint64_t it = uint64_t(i) * p.nW + w;
+      const uint32_t swbase = w << p.sh;
+      const uint32_t wlen = min(S, p.n - swbase);
+      const uint32_t nwords = (wlen + 31) >> 5;
+      uint32_t* const cw = cand + sub * SW;
+      uint32_t anyc = 0;
+      if (any)
+        for (uint32_t q = lane; q < nwords; q += 32) anyc |= cw[q];
+      if (!__any_sync(0xffffffffu, anyc != 0)) {
+        if (lane == 0) p.item_cnt[it] = 0;
+        continue;
+      }
+      const uint32_t fs = B * sub;
+      const uint32_t per = (nwords + 31) >> 5;
+      const uint32_t q0 = min(nwords, lane * per), q1 = min(nwords, q0 + per);
+      uint32_t mine = 0;
+      for (uint32_t q = q0; q < q1; ++q) {
+        uint32_t t = cw[q], keepw = 0;
+        while (t) {
+          const uint32_t bt = __ffs(t) - 1;
+          t &= t - 1;
+          const int ai = int((acc[q * 32 + bt] >> fs) & fmask) - int(fbias);
+          if (__int2float_rn(ai) > thr) {
+            const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
+            const float z = kLayer ? layer_epilogue(x, b, p.clip) : x;
+            if (!kLayer || z != 0.0f) keepw |= 1u << bt;
           }
         }
+        cw[q] = keepw;
+        mine += __popc(keepw);
       }
-      ws.surv[q] = keepw;
-      mine += __popc(keepw);
-    }
-    const uint32_t incl = warp_incl_scan(mine, lane);
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    bool can_write;
-    const unsigned long long off = reserve(p, it, tot, lane, can_write);
-    unsigned long long pos = off + (incl - mine);
-    for (uint32_t q = q0; q < q1; ++q) {
-      uint32_t t = ws.surv[q];
-      if (!t) continue;
-      ws.surv[q] = 0;
-      while (t) {
-        const uint32_t bt = __ffs(t) - 1;
-        t &= t - 1;
-        const uint32_t sl = q * 32 + bt;
-        if (can_write) {
-          p.sc_c[pos] = wbase + sl;
-          p.sc_v[pos] = __uint_as_float(ws.acc[sl]);
+      const uint32_t incl = warp_incl_scan(mine, lane);
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      bool can_write;
+      const unsigned long long off = reserve(p, it, tot, lane, can_write);
+      unsigned long long pos = off + (incl - mine);
+      for (uint32_t q = q0; q < q1; ++q) {
+        uint32_t t = cw[q];
+        if (!t) continue;
+        cw[q] = 0u;
+        while (t) {
+          const uint32_t bt = __ffs(t) - 1;
+          t &= t - 1;
+          if (can_write) {
+            const int ai = int((acc[q * 32 + bt] >> fs) & fmask) - int(fbias);
+            const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
+            p.sc_c[pos] = swbase + q * 32 + bt;
+            p.sc_v[pos] = kLayer ? layer_epilogue(x, b, p.clip) : x;
+          }
+          ++pos;
         }
-        ++pos;
       }
+      __syncwarp();
     }
-    __syncwarp();
-    // touched positions are not tracked: clear the window with vector stores
-    for (uint32_t t = lane * 4; t < wlen; t += 128)
-      *reinterpret_cast<uint4*>(ws.acc + t) = make_uint4(0u, 0u, 0u, 0u);
+    if (any) {
+      // candidates of windows without survivors were never cleared above
+      for (uint32_t q = lane; q < np * SW; q += 32) cand[q] = 0u;
+      for (uint32_t t = lane * 4; t < S; t += 128)
+        *reinterpret_cast<uint4*>(acc + t) = make_uint4(clearw, clearw, clearw, clearw);
+    }
     __syncwarp();
   }
 }
@@ -684,19 +729,35 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
                                         const uint32_t* rows = nullptr, uint32_t nrows = 0) {
   const uint32_t ng = (p.nW + kGroup - 1) / kGroup;
   const uint32_t nr = rows ? nrows : p.m;
-  const uint64_t items = uint64_t(ng) * nr;
-  for (uint64_t it = gw; it < items; it += nwarps) {
-    const uint32_t r = uint32_t(it % nr);
+  if (nr == 0) return;
+  // item it = g * nr + r, walked incrementally (no 64-bit division per item)
+  const uint64_t dg = nwarps / nr;
+  const uint32_t dr = uint32_t(nwarps % nr);
+  uint64_t g = gw / nr;
+  uint32_t r = uint32_t(gw % nr);
+  for (; g < ng;) {
     const uint32_t i = rows ? rows[r] : r;
     if (kExact) {
       // rows whose untouched positions survive (epilogue(0 + b) != 0) need the
       // dense sweep of the float exact path
-      if (kLayer && layer_epilogue(0.0f, p.bias[i], p.clip) != 0.0f)
-        process_item<Ops, kLayer, true>(p, i, uint32_t(it / nr), ws, lane);
-      else
-        process_item_exact<kLayer>(p, i, uint32_t(it / nr), ws, lane);
+      if (kLayer && layer_epilogue(0.0f, p.bias[i], p.clip) != 0.0f) {
+        // the float exact path expects a zeroed accumulator
+        const uint32_t S = 1u << p.sh, cw = fx_clear_word(p.fx_pack);
+        for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = 0u;
+        __syncwarp();
+        process_item<Ops, kLayer, true>(p, i, uint32_t(g), ws, lane);
+        for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
+        __syncwarp();
+      } else
+        process_item_exact<kLayer>(p, i, uint32_t(g), ws, lane);
     } else {
-      process_item<Ops, kLayer, false>(p, i, uint32_t(it / nr), ws, lane);
+      process_item<Ops, kLayer, false>(p, i, uint32_t(g), ws, lane);
+    }
+    g += dg;
+    r += dr;
+    if (r >= nr) {
+      r -= nr;
+      ++g;
     }
   }
 }
@@ -976,6 +1037,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     ra.err = p.err;
     ra.fx_scale = 1.0f;
     ra.fx_unscale = 1.0f;
+    ra.fx_pack = 1;
 
     // ---- phase A: rows ---------------------------------------------------------------
     // Layer 0's operand statistics are known: if every partial sum is exact, the
@@ -983,10 +1045,18 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     // ascending fold.  Decided identically by every warp.
     const bool exact = layer == 0 && p.exact_ok && products_exact(p.wstats[0], *p.y0stats);
     if (exact) {
-      const int wl = p.wstats[0].lowbit, yl = p.y0stats->lowbit;
-      const int gran = (wl == INT_MAX || yl == INT_MAX) ? 0 : wl + yl;
+      const ValueStats& wst = p.wstats[0];
+      const ValueStats& yst = *p.y0stats;
+      const bool zero = wst.lowbit == INT_MAX || yst.lowbit == INT_MAX;
+      const int gran = zero ? 0 : wst.lowbit + yst.lowbit;
       ra.fx_scale = pow2f(-gran);
       ra.fx_unscale = pow2f(gran);
+      int lg = 0;
+      while ((1 << lg) < max(wst.maxdeg, 1)) ++lg;
+      const int range = zero ? 0 : lg + wst.ehi + yst.ehi - gran;  // |partial sums| < 2^range
+      uint32_t P = range <= 7 ? 4u : (range <= 15 ? 2u : 1u);
+      while (P > 1 && P * (S / 32) > 384) P >>= 1;  // candidate bitmaps live in st_p
+      ra.fx_pack = P;
     }
     // Near-empty input with every bias <= 0: an output row with no in-edge from
     // an input row holding entries has no entries, so only the frontier rows are
@@ -1020,7 +1090,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
       const uint32_t nrows = __ldcg(p.nfront + layer);
       phase_a<OpArith, true, false>(ra, ws, lane, gw, nwarps, p.frontier, nrows);
     } else if (exact) {
-      for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = 0u;
+      const uint32_t cw = fx_clear_word(ra.fx_pack);
+      for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
+      for (uint32_t t = lane; t < ra.fx_pack * (S / 32); t += 32)
+        reinterpret_cast<uint32_t*>(ws.st_p)[128 + t] = 0u;
       __syncwarp();
       phase_a<OpArith, true, true>(ra, ws, lane, gw, nwarps);
       for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = kSent;
@@ -1234,6 +1307,7 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   p.err = ctx->d_err;
   p.fx_scale = 1.0f;
   p.fx_unscale = 1.0f;
+  p.fx_pack = 1;
   const size_t smem = block_smem(g);
   if (d_bias) {
     launch_rows<OpArith, true>(ctx, p, m, smem);

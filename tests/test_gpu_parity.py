@@ -434,6 +434,38 @@ def test_density_switch_argument_checks(sk):
     ctx.set_density_switch()
 
 
+@pytest.mark.parametrize("ymax", [1, 300, 20000])
+def test_exact_fixed_point_layer_matches_oracle(sk, port, ymax):
+    # Layer 0 with exactly representable partial sums takes the order-free
+    # fixed-point path; ymax sets the partial-sum range and with it the packing
+    # (range 7 -> four 8-bit fields per word, ~15 -> two 16-bit, ~21 -> int32).
+    # Signed weights, rows with positive bias (dense rows) mixed in.
+    from oracle.oracle import Csr
+    m, n, L, seed = 4096, 3000, 2, 41
+    rng = np.random.default_rng(seed)
+    hW = []
+    for k in range(L):
+        w = port.gen_layer_fixed(m, 32, port.layer_seed(seed, k), float("nan"))
+        q = np.round(w.values * 8.0)
+        q[q == 0] = 1.0
+        hW.append(Csr(m, m, w.row_ptr, w.col_idx, (q / 16.0).astype(np.float32)))
+    ent = 60000
+    flat = rng.choice(m * n, size=ent, replace=False)
+    r, c = (flat // n).astype(np.uint32), (flat % n).astype(np.uint32)
+    v = rng.integers(1, ymax + 1, ent).astype(np.float32)
+    Y = sk.csr_from_triples(m, n, (r, c, v))
+    hY = host_csr(Y)
+    b = np.where(np.arange(m) % 13 == 0, 0.25, -0.5).astype(np.float32)
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], [b] * L)
+    out, trace = sk.relu_forward_sparse(model, Y, sk.ForwardOptions(clip=0.0))
+    y, want_trace = hY, [hY.nnz]
+    for k in range(L):
+        y = port.layer_sparse(hW[k], b, y, 0.0)
+        want_trace.append(y.nnz)
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, y)
+
+
 @pytest.mark.parametrize("entries,bias", [(1, -0.01), (40, -0.01), (40, -0.2), (900, 0.0)])
 def test_sparse_forward_frontier_layers(sk, port, entries, bias):
     # near-empty inputs take the frontier path (only rows with an in-edge from an

@@ -32,3 +32,10 @@ ti = sum(a[1] for a in agg.values()) or 1
 print(f"total stall samples {ts:.0f}, warp instructions {ti:.3g}")
 for ln, (st, ie, src) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
     print(f"L{ln:5d} inst {100 * ie / ti:5.1f}%  stall {100 * st / ts:5.1f}%  {src}")
+
+if len(sys.argv) > 3:  # line ranges "a-b,c-d" -> totals
+    for rg in sys.argv[3].split(","):
+        a, b = (int(x) for x in rg.split("-"))
+        ie = sum(v[1] for ln, v in agg.items() if a <= ln <= b)
+        st = sum(v[0] for ln, v in agg.items() if a <= ln <= b)
+        print(f"lines {a}-{b}: inst {100 * ie / ti:5.1f}% ({ie:.3g})  stall {100 * st / ts:5.1f}%")
