@@ -535,10 +535,11 @@ __device__ __forceinline__ uint32_t fx_clear_word(uint32_t P) {
   return P == 1 ? 0u : (P == 2 ? 0x80008000u : 0x80808080u);
 }
 
-template <bool kLayer>
+template <bool kLayer, int kSh>  // kSh: compile-time log2 window (0 = runtime p.sh)
 __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
                                    int lane) {
-  const uint32_t S = 1u << p.sh, SW = S / 32;
+  const int sh = kSh ? kSh : p.sh;
+  const uint32_t S = 1u << sh, SW = S / 32;
   const uint32_t P = p.fx_pack;
   const uint32_t B = 32 / P;
   const uint32_t fmask = P == 1 ? 0xFFFFFFFFu : ((1u << B) - 1u);
@@ -572,7 +573,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
 #pragma unroll 1
   for (uint32_t gw = 0; gw < wn; gw += P) {
     const uint32_t np = min(P, wn - gw);  // windows sharing this accumulator
-    const uint32_t wbase = (w0 + gw) << p.sh;
+    const uint32_t wbase = (w0 + gw) << sh;
     bool any = false;
 #pragma unroll 1
     for (uint32_t c = 0; c < nchunks; ++c) {
@@ -632,15 +633,15 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
           const uint32_t off = __shfl_sync(0xffffffffu, coff, o);
           ao[u] = __shfl_sync(0xffffffffu, ca, o);
           if (j < total) {
-            cc[u] = __ldg(p.bci + j + off);
-            yy[u] = __ldg(p.bv + j + off);
+            cc[u] = __ldg(&p.bci[j + off]);
+            yy[u] = __ldg(&p.bv[j + off]);
           }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (j0 + u < total) {
             const uint32_t sl = cc[u] - wbase;
-            const uint32_t sub = sl >> p.sh, wl = sl & (S - 1);
+            const uint32_t sub = sl >> sh, wl = sl & (S - 1);
             const uint32_t fs = B * sub;
             const uint32_t delta =
                 uint32_t(__float2int_rn(__fmul_rn(__fmul_rn(ao[u], yy[u]), p.fx_scale))) << fs;
@@ -657,7 +658,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
     for (uint32_t sub = 0; sub < np; ++sub) {
       const uint32_t w = w0 + gw + sub;
       const uint64_t it = uint64_t(i) * p.nW + w;
-      const uint32_t swbase = w << p.sh;
+      const uint32_t swbase = w << sh;
       const uint32_t wlen = min(S, p.n - swbase);
       const uint32_t nwords = (wlen + 31) >> 5;
       uint32_t* const cw = cand + sub * SW;
@@ -748,8 +749,11 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
         process_item<Ops, kLayer, true>(p, i, uint32_t(g), ws, lane);
         for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
         __syncwarp();
-      } else
-        process_item_exact<kLayer>(p, i, uint32_t(g), ws, lane);
+      } else if (p.sh == 10) {
+        process_item_exact<kLayer, 10>(p, i, uint32_t(g), ws, lane);
+      } else {
+        process_item_exact<kLayer, 0>(p, i, uint32_t(g), ws, lane);
+      }
     } else {
       process_item<Ops, kLayer, false>(p, i, uint32_t(g), ws, lane);
     }
