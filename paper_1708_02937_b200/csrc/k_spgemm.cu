@@ -561,15 +561,23 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
   // first chunk's in-edges and their window-table entries for the whole group
   uint32_t k0 = 0;
   float a0 = 0.0f;
-  uint32_t wq[kGroup + 1] = {0, 0, 0, 0, 0};
+  // window-table entries of the group (named scalars: a dynamically indexed
+  // array would live in local memory)
+  uint32_t wq0 = 0, wq1 = 0, wq2 = 0, wq3 = 0, wq4 = 0;
+  static_assert(kGroup == 4, "wq0..wq4 cover one group");
   if (nchunks && uint32_t(lane) < deg) {
     k0 = p.aci[eb + lane];
     a0 = p.av[eb + lane];
     const uint32_t* wk = p.wp + size_t(k0) * p.nW + w0;
-#pragma unroll
-    for (uint32_t q = 0; q <= kGroup; ++q)
-      if (q <= wn) wq[q] = wk[q];
+    wq0 = wk[0];
+    wq1 = wk[1];
+    if (wn >= 2) wq2 = wk[2];
+    if (wn >= 3) wq3 = wk[3];
+    if (wn >= 4) wq4 = wk[4];
   }
+  auto wq_at = [&](uint32_t q) {
+    return q == 0 ? wq0 : q == 1 ? wq1 : q == 2 ? wq2 : q == 3 ? wq3 : wq4;
+  };
 #pragma unroll 1
   for (uint32_t gw = 0; gw < wn; gw += P) {
     const uint32_t np = min(P, wn - gw);  // windows sharing this accumulator
@@ -581,12 +589,8 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
       float aa = 0.0f;
       if (c == 0) {
         aa = a0;
-#pragma unroll
-        for (uint32_t q = 0; q < kGroup; ++q)
-          if (q == gw) beg = wq[q];
-#pragma unroll
-        for (uint32_t q = 1; q <= kGroup; ++q)
-          if (q == gw + np) cnt = wq[q] - beg;
+        beg = wq_at(gw);
+        cnt = wq_at(gw + np) - beg;
       } else {
         const uint32_t e = eb + 32 * c + lane;
         if (e < ee) {
