@@ -123,6 +123,8 @@ struct RowArgs {
   int* err;
   float fx_scale, fx_unscale;  // exact mode: 2^-gran and 2^gran (fixed-point accumulation)
   uint32_t fx_pack;            // exact mode: windows per accumulator word (1, 2, 4)
+  int y_const;                 // exact mode: every B value is y_cval (no value loads)
+  float y_cval;
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
@@ -638,7 +640,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
           ao[u] = __shfl_sync(0xffffffffu, ca, o);
           if (j < total) {
             cc[u] = __ldg(&p.bci[j + off]);
-            yy[u] = __ldg(&p.bv[j + off]);
+            yy[u] = p.y_const ? p.y_cval : __ldg(&p.bv[j + off]);
           }
         }
 #pragma unroll
@@ -778,7 +780,9 @@ struct ValueStats {
   int ehi;        // max over nonzero values
   int nonfinite;  // any Inf/NaN
   int maxdeg;     // max stored entries per row (weights only)
+  unsigned int vmin, vmax;  // min / max bit pattern over all stored values (equal: constant)
 };
+#define SK_VALUESTATS_INIT {INT_MAX, INT_MIN, 0, 0, 0xFFFFFFFFu, 0u}
 
 __device__ __forceinline__ void value_bits(float v, int& lowbit, int& ehi) {
   const uint32_t b = __float_as_uint(v) & 0x7fffffffu;
@@ -797,9 +801,12 @@ __device__ __forceinline__ void value_bits(float v, int& lowbit, int& ehi) {
 
 __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
   int lo = INT_MAX, hi = INT_MIN, nf = 0;
+  unsigned int bmin = 0xFFFFFFFFu, bmax = 0u;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x) {
     const float x = v[i];
+    bmin = min(bmin, __float_as_uint(x));
+    bmax = max(bmax, __float_as_uint(x));
     if (!isfinite(x)) {
       nf = 1;
     } else if (x != 0.0f) {
@@ -813,11 +820,15 @@ __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     nf |= __shfl_xor_sync(0xffffffffu, nf, o);
+    bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+    bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMin(&out->lowbit, lo);
     atomicMax(&out->ehi, hi);
     if (nf) atomicOr(&out->nonfinite, 1);
+    atomicMin(&out->vmin, bmin);
+    atomicMax(&out->vmax, bmax);
   }
 }
 
@@ -1046,6 +1057,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     ra.fx_scale = 1.0f;
     ra.fx_unscale = 1.0f;
     ra.fx_pack = 1;
+    ra.y_const = 0;
+    ra.y_cval = 0.0f;
 
     // ---- phase A: rows ---------------------------------------------------------------
     // Layer 0's operand statistics are known: if every partial sum is exact, the
@@ -1065,6 +1078,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
       uint32_t P = range <= 7 ? 4u : (range <= 15 ? 2u : 1u);
       while (P > 1 && P * (S / 32) > 384) P >>= 1;  // candidate bitmaps live in st_p
       ra.fx_pack = P;
+      // binary (constant-valued) inputs: the value array need not be read
+      ra.y_const = yst.vmin == yst.vmax;
+      ra.y_cval = __uint_as_float(yst.vmin);
     }
     // Near-empty input with every bias <= 0: an output row with no in-edge from
     // an input row holding entries has no entries, so only the frontier rows are
@@ -1316,6 +1332,8 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   p.fx_scale = 1.0f;
   p.fx_unscale = 1.0f;
   p.fx_pack = 1;
+  p.y_const = 0;
+  p.y_cval = 0.0f;
   const size_t smem = block_smem(g);
   if (d_bias) {
     launch_rows<OpArith, true>(ctx, p, m, smem);
@@ -1374,7 +1392,7 @@ void ensure_model_tables(sk_ctx* ctx, sk_model* mm) {
                             cudaMemcpyHostToDevice, ctx->stream));
     SK_CUDA(cudaMemcpyAsync(mm->d_bias_nonpos, mm->bias_nonpos.data(), L,
                             cudaMemcpyHostToDevice, ctx->stream));
-    std::vector<ValueStats> init(L, ValueStats{INT_MAX, INT_MIN, 0, 0});
+    std::vector<ValueStats> init(L, ValueStats SK_VALUESTATS_INIT);
     SK_CUDA(cudaMemcpyAsync(mm->d_wstats, init.data(), L * sizeof(ValueStats),
                             cudaMemcpyHostToDevice, ctx->stream));
   }
@@ -1416,7 +1434,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
   const int exact_ok = exact_env;
   ValueStats* y0stats = dalloc<ValueStats>(ctx, 1);
   {
-    const ValueStats init{INT_MAX, INT_MIN, 0, 0};
+    const ValueStats init SK_VALUESTATS_INIT;
     SK_CUDA(cudaMemcpyAsync(y0stats, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
     if (y0->nnz)
       SK_LAUNCH(k_value_stats, grid_warps(ctx, y0->nnz / 32 + 1), 256, 0, ctx->stream, y0->v,
