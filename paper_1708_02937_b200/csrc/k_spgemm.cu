@@ -802,9 +802,7 @@ __device__ __forceinline__ void value_bits(float v, int& lowbit, int& ehi) {
 __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
   int lo = INT_MAX, hi = INT_MIN, nf = 0;
   unsigned int bmin = 0xFFFFFFFFu, bmax = 0u;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
-       i += size_t(gridDim.x) * blockDim.x) {
-    const float x = v[i];
+  auto visit = [&](float x) {
     bmin = min(bmin, __float_as_uint(x));
     bmax = max(bmax, __float_as_uint(x));
     if (!isfinite(x)) {
@@ -815,6 +813,21 @@ __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
       lo = min(lo, l);
       hi = max(hi, h);
     }
+  };
+  const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  const size_t nth = size_t(gridDim.x) * blockDim.x;
+  if ((reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+    const size_t n4 = n / 4;
+    for (size_t i = tid; i < n4; i += nth) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(v) + i);
+      visit(x.x);
+      visit(x.y);
+      visit(x.z);
+      visit(x.w);
+    }
+    for (size_t i = n4 * 4 + tid; i < n; i += nth) visit(v[i]);
+  } else {
+    for (size_t i = tid; i < n; i += nth) visit(v[i]);
   }
   for (int o = 16; o; o >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -823,7 +836,26 @@ __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
     bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
     bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
   }
+  // block reduction, then one set of atomics per block
+  __shared__ int r_lo[32], r_hi[32], r_nf[32];
+  __shared__ unsigned int r_bmin[32], r_bmax[32];
+  const int wq = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    r_lo[wq] = lo;
+    r_hi[wq] = hi;
+    r_nf[wq] = nf;
+    r_bmin[wq] = bmin;
+    r_bmax[wq] = bmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < int(blockDim.x >> 5); ++q) {
+      lo = min(lo, r_lo[q]);
+      hi = max(hi, r_hi[q]);
+      nf |= r_nf[q];
+      bmin = min(bmin, r_bmin[q]);
+      bmax = max(bmax, r_bmax[q]);
+    }
     atomicMin(&out->lowbit, lo);
     atomicMax(&out->ehi, hi);
     if (nf) atomicOr(&out->nonfinite, 1);
@@ -1437,7 +1469,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     const ValueStats init SK_VALUESTATS_INIT;
     SK_CUDA(cudaMemcpyAsync(y0stats, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
     if (y0->nnz)
-      SK_LAUNCH(k_value_stats, grid_warps(ctx, y0->nnz / 32 + 1), 256, 0, ctx->stream, y0->v,
+      SK_LAUNCH(k_value_stats, grid_warps(ctx, y0->nnz / 128 + 1), 256, 0, ctx->stream, y0->v,
                 y0->nnz, y0stats);
   }
 
