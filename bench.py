@@ -50,6 +50,10 @@ WORKLOADS = {
                            desc="sustained-work variant of BASELINE configs[2] (NOT a BASELINE "
                                 "config): cfg3 network, Y0 binary 50%/sample -> activations "
                                 "saturate (dense) from layer 1, 60000 samples/GPU"),
+    "cfg5": dict(m=262144, L=120, B=60000, kW=32, value=1.0 / 16, bias=-0.45, clip=32.0,
+                 y0="binary", density=0.001,
+                 desc="BASELINE configs[4]: 120-layer sparse DNN, N=262144, 32 nnz/row (1/16), "
+                      "bias -0.45, ReLU clip 32, Y0 binary 0.1%/sample, 60000 samples/GPU"),
     "cfg1": dict(m=1024, L=4, B=256, kW=16, value=float("nan"), bias=-0.05, clip=0.0,
                  y0="dense", density=1.0,
                  desc="BASELINE configs[0]: 4-layer sparse DNN, N=1024, 16 nnz/row U[-1,1), "
@@ -67,13 +71,68 @@ def env_rank():
 # clocks sampled during the timed region (B200_PROFILING.md "clocks line")
 
 class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled during the timed
+    region.  In-process NVML (nvidia_ml_py) from a background thread: spawning
+    nvidia-smi stalls CUDA API calls while it initialises NVML, which lands in
+    short timed regions.  NVML is initialised and queried once before the region
+    starts; a sample is also taken at entry and exit so short regions still get
+    samples.  Falls back to `nvidia-smi -lms` if NVML is unavailable."""
+
+    PERIOD_S = 0.05
+
     def __init__(self, gpu_index: int):
-        self.path = os.path.join("/tmp", f"sk_clocks_{os.getpid()}_{gpu_index}.csv")
-        self.proc = None
         self.gpu = gpu_index
+        self.rows = []  # (sm_mhz, max_mhz, reasons_bitmask)
+        self.nv = None
+        self.h = None
+        self.thread = None
+        self.proc = None
+        self.path = os.path.join("/tmp", f"sk_clocks_{os.getpid()}_{gpu_index}.csv")
+        if os.environ.get("SK_BENCH_NO_CLOCKS"):  # diagnostics only
+            return
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = None
+            try:  # the CUDA device's own GPU (NVML ignores CUDA_VISIBLE_DEVICES)
+                import torch
+                uuid = str(torch.cuda.get_device_properties(self.gpu).uuid)
+                self.h = pynvml.nvmlDeviceGetHandleByUUID(
+                    uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self.rows.clear()
+        except Exception:
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.rows.append((float(sm), float(self.max_mhz), int(reasons)))
+
+    def _loop(self):
+        import threading  # noqa: F401
+        while not self.stop.wait(self.PERIOD_S):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def __enter__(self):
-        try:
+        if os.environ.get("SK_BENCH_NO_CLOCKS"):
+            return self
+        if self.nv is not None:
+            import threading
+            self.stop = threading.Event()
+            self._sample()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
+            self.thread.start()
+            return self
+        try:  # fallback: nvidia-smi, started well before the region
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}",
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
@@ -81,23 +140,22 @@ class ClockSampler:
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            t0 = time.time()
+            while time.time() - t0 < 10 and os.path.getsize(self.path) == 0:
+                time.sleep(0.05)
+            time.sleep(0.5)
         except Exception:
             self.proc = None
-        # nvidia-smi's start-up (NVML init) takes driver locks that stall CUDA
-        # API calls: wait for its first sample so that never lands in the timed
-        # region.
-        t0 = time.time()
-        while self.proc and time.time() - t0 < 10:
-            try:
-                if os.path.getsize(self.path) > 0:
-                    break
-            except OSError:
-                pass
-            time.sleep(0.05)
-        time.sleep(0.1)
         return self
 
     def __exit__(self, *a):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -106,6 +164,19 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nv is not None and self.rows:
+            nv = self.nv
+            bits = [getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                    getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                    getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                    getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4)]
+            sm = [r[0] for r in self.rows]
+            mx = max(r[1] for r in self.rows)
+            reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2] & bits[i]})
+            loaded = [x for x in sm if x > 0.5 * mx] or sm
+            return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                    "samples": len(self.rows), "source": "nvml"}
         rows = []
         try:
             for line in open(self.path):
@@ -118,11 +189,10 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         sm = [float(r[0]) for r in rows]
         mx = max(float(r[1]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
         loaded = [s for s in sm if s > 0.5 * mx] or sm
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "source": "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -314,7 +384,7 @@ def run_ours(args, w):
     import torch
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or (args.shard == "cols" and "MASTER_ADDR" in os.environ):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1708_02937_b200 as sk
@@ -324,19 +394,41 @@ def run_ours(args, w):
     ctx.set_stream(stream.cuda_stream)  # the library launches on torch's current stream
 
     m, L, B = w["m"], w["L"], w["B"]
-    model, Ws = build_model(sk, w)
-    nnzW = [x.nnz() for x in Ws]
-    if w["y0"] == "binary":
+    cols = args.shard == "cols" and w["y0"] == "binary"
+    if cols:
+        # column sharding: this rank owns output neurons [r0, r1) of every W_ref and
+        # the whole batch; one all-gather of the sparse activations per layer
+        from paper_1708_02937_b200 import shard
+        dev = torch.device("cuda", local)
+        r0, r1 = shard.block_range(m, world, rank)
+        blocks, nnzW = [], []
+        for k in range(L):
+            wf = sk.gen_layer_fixed(m, w["kW"], sk.layer_seed(SEED, k), w["value"])
+            nnzW.append(wf.nnz())
+            blocks.append(shard.row_block(wf, r0, r1, dev))
+            del wf
+        bblocks = [np.full(r1 - r0, w["bias"], np.float32)] * L
+        Y0 = sk.gen_input_binary(m, B, kY_of(w), SEED)
+        run = lambda y: shard.relu_forward_sparse_colsharded(  # noqa
+            blocks, bblocks, y, w["clip"], device=dev)
+        host_rp, host_ci, host_v = (np.array(a) for a in Y0.extract())
+        nnz0 = int(host_rp[-1])
+    elif w["y0"] == "binary":
+        model, Ws = build_model(sk, w)
+        nnzW = [x.nnz() for x in Ws]
         Y0 = sk.gen_input_binary(m, B, kY_of(w), SEED, sample_offset=rank * B)
         run = lambda y: sk.relu_forward_sparse(model, y, sk.ForwardOptions(clip=w["clip"]))  # noqa
         host_rp, host_ci, host_v = (np.array(a) for a in Y0.extract())
         nnz0 = int(host_rp[-1])
     else:
+        model, Ws = build_model(sk, w)
+        nnzW = [x.nnz() for x in Ws]
         Y0 = sk.gen_input_dense(m, B, SEED)
         run = lambda y: (sk.relu_forward(model, y, sk.ForwardOptions(clip=w["clip"])), None)  # noqa
         host_y = Y0.numpy()
         nnz0 = m * B
     torch.cuda.synchronize()
+    sampler = ClockSampler(local)  # NVML initialised well before the timed region
 
     def barrier():
         if dist is not None:
@@ -353,7 +445,7 @@ def run_ours(args, w):
     # ---- timed region: resident inputs ----------------------------------------------
     ctx.set_timing(True)
     launches0 = sk._lib.launches()
-    with ClockSampler(local) as clocks:
+    with sampler as clocks:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(stream)
@@ -372,7 +464,8 @@ def run_ours(args, w):
     ms_max = float(t_local.item())
     ms_step = ms_max / args.steps
     edges = edges_per_inference(w, B)
-    value = world * edges / (ms_step / 1e3)
+    job_edges = edges if cols else world * edges  # cols: all ranks share one batch
+    value = job_edges / (ms_step / 1e3)
 
     ctx.set_timing(False)
     # ---- e2e: host buffers in, result read back, through the public API ---------------
@@ -383,7 +476,7 @@ def run_ours(args, w):
 
         def e2e_step():
             y = sk.CsrMatrix(m, B, host_rp, host_ci, host_v, validate=False)
-            out, tr = sk.relu_forward_sparse(model, y, sk.ForwardOptions(clip=w["clip"]))
+            out, tr = run(y)
             cats = sk.categories(out)
             return cats.nbytes + 8 * (L + 1)
     else:
@@ -411,13 +504,28 @@ def run_ours(args, w):
     if dist is not None:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_step_ms = float(t_e2e.item()) / args.steps
-    e2e_value = world * edges / (e2e_step_ms / 1e3)
+    e2e_value = job_edges / (e2e_step_ms / 1e3)
 
     # ---- roofline of the dominant kernel ---------------------------------------------
     pk, pk_kind = peaks()
     tr = [int(x) for x in trace] if trace is not None else [nnz0] * (L + 1)
     roof = None
-    if w["y0"] == "binary" and len(ktimes):
+    if cols and len(ktimes):
+        # per layer: this rank's block SpGEMM + epilogue (k_spgemm_rows); bytes =
+        # SURVEY §8(d) with the block's rows and weights, the full input Y_k
+        mg = r1 - r0
+        nnzb = [x.nnz() for x in blocks]
+        byts = sum(sparse_layer_bytes(tr[k], tr[k + 1] * mg // m, B, mg, nnzb[k])
+                   for k in range(L) if tr[k] > 0)
+        t_launch = float(np.sum(ktimes)) / args.steps / 1e3
+        achieved = byts / t_launch / 1e9 if t_launch > 0 else 0.0
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "kernel": "k_spgemm_rows (per layer, this rank's output-neuron block)",
+                "algorithmic_bytes": byts, "launch_ms": t_launch * 1e3,
+                "launches_per_inference": len(ktimes) / args.steps,
+                "kernel_share_of_step": float(t_launch * 1e3 / ms_step), "peak_kind": pk_kind}
+    elif w["y0"] == "binary" and len(ktimes):
         # The sparse forward is one k_sparse_engine launch per inference unless the
         # density-adaptive rule hands dense layers to k_dense_engine.  Algorithmic
         # bytes per layer follow SURVEY §8(d) for the representation that layer ran
@@ -489,12 +597,14 @@ def run_ours(args, w):
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if cols else "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded SplitMix64; BASELINE shapes/distributions)",
             "config": {"workload": w["desc"], "neurons": m, "layers": L,
-                       "per_gpu_batch": B, "global_batch": B * world,
-                       "edges_per_inference_per_gpu": edges,
-                       "parallelism": f"batch-row x{world}, replicated W, no data-path collective",
+                       "per_gpu_batch": B if not cols else B, "global_batch": B if cols else B * world,
+                       "edges_per_inference_per_gpu": edges if not cols else edges // world,
+                       "parallelism": (f"column-sharded W x{world}, per-layer NCCL all-gather "
+                                       "of the sparse activations" if cols else
+                                       f"batch-row x{world}, replicated W, no data-path collective"),
                        "l2": "inputs larger than L2 (W %.2f GB + Y0 %.0f MB vs 126 MB L2)"
                              % (sum(nnzW) * 8 / 1e9, nnz0 * 8 / 1e6)},
             "nnz_trace": ([int(x) for x in trace[:6]] + (["..."] if len(trace) > 6 else [])
@@ -520,6 +630,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="rows", choices=["rows", "cols"],
+                    help="N>1 decomposition: batch-row sharding with replicated W (default, no "
+                         "data-path collective) or column sharding of W_k with a per-layer "
+                         "NCCL all-gather of the sparse activations (BASELINE cfg5's layout)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":

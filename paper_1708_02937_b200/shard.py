@@ -119,6 +119,22 @@ def csr_to_torch(a, device):
     return rp.to(torch.int64), ci[:nnz], v[:nnz]
 
 
+def row_block(a, r0: int, r1: int, device):
+    """Rows [r0, r1) of a device CSR as a new handle (device-side slice)."""
+    import torch
+    from . import semikern as skm
+    rp, ci, v = csr_to_torch(a, device)
+    e0, e1 = int(rp[r0].item()), int(rp[r1].item())
+    brp = (rp[r0:r1 + 1] - e0).to(torch.int32).contiguous()
+    bci = ci[e0:e1].contiguous() if e1 > e0 else torch.zeros(1, dtype=torch.int32, device=device)
+    bv = v[e0:e1].contiguous() if e1 > e0 else torch.zeros(1, dtype=torch.float32, device=device)
+    torch.cuda.synchronize(device)
+    out = skm.csr_from_device(r1 - r0, a.cols(), e1 - e0, brp.data_ptr(), bci.data_ptr(),
+                              bv.data_ptr(), ctx=a.ctx)
+    out.ctx.synchronize()
+    return out
+
+
 def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None, device=None):
     """Column-sharded sparse forward pass.  `w_blocks[k]` is this rank's block
     of output-neuron rows of W_ref[k] (a CsrMatrix m_g x m), `b_blocks[k]` its
