@@ -470,12 +470,14 @@ def run_ours(args, w):
     ctx.set_timing(False)
     # ---- e2e: host buffers in, result read back, through the public API ---------------
     if w["y0"] == "binary":
-        for a in (host_rp, host_ci, host_v):
+        # Y0 is binary: only its pattern crosses the host link (sk_csr_from_pattern)
+        assert np.all(host_v == 1.0), "pattern upload needs a binary Y0"
+        for a in (host_rp, host_ci):
             sk._lib.load().sk_host_register(a.ctypes.data, a.nbytes)
-        h2d = host_rp.nbytes + host_ci.nbytes + host_v.nbytes
+        h2d = host_rp.nbytes + host_ci.nbytes
 
         def e2e_step():
-            y = sk.CsrMatrix(m, B, host_rp, host_ci, host_v, validate=False)
+            y = sk.CsrMatrix.from_pattern(m, B, host_rp, host_ci, 1.0, validate=False)
             out, tr = run(y)
             cats = sk.categories(out)
             return cats.nbytes + 8 * (L + 1)

@@ -130,6 +130,13 @@ sk_status sk_csr_from_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
 sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                             const uint32_t* row_ptr, const uint32_t* col_idx,
                             const float* values, int validate, sk_csr** out);
+/* Pattern-only construction (no reference counterpart; the binary activation
+ * matrices of the Graph Challenge inputs and gen_input carry no information in
+ * their values): the host sends row_ptr and col_idx, every stored value is
+ * `value` (filled on the device). Same validation as sk_csr_from_parts. */
+sk_status sk_csr_from_pattern(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                              const uint32_t* row_ptr, const uint32_t* col_idx,
+                              float value, int validate, sk_csr** out);
 sk_status sk_csr_shape(const sk_csr* a, uint32_t* rows, uint32_t* cols,
                        size_t* nnz);
 /* extractTuples / span accessors (matrix.hpp:99-108): D2H copy of the three

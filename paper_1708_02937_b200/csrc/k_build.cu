@@ -266,9 +266,19 @@ extern "C" sk_status sk_csr_from_triples(sk_ctx* ctx, uint32_t rows, uint32_t co
   });
 }
 
-extern "C" sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols,
-                                       const uint32_t* rp, const uint32_t* ci,
-                                       const float* v, int validate, sk_csr** out) {
+namespace sk {
+__global__ void k_fill_f32(float* p, size_t n, float x) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    p[i] = x;
+}
+}  // namespace sk
+
+// Shared by sk_csr_from_parts (values from the host) and sk_csr_from_pattern
+// (v == nullptr: every stored value is `fill`, written on the device).
+static sk_status csr_from_host(sk_ctx* ctx, uint32_t rows, uint32_t cols, const uint32_t* rp,
+                               const uint32_t* ci, const float* v, float fill, int validate,
+                               sk_csr** out) {
   return guarded([&] {
     if (!ctx) fail(SK_ERR_INVALID_ARGUMENT, "null context");
     SK_CUDA(cudaSetDevice(ctx->device));
@@ -279,7 +289,10 @@ extern "C" sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols
                             ctx->stream));
     if (nnz) {
       SK_CUDA(cudaMemcpyAsync(a->ci, ci, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
-      SK_CUDA(cudaMemcpyAsync(a->v, v, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+      if (v)
+        SK_CUDA(cudaMemcpyAsync(a->v, v, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+      else
+        SK_LAUNCH(k_fill_f32, grid_for(ctx, nnz), 256, 0, ctx->stream, a->v, nnz, fill);
     }
     if (validate && rows) {
       unsigned long long* bad = reinterpret_cast<unsigned long long*>(ctx->d_u64);
@@ -307,6 +320,22 @@ extern "C" sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols
     sync(ctx);  // host arrays are borrowed only for the call
     *out = a;
   });
+}
+
+extern "C" sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                       const uint32_t* rp, const uint32_t* ci,
+                                       const float* v, int validate, sk_csr** out) {
+  if (!v && rp && rp[rows] != 0) {
+    set_last_error("null values array");
+    return SK_ERR_INVALID_ARGUMENT;
+  }
+  return csr_from_host(ctx, rows, cols, rp, ci, v, 0.0f, validate, out);
+}
+
+extern "C" sk_status sk_csr_from_pattern(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                         const uint32_t* rp, const uint32_t* ci, float value,
+                                         int validate, sk_csr** out) {
+  return csr_from_host(ctx, rows, cols, rp, ci, nullptr, value, validate, out);
 }
 
 // ==== to_dense / from_dense / nnz ====================================================

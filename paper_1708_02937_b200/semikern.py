@@ -323,6 +323,25 @@ class CsrMatrix:
     def from_parts_unchecked(rows, cols, row_ptr, col_idx, values, ctx=None) -> "CsrMatrix":
         return CsrMatrix(rows, cols, row_ptr, col_idx, values, validate=False, ctx=ctx)
 
+    @staticmethod
+    def from_pattern(rows, cols, row_ptr, col_idx, value: float = 1.0, *, validate=True,
+                     ctx=None) -> "CsrMatrix":
+        """Pattern-only upload: every stored value is `value` (set on the device),
+        so only row_ptr and col_idx cross the host link (binary activations)."""
+        c = _ctx(ctx)
+        rp, ci = _u32(row_ptr), _u32(col_idx)
+        if validate:
+            if rp.size != rows + 1:
+                raise InvalidArgument("row_ptr length must be rows+1")
+            if rp[0] != 0:
+                raise InvalidArgument("row_ptr[0] must be 0")
+            if rp[-1] != ci.size:
+                raise InvalidArgument("row_ptr[rows] and col_idx disagree on nnz")
+        h = vp()
+        _check(c._L.sk_csr_from_pattern(c.h, rows, cols, rp.ctypes.data, ci.ctypes.data,
+                                        float(value), int(validate), C.byref(h)))
+        return CsrMatrix(rows, cols, ctx=c, _handle=h)
+
     def rows(self) -> int:
         return self._rows
 

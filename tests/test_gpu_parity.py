@@ -100,6 +100,18 @@ def test_csr_from_triples_matches_reference(sk, ref):
     assert e.nnz() == 0 and e.row_ptr().tolist() == [0, 0, 0]
 
 
+def test_csr_from_pattern(sk, port):
+    Y = port.gen_input_binary(4096, 700, 50, 3)
+    a = sk.CsrMatrix.from_pattern(Y.rows, Y.cols, Y.row_ptr, Y.col_idx, 1.0)
+    assert_csr_bitwise(a, Y)
+    b = sk.CsrMatrix.from_pattern(2, 3, [0, 1, 3], [2, 0, 1], -0.5)
+    assert b.values().tolist() == [-0.5, -0.5, -0.5] and b.col_idx().tolist() == [2, 0, 1]
+    with pytest.raises(sk.InvalidArgument):
+        sk.CsrMatrix.from_pattern(1, 2, [0, 2], [1, 0], 1.0)  # not increasing
+    e = sk.CsrMatrix.from_pattern(3, 3, [0, 0, 0, 0], [], 1.0)
+    assert e.nnz() == 0
+
+
 def test_validating_constructor_messages(sk):
     kat = json.load(open(os.path.join(GOLDEN, "kat.json")))["validate_errors"]
     cases = {"not_monotone": (3, 2, [0, 1, 0, 1], [0], [1.0]),
