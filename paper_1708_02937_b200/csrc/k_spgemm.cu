@@ -718,8 +718,8 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
       __syncwarp();
     }
     if (any) {
-      // candidates of windows without survivors were never cleared above
-      for (uint32_t q = lane; q < np * SW; q += 32) cand[q] = 0u;
+      // (candidate words are already zero: windows without candidates never set
+      // any, and the emit leaves the others cleared)
       for (uint32_t t = lane * 4; t < S; t += 128)
         *reinterpret_cast<uint4*>(acc + t) = make_uint4(clearw, clearw, clearw, clearw);
     }

@@ -13,12 +13,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1708_02937_b200 as sk  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--workload", default="cfg4", choices=["cfg3", "cfg4"])
+ap.add_argument("--workload", default="cfg4", choices=["cfg3", "cfg4", "cfg5"])
 ap.add_argument("--layers", type=int, default=2)
 ap.add_argument("--batch", type=int, default=60000)
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
-m, dens, bias = {"cfg3": (16384, 0.015, -0.3), "cfg4": (65536, 0.004, -0.35)}[a.workload]
+m, dens, bias = {"cfg3": (16384, 0.015, -0.3), "cfg4": (65536, 0.004, -0.35),
+                  "cfg5": (262144, 0.001, -0.45)}[a.workload]
 Ws = [sk.gen_layer_fixed(m, 32, sk.layer_seed(42, k), 1.0 / 16) for k in range(a.layers)]
 model = sk.DnnModel(Ws, [np.full(m, bias, np.float32)] * a.layers)
 Y0 = sk.gen_input_binary(m, a.batch, int(round(dens * m)), 42)
