@@ -146,12 +146,44 @@ __device__ __forceinline__ unsigned long long reserve(const RowArgs& p, uint64_t
   return off;
 }
 
+// One application step: up to 32 products (lane j holds product j of the step,
+// products in flattened = ascending-k order).  Lanes that hit the same sample
+// are grouped by __match_any_sync and apply in rounds by rank, i.e. in lane
+// order = ascending k; first touches append to the touched list.
+template <typename Ops>
+__device__ __forceinline__ void apply_step(const RowArgs& p, const WarpSmem& ws, int lane,
+                                           bool act, uint32_t s_loc, float prod, uint32_t cap,
+                                           uint32_t& T) {
+  const uint32_t key = act ? s_loc : (0x80000000u | uint32_t(lane));
+  const uint32_t mm = __match_any_sync(0xffffffffu, key);
+  const uint32_t rank = __popc(mm & lanemask_lt(lane));
+  const uint32_t rounds = __reduce_max_sync(0xffffffffu, act ? __popc(mm) : 1u);
+  for (uint32_t r = 0; r < rounds; ++r) {
+    bool first = false;
+    if (act && rank == r) {
+      const uint32_t x = ws.acc[s_loc];
+      first = x == kSent;
+      const float xf = first ? Ops::zero() : __uint_as_float(x);
+      uint32_t nx = __float_as_uint(Ops::add(xf, prod, p.err));
+      if (Ops::kind != SK_ARITHMETIC && nx == kSent) nx = 0x7fffffffu;
+      ws.acc[s_loc] = nx;
+    }
+    const uint32_t fm = __ballot_sync(0xffffffffu, first);
+    if (first) {
+      const uint32_t pos = T + __popc(fm & lanemask_lt(lane));
+      if (pos < cap) ws.list[pos] = uint16_t(s_loc);
+    }
+    T += __popc(fm);
+    __syncwarp();
+  }
+}
+
 // Fold one in-edge chunk's window slices into the accumulator, in ascending k.
-// Lane l owns in-edge l of the chunk (weight a, slice [beg, beg+cnt)).  The
-// slices are expanded lane-parallel into the warp's staging buffer in
-// flattened (ascending k, ascending sample) order, then applied 32 at a time;
-// products of one step that hit the same sample are applied in rounds by rank,
-// i.e. lane order = ascending k.
+// Lane l owns in-edge l of the chunk (weight a, slice [beg, beg+cnt)).  Up to
+// 32 products are taken directly (lane j finds the owner of product j by a
+// shuffle binary search over the slice offsets); larger chunks are expanded
+// lane-parallel into the warp's staging buffer in flattened (ascending k,
+// ascending sample) order and applied 32 at a time.
 template <typename Ops>
 __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws, int lane,
                                            uint32_t wbase, float a, uint32_t beg, uint32_t cnt,
@@ -162,6 +194,24 @@ __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws,
   if (total == 0) return;
   any = true;
   const uint32_t excl = incl - cnt;
+  if (total <= 32) {
+    const uint32_t j = uint32_t(lane);
+    uint32_t o = 0;
+#pragma unroll
+    for (uint32_t st = 16; st; st >>= 1)
+      if (__shfl_sync(0xffffffffu, excl, o + st) <= j) o += st;
+    const uint32_t off = __shfl_sync(0xffffffffu, beg - excl, o);
+    const float ao = __shfl_sync(0xffffffffu, a, o);
+    const bool act = j < total;
+    uint32_t s_loc = 0;
+    float prod = 0.0f;
+    if (act) {
+      s_loc = __ldg(p.bci + j + off) - wbase;
+      prod = Ops::mul(ao, __ldg(p.bv + j + off), p.err);
+    }
+    apply_step<Ops>(p, ws, lane, act, s_loc, prod, cap, T);
+    return;
+  }
   for (uint32_t base = 0; base < total; base += kStage) {
     // ---- expansion: this lane's entries whose flattened index is in the batch
     const uint32_t lo = max(excl, base), hi = min(excl + cnt, base + kStage);
@@ -189,33 +239,12 @@ __device__ __forceinline__ void fold_chunk(const RowArgs& p, const WarpSmem& ws,
     __syncwarp();
     // ---- application, 32 staged products per step
     const uint32_t nb = min(kStage, total - base);
+#pragma unroll 1
     for (uint32_t t = 0; t < nb; t += 32) {
       const uint32_t j = t + lane;
       const bool act = j < nb;
-      const uint32_t s_loc = act ? uint32_t(ws.st_s[j]) : 0u;
-      const float prod = act ? ws.st_p[j] : 0.0f;
-      const uint32_t key = act ? s_loc : (0x80000000u | uint32_t(lane));
-      const uint32_t mm = __match_any_sync(0xffffffffu, key);
-      const uint32_t rank = __popc(mm & lanemask_lt(lane));
-      const uint32_t rounds = __reduce_max_sync(0xffffffffu, act ? __popc(mm) : 1u);
-      for (uint32_t r = 0; r < rounds; ++r) {
-        bool first = false;
-        if (act && rank == r) {
-          const uint32_t x = ws.acc[s_loc];
-          first = x == kSent;
-          const float xf = first ? Ops::zero() : __uint_as_float(x);
-          uint32_t nx = __float_as_uint(Ops::add(xf, prod, p.err));
-          if (Ops::kind != SK_ARITHMETIC && nx == kSent) nx = 0x7fffffffu;
-          ws.acc[s_loc] = nx;
-        }
-        const uint32_t fm = __ballot_sync(0xffffffffu, first);
-        if (first) {
-          const uint32_t pos = T + __popc(fm & lanemask_lt(lane));
-          if (pos < cap) ws.list[pos] = uint16_t(s_loc);
-        }
-        T += __popc(fm);
-        __syncwarp();
-      }
+      apply_step<Ops>(p, ws, lane, act, act ? uint32_t(ws.st_s[j]) : 0u,
+                      act ? ws.st_p[j] : 0.0f, cap, T);
     }
   }
 }
@@ -329,6 +358,7 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
   }
   if (!kExact && !dense_row && T <= cap) {
     // sparse epilogue over the touched list; survivors -> bitmap -> ordered emit
+    bool anykeep = false;
     for (uint32_t t = lane; t < T; t += 32) {
       const uint32_t s = ws.list[t];
       const uint32_t x = ws.acc[s];
@@ -343,6 +373,12 @@ __device__ __forceinline__ void emit_window(const RowArgs& p, const WarpSmem& ws
       }
       ws.acc[s] = keep ? __float_as_uint(z) : kSent;
       if (keep) atomicOr(&ws.surv[s >> 5], 1u << (s & 31));
+      anykeep |= keep;
+    }
+    if (!__any_sync(0xffffffffu, anykeep)) {  // nothing survives (common in decaying layers)
+      if (lane == 0) p.item_cnt[it] = 0;
+      __syncwarp();
+      return;
     }
     __syncwarp();
     const uint32_t nwords = (wlen + 31) >> 5;
@@ -475,6 +511,17 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
     a1 = p.av[eb + 32 + lane];
   }
   const uint32_t nchunks = p.b_empty ? 0u : (deg + 31) / 32;
+  // window-table entries of the first in-edge chunk for the whole group: one
+  // (usually single-line) load burst instead of two dependent loads per window
+  uint32_t wq0 = 0, wq1 = 0, wq2 = 0, wq3 = 0, wq4 = 0;
+  if (nchunks && uint32_t(lane) < deg) {
+    const uint32_t* wk = p.wp + size_t(k0) * p.nW + w0;
+    wq0 = wk[0];
+    wq1 = wk[1];
+    if (wn >= 2) wq2 = wk[2];
+    if (wn >= 3) wq3 = wk[3];
+    if (wn >= 4) wq4 = wk[4];
+  }
 #pragma unroll 1
   for (uint32_t gw = 0; gw < wn; ++gw) {
     const uint32_t w = w0 + gw;
@@ -498,11 +545,15 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
         aa = valid ? p.av[e] : 0.0f;
       }
       uint32_t beg = 0, cnt = 0;
-      if (valid) {
+      if (c == 0) {
+        beg = gw == 0 ? wq0 : gw == 1 ? wq1 : gw == 2 ? wq2 : wq3;
+        cnt = (gw == 0 ? wq1 : gw == 1 ? wq2 : gw == 2 ? wq3 : wq4) - beg;
+      } else if (valid) {
         const uint32_t* wk = p.wp + size_t(kk) * p.nW + w;
         beg = wk[0];
         cnt = wk[1] - beg;
       }
+      if (!__any_sync(0xffffffffu, cnt != 0)) continue;  // no entries in this window
       if (kExact)
         fold_chunk_exact(p, ws, wbase, aa, beg, cnt, any);
       else

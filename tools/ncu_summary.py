@@ -14,7 +14,7 @@ def ncu(*a):
 
 
 raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
-hdr, vals = raw[0], raw[2]
+hdr, units, vals = raw[0], raw[1], raw[2]
 want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -26,9 +26,9 @@ want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum",
         "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
         "smsp__issue_active.avg.pct_of_peak_sustained_active"]
-for h, v in zip(hdr, vals):
+for h, un, v in zip(hdr, units, vals):
     if h in want:
-        print(f"{h:70s} {v}")
+        print(f"{h:70s} {v} {un}")
 sass = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source", "sass"))))
 h2 = sass[1]
 ix = {h: i for i, h in enumerate(h2)}
