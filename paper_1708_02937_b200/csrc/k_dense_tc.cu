@@ -12,17 +12,18 @@
 // tensor core can never reproduce the fp32 fold bitwise, which is why the
 // sparse leg (K1/K3) is the bitwise path and this leg is tolerance-checked.
 //
-// Structure (one CTA = one 128x128 output tile, 4 warps):
-//  * mainloop over K in 32-wide slabs, two smem stages.  All 128 threads load
-//    the A (128x32) and B (32x128, staged transposed) slabs, both K-major,
-//    split them, and store hi/lo copies in the no-swizzle canonical UMMA
-//    layouts (8-row x 16-byte core matrices); fence.proxy.async makes the
-//    generic-proxy writes visible to the tensor core;
-//  * one elected thread issues 3 x 4 tcgen05.mma.cta_group::1.kind::tf32
-//    (M=128, N=128, K=8) per slab and tcgen05.commit's them to the stage's
-//    mbarrier, so loading slab t+1 overlaps the MMAs of slab t;
-//  * epilogue: each warp reads its 32 TMEM lanes (= 32 output rows) with
-//    tcgen05.ld.32x32b.x32, adds the bias, applies the ReLU select, stores.
+// Two kernels (SK_TC_VER selects; 3 is the default):
+//  * v3 (k_pack_split + k_gemm_packed): each operand is split ONCE by a pack
+//    kernel that writes hi/lo directly in the canonical K-major UMMA layout,
+//    tile by tile; the GEMM is a pure pipeline -- one producer thread issues
+//    four 1-D cp.async.bulk copies per 16-k stage into a 4-stage shared-memory
+//    ring (completion counted on the stage mbarrier), one thread issues the
+//    3 x 2 tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=256, K=8) and commits
+//    to the stage's "empty" barrier, four warps drain the TMEM accumulator
+//    (bias + ReLU fused).  Tensor pipe ~93 % active (profiles/r01/k4_packed_*).
+//  * v1 (k_gemm_tf32x3, SK_TC_VER=1 or SK_TC_DBG): one CTA per 128x128 tile,
+//    all threads load, split and store each slab (register double buffering),
+//    one thread issues the MMAs; kept for bring-up/debug (descriptor overrides).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -325,268 +326,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
 }
 
-// ---- v2: warp-specialised pipeline ----------------------------------------------------
-// NCW converter warps load slabs (global -> registers, one slab ahead), split
-// them into hi/lo and store the canonical K-major layouts into an NS-stage
-// shared-memory ring; one MMA warp waits on the stage's "full" barrier, issues
-// the 3 x (BK/8) tcgen05.mma (M=128, N=BN, K=8) and commits to the stage's
-// "empty" barrier, so staging runs up to NS slabs ahead of the tensor core and
-// no thread waits on a block-wide barrier in the main loop.  BN = 256 halves
-// the A traffic per FLOP (one M=128 x N=256 instruction).  Epilogue: the
-// converter warps read the accumulator (warp w: TMEM lanes 32*(w%4), columns
-// half (w/4)), add bias, ReLU, store.
-template <int BN_, int BK, int NS, int NCW>
-struct Cfg2 {
-  static constexpr int kConvThreads = NCW * 32;
-  static constexpr int kThreads = kConvThreads + 32;  // + MMA warp
-  static constexpr uint32_t KC = BK / 4;
-  static constexpr uint32_t kA = BM * BK * 4;         // one A copy (hi or lo)
-  static constexpr uint32_t kB = BN_ * BK * 4;        // one B copy
-  static constexpr uint32_t kStage = 2 * kA + 2 * kB;
-  static constexpr uint32_t kSmem = NS * kStage + 1024;
-  static constexpr uint32_t LBO = 128, SBO = KC * 128;
-  static constexpr int NJA = int(BM * KC) / kConvThreads;   // A 16-B chunks per thread
-  static constexpr int NJB = int(BN_ * KC) / kConvThreads;  // B chunks per thread
-  static_assert(NJA * kConvThreads == int(BM * KC), "A chunks");
-  static_assert(NJB * kConvThreads == int(BN_ * KC), "B chunks");
-  static constexpr uint32_t kTmemCols = BN_ <= 128 ? 128 : 256;
-};
-
-__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
-}
-
-template <int BN_, int BK, int NS, int NCW>
-__global__ void __launch_bounds__(Cfg2<BN_, BK, NS, NCW>::kThreads, 1)
-    k_gemm_tf32x3_ws(const float* __restrict__ A, const float* __restrict__ B, uint32_t M,
-                     uint32_t K, uint32_t N, const float* __restrict__ bias, int relu,
-                     float* __restrict__ C, int dbg) {
-  using G = Cfg2<BN_, BK, NS, NCW>;
-  constexpr uint32_t KC = G::KC;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t full[NS], empty[NS], done;
-  __shared__ uint32_t tmem_slot;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN_;
-  const uint32_t sbase = (smem_u32(smem) + 1023) & ~1023u;
-  const uint32_t nk = (K + BK - 1) / BK;
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_slot)), "r"(G::kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(smem_u32(&full[s]), NCW);  // one arrival per converter warp
-      mbar_init(smem_u32(&empty[s]), 1);   // tcgen05.commit
-    }
-    mbar_init(smem_u32(&done), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = tmem_slot;
-
-  if (warp == NCW) {
-    // ---------------- MMA warp ----------------
-    if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(BM, BN_);
-      for (uint32_t t = 0; t < nk; ++t) {
-        const uint32_t s = t % NS;
-        mbar_wait(smem_u32(&full[s]), (t / NS) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t st = sbase + s * G::kStage;
-        const uint32_t a_hi = st, a_lo = st + G::kA, b_hi = st + 2 * G::kA,
-                       b_lo = st + 2 * G::kA + G::kB;
-#pragma unroll
-        for (uint32_t kk = 0; kk < BK / 8; ++kk) {
-          if (dbg == 2) break;  // diagnostics: staging only
-          const uint32_t o = kk * 2 * G::LBO;  // K=8 = two 16-byte k-chunks
-          const uint32_t acc0 = (t | kk) ? 1u : 0u;
-          mma_tf32(tmem, umma_desc(a_hi + o, G::LBO, G::SBO), umma_desc(b_hi + o, G::LBO, G::SBO),
-                   idesc, acc0);
-          mma_tf32(tmem, umma_desc(a_hi + o, G::LBO, G::SBO), umma_desc(b_lo + o, G::LBO, G::SBO),
-                   idesc, 1u);
-          mma_tf32(tmem, umma_desc(a_lo + o, G::LBO, G::SBO), umma_desc(b_hi + o, G::LBO, G::SBO),
-                   idesc, 1u);
-        }
-        mma_commit(smem_u32(&empty[s]));
-      }
-      mma_commit(smem_u32(&done));
-    }
-    __syncwarp();
-  } else {
-    // ---------------- converter warps ----------------
-    // A: chunk c = (row r, k-chunk kc), 8 consecutive lanes take 8 rows of one
-    // k-chunk (their 16-byte stores fill one 128-byte core-matrix row band:
-    // conflict-free).  B: thread = one 4(n) x 4(k) block, loaded as four
-    // float4 rows along n (coalesced) and transposed in registers into four
-    // K-major chunks; the store order is rotated per lane pair so that each
-    // quarter-warp's 16-byte stores hit distinct banks.  Two slabs of loads are
-    // kept in flight (register ring of depth 2).
-    static_assert(BN_ % 64 == 0 && BK == 16 && NCW == 8, "converter mapping");
-    constexpr int NJA2 = int(BM * KC) / G::kConvThreads;  // 2
-    struct Slab {
-      float4 a[NJA2];
-      float4 b[4];
-    };
-    const uint32_t bn = uint32_t(tid) % (BN_ / 4), bkc = uint32_t(tid) / (BN_ / 4);
-    constexpr uint32_t kBThreads = (BN_ / 4) * KC;  // threads holding a B block
-    auto load_slab = [&](uint32_t t, Slab& sl) {
-      const uint32_t k0 = t * BK;
-#pragma unroll
-      for (int j = 0; j < NJA2; ++j) {
-        const uint32_t c = uint32_t(j) * G::kConvThreads + tid;
-        const uint32_t kc = (c >> 3) & (KC - 1), r = (c >> 5) * 8 + (c & 7);
-        const uint32_t gr = m0 + r, gk = k0 + kc * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gr < M) {
-          const float* src = A + size_t(gr) * K + gk;
-          if (gk + 3 < K && (K & 3) == 0) {
-            v = __ldg(reinterpret_cast<const float4*>(src));
-          } else {
-            if (gk + 0 < K) v.x = __ldg(src + 0);
-            if (gk + 1 < K) v.y = __ldg(src + 1);
-            if (gk + 2 < K) v.z = __ldg(src + 2);
-            if (gk + 3 < K) v.w = __ldg(src + 3);
-          }
-        }
-        sl.a[j] = v;
-      }
-      if (uint32_t(tid) < kBThreads) {
-        const uint32_t gn = n0 + 4 * bn;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t gk = k0 + 4 * bkc + q;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (gk < K) {
-            const float* src = B + size_t(gk) * N + gn;
-            if (gn + 3 < N && (N & 3) == 0) {
-              v = __ldg(reinterpret_cast<const float4*>(src));
-            } else {
-              if (gn + 0 < N) v.x = __ldg(src + 0);
-              if (gn + 1 < N) v.y = __ldg(src + 1);
-              if (gn + 2 < N) v.z = __ldg(src + 2);
-              if (gn + 3 < N) v.w = __ldg(src + 3);
-            }
-          }
-          sl.b[q] = v;
-        }
-      }
-    };
-    auto comp = [](const float4& v, uint32_t i) {
-      return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-    };
-    auto store_slab = [&](uint32_t st, const Slab& sl) {
-#pragma unroll
-      for (int j = 0; j < NJA2; ++j) {
-        const uint32_t c = uint32_t(j) * G::kConvThreads + tid;
-        const uint32_t kc = (c >> 3) & (KC - 1), r = (c >> 5) * 8 + (c & 7);
-        float h[4], l[4];
-        split(sl.a[j].x, h[0], l[0]);
-        split(sl.a[j].y, h[1], l[1]);
-        split(sl.a[j].z, h[2], l[2]);
-        split(sl.a[j].w, h[3], l[3]);
-        const uint32_t off = (r >> 3) * G::SBO + kc * G::LBO + (r & 7) * 16;
-        st_shared_v4(st + off, h[0], h[1], h[2], h[3]);
-        st_shared_v4(st + G::kA + off, l[0], l[1], l[2], l[3]);
-      }
-      if (uint32_t(tid) < kBThreads) {
-#pragma unroll
-        for (uint32_t i = 0; i < 4; ++i) {
-          const uint32_t ii = (i + (bn >> 1)) & 3;  // rotated: conflict-free quarter-warps
-          const uint32_t nr = 4 * bn + ii;
-          float h[4], l[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) split(comp(sl.b[q], ii), h[q], l[q]);
-          const uint32_t off = (nr >> 3) * G::SBO + bkc * G::LBO + (nr & 7) * 16;
-          st_shared_v4(st + 2 * G::kA + off, h[0], h[1], h[2], h[3]);
-          st_shared_v4(st + 2 * G::kA + G::kB + off, l[0], l[1], l[2], l[3]);
-        }
-      }
-    };
-    Slab s0, s1;
-    if (nk > 0) load_slab(0, s0);
-    if (nk > 1) load_slab(1, s1);
-#pragma unroll 1
-    for (uint32_t t = 0; t < nk; t += 2) {
-#pragma unroll
-      for (uint32_t u = 0; u < 2; ++u) {
-        const uint32_t tt = t + u;
-        if (tt < nk) {
-          const uint32_t s = tt % NS;
-          if (tt >= NS) mbar_wait(smem_u32(&empty[s]), ((tt / NS) - 1) & 1);
-          if (dbg != 1) {  // diagnostics: dbg 1 = MMA only
-            store_slab(sbase + s * G::kStage, u == 0 ? s0 : s1);
-            if (tt + 2 < nk) load_slab(tt + 2, u == 0 ? s0 : s1);
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&full[s]));
-        }
-      }
-    }
-    // ---- epilogue ----
-    if (nk > 0) mbar_wait(smem_u32(&done), 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t quarter = uint32_t(warp & 3), half = uint32_t(warp >> 2);
-    constexpr uint32_t kCols = BN_ / (NCW / 4);
-    const uint32_t row = m0 + quarter * 32 + lane;
-    const float b = (bias && row < M) ? bias[row] : 0.0f;
-#pragma unroll 1
-    for (uint32_t c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 32) {
-      uint32_t r[32];
-      if (nk > 0) {
-        const uint32_t taddr = tmem + ((quarter * 32) << 16) + c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
-            "tcgen05.wait::ld.sync.aligned;"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-              "=r"(r[31])
-            : "r"(taddr)
-            : "memory");
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) r[q] = 0u;
-      }
-      if (row < M) {
-        float* dst = C + size_t(row) * N + n0 + c0;
-        const bool vec = (N & 3) == 0 && n0 + c0 + 32 <= N;
-        float z[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          z[q] = __uint_as_float(r[q]);
-          if (bias) z[q] = __fadd_rn(z[q], b);
-          if (relu) z[q] = (z[q] < 0.0f) ? 0.0f : z[q];
-        }
-        if (vec) {
-#pragma unroll
-          for (int q = 0; q < 32; q += 4)
-            *reinterpret_cast<float4*>(dst + q) = make_float4(z[q], z[q + 1], z[q + 2], z[q + 3]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (n0 + c0 + q < N) dst[q] = z[q];
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(G::kTmemCols)
-                 : "memory");
-}
-
 // ---- v3: pre-split operands, bulk-copy pipeline -----------------------------------------
 // Splitting inside the GEMM repeats the work once per tile visit (every B tile
 // is split M/128 times) and that staging, not the tensor core, bounds v1/v2.
@@ -852,9 +591,9 @@ void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t 
   }
   static const int ver = [] {
     const char* e = getenv("SK_TC_VER");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 3;
   }();
-  if (ver == 4 && !getenv("SK_TC_DBG")) {
+  if (ver == 3 && !getenv("SK_TC_DBG")) {
     // v3 kernel: pack (split once) + bulk-copy pipeline
     constexpr int BNp = 256, NSp = 4;
     using G = tc::Cfg3<BNp, NSp>;
@@ -884,39 +623,6 @@ void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t 
               bhi, blo, M, N, Kp / tc::kPK, bias, relu, c);
     timing_mark(ctx);
     dfree(ctx, buf);
-    return;
-  }
-  static const int dbg = [] {
-    const char* e = getenv("SK_TC_MODE");  // diagnostics: 1 MMA only, 2 staging only
-    return e ? atoi(e) : 0;
-  }();
-  if (ver >= 2 && !getenv("SK_TC_DBG")) {
-    // v2: warp-specialised, BN = 256 (SK_TC_VER=3: BN = 128)
-    timing_mark(ctx);
-    if (ver == 3) {
-      using G = tc::Cfg2<128, 16, 4, 8>;
-      static bool a2 = false;
-      if (!a2) {
-        SK_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32x3_ws<128, 16, 4, 8>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
-        a2 = true;
-      }
-      dim3 g2(ceil_div(N, 128), ceil_div(M, tc::BM));
-      SK_LAUNCH((tc::k_gemm_tf32x3_ws<128, 16, 4, 8>), g2, G::kThreads, G::kSmem, ctx->stream, a,
-                b, M, K, N, bias, relu, c, dbg);
-    } else {
-      using G = tc::Cfg2<256, 16, 4, 8>;
-      static bool a2 = false;
-      if (!a2) {
-        SK_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32x3_ws<256, 16, 4, 8>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
-        a2 = true;
-      }
-      dim3 g2(ceil_div(N, 256), ceil_div(M, tc::BM));
-      SK_LAUNCH((tc::k_gemm_tf32x3_ws<256, 16, 4, 8>), g2, G::kThreads, G::kSmem, ctx->stream, a,
-                b, M, K, N, bias, relu, c, dbg);
-    }
-    timing_mark(ctx);
     return;
   }
   timing_mark(ctx);
