@@ -462,7 +462,9 @@ extern "C" sk_status sk_layer_step(sk_ctx* ctx, const sk_csr* w, const float* bi
     SK_CUDA(cudaMemcpyAsync(db, bias, size_t(w->rows) * 4, cudaMemcpyHostToDevice,
                             ctx->stream));
     sk_dense* o = new_dense(ctx, w->rows, y->cols);
+    timing_mark(ctx);  // K1 is the layer's only kernel (measurement hook)
     launch_layer_dense(ctx, w, db, y->d, y->cols, opt_clip(opt), o->d);
+    timing_mark(ctx);
     dfree(ctx, db);
     sync(ctx);  // the host bias buffer is borrowed only for this call
     *out = o;
