@@ -242,6 +242,12 @@ sk_status sk_gen_layer_fixed(sk_ctx* ctx, uint32_t m, uint32_t k,
 /* Bernoulli(density) layer with U[-1,1) values (cfg2). */
 sk_status sk_gen_layer_density(sk_ctx* ctx, uint32_t m, double density,
                                uint64_t layer_seed, sk_csr** out);
+/* The reference's gen_weight (matgen.hpp:46, matgen.cpp:50-87) bitwise: m x m
+ * CSR, entry (i,j) present with probability 1/inverse_sparsity, value
+ * float(-1 + 4 u), zeros elided; GenSpec validation messages. Used by the
+ * paper-style sweep (paper_1708_02937_b200/bench_sweep.py). */
+sk_status sk_gen_weight(sk_ctx* ctx, uint32_t m, double inverse_sparsity,
+                        uint64_t seed, sk_csr** out);
 /* Dense U[0,1) neuron-major input = the reference gen_input formula. */
 sk_status sk_gen_input_dense(sk_ctx* ctx, uint32_t m, uint32_t n,
                              uint64_t seed, sk_dense** out);

@@ -113,6 +113,17 @@ class Ref:
         L.skref_gen_weight.argtypes = [C.c_uint32, C.c_double, C.c_uint64, C.c_void_p]
         L.skref_gen_input.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, f32p]
         L.skref_gen_bias.argtypes = [C.c_uint32, C.c_uint64, C.c_int, f32p]
+        vp_, sz = C.c_void_p, C.c_size_t
+        L.skref_bench_analyze.argtypes = [sz, vp_, vp_, vp_, vp_, vp_, C.c_uint32, sz, vp_,
+                                          C.POINTER(sz)]
+        L.skref_bench_records_csv.argtypes = [sz, vp_, vp_, vp_, vp_, vp_, vp_, vp_, vp_,
+                                              C.c_char_p, sz, C.POINTER(sz)]
+        L.skref_bench_params_csv.argtypes = [sz, vp_, vp_, vp_, vp_, vp_, C.c_uint32,
+                                             C.c_char_p, sz, C.POINTER(sz)]
+        L.skref_bench_read_csv.argtypes = [C.c_char_p, sz, vp_, vp_, vp_, vp_, vp_, vp_, vp_,
+                                           vp_, C.POINTER(sz)]
+        L.skref_bench_validate.argtypes = [sz, vp_, sz, vp_, C.c_uint32, C.c_uint32, sz, vp_,
+                                           C.c_int, C.c_int]
         L.skref_to_dense.argtypes = [C.c_void_p, C.c_float, f32p]
 
     def _check(self, rc):
@@ -321,6 +332,81 @@ class Ref:
         out = np.zeros(m, np.float32)
         self._check(self.lib.skref_gen_bias(m, seed, int(uniform01), _p(out, f32p)))
         return out
+
+    # ---- benchmark sweep analysis / CSV (proj/include/semikern/bench.hpp) ----
+
+    @staticmethod
+    def _rec_arrays(records):
+        """records: iterables of (m, is, impl(0 sparse / 1 dense), workers, mean,
+        stddev, nnz, bytes)."""
+        r = list(records)
+        n = len(r)
+        cols = list(zip(*r)) if n else [[]] * 8
+        return (n, np.asarray(cols[0], np.uint32), np.asarray(cols[1], np.float64),
+                np.asarray(cols[2], np.int32), np.asarray(cols[3], np.int32),
+                np.asarray(cols[4], np.float64), np.asarray(cols[5], np.float64),
+                np.asarray(cols[6], np.uint64), np.asarray(cols[7], np.uint64))
+
+    def bench_analyze(self, records, reference_m):
+        n, m, is_, impl, wk, mean, _, _, _ = self._rec_arrays(records)
+        cap = 4096
+        out = np.zeros(9 * cap)
+        cnt = C.c_size_t()
+        self._check(self.lib.skref_bench_analyze(
+            C.c_size_t(n), m.ctypes.data_as(C.c_void_p), is_.ctypes.data_as(C.c_void_p),
+            impl.ctypes.data_as(C.c_void_p), wk.ctypes.data_as(C.c_void_p),
+            mean.ctypes.data_as(C.c_void_p), C.c_uint32(reference_m), C.c_size_t(cap),
+            out.ctypes.data_as(C.c_void_p), C.byref(cnt)))
+        return out[: 9 * cnt.value].reshape(cnt.value, 9)
+
+    def _text(self, fn, *args):
+        cap = 1 << 22
+        buf = C.create_string_buffer(cap)
+        ln = C.c_size_t()
+        self._check(fn(*args, buf, C.c_size_t(cap), C.byref(ln)))
+        return buf.value.decode()
+
+    def bench_records_csv(self, records) -> str:
+        n, m, is_, impl, wk, mean, sd, nnz, byt = self._rec_arrays(records)
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        return self._text(self.lib.skref_bench_records_csv, C.c_size_t(n), ptr(m), ptr(is_),
+                          ptr(impl), ptr(wk), ptr(mean), ptr(sd), ptr(nnz), ptr(byt))
+
+    def bench_params_csv(self, records, reference_m) -> str:
+        n, m, is_, impl, wk, mean, _, _, _ = self._rec_arrays(records)
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        return self._text(self.lib.skref_bench_params_csv, C.c_size_t(n), ptr(m), ptr(is_),
+                          ptr(impl), ptr(wk), ptr(mean), C.c_uint32(reference_m))
+
+    def bench_read_csv(self, text: str):
+        cap = 65536
+        m = np.zeros(cap, np.uint32)
+        is_ = np.zeros(cap)
+        impl = np.zeros(cap, np.int32)
+        wk = np.zeros(cap, np.int32)
+        mean = np.zeros(cap)
+        sd = np.zeros(cap)
+        nnz = np.zeros(cap, np.uint64)
+        byt = np.zeros(cap, np.uint64)
+        cnt = C.c_size_t()
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self.lib.skref_bench_read_csv(
+            C.c_char_p(text.encode()), C.c_size_t(cap), ptr(m), ptr(is_), ptr(impl), ptr(wk),
+            ptr(mean), ptr(sd), ptr(nnz), ptr(byt), C.byref(cnt)))
+        k = cnt.value
+        return [(int(m[i]), float(is_[i]), int(impl[i]), int(wk[i]), float(mean[i]),
+                 float(sd[i]), int(nnz[i]), int(byt[i])) for i in range(k)]
+
+    def bench_validate(self, sizes, inverse_sparsities, batch, layers, workers, repetitions,
+                       warmup):
+        sz = np.asarray(sizes, np.uint32)
+        isx = np.asarray(inverse_sparsities, np.float64)
+        wk = np.asarray(workers, np.int32)
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(self.lib.skref_bench_validate(
+            C.c_size_t(sz.size), ptr(sz), C.c_size_t(isx.size), ptr(isx), C.c_uint32(batch),
+            C.c_uint32(layers), C.c_size_t(wk.size), ptr(wk), C.c_int(repetitions),
+            C.c_int(warmup)))
 
 
 class Port:

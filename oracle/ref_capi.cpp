@@ -25,6 +25,9 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
+#include "semikern/bench.hpp"
 #include "semikern/dnn.hpp"
 #include "semikern/error.hpp"
 #include "semikern/matgen.hpp"
@@ -291,6 +294,115 @@ int skref_gen_bias(uint32_t m, uint64_t seed, int uniform01, float* out) {
     const auto b = gen_bias(GenSpec{m, 1.0, 1, seed},
                             uniform01 ? BiasMode::uniform01 : BiasMode::zero);
     std::memcpy(out, b.data(), b.size() * sizeof(float));
+  });
+}
+
+// ---- benchmark sweep analysis and CSV (proj/include/semikern/bench.hpp) -----------
+
+static std::vector<BenchRecord> records_of(size_t n, const uint32_t* m, const double* is,
+                                           const int* impl, const int* workers,
+                                           const double* mean, const double* sd,
+                                           const uint64_t* nnz, const uint64_t* bytes) {
+  std::vector<BenchRecord> r(n);
+  for (size_t i = 0; i < n; ++i) {
+    r[i].m = m[i];
+    r[i].inverse_sparsity = is[i];
+    r[i].implementation = impl[i] ? Impl::dense : Impl::sparse;
+    r[i].workers = workers[i];
+    r[i].mean_layer_seconds = mean[i];
+    r[i].stddev_seconds = sd ? sd[i] : 0.0;
+    r[i].nnz = nnz ? nnz[i] : 0;
+    r[i].matrix_bytes = bytes ? bytes[i] : 0;
+  }
+  return r;
+}
+
+static void text_out(const std::string& t, char* buf, size_t cap, size_t* len) {
+  *len = t.size();
+  if (buf && cap) {
+    const size_t k = std::min(cap - 1, t.size());
+    std::memcpy(buf, t.data(), k);
+    buf[k] = 0;
+  }
+}
+
+/* analyze (bench.cpp): out[9*j..] = m, ratio_dense, slope, saturation,
+ * blas_per_element, and the four normalized values, per size. */
+int skref_bench_analyze(size_t n, const uint32_t* m, const double* is, const int* impl,
+                        const int* workers, const double* mean, uint32_t ref_m, size_t cap,
+                        double* out, size_t* count) {
+  return guarded([&] {
+    const auto rec = records_of(n, m, is, impl, workers, mean, nullptr, nullptr, nullptr);
+    const auto p = analyze(rec, ref_m);
+    *count = p.size();
+    for (size_t j = 0; j < p.size() && j < cap; ++j) {
+      const double v[9] = {double(p[j].m), p[j].ratio_dense, p[j].slope, p[j].saturation,
+                           p[j].blas_per_element, p[j].ratio_dense_normalized,
+                           p[j].slope_normalized, p[j].saturation_normalized,
+                           p[j].blas_per_element_normalized};
+      std::memcpy(out + 9 * j, v, sizeof v);
+    }
+  });
+}
+
+int skref_bench_records_csv(size_t n, const uint32_t* m, const double* is, const int* impl,
+                            const int* workers, const double* mean, const double* sd,
+                            const uint64_t* nnz, const uint64_t* bytes, char* buf, size_t cap,
+                            size_t* len) {
+  return guarded([&] {
+    std::ostringstream o;
+    write_records_csv(records_of(n, m, is, impl, workers, mean, sd, nnz, bytes), o);
+    text_out(o.str(), buf, cap, len);
+  });
+}
+
+int skref_bench_params_csv(size_t n, const uint32_t* m, const double* is, const int* impl,
+                           const int* workers, const double* mean, uint32_t ref_m, char* buf,
+                           size_t cap, size_t* len) {
+  return guarded([&] {
+    const auto p = analyze(records_of(n, m, is, impl, workers, mean, nullptr, nullptr, nullptr),
+                           ref_m);
+    std::ostringstream o;
+    write_params_csv(p, o);
+    text_out(o.str(), buf, cap, len);
+  });
+}
+
+/* read_records_csv: parsed fields (cap records) or the ParseError message. */
+int skref_bench_read_csv(const char* text, size_t cap, uint32_t* m, double* is, int* impl,
+                         int* workers, double* mean, double* sd, uint64_t* nnz, uint64_t* bytes,
+                         size_t* count) {
+  return guarded([&] {
+    std::istringstream in{std::string(text)};
+    const auto r = read_records_csv(in);
+    *count = r.size();
+    for (size_t i = 0; i < r.size() && i < cap; ++i) {
+      m[i] = r[i].m;
+      is[i] = r[i].inverse_sparsity;
+      impl[i] = r[i].implementation == Impl::dense;
+      workers[i] = r[i].workers;
+      mean[i] = r[i].mean_layer_seconds;
+      sd[i] = r[i].stddev_seconds;
+      nnz[i] = r[i].nnz;
+      bytes[i] = r[i].matrix_bytes;
+    }
+  });
+}
+
+/* BenchConfig::validate on the given fields (bench.cpp). */
+int skref_bench_validate(size_t nsizes, const uint32_t* sizes, size_t nis, const double* is,
+                         uint32_t batch, uint32_t layers, size_t nworkers, const int* workers,
+                         int repetitions, int warmup) {
+  return guarded([&] {
+    BenchConfig c;
+    c.sizes.assign(sizes, sizes + nsizes);
+    c.inverse_sparsities.assign(is, is + nis);
+    c.batch = batch;
+    c.layers = layers;
+    c.workers.assign(workers, workers + nworkers);
+    c.repetitions = repetitions;
+    c.warmup = warmup;
+    c.validate();
   });
 }
 

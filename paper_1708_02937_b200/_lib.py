@@ -39,7 +39,7 @@ EXPORTS = [
     "sk_categories_csr", "sk_categories_dense",
     "sk_sparse_layer", "sk_csr_device_arrays", "sk_csr_from_device", "sk_memcpy_d2d",
     "sk_dense_layer_step", "sk_dense_relu_forward",
-    "sk_gen_layer_fixed", "sk_gen_layer_density", "sk_gen_input_dense",
+    "sk_gen_layer_fixed", "sk_gen_layer_density", "sk_gen_weight", "sk_gen_input_dense",
     "sk_gen_input_binary", "sk_layer_seed",
 ]
 
@@ -123,6 +123,7 @@ def load() -> C.CDLL:
     L.sk_dense_relu_forward.argtypes = [vp, vp, vp, C.POINTER(vp)]
     L.sk_gen_layer_fixed.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint64, C.c_float,
                                      C.POINTER(vp)]
+    L.sk_gen_weight.argtypes = [vp, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(vp)]
     L.sk_gen_layer_density.argtypes = [vp, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(vp)]
     L.sk_gen_input_dense.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(vp)]
     L.sk_gen_input_binary.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,

@@ -805,6 +805,52 @@ __global__ void k_gen_density(uint32_t m, double density, uint64_t sel, uint64_t
   }
 }
 
+__global__ void k_widen_u32(const uint32_t* in, uint64_t* out, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+__global__ void k_narrow_u64(const uint64_t* in, uint32_t* out, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    out[i] = uint32_t(in[i]);
+}
+
+// The reference's own gen_weight (proj/src/matgen.cpp:50-87): entry (i, j) of the
+// m x m CSR owns counter i*m+j of the select and value streams; present iff
+// to_unit(select) < 1/inverse_sparsity, value float(-1 + 4 to_unit(value)),
+// exact zeros elided.  Warp per row, lanes over columns, ballot compaction keeps
+// the columns ascending.  Pass 1 (rp == nullptr) counts, pass 2 writes.
+__global__ void k_gen_weight_ref(uint32_t m, double p, uint64_t sel, uint64_t val,
+                                 const uint32_t* rp, uint32_t* cnt, uint32_t* ci, float* v) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    uint32_t o = rp ? rp[i] : 0u;
+    uint32_t c = 0;
+    for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      bool keep = false;
+      float x = 0.0f;
+      if (j < m) {
+        const uint64_t idx = uint64_t(i) * m + j;
+        if (to_unit(splitmix_at(sel, idx)) < p) {
+          x = float(__dadd_rn(-1.0, __dmul_rn(4.0, to_unit(splitmix_at(val, idx)))));
+          keep = x != 0.0f;
+        }
+      }
+      const uint32_t bm = __ballot_sync(0xffffffffu, keep);
+      if (rp && keep) {
+        const uint32_t pos = o + __popc(bm & ((1u << lane) - 1u));
+        ci[pos] = j;
+        v[pos] = x;
+      }
+      o += __popc(bm);
+      c += __popc(bm);
+    }
+    if (!rp && lane == 0) cnt[i] = c;
+  }
+}
+
 __global__ void k_gen_input_dense(float* y, size_t n, uint64_t stream) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x)
@@ -859,6 +905,44 @@ extern "C" sk_status sk_gen_layer_density(sk_ctx* ctx, uint32_t m, double densit
               a->rp, nullptr, a->ci, a->v);
     dfree(ctx, cnt);
     dfree(ctx, rp);
+    *out = a;
+  });
+}
+
+extern "C" sk_status sk_gen_weight(sk_ctx* ctx, uint32_t m, double inverse_sparsity,
+                                   uint64_t seed, sk_csr** out) {
+  return guarded([&] {
+    SK_CUDA(cudaSetDevice(ctx->device));
+    // GenSpec::validate (matgen.cpp:25-31)
+    if (m < 1) fail(SK_ERR_INVALID_ARGUMENT, "GenSpec: m must be >= 1");
+    if (!(inverse_sparsity >= 1.0))
+      fail(SK_ERR_INVALID_ARGUMENT, "GenSpec: inverse_sparsity must be >= 1");
+    const double p = 1.0 / inverse_sparsity;
+    const uint64_t sel = splitmix_at(seed, 0), val = splitmix_at(seed, 1);  // kWeightSelect/Value
+    uint32_t* cnt = dalloc<uint32_t>(ctx, size_t(m) + 1);
+    unsigned long long* rp64 =
+        reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, size_t(m) + 1));
+    uint64_t* cnt64 = dalloc<uint64_t>(ctx, size_t(m) + 1);
+    SK_LAUNCH(k_gen_weight_ref, grid_for(ctx, size_t(m) * 32), 256, 0, ctx->stream, m, p, sel,
+              val, nullptr, cnt, nullptr, nullptr);
+    SK_LAUNCH(k_widen_u32, grid_for(ctx, m), 256, 0, ctx->stream, cnt, cnt64, m);
+    SK_CUDA(cudaMemsetAsync(cnt64 + m, 0, 8, ctx->stream));
+    exclusive_scan_u64(ctx, cnt64, reinterpret_cast<uint64_t*>(rp64), size_t(m) + 1);
+    const uint64_t nnz = read_u64(ctx, rp64 + m);
+    if (nnz > 0xFFFFFFFFull) {
+      dfree(ctx, cnt);
+      dfree(ctx, rp64);
+      dfree(ctx, cnt64);
+      fail(SK_ERR_INVALID_ARGUMENT, "generated nnz exceeds the 32-bit index range");
+    }
+    sk_csr* a = new_csr(ctx, m, m, nnz);
+    SK_LAUNCH(k_narrow_u64, grid_for(ctx, size_t(m) + 1), 256, 0, ctx->stream,
+              reinterpret_cast<const uint64_t*>(rp64), a->rp, size_t(m) + 1);
+    SK_LAUNCH(k_gen_weight_ref, grid_for(ctx, size_t(m) * 32), 256, 0, ctx->stream, m, p, sel,
+              val, a->rp, nullptr, a->ci, a->v);
+    dfree(ctx, cnt);
+    dfree(ctx, rp64);
+    dfree(ctx, cnt64);
     *out = a;
   });
 }

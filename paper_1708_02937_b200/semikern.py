@@ -729,6 +729,15 @@ def gen_layer_density(m: int, density: float, lseed: int, ctx: Context | None = 
     return CsrMatrix(m, m, ctx=c, _handle=h)
 
 
+def gen_weight(m: int, inverse_sparsity: float, seed: int,
+               ctx: Context | None = None) -> CsrMatrix:
+    """The reference's gen_weight (matgen.cpp:50-87), bitwise, on the device."""
+    c = _ctx(ctx)
+    h = vp()
+    _check(c._L.sk_gen_weight(c.h, m, float(inverse_sparsity), seed, C.byref(h)))
+    return CsrMatrix(m, m, ctx=c, _handle=h)
+
+
 def gen_input_dense(m: int, n: int, seed: int, ctx: Context | None = None) -> DenseMatrix:
     c = _ctx(ctx)
     h = vp()
