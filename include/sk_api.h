@@ -41,7 +41,7 @@ typedef enum sk_status {
   SK_ERR_DIMENSION = 2,        /* semikern::DimensionError */
   SK_ERR_DOMAIN = 3,           /* semikern::DomainError */
   SK_ERR_INVALID_ARGUMENT = 4, /* semikern::InvalidArgument */
-  SK_ERR_PARSE = 5,            /* semikern::ParseError (not used on this path) */
+  SK_ERR_PARSE = 5,            /* semikern::ParseError (Matrix Market reader) */
   SK_ERR_OOM = 6,              /* device allocation failed (cf. SkippedRun, bench.hpp:64-79) */
   SK_ERR_CUDA = 7              /* CUDA runtime failure / no device */
 } sk_status;
@@ -232,6 +232,25 @@ sk_status sk_dense_layer_step(sk_ctx* ctx, const sk_dense* w, const float* bias,
                               const sk_dense* y, sk_dense** out);
 sk_status sk_dense_relu_forward(sk_ctx* ctx, const sk_model* m,
                                 const sk_dense* y0, sk_dense** out);
+
+/* ---- Matrix Market exchange (matio.hpp:23-55, matio.cpp) ---------------
+ * "real general" only: coordinate files yield a CSR (*kind = 0, *csr set),
+ * array files a dense matrix (*kind = 1, *dense set).  The text is parsed on
+ * the host with the reference's rules; the CSR is built on the device.
+ * Malformed input -> SK_ERR_PARSE with "line N: <reference message>";
+ * unreadable path -> SK_ERR "cannot open '<path>' for reading". */
+sk_status sk_read_matrix(sk_ctx* ctx, const char* path, int* kind, sk_csr** csr,
+                         sk_dense** dense);
+/* read_matrix(std::istream&) analogue on an in-memory text. */
+sk_status sk_read_matrix_text(sk_ctx* ctx, const char* text, size_t len, int* kind,
+                              sk_csr** csr, sk_dense** dense);
+/* write_matrix: exactly one of csr / dense; values as %.9g (binary32 round
+ * trips).  sk_format_matrix writes into buf (NUL-terminated, truncated to
+ * cap-1) and returns the full length in *len (the std::ostream overload). */
+sk_status sk_write_matrix(sk_ctx* ctx, const sk_csr* csr, const sk_dense* dense,
+                          const char* path);
+sk_status sk_format_matrix(sk_ctx* ctx, const sk_csr* csr, const sk_dense* dense,
+                           char* buf, size_t cap, size_t* len);
 
 /* ---- BASELINE workload generators (device-side, bitwise equal to
  * oracle/sk_oracle.c) ----------------- */

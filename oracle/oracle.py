@@ -124,6 +124,11 @@ class Ref:
                                            vp_, C.POINTER(sz)]
         L.skref_bench_validate.argtypes = [sz, vp_, sz, vp_, C.c_uint32, C.c_uint32, sz, vp_,
                                            C.c_int, C.c_int]
+        L.skref_read_matrix_text.argtypes = [C.c_char_p, C.POINTER(C.c_int),
+                                             C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                             C.POINTER(vp_), vp_, sz]
+        L.skref_format_matrix.argtypes = [vp_, C.c_uint32, C.c_uint32, vp_, C.c_char_p, sz,
+                                          C.POINTER(sz)]
         L.skref_to_dense.argtypes = [C.c_void_p, C.c_float, f32p]
 
     def _check(self, rc):
@@ -332,6 +337,34 @@ class Ref:
         out = np.zeros(m, np.float32)
         self._check(self.lib.skref_gen_bias(m, seed, int(uniform01), _p(out, f32p)))
         return out
+
+    # ---- Matrix Market (proj/include/semikern/matio.hpp) ----
+
+    def read_matrix_text(self, text: str):
+        """('csr', Csr) or ('dense', ndarray) -- read_matrix(std::istream&)."""
+        kind, r, c = C.c_int(), C.c_uint32(), C.c_uint32()
+        h = C.c_void_p()
+        cap = 1 << 24
+        dense = np.zeros(cap, np.float32)
+        self._check(self.lib.skref_read_matrix_text(
+            text.encode(), C.byref(kind), C.byref(r), C.byref(c), C.byref(h),
+            dense.ctypes.data_as(C.c_void_p), C.c_size_t(cap)))
+        if kind.value == 0:
+            return "csr", self._take(h)
+        return "dense", dense[: r.value * c.value].reshape(r.value, c.value).copy()
+
+    def format_matrix(self, a) -> str:
+        """write_matrix(Matrix, std::ostream&) of a Csr or a dense ndarray."""
+        if isinstance(a, Csr):
+            h = self.handle(a)
+            try:
+                return self._text(self.lib.skref_format_matrix, h, C.c_uint32(0),
+                                  C.c_uint32(0), None)
+            finally:
+                self.free(h)
+        d = np.ascontiguousarray(a, np.float32)
+        return self._text(self.lib.skref_format_matrix, None, C.c_uint32(d.shape[0]),
+                          C.c_uint32(d.shape[1]), d.ctypes.data_as(C.c_void_p))
 
     # ---- benchmark sweep analysis / CSV (proj/include/semikern/bench.hpp) ----
 

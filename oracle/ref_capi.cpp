@@ -28,6 +28,7 @@
 #include <sstream>
 
 #include "semikern/bench.hpp"
+#include "semikern/matio.hpp"
 #include "semikern/dnn.hpp"
 #include "semikern/error.hpp"
 #include "semikern/matgen.hpp"
@@ -294,6 +295,43 @@ int skref_gen_bias(uint32_t m, uint64_t seed, int uniform01, float* out) {
     const auto b = gen_bias(GenSpec{m, 1.0, 1, seed},
                             uniform01 ? BiasMode::uniform01 : BiasMode::zero);
     std::memcpy(out, b.data(), b.size() * sizeof(float));
+  });
+}
+
+static void text_out(const std::string& t, char* buf, size_t cap, size_t* len);
+
+// ---- Matrix Market (proj/include/semikern/matio.hpp) ------------------------------
+
+/* read_matrix(std::istream&): *kind 0 = coordinate (CSR in *csr), 1 = array
+ * (dense copied into `dense` when *rows * *cols <= cap). */
+int skref_read_matrix_text(const char* text, int* kind, uint32_t* rows, uint32_t* cols,
+                           skref_csr** csr, float* dense, size_t cap) {
+  return guarded([&] {
+    std::istringstream in{std::string(text)};
+    Matrix m = read_matrix(in);
+    *rows = m.rows();
+    *cols = m.cols();
+    if (m.is_sparse()) {
+      *kind = 0;
+      *csr = new skref_csr{m.csr()};
+    } else {
+      *kind = 1;
+      const auto d = m.dense().data();
+      if (d.size() <= cap) std::memcpy(dense, d.data(), d.size_bytes());
+    }
+  });
+}
+
+/* write_matrix(Matrix, std::ostream&) of a CSR (csr != null) or a dense matrix. */
+int skref_format_matrix(const skref_csr* csr, uint32_t rows, uint32_t cols, const float* dense,
+                        char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    std::ostringstream o;
+    if (csr)
+      write_matrix(Matrix(csr->m), o);
+    else
+      write_matrix(Matrix(dense_of(rows, cols, dense)), o);
+    text_out(o.str(), buf, cap, len);
   });
 }
 

@@ -39,7 +39,8 @@ EXPORTS = [
     "sk_categories_csr", "sk_categories_dense",
     "sk_sparse_layer", "sk_csr_device_arrays", "sk_csr_from_device", "sk_memcpy_d2d",
     "sk_dense_layer_step", "sk_dense_relu_forward",
-    "sk_gen_layer_fixed", "sk_gen_layer_density", "sk_gen_weight", "sk_gen_input_dense",
+    "sk_gen_layer_fixed", "sk_gen_layer_density", "sk_gen_weight",
+    "sk_read_matrix", "sk_read_matrix_text", "sk_write_matrix", "sk_format_matrix", "sk_gen_input_dense",
     "sk_gen_input_binary", "sk_layer_seed",
 ]
 
@@ -124,6 +125,12 @@ def load() -> C.CDLL:
     L.sk_gen_layer_fixed.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint64, C.c_float,
                                      C.POINTER(vp)]
     L.sk_gen_weight.argtypes = [vp, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(vp)]
+    L.sk_read_matrix.argtypes = [vp, C.c_char_p, C.POINTER(C.c_int), C.POINTER(vp),
+                                 C.POINTER(vp)]
+    L.sk_read_matrix_text.argtypes = [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_int),
+                                      C.POINTER(vp), C.POINTER(vp)]
+    L.sk_write_matrix.argtypes = [vp, vp, vp, C.c_char_p]
+    L.sk_format_matrix.argtypes = [vp, vp, vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
     L.sk_gen_layer_density.argtypes = [vp, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(vp)]
     L.sk_gen_input_dense.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(vp)]
     L.sk_gen_input_binary.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,

@@ -141,7 +141,7 @@ static void sort_pairs(sk_ctx* ctx, uint64_t* kin, uint64_t* kout, uint32_t* vin
 sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                                 const uint32_t* d_r, const uint32_t* d_c,
                                 const float* d_v, size_t n, const uint32_t* h_r,
-                                const uint32_t* h_c) {
+                                const uint32_t* h_c, uint64_t* dup_index) {
   unsigned long long* first_bad = reinterpret_cast<unsigned long long*>(ctx->d_u64);
   // 1. range (matrix.cpp:147-153)
   set_u64(ctx, first_bad, ~0ull);
@@ -175,7 +175,14 @@ sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
   bad = read_u64(ctx, first_bad);
   if (bad != ~0ull) {
     const uint64_t key = read_u64(ctx, k1 + bad);
+    uint32_t orig = 0;  // input position of the later duplicate (the sort is stable)
+    SK_CUDA(cudaMemcpyAsync(&orig, i1 + bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
     for (void* p : {(void*)k0, (void*)k1, (void*)i0, (void*)i1}) dfree(ctx, p);
+    if (dup_index) {  // caller reports it (the Matrix Market reader: by line)
+      *dup_index = orig;
+      return nullptr;
+    }
     fail(SK_ERR_INVALID_ARGUMENT, "duplicate coordinate (" + std::to_string(key >> 32) + ", " +
                                       std::to_string(uint32_t(key)) + ")");
   }

@@ -245,7 +245,8 @@ __device__ __forceinline__ double to_unit(uint64_t bits) {
 sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                                 const uint32_t* d_r, const uint32_t* d_c,
                                 const float* d_v, size_t n,
-                                const uint32_t* h_r, const uint32_t* h_c);
+                                const uint32_t* h_r, const uint32_t* h_c,
+                                uint64_t* dup_index = nullptr);
 sk_csr* csr_transpose(sk_ctx* ctx, const sk_csr* a);
 void ensure_model_tables(sk_ctx* ctx, sk_model* md);
 void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const float* y0,

@@ -417,6 +417,67 @@ class Matrix:
         return self._rep
 
 
+# ---- Matrix Market exchange (matio.hpp) ------------------------------------------------
+
+
+class MatrixFileKind(IntEnum):
+    coordinate = 0
+    array = 1
+
+
+@dataclass
+class MatrixFileInfo:  # matio.hpp:32-38
+    path: str | None
+    kind: MatrixFileKind
+    rows: int
+    cols: int
+    entries: int
+
+
+def _from_read(c, kind, hc, hd) -> "Matrix":
+    if kind.value == 0:
+        return Matrix(CsrMatrix(0, 0, ctx=c, _handle=hc))
+    return Matrix(DenseMatrix(0, 0, ctx=c, _handle=hd))
+
+
+def read_matrix(src, ctx: Context | None = None) -> "Matrix":
+    """read_matrix(path) or read_matrix(file-like) (matio.hpp:46-51): coordinate
+    files yield CSR, array files dense; ParseError carries "line N: ..."."""
+    c = _ctx(ctx)
+    kind, hc, hd = C.c_int(), vp(), vp()
+    if hasattr(src, "read"):
+        text = src.read()
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        _check(c._L.sk_read_matrix_text(c.h, data, len(data), C.byref(kind), C.byref(hc),
+                                        C.byref(hd)))
+    else:
+        _check(c._L.sk_read_matrix(c.h, str(src).encode(), C.byref(kind), C.byref(hc),
+                                   C.byref(hd)))
+    return _from_read(c, kind, hc, hd)
+
+
+def write_matrix(a, dst, ctx: Context | None = None) -> MatrixFileInfo:
+    """write_matrix(a, path) or write_matrix(a, file-like) (matio.hpp:43-44)."""
+    m = a if isinstance(a, Matrix) else Matrix(a)
+    rep = m._rep
+    c = rep.ctx
+    csr_h = rep.h if m.is_sparse() else None
+    dense_h = None if m.is_sparse() else rep.h
+    info = MatrixFileInfo(None, MatrixFileKind.coordinate if m.is_sparse() else
+                          MatrixFileKind.array, m.rows(), m.cols(),
+                          rep.nnz() if m.is_sparse() else m.rows() * m.cols())
+    if hasattr(dst, "write"):
+        n = C.c_size_t()
+        _check(c._L.sk_format_matrix(c.h, csr_h, dense_h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(c._L.sk_format_matrix(c.h, csr_h, dense_h, buf, n.value + 1, C.byref(n)))
+        dst.write(buf.raw[: n.value].decode())
+    else:
+        _check(c._L.sk_write_matrix(c.h, csr_h, dense_h, str(dst).encode()))
+        info.path = str(dst)
+    return info
+
+
 def _unwrap(m):
     return m._rep if isinstance(m, Matrix) else m
 
