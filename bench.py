@@ -547,8 +547,11 @@ def run_ours(args, w):
                   "layer1_achieved_gbs": b1 / (l1_ms / 1e3) / 1e9}
             if n_dense == 0:
                 l1["layers_2_to_L_ms"] = float(stamps[L] - stamps[1]) / 1e6
-        kern = ("k_sparse_engine (persistent: per layer windowed SpGEMM + bias/ReLU/clip + "
-                "prune + compaction)")
+        kern = ("k_exact_layer (order-free fixed-point layer 1, its partial sums provably "
+                "exact) + k_sparse_engine (persistent: per layer windowed SpGEMM + "
+                "bias/ReLU/clip + prune + compaction)") if len(ktimes) > args.steps else \
+            ("k_sparse_engine (persistent: per layer windowed SpGEMM + bias/ReLU/clip + "
+             "prune + compaction)")
         if n_dense:
             kern = (f"k_sparse_engine ({L - n_dense} layers) + k_dense_engine ({n_dense} "
                     "layers, fused SpMM + bias/ReLU) via the density-adaptive hand-off")

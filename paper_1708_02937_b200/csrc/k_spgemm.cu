@@ -41,6 +41,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <climits>
 
@@ -52,6 +53,12 @@ namespace sk {
 
 constexpr uint32_t kSent = 0xFFFFFFFFu;  // never produced by FADD (canonical NaN is 0x7fffffff)
 constexpr int kWarps = 8;                // warps per block
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
@@ -826,14 +833,6 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
 // Per-matrix value statistics for the exactness test: the smallest power of
 // two every nonzero value is a multiple of ("granularity", lowbit exponent),
 // the smallest e with |v| < 2^e, and whether any value is not finite.
-struct ValueStats {
-  int lowbit;     // min over nonzero values
-  int ehi;        // max over nonzero values
-  int nonfinite;  // any Inf/NaN
-  int maxdeg;     // max stored entries per row (weights only)
-  unsigned int vmin, vmax;  // min / max bit pattern over all stored values (equal: constant)
-};
-#define SK_VALUESTATS_INIT {INT_MAX, INT_MIN, 0, 0, 0xFFFFFFFFu, 0u}
 
 __device__ __forceinline__ void value_bits(float v, int& lowbit, int& ehi) {
   const uint32_t b = __float_as_uint(v) & 0x7fffffffu;
@@ -923,20 +922,75 @@ __global__ void k_max_row_len(const uint32_t* rp, uint32_t rows, ValueStats* out
   if ((threadIdx.x & 31) == 0) atomicMax(&out->maxdeg, mx);
 }
 
-__device__ __forceinline__ float pow2f(int e) {
-  return (e >= -126 && e <= 127) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e);
+__host__ __device__ __forceinline__ float pow2f(int e) { return ldexpf(1.0f, e); }
+
+__host__ __device__ __forceinline__ int ceil_log2_deg(int maxdeg) {
+  int lg = 0;
+  while ((1 << lg) < (maxdeg > 1 ? maxdeg : 1)) ++lg;
+  return lg;
 }
 
 // True when every partial sum of W.Y is exactly representable in fp32, so the
 // accumulation order cannot change any bit of the result.
-__device__ __forceinline__ bool products_exact(const ValueStats& w, const ValueStats& y) {
+__host__ __device__ __forceinline__ bool products_exact(const ValueStats& w, const ValueStats& y) {
   if (w.nonfinite || y.nonfinite) return false;
   if (w.lowbit == INT_MAX || y.lowbit == INT_MAX) return true;  // an operand is all zero
-  int lg = 0;
-  while ((1 << lg) < max(w.maxdeg, 1)) ++lg;
-  const int top = lg + w.ehi + y.ehi;     // |partial sum| < 2^top
-  const int gran = w.lowbit + y.lowbit;   // every partial sum is a multiple of 2^gran
+  const int top = ceil_log2_deg(w.maxdeg) + w.ehi + y.ehi;  // |partial sum| < 2^top
+  const int gran = w.lowbit + y.lowbit;  // every partial sum is a multiple of 2^gran
   return gran >= -126 && top <= 127 && top - gran <= 24;
+}
+
+// Fixed-point parameters of the exact path for operand statistics w, y.
+__host__ __device__ __forceinline__ void exact_params(const ValueStats& wst, const ValueStats& yst,
+                                                     uint32_t S, RowArgs& ra) {
+  const bool zero = wst.lowbit == INT_MAX || yst.lowbit == INT_MAX;
+  const int gran = zero ? 0 : wst.lowbit + yst.lowbit;
+  ra.fx_scale = pow2f(-gran);
+  ra.fx_unscale = pow2f(gran);
+  const int range = zero ? 0 : ceil_log2_deg(wst.maxdeg) + wst.ehi + yst.ehi - gran;
+  uint32_t P = range <= 7 ? 4u : (range <= 15 ? 2u : 1u);  // |partial sums| < 2^range
+  while (P > 1 && P * (S / 32) > 384) P >>= 1;             // candidate bitmaps live in st_p
+  ra.fx_pack = P;
+  // binary (constant-valued) inputs: the value array need not be read
+  ra.y_const = yst.vmin == yst.vmax;
+  union {
+    uint32_t u;
+    float f;
+  } cv{yst.vmin};
+  ra.y_cval = cv.f;
+}
+
+// ---- the exact layer as a standalone kernel ------------------------------------------
+// The persistent engine's register and shared-memory budget is set by the
+// ordered path (80 registers, 7.8 KB per warp: 24 warps per SM).  The exact
+// path needs only the accumulator, the touched bitmap of its dense-row fallback
+// and 1 KB of table/candidates, so as its own kernel it runs 32 warps per SM
+// (64 registers, 5.2 KB per warp); the gathered loads it waits on are hidden
+// by more warps.
+__host__ __device__ constexpr size_t exact_warp_bytes(uint32_t S) {
+  return (size_t(S) + S / 32 + 256) * 4;
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long long* stamp) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t S = 1u << p.sh;
+  if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer();
+  uint8_t* base = reinterpret_cast<uint8_t*>(sm) + size_t(wid) * exact_warp_bytes(S);
+  WarpSmem ws;
+  ws.acc = reinterpret_cast<uint32_t*>(base);
+  ws.surv = ws.acc + S;
+  ws.st_p = reinterpret_cast<float*>(ws.surv + S / 32);
+  ws.list = nullptr;
+  ws.st_s = nullptr;
+  const uint32_t cw = fx_clear_word(p.fx_pack);
+  for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
+  for (uint32_t t = lane; t < S / 32; t += 32) ws.surv[t] = 0u;
+  for (uint32_t t = lane; t < 256; t += 32) reinterpret_cast<uint32_t*>(ws.st_p)[t] = 0u;
+  __syncwarp();
+  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  phase_a<OpArith, true, true>(p, ws, lane, gw, nw);
 }
 
 // ---- generic SpGEMM (mxm over any semiring): separate kernels -------------------------
@@ -1061,11 +1115,6 @@ struct EngineArgs {
   unsigned int* nfront;            // L counters, zeroed
 };
 
-__device__ __forceinline__ long long globaltimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 __device__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1148,23 +1197,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     // order-free path (shared atomics, zero-initialised windows) is bitwise the
     // ascending fold.  Decided identically by every warp.
     const bool exact = layer == 0 && p.exact_ok && products_exact(p.wstats[0], *p.y0stats);
-    if (exact) {
-      const ValueStats& wst = p.wstats[0];
-      const ValueStats& yst = *p.y0stats;
-      const bool zero = wst.lowbit == INT_MAX || yst.lowbit == INT_MAX;
-      const int gran = zero ? 0 : wst.lowbit + yst.lowbit;
-      ra.fx_scale = pow2f(-gran);
-      ra.fx_unscale = pow2f(gran);
-      int lg = 0;
-      while ((1 << lg) < max(wst.maxdeg, 1)) ++lg;
-      const int range = zero ? 0 : lg + wst.ehi + yst.ehi - gran;  // |partial sums| < 2^range
-      uint32_t P = range <= 7 ? 4u : (range <= 15 ? 2u : 1u);
-      while (P > 1 && P * (S / 32) > 384) P >>= 1;  // candidate bitmaps live in st_p
-      ra.fx_pack = P;
-      // binary (constant-valued) inputs: the value array need not be read
-      ra.y_const = yst.vmin == yst.vmax;
-      ra.y_cval = __uint_as_float(yst.vmin);
-    }
+    if (exact) exact_params(p.wstats[0], *p.y0stats, S, ra);
     // Near-empty input with every bias <= 0: an output row with no in-edge from
     // an input row holding entries has no entries, so only the frontier rows are
     // processed (and the others' item counts zeroed).  Uniform decision.
@@ -1326,9 +1359,9 @@ static unsigned grid_warps(sk_ctx* ctx, uint64_t warps) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, uint64_t(ctx->num_sms) * 16)));
 }
 
-static uint32_t* build_wp(sk_ctx* ctx, const sk_csr* b, const WinGeom& g) {
+static uint32_t* build_wp(sk_ctx* ctx, const sk_csr* b, const WinGeom& g, bool arena = false) {
   const uint64_t n = uint64_t(b->rows) * g.nW;
-  uint32_t* wp = dalloc<uint32_t>(ctx, n + 1);
+  uint32_t* wp = arena ? aalloc<uint32_t>(ctx, n + 1) : dalloc<uint32_t>(ctx, n + 1);
   SK_LAUNCH(k_build_wp, unsigned(std::min<uint64_t>((n + 256) / 256, uint64_t(ctx->num_sms) * 16)),
             256, 0, ctx->stream, b->rp, b->ci, b->rows, g.nW, g.sh, wp);
   return wp;
@@ -1365,7 +1398,12 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
     return o;
   }
   const WinGeom g = geometry(n);
-  uint32_t* wp_b = build_wp(ctx, b, g);
+  arena_begin(ctx);  // temporaries from the context arena; the output is right-sized
+  struct ArenaScope {
+    sk_ctx* c;
+    ~ArenaScope() { arena_end(c); }
+  } arena_scope{ctx};
+  uint32_t* wp_b = build_wp(ctx, b, g, true);
   unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
   SK_CUDA(cudaMemsetAsync(d, 0, 16, ctx->stream));
   SK_LAUNCH(k_count_products, grid_warps(ctx, m), 256, 0, ctx->stream, a->rp, a->ci, m, b->rp, d);
@@ -1379,14 +1417,12 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   if (cap > 0xFFFFFFFFull)
     fail(SK_ERR_INVALID_ARGUMENT, "mxm result nnz exceeds the 32-bit index range");
   const uint64_t items = uint64_t(m) * g.nW;
-  uint32_t* item_cnt = dalloc<uint32_t>(ctx, items + 1);
+  uint32_t* item_cnt = aalloc<uint32_t>(ctx, items + 1);
   unsigned long long* item_off =
-      reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, items));
-  uint32_t* sc_c = dalloc<uint32_t>(ctx, cap);
-  float* sc_v = dalloc<float>(ctx, cap);
-  uint32_t* wp_out = dalloc<uint32_t>(ctx, items + 1);
-  uint32_t* oc = dalloc<uint32_t>(ctx, cap);
-  float* ov = dalloc<float>(ctx, cap);
+      reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, items));
+  uint32_t* sc_c = aalloc<uint32_t>(ctx, cap);
+  float* sc_v = aalloc<float>(ctx, cap);
+  uint32_t* wp_out = aalloc<uint32_t>(ctx, items + 1);
   int* overflow = reinterpret_cast<int*>(d + 1);
 
   RowArgs p;
@@ -1427,23 +1463,16 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   }
   SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
   exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
-  SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, item_cnt, item_off,
-            wp_out, items, sc_c, sc_v, oc, ov, overflow);
   uint32_t nnz = 0;
+  int ovf = 0;
   SK_CUDA(cudaMemcpyAsync(&nnz, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  SK_CUDA(cudaMemcpyAsync(&ovf, overflow, 4, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
-  sk_csr* o = new sk_csr;
-  o->ctx = ctx;
-  o->rows = m;
-  o->cols = n;
-  o->nnz = nnz;
-  o->rp = dalloc<uint32_t>(ctx, size_t(m) + 1);
-  o->ci = oc;
-  o->v = ov;
+  if (ovf) fail(SK_ERR_INVALID_ARGUMENT, "mxm scratch capacity exceeded");
+  sk_csr* o = new_csr(ctx, m, n, nnz);
+  SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, item_cnt, item_off,
+            wp_out, items, sc_c, sc_v, o->ci, o->v, overflow);
   SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, g.nW, o->rp);
-  for (void* q : {(void*)wp_b, (void*)wp_out, (void*)item_cnt, (void*)item_off, (void*)sc_c,
-                  (void*)sc_v})
-    dfree(ctx, q);
   return o;
 }
 
@@ -1498,6 +1527,7 @@ void ensure_model_tables(sk_ctx* ctx, sk_model* mm) {
   mm->weights_finite = 1;
   for (const ValueStats& v : hs)
     if (v.nonfinite) mm->weights_finite = 0;
+  mm->wstats_host = hs;
 }
 
 // One launch of the sparse engine over layers [k0, L): returns Y after the last
@@ -1505,7 +1535,8 @@ void ensure_model_tables(sk_ctx* ctx, sk_model* mm) {
 // With stop_above > 0 it stops after the first layer with more output entries.
 static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, uint32_t k0,
                               float clip, unsigned long long stop_above,
-                              unsigned long long* trace_out, uint32_t* done) {
+                              unsigned long long* trace_out, uint32_t* done,
+                              const uint32_t* wp_in = nullptr) {
   const uint32_t m = md->neurons, n = y0->cols, Lm = md->layers, L = Lm - k0;
   const WinGeom g = geometry(n);
   const uint64_t items = uint64_t(m) * g.nW;
@@ -1517,7 +1548,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
   // it for A/B measurements.
   static const int exact_env = getenv("SK_NO_EXACT") ? 0 : 1;
   const int exact_ok = exact_env;
-  ValueStats* y0stats = dalloc<ValueStats>(ctx, 1);
+  ValueStats* y0stats = aalloc<ValueStats>(ctx, 1);
   {
     const ValueStats init SK_VALUESTATS_INIT;
     SK_CUDA(cudaMemcpyAsync(y0stats, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
@@ -1551,18 +1582,20 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
   if (per_sm < 1) fail(SK_ERR_CUDA, "sparse engine does not fit on an SM");
   const unsigned grid = unsigned(ctx->num_sms * per_sm);
 
-  uint32_t* wp0 = build_wp(ctx, y0, g);
+  // window table of the input (prebuilt by the exact layer, or built here)
+  uint32_t* wp0 = wp_in ? const_cast<uint32_t*>(wp_in) : build_wp(ctx, y0, g, true);
+  auto free_wp0 = [] {};  // arena memory
   const uint32_t kbw = m / 32 + 1;
   const size_t nsmall = size_t(L) + 1 + L + grid + 4 + (size_t(L) + 1) / 2 + kbw;
   unsigned long long* small =
-      reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, nsmall));
+      reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, nsmall));
   unsigned long long* trace_d = small;
   unsigned long long* bump = small + L + 1;
   unsigned long long* block_sums = bump + L;
   int* flags = reinterpret_cast<int*>(block_sums + grid);  // [0] overflow, [1] result, [2] done
   unsigned int* nfront = reinterpret_cast<unsigned int*>(block_sums + grid + 4);
   uint32_t* kbits = reinterpret_cast<uint32_t*>(block_sums + grid + 4 + (size_t(L) + 1) / 2);
-  uint32_t* frontier = dalloc<uint32_t>(ctx, m);
+  uint32_t* frontier = aalloc<uint32_t>(ctx, m);
 
   for (int attempt = 0; attempt < 2; ++attempt) {
     SK_CUDA(cudaMemsetAsync(small, 0, nsmall * 8, ctx->stream));
@@ -1583,14 +1616,14 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     p.y0_wp = wp0;
     p.nnz0 = y0->nnz;
     for (int q = 0; q < 2; ++q) {
-      p.ci[q] = dalloc<uint32_t>(ctx, cap);
-      p.v[q] = dalloc<float>(ctx, cap);
-      p.wp[q] = dalloc<uint32_t>(ctx, items + 1);
+      p.ci[q] = aalloc<uint32_t>(ctx, cap);
+      p.v[q] = aalloc<float>(ctx, cap);
+      p.wp[q] = aalloc<uint32_t>(ctx, items + 1);
     }
-    p.item_cnt = dalloc<uint32_t>(ctx, items + 1);
-    p.item_off = reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, items));
-    p.sc_c = dalloc<uint32_t>(ctx, cap);
-    p.sc_v = dalloc<float>(ctx, cap);
+    p.item_cnt = aalloc<uint32_t>(ctx, items + 1);
+    p.item_off = reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, items));
+    p.sc_c = aalloc<uint32_t>(ctx, cap);
+    p.sc_v = aalloc<float>(ctx, cap);
     p.cap = cap;
     p.bump = bump;
     p.block_sums = block_sums;
@@ -1621,17 +1654,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     SK_CUDA(cudaMemcpyAsync(trace.data(), trace_d, trace.size() * 8, cudaMemcpyDeviceToHost,
                             ctx->stream));
     sync(ctx);
-    auto release = [&] {
-      for (int q = 0; q < 2; ++q) {
-        dfree(ctx, p.ci[q]);
-        dfree(ctx, p.v[q]);
-        dfree(ctx, p.wp[q]);
-      }
-      dfree(ctx, p.item_cnt);
-      dfree(ctx, p.item_off);
-      dfree(ctx, p.sc_c);
-      dfree(ctx, p.sc_v);
-    };
+    auto release = [] {};  // arena memory: released with the forward call
     const uint32_t ran = hflags[2] ? uint32_t(hflags[2]) : L;
     if (!hflags[0]) {
       const int res = hflags[1];
@@ -1660,10 +1683,6 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
       for (uint32_t k = 0; k <= ran; ++k) trace_out[k] = trace[k];
       *done = ran;
       release();
-      dfree(ctx, wp0);
-      dfree(ctx, small);
-      dfree(ctx, y0stats);
-      dfree(ctx, frontier);
       return o;
     }
     release();
@@ -1676,10 +1695,112 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     if (bigger <= cap) break;
     cap = bigger;  // retry once with the largest capacity memory allows
   }
-  dfree(ctx, wp0);
-  dfree(ctx, small);
-  dfree(ctx, y0stats);
-  dfree(ctx, frontier);
+  fail(SK_ERR_OOM, "sparse forward: activation nnz exceeds the device capacity");
+}
+
+// Value statistics of a CSR's values, on the host (one small launch + sync).
+static ValueStats host_value_stats(sk_ctx* ctx, const sk_csr* y) {
+  ValueStats* d = dalloc<ValueStats>(ctx, 1);
+  const ValueStats init SK_VALUESTATS_INIT;
+  SK_CUDA(cudaMemcpyAsync(d, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+  if (y->nnz)
+    SK_LAUNCH(k_value_stats, grid_warps(ctx, y->nnz / 128 + 1), 256, 0, ctx->stream, y->v,
+              y->nnz, d);
+  ValueStats h;
+  SK_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  dfree(ctx, d);
+  return h;
+}
+
+// Layer k0 on the order-free path as a standalone kernel (k_exact_layer), then
+// the count scan and the gather: the output CSR and its window table (for the
+// engine that continues from layer k0 + 1).
+static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, uint32_t k0,
+                           float clip, const ValueStats& ystats, uint32_t** wp_out_ptr) {
+  const uint32_t m = md->neurons, n = y0->cols;
+  const WinGeom g = geometry(n);
+  const uint64_t items = uint64_t(m) * g.nW;
+  const uint64_t full = uint64_t(m) * n;
+  const sk_csr* w = md->w[k0];
+  uint32_t* wp0 = build_wp(ctx, y0, g, true);
+  static bool attr = false;
+  const size_t smem = size_t(kWarps) * exact_warp_bytes(g.S);
+  if (!attr) {
+    set_smem_attr(k_exact_layer);
+    attr = true;
+  }
+  int per_sm = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exact_layer, kWarps * 32, smem));
+  const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
+  auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
+    c = std::min<unsigned long long>(c, full);
+    c = std::min<unsigned long long>(c, mem_cap);
+    c = std::min<unsigned long long>(c, 0xFFFFFFFFull);
+    return std::max<unsigned long long>(c, 1);
+  };
+  unsigned long long cap = clamp_cap(std::max<unsigned long long>(4ull * y0->nnz, 1ull << 24),
+                                     (unsigned long long)(ctx->total_mem * 0.3 / 24.0));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    uint32_t* item_cnt = aalloc<uint32_t>(ctx, items + 1);
+    unsigned long long* item_off =
+        reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, items));
+    uint32_t* sc_c = aalloc<uint32_t>(ctx, cap);
+    float* sc_v = aalloc<float>(ctx, cap);
+    uint32_t* wp_out = aalloc<uint32_t>(ctx, items + 1);
+    SK_CUDA(cudaMemsetAsync(d, 0, 16, ctx->stream));  // d[0] bump, d[1] overflow flag
+    RowArgs p;
+    p.arp = w->rp;
+    p.aci = w->ci;
+    p.av = w->v;
+    p.bci = y0->ci;
+    p.bv = y0->v;
+    p.wp = wp0;
+    p.b_empty = y0->nnz == 0;
+    p.m = m;
+    p.n = n;
+    p.nW = g.nW;
+    p.sh = g.sh;
+    p.bias = md->bias + size_t(k0) * m;
+    p.clip = clip;
+    p.item_cnt = item_cnt;
+    p.item_off = item_off;
+    p.sc_c = sc_c;
+    p.sc_v = sc_v;
+    p.bump = d;
+    p.cap = cap;
+    p.overflow = reinterpret_cast<int*>(d + 1);
+    p.err = ctx->d_err;
+    exact_params(md->wstats_host[k0], ystats, g.S, p);
+    long long* stamp = (ctx->stamps && k0 < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
+    timing_mark(ctx);
+    SK_LAUNCH(k_exact_layer, grid, kWarps * 32, smem, ctx->stream, p, stamp);
+    SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
+    exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
+    uint32_t nnz = 0;
+    int ovf = 0;
+    SK_CUDA(cudaMemcpyAsync(&nnz, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SK_CUDA(cudaMemcpyAsync(&ovf, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (!ovf) {
+      // the layer's output, right-sized (an owned CSR: the caller releases it)
+      sk_csr* o = new_csr(ctx, m, n, nnz);
+      SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, item_cnt, item_off,
+                wp_out, items, sc_c, sc_v, o->ci, o->v, p.overflow);
+      SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, g.nW,
+                o->rp);
+      timing_mark(ctx);
+      *wp_out_ptr = wp_out;  // arena memory, valid for the rest of the forward call
+      return o;
+    }
+    timing_mark(ctx);
+    size_t free_b = 0, total_b = 0;
+    SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const unsigned long long bigger = clamp_cap(full, (unsigned long long)(free_b * 0.6 / 24.0));
+    if (bigger <= cap) break;
+    cap = bigger;
+  }
   fail(SK_ERR_OOM, "sparse forward: activation nnz exceeds the device capacity");
 }
 
@@ -1722,22 +1843,41 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   float* dbuf[2] = {nullptr, nullptr};
   unsigned long long* counts = nullptr;
   uint32_t k = 0;
-  auto cleanup = [&] {
-    for (float* b : dbuf)
-      if (b) dfree(ctx, b);
-    if (counts) dfree(ctx, counts);
-  };
+  uint32_t* pending_wp = nullptr;  // window table of cur from the exact layer (arena)
+  static const int exact_env = getenv("SK_NO_EXACT") ? 0 : 1;
+  arena_begin(ctx);  // every temporary of this call comes from the context's arena
+  auto cleanup = [&] { arena_end(ctx); };
   try {
     for (;;) {
       if (!(hi && k < L && cur->nnz > hi)) {
+        // a layer whose partial sums are provably exact runs as its own kernel
+        // (k_exact_layer, higher occupancy); the engine continues after it
+        if (exact_env && k < L && cur->nnz) {
+          const ValueStats ys = host_value_stats(ctx, cur);
+          if (products_exact(md->wstats_host[k], ys)) {
+            uint32_t* wp1 = nullptr;
+            sk_csr* r = exact_layer(ctx, md, cur, k, clip, ys, &wp1);
+            if (owned) csr_release(owned);
+            owned = r;
+            cur = r;
+            trace[k + 1] = r->nnz;
+            k += 1;
+            pending_wp = wp1;
+            if (k >= L) break;
+            continue;
+          }
+        }
         uint32_t done = 0;
-        sk_csr* r = sparse_segment(ctx, md, cur, k, clip, hi, trace.data() + k, &done);
+        sk_csr* r = sparse_segment(ctx, md, cur, k, clip, hi, trace.data() + k, &done,
+                                   pending_wp);
+        pending_wp = nullptr;
         if (owned) csr_release(owned);
         owned = r;
         cur = r;
         k += done;
         if (k >= L) break;
       }
+      pending_wp = nullptr;
       // dense segment from layer k: Y_k is scattered into buffer 1, layer k
       // writes buffer 0, and the engine ping-pongs from there
       if (!dbuf[0] && !dense_fits()) {
@@ -1745,9 +1885,9 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
         continue;
       }
       if (!dbuf[0]) {
-        dbuf[0] = dalloc<float>(ctx, full);
-        dbuf[1] = dalloc<float>(ctx, full);
-        counts = reinterpret_cast<unsigned long long*>(dalloc<uint64_t>(ctx, size_t(L) + 1));
+        dbuf[0] = aalloc<float>(ctx, full);
+        dbuf[1] = aalloc<float>(ctx, full);
+        counts = reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, size_t(L) + 1));
       }
       csr_scatter_dense(ctx, cur, dbuf[1]);
       if (owned) {

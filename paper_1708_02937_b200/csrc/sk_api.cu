@@ -20,6 +20,42 @@ void dfree(sk_ctx* ctx, void* p) {
   if (p) cudaFreeAsync(p, ctx->stream);
 }
 
+void arena_begin(sk_ctx* ctx) {
+  if (ctx->arena_depth++ > 0) return;
+  ctx->arena_top = 0;
+  if (ctx->arena_high > ctx->arena_cap) {  // grow once to the last call's high-water mark
+    if (ctx->arena) cudaFreeAsync(ctx->arena, ctx->stream);
+    ctx->arena = nullptr;
+    ctx->arena_cap = 0;
+    const size_t cap = ctx->arena_high + ctx->arena_high / 8;
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, cap, ctx->stream) == cudaSuccess) {
+      ctx->arena = static_cast<uint8_t*>(p);
+      ctx->arena_cap = cap;
+    } else {
+      cudaGetLastError();  // fall back to per-allocation memory this call
+    }
+  }
+}
+
+void* arena_alloc_bytes(sk_ctx* ctx, size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  if (ctx->arena_depth == 0) return dalloc<uint8_t>(ctx, bytes);  // not inside a call
+  const size_t top = ctx->arena_top;
+  ctx->arena_top += bytes;
+  ctx->arena_high = std::max(ctx->arena_high, ctx->arena_top);
+  if (top + bytes <= ctx->arena_cap) return ctx->arena + top;
+  void* p = dalloc<uint8_t>(ctx, bytes);  // spill; the next call's arena covers it
+  ctx->arena_spill.push_back(p);
+  return p;
+}
+
+void arena_end(sk_ctx* ctx) {
+  if (--ctx->arena_depth > 0) return;
+  for (void* p : ctx->arena_spill) dfree(ctx, p);
+  ctx->arena_spill.clear();
+}
+
 sk_dense* new_dense(sk_ctx* ctx, uint32_t rows, uint32_t cols) {
   auto* d = new sk_dense;
   d->ctx = ctx;
@@ -180,6 +216,8 @@ extern "C" sk_status sk_ctx_destroy(sk_ctx* ctx) {
     cudaFreeHost(ctx->h_u64);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
     if (ctx->stamps) cudaFree(ctx->stamps);
+    if (ctx->arena) cudaFreeAsync(ctx->arena, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -188,7 +226,9 @@ extern "C" sk_status sk_ctx_destroy(sk_ctx* ctx) {
 extern "C" sk_status sk_ctx_set_stream(sk_ctx* ctx, void* s) {
   return guarded([&] {
     require_ctx(ctx);
-    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    const cudaStream_t next = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    if (next != ctx->stream) SK_CUDA(cudaStreamSynchronize(ctx->stream));  // arena reuse order
+    ctx->stream = next;
   });
 }
 

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <climits>
 #include <vector>
 
 #include "sk_api.h"
@@ -110,6 +111,14 @@ struct sk_ctx {
   // below sparse_below * m * n (sk_ctx_set_density_switch; dense_above <= 0 = off).
   double dense_above = 1.0 / 32;
   double sparse_below = 1.0 / 128;
+  // Grow-only scratch arena for the temporaries of one forward call (window
+  // tables, item counts, scratch spans, ping-pong buffers): per-call pool
+  // allocations of ~1 GB cost milliseconds of host time with the GPU idle.
+  // Reuse is stream-ordered (set_stream synchronises the previous stream).
+  uint8_t* arena = nullptr;
+  size_t arena_cap = 0, arena_top = 0, arena_high = 0;
+  int arena_depth = 0;
+  std::vector<void*> arena_spill;  // overflow allocations of the current call
 };
 
 struct sk_dense {
@@ -129,6 +138,19 @@ struct sk_csr {
   std::atomic<int> refs{1};
 };
 
+// Per-matrix value statistics (the exactness test of the sparse engine): the
+// smallest power of two every nonzero value is a multiple of ("granularity",
+// lowbit exponent), the smallest e with |v| < 2^e, non-finite values, the
+// longest row, and the min/max value bit patterns (equal: constant values).
+struct ValueStats {
+  int lowbit;     // min over nonzero values
+  int ehi;        // max over nonzero values
+  int nonfinite;  // any Inf/NaN
+  int maxdeg;     // max stored entries per row (weights only)
+  unsigned int vmin, vmax;  // min / max bit pattern over all stored values (equal: constant)
+};
+#define SK_VALUESTATS_INIT {INT_MAX, INT_MIN, 0, 0, 0xFFFFFFFFu, 0u}
+
 struct sk_model {
   sk_ctx* ctx = nullptr;
   uint32_t layers = 0, neurons = 0;
@@ -140,6 +162,7 @@ struct sk_model {
   void* d_wstats = nullptr;          // device per-layer value statistics (exactness test)
   uint8_t* d_bias_nonpos = nullptr;
   int weights_finite = -1;           // every weight finite (-1 = not computed yet)
+  std::vector<ValueStats> wstats_host;  // host copy of d_wstats
 };
 
 namespace sk {
@@ -153,6 +176,16 @@ T* dalloc(sk_ctx* ctx, size_t n) {
   return static_cast<T*>(p);
 }
 void dfree(sk_ctx* ctx, void* p);
+
+// Arena scope (nestable): arena_begin / arena_end bracket one forward call;
+// aalloc memory is valid until the outermost arena_end.
+void arena_begin(sk_ctx* ctx);
+void arena_end(sk_ctx* ctx);
+void* arena_alloc_bytes(sk_ctx* ctx, size_t bytes);
+template <typename T>
+T* aalloc(sk_ctx* ctx, size_t n) {
+  return static_cast<T*>(arena_alloc_bytes(ctx, (n ? n : 1) * sizeof(T)));
+}
 
 sk_dense* new_dense(sk_ctx* ctx, uint32_t rows, uint32_t cols);
 sk_csr* new_csr(sk_ctx* ctx, uint32_t rows, uint32_t cols, size_t nnz);

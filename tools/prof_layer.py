@@ -37,5 +37,5 @@ for r in range(a.reps):
     kt = ctx.kernel_times_ms()
     st = ctx.layer_stamps_ns(a.layers - a.skip + 1).astype(np.float64)
     per = np.round(np.diff(st) / 1e3, 1).tolist()
-    print(f"rep {r}: wall {1e3 * (time.perf_counter() - t):.2f} ms engine {kt[-1]:.3f} ms "
+    print(f"rep {r}: wall {1e3 * (time.perf_counter() - t):.2f} ms kernels {[round(float(x), 3) for x in kt]} ms "
           f"trace {[int(x) for x in trace][:8]} layer_us {per[:8]}", flush=True)
