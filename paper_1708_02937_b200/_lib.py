@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsk_b200.so")
+# SK_LIB_PATH selects an alternative build (tuning experiments only)
+LIB_PATH = os.environ.get("SK_LIB_PATH") or os.path.join(HERE, "libsk_b200.so")
 
 u32p = C.POINTER(C.c_uint32)
 f32p = C.POINTER(C.c_float)
