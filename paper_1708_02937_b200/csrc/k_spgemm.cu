@@ -968,7 +968,8 @@ __host__ __device__ __forceinline__ void exact_params(const ValueStats& wst, con
 // (64 registers, 5.2 KB per warp); the gathered loads it waits on are hidden
 // by more warps.
 __host__ __device__ constexpr size_t exact_warp_bytes(uint32_t S) {
-  return (size_t(S) + S / 32 + 256) * 4;
+  // accumulator | dense-row touched bitmap | in-edge table (128) + candidates (4 S/32)
+  return (size_t(S) + S / 32 + 128 + 4 * (S / 32)) * 4;
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long long* stamp) {
@@ -986,7 +987,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long 
   const uint32_t cw = fx_clear_word(p.fx_pack);
   for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
   for (uint32_t t = lane; t < S / 32; t += 32) ws.surv[t] = 0u;
-  for (uint32_t t = lane; t < 256; t += 32) reinterpret_cast<uint32_t*>(ws.st_p)[t] = 0u;
+  for (uint32_t t = lane; t < 128 + 4 * (S / 32); t += 32)
+    reinterpret_cast<uint32_t*>(ws.st_p)[t] = 0u;
   __syncwarp();
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -1716,10 +1718,27 @@ static ValueStats host_value_stats(sk_ctx* ctx, const sk_csr* y) {
 // Layer k0 on the order-free path as a standalone kernel (k_exact_layer), then
 // the count scan and the gather: the output CSR and its window table (for the
 // engine that continues from layer k0 + 1).
+static WinGeom exact_geometry(uint32_t n) {
+  // the exact layer's own window (SK_EXACT_WINDOW_LOG2 overrides, 8..12)
+  static const int env_sh = [] {
+    const char* e = getenv("SK_EXACT_WINDOW_LOG2");
+    const int v = e ? atoi(e) : 10;
+    return (v >= 8 && v <= 12) ? v : 10;
+  }();
+  int sh = env_sh;
+  while (sh > 7 && (1u << (sh - 1)) >= n) --sh;
+  WinGeom g;
+  g.sh = sh;
+  g.S = 1u << sh;
+  g.nW = std::max<uint32_t>(1, (n + g.S - 1) >> sh);
+  return g;
+}
+
 static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, uint32_t k0,
                            float clip, const ValueStats& ystats, uint32_t** wp_out_ptr) {
   const uint32_t m = md->neurons, n = y0->cols;
-  const WinGeom g = geometry(n);
+  const WinGeom g = exact_geometry(n);
+  const bool same_geometry = g.sh == geometry(n).sh;
   const uint64_t items = uint64_t(m) * g.nW;
   const uint64_t full = uint64_t(m) * n;
   const sk_csr* w = md->w[k0];
@@ -1791,7 +1810,9 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
       SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, g.nW,
                 o->rp);
       timing_mark(ctx);
-      *wp_out_ptr = wp_out;  // arena memory, valid for the rest of the forward call
+      // arena memory, valid for the rest of the forward call; a window table of
+      // another geometry is useless to the engine (it builds its own)
+      *wp_out_ptr = same_geometry ? wp_out : nullptr;
       return o;
     }
     timing_mark(ctx);
