@@ -446,8 +446,9 @@ def test_density_switch_argument_checks(sk):
     ctx.set_density_switch()
 
 
-@pytest.mark.parametrize("ymax", [1, 300, 20000])
-def test_exact_fixed_point_layer_matches_oracle(sk, port, ymax):
+@pytest.mark.parametrize("ymax,dense_rows", [(1, True), (300, True), (20000, True),
+                                             (1, False), (300, False), (20000, False)])
+def test_exact_fixed_point_layer_matches_oracle(sk, port, ymax, dense_rows):
     # Layer 0 with exactly representable partial sums takes the order-free
     # fixed-point path; ymax sets the partial-sum range and with it the packing
     # (range 7 -> four 8-bit fields per word, ~15 -> two 16-bit, ~21 -> int32).
@@ -467,7 +468,8 @@ def test_exact_fixed_point_layer_matches_oracle(sk, port, ymax):
     v = rng.integers(1, ymax + 1, ent).astype(np.float32)
     Y = sk.csr_from_triples(m, n, (r, c, v))
     hY = host_csr(Y)
-    b = np.where(np.arange(m) % 13 == 0, 0.25, -0.5).astype(np.float32)
+    # positive-bias rows take the float fallback inside the exact kernel
+    b = np.where(np.arange(m) % 13 == 0, 0.25 if dense_rows else -1.5, -0.5).astype(np.float32)
     model = sk.DnnModel([dev_csr(sk, w) for w in hW], [b] * L)
     out, trace = sk.relu_forward_sparse(model, Y, sk.ForwardOptions(clip=0.0))
     y, want_trace = hY, [hY.nnz]
