@@ -572,22 +572,22 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
 }
 
 // Exact mode, fixed point.  Every product and partial sum is a multiple of
-// 2^gran below 2^R * 2^gran in magnitude, R = top - gran <= 24
+// 2^gran of magnitude <= qb * 2^gran, qb = rowsum(W) * max|Y| * 2^-gran < 2^24
 // (products_exact), so q = p * 2^-gran is an exact integer and any order of
 // integer adds gives the exact sum; the float ascending fold of the reference
 // equals it bit for bit (acc * 2^gran, +0 for 0).  Integer shared atomics are
 // native (float ones are a CAS loop).
 //
-// Packing: when R <= 15 (or <= 7) every partial sum fits a biased 16-bit (8-bit)
-// field, so one 32-bit accumulator word holds P = 2 (4) fields: field `sub` of
+// Packing: when qb <= 32767 (or <= 127) every partial sum fits a biased 16-bit
+// (8-bit) field, so one 32-bit accumulator word holds P = 2 (4) fields: field `sub` of
 // word s is window (first + sub), sample s.  Adding q << (B*sub) to the word
 // never carries across fields (the biased field stays in [0, 2^B)), so one
 // S-word accumulator serves P consecutive windows and the per-window overhead
 // is paid once per P windows.
 //
-// The accumulator's products are spread flat over the warp, four consecutive
-// ones per lane with all loads in flight before any update (the path is load
-// latency bound); owners come from a compacted table of non-empty slices.  A
+// The accumulator's products are cut into pieces of <= 4 consecutive products
+// of one in-edge; each lane takes one piece record per round (all four loads in
+// flight before any update) and the in-edge's increment by one shuffle.  A
 // position can only survive if its final sum is above thr = -b * 2^-gran, so
 // updates that leave the sum above thr mark a candidate bit; the epilogue walks
 // candidates only and the accumulator is reset with vector stores.
@@ -595,7 +595,10 @@ __device__ __forceinline__ uint32_t fx_clear_word(uint32_t P) {
   return P == 1 ? 0u : (P == 2 ? 0x80008000u : 0x80808080u);
 }
 
-template <bool kLayer, int kSh>  // kSh: compile-time log2 window (0 = runtime p.sh)
+constexpr uint32_t kPieceCap = 64;  // piece records per batch (the 128-word table area)
+
+// kSh: compile-time log2 window (0 = runtime p.sh); kYC: Y is constant-valued
+template <bool kLayer, int kSh, bool kYC>
 __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
                                    int lane) {
   const int sh = kSh ? kSh : p.sh;
@@ -611,33 +614,25 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
   const uint32_t deg = ee - eb;
   const float b = kLayer ? p.bias[i] : 0.0f;
   const float thr = kLayer ? __fmul_rn(-b, p.fx_scale) : -INFINITY;
+  // a partial sum nv (an integer) is a candidate iff nv > thr iff nv > floor(thr);
+  // compared on the biased field: field > floor(thr) + fbias (NaN: never)
+  int thr_i;
+  if (!(thr == thr) || thr >= 1073741824.0f) thr_i = 1 << 30;
+  else if (thr < -1073741824.0f) thr_i = -(1 << 30);
+  else thr_i = int(floorf(thr));
+  const int thr_b = thr_i + int(fbias);
   uint32_t* const acc = ws.acc;
-  // staging area (unused in exact mode): compacted in-edge table + candidates
-  uint32_t* const tab_ex = reinterpret_cast<uint32_t*>(ws.st_p);
-  uint32_t* const tab_off = tab_ex + 32;
-  float* const tab_a = reinterpret_cast<float*>(tab_ex + 64);
-  uint32_t* const cand = tab_ex + 128;  // P * SW words
+  // staging area (unused in exact mode): piece records + candidates
+  uint2* const rec = reinterpret_cast<uint2*>(ws.st_p);                // kPieceCap
+  uint32_t* const cand = reinterpret_cast<uint32_t*>(ws.st_p) + 128;  // P * SW words
   const uint32_t nchunks = p.b_empty ? 0u : (deg + 31) / 32;
-  // first chunk's in-edges and their window-table entries for the whole group
+  // first chunk's in-edges (kept for every accumulator pass)
   uint32_t k0 = 0;
   float a0 = 0.0f;
-  // window-table entries of the group (named scalars: a dynamically indexed
-  // array would live in local memory)
-  uint32_t wq0 = 0, wq1 = 0, wq2 = 0, wq3 = 0, wq4 = 0;
-  static_assert(kGroup == 4, "wq0..wq4 cover one group");
   if (nchunks && uint32_t(lane) < deg) {
     k0 = p.aci[eb + lane];
     a0 = p.av[eb + lane];
-    const uint32_t* wk = p.wp + size_t(k0) * p.nW + w0;
-    wq0 = wk[0];
-    wq1 = wk[1];
-    if (wn >= 2) wq2 = wk[2];
-    if (wn >= 3) wq3 = wk[3];
-    if (wn >= 4) wq4 = wk[4];
   }
-  auto wq_at = [&](uint32_t q) {
-    return q == 0 ? wq0 : q == 1 ? wq1 : q == 2 ? wq2 : q == 3 ? wq3 : wq4;
-  };
 #pragma unroll 1
   for (uint32_t gw = 0; gw < wn; gw += P) {
     const uint32_t np = min(P, wn - gw);  // windows sharing this accumulator
@@ -647,73 +642,63 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
     for (uint32_t c = 0; c < nchunks; ++c) {
       uint32_t beg = 0, cnt = 0;
       float aa = 0.0f;
-      if (c == 0) {
-        aa = a0;
-        beg = wq_at(gw);
-        cnt = wq_at(gw + np) - beg;
-      } else {
-        const uint32_t e = eb + 32 * c + lane;
-        if (e < ee) {
-          const uint32_t kk = p.aci[e];
-          aa = p.av[e];
-          const uint32_t* wk = p.wp + size_t(kk) * p.nW + w0 + gw;
-          beg = wk[0];
-          cnt = wk[np] - beg;
-        }
+      const uint32_t e = eb + 32 * c + lane;
+      if (e < ee) {
+        const uint32_t kk = c == 0 ? k0 : p.aci[e];
+        aa = c == 0 ? a0 : p.av[e];
+        const uint32_t* wk = p.wp + size_t(kk) * p.nW + w0 + gw;
+        beg = wk[0];
+        cnt = wk[np] - beg;
       }
-      const uint32_t nzm = __ballot_sync(0xffffffffu, cnt != 0);
-      if (!nzm) continue;
+      if (!__any_sync(0xffffffffu, cnt != 0)) continue;
       any = true;
-      const uint32_t incl = warp_incl_scan(cnt, lane);
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t nnzl = __popc(nzm);
-      if (cnt) {
-        const uint32_t r = __popc(nzm & lanemask_lt(lane));
-        tab_ex[r] = incl - cnt;
-        tab_off[r] = beg - (incl - cnt);
-        tab_a[r] = aa;
-      }
-      __syncwarp();
-      const uint32_t cex = uint32_t(lane) < nnzl ? tab_ex[lane] : 0xFFFFFFFFu;
-      const uint32_t coff = tab_off[lane];
-      const float ca = tab_a[lane];
-      __syncwarp();
+      // this lane's slice as pieces of <= 4 consecutive products; a piece record
+      // (start, len | owner << 3) per lane and round replaces any owner search
+      const uint32_t npc = (cnt + 3) >> 2;
+      const uint32_t pincl = warp_incl_scan(npc, lane);
+      const uint32_t ptot = __shfl_sync(0xffffffffu, pincl, 31);
+      const uint32_t pex = pincl - npc;
+      // per-owner fixed-point increment of a constant-valued Y (exact integer)
+      const int qown = kYC ? __float2int_rn(__fmul_rn(__fmul_rn(aa, p.y_cval), p.fx_scale)) : 0;
 #pragma unroll 1
-      for (uint32_t j0 = 4 * lane; j0 < total + 4 * lane; j0 += 128) {
-        // lane owns products j0 .. j0+3: one search, then step-wise advance
-        uint32_t o = 0;
+      for (uint32_t pb = 0; pb < ptot; pb += kPieceCap) {
+        const uint32_t lo = max(pex, pb), hi = min(pex + npc, pb + kPieceCap);
+        for (uint32_t t = lo; t < hi; ++t) {
+          const uint32_t st = beg + 4 * (t - pex);
+          rec[t - pb] = make_uint2(st, min(4u, beg + cnt - st) | (uint32_t(lane) << 3));
+        }
+        __syncwarp();
+        const uint32_t nb = min(kPieceCap, ptot - pb);
+#pragma unroll 1
+        for (uint32_t r0 = 0; r0 < nb; r0 += 32) {
+          const uint32_t t = r0 + lane;
+          const uint2 rc = t < nb ? rec[t] : make_uint2(0u, 0u);
+          const uint32_t len = rc.y & 7u, own = rc.y >> 3;
+          const int qo = __shfl_sync(0xffffffffu, qown, own);
+          const float ao = kYC ? 0.0f : __shfl_sync(0xffffffffu, aa, own);
+          uint32_t cc[4];
+          float yy[4];
 #pragma unroll
-        for (uint32_t st = 16; st; st >>= 1)
-          if (__shfl_sync(0xffffffffu, cex, o + st) <= j0) o += st;
-        uint32_t cc[4];
-        float yy[4], ao[4];
+          for (int u = 0; u < 4; ++u)
+            if (uint32_t(u) < len) {
+              cc[u] = __ldg(&p.bci[rc.x + u]);
+              if (!kYC) yy[u] = __ldg(&p.bv[rc.x + u]);
+            }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t j = j0 + u;
-          if (u) {
-            const uint32_t nx = __shfl_sync(0xffffffffu, cex, min(o + 1, 31u));
-            if (o < 31 && nx <= j) ++o;
-          }
-          const uint32_t off = __shfl_sync(0xffffffffu, coff, o);
-          ao[u] = __shfl_sync(0xffffffffu, ca, o);
-          if (j < total) {
-            cc[u] = __ldg(&p.bci[j + off]);
-            yy[u] = p.y_const ? p.y_cval : __ldg(&p.bv[j + off]);
+          for (int u = 0; u < 4; ++u) {
+            if (uint32_t(u) < len) {
+              const uint32_t sl = cc[u] - wbase;
+              const uint32_t sub = sl >> sh, wl = sl & (S - 1);
+              const uint32_t fs = B * sub;
+              const int q = kYC ? qo : __float2int_rn(__fmul_rn(__fmul_rn(ao, yy[u]), p.fx_scale));
+              const uint32_t delta = uint32_t(q) << fs;
+              const uint32_t old = atomicAdd(acc + wl, delta);
+              if (int(((old + delta) >> fs) & fmask) > thr_b)
+                atomicOr(cand + sub * SW + (wl >> 5), 1u << (wl & 31));
+            }
           }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (j0 + u < total) {
-            const uint32_t sl = cc[u] - wbase;
-            const uint32_t sub = sl >> sh, wl = sl & (S - 1);
-            const uint32_t fs = B * sub;
-            const uint32_t delta =
-                uint32_t(__float2int_rn(__fmul_rn(__fmul_rn(ao[u], yy[u]), p.fx_scale))) << fs;
-            const uint32_t old = atomicAdd(acc + wl, delta);
-            const int nv = int(((old + delta) >> fs) & fmask) - int(fbias);
-            if (__int2float_rn(nv) > thr) atomicOr(cand + sub * SW + (wl >> 5), 1u << (wl & 31));
-          }
-        }
+        __syncwarp();
       }
     }
     __syncwarp();
@@ -813,10 +798,12 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
         process_item<Ops, kLayer, true>(p, i, uint32_t(g), ws, lane);
         for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
         __syncwarp();
-      } else if (p.sh == 10) {
-        process_item_exact<kLayer, 10>(p, i, uint32_t(g), ws, lane);
+      } else if (p.sh == 10 && p.y_const) {
+        process_item_exact<kLayer, 10, true>(p, i, uint32_t(g), ws, lane);
+      } else if (p.y_const) {
+        process_item_exact<kLayer, 0, true>(p, i, uint32_t(g), ws, lane);
       } else {
-        process_item_exact<kLayer, 0>(p, i, uint32_t(g), ws, lane);
+        process_item_exact<kLayer, 0, false>(p, i, uint32_t(g), ws, lane);
       }
     } else {
       process_item<Ops, kLayer, false>(p, i, uint32_t(g), ws, lane);
@@ -851,13 +838,14 @@ __device__ __forceinline__ void value_bits(float v, int& lowbit, int& ehi) {
 
 __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
   int lo = INT_MAX, hi = INT_MIN, nf = 0;
-  unsigned int bmin = 0xFFFFFFFFu, bmax = 0u;
+  unsigned int bmin = 0xFFFFFFFFu, bmax = 0u, amax = 0u;
   auto visit = [&](float x) {
     bmin = min(bmin, __float_as_uint(x));
     bmax = max(bmax, __float_as_uint(x));
     if (!isfinite(x)) {
       nf = 1;
     } else if (x != 0.0f) {
+      amax = max(amax, __float_as_uint(x) & 0x7fffffffu);
       int l, h;
       value_bits(x, l, h);
       lo = min(lo, l);
@@ -885,10 +873,11 @@ __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
     nf |= __shfl_xor_sync(0xffffffffu, nf, o);
     bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
     bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   }
   // block reduction, then one set of atomics per block
   __shared__ int r_lo[32], r_hi[32], r_nf[32];
-  __shared__ unsigned int r_bmin[32], r_bmax[32];
+  __shared__ unsigned int r_bmin[32], r_bmax[32], r_amax[32];
   const int wq = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
     r_lo[wq] = lo;
@@ -896,6 +885,7 @@ __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
     r_nf[wq] = nf;
     r_bmin[wq] = bmin;
     r_bmax[wq] = bmax;
+    r_amax[wq] = amax;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -905,39 +895,67 @@ __global__ void k_value_stats(const float* v, size_t n, ValueStats* out) {
       nf |= r_nf[q];
       bmin = min(bmin, r_bmin[q]);
       bmax = max(bmax, r_bmax[q]);
+      amax = max(amax, r_amax[q]);
     }
     atomicMin(&out->lowbit, lo);
     atomicMax(&out->ehi, hi);
     if (nf) atomicOr(&out->nonfinite, 1);
     atomicMin(&out->vmin, bmin);
     atomicMax(&out->vmax, bmax);
+    atomicMax(&out->absmax, amax);
   }
 }
 
-__global__ void k_max_row_len(const uint32_t* rp, uint32_t rows, ValueStats* out) {
+// Per-row bounds of a weight matrix: the longest row and an upper bound on the
+// largest row sum of |w| (round-up adds: every partial sum of the warp's
+// reduction is >= the exact one).  Nonnegative floats order like their bits.
+__global__ void k_row_bounds(const uint32_t* rp, const float* v, uint32_t rows, ValueStats* out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   int mx = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
-    mx = max(mx, int(rp[i + 1] - rp[i]));
-  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(&out->maxdeg, mx);
+  float smax = 0.0f;
+  for (uint32_t i = w0; i < rows; i += nw) {
+    const uint32_t b = rp[i], e = rp[i + 1];
+    float sum = 0.0f;
+    for (uint32_t q = b + lane; q < e; q += 32) sum = __fadd_ru(sum, fabsf(v[q]));
+    for (int o = 16; o; o >>= 1) sum = __fadd_ru(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+    mx = max(mx, int(e - b));
+    smax = fmaxf(smax, sum);  // a NaN sum (nonfinite weights) is flagged by k_value_stats
+  }
+  if (lane == 0) {
+    atomicMax(&out->maxdeg, mx);
+    atomicMax(&out->rowsum, __float_as_uint(smax));
+  }
 }
 
 __host__ __device__ __forceinline__ float pow2f(int e) { return ldexpf(1.0f, e); }
 
-__host__ __device__ __forceinline__ int ceil_log2_deg(int maxdeg) {
-  int lg = 0;
-  while ((1 << lg) < (maxdeg > 1 ? maxdeg : 1)) ++lg;
-  return lg;
+__host__ __device__ __forceinline__ float bits_float(unsigned int u) {
+  union {
+    unsigned int u;
+    float f;
+  } c{u};
+  return c.f;
 }
 
-// True when every partial sum of W.Y is exactly representable in fp32, so the
+// Every product w*y is a multiple of 2^gran (gran = lowbit(W) + lowbit(Y)), so
+// every partial sum of a row is an integer multiple of 2^gran; its magnitude is
+// at most rowsum(W) * max|Y|.  exact_qbound is that bound in units of 2^gran
+// (exact: a product of two floats and a power of two in double).
+__host__ __device__ __forceinline__ double exact_qbound(const ValueStats& w, const ValueStats& y) {
+  const int gran = w.lowbit + y.lowbit;
+  return ldexp(double(bits_float(w.rowsum)) * double(bits_float(y.absmax)), -gran);
+}
+
+// True when every partial sum of W.Y is exactly representable in fp32 (an
+// integer below 2^24 times 2^gran, gran in the normal range), so the
 // accumulation order cannot change any bit of the result.
 __host__ __device__ __forceinline__ bool products_exact(const ValueStats& w, const ValueStats& y) {
   if (w.nonfinite || y.nonfinite) return false;
   if (w.lowbit == INT_MAX || y.lowbit == INT_MAX) return true;  // an operand is all zero
-  const int top = ceil_log2_deg(w.maxdeg) + w.ehi + y.ehi;  // |partial sum| < 2^top
-  const int gran = w.lowbit + y.lowbit;  // every partial sum is a multiple of 2^gran
-  return gran >= -126 && top <= 127 && top - gran <= 24;
+  const int gran = w.lowbit + y.lowbit;
+  return gran >= -126 && gran <= 103 && exact_qbound(w, y) < 16777216.0;
 }
 
 // Fixed-point parameters of the exact path for operand statistics w, y.
@@ -947,8 +965,10 @@ __host__ __device__ __forceinline__ void exact_params(const ValueStats& wst, con
   const int gran = zero ? 0 : wst.lowbit + yst.lowbit;
   ra.fx_scale = pow2f(-gran);
   ra.fx_unscale = pow2f(gran);
-  const int range = zero ? 0 : ceil_log2_deg(wst.maxdeg) + wst.ehi + yst.ehi - gran;
-  uint32_t P = range <= 7 ? 4u : (range <= 15 ? 2u : 1u);  // |partial sums| < 2^range
+  // |partial sums| <= qb (integers): biased 8-bit fields hold [-127, 127], 16-bit
+  // fields [-32767, 32767]
+  const double qb = zero ? 0.0 : exact_qbound(wst, yst);
+  uint32_t P = qb <= 127.0 ? 4u : (qb <= 32767.0 ? 2u : 1u);
   while (P > 1 && P * (S / 32) > 384) P >>= 1;             // candidate bitmaps live in st_p
   ra.fx_pack = P;
   // binary (constant-valued) inputs: the value array need not be read
@@ -1518,7 +1538,7 @@ void ensure_model_tables(sk_ctx* ctx, sk_model* mm) {
     if (w->nnz)
       SK_LAUNCH(k_value_stats, grid_warps(ctx, w->nnz / 32 + 1), 256, 0, ctx->stream, w->v,
                 w->nnz, o);
-    SK_LAUNCH(k_max_row_len, grid_warps(ctx, w->rows / 32 + 1), 256, 0, ctx->stream, w->rp,
+    SK_LAUNCH(k_row_bounds, grid_warps(ctx, w->rows), 256, 0, ctx->stream, w->rp, w->v,
               w->rows, o);
   }
   std::vector<ValueStats> hs(L);

@@ -148,8 +148,10 @@ struct ValueStats {
   int nonfinite;  // any Inf/NaN
   int maxdeg;     // max stored entries per row (weights only)
   unsigned int vmin, vmax;  // min / max bit pattern over all stored values (equal: constant)
+  unsigned int absmax;      // bit pattern of max |v| over finite values
+  unsigned int rowsum;      // weights: bit pattern of an upper bound on max_i sum_k |w_ik|
 };
-#define SK_VALUESTATS_INIT {INT_MAX, INT_MIN, 0, 0, 0xFFFFFFFFu, 0u}
+#define SK_VALUESTATS_INIT {INT_MAX, INT_MIN, 0, 0, 0xFFFFFFFFu, 0u, 0u, 0u}
 
 struct sk_model {
   sk_ctx* ctx = nullptr;

@@ -480,6 +480,55 @@ def test_exact_fixed_point_layer_matches_oracle(sk, port, ymax, dense_rows):
     assert_csr_bitwise(out, y)
 
 
+@pytest.mark.parametrize("target", [127, 128, 32767, 32768, (1 << 24) - 1, 1 << 24])
+@pytest.mark.parametrize("yvals", [(1.0,), (0.5, 1.0)])
+def test_exact_path_field_boundaries(sk, port, target, yvals):
+    # The fixed-point packing is chosen from qb = max row sum |w| * max|y| * 2^-gran:
+    # qb <= 127 -> 8-bit fields, <= 32767 -> 16-bit, < 2^24 -> int32, else the
+    # ordered path.  Rows whose partial sums reach exactly +-qb (one sample has
+    # every neuron active) sit on each boundary; any overflow of a field shows.
+    from oracle.oracle import Csr
+    m, n = 64, 8
+    scale = 2.0 if len(yvals) > 1 else 1.0  # lowbit(Y) = -1 doubles qb
+    t = int(target / scale)
+    pw = [float(1 << e) for e in range(25) if (t - 1) >> e & 1] + [1.0]  # sums to t
+    rows, cols, vals = [], [], []
+    for i in range(m):
+        if i < 3:
+            sign = [1.0, -1.0, None][i]
+            for k, w in enumerate(sorted(pw)):
+                s = sign if sign is not None else (1.0 if k % 2 == 0 else -1.0)
+                rows.append(i), cols.append(k), vals.append(s * w)
+        else:
+            for k in sorted({(i * 7) % m, (i * 13 + 5) % m, (i * 3 + 1) % m}):
+                rows.append(i), cols.append(k), vals.append(1.0 if (i + k) % 3 else -2.0)
+    W = sk.csr_from_triples(m, m, (np.array(rows, np.uint32), np.array(cols, np.uint32),
+                                   np.array(vals, np.float32)))
+    hW = host_csr(W)
+    rng = np.random.default_rng(target % 1000)
+    yr, yc, yv = [], [], []
+    for j in range(n):
+        act = np.arange(m) if j == 0 else np.flatnonzero(rng.random(m) < 0.4)
+        for k in act:
+            yr.append(k), yc.append(j), yv.append(yvals[-1] if j == 0 else rng.choice(yvals))
+    Y = sk.csr_from_triples(m, n, (np.array(yr, np.uint32), np.array(yc, np.uint32),
+                                   np.array(yv, np.float32)))
+    hY = host_csr(Y)
+    b = np.full(m, -0.5, np.float32)
+    model = sk.DnnModel([dev_csr(sk, Csr(m, m, hW.row_ptr, hW.col_idx, hW.values))] * 2, [b] * 2)
+    out, trace = sk.relu_forward_sparse(model, Y, sk.ForwardOptions(clip=0.0))
+    y, want_trace = hY, [hY.nnz]
+    for k in range(2):
+        y = port.layer_sparse(hW, b, y, 0.0)
+        want_trace.append(y.nnz)
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, y)
+    # the boundary row really reaches its bound t on sample 0 (z = t + b)
+    first = port.layer_sparse(hW, b, hY, 0.0)
+    assert first.col_idx[first.row_ptr[0]] == 0
+    assert first.values[first.row_ptr[0]] == np.float32(t) + np.float32(-0.5)
+
+
 @pytest.mark.parametrize("entries,bias", [(1, -0.01), (40, -0.01), (40, -0.2), (900, 0.0)])
 def test_sparse_forward_frontier_layers(sk, port, entries, bias):
     # near-empty inputs take the frontier path (only rows with an in-edge from an
