@@ -773,7 +773,8 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
 // Phase A over all items, window-group-major so the live slice of B stays in L2.
 // With a frontier (rows != nullptr) only the nrows listed output rows are
 // processed; every other row's items were zeroed by the caller.
-template <typename Ops, bool kLayer, bool kExact>
+// kSh (exact path): compile-time log2 window, 0 = dispatch on p.sh
+template <typename Ops, bool kLayer, bool kExact, int kSh = 0>
 __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
                                         uint64_t gw, uint64_t nwarps,
                                         const uint32_t* rows = nullptr, uint32_t nrows = 0) {
@@ -798,7 +799,9 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
         process_item<Ops, kLayer, true>(p, i, uint32_t(g), ws, lane);
         for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
         __syncwarp();
-      } else if (p.sh == 10 && p.y_const) {
+      } else if (kSh && p.y_const) {
+        process_item_exact<kLayer, kSh, true>(p, i, uint32_t(g), ws, lane);
+      } else if (!kSh && p.sh == 10 && p.y_const) {
         process_item_exact<kLayer, 10, true>(p, i, uint32_t(g), ws, lane);
       } else if (p.y_const) {
         process_item_exact<kLayer, 0, true>(p, i, uint32_t(g), ws, lane);
@@ -992,11 +995,11 @@ __host__ __device__ constexpr size_t exact_warp_bytes(uint32_t S) {
   return (size_t(S) + S / 32 + 128 + 4 * (S / 32)) * 4;
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long long* stamp) {
+template <int kSh>  // 0: runtime p.sh
+__device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t S = 1u << p.sh;
-  if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer();
+  const uint32_t S = kSh ? 1u << kSh : 1u << p.sh;
   uint8_t* base = reinterpret_cast<uint8_t*>(sm) + size_t(wid) * exact_warp_bytes(S);
   WarpSmem ws;
   ws.acc = reinterpret_cast<uint32_t*>(base);
@@ -1012,7 +1015,15 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long 
   __syncwarp();
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  phase_a<OpArith, true, true>(p, ws, lane, gw, nw);
+  phase_a<OpArith, true, true, kSh>(p, ws, lane, gw, nw);
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long long* stamp) {
+  if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer();
+  if (p.sh == 10)
+    exact_layer_body<10>(p);
+  else
+    exact_layer_body<0>(p);
 }
 
 // ---- generic SpGEMM (mxm over any semiring): separate kernels -------------------------
