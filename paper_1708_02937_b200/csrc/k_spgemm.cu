@@ -1112,6 +1112,7 @@ struct EngineArgs {
   const float* const* w_v;
   const float* bias;
   const uint8_t* bias_nonpos;
+  const uint32_t* nonpos_run;  // consecutive layers from k with every bias <= 0
   uint32_t m, n, L, nW;
   int sh;
   float clip;
@@ -1188,13 +1189,19 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
 
   for (uint32_t layer = 0; layer < p.L; ++layer) {
     if (total_in == 0 && p.bias_nonpos[layer]) {
-      // Empty input and every bias <= 0: the output is empty.  Every block makes
-      // the same decision from the same count, so no synchronisation is needed.
+      // Empty input and every bias <= 0: the output is empty, and so is every
+      // following layer's while their biases stay <= 0.  Every block makes the
+      // same decision from the same count, so no synchronisation is needed.
+      const uint32_t run = min(p.nonpos_run[layer], p.L - layer);
       last = -1;
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        p.trace[layer + 1] = 0;
-        if (p.stamps) p.stamps[layer + 1] = globaltimer();
+      if (blockIdx.x == 0) {
+        const long long now = p.stamps ? globaltimer() : 0;
+        for (uint32_t q = threadIdx.x; q < run; q += blockDim.x) {
+          p.trace[layer + 1 + q] = 0;
+          if (p.stamps) p.stamps[layer + 1 + q] = now;
+        }
       }
+      layer += run - 1;
       continue;
     }
     RowArgs ra;
@@ -1524,7 +1531,7 @@ sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, con
 // weight pointers, "every bias <= 0" flags and weight value statistics.
 void ensure_model_tables(sk_ctx* ctx, sk_model* mm) {
   const uint32_t L = mm->layers;
-  if (mm->d_wptr && mm->d_bias_nonpos && mm->d_wstats) return;
+  if (mm->d_wptr && mm->d_bias_nonpos && mm->d_nonpos_run && mm->d_wstats) return;
   std::vector<const void*> h(size_t(3) * L);
   for (uint32_t k = 0; k < L; ++k) {
     h[k] = mm->w[k]->rp;
@@ -1533,11 +1540,16 @@ void ensure_model_tables(sk_ctx* ctx, sk_model* mm) {
   }
   if (!mm->d_wptr) mm->d_wptr = dalloc<const void*>(ctx, std::max<size_t>(1, h.size()));
   if (!mm->d_bias_nonpos) mm->d_bias_nonpos = dalloc<uint8_t>(ctx, std::max<uint32_t>(1, L));
+  if (!mm->d_nonpos_run) mm->d_nonpos_run = dalloc<uint32_t>(ctx, std::max<uint32_t>(1, L));
+  std::vector<uint32_t> run(L);
+  for (uint32_t k = L; k-- > 0;) run[k] = mm->bias_nonpos[k] ? 1u + (k + 1 < L ? run[k + 1] : 0u) : 0u;
   if (!mm->d_wstats) mm->d_wstats = dalloc<ValueStats>(ctx, std::max<uint32_t>(1, L));
   if (L) {
     SK_CUDA(cudaMemcpyAsync(mm->d_wptr, h.data(), h.size() * sizeof(void*),
                             cudaMemcpyHostToDevice, ctx->stream));
     SK_CUDA(cudaMemcpyAsync(mm->d_bias_nonpos, mm->bias_nonpos.data(), L,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    SK_CUDA(cudaMemcpyAsync(mm->d_nonpos_run, run.data(), L * sizeof(uint32_t),
                             cudaMemcpyHostToDevice, ctx->stream));
     std::vector<ValueStats> init(L, ValueStats SK_VALUESTATS_INIT);
     SK_CUDA(cudaMemcpyAsync(mm->d_wstats, init.data(), L * sizeof(ValueStats),
@@ -1638,6 +1650,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     p.w_v = reinterpret_cast<const float* const*>(mm->d_wptr + 2 * Lm) + k0;
     p.bias = md->bias + size_t(k0) * m;
     p.bias_nonpos = mm->d_bias_nonpos + k0;
+    p.nonpos_run = mm->d_nonpos_run + k0;
     p.m = m;
     p.n = n;
     p.L = L;

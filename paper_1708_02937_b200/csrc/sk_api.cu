@@ -471,6 +471,7 @@ extern "C" sk_status sk_model_free(sk_model* m) {
     dfree(m->ctx, m->d_wptr);
     dfree(m->ctx, m->d_wstats);
     dfree(m->ctx, m->d_bias_nonpos);
+    dfree(m->ctx, m->d_nonpos_run);
     delete m;
   });
 }

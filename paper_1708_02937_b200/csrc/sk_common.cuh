@@ -163,6 +163,7 @@ struct sk_model {
   const void** d_wptr = nullptr;     // device [rp[L], ci[L], v[L]] for the engine
   void* d_wstats = nullptr;          // device per-layer value statistics (exactness test)
   uint8_t* d_bias_nonpos = nullptr;
+  uint32_t* d_nonpos_run = nullptr;  // per layer k: consecutive layers from k with every b <= 0
   int weights_finite = -1;           // every weight finite (-1 = not computed yet)
   std::vector<ValueStats> wstats_host;  // host copy of d_wstats
 };
