@@ -1135,6 +1135,7 @@ struct EngineArgs {
   int* overflow;
   int* err;
   long long* stamps;               // optional %globaltimer per layer end (L+1)
+  int debug_phases;                // record g_phase_ts for layer 0
   const ValueStats* wstats;        // per layer
   const ValueStats* y0stats;       // of Y0's values
   int exact_ok;                    // layer 0 may use the order-free path (SK_NO_EXACT unset)
@@ -1163,15 +1164,28 @@ __device__ unsigned long long block_sum_u64(unsigned long long v, unsigned long 
   return t;
 }
 
+// phase timestamps of the engine's first layer (SK_DEBUG_PHASES diagnostics)
+__device__ long long g_phase_ts[16];
+#define SK_PHASE_MARK(slot)                                                    \
+  do {                                                                         \
+    if (p.debug_phases && layer == 0 && blockIdx.x == 0 && threadIdx.x == 0) \
+      g_phase_ts[slot] = globaltimer();                                        \
+  } while (0)
+
+constexpr uint32_t kFoldWords = 256;  // folded input-row bitmap per block (8192 bits)
+
 __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) {
   extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ uint32_t fold[kFoldWords];
   __shared__ unsigned long long red[kWarps];
   __shared__ unsigned long long tile_carry;
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t S = 1u << p.sh;
+  if (p.debug_phases && blockIdx.x == 0 && threadIdx.x == 0) g_phase_ts[8] = globaltimer();
   const WarpSmem ws = warp_smem(sm, wid, S);
   warp_smem_init(ws, S, lane);
+  if (p.debug_phases && blockIdx.x == 0 && threadIdx.x == 0) g_phase_ts[9] = globaltimer();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t items = uint64_t(p.m) * p.nW;
@@ -1204,6 +1218,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
       layer += run - 1;
       continue;
     }
+    SK_PHASE_MARK(0);
     RowArgs ra;
     ra.arp = p.w_rp[layer];
     ra.aci = p.w_ci[layer];
@@ -1244,29 +1259,55 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     const bool frontier = !exact && p.bias_nonpos[layer] && total_in * 64 < p.m;
     if (frontier) {
       uint32_t* const kb = p.kbits + (nfilt & 1) * p.kbits_words;
-      uint32_t* const kb_next = p.kbits + ((nfilt + 1) & 1) * p.kbits_words;
       ++nfilt;
-      const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
-      const uint32_t nt = gridDim.x * blockDim.x;
-      for (uint32_t k = gt; k < p.m; k += nt)
-        if (in_wp[size_t(k + 1) * p.nW] > in_wp[size_t(k) * p.nW])
-          atomicOr(kb + (k >> 5), 1u << (k & 31));
-      grid.sync();
-      for (uint32_t q = gt; q < p.kbits_words; q += nt) kb_next[q] = 0u;
-      for (uint32_t i = gw; i < p.m; i += nwarps) {
-        const uint32_t eb = ra.arp[i], ee = ra.arp[i + 1];
-        bool hit = false;
-        for (uint32_t e = eb + lane; e < ee && !hit; e += 32) {
-          const uint32_t k = ra.aci[e];
-          hit = (__ldcg(kb + (k >> 5)) >> (k & 31)) & 1u;
-        }
-        if (__any_sync(0xffffffffu, hit)) {
-          if (lane == 0) p.frontier[atomicAdd(p.nfront + layer, 1u)] = i;
-        } else {
-          for (uint32_t w = lane; w < p.nW; w += 32) p.item_cnt[size_t(i) * p.nW + w] = 0u;
-        }
+      // bitmap of input rows holding entries: whole words from ballots (every
+      // word written, no zeroing pass)
+      for (uint32_t k0 = gw * 32; k0 < p.m; k0 += nwarps * 32) {
+        const uint32_t k = k0 + lane;
+        const bool act = k < p.m && in_wp[size_t(k + 1) * p.nW] > in_wp[size_t(k) * p.nW];
+        const uint32_t word = __ballot_sync(0xffffffffu, act);
+        if (lane == 0) kb[k0 >> 5] = word;
       }
       grid.sync();
+      SK_PHASE_MARK(1);
+      // the bitmap folded to 8192 bits in shared memory: an in-edge whose folded
+      // bit is clear cannot come from an active row, so the (hot, L2-resident)
+      // bitmap is read only for the rest
+      for (uint32_t q = threadIdx.x; q < kFoldWords; q += blockDim.x) {
+        uint32_t f = 0;
+        for (uint32_t w = q; w < p.kbits_words; w += kFoldWords) f |= __ldcg(kb + w);
+        fold[q] = f;
+      }
+      __syncthreads();
+      // frontier rows, a row per lane with eight in-edge loads in flight; the 32
+      // rows' item counts are zeroed (frontier rows rewrite theirs in phase A)
+      for (uint32_t i0 = gw * 32; i0 < p.m; i0 += nwarps * 32) {
+        const uint32_t i = i0 + lane;
+        bool hit = false;
+        if (i < p.m) {
+          const uint32_t eb = ra.arp[i], ee = ra.arp[i + 1];
+          for (uint32_t e = eb; e < ee && !hit; e += 8) {
+            uint32_t kk[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) kk[u] = e + u < ee ? ra.aci[e + u] : 0xFFFFFFFFu;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (kk[u] != 0xFFFFFFFFu && ((fold[(kk[u] >> 5) % kFoldWords] >> (kk[u] & 31)) & 1u))
+                hit |= (__ldcg(kb + (kk[u] >> 5)) >> (kk[u] & 31)) & 1u;
+          }
+        }
+        const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+        uint32_t fb = 0;
+        if (lane == 0 && hm) fb = atomicAdd(p.nfront + layer, uint32_t(__popc(hm)));
+        fb = __shfl_sync(0xffffffffu, fb, 0);
+        if (hit) p.frontier[fb + __popc(hm & lanemask_lt(lane))] = i;
+        const uint64_t z0 = uint64_t(i0) * p.nW, z1 = min(uint64_t(i0 + 32), uint64_t(p.m)) * p.nW;
+        uint64_t z = z0 + 4 * lane;
+        for (; z + 4 <= z1; z += 128) *reinterpret_cast<uint4*>(p.item_cnt + z) = make_uint4(0, 0, 0, 0);
+        for (; z < z1; ++z) p.item_cnt[z] = 0u;
+      }
+      grid.sync();
+      SK_PHASE_MARK(2);
       const uint32_t nrows = __ldcg(p.nfront + layer);
       phase_a<OpArith, true, false>(ra, ws, lane, gw, nwarps, p.frontier, nrows);
     } else if (exact) {
@@ -1282,16 +1323,36 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
       phase_a<OpArith, true, false>(ra, ws, lane, gw, nwarps);
     }
     grid.sync();
+    SK_PHASE_MARK(3);
 
     // ---- phase B: exclusive scan of item counts -> output window table ---------------
     uint32_t* const out_wp = cur ? p.wp[1] : p.wp[0];
-    const uint64_t per = (items + gridDim.x - 1) / gridDim.x;
+    // block ranges in multiples of 4 items (16-byte aligned count / table vectors);
+    // each thread owns kScanV vectors of four consecutive counts per tile
+    constexpr uint32_t kScanV = 4;
+    const uint64_t per = ((items + gridDim.x - 1) / gridDim.x + 3) & ~uint64_t(3);
     const uint64_t lo = min(items, uint64_t(blockIdx.x) * per), hi = min(items, lo + per);
+    const uint64_t tile = uint64_t(4 * kScanV) * blockDim.x;
+    auto load4 = [&](uint64_t t, uint32_t (&c)[4]) {
+      if (t + 4 <= hi) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p.item_cnt + t);
+        c[0] = v.x, c[1] = v.y, c[2] = v.z, c[3] = v.w;
+      } else {
+        for (int q = 0; q < 4; ++q) c[q] = t + q < hi ? p.item_cnt[t + q] : 0u;
+      }
+    };
     unsigned long long mine = 0;
-    for (uint64_t t = lo + threadIdx.x; t < hi; t += blockDim.x) mine += p.item_cnt[t];
+    for (uint64_t t0 = lo; t0 < hi; t0 += tile) {
+      uint32_t c[kScanV][4];
+#pragma unroll
+      for (uint32_t v = 0; v < kScanV; ++v) load4(t0 + 4 * (uint64_t(v) * blockDim.x + threadIdx.x), c[v]);
+#pragma unroll
+      for (uint32_t v = 0; v < kScanV; ++v) mine += uint64_t(c[v][0]) + c[v][1] + c[v][2] + c[v][3];
+    }
     const unsigned long long bsum = block_sum_u64(mine, red);
     if (threadIdx.x == 0) p.block_sums[blockIdx.x] = bsum;
     grid.sync();
+    SK_PHASE_MARK(4);
     unsigned long long pre = 0, grand = 0;
     for (uint32_t q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
       const unsigned long long v = p.block_sums[q];
@@ -1302,17 +1363,36 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     grand = block_sum_u64(grand, red);
     if (threadIdx.x == 0) tile_carry = pre;
     __syncthreads();
-    for (uint64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
-      const uint64_t t = t0 + threadIdx.x;
-      const uint32_t c = t < hi ? p.item_cnt[t] : 0u;
-      const uint32_t incl = warp_incl_scan(c, lane);
+    // a thread's 4 * kScanV items are consecutive within the tile
+    for (uint64_t t0 = lo; t0 < hi; t0 += tile) {
+      const uint64_t tb = t0 + uint64_t(4 * kScanV) * threadIdx.x;
+      uint32_t c[kScanV][4];
+#pragma unroll
+      for (uint32_t v = 0; v < kScanV; ++v) load4(tb + 4 * v, c[v]);
+      uint32_t s = 0;
+#pragma unroll
+      for (uint32_t v = 0; v < kScanV; ++v) s += c[v][0] + c[v][1] + c[v][2] + c[v][3];
+      const uint32_t incl = warp_incl_scan(s, lane);
       if (lane == 31) red[wid] = incl;
       __syncthreads();
       unsigned long long base = tile_carry;
       for (int q = 0; q < wid; ++q) base += red[q];
       unsigned long long tile_total = 0;
       for (int q = 0; q < kWarps; ++q) tile_total += red[q];
-      if (t < hi) out_wp[t] = uint32_t(base + incl - c);
+      uint32_t e = uint32_t(base + incl - s);
+#pragma unroll
+      for (uint32_t v = 0; v < kScanV; ++v) {
+        const uint64_t t = tb + 4 * v;
+        const uint32_t e0 = e, e1 = e0 + c[v][0], e2 = e1 + c[v][1], e3 = e2 + c[v][2];
+        if (t + 4 <= hi) {
+          *reinterpret_cast<uint4*>(out_wp + t) = make_uint4(e0, e1, e2, e3);
+        } else {
+          const uint32_t ev[4] = {e0, e1, e2, e3};
+          for (int q = 0; q < 4; ++q)
+            if (t + q < hi) out_wp[t + q] = ev[q];
+        }
+        e = e3 + c[v][3];
+      }
       __syncthreads();
       if (threadIdx.x == 0) tile_carry += tile_total;
       __syncthreads();
@@ -1322,6 +1402,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
       if (grand > p.cap) atomicExch(p.overflow, 1);
     }
     grid.sync();
+    SK_PHASE_MARK(5);
 
     // ---- phase C: gather scratch spans into CSR order -------------------------------
     uint32_t* const oc = cur ? p.ci[1] : p.ci[0];
@@ -1352,6 +1433,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
       if (p.stamps) p.stamps[layer + 1] = globaltimer();
     }
     grid.sync();
+    SK_PHASE_MARK(6);
 
     total_in = grand;
     in_ci = oc;
@@ -1678,6 +1760,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     p.overflow = flags;
     p.err = ctx->d_err;
     p.stamps = (ctx->stamps && k0 + L < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
+    p.debug_phases = getenv("SK_DEBUG_PHASES") ? 1 : 0;
     p.wstats = static_cast<const ValueStats*>(mm->d_wstats) + k0;
     p.y0stats = y0stats;
     p.exact_ok = exact_ok;
@@ -1691,6 +1774,16 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     timing_mark(ctx);
     SK_CUDA(cudaLaunchCooperativeKernel((void*)k_sparse_engine, dim3(grid), dim3(kWarps * 32),
                                         args, smem, ctx->stream));
+    static const int dbg_phases = getenv("SK_DEBUG_PHASES") ? 1 : 0;
+    if (dbg_phases) {
+      long long ts[16];
+      SK_CUDA(cudaMemcpyFromSymbolAsync(ts, g_phase_ts, sizeof(ts), 0, cudaMemcpyDeviceToHost,
+                                        ctx->stream));
+      SK_CUDA(cudaStreamSynchronize(ctx->stream));
+      fprintf(stderr, "[sk phases] init %.1f us |", (ts[9] - ts[8]) / 1e3);
+      for (int q = 1; q <= 6; ++q) fprintf(stderr, " %.1f", (ts[q] - ts[q - 1]) / 1e3);
+      fprintf(stderr, " us (layer 0: marks 0-6)\n");
+    }
     g_launches.fetch_add(1);
     timing_mark(ctx);
 
