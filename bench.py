@@ -456,7 +456,6 @@ def run_ours(args, w):
         barrier()
     launches = sk._lib.launches() - launches0
     ktimes = ctx.kernel_times_ms()
-    stamps = ctx.layer_stamps_ns(L + 1) if w["y0"] == "binary" else None
     ms = e0.elapsed_time(e1)
     t_local = torch.tensor([ms], device="cuda")
     if dist is not None:
@@ -528,39 +527,42 @@ def run_ours(args, w):
                 "launches_per_inference": len(ktimes) / args.steps,
                 "kernel_share_of_step": float(t_launch * 1e3 / ms_step), "peak_kind": pk_kind}
     elif w["y0"] == "binary" and len(ktimes):
-        # The sparse forward is one k_sparse_engine launch per inference unless the
-        # density-adaptive rule hands dense layers to k_dense_engine.  Algorithmic
-        # bytes per layer follow SURVEY §8(d) for the representation that layer ran
-        # in (a sparse layer with an empty input and biases <= 0 needs no bytes).
-        eng = layer_engines(tr, m, B)
-        byts = sum((sparse_layer_bytes(tr[k], tr[k + 1], B, m, nnzW[k]) if tr[k] > 0 else 0)
-                   if eng[k] == "sparse" else dense_layer_bytes(B, m, nnzW[k])
-                   for k in range(L))
-        t_launch = float(np.sum(ktimes)) / args.steps / 1e3  # engine time per inference
-        achieved = byts / t_launch / 1e9
-        n_dense = eng.count("dense")
-        l1 = {}
-        if eng[0] == "sparse" and stamps is not None and stamps[1] > stamps[0]:
+        # Per inference: layer 1 on the order-free fixed-point path (k_exact_layer,
+        # its partial sums provably exact) when the statistics allow it, then the
+        # thin layers on expand-sort-compress, the windowed engine or the dense
+        # engine (ctx.layer_paths).  The timed launches are k_exact_layer and one
+        # per engine segment, in that order.  Algorithmic bytes per layer follow
+        # SURVEY §8(d) for the representation it ran in.
+        paths = ctx.layer_paths(L)
+        per_step = len(ktimes) // args.steps if len(ktimes) % args.steps == 0 else 0
+        path_count = {p_: paths.count(p_) for p_ in sorted(set(paths))}
+        if paths[0] == "exact" and per_step >= 1:
+            t1 = float(np.mean(ktimes[0::per_step])) / 1e3
             b1 = sparse_layer_bytes(tr[0], tr[1], B, m, nnzW[0])
-            l1_ms = float(stamps[1] - stamps[0]) / 1e6
-            l1 = {"layer1_ms": l1_ms, "layer1_bytes": b1,
-                  "layer1_achieved_gbs": b1 / (l1_ms / 1e3) / 1e9}
-            if n_dense == 0:
-                l1["layers_2_to_L_ms"] = float(stamps[L] - stamps[1]) / 1e6
-        kern = ("k_exact_layer (order-free fixed-point layer 1, its partial sums provably "
-                "exact) + k_sparse_engine (persistent: per layer windowed SpGEMM + "
-                "bias/ReLU/clip + prune + compaction)") if len(ktimes) > args.steps else \
-            ("k_sparse_engine (persistent: per layer windowed SpGEMM + bias/ReLU/clip + "
-             "prune + compaction)")
-        if n_dense:
-            kern = (f"k_sparse_engine ({L - n_dense} layers) + k_dense_engine ({n_dense} "
-                    "layers, fused SpMM + bias/ReLU) via the density-adaptive hand-off")
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": kern,
-                "algorithmic_bytes": byts, "launch_ms": t_launch * 1e3,
-                "launches_per_inference": len(ktimes) / args.steps,
-                "kernel_share_of_step": float(t_launch * 1e3 / ms_step),
-                "peak_kind": pk_kind, **l1}
+            achieved = b1 / t1 / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                    "kernel": "k_exact_layer (layer 1: order-free fixed-point windowed SpGEMM + "
+                              "bias/ReLU/clip + prune; its partial sums provably exact)",
+                    "algorithmic_bytes": b1, "launch_ms": t1 * 1e3, "launches_per_inference": 1,
+                    "kernel_share_of_step": float(t1 * 1e3 / ms_step), "peak_kind": pk_kind,
+                    "layer_paths": path_count,
+                    "rest_of_step_ms": float(ms_step - t1 * 1e3)}
+        else:
+            eng = layer_engines(tr, m, B)
+            byts = sum((sparse_layer_bytes(tr[k], tr[k + 1], B, m, nnzW[k]) if tr[k] > 0 else 0)
+                       if eng[k] == "sparse" else dense_layer_bytes(B, m, nnzW[k])
+                       for k in range(L))
+            t_launch = float(np.sum(ktimes)) / args.steps / 1e3  # timed kernels per inference
+            achieved = byts / t_launch / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                    "kernel": "k_sparse_engine (persistent: per layer windowed SpGEMM + "
+                              "bias/ReLU/clip + prune + compaction) / k_dense_engine",
+                    "algorithmic_bytes": byts, "launch_ms": t_launch * 1e3,
+                    "launches_per_inference": len(ktimes) / args.steps,
+                    "kernel_share_of_step": float(t_launch * 1e3 / ms_step),
+                    "peak_kind": pk_kind, "layer_paths": path_count}
     elif len(ktimes):
         # One launch of k_dense_engine per inference (all layers, grid barriers
         # between them): algorithmic bytes = SURVEY §8(d) dense-Y bytes per layer.

@@ -91,6 +91,14 @@ sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count)
 /* With timing enabled, the sparse engine writes %globaltimer (ns) at the start
  * (entry 0) and at the end of every layer (entry k+1) of the last forward. */
 sk_status sk_ctx_layer_stamps(sk_ctx* ctx, long long* ns, size_t n);
+/* The path each layer of the last sparse forward (sk_relu_forward_sparse) took,
+ * one code per layer: SK_PATH_EMPTY (empty input, every bias <= 0: no work),
+ * SK_PATH_EXACT (order-free fixed-point layer), SK_PATH_ESC (expand-sort-
+ * compress), SK_PATH_ENGINE (windowed sparse engine), SK_PATH_DENSE (dense
+ * engine after the density switch).  Introspection only; results are bitwise
+ * the same on every path.  No reference counterpart. */
+enum { SK_PATH_EMPTY = 0, SK_PATH_EXACT = 1, SK_PATH_ESC = 2, SK_PATH_ENGINE = 3, SK_PATH_DENSE = 4 };
+sk_status sk_ctx_layer_paths(sk_ctx* ctx, unsigned char* paths, size_t n);
 /* Density-adaptive sparse forward (sk_relu_forward_sparse): the activations
  * move to the dense engine when a layer's output holds more than
  * dense_above * m * n entries and back to the sparse engine below

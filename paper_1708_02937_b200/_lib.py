@@ -25,7 +25,7 @@ EXPORTS = [
     "sk_last_error", "sk_version", "sk_kernel_launch_count",
     "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_stream", "sk_ctx_stream",
     "sk_ctx_synchronize", "sk_ctx_set_timing", "sk_ctx_kernel_times",
-    "sk_ctx_layer_stamps", "sk_ctx_set_density_switch",
+    "sk_ctx_layer_stamps", "sk_ctx_layer_paths", "sk_ctx_set_density_switch",
     "sk_host_register", "sk_host_unregister",
     "sk_dense_create", "sk_dense_upload", "sk_dense_write", "sk_dense_download",
     "sk_dense_download_async", "sk_dense_shape", "sk_dense_device_ptr",
@@ -79,6 +79,7 @@ def load() -> C.CDLL:
     L.sk_ctx_set_timing.argtypes = [vp, C.c_int]
     L.sk_ctx_kernel_times.argtypes = [vp, f32p, C.c_size_t, C.POINTER(C.c_size_t)]
     L.sk_ctx_layer_stamps.argtypes = [vp, C.POINTER(C.c_longlong), C.c_size_t]
+    L.sk_ctx_layer_paths.argtypes = [vp, C.POINTER(C.c_ubyte), C.c_size_t]
     L.sk_ctx_set_density_switch.argtypes = [vp, C.c_double, C.c_double]
     L.sk_host_register.argtypes = [vp, C.c_size_t]
     L.sk_host_unregister.argtypes = [vp]

@@ -1,0 +1,238 @@
+// Thin layers by expand-sort-compress (ESC).
+//
+// When a layer's input is small against its (row, window) item space the
+// windowed engine pays its per-item work for almost no products (cfg3 layer 2:
+// 136 K inputs, ~4.4 M products spread over 967 K windows).  Here the products
+// are generated directly instead: every input entry (k, j, y) walks the
+// out-edges of neuron k (W^T row k: the in-edges of the reference orientation,
+// dnn.cpp:65-103, seen from the input side) and emits (key = i*n + j, w_ik*y).
+// Products are generated in input order -- ascending k -- so a STABLE radix
+// sort by key leaves every output's products in ascending k, and the run-wise
+// fold acc = +0, acc += p (ascending k) is the reference's fold bit for bit
+// (semiring.hpp:59-66); z = epilogue(acc + b) and the z == 0 prune follow.  The
+// sorted keys are the output's CSR order (row i, then sample j).
+//
+// Only layers with every bias <= 0 come here: a position without products then
+// gives epilogue(0 + b) == 0, so outputs exist only where products exist.
+#include <cub/cub.cuh>
+
+#include "sk_common.cuh"
+
+namespace sk {
+
+namespace {
+
+// deg[e] = out-degree of the input entry's neuron (warp per input row)
+__global__ void k_esc_degrees(const uint32_t* yrp, uint32_t rows, const uint32_t* trp,
+                              uint32_t* deg, size_t nnz) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < rows;
+       k += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t d = trp[k + 1] - trp[k];
+    for (uint32_t e = yrp[k] + lane; e < yrp[k + 1]; e += 32) deg[e] = d;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) deg[nnz] = 0;  // scan sentinel -> total
+}
+
+// products of input row k: entry e writes its out-edges at off[e] .. off[e]+d
+template <typename K>
+__global__ void k_esc_expand(const uint32_t* yrp, const uint32_t* yci, const float* yv,
+                             uint32_t rows, uint32_t n, const uint32_t* trp,
+                             const uint32_t* tci, const float* tv, const uint32_t* off,
+                             K* keys, float* vals) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < rows;
+       k += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t tb = trp[k], d = trp[k + 1] - tb;
+    if (d == 0) continue;
+    for (uint32_t e = yrp[k]; e < yrp[k + 1]; ++e) {
+      const uint32_t j = yci[e];
+      const float y = yv[e];
+      const uint32_t o = off[e];
+      for (uint32_t t = lane; t < d; t += 32) {
+        const uint32_t i = tci[tb + t];
+        keys[o + t] = K(i) * K(n) + K(j);
+        vals[o + t] = __fmul_rn(tv[tb + t], y);
+      }
+    }
+  }
+}
+
+// run heads fold their run (ascending k) and apply the layer epilogue
+template <typename K>
+__global__ void k_esc_fold(const K* keys, const float* vals, uint32_t P, uint32_t n,
+                           const float* bias, float clip, uint32_t* keep, float* z) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P; t += gridDim.x * blockDim.x) {
+    const K key = keys[t];
+    uint32_t f = 0;
+    if (t == 0 || keys[t - 1] != key) {
+      float acc = 0.0f;
+      for (uint32_t u = t; u < P && keys[u] == key; ++u) acc = __fadd_rn(acc, vals[u]);
+      const float zz = layer_epilogue(acc, bias[uint32_t(key / K(n))], clip);
+      f = zz != 0.0f ? 1u : 0u;
+      z[t] = zz;
+    }
+    keep[t] = f;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) keep[P] = 0;
+}
+
+template <typename K>
+__global__ void k_esc_scatter(const K* keys, const float* z, const uint32_t* keep,
+                              const uint32_t* pos, uint32_t P, uint32_t n, K* okey,
+                              uint32_t* oci, float* ov) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P; t += gridDim.x * blockDim.x)
+    if (keep[t]) {
+      const uint32_t s = pos[t];
+      okey[s] = keys[t];
+      oci[s] = uint32_t(keys[t] % K(n));
+      ov[s] = z[t];
+    }
+}
+
+// row_ptr[i] = first survivor with row >= i (sorted keys)
+template <typename K>
+__global__ void k_esc_row_ptr(const K* okey, uint32_t S, uint32_t rows, uint32_t n,
+                              uint32_t* rp) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= rows;
+       i += gridDim.x * blockDim.x) {
+    const K lo_key = K(i) * K(n);
+    uint32_t lo = 0, hi = S;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (okey[mid] < lo_key) lo = mid + 1;
+      else hi = mid;
+    }
+    rp[i] = lo;
+  }
+}
+
+unsigned grid_of(sk_ctx* ctx, uint64_t threads) {
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((threads + 255) / 256,
+                                                            uint64_t(ctx->num_sms) * 16)));
+}
+
+int bits_for(uint64_t v) {  // smallest b with v <= 2^b
+  int b = 0;
+  while (b < 64 && (uint64_t(1) << b) < v) ++b;
+  return b;
+}
+
+template <typename K>
+sk_csr* esc_run(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip) {
+  const uint32_t m = wt->cols, n = y->cols, rows = y->rows;
+  const size_t nnz = y->nnz;
+  // 1. per-entry product counts, scanned (sentinel entry -> total)
+  uint32_t* deg = aalloc<uint32_t>(ctx, nnz + 1);
+  uint32_t* off = aalloc<uint32_t>(ctx, nnz + 1);
+  SK_LAUNCH(k_esc_degrees, grid_of(ctx, uint64_t(rows) * 32), 256, 0, ctx->stream, y->rp, rows,
+            wt->rp, deg, nnz);
+  size_t tmp = 0;
+  SK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, deg, off, nnz + 1, ctx->stream));
+  void* t0 = aalloc<char>(ctx, tmp);
+  SK_CUDA(cub::DeviceScan::ExclusiveSum(t0, tmp, deg, off, nnz + 1, ctx->stream));
+  g_launches.fetch_add(1);
+  uint32_t P = 0;
+  SK_CUDA(cudaMemcpyAsync(&P, off + nnz, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  sk_csr* out = nullptr;
+  if (P == 0) {
+    out = new_csr(ctx, m, n, 0);
+    SK_CUDA(cudaMemsetAsync(out->rp, 0, (size_t(m) + 1) * 4, ctx->stream));
+    return out;
+  }
+  // 2. expand, 3. stable sort by (i, j)
+  K* k0 = aalloc<K>(ctx, P);
+  K* k1 = aalloc<K>(ctx, P);
+  float* v0 = aalloc<float>(ctx, P);
+  float* v1 = aalloc<float>(ctx, P);
+  SK_LAUNCH(k_esc_expand<K>, grid_of(ctx, uint64_t(rows) * 32), 256, 0, ctx->stream, y->rp,
+            y->ci, y->v, rows, n, wt->rp, wt->ci, wt->v, off, k0, v0);
+  const int end_bit = bits_for(uint64_t(m) * n);
+  tmp = 0;
+  SK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0, k1, v0, v1, P, 0, end_bit,
+                                          ctx->stream));
+  void* t1 = aalloc<char>(ctx, tmp);
+  SK_CUDA(cub::DeviceRadixSort::SortPairs(t1, tmp, k0, k1, v0, v1, P, 0, end_bit, ctx->stream));
+  g_launches.fetch_add(1);
+  // 4. fold runs + epilogue, 5. compact survivors
+  uint32_t* keep = aalloc<uint32_t>(ctx, size_t(P) + 1);
+  uint32_t* pos = aalloc<uint32_t>(ctx, size_t(P) + 1);
+  float* z = v0;  // free after the sort
+  SK_LAUNCH(k_esc_fold<K>, grid_of(ctx, P), 256, 0, ctx->stream, k1, v1, P, n, bias, clip, keep,
+            z);
+  tmp = 0;
+  SK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, keep, pos, size_t(P) + 1, ctx->stream));
+  void* t2 = aalloc<char>(ctx, tmp);
+  SK_CUDA(cub::DeviceScan::ExclusiveSum(t2, tmp, keep, pos, size_t(P) + 1, ctx->stream));
+  g_launches.fetch_add(1);
+  uint32_t S = 0;
+  SK_CUDA(cudaMemcpyAsync(&S, pos + P, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  out = new_csr(ctx, m, n, S);
+  K* okey = k0;  // free after the sort
+  if (S)
+    SK_LAUNCH(k_esc_scatter<K>, grid_of(ctx, P), 256, 0, ctx->stream, k1, z, keep, pos, P, n,
+              okey, out->ci, out->v);
+  SK_LAUNCH(k_esc_row_ptr<K>, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, okey, S, m, n,
+            out->rp);
+  return out;
+}
+
+}  // namespace
+
+__global__ void k_esc_max_row(const uint32_t* rp, uint32_t rows, unsigned int* out) {
+  unsigned int mx = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
+    mx = max(mx, rp[i + 1] - rp[i]);
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+// W^T of layer k (out-edges of every neuron) and its longest row, built on
+// first use and cached with the model.
+static const sk_csr* layer_transpose(sk_ctx* ctx, sk_model* mm, uint32_t k) {
+  if (mm->wT.size() != mm->layers) {
+    mm->wT.assign(mm->layers, nullptr);
+    mm->wT_maxdeg.assign(mm->layers, 0);
+  }
+  if (!mm->wT[k]) {
+    sk_csr* t = csr_transpose(ctx, mm->w[k]);
+    unsigned int* d = dalloc<unsigned int>(ctx, 1);
+    SK_CUDA(cudaMemsetAsync(d, 0, 4, ctx->stream));
+    SK_LAUNCH(k_esc_max_row, grid_of(ctx, t->rows), 256, 0, ctx->stream, t->rp, t->rows, d);
+    unsigned int h = 0;
+    SK_CUDA(cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    dfree(ctx, d);
+    mm->wT[k] = t;
+    mm->wT_maxdeg[k] = h;
+  }
+  return mm->wT[k];
+}
+
+// ESC pays for the layer's products (estimated from the mean degree) where the
+// windowed engine pays per (row, window) item: taken while the products stay
+// within `ratio` per item, and while the exact product count fits the 32-bit
+// offsets (input entries * longest W^T row).
+bool esc_applicable(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y, double ratio) {
+  if (!md->bias_nonpos[k] || y->nnz == 0) return false;
+  const double m = double(std::max<uint32_t>(1, md->neurons));
+  const double est = double(y->nnz) * double(md->w[k]->nnz) / m;
+  const double items = m * double((uint64_t(y->cols) + 1023) / 1024);
+  if (est > ratio * items || est > double(1u << 28)) return false;
+  auto* mm = const_cast<sk_model*>(md);
+  layer_transpose(ctx, mm, k);
+  return double(y->nnz) * double(mm->wT_maxdeg[k]) < double(1u << 31);
+}
+
+sk_csr* esc_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y, uint32_t k, float clip) {
+  auto* mm = const_cast<sk_model*>(md);
+  const sk_csr* wt = layer_transpose(ctx, mm, k);
+  const float* bias = md->bias + size_t(k) * md->neurons;
+  return uint64_t(md->neurons) * y->cols <= 0xFFFFFFFFull
+             ? esc_run<uint32_t>(ctx, y, wt, bias, clip)
+             : esc_run<uint64_t>(ctx, y, wt, bias, clip);
+}
+
+}  // namespace sk

@@ -1932,6 +1932,7 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     long long* stamp = (ctx->stamps && k0 < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
     timing_mark(ctx);
     SK_LAUNCH(k_exact_layer, grid, kWarps * 32, smem, ctx->stream, p, stamp);
+    timing_mark(ctx);
     SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
     exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
     uint32_t nnz = 0;
@@ -1946,13 +1947,11 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
                 wp_out, items, sc_c, sc_v, o->ci, o->v, p.overflow);
       SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, g.nW,
                 o->rp);
-      timing_mark(ctx);
       // arena memory, valid for the rest of the forward call; a window table of
       // another geometry is useless to the engine (it builds its own)
       *wp_out_ptr = same_geometry ? wp_out : nullptr;
       return o;
     }
-    timing_mark(ctx);
     size_t free_b = 0, total_b = 0;
     SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const unsigned long long bigger = clamp_cap(full, (unsigned long long)(free_b * 0.6 / 24.0));
@@ -1996,6 +1995,10 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
 
   std::vector<unsigned long long> trace(size_t(L) + 1, 0);
   trace[0] = y0->nnz;
+  ctx->last_paths.assign(L, (unsigned char)SK_PATH_EMPTY);
+  auto set_paths = [&](uint32_t k0, uint32_t cnt, unsigned char path) {
+    for (uint32_t q = k0; q < k0 + cnt && q < L; ++q) ctx->last_paths[q] = path;
+  };
   const sk_csr* cur = y0;
   sk_csr* owned = nullptr;
   float* dbuf[2] = {nullptr, nullptr};
@@ -2003,6 +2006,16 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   uint32_t k = 0;
   uint32_t* pending_wp = nullptr;  // window table of cur from the exact layer (arena)
   static const int exact_env = getenv("SK_NO_EXACT") ? 0 : 1;
+  // expand-sort-compress for thin layers (SK_ESC=0 disables, SK_ESC_RATIO sets the
+  // products-per-item limit; A/B measurements)
+  static const int esc_env = [] {
+    const char* e = getenv("SK_ESC");
+    return e && atoi(e) == 0 ? 0 : 1;
+  }();
+  static const double esc_ratio = [] {
+    const char* e = getenv("SK_ESC_RATIO");
+    return e ? atof(e) : 8.0;
+  }();
   arena_begin(ctx);  // every temporary of this call comes from the context's arena
   auto cleanup = [&] { arena_end(ctx); };
   try {
@@ -2019,16 +2032,48 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
             owned = r;
             cur = r;
             trace[k + 1] = r->nnz;
+            set_paths(k, 1, SK_PATH_EXACT);
             k += 1;
             pending_wp = wp1;
             if (k >= L) break;
             continue;
           }
         }
+        // every bias <= 0: an empty input stays empty through the whole run of such
+        // layers, and a thin one takes expand-sort-compress
+        if (esc_env && k < L && md->bias_nonpos[k] && cur->nnz == 0) {
+          uint32_t run = 0;
+          while (k + run < L && md->bias_nonpos[k + run]) ++run;
+          for (uint32_t q = 0; q < run; ++q) trace[k + 1 + q] = 0;
+          if (!owned) {
+            owned = new_csr(ctx, m, n, 0);
+            SK_CUDA(cudaMemsetAsync(owned->rp, 0, (size_t(m) + 1) * 4, ctx->stream));
+            cur = owned;
+          }
+          k += run;
+          pending_wp = nullptr;
+          if (k >= L) break;
+          continue;
+        }
+        if (esc_env && k < L && esc_applicable(ctx, md, k, cur, esc_ratio)) {
+          sk_csr* r = esc_layer(ctx, md, cur, k, clip);
+          if (owned) csr_release(owned);
+          owned = r;
+          cur = r;
+          trace[k + 1] = r->nnz;
+          set_paths(k, 1, SK_PATH_ESC);
+          k += 1;
+          pending_wp = nullptr;
+          if (k >= L) break;
+          continue;
+        }
         uint32_t done = 0;
         sk_csr* r = sparse_segment(ctx, md, cur, k, clip, hi, trace.data() + k, &done,
                                    pending_wp);
         pending_wp = nullptr;
+        // the engine skips empty runs itself: those layers keep SK_PATH_EMPTY
+        for (uint32_t q = 0; q < done; ++q)
+          if (trace[k + q] != 0 || !md->bias_nonpos[k + q]) set_paths(k + q, 1, SK_PATH_ENGINE);
         if (owned) csr_release(owned);
         owned = r;
         cur = r;
@@ -2063,6 +2108,7 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
       const int dflag = int(hc[L] & 0xFFFFFFFFull);
       const uint32_t done = dflag ? uint32_t(dflag) : L - k;
       for (uint32_t j = 0; j < done; ++j) trace[k + 1 + j] = hc[j];
+      set_paths(k, done, SK_PATH_DENSE);
       owned = from_dense_impl(ctx, dbuf[(done - 1) & 1], m, n);
       cur = owned;
       k += done;

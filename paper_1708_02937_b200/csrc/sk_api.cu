@@ -274,6 +274,15 @@ extern "C" sk_status sk_ctx_layer_stamps(sk_ctx* ctx, long long* ns, size_t n) {
   });
 }
 
+extern "C" sk_status sk_ctx_layer_paths(sk_ctx* ctx, unsigned char* paths, size_t n) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (n && !paths) fail(SK_ERR_INVALID_ARGUMENT, "null paths buffer");
+    for (size_t q = 0; q < n; ++q)
+      paths[q] = q < ctx->last_paths.size() ? ctx->last_paths[q] : (unsigned char)SK_PATH_EMPTY;
+  });
+}
+
 extern "C" sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count) {
   return guarded([&] {
     require_ctx(ctx);
@@ -472,6 +481,7 @@ extern "C" sk_status sk_model_free(sk_model* m) {
     dfree(m->ctx, m->d_wstats);
     dfree(m->ctx, m->d_bias_nonpos);
     dfree(m->ctx, m->d_nonpos_run);
+    for (sk_csr* t : m->wT) csr_release(t);
     delete m;
   });
 }

@@ -106,6 +106,7 @@ struct sk_ctx {
   // Optional per-layer %globaltimer stamps written by the sparse engine.
   long long* stamps = nullptr;
   uint32_t stamps_cap = 0;
+  std::vector<unsigned char> last_paths;  // per layer of the last sparse forward (SK_PATH_*)
   // Density-adaptive sparse forward: switch to the dense engine when a layer's
   // output has more than dense_above * m * n entries, back to the sparse engine
   // below sparse_below * m * n (sk_ctx_set_density_switch; dense_above <= 0 = off).
@@ -166,6 +167,8 @@ struct sk_model {
   uint32_t* d_nonpos_run = nullptr;  // per layer k: consecutive layers from k with every b <= 0
   int weights_finite = -1;           // every weight finite (-1 = not computed yet)
   std::vector<ValueStats> wstats_host;  // host copy of d_wstats
+  std::vector<sk_csr*> wT;              // per layer W^T (out-edges), built on first ESC use
+  std::vector<uint32_t> wT_maxdeg;      // longest W^T row
 };
 
 namespace sk {
@@ -284,6 +287,9 @@ sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                                 const uint32_t* h_r, const uint32_t* h_c,
                                 uint64_t* dup_index = nullptr);
 sk_csr* csr_transpose(sk_ctx* ctx, const sk_csr* a);
+// Thin layers by expand-sort-compress (k_esc.cu); every bias of layer k <= 0.
+bool esc_applicable(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y, double ratio);
+sk_csr* esc_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y, uint32_t k, float clip);
 void ensure_model_tables(sk_ctx* ctx, sk_model* md);
 void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const float* y0,
                           uint32_t n, float clip, float* buf0, float* buf1,

@@ -135,6 +135,9 @@ def approx_equal_scaled(x, y, scale) -> bool:
 
 # ---- device context ------------------------------------------------------------------
 
+LAYER_PATHS = ("empty", "exact", "esc", "engine", "dense")  # SK_PATH_* (sk_api.h)
+
+
 class Context:
     """One CUDA device + stream (sk_ctx)."""
 
@@ -166,6 +169,13 @@ class Context:
         buf = np.zeros(n, np.int64)
         _check(self._L.sk_ctx_layer_stamps(self.h, buf.ctypes.data_as(C.POINTER(C.c_longlong)), n))
         return buf
+
+    def layer_paths(self, n: int) -> list:
+        """Path names the first n layers of the last sparse forward took: "empty"
+        (no work: empty input, biases <= 0), "exact", "esc", "engine", "dense"."""
+        buf = np.zeros(max(n, 1), np.uint8)
+        _check(self._L.sk_ctx_layer_paths(self.h, buf.ctypes.data_as(C.POINTER(C.c_ubyte)), n))
+        return [LAYER_PATHS[int(x)] for x in buf[:n]]
 
     def set_density_switch(self, dense_above: float = 1.0 / 32, sparse_below: float = 1.0 / 128):
         """Activation density (fraction of m*n) above which relu_forward_sparse

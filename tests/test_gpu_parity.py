@@ -472,6 +472,7 @@ def test_exact_fixed_point_layer_matches_oracle(sk, port, ymax, dense_rows):
     b = np.where(np.arange(m) % 13 == 0, 0.25 if dense_rows else -1.5, -0.5).astype(np.float32)
     model = sk.DnnModel([dev_csr(sk, w) for w in hW], [b] * L)
     out, trace = sk.relu_forward_sparse(model, Y, sk.ForwardOptions(clip=0.0))
+    assert sk.default_context().layer_paths(1) == ["exact"]
     y, want_trace = hY, [hY.nnz]
     for k in range(L):
         y = port.layer_sparse(hW[k], b, y, 0.0)
@@ -527,6 +528,69 @@ def test_exact_path_field_boundaries(sk, port, target, yvals):
     first = port.layer_sparse(hW, b, hY, 0.0)
     assert first.col_idx[first.row_ptr[0]] == 0
     assert first.values[first.row_ptr[0]] == np.float32(t) + np.float32(-0.5)
+
+
+def _thin_model(port, m, L, deg, seed, rng, special=False):
+    from oracle.oracle import Csr
+    hW = []
+    for k in range(L):
+        w = port.gen_layer_fixed(m, deg, port.layer_seed(seed, k), float("nan"))
+        v = rng.uniform(-1.0, 1.0, w.values.size).astype(np.float32)  # not exact
+        if special and k == 0:
+            v[::97] = np.inf
+        hW.append(Csr(m, m, w.row_ptr, w.col_idx, v))
+    return hW
+
+
+@pytest.mark.parametrize("m,n,L,entries", [(4096, 3000, 4, 5000), (4096, 3000, 3, 7),
+                                           (70000, 70000, 2, 300)])
+def test_esc_thin_layers_bitwise(sk, port, m, n, L, entries):
+    # Thin inputs with every bias <= 0 take expand-sort-compress (stable sort of
+    # (i, j) keys, ascending-k run fold); 70000 x 70000 needs 64-bit keys.
+    rng = np.random.default_rng(m + entries)
+    hW = _thin_model(port, m, L, 8, 17, rng, special=(entries == 5000))
+    flat = rng.choice(m * n, size=entries, replace=False)
+    r, c = (flat // n).astype(np.uint32), (flat % n).astype(np.uint32)
+    v = rng.uniform(0.2, 3.0, entries).astype(np.float32)
+    v[::11] = -0.0
+    Y = sk.csr_from_triples(m, n, (r, c, v))
+    hY = host_csr(Y)
+    b = (-rng.uniform(0.0, 0.3, m)).astype(np.float32)
+    b[::5] = 0.0
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], [b] * L)
+    out, trace = sk.relu_forward_sparse(model, Y, sk.ForwardOptions(clip=2.5))
+    paths = sk.default_context().layer_paths(L)
+    y, want_trace = hY, [hY.nnz]
+    for k in range(L):
+        y = port.layer_sparse(hW[k], b, y, 2.5)
+        want_trace.append(y.nnz)
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, y)
+    assert paths[0] == "esc", paths
+
+
+def test_empty_input_runs_and_positive_bias_after(sk, port):
+    # an empty input stays empty through the layers with every bias <= 0 (no
+    # work at all), then a layer with positive biases makes dense rows
+    from oracle.oracle import Csr
+    m, n, L = 2048, 500, 5
+    rng = np.random.default_rng(3)
+    hW = _thin_model(port, m, L, 8, 5, rng)
+    bs = [np.full(m, -0.1, np.float32)] * 3 + [np.where(np.arange(m) % 7 == 0, 0.5, -0.2)
+                                             .astype(np.float32)] + [np.full(m, -0.1, np.float32)]
+    Y = sk.csr_from_triples(m, n, (np.zeros(0, np.uint32), np.zeros(0, np.uint32),
+                                   np.zeros(0, np.float32)))
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], bs)
+    out, trace = sk.relu_forward_sparse(model, Y, sk.ForwardOptions(clip=0.0))
+    paths = sk.default_context().layer_paths(L)
+    y, want_trace = Csr(m, n, np.zeros(m + 1, np.uint32), np.zeros(0, np.uint32),
+                        np.zeros(0, np.float32)), [0]
+    for k in range(L):
+        y = port.layer_sparse(hW[k], bs[k], y, 0.0)
+        want_trace.append(y.nnz)
+    assert list(trace) == want_trace and want_trace[4] > 0
+    assert_csr_bitwise(out, y)
+    assert paths[:3] == ["empty"] * 3 and paths[3] != "empty", paths
 
 
 @pytest.mark.parametrize("entries,bias", [(1, -0.01), (40, -0.01), (40, -0.2), (900, 0.0)])
