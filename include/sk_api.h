@@ -218,7 +218,9 @@ sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m,
  * neurons, BASELINE cfg5); bias is host memory of length m_blk. */
 sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* bias,
                           const sk_csr* y, float clip, sk_csr** out);
-/* Zero-copy view of a handle's device arrays (valid while the handle lives). */
+/* Zero-copy view of a handle's device arrays (valid while the handle lives).
+ * Read-only: handles are immutable (the library caches per-matrix value
+ * statistics). */
 sk_status sk_csr_device_arrays(const sk_csr* a, uint32_t** row_ptr,
                                uint32_t** col_idx, float** values);
 /* New handle from device arrays (copied; e.g. buffers owned by torch/NCCL). */

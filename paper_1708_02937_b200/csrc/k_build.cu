@@ -301,6 +301,10 @@ static sk_status csr_from_host(sk_ctx* ctx, uint32_t rows, uint32_t cols, const 
       else
         SK_LAUNCH(k_fill_f32, grid_for(ctx, nnz), 256, 0, ctx->stream, a->v, nnz, fill);
     }
+    if (!v) {
+      a->stats = const_value_stats(fill, nnz);
+      a->stats_valid = true;
+    }
     if (validate && rows) {
       unsigned long long* bad = reinterpret_cast<unsigned long long*>(ctx->d_u64);
       set_u64(ctx, bad, ~0ull);

@@ -45,6 +45,8 @@
 #include <cstdlib>
 #include <climits>
 
+#include <cstring>
+
 #include "sk_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -1839,6 +1841,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
 
 // Value statistics of a CSR's values, on the host (one small launch + sync).
 static ValueStats host_value_stats(sk_ctx* ctx, const sk_csr* y) {
+  if (y->stats_valid) return y->stats;
   ValueStats* d = dalloc<ValueStats>(ctx, 1);
   const ValueStats init SK_VALUESTATS_INIT;
   SK_CUDA(cudaMemcpyAsync(d, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
@@ -1849,6 +1852,9 @@ static ValueStats host_value_stats(sk_ctx* ctx, const sk_csr* y) {
   SK_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
   dfree(ctx, d);
+  auto* yy = const_cast<sk_csr*>(y);
+  yy->stats = h;
+  yy->stats_valid = true;
   return h;
 }
 
@@ -2126,3 +2132,30 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
 }
 
 }  // namespace sk
+
+// (global scope, next to sk_csr)
+ValueStats const_value_stats(float c, size_t nnz) {
+  ValueStats s SK_VALUESTATS_INIT;
+  if (nnz == 0) return s;
+  uint32_t bits;
+  std::memcpy(&bits, &c, 4);
+  s.vmin = s.vmax = bits;
+  if (!std::isfinite(c)) {
+    s.nonfinite = 1;
+  } else if (c != 0.0f) {
+    const uint32_t b = bits & 0x7fffffffu;
+    const int E = int(b >> 23);
+    uint32_t M = b & 0x7fffffu;
+    int e0;
+    if (E == 0) {
+      e0 = -149;
+    } else {
+      M |= 0x800000u;
+      e0 = E - 150;
+    }
+    s.lowbit = e0 + __builtin_ctz(M);
+    s.ehi = e0 + (32 - __builtin_clz(M));
+    s.absmax = b;
+  }
+  return s;
+}

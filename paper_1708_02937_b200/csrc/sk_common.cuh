@@ -129,16 +129,6 @@ struct sk_dense {
   size_t elems() const { return size_t(rows) * cols; }
 };
 
-struct sk_csr {
-  sk_ctx* ctx = nullptr;
-  uint32_t rows = 0, cols = 0;
-  size_t nnz = 0;
-  uint32_t* rp = nullptr;  // rows+1
-  uint32_t* ci = nullptr;  // nnz
-  float* v = nullptr;      // nnz
-  std::atomic<int> refs{1};
-};
-
 // Per-matrix value statistics (the exactness test of the sparse engine): the
 // smallest power of two every nonzero value is a multiple of ("granularity",
 // lowbit exponent), the smallest e with |v| < 2^e, non-finite values, the
@@ -153,6 +143,26 @@ struct ValueStats {
   unsigned int rowsum;      // weights: bit pattern of an upper bound on max_i sum_k |w_ik|
 };
 #define SK_VALUESTATS_INIT {INT_MAX, INT_MIN, 0, 0, 0xFFFFFFFFu, 0u, 0u, 0u}
+
+// Value statistics of a constant-valued matrix (every one of nnz stored values
+// is c), on the host: the same rules as the device reduction (k_value_stats).
+ValueStats const_value_stats(float c, size_t nnz);
+
+struct sk_csr {
+  sk_ctx* ctx = nullptr;
+  uint32_t rows = 0, cols = 0;
+  size_t nnz = 0;
+  uint32_t* rp = nullptr;  // rows+1
+  uint32_t* ci = nullptr;  // nnz
+  float* v = nullptr;      // nnz
+  std::atomic<int> refs{1};
+  // value statistics, computed once (handles are immutable: the zero-copy
+  // device view is read-only) or known at construction (constant values)
+  bool stats_valid = false;
+  ValueStats stats;
+};
+
+
 
 struct sk_model {
   sk_ctx* ctx = nullptr;

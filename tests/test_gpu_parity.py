@@ -112,6 +112,30 @@ def test_csr_from_pattern(sk, port):
     assert e.nnz() == 0
 
 
+@pytest.mark.parametrize("c", [1.0, 0.375, -2.0, 0.0, float("nan"), 3e-39, 6.0])
+def test_pattern_inputs_forward_like_explicit_values(sk, port, c):
+    # a constant-valued input's statistics are known on the host (no device
+    # pass): the forward must match the same matrix built from explicit values
+    # and the oracle, whatever path the statistics select
+    m, n, L = 2048, 1500, 3
+    Y = port.gen_input_binary(m, n, 40, 9)
+    vals = np.full(Y.nnz, c, np.float32)
+    a = sk.CsrMatrix.from_pattern(m, n, Y.row_ptr, Y.col_idx, c)
+    b = sk.CsrMatrix(m, n, Y.row_ptr, Y.col_idx, vals)
+    hW = [port.gen_layer_fixed(m, 16, port.layer_seed(4, k), 1.0 / 8) for k in range(L)]
+    bias = np.full(m, -0.25, np.float32)
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], [bias] * L)
+    oa, ta = sk.relu_forward_sparse(model, a, sk.ForwardOptions(clip=4.0))
+    ob, tb = sk.relu_forward_sparse(model, b, sk.ForwardOptions(clip=4.0))
+    from oracle.oracle import Csr
+    y = Csr(m, n, Y.row_ptr, Y.col_idx, vals)
+    for k in range(L):
+        y = port.layer_sparse(hW[k], bias, y, 4.0)
+    assert list(ta) == list(tb)
+    assert_csr_bitwise(oa, y)
+    assert_csr_bitwise(ob, y)
+
+
 def test_validating_constructor_messages(sk):
     kat = json.load(open(os.path.join(GOLDEN, "kat.json")))["validate_errors"]
     cases = {"not_monotone": (3, 2, [0, 1, 0, 1], [0], [1.0]),
