@@ -977,6 +977,8 @@ extern "C" sk_status sk_gen_input_binary(sk_ctx* ctx, uint32_t m, uint32_t n, ui
     sk_csr* b = gen_fixed_csr(ctx, n, m, k, splitmix_at(seed, 4), sample_offset, 0, 1.0f, 0);
     sk_csr* t = csr_transpose(ctx, b);
     csr_release(b);
+    t->stats = const_value_stats(1.0f, t->nnz);  // binary: known at construction
+    t->stats_valid = true;
     *out = t;
   });
 }

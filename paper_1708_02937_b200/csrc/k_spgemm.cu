@@ -1070,24 +1070,40 @@ __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
 }
 
 // Window table of a plain CSR: wp[k*nW+w] = rp[k] + lower_bound(row k, w*S).
+// Window table wp[k*nW + w] = first entry of row k with sample >= w*S (warp per
+// row: the row's samples are read once, coalesced; an entry whose window
+// differs from its predecessor's opens the windows in between).
 __global__ void k_build_wp(const uint32_t* rp, const uint32_t* ci, uint32_t rows, uint32_t nW,
                            int sh, uint32_t* wp) {
-  const uint64_t n = uint64_t(rows) * nW;
-  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t <= n;
-       t += uint64_t(gridDim.x) * blockDim.x) {
-    if (t == n) {
-      wp[n] = rows ? rp[rows] : 0;
-      continue;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k = gw; k < rows; k += nw) {
+    const uint32_t rb = rp[k], re = rp[k + 1];
+    uint32_t* const out = wp + size_t(k) * nW;
+    int carry = -1;  // window of the entry before this chunk (-1: none)
+    for (uint32_t e0 = rb; e0 < re; e0 += 128) {
+      int we[4];  // four chunks' loads in flight before any is used
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t e = e0 + 32 * u + lane;
+        we[u] = e < re ? int(__ldg(ci + e) >> sh) : int(nW);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t e = e0 + 32 * u + lane;
+        int prev = __shfl_up_sync(0xffffffffu, we[u], 1);
+        if (lane == 0) prev = carry;
+        if (e < re)
+          for (int w = prev + 1; w <= we[u]; ++w) out[w] = e;
+        carry = __shfl_sync(0xffffffffu, we[u], 31);
+      }
     }
-    const uint32_t k = uint32_t(t / nW), w = uint32_t(t % nW);
-    uint32_t lo = rp[k], hi = rp[k + 1];
-    const uint32_t target = w << sh;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (ci[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    wp[t] = lo;
+    // windows after the row's last entry (all of them for an empty row)
+    const int last = re > rb ? int(ci[re - 1] >> sh) : -1;
+    for (int w = last + 1 + lane; w < int(nW); w += 32) out[w] = re;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) wp[size_t(rows) * nW] = rows ? rp[rows] : 0;
 }
 
 __global__ void k_rp_from_wp(const uint32_t* wp, uint32_t rows, uint32_t nW, uint32_t* rp) {
@@ -1486,8 +1502,8 @@ static unsigned grid_warps(sk_ctx* ctx, uint64_t warps) {
 static uint32_t* build_wp(sk_ctx* ctx, const sk_csr* b, const WinGeom& g, bool arena = false) {
   const uint64_t n = uint64_t(b->rows) * g.nW;
   uint32_t* wp = arena ? aalloc<uint32_t>(ctx, n + 1) : dalloc<uint32_t>(ctx, n + 1);
-  SK_LAUNCH(k_build_wp, unsigned(std::min<uint64_t>((n + 256) / 256, uint64_t(ctx->num_sms) * 16)),
-            256, 0, ctx->stream, b->rp, b->ci, b->rows, g.nW, g.sh, wp);
+  SK_LAUNCH(k_build_wp, grid_warps(ctx, b->rows), 256, 0, ctx->stream, b->rp, b->ci, b->rows,
+            g.nW, g.sh, wp);
   return wp;
 }
 
