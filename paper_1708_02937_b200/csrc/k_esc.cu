@@ -107,6 +107,130 @@ __global__ void k_esc_row_ptr(const K* okey, uint32_t S, uint32_t rows, uint32_t
   }
 }
 
+// ---- small layers: one block does everything in shared memory ------------------
+// (products <= kSmallCap: expand, stable block radix sort, run fold, compaction)
+constexpr int kSmallThreads = 1024, kSmallItems = 2;
+constexpr uint32_t kSmallCap = uint32_t(kSmallThreads) * kSmallItems;  // products
+constexpr uint32_t kSmallEntries = 512;                                 // input entries
+
+// row id of every input entry (warp per row; only the small path needs it)
+__global__ void k_esc_entry_rows(const uint32_t* yrp, uint32_t rows, uint32_t* erow) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < rows;
+       k += (gridDim.x * blockDim.x) >> 5)
+    for (uint32_t e = yrp[k] + lane; e < yrp[k + 1]; e += 32) erow[e] = k;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSmallThreads)
+    k_esc_small(const uint32_t* erow, const uint32_t* yci, const float* yv, uint32_t nnz,
+                uint32_t n, const uint32_t* trp, const uint32_t* tci, const float* tv,
+                const float* bias, float clip, int end_bit, K* okey, float* ov,
+                uint32_t* count) {
+  using Sort = cub::BlockRadixSort<K, kSmallThreads, kSmallItems, float>;
+  using Scan = cub::BlockScan<uint32_t, kSmallThreads>;
+  // the staging arrays share storage with the block primitives' temporaries
+  // (every hand-off is separated by a barrier)
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+    struct {
+      K key[kSmallCap];
+      float val[kSmallCap];
+    } buf;
+  } tmp;
+  __shared__ uint32_t s_off[kSmallEntries + 1];  // entry -> first product
+  __shared__ uint32_t s_tb[kSmallEntries];       // entry -> its W^T row start
+  K* const skey = tmp.buf.key;
+  float* const sval = tmp.buf.val;
+  const uint32_t tid = threadIdx.x;
+  // 1. product offsets of the thread's entries (blocked)
+  uint32_t ed[kSmallItems], eo[kSmallItems];
+#pragma unroll
+  for (int u = 0; u < kSmallItems; ++u) {
+    const uint32_t e = tid * kSmallItems + u;
+    ed[u] = 0;
+    if (e < nnz) {
+      const uint32_t k = erow[e], tb = trp[k];
+      s_tb[e] = tb;
+      ed[u] = trp[k + 1] - tb;
+    }
+  }
+  uint32_t P;
+  Scan(tmp.scan).ExclusiveSum(ed, eo, P);
+#pragma unroll
+  for (int u = 0; u < kSmallItems; ++u) {
+    const uint32_t e = tid * kSmallItems + u;
+    if (e < nnz) s_off[e] = eo[u];
+  }
+  if (tid == 0) s_off[nnz] = P;
+  __syncthreads();
+  // 2. expand, a product per thread (entry found in the offsets); input order
+  //    (ascending k) is the product index order
+  for (uint32_t q = tid; q < P; q += kSmallThreads) {
+    uint32_t lo = 0, hi = nnz;  // last entry with s_off[e] <= q
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_off[mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t t = s_tb[lo] + (q - s_off[lo]);
+    skey[q] = K(tci[t]) * K(n) + K(yci[lo]);
+    sval[q] = __fmul_rn(tv[t], yv[lo]);
+  }
+  __syncthreads();
+  // 3. stable sort; padding sorts after every product (largest key, last in order)
+  K keys[kSmallItems];
+  float vals[kSmallItems];
+#pragma unroll
+  for (int u = 0; u < kSmallItems; ++u) {
+    const uint32_t q = tid * kSmallItems + u;
+    keys[u] = q < P ? skey[q] : ~K(0);
+    vals[u] = q < P ? sval[q] : 0.0f;
+  }
+  __syncthreads();
+  Sort(tmp.sort).Sort(keys, vals, 0, end_bit);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kSmallItems; ++u) {
+    skey[tid * kSmallItems + u] = keys[u];
+    sval[tid * kSmallItems + u] = vals[u];
+  }
+  __syncthreads();
+  // 4. run heads fold ascending k, epilogue, 5. compaction in key order
+  uint32_t keep[kSmallItems], pos[kSmallItems];
+  float z[kSmallItems];
+#pragma unroll
+  for (int u = 0; u < kSmallItems; ++u) {
+    const uint32_t q = tid * kSmallItems + u;
+    keep[u] = 0;
+    z[u] = 0.0f;
+    keys[u] = skey[q];
+    if (q < P && (q == 0 || skey[q - 1] != skey[q])) {
+      float acc = 0.0f;
+      for (uint32_t r = q; r < P && skey[r] == skey[q]; ++r) acc = __fadd_rn(acc, sval[r]);
+      z[u] = layer_epilogue(acc, bias[uint32_t(skey[q] / K(n))], clip);
+      keep[u] = z[u] != 0.0f ? 1u : 0u;
+    }
+  }
+  uint32_t S;
+  __syncthreads();
+  Scan(tmp.scan).ExclusiveSum(keep, pos, S);
+#pragma unroll
+  for (int u = 0; u < kSmallItems; ++u)
+    if (keep[u]) {
+      okey[pos[u]] = keys[u];
+      ov[pos[u]] = z[u];
+    }
+  if (tid == 0) *count = S;
+}
+
+template <typename K>
+__global__ void k_esc_cols(const K* okey, uint32_t S, uint32_t n, uint32_t* oci) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < S; t += gridDim.x * blockDim.x)
+    oci[t] = uint32_t(okey[t] % K(n));
+}
+
 unsigned grid_of(sk_ctx* ctx, uint64_t threads) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((threads + 255) / 256,
                                                             uint64_t(ctx->num_sms) * 16)));
@@ -119,7 +243,35 @@ int bits_for(uint64_t v) {  // smallest b with v <= 2^b
 }
 
 template <typename K>
-sk_csr* esc_run(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip) {
+sk_csr* esc_small(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip) {
+  const uint32_t m = wt->cols, n = y->cols;
+  K* okey = aalloc<K>(ctx, kSmallCap);
+  float* ov = aalloc<float>(ctx, kSmallCap);
+  uint32_t* cnt = aalloc<uint32_t>(ctx, 1);
+  uint32_t* erow = aalloc<uint32_t>(ctx, y->nnz);
+  SK_LAUNCH(k_esc_entry_rows, grid_of(ctx, uint64_t(y->rows) * 32), 256, 0, ctx->stream, y->rp,
+            y->rows, erow);
+  SK_LAUNCH(k_esc_small<K>, 1, kSmallThreads, 0, ctx->stream, erow, y->ci, y->v,
+            uint32_t(y->nnz), n, wt->rp, wt->ci, wt->v, bias, clip, bits_for(uint64_t(m) * n),
+            okey, ov, cnt);
+  uint32_t S = 0;
+  SK_CUDA(cudaMemcpyAsync(&S, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  sk_csr* out = new_csr(ctx, m, n, S);
+  if (S) {
+    SK_CUDA(cudaMemcpyAsync(out->v, ov, size_t(S) * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    SK_LAUNCH(k_esc_cols<K>, grid_of(ctx, S), 256, 0, ctx->stream, okey, S, n, out->ci);
+  }
+  SK_LAUNCH(k_esc_row_ptr<K>, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, okey, S, m, n,
+            out->rp);
+  return out;
+}
+
+template <typename K>
+sk_csr* esc_run(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip,
+                uint32_t maxdeg) {
+  if (y->nnz <= kSmallEntries && double(y->nnz) * double(maxdeg) <= double(kSmallCap))
+    return esc_small<K>(ctx, y, wt, bias, clip);
   const uint32_t m = wt->cols, n = y->cols, rows = y->rows;
   const size_t nnz = y->nnz;
   // 1. per-entry product counts, scanned (sentinel entry -> total)
@@ -230,9 +382,10 @@ sk_csr* esc_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y, uint32_t k, 
   auto* mm = const_cast<sk_model*>(md);
   const sk_csr* wt = layer_transpose(ctx, mm, k);
   const float* bias = md->bias + size_t(k) * md->neurons;
+  const uint32_t maxdeg = mm->wT_maxdeg[k];
   return uint64_t(md->neurons) * y->cols <= 0xFFFFFFFFull
-             ? esc_run<uint32_t>(ctx, y, wt, bias, clip)
-             : esc_run<uint64_t>(ctx, y, wt, bias, clip);
+             ? esc_run<uint32_t>(ctx, y, wt, bias, clip, maxdeg)
+             : esc_run<uint64_t>(ctx, y, wt, bias, clip, maxdeg);
 }
 
 }  // namespace sk

@@ -570,7 +570,7 @@ def _thin_model(port, m, L, deg, seed, rng, special=False):
 
 
 @pytest.mark.parametrize("m,n,L,entries", [(4096, 3000, 4, 5000), (4096, 3000, 3, 7),
-                                           (70000, 70000, 2, 300)])
+                                           (70000, 70000, 2, 300), (70000, 70000, 2, 40)])
 def test_esc_thin_layers_bitwise(sk, port, m, n, L, entries):
     # Thin inputs with every bias <= 0 take expand-sort-compress (stable sort of
     # (i, j) keys, ascending-k run fold); 70000 x 70000 needs 64-bit keys.
