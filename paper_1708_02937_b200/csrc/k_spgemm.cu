@@ -74,6 +74,16 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 __host__ __device__ constexpr uint32_t list_cap(uint32_t S) { return S / 4; }
 constexpr uint32_t kStage = 512;  // staged products per warp (expansion buffer)
 constexpr uint32_t kGroup = 4;    // windows per work item
+// Windows per exact-path item: an item's in-edge loads and window-table sectors
+// are shared by its xgroup / P accumulator passes, so larger items cut the L2
+// traffic of wide layers (cfg5: 16 windows instead of 4 took 5.1 -> 4.1 ms);
+// the largest of 16 / 8 / 4 that still leaves >= 16 items per warp.
+__host__ __device__ __forceinline__ uint32_t exact_group(uint32_t m, uint32_t nW,
+                                                         uint64_t warps) {
+  for (uint32_t G = 16; G > kGroup; G >>= 1)
+    if (uint64_t(m) * ((nW + G - 1) / G) >= 16 * warps) return G;
+  return kGroup;
+}
 __host__ __device__ constexpr size_t warp_smem_bytes(uint32_t S) {
   // acc | surv | staged prod | list | staged sample; rounded to 16 B (acc is
   // read and written as uint4)
@@ -134,6 +144,7 @@ struct RowArgs {
   uint32_t fx_pack;            // exact mode: windows per accumulator word (1, 2, 4)
   int y_const;                 // exact mode: every B value is y_cval (no value loads)
   float y_cval;
+  uint32_t xgroup;             // exact mode: windows per item (multiple of kGroup)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
@@ -610,8 +621,8 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
   const uint32_t fmask = P == 1 ? 0xFFFFFFFFu : ((1u << B) - 1u);
   const uint32_t fbias = P == 1 ? 0u : (1u << (B - 1));
   const uint32_t clearw = fx_clear_word(P);
-  const uint32_t w0 = g * kGroup;
-  const uint32_t wn = min(kGroup, p.nW - w0);
+  const uint32_t w0 = g * p.xgroup;
+  const uint32_t wn = min(p.xgroup, p.nW - w0);
   const uint32_t eb = p.arp[i], ee = p.arp[i + 1];
   const uint32_t deg = ee - eb;
   const float b = kLayer ? p.bias[i] : 0.0f;
@@ -780,7 +791,8 @@ template <typename Ops, bool kLayer, bool kExact, int kSh = 0>
 __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
                                         uint64_t gw, uint64_t nwarps,
                                         const uint32_t* rows = nullptr, uint32_t nrows = 0) {
-  const uint32_t ng = (p.nW + kGroup - 1) / kGroup;
+  const uint32_t G = kExact ? p.xgroup : kGroup;  // windows per item
+  const uint32_t ng = (p.nW + G - 1) / G;
   const uint32_t nr = rows ? nrows : p.m;
   if (nr == 0) return;
   // item it = g * nr + r, walked incrementally (no 64-bit division per item)
@@ -798,7 +810,12 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
         const uint32_t S = 1u << p.sh, cw = fx_clear_word(p.fx_pack);
         for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = 0u;
         __syncwarp();
-        process_item<Ops, kLayer, true>(p, i, uint32_t(g), ws, lane);
+        // the item's engine-sized groups
+        const uint32_t ng4 = (p.nW + kGroup - 1) / kGroup;
+        for (uint32_t q = 0; q < G / kGroup; ++q) {
+          const uint32_t g4 = uint32_t(g) * (G / kGroup) + q;
+          if (g4 < ng4) process_item<Ops, kLayer, true>(p, i, g4, ws, lane);
+        }
         for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
         __syncwarp();
       } else if (kSh && p.y_const) {
@@ -1262,6 +1279,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     ra.fx_scale = 1.0f;
     ra.fx_unscale = 1.0f;
     ra.fx_pack = 1;
+    ra.xgroup = kGroup;
     ra.y_const = 0;
     ra.y_cval = 0.0f;
 
@@ -1270,7 +1288,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     // order-free path (shared atomics, zero-initialised windows) is bitwise the
     // ascending fold.  Decided identically by every warp.
     const bool exact = layer == 0 && p.exact_ok && products_exact(p.wstats[0], *p.y0stats);
-    if (exact) exact_params(p.wstats[0], *p.y0stats, S, ra);
+    if (exact) {
+      exact_params(p.wstats[0], *p.y0stats, S, ra);
+      ra.xgroup = exact_group(p.m, p.nW, nwarps);
+    }
     // Near-empty input with every bias <= 0: an output row with no in-edge from
     // an input row holding entries has no entries, so only the frontier rows are
     // processed (and the others' item counts zeroed).  Uniform decision.
@@ -1566,6 +1587,7 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   int* overflow = reinterpret_cast<int*>(d + 1);
 
   RowArgs p;
+  p.xgroup = kGroup;
   p.arp = a->rp;
   p.aci = a->ci;
   p.av = a->v;
@@ -1951,6 +1973,12 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     p.overflow = reinterpret_cast<int*>(d + 1);
     p.err = ctx->d_err;
     exact_params(md->wstats_host[k0], ystats, g.S, p);
+    static const uint32_t env_group = [] {  // SK_EXACT_GROUP=4|8|16 (A/B measurements)
+      const char* e = getenv("SK_EXACT_GROUP");
+      const int v = e ? atoi(e) : 0;
+      return (v == 4 || v == 8 || v == 16) ? uint32_t(v) : 0u;
+    }();
+    p.xgroup = env_group ? env_group : exact_group(m, g.nW, uint64_t(grid) * kWarps);
     long long* stamp = (ctx->stamps && k0 < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
     timing_mark(ctx);
     SK_LAUNCH(k_exact_layer, grid, kWarps * 32, smem, ctx->stream, p, stamp);
