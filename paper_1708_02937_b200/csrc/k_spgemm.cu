@@ -716,21 +716,26 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
     }
     __syncwarp();
     // ---- emit each window of the accumulator ---------------------------------------
+    // windows holding candidates (candidate bits exist only below n); the others
+    // have no output and their counts are written at once
+    uint32_t cmask = 0;
+    if (any)
+      for (uint32_t sub = 0; sub < np; ++sub) {
+        uint32_t anyc = 0;
+        for (uint32_t q = lane; q < SW; q += 32) anyc |= cand[sub * SW + q];
+        if (__any_sync(0xffffffffu, anyc != 0)) cmask |= 1u << sub;
+      }
+    if (uint32_t(lane) < np && !((cmask >> lane) & 1u))
+      p.item_cnt[uint64_t(i) * p.nW + w0 + gw + lane] = 0;
 #pragma unroll 1
-    for (uint32_t sub = 0; sub < np; ++sub) {
+    for (; cmask; cmask &= cmask - 1) {
+      const uint32_t sub = __ffs(cmask) - 1;
       const uint32_t w = w0 + gw + sub;
       const uint64_t it = uint64_t(i) * p.nW + w;
       const uint32_t swbase = w << sh;
       const uint32_t wlen = min(S, p.n - swbase);
       const uint32_t nwords = (wlen + 31) >> 5;
       uint32_t* const cw = cand + sub * SW;
-      uint32_t anyc = 0;
-      if (any)
-        for (uint32_t q = lane; q < nwords; q += 32) anyc |= cw[q];
-      if (!__any_sync(0xffffffffu, anyc != 0)) {
-        if (lane == 0) p.item_cnt[it] = 0;
-        continue;
-      }
       const uint32_t fs = B * sub;
       const uint32_t per = (nwords + 31) >> 5;
       const uint32_t q0 = min(nwords, lane * per), q1 = min(nwords, q0 + per);
