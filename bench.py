@@ -474,9 +474,24 @@ def run_ours(args, w):
         for a in (host_rp, host_ci):
             sk._lib.load().sk_host_register(a.ctypes.data, a.nbytes)
         h2d = host_rp.nbytes + host_ci.nbytes
+        copy_stream = torch.cuda.Stream()
+
+        def upload():
+            # on a copy stream: overlaps the forward already queued on the compute stream
+            return sk.CsrMatrix.from_pattern_async(m, B, host_rp, host_ci, 1.0,
+                                                   stream=copy_stream.cuda_stream)
+
+        pending = []
+        left = [0]  # steps still to run after this one (no upload beyond the last)
 
         def e2e_step():
-            y = sk.CsrMatrix.from_pattern(m, B, host_rp, host_ci, 1.0, validate=False)
+            # double-buffered input: step s+1's upload is issued before step s's
+            # forward, so the host link and the GPU work overlap; every step's
+            # copy still happens inside the timed region
+            y = pending.pop() if pending else upload()
+            if left[0] > 0:
+                pending.append(upload())
+                left[0] -= 1
             out, tr = run(y)
             cats = sk.categories(out)
             return cats.nbytes + 8 * (L + 1)
@@ -489,8 +504,12 @@ def run_ours(args, w):
         def e2e_step():
             sk.relu_forward_host(model, host_y, sk.ForwardOptions(clip=w["clip"]), out=out_host)
             return out_host.nbytes
+    if w["y0"] == "binary":
+        left[0] = max(1, args.warmup) - 1
     for _ in range(max(1, args.warmup)):
         e2e_step()
+    if w["y0"] == "binary":
+        left[0] = args.steps - 1  # the timed region uploads its own inputs
     barrier()
     t0 = time.perf_counter()
     e0.record(stream)
@@ -619,7 +638,12 @@ def run_ours(args, w):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step_ms},
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step_ms,
+                    "input_upload": ("double-buffered: step s+1's pattern upload (copy stream, "
+                                     "sk_csr_from_pattern_async) overlaps step s's forward; "
+                                     "every step's upload and result read inside the timed "
+                                     "region" if w["y0"] == "binary" else
+                                     "synchronous per step (sk_relu_forward_host)")},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }

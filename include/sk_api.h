@@ -145,6 +145,14 @@ sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols,
 sk_status sk_csr_from_pattern(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                               const uint32_t* row_ptr, const uint32_t* col_idx,
                               float value, int validate, sk_csr** out);
+/* sk_csr_from_pattern without validation, on a caller stream (cudaStream_t):
+ * the copies run there, overlapping work queued on the context's stream, and
+ * every later use of the handle is ordered after them (an event on the handle).
+ * The host arrays must stay valid (and should be page-locked) until then.  For
+ * double-buffered input uploads.  No reference counterpart. */
+sk_status sk_csr_from_pattern_async(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                    const uint32_t* row_ptr, const uint32_t* col_idx,
+                                    float value, void* stream, sk_csr** out);
 sk_status sk_csr_shape(const sk_csr* a, uint32_t* rows, uint32_t* cols,
                        size_t* nnz);
 /* extractTuples / span accessors (matrix.hpp:99-108): D2H copy of the three

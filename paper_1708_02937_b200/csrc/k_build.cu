@@ -343,6 +343,43 @@ extern "C" sk_status sk_csr_from_parts(sk_ctx* ctx, uint32_t rows, uint32_t cols
   return csr_from_host(ctx, rows, cols, rp, ci, v, 0.0f, validate, out);
 }
 
+// The pattern upload on a caller stream (e.g. a copy stream), so that it
+// overlaps work already queued on the context's stream; the handle carries an
+// event every consumer waits on.  No validation (the caller's pattern is
+// trusted, as with validate = 0).
+extern "C" sk_status sk_csr_from_pattern_async(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                               const uint32_t* rp, const uint32_t* ci,
+                                               float value, void* stream, sk_csr** out) {
+  return guarded([&] {
+    if (!ctx) fail(SK_ERR_INVALID_ARGUMENT, "null context");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t nnz = rp[rows];
+    auto* a = new sk_csr;
+    a->ctx = ctx;
+    a->rows = rows;
+    a->cols = cols;
+    a->nnz = nnz;
+    void* p = nullptr;
+    SK_CUDA(cudaMallocAsync(&p, (size_t(rows) + 1) * 4, s));
+    a->rp = static_cast<uint32_t*>(p);
+    SK_CUDA(cudaMallocAsync(&p, std::max<size_t>(nnz, 1) * 4, s));
+    a->ci = static_cast<uint32_t*>(p);
+    SK_CUDA(cudaMallocAsync(&p, std::max<size_t>(nnz, 1) * 4, s));
+    a->v = static_cast<float*>(p);
+    SK_CUDA(cudaMemcpyAsync(a->rp, rp, (size_t(rows) + 1) * 4, cudaMemcpyHostToDevice, s));
+    if (nnz) {
+      SK_CUDA(cudaMemcpyAsync(a->ci, ci, nnz * 4, cudaMemcpyHostToDevice, s));
+      SK_LAUNCH(k_fill_f32, grid_for(ctx, nnz), 256, 0, s, a->v, nnz, value);
+    }
+    a->stats = const_value_stats(value, nnz);
+    a->stats_valid = true;
+    SK_CUDA(cudaEventCreateWithFlags(&a->ready, cudaEventDisableTiming));
+    SK_CUDA(cudaEventRecord(a->ready, s));
+    *out = a;
+  });
+}
+
 extern "C" sk_status sk_csr_from_pattern(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                                          const uint32_t* rp, const uint32_t* ci, float value,
                                          int validate, sk_csr** out) {
@@ -404,6 +441,7 @@ __global__ void k_compact_rows(const float* d, uint32_t rows, uint32_t cols,
 
 extern "C" sk_status sk_to_dense(sk_ctx* ctx, const sk_csr* a, float ambient, sk_dense** out) {
   return guarded([&] {
+    csr_ready(ctx, a);
     SK_CUDA(cudaSetDevice(ctx->device));
     sk_dense* d = new_dense(ctx, a->rows, a->cols);
     fill(ctx, d->d, d->elems(), ambient);
@@ -602,6 +640,7 @@ extern "C" sk_status sk_ewise_dense(sk_ctx* ctx, int mul, const sk_dense* a,
 extern "C" sk_status sk_ewise_mixed(sk_ctx* ctx, int mul, const sk_csr* sp, const sk_dense* dn,
                                     int sparse_left, sk_semiring s, sk_dense** out) {
   return guarded([&] {
+    csr_ready(ctx, sp);
     SK_CUDA(cudaSetDevice(ctx->device));
     const char* op = mul ? "ewise_mul" : "ewise_add";
     if (sparse_left)
@@ -642,6 +681,8 @@ extern "C" sk_status sk_ewise_mixed(sk_ctx* ctx, int mul, const sk_csr* sp, cons
 extern "C" sk_status sk_ewise_csr(sk_ctx* ctx, int mul, const sk_csr* a, const sk_csr* b,
                                   sk_semiring s, sk_csr** out) {
   return guarded([&] {
+    csr_ready(ctx, a);
+    csr_ready(ctx, b);
     SK_CUDA(cudaSetDevice(ctx->device));
     require_same_shape(mul ? "ewise_mul" : "ewise_add", a->rows, a->cols, b->rows, b->cols);
     const uint32_t rows = a->rows;
@@ -723,6 +764,7 @@ void categories_from_flags(sk_ctx* ctx, uint8_t* flags, uint32_t n, uint32_t* id
 extern "C" sk_status sk_categories_csr(sk_ctx* ctx, const sk_csr* y, uint32_t* idx, size_t cap,
                                        size_t* count) {
   return guarded([&] {
+    csr_ready(ctx, y);
     SK_CUDA(cudaSetDevice(ctx->device));
     uint8_t* flags = dalloc<uint8_t>(ctx, y->cols);
     SK_CUDA(cudaMemsetAsync(flags, 0, y->cols, ctx->stream));

@@ -283,6 +283,7 @@ static void require_inner(const char* op, uint32_t ac, uint32_t br) {
 extern "C" sk_status sk_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const sk_dense* b,
                                       sk_semiring s, sk_dense** out) {
   return guarded([&] {
+    csr_ready(ctx, a);
     SK_CUDA(cudaSetDevice(ctx->device));
     require_inner("mxm", a->cols, b->rows);
     sk_dense* o = new_dense(ctx, a->rows, b->cols);
@@ -321,6 +322,8 @@ extern "C" sk_status sk_mxm_dense_dense(sk_ctx* ctx, const sk_dense* a, const sk
 extern "C" sk_status sk_mxm_csr_csr(sk_ctx* ctx, const sk_csr* a, const sk_csr* b,
                                     sk_semiring s, sk_csr** out) {
   return guarded([&] {
+    csr_ready(ctx, a);
+    csr_ready(ctx, b);
     SK_CUDA(cudaSetDevice(ctx->device));
     require_inner("mxm", a->cols, b->rows);
     sk_csr* o = mxm_csr_csr_impl(ctx, a, b, s);

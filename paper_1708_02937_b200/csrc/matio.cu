@@ -306,6 +306,7 @@ extern "C" sk_status sk_read_matrix(sk_ctx* ctx, const char* path, int* kind, sk
 extern "C" sk_status sk_format_matrix(sk_ctx* ctx, const sk_csr* csr, const sk_dense* dense,
                                       char* buf, size_t cap, size_t* len) {
   return guarded([&] {
+    csr_ready(ctx, csr);
     if (!csr == !dense) fail(SK_ERR_INVALID_ARGUMENT, "pass exactly one of csr / dense");
     const std::string t = format_matrix(ctx, csr, dense);
     *len = t.size();
@@ -320,6 +321,7 @@ extern "C" sk_status sk_format_matrix(sk_ctx* ctx, const sk_csr* csr, const sk_d
 extern "C" sk_status sk_write_matrix(sk_ctx* ctx, const sk_csr* csr, const sk_dense* dense,
                                      const char* path) {
   return guarded([&] {
+    csr_ready(ctx, csr);
     if (!csr == !dense) fail(SK_ERR_INVALID_ARGUMENT, "pass exactly one of csr / dense");
     std::ofstream out(path, std::ios::binary);
     if (!out) fail(SK_ERR, std::string("cannot open '") + path + "' for writing");

@@ -80,6 +80,10 @@ sk_csr* new_csr(sk_ctx* ctx, uint32_t rows, uint32_t cols, size_t nnz) {
 void csr_release(sk_csr* a) {
   if (!a) return;
   if (a->refs.fetch_sub(1) == 1) {
+    if (a->ready) {
+      csr_ready(a->ctx, a);  // the copies finish before the stream-ordered frees
+      cudaEventDestroy(a->ready);
+    }
     dfree(a->ctx, a->rp);
     dfree(a->ctx, a->ci);
     dfree(a->ctx, a->v);
@@ -403,6 +407,7 @@ extern "C" sk_status sk_csr_shape(const sk_csr* a, uint32_t* rows, uint32_t* col
 extern "C" sk_status sk_csr_extract(sk_ctx* ctx, const sk_csr* a, uint32_t* rp,
                                     uint32_t* ci, float* v) {
   return guarded([&] {
+    csr_ready(ctx, a);
     require_ctx(ctx);
     if (rp)
       SK_CUDA(cudaMemcpyAsync(rp, a->rp, (size_t(a->rows) + 1) * 4,
@@ -434,6 +439,7 @@ extern "C" sk_status sk_model_create(sk_ctx* ctx, uint32_t layers,
     const uint32_t m = weights[0]->rows;
     for (uint32_t k = 0; k < layers; ++k) {
       const sk_csr* w = weights[k];
+      csr_ready(ctx, w);
       if (w->rows != m || w->cols != m)
         fail(SK_ERR_DIMENSION, "layer " + std::to_string(k) + " weight is " +
                                    dim_string(w->rows, w->cols) + "; all layers must be " +
@@ -501,6 +507,7 @@ extern "C" sk_status sk_layer_step(sk_ctx* ctx, const sk_csr* w, const float* bi
                                    const sk_dense* y, const sk_fwd_opts* opt,
                                    sk_dense** out) {
   return guarded([&] {
+    csr_ready(ctx, w);
     require_ctx(ctx);
     // dnn.cpp:89-98
     if (w->cols != y->rows)
@@ -567,6 +574,7 @@ extern "C" sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m, cons
                                             const sk_fwd_opts* opt, sk_csr** out,
                                             uint64_t* nnz_trace) {
   return guarded([&] {
+    csr_ready(ctx, y0);
     require_ctx(ctx);
     if (y0->rows != m->neurons || y0->cols < 1)
       fail(SK_ERR_DIMENSION, "input batch is " + dim_string(y0->rows, y0->cols) +
@@ -583,6 +591,8 @@ extern "C" uint64_t sk_layer_seed(uint64_t seed, uint32_t layer) {
 extern "C" sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* bias,
                                      const sk_csr* y, float clip, sk_csr** out) {
   return guarded([&] {
+    csr_ready(ctx, w);
+    csr_ready(ctx, y);
     require_ctx(ctx);
     if (w->cols != y->rows)
       fail(SK_ERR_DIMENSION, "weight is " + dim_string(w->rows, w->cols) + " but input has " +
@@ -604,6 +614,7 @@ extern "C" sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* 
 extern "C" sk_status sk_csr_device_arrays(const sk_csr* a, uint32_t** rp, uint32_t** ci,
                                           float** v) {
   return guarded([&] {
+    if (a && a->ready) SK_CUDA(cudaEventSynchronize(a->ready));  // no stream to order
     if (rp) *rp = a->rp;
     if (ci) *ci = a->ci;
     if (v) *v = a->v;

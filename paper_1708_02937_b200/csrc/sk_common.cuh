@@ -160,6 +160,9 @@ struct sk_csr {
   // device view is read-only) or known at construction (constant values)
   bool stats_valid = false;
   ValueStats stats;
+  // set by the stream-asynchronous constructor: the arrays are complete once
+  // this event has fired (every consumer orders its stream after it)
+  cudaEvent_t ready = nullptr;
 };
 
 
@@ -206,6 +209,11 @@ T* aalloc(sk_ctx* ctx, size_t n) {
 sk_dense* new_dense(sk_ctx* ctx, uint32_t rows, uint32_t cols);
 sk_csr* new_csr(sk_ctx* ctx, uint32_t rows, uint32_t cols, size_t nnz);
 void csr_release(sk_csr* a);
+// Orders ctx's stream after an asynchronously built handle's copies (no-op
+// for every other handle).
+inline void csr_ready(sk_ctx* ctx, const sk_csr* a) {
+  if (ctx && a && a->ready) SK_CUDA(cudaStreamWaitEvent(ctx->stream, a->ready, 0));
+}
 
 // Reads and clears the context's device error word (synchronising).
 void check_device_error(sk_ctx* ctx, const char* op);

@@ -352,6 +352,25 @@ class CsrMatrix:
                                         float(value), int(validate), C.byref(h)))
         return CsrMatrix(rows, cols, ctx=c, _handle=h)
 
+    @staticmethod
+    def from_pattern_async(rows, cols, row_ptr, col_idx, value: float = 1.0, *, stream: int,
+                           ctx=None) -> "CsrMatrix":
+        """from_pattern (unvalidated) with the copies on `stream` (a cudaStream_t
+        handle, e.g. torch.cuda.Stream().cuda_stream): they overlap work already
+        queued on the context's stream, and every later use of the matrix is
+        ordered after them.  The host arrays are kept alive by the returned
+        matrix; page-locked arrays (host_register) make the copies asynchronous."""
+        c = _ctx(ctx)
+        rp, ci = _u32(row_ptr), _u32(col_idx)
+        if rp.size != rows + 1:
+            raise InvalidArgument("row_ptr length must be rows+1")
+        h = vp()
+        _check(c._L.sk_csr_from_pattern_async(c.h, rows, cols, rp.ctypes.data, ci.ctypes.data,
+                                              float(value), vp(stream), C.byref(h)))
+        m = CsrMatrix(rows, cols, ctx=c, _handle=h)
+        m._host_refs = (rp, ci)
+        return m
+
     def rows(self) -> int:
         return self._rows
 

@@ -139,6 +139,30 @@ def test_pattern_inputs_forward_like_explicit_values(sk, port, c):
     assert_csr_bitwise(ob, y, nan_payloads=np.isnan(c))
 
 
+def test_csr_from_pattern_async(sk, port):
+    # copies on another stream; every use is ordered after them (event on the
+    # handle): extract, a forward, and freeing a handle nobody used
+    import torch
+    cs = torch.cuda.Stream()
+    m, n, L = 4096, 2000, 2
+    Y = port.gen_input_binary(m, n, 40, 11)
+    a = sk.CsrMatrix.from_pattern_async(m, n, Y.row_ptr, Y.col_idx, 1.0, stream=cs.cuda_stream)
+    assert_csr_bitwise(a, Y)
+    hW = [port.gen_layer_fixed(m, 16, port.layer_seed(6, k), 1.0 / 8) for k in range(L)]
+    bias = np.full(m, -0.2, np.float32)
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], [bias] * L)
+    ya = sk.CsrMatrix.from_pattern_async(m, n, Y.row_ptr, Y.col_idx, 1.0, stream=cs.cuda_stream)
+    yb = sk.CsrMatrix.from_pattern(m, n, Y.row_ptr, Y.col_idx, 1.0)
+    oa, ta = sk.relu_forward_sparse(model, ya, sk.ForwardOptions(clip=4.0))
+    ob, tb = sk.relu_forward_sparse(model, yb, sk.ForwardOptions(clip=4.0))
+    assert list(ta) == list(tb)
+    assert_csr_bitwise(oa, host_csr(ob))
+    unused = sk.CsrMatrix.from_pattern_async(m, n, Y.row_ptr, Y.col_idx, 2.0,
+                                             stream=cs.cuda_stream)
+    del unused
+    torch.cuda.synchronize()
+
+
 def test_validating_constructor_messages(sk):
     kat = json.load(open(os.path.join(GOLDEN, "kat.json")))["validate_errors"]
     cases = {"not_monotone": (3, 2, [0, 1, 0, 1], [0], [1.0]),
