@@ -608,10 +608,12 @@ __device__ __forceinline__ uint32_t fx_clear_word(uint32_t P) {
   return P == 1 ? 0u : (P == 2 ? 0x80008000u : 0x80808080u);
 }
 
-constexpr uint32_t kPieceCap = 64;  // piece records per batch (the 128-word table area)
+// piece records per batch: 64 in the engine (its 128-word table area), 192 in the
+// standalone exact layer (one batch covers almost every accumulator pass)
+constexpr int kEngineRecCap = 64, kExactRecCap = 192;
 
 // kSh: compile-time log2 window (0 = runtime p.sh); kYC: Y is constant-valued
-template <bool kLayer, int kSh, bool kYC>
+template <bool kLayer, int kSh, bool kYC, int kCap>
 __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
                                    int lane) {
   const int sh = kSh ? kSh : p.sh;
@@ -636,8 +638,8 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
   const int thr_b = thr_i + int(fbias);
   uint32_t* const acc = ws.acc;
   // staging area (unused in exact mode): piece records + candidates
-  uint2* const rec = reinterpret_cast<uint2*>(ws.st_p);                // kPieceCap
-  uint32_t* const cand = reinterpret_cast<uint32_t*>(ws.st_p) + 128;  // P * SW words
+  uint2* const rec = reinterpret_cast<uint2*>(ws.st_p);                    // kCap
+  uint32_t* const cand = reinterpret_cast<uint32_t*>(ws.st_p) + 2 * kCap;  // P * SW words
   const uint32_t nchunks = p.b_empty ? 0u : (deg + 31) / 32;
   // first chunk's in-edges (kept for every accumulator pass)
   uint32_t k0 = 0;
@@ -674,14 +676,14 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
       // per-owner fixed-point increment of a constant-valued Y (exact integer)
       const int qown = kYC ? __float2int_rn(__fmul_rn(__fmul_rn(aa, p.y_cval), p.fx_scale)) : 0;
 #pragma unroll 1
-      for (uint32_t pb = 0; pb < ptot; pb += kPieceCap) {
-        const uint32_t lo = max(pex, pb), hi = min(pex + npc, pb + kPieceCap);
+      for (uint32_t pb = 0; pb < ptot; pb += kCap) {
+        const uint32_t lo = max(pex, pb), hi = min(pex + npc, pb + kCap);
         for (uint32_t t = lo; t < hi; ++t) {
           const uint32_t st = beg + 4 * (t - pex);
           rec[t - pb] = make_uint2(st, min(4u, beg + cnt - st) | (uint32_t(lane) << 3));
         }
         __syncwarp();
-        const uint32_t nb = min(kPieceCap, ptot - pb);
+        const uint32_t nb = min(uint32_t(kCap), ptot - pb);
 #pragma unroll 1
         for (uint32_t r0 = 0; r0 < nb; r0 += 32) {
           const uint32_t t = r0 + lane;
@@ -791,8 +793,9 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
 // Phase A over all items, window-group-major so the live slice of B stays in L2.
 // With a frontier (rows != nullptr) only the nrows listed output rows are
 // processed; every other row's items were zeroed by the caller.
-// kSh (exact path): compile-time log2 window, 0 = dispatch on p.sh
-template <typename Ops, bool kLayer, bool kExact, int kSh = 0>
+// kSh (exact path): compile-time log2 window, 0 = dispatch on p.sh; kCap: piece
+// records per batch (exact path)
+template <typename Ops, bool kLayer, bool kExact, int kSh = 0, int kCap = kEngineRecCap>
 __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
                                         uint64_t gw, uint64_t nwarps,
                                         const uint32_t* rows = nullptr, uint32_t nrows = 0) {
@@ -824,13 +827,13 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
         for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
         __syncwarp();
       } else if (kSh && p.y_const) {
-        process_item_exact<kLayer, kSh, true>(p, i, uint32_t(g), ws, lane);
+        process_item_exact<kLayer, kSh, true, kCap>(p, i, uint32_t(g), ws, lane);
       } else if (!kSh && p.sh == 10 && p.y_const) {
-        process_item_exact<kLayer, 10, true>(p, i, uint32_t(g), ws, lane);
+        process_item_exact<kLayer, 10, true, kCap>(p, i, uint32_t(g), ws, lane);
       } else if (p.y_const) {
-        process_item_exact<kLayer, 0, true>(p, i, uint32_t(g), ws, lane);
+        process_item_exact<kLayer, 0, true, kCap>(p, i, uint32_t(g), ws, lane);
       } else {
-        process_item_exact<kLayer, 0, false>(p, i, uint32_t(g), ws, lane);
+        process_item_exact<kLayer, 0, false, kCap>(p, i, uint32_t(g), ws, lane);
       }
     } else {
       process_item<Ops, kLayer, false>(p, i, uint32_t(g), ws, lane);
@@ -1010,21 +1013,21 @@ __host__ __device__ __forceinline__ void exact_params(const ValueStats& wst, con
 // ---- the exact layer as a standalone kernel ------------------------------------------
 // The persistent engine's register and shared-memory budget is set by the
 // ordered path (80 registers, 7.8 KB per warp: 24 warps per SM).  The exact
-// path needs only the accumulator, the touched bitmap of its dense-row fallback
-// and 1 KB of table/candidates, so as its own kernel it runs 32 warps per SM
-// (64 registers, 5.2 KB per warp); the gathered loads it waits on are hidden
-// by more warps.
-__host__ __device__ constexpr size_t exact_warp_bytes(uint32_t S) {
-  // accumulator | dense-row touched bitmap | in-edge table (128) + candidates (4 S/32)
-  return (size_t(S) + S / 32 + 128 + 4 * (S / 32)) * 4;
+// path needs only the accumulator, the touched bitmap of its dense-row fallback,
+// the piece records and the candidates, so as its own kernel it runs 32 warps
+// per SM (64 registers, 6.1 KB per warp); the gathered loads it waits on are
+// hidden by more warps.
+__host__ __device__ constexpr size_t exact_warp_bytes(uint32_t S, int cap) {
+  // accumulator | dense-row touched bitmap | piece records | candidates (4 S/32)
+  return (size_t(S) + S / 32 + 2 * size_t(cap) + 4 * (S / 32)) * 4;
 }
 
-template <int kSh>  // 0: runtime p.sh
+template <int kSh, int kCap>  // kSh 0: runtime p.sh
 __device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t S = kSh ? 1u << kSh : 1u << p.sh;
-  uint8_t* base = reinterpret_cast<uint8_t*>(sm) + size_t(wid) * exact_warp_bytes(S);
+  uint8_t* base = reinterpret_cast<uint8_t*>(sm) + size_t(wid) * exact_warp_bytes(S, kCap);
   WarpSmem ws;
   ws.acc = reinterpret_cast<uint32_t*>(base);
   ws.surv = ws.acc + S;
@@ -1034,20 +1037,24 @@ __device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   const uint32_t cw = fx_clear_word(p.fx_pack);
   for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
   for (uint32_t t = lane; t < S / 32; t += 32) ws.surv[t] = 0u;
-  for (uint32_t t = lane; t < 128 + 4 * (S / 32); t += 32)
+  for (uint32_t t = lane; t < 2 * kCap + 4 * (S / 32); t += 32)
     reinterpret_cast<uint32_t*>(ws.st_p)[t] = 0u;
   __syncwarp();
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  phase_a<OpArith, true, true, kSh>(p, ws, lane, gw, nw);
+  phase_a<OpArith, true, true, kSh, kCap>(p, ws, lane, gw, nw);
 }
 
+// kCap: piece records per batch -- 192 when an accumulator pass holds many
+// products (one batch), 64 otherwise (the smaller area leaves L1 to the
+// gathered loads of wide, thin layers)
+template <int kCap>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long long* stamp) {
   if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer();
   if (p.sh == 10)
-    exact_layer_body<10>(p);
+    exact_layer_body<10, kCap>(p);
   else
-    exact_layer_body<0>(p);
+    exact_layer_body<0, kCap>(p);
 }
 
 // ---- generic SpGEMM (mxm over any semiring): separate kernels -------------------------
@@ -1358,7 +1365,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
       const uint32_t cw = fx_clear_word(ra.fx_pack);
       for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
       for (uint32_t t = lane; t < ra.fx_pack * (S / 32); t += 32)
-        reinterpret_cast<uint32_t*>(ws.st_p)[128 + t] = 0u;
+        reinterpret_cast<uint32_t*>(ws.st_p)[2 * kEngineRecCap + t] = 0u;
       __syncwarp();
       phase_a<OpArith, true, true>(ra, ws, lane, gw, nwarps);
       for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = kSent;
@@ -1929,14 +1936,28 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
   const uint64_t full = uint64_t(m) * n;
   const sk_csr* w = md->w[k0];
   uint32_t* wp0 = build_wp(ctx, y0, g, true);
+  // products per accumulator pass (mean in-degree x mean input row x P*S/n)
+  // select the record capacity
+  RowArgs probe;
+  exact_params(md->wstats_host[k0], ystats, g.S, probe);
+  const double per_pass = double(w->nnz) / double(std::max<uint32_t>(1, m)) *
+                          double(y0->nnz) / double(std::max<uint32_t>(1, y0->rows)) *
+                          double(probe.fx_pack) * double(g.S) / double(std::max<uint32_t>(1, n));
+  const bool big = per_pass > 200.0;
   static bool attr = false;
-  const size_t smem = size_t(kWarps) * exact_warp_bytes(g.S);
   if (!attr) {
-    set_smem_attr(k_exact_layer);
+    set_smem_attr(k_exact_layer<kEngineRecCap>);
+    set_smem_attr(k_exact_layer<kExactRecCap>);
     attr = true;
   }
+  const size_t smem = size_t(kWarps) * exact_warp_bytes(g.S, big ? kExactRecCap : kEngineRecCap);
   int per_sm = 0;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exact_layer, kWarps * 32, smem));
+  if (big)
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exact_layer<kExactRecCap>,
+                                                          kWarps * 32, smem));
+  else
+    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exact_layer<kEngineRecCap>,
+                                                          kWarps * 32, smem));
   const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
   unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
   auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
@@ -1986,7 +2007,10 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     p.xgroup = env_group ? env_group : exact_group(m, g.nW, uint64_t(grid) * kWarps);
     long long* stamp = (ctx->stamps && k0 < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
     timing_mark(ctx);
-    SK_LAUNCH(k_exact_layer, grid, kWarps * 32, smem, ctx->stream, p, stamp);
+    if (big)
+      SK_LAUNCH(k_exact_layer<kExactRecCap>, grid, kWarps * 32, smem, ctx->stream, p, stamp);
+    else
+      SK_LAUNCH(k_exact_layer<kEngineRecCap>, grid, kWarps * 32, smem, ctx->stream, p, stamp);
     timing_mark(ctx);
     SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
     exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
