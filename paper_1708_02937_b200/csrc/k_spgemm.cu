@@ -142,6 +142,7 @@ struct RowArgs {
   int* err;
   float fx_scale, fx_unscale;  // exact mode: 2^-gran and 2^gran (fixed-point accumulation)
   uint32_t fx_pack;            // exact mode: windows per accumulator word (1, 2, 4)
+  uint32_t fx_off, fx_clearw;  // exact mode: field offset 2^(B-1)-1-thr and the cleared word
   int y_const;                 // exact mode: every B value is y_cval (no value loads)
   float y_cval;
   uint32_t xgroup;             // exact mode: windows per item (multiple of kGroup)
@@ -604,8 +605,9 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
 // position can only survive if its final sum is above thr = -b * 2^-gran, so
 // updates that leave the sum above thr mark a candidate bit; the epilogue walks
 // candidates only and the accumulator is reset with vector stores.
-__device__ __forceinline__ uint32_t fx_clear_word(uint32_t P) {
-  return P == 1 ? 0u : (P == 2 ? 0x80008000u : 0x80808080u);
+// top bit of every field of a word with P fields
+__host__ __device__ __forceinline__ uint32_t fx_top_bits(uint32_t P) {
+  return P == 1 ? 0x80000000u : (P == 2 ? 0x80008000u : 0x80808080u);
 }
 
 // piece records per batch: 64 in the engine (its 128-word table area), 192 in the
@@ -621,21 +623,19 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
   const uint32_t P = p.fx_pack;
   const uint32_t B = 32 / P;
   const uint32_t fmask = P == 1 ? 0xFFFFFFFFu : ((1u << B) - 1u);
-  const uint32_t fbias = P == 1 ? 0u : (1u << (B - 1));
-  const uint32_t clearw = fx_clear_word(P);
+  const uint32_t foff = p.fx_off;
+  const uint32_t topb = fx_top_bits(P);
+  const uint32_t clearw = p.fx_clearw;
   const uint32_t w0 = g * p.xgroup;
   const uint32_t wn = min(p.xgroup, p.nW - w0);
   const uint32_t eb = p.arp[i], ee = p.arp[i + 1];
   const uint32_t deg = ee - eb;
   const float b = kLayer ? p.bias[i] : 0.0f;
   const float thr = kLayer ? __fmul_rn(-b, p.fx_scale) : -INFINITY;
-  // a partial sum nv (an integer) is a candidate iff nv > thr iff nv > floor(thr);
-  // compared on the biased field: field > floor(thr) + fbias (NaN: never)
-  int thr_i;
-  if (!(thr == thr) || thr >= 1073741824.0f) thr_i = 1 << 30;
-  else if (thr < -1073741824.0f) thr_i = -(1 << 30);
-  else thr_i = int(floorf(thr));
-  const int thr_b = thr_i + int(fbias);
+  // Every field holds sum + foff, foff = 2^(B-1) - 1 - thr_min (exact_params):
+  // its top bit is set iff sum > thr_min, and thr_min <= floor(this row's thr),
+  // so an update that sets a top bit the old word did not have marks a
+  // candidate; the emit applies this row's own threshold.
   uint32_t* const acc = ws.acc;
   // staging area (unused in exact mode): piece records + candidates
   uint2* const rec = reinterpret_cast<uint2*>(ws.st_p);                    // kCap
@@ -708,7 +708,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
               const int q = kYC ? qo : __float2int_rn(__fmul_rn(__fmul_rn(ao, yy[u]), p.fx_scale));
               const uint32_t delta = uint32_t(q) << fs;
               const uint32_t old = atomicAdd(acc + wl, delta);
-              if (int(((old + delta) >> fs) & fmask) > thr_b)
+              if ((old + delta) & ~old & topb)
                 atomicOr(cand + sub * SW + (wl >> 5), 1u << (wl & 31));
             }
           }
@@ -747,7 +747,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
         while (t) {
           const uint32_t bt = __ffs(t) - 1;
           t &= t - 1;
-          const int ai = int((acc[q * 32 + bt] >> fs) & fmask) - int(fbias);
+          const int ai = int(((acc[q * 32 + bt] >> fs) & fmask) - foff);
           if (__int2float_rn(ai) > thr) {
             const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
             const float z = kLayer ? layer_epilogue(x, b, p.clip) : x;
@@ -770,7 +770,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
           const uint32_t bt = __ffs(t) - 1;
           t &= t - 1;
           if (can_write) {
-            const int ai = int((acc[q * 32 + bt] >> fs) & fmask) - int(fbias);
+            const int ai = int(((acc[q * 32 + bt] >> fs) & fmask) - foff);
             const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
             p.sc_c[pos] = swbase + q * 32 + bt;
             p.sc_v[pos] = kLayer ? layer_epilogue(x, b, p.clip) : x;
@@ -815,7 +815,7 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
       // dense sweep of the float exact path
       if (kLayer && layer_epilogue(0.0f, p.bias[i], p.clip) != 0.0f) {
         // the float exact path expects a zeroed accumulator
-        const uint32_t S = 1u << p.sh, cw = fx_clear_word(p.fx_pack);
+        const uint32_t S = 1u << p.sh, cw = p.fx_clearw;
         for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = 0u;
         __syncwarp();
         // the item's engine-sized groups
@@ -988,19 +988,31 @@ __host__ __device__ __forceinline__ bool products_exact(const ValueStats& w, con
   return gran >= -126 && gran <= 103 && exact_qbound(w, y) < 16777216.0;
 }
 
-// Fixed-point parameters of the exact path for operand statistics w, y.
+// Fixed-point parameters of the exact path for operand statistics w, y and a
+// threshold thr >= 0 no nonpositive-bias row's floor(-b_i 2^-gran) is below
+// (0 is always valid).  Fields (B bits, P = 32 / B per word) hold sum + foff,
+// foff = 2^(B-1) - 1 - thr' (thr' = min(thr, ceil(qb))), so a field's top bit
+// is set iff its sum > thr'.  The narrowest B whose fields hold every partial
+// sum (in [0, qb] when every product is >= 0, else [-qb, qb]) with no carry
+// across fields is chosen.
 __host__ __device__ __forceinline__ void exact_params(const ValueStats& wst, const ValueStats& yst,
-                                                     uint32_t S, RowArgs& ra) {
+                                                     uint32_t S, RowArgs& ra, double thr = 0.0) {
   const bool zero = wst.lowbit == INT_MAX || yst.lowbit == INT_MAX;
   const int gran = zero ? 0 : wst.lowbit + yst.lowbit;
   ra.fx_scale = pow2f(-gran);
   ra.fx_unscale = pow2f(gran);
-  // |partial sums| <= qb (integers): biased 8-bit fields hold [-127, 127], 16-bit
-  // fields [-32767, 32767]
   const double qb = zero ? 0.0 : exact_qbound(wst, yst);
-  uint32_t P = qb <= 127.0 ? 4u : (qb <= 32767.0 ? 2u : 1u);
+  const bool nonneg = wst.vmax < 0x80000000u && yst.vmax < 0x80000000u;
+  const double t = fmin(fmax(floor(thr), 0.0), ceil(qb));
+  const double smin = nonneg ? 0.0 : -qb;
+  uint32_t P = 1u;
+  if (127.0 - t + smin >= 0.0 && 127.0 - t + qb <= 255.0) P = 4u;
+  else if (32767.0 - t + smin >= 0.0 && 32767.0 - t + qb <= 65535.0) P = 2u;
   while (P > 1 && P * (S / 32) > 384) P >>= 1;             // candidate bitmaps live in st_p
+  const double c = P == 4 ? 127.0 - t : (P == 2 ? 32767.0 - t : 2147483647.0 - t);
   ra.fx_pack = P;
+  ra.fx_off = uint32_t(c);
+  ra.fx_clearw = P == 4 ? ra.fx_off * 0x01010101u : (P == 2 ? ra.fx_off * 0x00010001u : ra.fx_off);
   // binary (constant-valued) inputs: the value array need not be read
   ra.y_const = yst.vmin == yst.vmax;
   union {
@@ -1034,7 +1046,7 @@ __device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   ws.st_p = reinterpret_cast<float*>(ws.surv + S / 32);
   ws.list = nullptr;
   ws.st_s = nullptr;
-  const uint32_t cw = fx_clear_word(p.fx_pack);
+  const uint32_t cw = p.fx_clearw;
   for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
   for (uint32_t t = lane; t < S / 32; t += 32) ws.surv[t] = 0u;
   for (uint32_t t = lane; t < 2 * kCap + 4 * (S / 32); t += 32)
@@ -1291,6 +1303,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     ra.fx_scale = 1.0f;
     ra.fx_unscale = 1.0f;
     ra.fx_pack = 1;
+    ra.fx_off = 0x7FFFFFFFu;
+    ra.fx_clearw = 0x7FFFFFFFu;
     ra.xgroup = kGroup;
     ra.y_const = 0;
     ra.y_cval = 0.0f;
@@ -1362,7 +1376,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
       const uint32_t nrows = __ldcg(p.nfront + layer);
       phase_a<OpArith, true, false>(ra, ws, lane, gw, nwarps, p.frontier, nrows);
     } else if (exact) {
-      const uint32_t cw = fx_clear_word(ra.fx_pack);
+      const uint32_t cw = ra.fx_clearw;
       for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
       for (uint32_t t = lane; t < ra.fx_pack * (S / 32); t += 32)
         reinterpret_cast<uint32_t*>(ws.st_p)[2 * kEngineRecCap + t] = 0u;
@@ -1625,6 +1639,8 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   p.fx_scale = 1.0f;
   p.fx_unscale = 1.0f;
   p.fx_pack = 1;
+  p.fx_off = 0x7FFFFFFFu;
+  p.fx_clearw = 0x7FFFFFFFu;
   p.y_const = 0;
   p.y_cval = 0.0f;
   const size_t smem = block_smem(g);
@@ -1938,8 +1954,13 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
   uint32_t* wp0 = build_wp(ctx, y0, g, true);
   // products per accumulator pass (mean in-degree x mean input row x P*S/n)
   // select the record capacity
+  // candidate threshold: the smallest floor(-b_i 2^-gran) over the rows whose
+  // untouched positions vanish (b_i <= 0); the other rows take the dense sweep
   RowArgs probe;
   exact_params(md->wstats_host[k0], ystats, g.S, probe);
+  const double negmin = md->bias_negmin[k0];
+  const double thr = std::isfinite(negmin) ? negmin * double(probe.fx_scale) : 0.0;
+  exact_params(md->wstats_host[k0], ystats, g.S, probe, thr);
   const double per_pass = double(w->nnz) / double(std::max<uint32_t>(1, m)) *
                           double(y0->nnz) / double(std::max<uint32_t>(1, y0->rows)) *
                           double(probe.fx_pack) * double(g.S) / double(std::max<uint32_t>(1, n));
@@ -1998,7 +2019,7 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     p.cap = cap;
     p.overflow = reinterpret_cast<int*>(d + 1);
     p.err = ctx->d_err;
-    exact_params(md->wstats_host[k0], ystats, g.S, p);
+    exact_params(md->wstats_host[k0], ystats, g.S, p, thr);
     static const uint32_t env_group = [] {  // SK_EXACT_GROUP=4|8|16 (A/B measurements)
       const char* e = getenv("SK_EXACT_GROUP");
       const int v = e ? atoi(e) : 0;

@@ -454,14 +454,21 @@ extern "C" sk_status sk_model_create(sk_ctx* ctx, uint32_t layers,
     md->neurons = m;
     md->bias_host.resize(size_t(layers) * m);
     md->bias_nonpos.resize(layers);
+    md->bias_negmin.resize(layers);
     for (uint32_t k = 0; k < layers; ++k) {
       auto* w = const_cast<sk_csr*>(weights[k]);
       w->refs.fetch_add(1);
       md->w.push_back(w);
       std::memcpy(md->bias_host.data() + size_t(k) * m, biases[k], size_t(m) * 4);
       bool nonpos = true;
-      for (uint32_t i = 0; i < m; ++i) nonpos &= (biases[k][i] <= 0.0f);
+      double negmin = INFINITY;
+      for (uint32_t i = 0; i < m; ++i) {
+        const float bi = biases[k][i];
+        nonpos &= (bi <= 0.0f);
+        if (bi <= 0.0f) negmin = std::min(negmin, -double(bi));
+      }
       md->bias_nonpos[k] = nonpos;
+      md->bias_negmin[k] = negmin;
     }
     md->bias = dalloc<float>(ctx, md->bias_host.size());
     SK_CUDA(cudaMemcpyAsync(md->bias, md->bias_host.data(), md->bias_host.size() * 4,

@@ -174,6 +174,7 @@ struct sk_model {
   float* bias = nullptr;        // device, layers*neurons
   std::vector<float> bias_host; // layers*neurons
   std::vector<uint8_t> bias_nonpos;  // per layer: every b <= 0 (no NaN)
+  std::vector<double> bias_negmin;   // per layer: min of -b_i over b_i <= 0 (inf: none)
   const void** d_wptr = nullptr;     // device [rp[L], ci[L], v[L]] for the engine
   void* d_wstats = nullptr;          // device per-layer value statistics (exactness test)
   uint8_t* d_bias_nonpos = nullptr;
