@@ -145,6 +145,8 @@ struct RowArgs {
   uint32_t fx_off, fx_clearw;  // exact mode: field offset 2^(B-1)-1-thr and the cleared word
   int y_const;                 // exact mode: every B value is y_cval (no value loads)
   float y_cval;
+  int q_const;                 // exact mode: constant A and B values: every product is q_cval
+  int q_cval;
   uint32_t xgroup;             // exact mode: windows per item (multiple of kGroup)
 };
 
@@ -549,6 +551,7 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
     const uint32_t wbase = w << p.sh;
     uint32_t T = 0;
     bool any = false;
+    uint32_t cflag = 0;  // windows (sub) in which this lane marked a candidate
 #pragma unroll 1
     for (uint32_t c = 0; c < nchunks; ++c) {
       const uint32_t e = eb + 32 * c + lane;
@@ -615,7 +618,7 @@ __host__ __device__ __forceinline__ uint32_t fx_top_bits(uint32_t P) {
 constexpr int kEngineRecCap = 64, kExactRecCap = 192;
 
 // kSh: compile-time log2 window (0 = runtime p.sh); kYC: Y is constant-valued
-template <bool kLayer, int kSh, bool kYC, int kCap>
+template <bool kLayer, int kSh, bool kYC, int kCap, bool kQC = false>
 __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
                                    int lane) {
   const int sh = kSh ? kSh : p.sh;
@@ -653,6 +656,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
     const uint32_t np = min(P, wn - gw);  // windows sharing this accumulator
     const uint32_t wbase = (w0 + gw) << sh;
     bool any = false;
+    uint32_t cflag = 0;  // windows (sub) in which this lane marked a candidate
 #pragma unroll 1
     for (uint32_t c = 0; c < nchunks; ++c) {
       uint32_t beg = 0, cnt = 0;
@@ -689,7 +693,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
           const uint32_t t = r0 + lane;
           const uint2 rc = t < nb ? rec[t] : make_uint2(0u, 0u);
           const uint32_t len = rc.y & 7u, own = rc.y >> 3;
-          const int qo = __shfl_sync(0xffffffffu, qown, own);
+          const int qo = kQC ? p.q_cval : __shfl_sync(0xffffffffu, qown, own);
           const float ao = kYC ? 0.0f : __shfl_sync(0xffffffffu, aa, own);
           uint32_t cc[4];
           float yy[4];
@@ -708,8 +712,10 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
               const int q = kYC ? qo : __float2int_rn(__fmul_rn(__fmul_rn(ao, yy[u]), p.fx_scale));
               const uint32_t delta = uint32_t(q) << fs;
               const uint32_t old = atomicAdd(acc + wl, delta);
-              if ((old + delta) & ~old & topb)
+              if ((old + delta) & ~old & topb) {
                 atomicOr(cand + sub * SW + (wl >> 5), 1u << (wl & 31));
+                cflag |= 1u << sub;
+              }
             }
           }
         }
@@ -720,13 +726,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
     // ---- emit each window of the accumulator ---------------------------------------
     // windows holding candidates (candidate bits exist only below n); the others
     // have no output and their counts are written at once
-    uint32_t cmask = 0;
-    if (any)
-      for (uint32_t sub = 0; sub < np; ++sub) {
-        uint32_t anyc = 0;
-        for (uint32_t q = lane; q < SW; q += 32) anyc |= cand[sub * SW + q];
-        if (__any_sync(0xffffffffu, anyc != 0)) cmask |= 1u << sub;
-      }
+    uint32_t cmask = __reduce_or_sync(0xffffffffu, cflag);
     if (uint32_t(lane) < np && !((cmask >> lane) & 1u))
       p.item_cnt[uint64_t(i) * p.nW + w0 + gw + lane] = 0;
 #pragma unroll 1
@@ -826,6 +826,8 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
         }
         for (uint32_t t = lane; t < S; t += 32) ws.acc[t] = cw;
         __syncwarp();
+      } else if (kSh && p.q_const) {
+        process_item_exact<kLayer, kSh, true, kCap, true>(p, i, uint32_t(g), ws, lane);
       } else if (kSh && p.y_const) {
         process_item_exact<kLayer, kSh, true, kCap>(p, i, uint32_t(g), ws, lane);
       } else if (!kSh && p.sh == 10 && p.y_const) {
@@ -1020,6 +1022,12 @@ __host__ __device__ __forceinline__ void exact_params(const ValueStats& wst, con
     float f;
   } cv{yst.vmin};
   ra.y_cval = cv.f;
+  ra.q_const = ra.y_const && wst.vmin == wst.vmax;
+  union {
+    uint32_t u;
+    float f;
+  } cw{wst.vmin};
+  ra.q_cval = int(llrint(double(cw.f) * double(cv.f) * double(ra.fx_scale)));
 }
 
 // ---- the exact layer as a standalone kernel ------------------------------------------
@@ -1308,6 +1316,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     ra.xgroup = kGroup;
     ra.y_const = 0;
     ra.y_cval = 0.0f;
+    ra.q_const = 0;
+    ra.q_cval = 0;
 
     // ---- phase A: rows ---------------------------------------------------------------
     // Layer 0's operand statistics are known: if every partial sum is exact, the
@@ -1643,6 +1653,8 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   p.fx_clearw = 0x7FFFFFFFu;
   p.y_const = 0;
   p.y_cval = 0.0f;
+  p.q_const = 0;
+  p.q_cval = 0;
   const size_t smem = block_smem(g);
   if (d_bias) {
     timing_mark(ctx);  // the dominant kernel of a sparse layer (column-sharded forward)
