@@ -143,6 +143,11 @@ struct RowArgs {
   float fx_scale, fx_unscale;  // exact mode: 2^-gran and 2^gran (fixed-point accumulation)
   uint32_t fx_pack;            // exact mode: windows per accumulator word (1, 2, 4)
   uint32_t fx_off, fx_clearw;  // exact mode: field offset 2^(B-1)-1-thr and the cleared word
+  // exact mode: coarse window table (one entry per accumulator pass of 2^wpc_lp
+  // windows, row stride nWc), or null to use wp
+  const uint32_t* wpc;
+  uint32_t nWc;
+  int wpc_lp;
   int y_const;                 // exact mode: every B value is y_cval (no value loads)
   float y_cval;
   int q_const;                 // exact mode: constant A and B values: every product is q_cval
@@ -665,9 +670,15 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
       if (e < ee) {
         const uint32_t kk = c == 0 ? k0 : p.aci[e];
         aa = c == 0 ? a0 : p.av[e];
-        const uint32_t* wk = p.wp + size_t(kk) * p.nW + w0 + gw;
-        beg = wk[0];
-        cnt = wk[np] - beg;
+        if (p.wpc) {  // one entry per pass: two adjacent words
+          const uint32_t* wk = p.wpc + size_t(kk) * p.nWc + ((w0 + gw) >> p.wpc_lp);
+          beg = wk[0];
+          cnt = wk[1] - beg;
+        } else {
+          const uint32_t* wk = p.wp + size_t(kk) * p.nW + w0 + gw;
+          beg = wk[0];
+          cnt = wk[np] - beg;
+        }
       }
       if (!__any_sync(0xffffffffu, cnt != 0)) continue;
       any = true;
@@ -1313,6 +1324,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_sparse_engine(EngineArgs p) 
     ra.fx_pack = 1;
     ra.fx_off = 0x7FFFFFFFu;
     ra.fx_clearw = 0x7FFFFFFFu;
+    ra.wpc = nullptr;
+    ra.nWc = 0;
+    ra.wpc_lp = 0;
     ra.xgroup = kGroup;
     ra.y_const = 0;
     ra.y_cval = 0.0f;
@@ -1651,6 +1665,9 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   p.fx_pack = 1;
   p.fx_off = 0x7FFFFFFFu;
   p.fx_clearw = 0x7FFFFFFFu;
+  p.wpc = nullptr;
+  p.nWc = 0;
+  p.wpc_lp = 0;
   p.y_const = 0;
   p.y_cval = 0.0f;
   p.q_const = 0;
@@ -1963,7 +1980,6 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
   const uint64_t items = uint64_t(m) * g.nW;
   const uint64_t full = uint64_t(m) * n;
   const sk_csr* w = md->w[k0];
-  uint32_t* wp0 = build_wp(ctx, y0, g, true);
   // products per accumulator pass (mean in-degree x mean input row x P*S/n)
   // select the record capacity
   // candidate threshold: the smallest floor(-b_i 2^-gran) over the rows whose
@@ -1973,6 +1989,18 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
   const double negmin = md->bias_negmin[k0];
   const double thr = std::isfinite(negmin) ? negmin * double(probe.fx_scale) : 0.0;
   exact_params(md->wstats_host[k0], ystats, g.S, probe, thr);
+  // Input window table.  With every bias <= 0 no row takes the dense sweep, and
+  // the order-free kernel only needs one entry per accumulator pass (P windows):
+  // a table P times smaller, two adjacent words per in-edge and pass.
+  const bool coarse = md->bias_nonpos[k0] != 0;
+  int plp = 0;
+  while ((1u << plp) < probe.fx_pack) ++plp;
+  WinGeom gc = g;
+  gc.sh = g.sh + plp;
+  gc.S = g.S << plp;
+  gc.nW = std::max<uint32_t>(1, uint32_t((uint64_t(n) + gc.S - 1) >> gc.sh));
+  uint32_t* wp0 = coarse ? nullptr : build_wp(ctx, y0, g, true);
+  uint32_t* wpc = coarse ? build_wp(ctx, y0, gc, true) : nullptr;
   const double per_pass = double(w->nnz) / double(std::max<uint32_t>(1, m)) *
                           double(y0->nnz) / double(std::max<uint32_t>(1, y0->rows)) *
                           double(probe.fx_pack) * double(g.S) / double(std::max<uint32_t>(1, n));
@@ -2032,6 +2060,9 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     p.overflow = reinterpret_cast<int*>(d + 1);
     p.err = ctx->d_err;
     exact_params(md->wstats_host[k0], ystats, g.S, p, thr);
+    p.wpc = wpc;
+    p.nWc = gc.nW;
+    p.wpc_lp = plp;
     static const uint32_t env_group = [] {  // SK_EXACT_GROUP=4|8|16 (A/B measurements)
       const char* e = getenv("SK_EXACT_GROUP");
       const int v = e ? atoi(e) : 0;
