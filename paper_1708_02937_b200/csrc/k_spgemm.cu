@@ -77,10 +77,10 @@ constexpr uint32_t kGroup = 4;    // windows per work item
 // Windows per exact-path item: an item's in-edge loads and window-table sectors
 // are shared by its xgroup / P accumulator passes, so larger items cut the L2
 // traffic of wide layers (cfg5: 16 windows instead of 4 took 5.1 -> 4.1 ms);
-// the largest of 16 / 8 / 4 that still leaves >= 16 items per warp.
+// the largest of 64 / 32 / 16 / 8 / 4 that still leaves >= 16 items per warp.
 __host__ __device__ __forceinline__ uint32_t exact_group(uint32_t m, uint32_t nW,
                                                          uint64_t warps) {
-  for (uint32_t G = 16; G > kGroup; G >>= 1)
+  for (uint32_t G = 64; G > kGroup; G >>= 1)
     if (uint64_t(m) * ((nW + G - 1) / G) >= 16 * warps) return G;
   return kGroup;
 }
@@ -2063,10 +2063,10 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     p.wpc = wpc;
     p.nWc = gc.nW;
     p.wpc_lp = plp;
-    static const uint32_t env_group = [] {  // SK_EXACT_GROUP=4|8|16 (A/B measurements)
+    static const uint32_t env_group = [] {  // SK_EXACT_GROUP=4|8|16|32|64 (A/B measurements)
       const char* e = getenv("SK_EXACT_GROUP");
       const int v = e ? atoi(e) : 0;
-      return (v == 4 || v == 8 || v == 16) ? uint32_t(v) : 0u;
+      return (v == 4 || v == 8 || v == 16 || v == 32 || v == 64) ? uint32_t(v) : 0u;
     }();
     p.xgroup = env_group ? env_group : exact_group(m, g.nW, uint64_t(grid) * kWarps);
     long long* stamp = (ctx->stamps && k0 < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
