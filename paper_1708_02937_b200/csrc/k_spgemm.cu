@@ -663,13 +663,12 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
     bool any = false;
     uint32_t cflag = 0;  // windows (sub) in which this lane marked a candidate
 #pragma unroll 1
-    for (uint32_t c = 0; c < nchunks; ++c) {
-      uint32_t beg = 0, cnt = 0;
-      float aa = 0.0f;
-      const uint32_t e = eb + 32 * c + lane;
-      if (e < ee) {
-        const uint32_t kk = c == 0 ? k0 : p.aci[e];
-        aa = c == 0 ? a0 : p.av[e];
+    // (a constant increment needs no owner: on sparse passes two chunks of
+    // in-edges share one record batch, so rows with 33-64 in-edges fill their
+    // rounds; dense passes keep one chunk per batch)
+    constexpr bool kPair = kQC && kCap == kEngineRecCap;
+    for (uint32_t c = 0; c < nchunks; c += kPair ? 2 : 1) {
+      auto slice = [&](uint32_t kk, uint32_t& beg, uint32_t& cnt) {
         if (p.wpc) {  // one entry per pass: two adjacent words
           const uint32_t* wk = p.wpc + size_t(kk) * p.nWc + ((w0 + gw) >> p.wpc_lp);
           beg = wk[0];
@@ -679,12 +678,22 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
           beg = wk[0];
           cnt = wk[np] - beg;
         }
+      };
+      uint32_t beg = 0, cnt = 0, beg2 = 0, cnt2 = 0;
+      float aa = 0.0f;
+      const uint32_t e = eb + 32 * c + lane;
+      if (e < ee) {
+        const uint32_t kk = c == 0 ? k0 : p.aci[e];
+        aa = c == 0 ? a0 : p.av[e];
+        slice(kk, beg, cnt);
       }
-      if (!__any_sync(0xffffffffu, cnt != 0)) continue;
+      if (kPair && e + 32 < ee) slice(p.aci[e + 32], beg2, cnt2);
+      if (!__any_sync(0xffffffffu, (cnt | cnt2) != 0)) continue;
       any = true;
       // this lane's slice as pieces of <= 4 consecutive products; a piece record
       // (start, len | owner << 3) per lane and round replaces any owner search
-      const uint32_t npc = (cnt + 3) >> 2;
+      const uint32_t npc1 = (cnt + 3) >> 2;
+      const uint32_t npc = npc1 + (kPair ? (cnt2 + 3) >> 2 : 0u);
       const uint32_t pincl = warp_incl_scan(npc, lane);
       const uint32_t ptot = __shfl_sync(0xffffffffu, pincl, 31);
       const uint32_t pex = pincl - npc;
@@ -694,8 +703,10 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
       for (uint32_t pb = 0; pb < ptot; pb += kCap) {
         const uint32_t lo = max(pex, pb), hi = min(pex + npc, pb + kCap);
         for (uint32_t t = lo; t < hi; ++t) {
-          const uint32_t st = beg + 4 * (t - pex);
-          rec[t - pb] = make_uint2(st, min(4u, beg + cnt - st) | (uint32_t(lane) << 3));
+          const bool first = !kPair || t - pex < npc1;
+          const uint32_t sb = first ? beg : beg2, se = first ? beg + cnt : beg2 + cnt2;
+          const uint32_t st = sb + 4 * (first ? t - pex : t - pex - npc1);
+          rec[t - pb] = make_uint2(st, min(4u, se - st) | (uint32_t(lane) << 3));
         }
         __syncwarp();
         const uint32_t nb = min(uint32_t(kCap), ptot - pb);
