@@ -84,10 +84,10 @@ static unsigned grid_for(sk_ctx* ctx, size_t n, unsigned block = 256) {
 }
 
 static uint64_t read_u64(sk_ctx* ctx, const void* d) {
-  uint64_t h = 0;
-  SK_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  // through the context's pinned mirror (a pageable copy is a staged, blocking one)
+  SK_CUDA(cudaMemcpyAsync(ctx->h_u64 + 2, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
-  return h;
+  return ctx->h_u64[2];
 }
 
 static void set_u64(sk_ctx* ctx, void* d, uint64_t v) {

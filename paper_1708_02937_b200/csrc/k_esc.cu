@@ -254,9 +254,10 @@ sk_csr* esc_small(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* b
   SK_LAUNCH(k_esc_small<K>, 1, kSmallThreads, 0, ctx->stream, erow, y->ci, y->v,
             uint32_t(y->nnz), n, wt->rp, wt->ci, wt->v, bias, clip, bits_for(uint64_t(m) * n),
             okey, ov, cnt);
-  uint32_t S = 0;
-  SK_CUDA(cudaMemcpyAsync(&S, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: an async copy
+  SK_CUDA(cudaMemcpyAsync(hp, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
+  const uint32_t S = hp[0];
   sk_csr* out = new_csr(ctx, m, n, S);
   if (S) {
     SK_CUDA(cudaMemcpyAsync(out->v, ov, size_t(S) * 4, cudaMemcpyDeviceToDevice, ctx->stream));

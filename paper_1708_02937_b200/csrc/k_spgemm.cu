@@ -1693,11 +1693,12 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   }
   SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
   exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
-  uint32_t nnz = 0;
-  int ovf = 0;
-  SK_CUDA(cudaMemcpyAsync(&nnz, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  SK_CUDA(cudaMemcpyAsync(&ovf, overflow, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
+  SK_CUDA(cudaMemcpyAsync(hp, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  SK_CUDA(cudaMemcpyAsync(hp + 1, overflow, 4, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
+  const uint32_t nnz = hp[0];
+  const int ovf = int(hp[1]);
   if (ovf) fail(SK_ERR_INVALID_ARGUMENT, "mxm scratch capacity exceeded");
   sk_csr* o = new_csr(ctx, m, n, nnz);
   SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, item_cnt, item_off,
@@ -1948,16 +1949,18 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
 // Value statistics of a CSR's values, on the host (one small launch + sync).
 static ValueStats host_value_stats(sk_ctx* ctx, const sk_csr* y) {
   if (y->stats_valid) return y->stats;
-  ValueStats* d = dalloc<ValueStats>(ctx, 1);
+  // through the context's pinned mirror: asynchronous copies, one sync
+  ValueStats* d = reinterpret_cast<ValueStats*>(ctx->d_u64 + 8);
+  ValueStats* hp = reinterpret_cast<ValueStats*>(ctx->h_u64 + 8);
   const ValueStats init SK_VALUESTATS_INIT;
-  SK_CUDA(cudaMemcpyAsync(d, &init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+  *hp = init;
+  SK_CUDA(cudaMemcpyAsync(d, hp, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
   if (y->nnz)
     SK_LAUNCH(k_value_stats, grid_warps(ctx, y->nnz / 128 + 1), 256, 0, ctx->stream, y->v,
               y->nnz, d);
-  ValueStats h;
-  SK_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  SK_CUDA(cudaMemcpyAsync(hp, d, sizeof(ValueStats), cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
-  dfree(ctx, d);
+  const ValueStats h = *hp;
   auto* yy = const_cast<sk_csr*>(y);
   yy->stats = h;
   yy->stats_valid = true;
@@ -2089,11 +2092,12 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     timing_mark(ctx);
     SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
     exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
-    uint32_t nnz = 0;
-    int ovf = 0;
-    SK_CUDA(cudaMemcpyAsync(&nnz, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    SK_CUDA(cudaMemcpyAsync(&ovf, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
+    SK_CUDA(cudaMemcpyAsync(hp, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SK_CUDA(cudaMemcpyAsync(hp + 1, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
+    const uint32_t nnz = hp[0];
+    const int ovf = int(hp[1]);
     if (!ovf) {
       // the layer's output, right-sized (an owned CSR: the caller releases it)
       sk_csr* o = new_csr(ctx, m, n, nnz);
@@ -2177,7 +2181,10 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
       if (!(hi && k < L && cur->nnz > hi)) {
         // a layer whose partial sums are provably exact runs as its own kernel
         // (k_exact_layer, higher occupancy); the engine continues after it
-        if (exact_env && k < L && cur->nnz) {
+        // a thin input goes to expand-sort-compress without the statistics round trip
+        const bool esc_ok =
+            esc_env && k < L && cur->nnz && esc_applicable(ctx, md, k, cur, esc_ratio);
+        if (exact_env && k < L && cur->nnz && !esc_ok) {
           const ValueStats ys = host_value_stats(ctx, cur);
           if (products_exact(md->wstats_host[k], ys)) {
             uint32_t* wp1 = nullptr;
@@ -2209,7 +2216,7 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
           if (k >= L) break;
           continue;
         }
-        if (esc_env && k < L && esc_applicable(ctx, md, k, cur, esc_ratio)) {
+        if (esc_ok) {
           sk_csr* r = esc_layer(ctx, md, cur, k, clip);
           if (owned) csr_release(owned);
           owned = r;
