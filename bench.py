@@ -445,6 +445,8 @@ def run_ours(args, w):
     # ---- timed region: resident inputs ----------------------------------------------
     ctx.set_timing(True)
     launches0 = sk._lib.launches()
+    if rank == 0:  # where a launch list (ncu -s) of the timed region starts
+        print(f"bench: {launches0} library launches before the timed region", file=sys.stderr)
     with sampler as clocks:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
