@@ -1711,8 +1711,60 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
   return spgemm_impl(ctx, a, b, s, nullptr, 0.0f, 0);
 }
 
+// One layer on the order-free path for a weight block w (rows = output neurons,
+// possibly a row block of a layer), its device bias, its statistics and the
+// bias summary (nonpos: every b <= 0; negmin: min of -b_i over b_i <= 0).
+struct ExactLayerIn {
+  const sk_csr* w;
+  const float* bias;  // device, w->rows
+  ValueStats wstats;
+  bool nonpos;
+  double negmin;
+  uint32_t stamp_layer;  // %globaltimer slot (ctx->stamps)
+};
+
+// Weight statistics of a bare CSR (value statistics + row bounds), cached on the
+// immutable handle (separately from its statistics as an activation).
+static ValueStats weight_stats(sk_ctx* ctx, const sk_csr* w);
+static ValueStats host_value_stats(sk_ctx* ctx, const sk_csr* y);
+static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* y0,
+                             float clip, const ValueStats& ystats, uint32_t** wp_out_ptr);
+
+// One layer for a weight block (sk_sparse_layer: a row block of W_ref under
+// column sharding).  An empty input with no surviving untouched position gives
+// an empty output; provably exact partial sums take the order-free kernel;
+// everything else the windowed SpGEMM + epilogue.  All three are the ascending
+// fold of the reference bit for bit.
 sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const sk_csr* y,
-                          float clip, uint64_t dense_rows) {
+                          float clip, uint64_t dense_rows, double negmin) {
+  if (y->nnz == 0 && dense_rows == 0) {
+    sk_csr* o = new_csr(ctx, w->rows, y->cols, 0);
+    SK_CUDA(cudaMemsetAsync(o->rp, 0, (size_t(w->rows) + 1) * 4, ctx->stream));
+    return o;
+  }
+  if (!getenv("SK_NO_EXACT") && y->nnz && w->rows && y->cols) {
+    const ValueStats ws = weight_stats(ctx, w);
+    const ValueStats ys = host_value_stats(ctx, y);
+    if (products_exact(ws, ys)) {
+      ExactLayerIn in;
+      in.w = w;
+      in.bias = d_bias;
+      in.wstats = ws;
+      in.nonpos = dense_rows == 0;
+      in.negmin = negmin;
+      in.stamp_layer = 0;
+      arena_begin(ctx);
+      try {
+        uint32_t* wp = nullptr;
+        sk_csr* o = exact_layer_w(ctx, in, y, clip, ys, &wp);
+        arena_end(ctx);
+        return o;
+      } catch (...) {
+        arena_end(ctx);
+        throw;
+      }
+    }
+  }
   return spgemm_impl(ctx, w, y, SK_ARITHMETIC, d_bias, clip, dense_rows);
 }
 
@@ -1967,6 +2019,27 @@ static ValueStats host_value_stats(sk_ctx* ctx, const sk_csr* y) {
   return h;
 }
 
+static ValueStats weight_stats(sk_ctx* ctx, const sk_csr* w) {
+  if (w->wstats_valid) return w->wstats;
+  ValueStats* d = reinterpret_cast<ValueStats*>(ctx->d_u64 + 8);
+  ValueStats* hp = reinterpret_cast<ValueStats*>(ctx->h_u64 + 8);
+  const ValueStats init SK_VALUESTATS_INIT;
+  *hp = init;
+  SK_CUDA(cudaMemcpyAsync(d, hp, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+  if (w->nnz)
+    SK_LAUNCH(k_value_stats, grid_warps(ctx, w->nnz / 32 + 1), 256, 0, ctx->stream, w->v, w->nnz,
+              d);
+  if (w->rows)
+    SK_LAUNCH(k_row_bounds, grid_warps(ctx, w->rows), 256, 0, ctx->stream, w->rp, w->v, w->rows,
+              d);
+  SK_CUDA(cudaMemcpyAsync(hp, d, sizeof(ValueStats), cudaMemcpyDeviceToHost, ctx->stream));
+  sync(ctx);
+  auto* ww = const_cast<sk_csr*>(w);
+  ww->wstats = *hp;
+  ww->wstats_valid = true;
+  return ww->wstats;
+}
+
 // Layer k0 on the order-free path as a standalone kernel (k_exact_layer), then
 // the count scan and the gather: the output CSR and its window table (for the
 // engine that continues from layer k0 + 1).
@@ -1986,27 +2059,43 @@ static WinGeom exact_geometry(uint32_t n) {
   return g;
 }
 
+static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* y0, float clip,
+                             const ValueStats& ystats, uint32_t** wp_out_ptr);
+
 static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, uint32_t k0,
                            float clip, const ValueStats& ystats, uint32_t** wp_out_ptr) {
-  const uint32_t m = md->neurons, n = y0->cols;
+  ExactLayerIn in;
+  in.w = md->w[k0];
+  in.bias = md->bias + size_t(k0) * md->neurons;
+  in.wstats = md->wstats_host[k0];
+  in.nonpos = md->bias_nonpos[k0] != 0;
+  in.negmin = md->bias_negmin[k0];
+  in.stamp_layer = k0;
+  return exact_layer_w(ctx, in, y0, clip, ystats, wp_out_ptr);
+}
+
+static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* y0, float clip,
+                             const ValueStats& ystats, uint32_t** wp_out_ptr) {
+  const sk_csr* w = L_.w;
+  const uint32_t m = w->rows, n = y0->cols;
+  const uint32_t k0 = L_.stamp_layer;
   const WinGeom g = exact_geometry(n);
   const bool same_geometry = g.sh == geometry(n).sh;
   const uint64_t items = uint64_t(m) * g.nW;
   const uint64_t full = uint64_t(m) * n;
-  const sk_csr* w = md->w[k0];
   // products per accumulator pass (mean in-degree x mean input row x P*S/n)
   // select the record capacity
   // candidate threshold: the smallest floor(-b_i 2^-gran) over the rows whose
   // untouched positions vanish (b_i <= 0); the other rows take the dense sweep
   RowArgs probe;
-  exact_params(md->wstats_host[k0], ystats, g.S, probe);
-  const double negmin = md->bias_negmin[k0];
+  exact_params(L_.wstats, ystats, g.S, probe);
+  const double negmin = L_.negmin;
   const double thr = std::isfinite(negmin) ? negmin * double(probe.fx_scale) : 0.0;
-  exact_params(md->wstats_host[k0], ystats, g.S, probe, thr);
+  exact_params(L_.wstats, ystats, g.S, probe, thr);
   // Input window table.  With every bias <= 0 no row takes the dense sweep, and
   // the order-free kernel only needs one entry per accumulator pass (P windows):
   // a table P times smaller, two adjacent words per in-edge and pass.
-  const bool coarse = md->bias_nonpos[k0] != 0;
+  const bool coarse = L_.nonpos;
   int plp = 0;
   while ((1u << plp) < probe.fx_pack) ++plp;
   WinGeom gc = g;
@@ -2063,7 +2152,7 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     p.n = n;
     p.nW = g.nW;
     p.sh = g.sh;
-    p.bias = md->bias + size_t(k0) * m;
+    p.bias = L_.bias;
     p.clip = clip;
     p.item_cnt = item_cnt;
     p.item_off = item_off;
@@ -2073,7 +2162,7 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
     p.cap = cap;
     p.overflow = reinterpret_cast<int*>(d + 1);
     p.err = ctx->d_err;
-    exact_params(md->wstats_host[k0], ystats, g.S, p, thr);
+    exact_params(L_.wstats, ystats, g.S, p, thr);
     p.wpc = wpc;
     p.nWc = gc.nW;
     p.wpc_lp = plp;

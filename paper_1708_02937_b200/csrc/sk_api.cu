@@ -610,8 +610,12 @@ extern "C" sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* 
     float* db = dalloc<float>(ctx, w->rows);
     SK_CUDA(cudaMemcpyAsync(db, bias, size_t(w->rows) * 4, cudaMemcpyHostToDevice, ctx->stream));
     uint64_t dense_rows = 0;  // rows whose untouched positions survive: 0 + b_i > 0 or NaN
-    for (uint32_t i = 0; i < w->rows; ++i) dense_rows += !(bias[i] <= 0.0f);
-    sk_csr* o = sparse_layer_impl(ctx, w, db, y, clip, dense_rows);
+    double negmin = INFINITY;  // min of -b_i over b_i <= 0 (the order-free path's threshold)
+    for (uint32_t i = 0; i < w->rows; ++i) {
+      dense_rows += !(bias[i] <= 0.0f);
+      if (bias[i] <= 0.0f) negmin = std::min(negmin, -double(bias[i]));
+    }
+    sk_csr* o = sparse_layer_impl(ctx, w, db, y, clip, dense_rows, negmin);
     dfree(ctx, db);
     sync(ctx);
     *out = o;

@@ -160,6 +160,9 @@ struct sk_csr {
   // device view is read-only) or known at construction (constant values)
   bool stats_valid = false;
   ValueStats stats;
+  // its statistics as a weight (value statistics + row bounds), cached likewise
+  bool wstats_valid = false;
+  ValueStats wstats;
   // set by the stream-asynchronous constructor: the arrays are complete once
   // this event has fired (every consumer orders its stream after it)
   cudaEvent_t ready = nullptr;
@@ -323,7 +326,7 @@ void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b,
 sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b,
                          sk_semiring s);
 sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const sk_csr* y,
-                          float clip, uint64_t dense_rows);
+                          float clip, uint64_t dense_rows, double negmin = INFINITY);
 sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* m, const sk_csr* y0,
                             float clip, uint64_t* nnz_trace);
 void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b,

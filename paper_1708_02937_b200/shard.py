@@ -139,17 +139,32 @@ def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None,
     """Column-sharded sparse forward pass.  `w_blocks[k]` is this rank's block
     of output-neuron rows of W_ref[k] (a CsrMatrix m_g x m), `b_blocks[k]` its
     bias slice, `y0` the full m x n input (replicated).  Returns (Y_L, trace).
-    Per layer: local block SpGEMM + epilogue on the GPU (sk_sparse_layer), then
-    one all-gather of the sparse row blocks over NCCL."""
+    Per layer: local block SpGEMM + epilogue on the GPU (sk_sparse_layer: the
+    order-free kernel when the layer's partial sums are provably exact), then
+    one all-gather of the sparse row blocks over NCCL; runs of layers with an
+    empty input and every bias <= 0 are skipped on every rank at once."""
     import torch
     from . import semikern as skm
     dist = _dist()
     if device is None:
         device = torch.device("cuda", torch.cuda.current_device())
     m, n = y0.rows(), y0.cols()
+    L = len(w_blocks)
+    # Per layer, is every bias <= 0 on every rank?  Then an empty input stays
+    # empty (untouched positions give epilogue(0 + b) = 0): those layers need no
+    # work and no exchange.  Every rank holds the same full Y_k, so all ranks
+    # take the same decision.
+    flags = torch.tensor([1 if np.all(np.asarray(b, np.float32) <= 0.0) else 0 for b in b_blocks],
+                         dtype=torch.int32, device=device)
+    if dist.is_initialized() and L:
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=group)
+    nonpos = [bool(x) for x in flags.cpu().tolist()]
     y = y0
     trace = [y.nnz()]
     for k, (w, b) in enumerate(zip(w_blocks, b_blocks)):
+        if y.nnz() == 0 and nonpos[k]:
+            trace.append(0)
+            continue
         local = skm.sparse_layer(w, b, y, clip)
         rp, ci, v = csr_to_torch(local, device)
         frp, fci, fv = allgather_csr_rows(rp, ci, v, group=group)

@@ -698,15 +698,20 @@ def test_sparse_route_equals_dense_route(sk):
 
 # ---- multi-GPU building blocks on one GPU ----------------------------------------------
 
-def test_sparse_layer_on_a_row_block_matches_oracle(sk, port):
+@pytest.mark.parametrize("kind", ["mixed_bias", "nonpos_bias", "random_weights"])
+def test_sparse_layer_on_a_row_block_matches_oracle(sk, port, kind):
+    # a row block of W_ref (column sharding): binary Y x 1/16 weights take the
+    # order-free kernel (with dense-sweep rows for positive biases, or the coarse
+    # window table when every bias <= 0); random weights the windowed SpGEMM
     from oracle.oracle import Csr
     m, n = 4096, 700
-    W = port.gen_layer_fixed(m, 32, 5, 1.0 / 16)
+    W = port.gen_layer_fixed(m, 32, 5, float("nan") if kind == "random_weights" else 1.0 / 16)
     Y = port.gen_input_binary(m, n, 300, 5)
     r0, r1 = 1000, 2500
     blk = Csr(r1 - r0, m, (W.row_ptr[r0:r1 + 1] - W.row_ptr[r0]).astype(np.uint32),
               W.col_idx[W.row_ptr[r0]:W.row_ptr[r1]], W.values[W.row_ptr[r0]:W.row_ptr[r1]])
-    b = np.where(np.arange(r1 - r0) % 7 == 0, 0.01, -0.05).astype(np.float32)
+    b = np.where(np.arange(r1 - r0) % 7 == 0, 0.01 if kind == "mixed_bias" else -0.2,
+                 -0.05).astype(np.float32)
     got = sk.sparse_layer(dev_csr(sk, blk), b, dev_csr(sk, Y), 32.0)
     assert_csr_bitwise(got, port.layer_sparse(blk, b, Y, 32.0))
 
@@ -723,19 +728,24 @@ def test_column_sharded_forward_single_rank_nccl(sk, port):
         s.close()
         dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port_no}", rank=0,
                                 world_size=1)
-    m, n, L = 4096, 500, 3
+    m, n, L = 4096, 500, 6
     hW = [port.gen_layer_fixed(m, 32, port.layer_seed(8, k), 1.0 / 16) for k in range(L)]
     hY = port.gen_input_binary(m, n, 400, 8)
-    b = np.full(m, -0.05, np.float32)
-    y, trace = relu_forward_sparse_colsharded([dev_csr(sk, w) for w in hW], [b] * L,
-                                              dev_csr(sk, hY), clip=32.0,
-                                              device=torch.device("cuda", 0))
-    want = hY
-    for w in hW:
-        want = port.layer_sparse(w, b, want, 32.0)
-    assert_csr_bitwise(y, want)
-    assert trace[-1] == want.nnz
-    dist.destroy_process_group()
+    # live layers, then a bias that empties the activations (the rest is skipped)
+    bs = [np.full(m, x, np.float32) for x in (-0.05, -0.05, -0.05, -9.0, -0.05, -0.05)]
+    try:
+        y, trace = relu_forward_sparse_colsharded([dev_csr(sk, w) for w in hW], bs,
+                                                  dev_csr(sk, hY), clip=32.0,
+                                                  device=torch.device("cuda", 0))
+        want, want_trace = hY, [hY.nnz]
+        for w, b in zip(hW, bs):
+            want = port.layer_sparse(w, b, want, 32.0)
+            want_trace.append(want.nnz)
+        assert_csr_bitwise(y, want)
+        assert list(trace) == want_trace
+        assert want_trace[1] > 0 and want_trace[4] == 0
+    finally:
+        dist.destroy_process_group()
 
 
 # ---- the dense comparator leg on tcgen05 (K4) ----------------------------------------
