@@ -245,12 +245,12 @@ def dense_layer_bytes(batch, m, nnzW):
 
 def measured_traffic(workload):
     """Per-launch DRAM traffic of the dominant kernel from the committed ncu
-    capture (profiles/r01/traffic.json), or None."""
+    capture (profiles/r01/traffic.json) and the unit that binds it there, or None."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
-        return t[workload]["bytes"], t[workload]["report"]
+        return t[workload]["bytes"], t[workload]["report"], t[workload].get("limiter")
     except Exception:
-        return None, None
+        return None, None, None
 
 
 def peaks():
@@ -618,9 +618,11 @@ def run_ours(args, w):
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
 
     if roof is not None:
-        tb, trep = measured_traffic(args.workload)
+        tb, trep, lim = measured_traffic(args.workload)
         roof["traffic"] = tb
         roof["traffic_source"] = trep
+        if lim is not None and not cols:
+            roof["measured_limiter"] = lim
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
