@@ -223,7 +223,11 @@ sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m,
 /* One sparse-activation layer with a RECTANGULAR weight block: W_ref rows are
  * a block of output neurons (m_blk x m), Y is m x n, the result m_blk x n.
  * Used by the column-sharded forward (each GPU owns a block of output
- * neurons, BASELINE cfg5); bias is host memory of length m_blk. */
+ * neurons, BASELINE cfg5); bias is host memory of length m_blk.  The layer
+ * takes the order-free exact kernel when its partial sums are provably exact
+ * (statistics of w cached on the handle), else the windowed SpGEMM; an empty
+ * input with every bias <= 0 returns an empty result without a launch.
+ * Bitwise the same either way. */
 sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* bias,
                           const sk_csr* y, float clip, sk_csr** out);
 /* Zero-copy view of a handle's device arrays (valid while the handle lives).
