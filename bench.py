@@ -409,8 +409,11 @@ def run_ours(args, w):
             del wf
         bblocks = [np.full(r1 - r0, w["bias"], np.float32)] * L
         Y0 = sk.gen_input_binary(m, B, kY_of(w), SEED)
+        # peer: one kernel per rank stores its block into every rank's next-layer
+        # buffers over NVLink (CUDA IPC); nccl: padded NCCL all-gathers
+        peer = shard.PeerExchange(m, ctx=sk.default_context()) if args.exchange == "peer" else None
         run = lambda y: shard.relu_forward_sparse_colsharded(  # noqa
-            blocks, bblocks, y, w["clip"], device=dev)
+            blocks, bblocks, y, w["clip"], device=dev, exchange=args.exchange, peer=peer)
         host_rp, host_ci, host_v = (np.array(a) for a in Y0.extract())
         nnz0 = int(host_rp[-1])
     elif w["y0"] == "binary":
@@ -632,8 +635,8 @@ def run_ours(args, w):
             "config": {"workload": w["desc"], "neurons": m, "layers": L,
                        "per_gpu_batch": B if not cols else B, "global_batch": B if cols else B * world,
                        "edges_per_inference_per_gpu": edges if not cols else edges // world,
-                       "parallelism": (f"column-sharded W x{world}, per-layer NCCL all-gather "
-                                       "of the sparse activations" if cols else
+                       "parallelism": (f"column-sharded W x{world}, per-layer exchange of the "
+                                       f"sparse activations ({args.exchange})" if cols else
                                        f"batch-row x{world}, replicated W, no data-path collective"),
                        "l2": "inputs larger than L2 (W %.2f GB + Y0 %.0f MB vs 126 MB L2)"
                              % (sum(nnzW) * 8 / 1e9, nnz0 * 8 / 1e6)},
@@ -669,6 +672,10 @@ def main():
                     help="N>1 decomposition: batch-row sharding with replicated W (default, no "
                          "data-path collective) or column sharding of W_k with a per-layer "
                          "NCCL all-gather of the sparse activations (BASELINE cfg5's layout)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="--shard cols: per-layer exchange of the sparse row blocks by peer-memory "
+                         "stores (one kernel per rank, CUDA IPC over NVLink) or padded NCCL "
+                         "all-gathers")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":

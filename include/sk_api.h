@@ -230,6 +230,23 @@ sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m,
  * Bitwise the same either way. */
 sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* bias,
                           const sk_csr* y, float clip, sk_csr** out);
+/* Column-sharded exchange over peer memory (no reference counterpart).
+ * sk_ipc_alloc: a cudaMalloc'd buffer of `bytes` and its 64-byte CUDA IPC
+ * handle; sk_ipc_open maps a peer's handle (peer access over NVLink);
+ * sk_ipc_close / sk_ipc_free release them.  sk_csr_publish writes the block
+ * `blk` (rows [row_off, row_off + rows) of the next layer's input) into each of
+ * `ndst` (<= 8) destinations with ONE kernel: col_idx / values at nnz_off, row
+ * pointers at row_off shifted by nnz_off, and the closing row pointer when
+ * write_last.  Stream-ordered on ctx's stream; the caller orders the readers
+ * after every rank's publish (a collective barrier). */
+sk_status sk_ipc_alloc(sk_ctx* ctx, size_t bytes, void** dptr, unsigned char* handle);
+sk_status sk_ipc_open(sk_ctx* ctx, const unsigned char* handle, void** dptr);
+sk_status sk_ipc_close(void* dptr);
+sk_status sk_ipc_free(void* dptr);
+sk_status sk_csr_publish(sk_ctx* ctx, const sk_csr* blk, uint32_t ndst,
+                         uint32_t* const* dst_rp, uint32_t* const* dst_ci,
+                         float* const* dst_v, uint32_t row_off, uint64_t nnz_off,
+                         int write_last);
 /* Zero-copy view of a handle's device arrays (valid while the handle lives).
  * Read-only: handles are immutable (the library caches per-matrix value
  * statistics). */

@@ -40,6 +40,7 @@ EXPORTS = [
     "sk_layer_step", "sk_relu_forward", "sk_relu_forward_host", "sk_relu_forward_sparse",
     "sk_categories_csr", "sk_categories_dense",
     "sk_sparse_layer", "sk_csr_device_arrays", "sk_csr_from_device", "sk_memcpy_d2d",
+    "sk_ipc_alloc", "sk_ipc_open", "sk_ipc_close", "sk_ipc_free", "sk_csr_publish",
     "sk_dense_layer_step", "sk_dense_relu_forward",
     "sk_gen_layer_fixed", "sk_gen_layer_density", "sk_gen_weight",
     "sk_read_matrix", "sk_read_matrix_text", "sk_write_matrix", "sk_format_matrix", "sk_gen_input_dense",
@@ -123,6 +124,12 @@ def load() -> C.CDLL:
     L.sk_csr_from_device.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_size_t, vp, vp, vp,
                                      C.POINTER(vp)]
     L.sk_memcpy_d2d.argtypes = [vp, vp, vp, C.c_size_t]
+    L.sk_ipc_alloc.argtypes = [vp, C.c_size_t, C.POINTER(vp), C.c_char_p]
+    L.sk_ipc_open.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
+    L.sk_ipc_close.argtypes = [vp]
+    L.sk_ipc_free.argtypes = [vp]
+    L.sk_csr_publish.argtypes = [vp, vp, C.c_uint32, C.POINTER(vp), C.POINTER(vp),
+                                 C.POINTER(vp), C.c_uint32, C.c_uint64, C.c_int]
     L.sk_categories_csr.argtypes = [vp, vp, vp, C.c_size_t, C.POINTER(C.c_size_t)]
     L.sk_categories_dense.argtypes = [vp, vp, vp, C.c_size_t, C.POINTER(C.c_size_t)]
     L.sk_dense_layer_step.argtypes = [vp, vp, vp, vp, C.POINTER(vp)]

@@ -1024,3 +1024,109 @@ extern "C" sk_status sk_gen_input_binary(sk_ctx* ctx, uint32_t m, uint32_t n, ui
     *out = t;
   });
 }
+
+// ---- column-sharded exchange over peer memory ----------------------------------------
+// Each rank's block of output rows (a CSR of rows [row_off, row_off + rows) of
+// Y_{k+1}) is written by ONE kernel straight into every rank's next-layer input
+// buffers (CUDA IPC pointers to the peers' memory: stores over NVLink), at its
+// entry offset nnz_off, with the row pointers shifted by nnz_off; the last rank
+// also writes the closing row pointer.  The buffers are plain cudaMalloc
+// allocations exported with cudaIpcGetMemHandle.
+
+namespace sk {
+namespace {
+
+struct PublishDst {
+  uint32_t* rp[8];
+  uint32_t* ci[8];
+  float* v[8];
+};
+
+__global__ void k_csr_publish(const uint32_t* rp, const uint32_t* ci, const float* v, uint32_t rows,
+                              size_t nnz, PublishDst dst, uint32_t nd, uint32_t row_off,
+                              uint32_t nnz_off, int write_last) {
+  const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+  const size_t nth = size_t(gridDim.x) * blockDim.x;
+  for (uint32_t d = 0; d < nd; ++d) {
+    uint32_t* const oci = dst.ci[d] + nnz_off;
+    float* const ov = dst.v[d] + nnz_off;
+    for (size_t e = tid; e < nnz; e += nth) {
+      oci[e] = ci[e];
+      ov[e] = v[e];
+    }
+    uint32_t* const orp = dst.rp[d] + row_off;
+    for (size_t i = tid; i < rows; i += nth) orp[i] = rp[i] + nnz_off;
+    if (write_last && tid == 0) orp[rows] = rp[rows] + nnz_off;
+  }
+}
+
+}  // namespace
+}  // namespace sk
+
+static void ipc_ctx(sk_ctx* ctx) {
+  if (!ctx) fail(SK_ERR_INVALID_ARGUMENT, "null context");
+  SK_CUDA(cudaSetDevice(ctx->device));
+}
+
+extern "C" sk_status sk_ipc_alloc(sk_ctx* ctx, size_t bytes, void** dptr, unsigned char* handle) {
+  return guarded([&] {
+    ipc_ctx(ctx);
+    void* p = nullptr;
+    SK_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      fail(SK_ERR_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+    }
+    std::memcpy(handle, &h, sizeof(h));
+    *dptr = p;
+  });
+}
+
+extern "C" sk_status sk_ipc_open(sk_ctx* ctx, const unsigned char* handle, void** dptr) {
+  return guarded([&] {
+    ipc_ctx(ctx);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    SK_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    *dptr = p;
+  });
+}
+
+extern "C" sk_status sk_ipc_close(void* dptr) {
+  return guarded([&] {
+    if (dptr) SK_CUDA(cudaIpcCloseMemHandle(dptr));
+  });
+}
+
+extern "C" sk_status sk_ipc_free(void* dptr) {
+  return guarded([&] {
+    if (dptr) SK_CUDA(cudaFree(dptr));
+  });
+}
+
+extern "C" sk_status sk_csr_publish(sk_ctx* ctx, const sk_csr* blk, uint32_t ndst,
+                                    uint32_t* const* dst_rp, uint32_t* const* dst_ci,
+                                    float* const* dst_v, uint32_t row_off, uint64_t nnz_off,
+                                    int write_last) {
+  return guarded([&] {
+    ipc_ctx(ctx);
+    csr_ready(ctx, blk);
+    if (ndst > 8) fail(SK_ERR_INVALID_ARGUMENT, "at most 8 destinations (one NVLink box)");
+    if (nnz_off + blk->nnz > 0xFFFFFFFFull)
+      fail(SK_ERR_INVALID_ARGUMENT, "exchange exceeds the 32-bit index range");
+    PublishDst d{};
+    for (uint32_t r = 0; r < ndst; ++r) {
+      d.rp[r] = dst_rp[r];
+      d.ci[r] = dst_ci[r];
+      d.v[r] = dst_v[r];
+    }
+    const uint64_t work = std::max<uint64_t>(blk->nnz, blk->rows);
+    const unsigned grid = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>((work + 255) / 256, uint64_t(ctx->num_sms) * 8)));
+    SK_LAUNCH(k_csr_publish, grid, 256, 0, ctx->stream, blk->rp, blk->ci, blk->v, blk->rows,
+              blk->nnz, d, ndst, row_off, uint32_t(nnz_off), write_last);
+  });
+}

@@ -874,3 +874,42 @@ def csr_from_device(rows: int, cols: int, nnz: int, rp_ptr: int, ci_ptr: int, v_
 def memcpy_d2d(dst_ptr: int, src_ptr: int, nbytes: int, ctx: Context | None = None):
     c = _ctx(ctx)
     _check(c._L.sk_memcpy_d2d(c.h, vp(dst_ptr), vp(src_ptr), nbytes))
+
+
+# ---- column-sharded exchange over peer memory (sk_ipc_*, sk_csr_publish) ----------------
+
+def ipc_alloc(nbytes: int, ctx: Context | None = None) -> tuple[int, bytes]:
+    """A cudaMalloc'd device buffer and its 64-byte CUDA IPC handle."""
+    c = _ctx(ctx)
+    p = vp()
+    h = C.create_string_buffer(64)
+    _check(c._L.sk_ipc_alloc(c.h, max(int(nbytes), 16), C.byref(p), h))
+    return p.value or 0, h.raw
+
+
+def ipc_open(handle: bytes, ctx: Context | None = None) -> int:
+    """Map a peer's buffer (peer access over NVLink)."""
+    c = _ctx(ctx)
+    p = vp()
+    _check(c._L.sk_ipc_open(c.h, C.create_string_buffer(bytes(handle), 64), C.byref(p)))
+    return p.value or 0
+
+
+def ipc_close(ptr: int):
+    _check(_lib.load().sk_ipc_close(vp(ptr)))
+
+
+def ipc_free(ptr: int):
+    _check(_lib.load().sk_ipc_free(vp(ptr)))
+
+
+def csr_publish(blk: CsrMatrix, dst_rp, dst_ci, dst_v, row_off: int, nnz_off: int,
+                write_last: bool):
+    """One kernel writes `blk` into every destination (device pointers, peers'
+    included): entries at nnz_off, row pointers at row_off shifted by nnz_off."""
+    n = len(dst_rp)
+    arr = vp * n
+    _check(blk.ctx._L.sk_csr_publish(blk.ctx.h, blk.h, n, arr(*[vp(x) for x in dst_rp]),
+                                     arr(*[vp(x) for x in dst_ci]),
+                                     arr(*[vp(x) for x in dst_v]), int(row_off), int(nnz_off),
+                                     1 if write_last else 0))

@@ -135,14 +135,112 @@ def row_block(a, r0: int, r1: int, device):
     return out
 
 
-def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None, device=None):
+def exchange_plan(counts, rank: int):
+    """Entry offset of `rank`'s block and the total, from every rank's block
+    nnz (rank order = row order)."""
+    counts = [int(c) for c in counts]
+    return sum(counts[:rank]), sum(counts)
+
+
+def grown_capacity(total: int, cap: int) -> int:
+    """Receive-buffer capacity (entries) after a layer of `total` entries: a
+    rank-independent rule, so every rank reallocates (and re-exchanges its IPC
+    handles) at the same layer."""
+    if total <= cap:
+        return cap
+    c = max(cap, 1 << 16)
+    while c < total:
+        c *= 2
+    return c
+
+
+class PeerExchange:
+    """Two sets (ping-pong) of next-layer input buffers per rank (row pointers
+    m+1, col_idx / values `cap` entries), exported with CUDA IPC and mapped by
+    every peer.  A rank's block is published by ONE kernel (sk_csr_publish:
+    stores over NVLink into every rank's buffers); readers are ordered after
+    every rank's publish by a collective barrier.  Layer k's output goes to set
+    k % 2: a rank can only write set s again after every rank passed the barrier
+    of the layer that read it."""
+
+    def __init__(self, m: int, group=None, ctx=None):
+        from . import semikern as skm
+        self.skm, self.m, self.group, self.ctx = skm, m, group, ctx
+        dist = _dist()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.cap = 0
+        self.sets = [None, None]
+
+    def _free_all(self):
+        # every rank unmaps its peers' buffers before any owner frees its own
+        for s in self.sets:
+            if s is not None:
+                for (_, peers) in s.values():
+                    for r, p in enumerate(peers):
+                        if r != self.rank:
+                            self.skm.ipc_close(p)
+        if self.world > 1:
+            _dist().barrier(group=self.group)
+        for s in self.sets:
+            if s is not None:
+                for (own, _) in s.values():
+                    self.skm.ipc_free(own)
+        self.sets = [None, None]
+
+    def _alloc_set(self):
+        import torch
+        dist = _dist()
+        out = {}
+        for name, nbytes in (("rp", (self.m + 1) * 4), ("ci", self.cap * 4), ("v", self.cap * 4)):
+            own, h = self.skm.ipc_alloc(nbytes, ctx=self.ctx)
+            hs = [h]
+            if self.world > 1:
+                hs = [None] * self.world
+                dist.all_gather_object(hs, h, group=self.group)
+            peers = [own if r == self.rank else self.skm.ipc_open(hs[r], ctx=self.ctx)
+                     for r in range(self.world)]
+            out[name] = (own, peers)
+        torch.cuda.synchronize()
+        return out
+
+    def ensure(self, total: int):
+        cap = grown_capacity(total, self.cap)
+        if cap != self.cap or self.sets[0] is None:
+            if self.world > 1:
+                _dist().barrier(group=self.group)  # nobody still reads the old buffers
+            self._free_all()
+            self.cap = cap
+            self.sets = [self._alloc_set(), self._alloc_set()]
+
+    def publish(self, blk, k: int, row_off: int, nnz_off: int, write_last: bool):
+        s = self.sets[k % 2]
+        self.skm.csr_publish(blk, s["rp"][1], s["ci"][1], s["v"][1], row_off, nnz_off,
+                             write_last)
+
+    def local(self, k: int):
+        s = self.sets[k % 2]
+        return s["rp"][0], s["ci"][0], s["v"][0]
+
+    def close(self):
+        if self.world > 1:
+            _dist().barrier(group=self.group)
+        self._free_all()
+
+
+def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None, device=None,
+                                   exchange="peer", peer=None):
     """Column-sharded sparse forward pass.  `w_blocks[k]` is this rank's block
     of output-neuron rows of W_ref[k] (a CsrMatrix m_g x m), `b_blocks[k]` its
     bias slice, `y0` the full m x n input (replicated).  Returns (Y_L, trace).
     Per layer: local block SpGEMM + epilogue on the GPU (sk_sparse_layer: the
     order-free kernel when the layer's partial sums are provably exact), then
-    one all-gather of the sparse row blocks over NCCL; runs of layers with an
-    empty input and every bias <= 0 are skipped on every rank at once."""
+    one exchange of the sparse row blocks; runs of layers with an empty input
+    and every bias <= 0 are skipped on every rank at once.  exchange="peer": the
+    block counts go through one tiny NCCL all-gather, then ONE kernel per rank
+    stores its block into every rank's next-layer buffers over NVLink (CUDA
+    IPC, PeerExchange; pass `peer` to reuse its buffers across calls);
+    exchange="nccl": padded NCCL all-gathers of the blocks."""
     import torch
     from . import semikern as skm
     dist = _dist()
@@ -161,20 +259,45 @@ def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None,
     nonpos = [bool(x) for x in flags.cpu().tolist()]
     y = y0
     trace = [y.nnz()]
+    own_peer = None
     for k, (w, b) in enumerate(zip(w_blocks, b_blocks)):
         if y.nnz() == 0 and nonpos[k]:
             trace.append(0)
             continue
         local = skm.sparse_layer(w, b, y, clip)
-        rp, ci, v = csr_to_torch(local, device)
-        frp, fci, fv = allgather_csr_rows(rp, ci, v, group=group)
-        nnz = int(frp[-1].item())
-        frp32 = frp.to(torch.int32)
-        torch.cuda.synchronize(device)
-        y = skm.csr_from_device(m, n, nnz, frp32.data_ptr(), fci.data_ptr(), fv.data_ptr(),
-                                ctx=y0.ctx)
-        y.ctx.synchronize()
+        if exchange == "peer":
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+            cnt = torch.tensor([local.nnz()], dtype=torch.int64, device=device)
+            cnts = [cnt]
+            if world > 1:
+                cnts = [torch.zeros_like(cnt) for _ in range(world)]
+                dist.all_gather(cnts, cnt, group=group)
+            off, nnz = exchange_plan([int(c.item()) for c in cnts], rank)
+            if peer is None:
+                peer = own_peer = PeerExchange(m, group=group, ctx=y0.ctx)
+            peer.ensure(nnz)
+            r0, _ = block_range(m, world, rank)
+            peer.publish(local, k, r0, off, rank == world - 1)
+            if world > 1:  # every rank's stores land before anyone reads
+                flag = torch.zeros(1, device=device)
+                torch.cuda.current_stream(device).synchronize()
+                dist.all_reduce(flag, group=group)
+            lrp, lci, lv = peer.local(k)
+            y = skm.csr_from_device(m, n, nnz, lrp, lci, lv, ctx=y0.ctx)
+            y.ctx.synchronize()
+        else:
+            rp, ci, v = csr_to_torch(local, device)
+            frp, fci, fv = allgather_csr_rows(rp, ci, v, group=group)
+            nnz = int(frp[-1].item())
+            frp32 = frp.to(torch.int32)
+            torch.cuda.synchronize(device)
+            y = skm.csr_from_device(m, n, nnz, frp32.data_ptr(), fci.data_ptr(), fv.data_ptr(),
+                                    ctx=y0.ctx)
+            y.ctx.synchronize()
         trace.append(nnz)
     if dist.is_initialized():
         dist.barrier(group=group)
+    if own_peer is not None:  # y is an owned copy: the exchange buffers can go
+        own_peer.close()
     return y, trace

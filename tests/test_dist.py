@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1708_02937_b200.shard import (allgather_csr_rows, batch_shard, block_range,
-                                         gather_categories)
+                                         exchange_plan, gather_categories, grown_capacity)
 
 
 def free_port():
@@ -136,3 +136,39 @@ def _w_batchshard(rank, world):
 
 def test_batch_sharded_categories_match_single_process():
     run_world(_w_batchshard)
+
+
+def _w_peer_plan(rank, world):
+    """The peer-memory exchange's host logic: every rank derives the same
+    entry offsets (a partition of the concatenated blocks, rank order) and the
+    same receive-buffer capacity from the gathered block counts, layer after
+    layer, so all ranks reallocate and re-exchange IPC handles together."""
+    rng = np.random.default_rng(7 + rank)
+    cap = 0
+    for layer in range(6):
+        mine = int(rng.integers(0, 50000 * (layer + 1)))
+        c = torch.tensor([mine], dtype=torch.int64)
+        cs = [torch.zeros_like(c) for _ in range(world)]
+        dist.all_gather(cs, c)
+        counts = [int(x.item()) for x in cs]
+        off, total = exchange_plan(counts, rank)
+        assert off == sum(counts[:rank]) and total == sum(counts)
+        cap = grown_capacity(total, cap)
+        assert cap >= total
+        agreed = [None] * world
+        dist.all_gather_object(agreed, (off, off + mine, total, cap))
+        spans = sorted((a, b) for a, b, _, _ in agreed)
+        assert spans[0][0] == 0 and spans[-1][1] == total
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+        assert len({(t, k) for _, _, t, k in agreed}) == 1
+
+
+def test_peer_exchange_plan_agrees_across_ranks():
+    run_world(_w_peer_plan)
+
+
+def test_grown_capacity_rule():
+    assert grown_capacity(0, 0) == 0
+    assert grown_capacity(10, 0) == 1 << 16
+    assert grown_capacity(70000, 1 << 16) == 1 << 17
+    assert grown_capacity(100, 1 << 17) == 1 << 17

@@ -716,7 +716,36 @@ def test_sparse_layer_on_a_row_block_matches_oracle(sk, port, kind):
     assert_csr_bitwise(got, port.layer_sparse(blk, b, Y, 32.0))
 
 
-def test_column_sharded_forward_single_rank_nccl(sk, port):
+def test_csr_publish_to_several_destinations(sk, port):
+    # the peer-exchange kernel: one launch writes a block into every destination
+    # at its entry offset, row pointers shifted (here: two buffers on this GPU)
+    import torch
+    from paper_1708_02937_b200 import semikern as skm
+    m, n = 300, 90
+    blk_h = port.gen_input_binary(120, n, 7, 3)  # a 120-row block
+    blk = dev_csr(sk, blk_h)
+    row_off, nnz_off, total = 100, 5000, 5000 + blk_h.nnz
+    dev = torch.device("cuda", 0)
+    bufs = [(torch.full((m + 1,), 7, dtype=torch.int32, device=dev),
+             torch.full((total,), 9, dtype=torch.int32, device=dev),
+             torch.full((total,), -1.0, dtype=torch.float32, device=dev)) for _ in range(2)]
+    for last in (False, True):
+        skm.csr_publish(blk, [b[0].data_ptr() for b in bufs], [b[1].data_ptr() for b in bufs],
+                        [b[2].data_ptr() for b in bufs], row_off, nnz_off, last)
+        torch.cuda.synchronize()
+        for rp, ci, v in bufs:
+            rp, ci, v = rp.cpu().numpy(), ci.cpu().numpy(), v.cpu().numpy()
+            assert np.array_equal(rp[row_off:row_off + 120],
+                                  blk_h.row_ptr[:120].astype(np.int64) + nnz_off)
+            assert rp[row_off + 120] == (total if last else 7)
+            assert rp[row_off - 1] == 7
+            assert np.array_equal(ci[nnz_off:], blk_h.col_idx.astype(np.int32))
+            assert np.array_equal(bits(v[nnz_off:]), bits(blk_h.values))
+            assert np.all(ci[:nnz_off] == 9)
+
+
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+def test_column_sharded_forward_single_rank_nccl(sk, port, exchange):
     import socket
     import torch
     import torch.distributed as dist
@@ -736,7 +765,8 @@ def test_column_sharded_forward_single_rank_nccl(sk, port):
     try:
         y, trace = relu_forward_sparse_colsharded([dev_csr(sk, w) for w in hW], bs,
                                                   dev_csr(sk, hY), clip=32.0,
-                                                  device=torch.device("cuda", 0))
+                                                  device=torch.device("cuda", 0),
+                                                  exchange=exchange)
         want, want_trace = hY, [hY.nnz]
         for w, b in zip(hW, bs):
             want = port.layer_sparse(w, b, want, 32.0)
