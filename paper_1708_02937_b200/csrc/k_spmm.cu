@@ -23,7 +23,11 @@ namespace sk {
 
 enum EpiMode { kEpiNone = 0, kEpiLayer = 1 };
 
-template <typename Ops, int kEpi, bool kVec4>
+// kU: 128-column chunks per task (a lane owns 4 columns of each).  Light rows
+// (few stored entries) take kU = 4: the row's (k, w) pairs are loaded once for
+// 512 columns and every entry issues four independent float4 loads, so a task
+// is not a chain of dependent round trips per 128 columns.
+template <typename Ops, int kEpi, bool kVec4, int kU = 1>
 __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
                                            const uint32_t* __restrict__ ci,
                                            const float* __restrict__ wv,
@@ -33,14 +37,17 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
                                            unsigned long long* nz_count = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t nz = 0;  // nonzero outputs written by this lane (only when nz_count)
-  const uint32_t chunks = (n + 127) / 128;
+  const uint32_t chunks = (n + 128 * kU - 1) / (128 * kU);
   const uint64_t tasks = uint64_t(chunks) * m;
   for (uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; task < tasks;
        task += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
     const uint32_t c = uint32_t(task / m);
     const uint32_t i = uint32_t(task % m);
-    const uint32_t col0 = c * 128 + lane * 4;
-    float acc0 = Ops::zero(), acc1 = Ops::zero(), acc2 = Ops::zero(), acc3 = Ops::zero();
+    float acc[kU][4];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[u][q] = Ops::zero();
     const uint32_t eb = rp[i], ee = rp[i + 1];
     for (uint32_t e0 = eb; e0 < ee; e0 += 32) {
       const uint32_t cnt = min(32u, ee - e0);
@@ -55,43 +62,46 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
         const uint32_t k = __shfl_sync(0xffffffffu, kk, t);
         const float a = __shfl_sync(0xffffffffu, aa, t);
         const float* yr = y + size_t(k) * n;
-        if (kVec4) {
-          if (col0 < n) {
-            const float4 v = *reinterpret_cast<const float4*>(yr + col0);
-            acc0 = Ops::add(acc0, Ops::mul(a, v.x, err), err);
-            acc1 = Ops::add(acc1, Ops::mul(a, v.y, err), err);
-            acc2 = Ops::add(acc2, Ops::mul(a, v.z, err), err);
-            acc3 = Ops::add(acc3, Ops::mul(a, v.w, err), err);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t col0 = (c * kU + u) * 128 + lane * 4;
+          if (kVec4) {
+            if (col0 < n) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(yr + col0));
+              acc[u][0] = Ops::add(acc[u][0], Ops::mul(a, v.x, err), err);
+              acc[u][1] = Ops::add(acc[u][1], Ops::mul(a, v.y, err), err);
+              acc[u][2] = Ops::add(acc[u][2], Ops::mul(a, v.z, err), err);
+              acc[u][3] = Ops::add(acc[u][3], Ops::mul(a, v.w, err), err);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (col0 + q < n) acc[u][q] = Ops::add(acc[u][q], Ops::mul(a, yr[col0 + q], err), err);
           }
-        } else {
-          if (col0 + 0 < n) acc0 = Ops::add(acc0, Ops::mul(a, yr[col0 + 0], err), err);
-          if (col0 + 1 < n) acc1 = Ops::add(acc1, Ops::mul(a, yr[col0 + 1], err), err);
-          if (col0 + 2 < n) acc2 = Ops::add(acc2, Ops::mul(a, yr[col0 + 2], err), err);
-          if (col0 + 3 < n) acc3 = Ops::add(acc3, Ops::mul(a, yr[col0 + 3], err), err);
         }
       }
     }
-    if (kEpi == kEpiLayer) {
-      const float b = bias[i];
-      acc0 = layer_epilogue(acc0, b, clip);
-      acc1 = layer_epilogue(acc1, b, clip);
-      acc2 = layer_epilogue(acc2, b, clip);
-      acc3 = layer_epilogue(acc3, b, clip);
-    }
-    if (nz_count) {
-      if (col0 + 0 < n) nz += acc0 != 0.0f;
-      if (col0 + 1 < n) nz += acc1 != 0.0f;
-      if (col0 + 2 < n) nz += acc2 != 0.0f;
-      if (col0 + 3 < n) nz += acc3 != 0.0f;
-    }
+    float b = 0.0f;
+    if (kEpi == kEpiLayer) b = bias[i];
     float* orow = out + size_t(i) * n;
-    if (kVec4) {
-      if (col0 < n) *reinterpret_cast<float4*>(orow + col0) = make_float4(acc0, acc1, acc2, acc3);
-    } else {
-      if (col0 + 0 < n) orow[col0 + 0] = acc0;
-      if (col0 + 1 < n) orow[col0 + 1] = acc1;
-      if (col0 + 2 < n) orow[col0 + 2] = acc2;
-      if (col0 + 3 < n) orow[col0 + 3] = acc3;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t col0 = (c * kU + u) * 128 + lane * 4;
+      if (kEpi == kEpiLayer)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[u][q] = layer_epilogue(acc[u][q], b, clip);
+      if (nz_count)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nz += (col0 + q < n && acc[u][q] != 0.0f) ? 1u : 0u;
+      if (kVec4) {
+        if (col0 < n)
+          *reinterpret_cast<float4*>(orow + col0) =
+              make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (col0 + q < n) orow[col0 + q] = acc[u][q];
+      }
     }
   }
   if (nz_count) {  // warp-uniform: nz_count is a kernel argument
@@ -101,13 +111,13 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
   }
 }
 
-template <typename Ops, int kEpi, bool kVec4>
+template <typename Ops, int kEpi, bool kVec4, int kU = 1>
 __global__ void __launch_bounds__(256)
     k_spmm_rows(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                 const float* __restrict__ wv, const float* __restrict__ bias,
                 const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
                 float* __restrict__ out, int* err) {
-  spmm_tasks<Ops, kEpi, kVec4>(rp, ci, wv, bias, y, m, n, clip, out, err);
+  spmm_tasks<Ops, kEpi, kVec4, kU>(rp, ci, wv, bias, y, m, n, clip, out, err);
 }
 
 // The whole dense-activation forward in ONE persistent cooperative launch: each
@@ -153,8 +163,8 @@ __global__ void __launch_bounds__(256) k_dense_engine(DenseEngineArgs p) {
   }
 }
 
-static unsigned spmm_grid(sk_ctx* ctx, uint32_t m, uint32_t n) {
-  const uint64_t warps = uint64_t((n + 127) / 128) * m;
+static unsigned spmm_grid(sk_ctx* ctx, uint32_t m, uint32_t n, int U = 1) {
+  const uint64_t warps = uint64_t((n + 128 * U - 1) / (128 * U)) * m;
   const uint64_t blocks = (warps + 7) / 8;
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(blocks, uint64_t(ctx->num_sms) * 16)));
 }
@@ -203,7 +213,13 @@ void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const
                         uint32_t n, float clip, float* out) {
   if (w->rows == 0 || n == 0) return;
   const bool vec = (n % 4 == 0);
-  if (vec)
+  // light rows (<= 16 stored entries on average) and wide activations: four
+  // 128-column chunks per task
+  const bool light = vec && n >= 512 && w->nnz <= size_t(16) * w->rows;
+  if (light)
+    SK_LAUNCH((k_spmm_rows<OpArith, kEpiLayer, true, 4>), spmm_grid(ctx, w->rows, n, 4), 256, 0,
+              ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n, clip, out, ctx->d_err);
+  else if (vec)
     SK_LAUNCH((k_spmm_rows<OpArith, kEpiLayer, true>), spmm_grid(ctx, w->rows, n), 256, 0,
               ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n, clip, out, ctx->d_err);
   else
