@@ -1584,8 +1584,11 @@ static unsigned grid_warps(sk_ctx* ctx, uint64_t warps) {
 static uint32_t* build_wp(sk_ctx* ctx, const sk_csr* b, const WinGeom& g, bool arena = false) {
   const uint64_t n = uint64_t(b->rows) * g.nW;
   uint32_t* wp = arena ? aalloc<uint32_t>(ctx, n + 1) : dalloc<uint32_t>(ctx, n + 1);
-  SK_LAUNCH(k_build_wp, grid_warps(ctx, b->rows), 256, 0, ctx->stream, b->rp, b->ci, b->rows,
-            g.nW, g.sh, wp);
+  // a warp per row, every row's warp resident in one wave when it fits: the
+  // kernel is a chain of dependent loads per row, not a bandwidth problem
+  const unsigned blocks = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((uint64_t(b->rows) + 7) / 8, uint64_t(ctx->num_sms) * 64)));
+  SK_LAUNCH(k_build_wp, blocks, 256, 0, ctx->stream, b->rp, b->ci, b->rows, g.nW, g.sh, wp);
   return wp;
 }
 
