@@ -47,6 +47,9 @@
 
 #include <cstring>
 
+#include <map>
+#include <mutex>
+
 #include "sk_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -2118,13 +2121,26 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     attr = true;
   }
   const size_t smem = size_t(kWarps) * exact_warp_bytes(g.S, big ? kExactRecCap : kEngineRecCap);
+  // occupancy per (variant, shared memory): a driver query, cached (host time
+  // between launches is GPU idle time)
+  static std::mutex occ_mu;
+  static std::map<std::pair<int, size_t>, int> occ;
   int per_sm = 0;
-  if (big)
-    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exact_layer<kExactRecCap>,
-                                                          kWarps * 32, smem));
-  else
-    SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exact_layer<kEngineRecCap>,
-                                                          kWarps * 32, smem));
+  {
+    std::lock_guard<std::mutex> lk(occ_mu);
+    auto it = occ.find({big ? 1 : 0, smem});
+    if (it != occ.end()) {
+      per_sm = it->second;
+    } else {
+      if (big)
+        SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_exact_layer<kExactRecCap>, kWarps * 32, smem));
+      else
+        SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_exact_layer<kEngineRecCap>, kWarps * 32, smem));
+      occ[{big ? 1 : 0, smem}] = per_sm;
+    }
+  }
   const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
   unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
   auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
