@@ -603,19 +603,24 @@ __device__ void process_item(const RowArgs& p, uint32_t i, uint32_t g, const War
 // equals it bit for bit (acc * 2^gran, +0 for 0).  Integer shared atomics are
 // native (float ones are a CAS loop).
 //
-// Packing: when qb <= 32767 (or <= 127) every partial sum fits a biased 16-bit
-// (8-bit) field, so one 32-bit accumulator word holds P = 2 (4) fields: field `sub` of
-// word s is window (first + sub), sample s.  Adding q << (B*sub) to the word
-// never carries across fields (the biased field stays in [0, 2^B)), so one
-// S-word accumulator serves P consecutive windows and the per-window overhead
-// is paid once per P windows.
+// Packing: when every partial sum (plus the field offset) fits a 16-bit (8-bit)
+// field, one 32-bit accumulator word holds P = 2 (4) fields: field `sub` of word
+// s is window (first + sub), sample s.  Adding q << (B*sub) to the word never
+// carries across fields (exact_params picks the width so the field stays in
+// [0, 2^B)), so one S-word accumulator serves P consecutive windows and the
+// per-window overhead is paid once per P windows.
+//
+// A field holds sum + foff, foff = 2^(B-1) - 1 - thr_min: its top bit is set iff
+// the sum is above the layer's smallest threshold.  A position can only survive
+// if its final sum is above its row's thr = -b * 2^-gran >= thr_min, so an update
+// whose result sets a top bit the old word lacked marks a candidate; the
+// epilogue walks candidates only (with the row's own threshold) and the
+// accumulator is reset to foff with vector stores.
 //
 // The accumulator's products are cut into pieces of <= 4 consecutive products
 // of one in-edge; each lane takes one piece record per round (all four loads in
-// flight before any update) and the in-edge's increment by one shuffle.  A
-// position can only survive if its final sum is above thr = -b * 2^-gran, so
-// updates that leave the sum above thr mark a candidate bit; the epilogue walks
-// candidates only and the accumulator is reset with vector stores.
+// flight before any update) and the in-edge's increment by one shuffle (none
+// when the increment is constant).
 // top bit of every field of a word with P fields
 __host__ __device__ __forceinline__ uint32_t fx_top_bits(uint32_t P) {
   return P == 1 ? 0x80000000u : (P == 2 ? 0x80008000u : 0x80808080u);
