@@ -631,12 +631,13 @@ __host__ __device__ __forceinline__ uint32_t fx_top_bits(uint32_t P) {
 constexpr int kEngineRecCap = 64, kExactRecCap = 192;
 
 // kSh: compile-time log2 window (0 = runtime p.sh); kYC: Y is constant-valued
-template <bool kLayer, int kSh, bool kYC, int kCap, bool kQC = false>
+// kP: compile-time fields per word (0 = runtime p.fx_pack)
+template <bool kLayer, int kSh, bool kYC, int kCap, bool kQC = false, int kP = 0>
 __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
                                    int lane) {
   const int sh = kSh ? kSh : p.sh;
   const uint32_t S = 1u << sh, SW = S / 32;
-  const uint32_t P = p.fx_pack;
+  const uint32_t P = kP ? uint32_t(kP) : p.fx_pack;
   const uint32_t B = 32 / P;
   const uint32_t fmask = P == 1 ? 0xFFFFFFFFu : ((1u << B) - 1u);
   const uint32_t foff = p.fx_off;
@@ -825,7 +826,11 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
 // processed; every other row's items were zeroed by the caller.
 // kSh (exact path): compile-time log2 window, 0 = dispatch on p.sh; kCap: piece
 // records per batch (exact path)
-template <typename Ops, bool kLayer, bool kExact, int kSh = 0, int kCap = kEngineRecCap>
+// kFast (standalone exact layer only): the one variant the host proved applies --
+// 1024-sample windows, a constant increment, four 8-bit fields, no dense rows --
+// compiled alone so its registers are not shared with the other paths
+template <typename Ops, bool kLayer, bool kExact, int kSh = 0, int kCap = kEngineRecCap,
+          bool kFast = false>
 __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
                                         uint64_t gw, uint64_t nwarps,
                                         const uint32_t* rows = nullptr, uint32_t nrows = 0) {
@@ -840,7 +845,9 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
   uint32_t r = uint32_t(gw % nr);
   for (; g < ng;) {
     const uint32_t i = rows ? rows[r] : r;
-    if (kExact) {
+    if (kFast) {
+      process_item_exact<kLayer, 10, true, kCap, true, 4>(p, i, uint32_t(g), ws, lane);
+    } else if (kExact) {
       // rows whose untouched positions survive (epilogue(0 + b) != 0) need the
       // dense sweep of the float exact path
       if (kLayer && layer_epilogue(0.0f, p.bias[i], p.clip) != 0.0f) {
@@ -1072,7 +1079,7 @@ __host__ __device__ constexpr size_t exact_warp_bytes(uint32_t S, int cap) {
   return (size_t(S) + S / 32 + 2 * size_t(cap) + 4 * (S / 32)) * 4;
 }
 
-template <int kSh, int kCap>  // kSh 0: runtime p.sh
+template <int kSh, int kCap, bool kFast = false>  // kSh 0: runtime p.sh
 __device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1092,16 +1099,18 @@ __device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   __syncwarp();
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  phase_a<OpArith, true, true, kSh, kCap>(p, ws, lane, gw, nw);
+  phase_a<OpArith, true, true, kSh, kCap, kFast>(p, ws, lane, gw, nw);
 }
 
 // kCap: piece records per batch -- 192 when an accumulator pass holds many
 // products (one batch), 64 otherwise (the smaller area leaves L1 to the
 // gathered loads of wide, thin layers)
-template <int kCap>
+template <int kCap, bool kFast = false>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long long* stamp) {
   if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer();
-  if (p.sh == 10)
+  if (kFast)
+    exact_layer_body<10, kCap, true>(p);
+  else if (p.sh == 10)
     exact_layer_body<10, kCap>(p);
   else
     exact_layer_body<0, kCap>(p);
@@ -2123,6 +2132,8 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   if (!attr) {
     set_smem_attr(k_exact_layer<kEngineRecCap>);
     set_smem_attr(k_exact_layer<kExactRecCap>);
+    set_smem_attr(k_exact_layer<kEngineRecCap, true>);
+    set_smem_attr(k_exact_layer<kExactRecCap, true>);
     attr = true;
   }
   const size_t smem = size_t(kWarps) * exact_warp_bytes(g.S, big ? kExactRecCap : kEngineRecCap);
@@ -2147,6 +2158,10 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     }
   }
   const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
+  // the specialised kernel (same block shape and shared memory) applies when the
+  // host knows the whole layer takes its one path
+  const bool fast = g.sh == 10 && coarse && probe.q_const && probe.fx_pack == 4 &&
+                    !getenv("SK_EXACT_GENERIC");
   unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
   auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
     c = std::min<unsigned long long>(c, full);
@@ -2198,7 +2213,13 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     p.xgroup = env_group ? env_group : exact_group(m, g.nW, uint64_t(grid) * kWarps);
     long long* stamp = (ctx->stamps && k0 < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
     timing_mark(ctx);
-    if (big)
+    if (big && fast)
+      SK_LAUNCH((k_exact_layer<kExactRecCap, true>), grid, kWarps * 32, smem, ctx->stream, p,
+                stamp);
+    else if (fast)
+      SK_LAUNCH((k_exact_layer<kEngineRecCap, true>), grid, kWarps * 32, smem, ctx->stream, p,
+                stamp);
+    else if (big)
       SK_LAUNCH(k_exact_layer<kExactRecCap>, grid, kWarps * 32, smem, ctx->stream, p, stamp);
     else
       SK_LAUNCH(k_exact_layer<kEngineRecCap>, grid, kWarps * 32, smem, ctx->stream, p, stamp);
