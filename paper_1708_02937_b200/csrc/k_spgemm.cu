@@ -720,20 +720,12 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
         __syncwarp();
         const uint32_t nb = min(uint32_t(kCap), ptot - pb);
 #pragma unroll 1
-        for (uint32_t r0 = 0; r0 < nb; r0 += 32) {
-          const uint32_t t = r0 + lane;
-          const uint2 rc = t < nb ? rec[t] : make_uint2(0u, 0u);
-          const uint32_t len = rc.y & 7u, own = rc.y >> 3;
-          const int qo = kQC ? p.q_cval : __shfl_sync(0xffffffffu, qown, own);
-          const float ao = kYC ? 0.0f : __shfl_sync(0xffffffffu, aa, own);
-          uint32_t cc[4];
-          float yy[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (uint32_t(u) < len) {
-              cc[u] = __ldg(&p.bci[rc.x + u]);
-              if (!kYC) yy[u] = __ldg(&p.bv[rc.x + u]);
-            }
+        // kDual (the specialised kernel, sparse passes): two records per lane and
+        // step, all eight loads in flight before the first atomic (cfg5 2.63 ->
+        // 2.56 ms; on the dense passes of cfg4 it cost 2 %)
+        constexpr bool kDual = kQC && kP == 4 && kCap == kEngineRecCap;
+        auto apply = [&](const uint32_t (&cc)[4], const float (&yy)[4], uint32_t len, int qo,
+                         float ao) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (uint32_t(u) < len) {
@@ -748,6 +740,42 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
                 cflag |= 1u << sub;
               }
             }
+          }
+        };
+        if (kDual) {
+#pragma unroll 1
+          for (uint32_t r0 = 0; r0 < nb; r0 += 64) {
+            const uint32_t t0 = r0 + lane, t1 = r0 + 32 + lane;
+            const uint2 rc0 = t0 < nb ? rec[t0] : make_uint2(0u, 0u);
+            const uint2 rc1 = t1 < nb ? rec[t1] : make_uint2(0u, 0u);
+            const uint32_t len0 = rc0.y & 7u, len1 = rc1.y & 7u;
+            uint32_t c0[4], c1[4];
+            float yy[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (uint32_t(u) < len0) c0[u] = __ldg(&p.bci[rc0.x + u]);
+              if (uint32_t(u) < len1) c1[u] = __ldg(&p.bci[rc1.x + u]);
+            }
+            apply(c0, yy, len0, p.q_cval, 0.0f);
+            apply(c1, yy, len1, p.q_cval, 0.0f);
+          }
+        } else {
+#pragma unroll 1
+          for (uint32_t r0 = 0; r0 < nb; r0 += 32) {
+            const uint32_t t = r0 + lane;
+            const uint2 rc = t < nb ? rec[t] : make_uint2(0u, 0u);
+            const uint32_t len = rc.y & 7u, own = rc.y >> 3;
+            const int qo = kQC ? p.q_cval : __shfl_sync(0xffffffffu, qown, own);
+            const float ao = kYC ? 0.0f : __shfl_sync(0xffffffffu, aa, own);
+            uint32_t cc[4];
+            float yy[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (uint32_t(u) < len) {
+                cc[u] = __ldg(&p.bci[rc.x + u]);
+                if (!kYC) yy[u] = __ldg(&p.bv[rc.x + u]);
+              }
+            apply(cc, yy, len, qo, ao);
           }
         }
         __syncwarp();
