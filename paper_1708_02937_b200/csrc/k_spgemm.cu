@@ -140,6 +140,7 @@ struct RowArgs {
   uint32_t* sc_c;
   float* sc_v;
   unsigned long long* bump;
+  unsigned int* work;          // specialised exact kernel: next item (dynamic distribution)
   unsigned long long cap;
   int* overflow;
   int* err;
@@ -874,7 +875,18 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
   for (; g < ng;) {
     const uint32_t i = rows ? rows[r] : r;
     if (kFast) {
-      process_item_exact<kLayer, 10, true, kCap, true, 4>(p, i, uint32_t(g), ws, lane);
+      // items handed out dynamically (one atomic per item): no tail of warps with
+      // heavier static shares; the order stays window-group-major for L2 reuse
+      (void)i;
+      const uint64_t total = uint64_t(ng) * nr;
+      for (;;) {
+        uint32_t it = 0;
+        if (lane == 0) it = atomicAdd(p.work, 1u);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= total) break;
+        process_item_exact<kLayer, 10, true, kCap, true, 4>(p, it % nr, it / nr, ws, lane);
+      }
+      return;
     } else if (kExact) {
       // rows whose untouched positions survive (epilogue(0 + b) != 0) need the
       // dense sweep of the float exact path
@@ -2206,7 +2218,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     uint32_t* sc_c = aalloc<uint32_t>(ctx, cap);
     float* sc_v = aalloc<float>(ctx, cap);
     uint32_t* wp_out = aalloc<uint32_t>(ctx, items + 1);
-    SK_CUDA(cudaMemsetAsync(d, 0, 16, ctx->stream));  // d[0] bump, d[1] overflow flag
+    SK_CUDA(cudaMemsetAsync(d, 0, 24, ctx->stream));  // d[0] bump, d[1] overflow, d[2] work
     RowArgs p;
     p.arp = w->rp;
     p.aci = w->ci;
@@ -2226,6 +2238,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     p.sc_c = sc_c;
     p.sc_v = sc_v;
     p.bump = d;
+    p.work = reinterpret_cast<unsigned int*>(d + 2);
     p.cap = cap;
     p.overflow = reinterpret_cast<int*>(d + 1);
     p.err = ctx->d_err;
