@@ -140,7 +140,7 @@ struct RowArgs {
   uint32_t* sc_c;
   float* sc_v;
   unsigned long long* bump;
-  unsigned int* work;          // specialised exact kernel: next item (dynamic distribution)
+  unsigned long long* work;    // standalone exact kernels: next item (dynamic distribution)
   unsigned long long cap;
   int* overflow;
   int* err;
@@ -859,7 +859,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
 // 1024-sample windows, a constant increment, four 8-bit fields, no dense rows --
 // compiled alone so its registers are not shared with the other paths
 template <typename Ops, bool kLayer, bool kExact, int kSh = 0, int kCap = kEngineRecCap,
-          bool kFast = false>
+          bool kFast = false, bool kDyn = false>
 __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
                                         uint64_t gw, uint64_t nwarps,
                                         const uint32_t* rows = nullptr, uint32_t nrows = 0) {
@@ -867,26 +867,9 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
   const uint32_t ng = (p.nW + G - 1) / G;
   const uint32_t nr = rows ? nrows : p.m;
   if (nr == 0) return;
-  // item it = g * nr + r, walked incrementally (no 64-bit division per item)
-  const uint64_t dg = nwarps / nr;
-  const uint32_t dr = uint32_t(nwarps % nr);
-  uint64_t g = gw / nr;
-  uint32_t r = uint32_t(gw % nr);
-  for (; g < ng;) {
-    const uint32_t i = rows ? rows[r] : r;
+  auto item = [&](uint32_t i, uint64_t g) {
     if (kFast) {
-      // items handed out dynamically (one atomic per item): no tail of warps with
-      // heavier static shares; the order stays window-group-major for L2 reuse
-      (void)i;
-      const uint64_t total = uint64_t(ng) * nr;
-      for (;;) {
-        uint32_t it = 0;
-        if (lane == 0) it = atomicAdd(p.work, 1u);
-        it = __shfl_sync(0xffffffffu, it, 0);
-        if (it >= total) break;
-        process_item_exact<kLayer, 10, true, kCap, true, 4>(p, it % nr, it / nr, ws, lane);
-      }
-      return;
+      process_item_exact<kLayer, 10, true, kCap, true, 4>(p, i, uint32_t(g), ws, lane);
     } else if (kExact) {
       // rows whose untouched positions survive (epilogue(0 + b) != 0) need the
       // dense sweep of the float exact path
@@ -917,6 +900,29 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
     } else {
       process_item<Ops, kLayer, false>(p, i, uint32_t(g), ws, lane);
     }
+  };
+  if (kDyn) {
+    // kDyn (standalone exact kernels): items handed out dynamically, one atomic
+    // per item, in the same window-group-major order -- no tail of warps whose
+    // static share happened to be heavier
+    const uint64_t total = uint64_t(ng) * nr;
+    for (;;) {
+      unsigned long long it = 0;
+      if (lane == 0) it = atomicAdd(p.work, 1ull);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= total) break;
+      const uint32_t r = uint32_t(it % nr);
+      item(rows ? rows[r] : r, it / nr);
+    }
+    return;
+  }
+  // item it = g * nr + r, walked incrementally (no 64-bit division per item)
+  const uint64_t dg = nwarps / nr;
+  const uint32_t dr = uint32_t(nwarps % nr);
+  uint64_t g = gw / nr;
+  uint32_t r = uint32_t(gw % nr);
+  for (; g < ng;) {
+    item(rows ? rows[r] : r, g);
     g += dg;
     r += dr;
     if (r >= nr) {
@@ -1139,7 +1145,7 @@ __device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   __syncwarp();
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  phase_a<OpArith, true, true, kSh, kCap, kFast>(p, ws, lane, gw, nw);
+  phase_a<OpArith, true, true, kSh, kCap, kFast, true>(p, ws, lane, gw, nw);
 }
 
 // kCap: piece records per batch -- 192 when an accumulator pass holds many
@@ -2238,7 +2244,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     p.sc_c = sc_c;
     p.sc_v = sc_v;
     p.bump = d;
-    p.work = reinterpret_cast<unsigned int*>(d + 2);
+    p.work = d + 2;
     p.cap = cap;
     p.overflow = reinterpret_cast<int*>(d + 1);
     p.err = ctx->d_err;
