@@ -4,12 +4,18 @@
 Default workload: BASELINE.json configs[3] ("cfg4"), the configuration the
 metric is quoted on at 1/2/4/8 GPUs: 480 layers, N = 65536 neurons, W_k with
 exactly 32 nonzeros per row (value 1/16), bias -0.35, ReLU clipped at 32,
-Y0 binary with round(0.4% * N) = 262 active neurons per sample, 60000 samples
-per GPU (batch-row sharding, replicated weights, no collective on the data
-path: weak scaling -- rank r owns samples [60000 r, 60000 (r+1)) of the
-global batch).  One step = one full 480-layer inference of the resident batch.
+Y0 binary with round(0.4% * N) = 262 active neurons per sample, ONE batch of
+60000 samples.  At N > 1 the batch is split into contiguous sample shards
+(batch-row sharding, replicated W, no collective on the data path; the
+partition is the reference's count*w/nw rule, proj/src/detail/parallel.hpp:
+29-43): strong scaling, 7500 samples per GPU at N = 8 (`--scaling weak` gives
+every GPU its own 60000 instead).  One step = one full 480-layer inference.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4|cfg3|cfg1]
+The line also carries a `sustained` object: the cfg3 network driven into its
+saturated regime (every layer does full work), because the
+BASELINE configs as specified die after 1-2 layers.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4|cfg3|cfg5|cfg1]
     python bench.py --impl reference ...   # the reference's CPU path, rank 0 only
 
 Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for every field.
@@ -36,11 +42,11 @@ WORKLOADS = {
     "cfg4": dict(m=65536, L=480, B=60000, kW=32, value=1.0 / 16, bias=-0.35, clip=32.0,
                  y0="binary", density=0.004,
                  desc="BASELINE configs[3]: 480-layer sparse DNN, N=65536, 32 nnz/row (1/16), "
-                      "bias -0.35, ReLU clip 32, Y0 binary 0.4%/sample, 60000 samples/GPU"),
+                      "bias -0.35, ReLU clip 32, Y0 binary 0.4%/sample, 60000 samples"),
     "cfg3": dict(m=16384, L=120, B=60000, kW=32, value=1.0 / 16, bias=-0.3, clip=32.0,
                  y0="binary", density=0.015,
                  desc="BASELINE configs[2]: 120-layer sparse DNN, N=16384, 32 nnz/row (1/16), "
-                      "bias -0.3, ReLU clip 32, Y0 binary 1.5%/sample, 60000 samples/GPU"),
+                      "bias -0.3, ReLU clip 32, Y0 binary 1.5%/sample, 60000 samples"),
     # Not a BASELINE config: the cfg3 network driven into its saturated regime
     # (Y0 50% ones -> every activation clips at 32 from layer 1 on), so every
     # layer carries full work.  Exercises the density-adaptive hand-off to the
@@ -49,15 +55,15 @@ WORKLOADS = {
                            clip=32.0, y0="binary", density=0.5,
                            desc="sustained-work variant of BASELINE configs[2] (NOT a BASELINE "
                                 "config): cfg3 network, Y0 binary 50%/sample -> activations "
-                                "saturate (dense) from layer 1, 60000 samples/GPU"),
+                                "saturate (dense) from layer 2, 60000 samples"),
     "cfg5": dict(m=262144, L=120, B=60000, kW=32, value=1.0 / 16, bias=-0.45, clip=32.0,
                  y0="binary", density=0.001,
                  desc="BASELINE configs[4]: 120-layer sparse DNN, N=262144, 32 nnz/row (1/16), "
-                      "bias -0.45, ReLU clip 32, Y0 binary 0.1%/sample, 60000 samples/GPU"),
+                      "bias -0.45, ReLU clip 32, Y0 binary 0.1%/sample, 60000 samples"),
     "cfg1": dict(m=1024, L=4, B=256, kW=16, value=float("nan"), bias=-0.05, clip=0.0,
                  y0="dense", density=1.0,
                  desc="BASELINE configs[0]: 4-layer sparse DNN, N=1024, 16 nnz/row U[-1,1), "
-                      "bias -0.05, Y0 dense U[0,1), batch 256/GPU"),
+                      "bias -0.05, Y0 dense U[0,1), batch 256"),
 }
 SEED = 42
 
@@ -213,26 +219,6 @@ def build_model(sk, w):
     return sk.DnnModel(Ws, [b] * w["L"]), Ws
 
 
-DENSE_ABOVE, SPARSE_BELOW = 1.0 / 32, 1.0 / 128  # library defaults (sk_ctx_set_density_switch)
-
-
-def layer_engines(trace, m, batch):
-    """Replays the density-adaptive rule of relu_forward_sparse on an nnz trace:
-    which engine ran each layer ("sparse" / "dense")."""
-    full = m * batch
-    hi, lo = max(1, int(DENSE_ABOVE * full)), int(SPARSE_BELOW * full)
-    out, dense = [], False
-    for k in range(len(trace) - 1):
-        if not dense and trace[k] > hi:
-            dense = True
-        out.append("dense" if dense else "sparse")
-        if dense and trace[k + 1] < lo:
-            dense = False
-        elif not dense and trace[k + 1] > hi:
-            dense = True
-    return out
-
-
 def sparse_layer_bytes(nnz_in, nnz_out, batch, m, nnzW):
     """8 nnz(Y_k) + 8 nnz(Y_k+1) + 8(B+1) + 4(N+1) + 8 nnz(W) + 4N."""
     return 8 * nnz_in + 8 * nnz_out + 8 * (batch + 1) + 4 * (m + 1) + 8 * nnzW + 4 * m
@@ -243,14 +229,32 @@ def dense_layer_bytes(batch, m, nnzW):
     return 8 * batch * m + 4 * (m + 1) + 8 * nnzW + 4 * m
 
 
+def useful_products(trace, paths, m, batch, nnzW, layer1_products):
+    """Multiply-adds the forward actually needs: layer 1 counted exactly
+    (sum over input neurons of out-degree x active samples), later sparse
+    layers at their expected count nnz(Y_k) nnz(W_k) / N, dense-engine layers
+    every MAC (the engine folds all of them).  Empty layers need none."""
+    tot = 0.0
+    for k in range(len(trace) - 1):
+        if k == 0 and layer1_products is not None:
+            tot += layer1_products
+        elif paths and paths[k] == "dense":
+            tot += nnzW[k] * batch
+        else:
+            tot += trace[k] * nnzW[k] / m
+    return tot
+
+
 def measured_traffic(workload):
     """Per-launch DRAM traffic of the dominant kernel from the committed ncu
-    capture (profiles/r01/traffic.json) and the unit that binds it there, or None."""
-    try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
-        return t[workload]["bytes"], t[workload]["report"], t[workload].get("limiter")
-    except Exception:
-        return None, None, None
+    capture (profiles/r02/traffic.json, else r01) and the unit that binds it."""
+    for r in ("r02", "r01"):
+        try:
+            t = json.load(open(os.path.join(ROOT, "profiles", r, "traffic.json")))
+            return t[workload]["bytes"], t[workload]["report"], t[workload].get("limiter")
+        except Exception:
+            continue
+    return None, None, None
 
 
 def peaks():
@@ -261,52 +265,68 @@ def peaks():
 
 
 # ---------------------------------------------------------------------------------------
-# reference arm: the reference's own CPU implementation (oracle/_ref)
+# the reference's CPU implementation (oracle/_ref): reference arm and cpu_baseline
 
-def cpu_reference_run(w, batch, layers_sampled, steps, warmup, workers, W_host=None):
-    """Times the reference's CPU path on `batch` samples over `layers_sampled`
-    layers: per layer the reference's mxm(CsrMatrix W_ref, CsrMatrix Y_ref)
-    (proj/src/matrix.cpp:541-547, 452-521) followed by the layer epilogue the
-    reference lacks (oracle/sk_oracle.c sko_sparse_epilogue); the dense-input
-    config uses the reference's relu_forward (proj/src/dnn.cpp:111-121)."""
+def host_weight_handles(R, P, w, cores):
+    """The L weight matrices as reference CsrMatrix handles (generated by the
+    oracle's C generators in parallel; setup, never timed)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(k):
+        x = P.gen_layer_fixed(w["m"], w["kW"], P.layer_seed(SEED, k), w["value"])
+        return R.handle(x)
+
+    with ThreadPoolExecutor(max_workers=max(1, cores)) as ex:
+        return list(ex.map(one, range(w["L"])))
+
+
+def cpu_reference_run(w, batch, steps, warmup, workers):
+    """Times the reference's CPU path on the FULL workload (`batch` samples, all
+    L layers), mirroring time_step (proj/src/bench.cpp:82-95): each step
+    restarts from Y0.  Sparse-activation configs: per layer the reference's
+    mxm(CsrMatrix W_ref, CsrMatrix Y_ref) (proj/src/matrix.cpp:541-547 ->
+    452-521) with `workers` threads, followed by the sparse epilogue the
+    reference lacks (restated in oracle/ref_capi.cpp), Y kept as a reference
+    CsrMatrix between layers.  Dense-input configs: the reference's relu_forward
+    (proj/src/dnn.cpp:111-121).  Returns (per-step seconds, per-step per-layer
+    seconds)."""
     from oracle.oracle import Port, Ref
     R, P = Ref.get(), Port.get()
     m = w["m"]
     b = np.full(m, w["bias"], np.float32)
-    if W_host is None:
-        W_host = [P.gen_layer_fixed(m, w["kW"], P.layer_seed(SEED, k), w["value"])
-                  for k in range(layers_sampled)]
-    times = []
+    times, per_layer = [], []
     if w["y0"] == "dense":
+        W_host = [P.gen_layer_fixed(m, w["kW"], P.layer_seed(SEED, k), w["value"])
+                  for k in range(w["L"])]
         y0 = P.gen_input_dense(m, batch, SEED)
         for it in range(warmup + steps):
             t0 = time.perf_counter()
-            R.relu_forward(W_host[:layers_sampled], [b] * layers_sampled, y0, workers=workers)
+            R.relu_forward(W_host, [b] * w["L"], y0, workers=workers)
             if it >= warmup:
                 times.append(time.perf_counter() - t0)
-        return times, [], W_host
-    Y0 = P.gen_input_binary(m, batch, kY_of(w), SEED)
-    hW = [R.handle(x) for x in W_host[:layers_sampled]]
-    per_layer = []
+        return times, per_layer
+    hW = host_weight_handles(R, P, w, workers)
+    hY0 = R.handle(P.gen_input_binary(m, batch, kY_of(w), SEED))
     try:
         for it in range(warmup + steps):
-            lt = []
-            t0 = time.perf_counter()
-            Y = Y0
-            for k in range(layers_sampled):
-                tl = time.perf_counter()
-                hY = R.handle(Y)
-                Z = R.take(R.mxm_csr_csr_h(hW[k], hY, workers=workers))
-                R.free(hY)
-                Y = P.sparse_epilogue(Z, b, w["clip"])
-                lt.append(time.perf_counter() - tl)
+            lt, hy = [], hY0
+            for k in range(w["L"]):
+                t0 = time.perf_counter()
+                hn = R.layer_sparse_h(hW[k], hy, b, w["clip"], workers)
+                lt.append(time.perf_counter() - t0)
+                if hy is not hY0:
+                    R.free(hy)
+                hy = hn
+            if hy is not hY0:
+                R.free(hy)
             if it >= warmup:
-                times.append(time.perf_counter() - t0)
+                times.append(sum(lt))
                 per_layer.append(lt)
     finally:
         for h in hW:
             R.free(h)
-    return times, per_layer, W_host
+        R.free(hY0)
+    return times, per_layer
 
 
 def cpu_cores():
@@ -326,50 +346,42 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_sample_plan(w):
-    """Bounded CPU sample: a slice of the batch over every layer when that
-    fits a few seconds per step, else the first 16 layers (then the empty-layer
-    cost is extrapolated and the sample string says so)."""
+def cpu_sample_desc(w, cores, per_layer):
     if w["y0"] == "dense":
-        return w["B"], w["L"]
-    return 600, min(w["L"], 16)
-
-
-def extrapolate(w, per_layer_steps, layers_sampled):
-    """Per-inference CPU time from a sampled prefix of layers: sampled layers as
-    measured, the remaining layers at the median cost of the last sampled half."""
-    tot = []
-    for lt in per_layer_steps:
-        tail = lt[layers_sampled // 2:] or lt
-        tot.append(sum(lt) + (w["L"] - layers_sampled) * statistics.median(tail))
-    return tot
+        return (f"full workload ({w['B']} samples, {w['L']} layers): reference relu_forward "
+                f"workers={cores}")
+    s = (f"full workload ({w['B']} samples, all {w['L']} layers, nothing extrapolated): per "
+         f"layer the reference's mxm(CsrMatrix,CsrMatrix) workers={cores} + the restated "
+         f"sparse epilogue (oracle/ref_capi.cpp skref_layer_sparse_h)")
+    if per_layer:
+        pl = np.mean(np.array(per_layer), axis=0) * 1e3
+        s += f"; mean ms per layer: layer 1 {pl[0]:.1f}, layer 2 {pl[1]:.1f}" if len(pl) > 1 else ""
+        if len(pl) > 2:
+            s += f", layers 3-{len(pl)} total {float(np.sum(pl[2:])):.1f}"
+    return s
 
 
 def run_reference(args, w):
+    """--impl reference: rank 0 times the reference's CPU path on the same
+    workload (the global batch, every layer); other ranks exit without work."""
     rank, _, world = env_rank()
     if rank != 0:
         return
-    batch, layers = cpu_sample_plan(w)
     cores = cpu_cores()
-    times, per_layer, _ = cpu_reference_run(w, batch, layers, args.steps, args.warmup, cores)
-    if per_layer and layers < w["L"]:
-        times = extrapolate(w, per_layer, layers)
+    times, per_layer = cpu_reference_run(w, w["B"], args.steps, args.warmup, cores)
     t = statistics.mean(times)
-    edges = edges_per_inference(w, batch)
-    value = edges / t
-    sample = (f"{batch} of {w['B']} samples/GPU, layers 1-{layers} of {w['L']} timed"
-              + (f", remaining {w['L'] - layers} layers at the median cost of layers "
-                 f"{layers // 2 + 1}-{layers}" if layers < w["L"] else "")
-              + f"; reference mxm(CsrMatrix,CsrMatrix) workers={cores} + C epilogue"
-              if w["y0"] != "dense" else f"full workload, reference relu_forward workers={cores}")
+    value = edges_per_inference(w, w["B"]) / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.scaling == "strong" else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": w["desc"], "cpu_batch": batch},
+        "config": {"workload": w["desc"], "global_batch": w["B"], "cpu_batch": w["B"],
+                   "layers": w["L"]},
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores,
-                         "kind": "reference", "sample": sample, "cpu": cpu_model()},
+                         "kind": "reference", "sample": cpu_sample_desc(w, cores, per_layer),
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -379,26 +391,145 @@ def run_reference(args, w):
 # ---------------------------------------------------------------------------------------
 # our arm
 
-def run_ours(args, w):
-    rank, local, world = env_rank()
+class Rank:
+    def __init__(self, args):
+        import torch
+        self.rank, self.local, self.world = env_rank()
+        torch.cuda.set_device(self.local)
+        self.dist = None
+        if self.world > 1 or (args.shard == "cols" and "MASTER_ADDR" in os.environ):
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+
+    def barrier(self):
+        import torch
+        if self.dist is not None:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(self, x):
+        import torch
+        t = torch.tensor([float(x)], device="cuda")
+        if self.dist is not None:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def timed_steps(R, stream, steps, fn):
+    """K steps of fn() between barriers, CUDA events on the library's stream;
+    returns the max over ranks of the elapsed ms."""
     import torch
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1 or (args.shard == "cols" and "MASTER_ADDR" in os.environ):
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    R.barrier()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    R.barrier()
+    return R.max_over_ranks(e0.elapsed_time(e1))
+
+
+def layer1_products(W0, host_rp):
+    """Exact multiply-add count of layer 1: sum over input neurons k of
+    out-degree(k) (column count of W_ref) x active samples of neuron k."""
+    ci = np.asarray(W0.col_idx(), np.int64)
+    outdeg = np.bincount(ci, minlength=len(host_rp) - 1).astype(np.float64)
+    return float(np.dot(outdeg, np.diff(host_rp.astype(np.int64)).astype(np.float64)))
+
+
+def run_sustained(sk, ctx, stream, R, args, pk, b0, Bl, Bg):
+    """The `sustained` object: the cfg3 network in its saturated regime
+    (WORKLOADS['cfg3_saturated'], not a BASELINE config), every layer full work;
+    the dense engine dominates.  Same timing rules as the headline."""
+    w = WORKLOADS["cfg3_saturated"]
+    model, Ws = build_model(sk, w)
+    nnzW = [x.nnz() for x in Ws]
+    del Ws
+    Y0 = sk.gen_input_binary(w["m"], Bl, kY_of(w), SEED, sample_offset=b0)
+    run = lambda: sk.relu_forward_sparse(model, Y0, sk.ForwardOptions(clip=w["clip"]))  # noqa
+    trace = None
+    for _ in range(3):
+        _, trace = run()
+    steps = 3
+    ctx.set_timing(True)
+    ctx.kernel_times_tagged()
+    ms = timed_steps(R, stream, steps, run) / steps
+    kt, tags = ctx.kernel_times_tagged()
+    ctx.set_timing(False)
+    paths = ctx.layer_paths(w["L"])
+    tr = [int(x) for x in trace]
+    dense_layers = paths.count("dense")
+    dense_ms = float(sum(t for t, g in zip(kt, tags) if g == "k_dense_engine")) / steps
+    byts = dense_layers * dense_layer_bytes(Bl, w["m"], nnzW[0])
+    macs = dense_layers * nnzW[0] * Bl
+    achieved = byts / (dense_ms / 1e3) / 1e9 if dense_ms > 0 else 0.0
+    fma_peak = ctx_fma_peak(sk)
+    edges = edges_per_inference(w, Bg)
+    useful = useful_products(tr, paths, w["m"], Bl, nnzW, None)
+    return {
+        "workload": w["desc"], "value": edges / (ms / 1e3), "unit": "edges/s",
+        "ms_per_step": ms, "steps": steps, "warmup": 3,
+        "useful_products_per_s": useful * (Bg / Bl) / (ms / 1e3),
+        "nnz_trace": tr[:4] + ["..."] + tr[-1:],
+        "layer_paths": {p_: paths.count(p_) for p_ in sorted(set(paths))},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "kernel": "k_dense_engine (dense-activation layers: fused SpMM + "
+                               "bias/ReLU/clip)",
+                     "algorithmic_bytes": byts, "launch_ms": dense_ms,
+                     "kernel_share_of_step": dense_ms / ms,
+                     "fp32_macs_per_s": macs / (dense_ms / 1e3) if dense_ms > 0 else 0.0,
+                     "fp32_frac": (macs / (dense_ms / 1e3)) / fma_peak if dense_ms > 0 else 0.0,
+                     "fp32_peak_macs_per_s": fma_peak,
+                     "fp32_note": "non-fused mul + add (bitwise parity): 2 FP32 pipe ops per "
+                                  "MAC; peak = SMs x 128 lanes x max SM clock / 2"},
+    }
+
+
+def ctx_fma_peak(sk):
+    """Non-fused FP32 multiply-add peak (MAC/s): 2 pipe ops per MAC."""
+    import torch
+    p = torch.cuda.get_device_properties(torch.cuda.current_device())
+    clk = 1965e6
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        clk = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM) * 1e6
+    except Exception:
+        pass
+    return p.multi_processor_count * 128 * clk / 2
+
+
+def run_ours(args, w):
+    import torch
+    R = Rank(args)
+    rank, local, world, dist = R.rank, R.local, R.world, R.dist
     import paper_1708_02937_b200 as sk
+    from paper_1708_02937_b200 import shard
     sk.set_device(local)
     ctx = sk.default_context()
-    stream = torch.cuda.current_stream()
-    ctx.set_stream(stream.cuda_stream)  # the library launches on torch's current stream
+    # a dedicated stream: the library launches on it and the timing events are
+    # recorded on it (torch's legacy default stream would map to the library's
+    # own private stream)
+    stream = torch.cuda.Stream(device=local)
+    ctx.set_stream(stream.cuda_stream)
 
-    m, L, B = w["m"], w["L"], w["B"]
+    m, L, Bg = w["m"], w["L"], w["B"]
     cols = args.shard == "cols" and w["y0"] == "binary"
+    strong = args.scaling == "strong"
+    if cols:
+        b0, Bl = 0, Bg
+    elif strong:
+        b0, Bl = shard.batch_shard(Bg, world, rank)
+    else:
+        b0, Bl = rank * Bg, Bg
+    job_batch = Bg if (cols or strong) else Bg * world
+    layer1 = None
     if cols:
         # column sharding: this rank owns output neurons [r0, r1) of every W_ref and
-        # the whole batch; one all-gather of the sparse activations per layer
-        from paper_1708_02937_b200 import shard
+        # the whole batch; one exchange of the sparse activations per layer
         dev = torch.device("cuda", local)
         r0, r1 = shard.block_range(m, world, rank)
         blocks, nnzW = [], []
@@ -408,10 +539,8 @@ def run_ours(args, w):
             blocks.append(shard.row_block(wf, r0, r1, dev))
             del wf
         bblocks = [np.full(r1 - r0, w["bias"], np.float32)] * L
-        Y0 = sk.gen_input_binary(m, B, kY_of(w), SEED)
-        # peer: one kernel per rank stores its block into every rank's next-layer
-        # buffers over NVLink (CUDA IPC); nccl: padded NCCL all-gathers
-        peer = shard.PeerExchange(m, ctx=sk.default_context()) if args.exchange == "peer" else None
+        Y0 = sk.gen_input_binary(m, Bg, kY_of(w), SEED)
+        peer = shard.PeerExchange(m, ctx=ctx) if args.exchange == "peer" else None
         run = lambda y: shard.relu_forward_sparse_colsharded(  # noqa
             blocks, bblocks, y, w["clip"], device=dev, exchange=args.exchange, peer=peer)
         host_rp, host_ci, host_v = (np.array(a) for a in Y0.extract())
@@ -419,59 +548,50 @@ def run_ours(args, w):
     elif w["y0"] == "binary":
         model, Ws = build_model(sk, w)
         nnzW = [x.nnz() for x in Ws]
-        Y0 = sk.gen_input_binary(m, B, kY_of(w), SEED, sample_offset=rank * B)
+        Y0 = sk.gen_input_binary(m, Bl, kY_of(w), SEED, sample_offset=b0)
         run = lambda y: sk.relu_forward_sparse(model, y, sk.ForwardOptions(clip=w["clip"]))  # noqa
         host_rp, host_ci, host_v = (np.array(a) for a in Y0.extract())
         nnz0 = int(host_rp[-1])
+        layer1 = layer1_products(Ws[0], host_rp)
+        del Ws
     else:
         model, Ws = build_model(sk, w)
         nnzW = [x.nnz() for x in Ws]
-        Y0 = sk.gen_input_dense(m, B, SEED)
+        Y0 = sk.gen_input_dense(m, Bl, SEED)
         run = lambda y: (sk.relu_forward(model, y, sk.ForwardOptions(clip=w["clip"])), None)  # noqa
         host_y = Y0.numpy()
-        nnz0 = m * B
+        nnz0 = m * Bl
     torch.cuda.synchronize()
     sampler = ClockSampler(local)  # NVML initialised well before the timed region
 
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # warm-up
     trace = None
     for _ in range(args.warmup):
         out, trace = run(Y0)
         del out
-    barrier()
+    R.barrier()
 
     # ---- timed region: resident inputs ----------------------------------------------
     ctx.set_timing(True)
+    ctx.kernel_times_tagged()
     launches0 = sk._lib.launches()
     if rank == 0:  # where a launch list (ncu -s) of the timed region starts
         print(f"bench: {launches0} library launches before the timed region", file=sys.stderr)
-    with sampler as clocks:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            out, trace = run(Y0)
-            del out
-        e1.record(stream)
-        barrier()
-    launches = sk._lib.launches() - launches0
-    ktimes = ctx.kernel_times_ms()
-    ms = e0.elapsed_time(e1)
-    t_local = torch.tensor([ms], device="cuda")
-    if dist is not None:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    ms_max = float(t_local.item())
-    ms_step = ms_max / args.steps
-    edges = edges_per_inference(w, B)
-    job_edges = edges if cols else world * edges  # cols: all ranks share one batch
-    value = job_edges / (ms_step / 1e3)
+    res = {}
 
+    def step():
+        out, res["trace"] = run(Y0)
+        del out
+
+    with sampler as clocks:
+        ms_max = timed_steps(R, stream, args.steps, step)
+    trace = res.get("trace", trace)
+    launches = sk._lib.launches() - launches0
+    ktimes, ktags = ctx.kernel_times_tagged()
     ctx.set_timing(False)
+    ms_step = ms_max / args.steps
+    edges = edges_per_inference(w, job_batch)
+    value = edges / (ms_step / 1e3)
+
     # ---- e2e: host buffers in, result read back, through the public API ---------------
     if w["y0"] == "binary":
         # Y0 is binary: only its pattern crosses the host link (sk_csr_from_pattern)
@@ -479,15 +599,15 @@ def run_ours(args, w):
         for a in (host_rp, host_ci):
             sk._lib.load().sk_host_register(a.ctypes.data, a.nbytes)
         h2d = host_rp.nbytes + host_ci.nbytes
-        copy_stream = torch.cuda.Stream()
+        copy_stream = torch.cuda.Stream(device=local)
+        ncols = Y0.cols()
 
         def upload():
             # on a copy stream: overlaps the forward already queued on the compute stream
-            return sk.CsrMatrix.from_pattern_async(m, B, host_rp, host_ci, 1.0,
+            return sk.CsrMatrix.from_pattern_async(m, ncols, host_rp, host_ci, 1.0,
                                                    stream=copy_stream.cuda_stream)
 
-        pending = []
-        left = [0]  # steps still to run after this one (no upload beyond the last)
+        pending, left = [], [0]  # left: steps still to run after this one
 
         def e2e_step():
             # double-buffered input: step s+1's upload is issued before step s's
@@ -515,137 +635,115 @@ def run_ours(args, w):
         e2e_step()
     if w["y0"] == "binary":
         left[0] = args.steps - 1  # the timed region uploads its own inputs
-    barrier()
+    d2h = [0]
+
+    def e2e_timed():
+        d2h[0] = e2e_step()
+
     t0 = time.perf_counter()
-    e0.record(stream)
-    d2h = 0
-    for _ in range(args.steps):
-        d2h = e2e_step()
-    e1.record(stream)
-    barrier()
-    e2e_wall = (time.perf_counter() - t0) * 1e3
-    e2e_ms = max(e0.elapsed_time(e1), e2e_wall)
-    t_e2e = torch.tensor([e2e_ms], device="cuda")
-    if dist is not None:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_step_ms = float(t_e2e.item()) / args.steps
-    e2e_value = job_edges / (e2e_step_ms / 1e3)
+    e2e_ms = timed_steps(R, stream, args.steps, e2e_timed)
+    e2e_wall = R.max_over_ranks((time.perf_counter() - t0) * 1e3)
+    e2e_step_ms = max(e2e_ms, e2e_wall) / args.steps
+    e2e_value = edges / (e2e_step_ms / 1e3)
 
     # ---- roofline of the dominant kernel ---------------------------------------------
     pk, pk_kind = peaks()
     tr = [int(x) for x in trace] if trace is not None else [nnz0] * (L + 1)
+    paths = ctx.layer_paths(L) if not cols else []
+    kt = np.array(ktimes, np.float64)
     roof = None
-    if cols and len(ktimes):
-        # per layer: this rank's block SpGEMM + epilogue (k_spgemm_rows); bytes =
-        # SURVEY §8(d) with the block's rows and weights, the full input Y_k
-        mg = r1 - r0
-        nnzb = [x.nnz() for x in blocks]
-        byts = sum(sparse_layer_bytes(tr[k], tr[k + 1] * mg // m, B, mg, nnzb[k])
-                   for k in range(L) if tr[k] > 0)
-        t_launch = float(np.sum(ktimes)) / args.steps / 1e3
-        achieved = byts / t_launch / 1e9 if t_launch > 0 else 0.0
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                "kernel": "k_spgemm_rows (per layer, this rank's output-neuron block)",
-                "algorithmic_bytes": byts, "launch_ms": t_launch * 1e3,
-                "launches_per_inference": len(ktimes) / args.steps,
-                "kernel_share_of_step": float(t_launch * 1e3 / ms_step), "peak_kind": pk_kind}
-    elif w["y0"] == "binary" and len(ktimes):
-        # Per inference: layer 1 on the order-free fixed-point path (k_exact_layer,
-        # its partial sums provably exact) when the statistics allow it, then the
-        # thin layers on expand-sort-compress, the windowed engine or the dense
-        # engine (ctx.layer_paths).  The timed launches are k_exact_layer and one
-        # per engine segment, in that order.  Algorithmic bytes per layer follow
-        # SURVEY §8(d) for the representation it ran in.
-        paths = ctx.layer_paths(L)
-        per_step = len(ktimes) // args.steps if len(ktimes) % args.steps == 0 else 0
-        path_count = {p_: paths.count(p_) for p_ in sorted(set(paths))}
-        if paths[0] == "exact" and per_step >= 1:
-            t1 = float(np.mean(ktimes[0::per_step])) / 1e3
-            b1 = sparse_layer_bytes(tr[0], tr[1], B, m, nnzW[0])
-            achieved = b1 / t1 / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                    "kernel": "k_exact_layer (layer 1: order-free fixed-point windowed SpGEMM + "
-                              "bias/ReLU/clip + prune; its partial sums provably exact)",
-                    "algorithmic_bytes": b1, "launch_ms": t1 * 1e3, "launches_per_inference": 1,
-                    "kernel_share_of_step": float(t1 * 1e3 / ms_step), "peak_kind": pk_kind,
-                    "layer_paths": path_count,
-                    "rest_of_step_ms": float(ms_step - t1 * 1e3)}
+    if len(kt):
+        by_kernel = {}
+        for t_, g_ in zip(kt, ktags):
+            by_kernel[g_] = by_kernel.get(g_, 0.0) + float(t_) / args.steps
+        dom = max(by_kernel, key=by_kernel.get)
+        t_dom = by_kernel[dom] / 1e3  # s per inference
+        if cols:
+            mg = shard.block_range(m, world, rank)[1] - shard.block_range(m, world, rank)[0]
+            nnzb = [x.nnz() for x in blocks]
+            byts = sum(sparse_layer_bytes(tr[k], tr[k + 1] * mg // m, Bl, mg, nnzb[k])
+                       for k in range(L) if tr[k] > 0)
+            desc = "this rank's output-neuron block per layer (k_exact_layer / k_spgemm_rows)"
+        elif dom == "k_exact_layer":
+            byts = sum(sparse_layer_bytes(tr[k], tr[k + 1], Bl, m, nnzW[k])
+                       for k in range(L) if paths[k] == "exact")
+            desc = ("k_exact_layer (order-free fixed-point windowed SpGEMM + bias/ReLU/clip + "
+                    "prune; its partial sums provably exact)")
+        elif dom == "k_dense_engine":
+            byts = sum(dense_layer_bytes(Bl, m, nnzW[k]) for k in range(L)
+                       if w["y0"] == "dense" or paths[k] == "dense")
+            desc = "k_dense_engine (per layer fused SpMM + bias/ReLU)"
         else:
-            eng = layer_engines(tr, m, B)
-            byts = sum((sparse_layer_bytes(tr[k], tr[k + 1], B, m, nnzW[k]) if tr[k] > 0 else 0)
-                       if eng[k] == "sparse" else dense_layer_bytes(B, m, nnzW[k])
-                       for k in range(L))
-            t_launch = float(np.sum(ktimes)) / args.steps / 1e3  # timed kernels per inference
-            achieved = byts / t_launch / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                    "kernel": "k_sparse_engine (persistent: per layer windowed SpGEMM + "
-                              "bias/ReLU/clip + prune + compaction) / k_dense_engine",
-                    "algorithmic_bytes": byts, "launch_ms": t_launch * 1e3,
-                    "launches_per_inference": len(ktimes) / args.steps,
-                    "kernel_share_of_step": float(t_launch * 1e3 / ms_step),
-                    "peak_kind": pk_kind, "layer_paths": path_count}
-    elif len(ktimes):
-        # One launch of k_dense_engine per inference (all layers, grid barriers
-        # between them): algorithmic bytes = SURVEY §8(d) dense-Y bytes per layer.
-        byts = sum(dense_layer_bytes(B, m, nnzW[k]) for k in range(L))
-        t_launch = float(np.mean(ktimes)) / 1e3
-        achieved = byts / t_launch / 1e9
+            byts = sum(sparse_layer_bytes(tr[k], tr[k + 1], Bl, m, nnzW[k])
+                       for k in range(L) if paths and paths[k] in ("engine",))
+            desc = dom
+        achieved = byts / t_dom / 1e9 if t_dom > 0 else 0.0
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                "kernel": "k_dense_engine (persistent: per layer fused SpMM + bias/ReLU)",
-                "algorithmic_bytes": byts, "launch_ms": t_launch * 1e3,
-                "kernel_share_of_step": float(t_launch * 1e3 / ms_step),
-                "peak_kind": pk_kind}
-
-    # ---- CPU baseline on rank 0 at N=1 --------------------------------------------------
-    cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        try:
-            batch, layers = cpu_sample_plan(w)
-            cores = cpu_cores()
-            times, per_layer, _ = cpu_reference_run(w, batch, layers, 1, 0, cores)
-            if per_layer and layers < L:
-                times = extrapolate(w, per_layer, layers)
-            cpu_v = edges_per_inference(w, batch) / statistics.mean(times)
-            cpu = {"value": cpu_v, "unit": "edges/s", "cores": cores, "kind": "reference",
-                   "sample": f"{batch} samples, {layers}/{L} layers timed"
-                             + (" (rest extrapolated from the empty-layer median)"
-                                if layers < L else "")
-                             + "; reference CPU path (oracle/_ref)",
-                   "cpu": cpu_model()}
-        except Exception as e:  # the reference library is test infrastructure
-            cpu = {"value": None, "unit": "edges/s", "cores": cpu_cores(), "kind": "reference",
-                   "sample": f"unavailable: {type(e).__name__}: {e}"}
-
-    if roof is not None:
+                "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": desc,
+                "algorithmic_bytes": byts, "launch_ms": t_dom * 1e3,
+                "kernel_share_of_step": float(t_dom * 1e3 / ms_step), "peak_kind": pk_kind,
+                "timed_kernels_ms_per_step": by_kernel,
+                "rest_of_step_ms": float(ms_step - t_dom * 1e3)}
+        if paths:
+            roof["layer_paths"] = {p_: paths.count(p_) for p_ in sorted(set(paths))}
         tb, trep, lim = measured_traffic(args.workload)
         roof["traffic"] = tb
         roof["traffic_source"] = trep
         if lim is not None and not cols:
             roof["measured_limiter"] = lim
+    useful = useful_products(tr, paths, m, Bl, nnzW, layer1) if not cols else None
+
+    # ---- sustained-work variant ---------------------------------------------------------
+    sustained = None
+    if args.sustained and w["y0"] == "binary" and not cols:
+        del model
+        sustained = run_sustained(sk, ctx, stream, R, args, pk, b0, Bl, Bg)
+
+    # ---- CPU baseline on rank 0 at N=1: the reference on the full workload -------------
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            cores = cpu_cores()
+            times, per_layer = cpu_reference_run(w, Bg, 1, 0, cores)
+            cpu = {"value": edges_per_inference(w, Bg) / statistics.mean(times),
+                   "unit": "edges/s", "cores": cores, "kind": "reference",
+                   "sample": "one step of the " + cpu_sample_desc(w, cores, per_layer),
+                   "ms_per_step": statistics.mean(times) * 1e3, "cpu": cpu_model()}
+        except Exception as e:  # the reference library is test infrastructure
+            cpu = {"value": None, "unit": "edges/s", "cores": cpu_cores(), "kind": "reference",
+                   "sample": f"unavailable: {type(e).__name__}: {e}"}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong" if cols else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if (cols or strong) else "weak",
+            "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded SplitMix64; BASELINE shapes/distributions)",
             "config": {"workload": w["desc"], "neurons": m, "layers": L,
-                       "per_gpu_batch": B if not cols else B, "global_batch": B if cols else B * world,
-                       "edges_per_inference_per_gpu": edges if not cols else edges // world,
+                       "global_batch": job_batch, "per_gpu_batch": Bl,
+                       "edges_per_inference": edges,
                        "parallelism": (f"column-sharded W x{world}, per-layer exchange of the "
                                        f"sparse activations ({args.exchange})" if cols else
-                                       f"batch-row x{world}, replicated W, no data-path collective"),
+                                       f"batch-row x{world} ({'strong' if strong else 'weak'}: "
+                                       f"{Bl} samples/GPU), replicated W, no data-path "
+                                       f"collective"),
                        "l2": "inputs larger than L2 (W %.2f GB + Y0 %.0f MB vs 126 MB L2)"
                              % (sum(nnzW) * 8 / 1e9, nnz0 * 8 / 1e6)},
             "nnz_trace": ([int(x) for x in trace[:6]] + (["..."] if len(trace) > 6 else [])
                           + [int(trace[-1])]) if trace is not None else None,
+            "useful_products_per_s": (useful * (job_batch / Bl) / (ms_step / 1e3)
+                                      if useful is not None else None),
+            "useful_products_note": ("edges/s counts every nominal MAC nnz(W)·B·L; the network "
+                                     "as specified dies after 1-2 layers (SURVEY F5), so this "
+                                     "counts the multiply-adds the forward needs (layer 1 exact, "
+                                     "later layers nnz(Y_k)·nnz(W_k)/N); see `sustained` for a "
+                                     "workload where every layer works"),
             "roofline": roof,
+            "sustained": sustained,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step_ms,
+                    "d2h_bytes_per_step": int(d2h[0]), "ms_per_step": e2e_step_ms,
                     "input_upload": ("double-buffered: step s+1's pattern upload (copy stream, "
                                      "sk_csr_from_pattern_async) overlaps step s's forward; "
                                      "every step's upload and result read inside the timed "
@@ -667,11 +765,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1 batch-row sharding: split the one global batch (strong, "
+                         "BASELINE cfg4) or give every GPU its own full batch (weak)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sustained", dest="sustained", action="store_false",
+                    help="skip the sustained-work (saturated cfg3) object")
     ap.add_argument("--shard", default="rows", choices=["rows", "cols"],
                     help="N>1 decomposition: batch-row sharding with replicated W (default, no "
                          "data-path collective) or column sharding of W_k with a per-layer "
-                         "NCCL all-gather of the sparse activations (BASELINE cfg5's layout)")
+                         "exchange of the sparse activations (BASELINE cfg5's layout)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="--shard cols: per-layer exchange of the sparse row blocks by peer-memory "
                          "stores (one kernel per rank, CUDA IPC over NVLink) or padded NCCL "

@@ -88,6 +88,11 @@ sk_status sk_ctx_synchronize(sk_ctx* ctx);
  * their durations in ms (synchronising) and resets the list. */
 sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable);
 sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count);
+/* Same, plus which kernel each timed launch was (SK_KT_*). */
+enum { SK_KT_OTHER = 0, SK_KT_EXACT = 1, SK_KT_ENGINE = 2, SK_KT_DENSE_ENGINE = 3,
+       SK_KT_SPMM = 4, SK_KT_GEMM_TC = 5, SK_KT_SPGEMM = 6 };
+sk_status sk_ctx_kernel_times_tagged(sk_ctx* ctx, float* ms, int* tags, size_t cap,
+                                     size_t* count);
 /* With timing enabled, the sparse engine writes %globaltimer (ns) at the start
  * (entry 0) and at the end of every layer (entry k+1) of the last forward. */
 sk_status sk_ctx_layer_stamps(sk_ctx* ctx, long long* ns, size_t n);
@@ -107,6 +112,48 @@ sk_status sk_ctx_layer_paths(sk_ctx* ctx, unsigned char* paths, size_t n);
  * Defaults 1/32 and 1/128.  No reference counterpart (the reference's
  * activation type is fixed by the caller, dnn.hpp:77-78). */
 sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double sparse_below);
+/* Per-context kernel selection (no reference counterpart; the reference has a
+ * single code path).  Every choice computes the same ascending fold bit for
+ * bit, so these only select WHICH kernel variant runs -- the parity tests force
+ * each one.  0 in any integer field means "automatic" (the default).
+ *   exact          1 (default) provably exact layers take the order-free kernel
+ *                  (k_exact_layer); -1 never (windowed engine / ESC instead)
+ *   exact_kernel   1 the generic k_exact_layer; 2 the specialised kernel
+ *                  (taken only where its preconditions hold: 1024-sample
+ *                  windows, constant increment, four 8-bit fields, every bias
+ *                  <= 0 -- otherwise the generic kernel runs)
+ *   exact_group    4, 8, 16, 32 or 64 windows per exact-layer work item
+ *   exact_records  64 or 192 piece records per batch
+ *   window_log2    8..12: sample window of the windowed engine (default 10)
+ *   exact_window_log2  8..12: sample window of the exact layer (default 10)
+ *   esc            1 (default) thin layers take expand-sort-compress; -1 never
+ *   esc_ratio      products per (row, window) below which ESC applies
+ *                  (<= 0: default 8) */
+typedef struct sk_tuning {
+  int exact;
+  int exact_kernel;
+  int exact_group;
+  int exact_records;
+  int window_log2;
+  int exact_window_log2;
+  int esc;
+  double esc_ratio;
+} sk_tuning;
+sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t);
+sk_status sk_ctx_get_tuning(const sk_ctx* ctx, sk_tuning* t);
+/* What the last exact-layer launch on this context ran (introspection for the
+ * parity tests): launches = exact-layer launches since the context was created;
+ * kernel 1 generic / 2 specialised; group = windows per item; records = piece
+ * records per batch; window_log2; fields = accumulator fields per word. */
+typedef struct sk_exact_info {
+  uint64_t launches;
+  int kernel;
+  int group;
+  int records;
+  int window_log2;
+  int fields;
+} sk_exact_info;
+sk_status sk_ctx_last_exact(const sk_ctx* ctx, sk_exact_info* info);
 /* Page-lock / unlock a caller host buffer for async copies. */
 sk_status sk_host_register(void* p, size_t bytes);
 sk_status sk_host_unregister(void* p);

@@ -130,6 +130,9 @@ class Ref:
         L.skref_format_matrix.argtypes = [vp_, C.c_uint32, C.c_uint32, vp_, C.c_char_p, sz,
                                           C.POINTER(sz)]
         L.skref_to_dense.argtypes = [C.c_void_p, C.c_float, f32p]
+        L.skref_layer_sparse_h.argtypes = [vp_, vp_, f32p, C.c_float, C.c_int,
+                                           C.POINTER(vp_)]
+        L.skref_csr_nnz.argtypes = [vp_]
 
     def _check(self, rc):
         if rc != 0:
@@ -171,6 +174,19 @@ class Ref:
         h = C.c_void_p()
         self._check(self.lib.skref_mxm_csr_csr(ha, hb, 0, workers, C.byref(h)))
         return h
+
+    def layer_sparse_h(self, hw, hy, bias, clip=0.0, workers=1):
+        """One sparse-activation layer on reference handles: the reference's
+        mxm(W_ref, Y_ref) + the restated epilogue (ref_capi.cpp).  Returns a new
+        handle (the caller frees it)."""
+        bias = np.ascontiguousarray(bias, np.float32)
+        h = C.c_void_p()
+        self._check(self.lib.skref_layer_sparse_h(hw, hy, _p(bias, f32p), clip, workers,
+                                                  C.byref(h)))
+        return h
+
+    def nnz_h(self, h) -> int:
+        return int(self.lib.skref_csr_nnz(h))
 
     def csr_from_triples(self, rows, cols, r, c, v) -> Csr:
         r = np.ascontiguousarray(r, np.uint32)

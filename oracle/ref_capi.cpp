@@ -5,7 +5,11 @@
 // exists so that Python tests, the golden-fixture generator and bench.py's
 // reference arm can call the reference's own hot-path functions through
 // ctypes.  Every function below forwards to the reference API named in its
-// comment; nothing here re-implements arithmetic.
+// comment; the one exception is skref_layer_sparse_h, which follows the
+// reference's mxm(CsrMatrix, CsrMatrix) with the sparse-activation layer
+// epilogue the reference has no function for (restated exactly as
+// oracle/sk_oracle.c sko_sparse_epilogue: z = Z + b_i -> ReLU select -> clip ->
+// prune, untouched positions give epilogue(0 + b_i)).
 //
 // Reference interfaces wrapped (paths relative to /root/reference):
 //   csr_from_triples            proj/include/semikern/matrix.hpp:144-150
@@ -183,6 +187,54 @@ int skref_mxm_csr_csr(const skref_csr* a, const skref_csr* b, int semiring,
                       int workers, skref_csr** out) {
   return guarded([&] {
     *out = new skref_csr{mxm(a->m, b->m, semiring_of(semiring), workers)};
+  });
+}
+
+// One sparse-activation layer on reference handles (bench.py's reference arm):
+// Z = mxm(W_ref, Y_ref) (proj/src/matrix.cpp:541-547 -> 452-521, the
+// reference's own Gustavson SpGEMM, `workers` threads), then the restated
+// epilogue; the result is a reference CsrMatrix (validating constructor,
+// matrix.hpp:84-89) so layers chain without leaving the reference's types.
+int skref_layer_sparse_h(const skref_csr* w, const skref_csr* y, const float* bias,
+                         float clip, int workers, skref_csr** out) {
+  return guarded([&] {
+    const CsrMatrix z = mxm(w->m, y->m, arithmetic_semiring(), workers);
+    const uint32_t m = z.rows(), n = z.cols();
+    auto epi = [clip](float acc, float b) {
+      float v = acc + b;
+      v = (v < 0.0f) ? 0.0f : v;
+      if (clip > 0.0f) v = (v > clip) ? clip : v;
+      return v;
+    };
+    std::vector<index_t> rp(size_t(m) + 1, 0), ci;
+    std::vector<Scalar> v;
+    const auto zrp = z.row_ptr();
+    const auto zci = z.col_idx();
+    const auto zv = z.values();
+    for (uint32_t i = 0; i < m; ++i) {
+      const float untouched = epi(0.0f, bias[i]);
+      size_t q = zrp[i];
+      const size_t qe = zrp[i + 1];
+      if (untouched == 0.0f) {
+        for (; q < qe; ++q) {
+          const float o = epi(zv[q], bias[i]);
+          if (o != 0.0f) {
+            ci.push_back(zci[q]);
+            v.push_back(o);
+          }
+        }
+      } else {
+        for (uint32_t s = 0; s < n; ++s) {
+          const float o = (q < qe && zci[q] == s) ? epi(zv[q++], bias[i]) : untouched;
+          if (o != 0.0f) {
+            ci.push_back(s);
+            v.push_back(o);
+          }
+        }
+      }
+      rp[i + 1] = index_t(ci.size());
+    }
+    *out = new skref_csr{CsrMatrix(m, n, std::move(rp), std::move(ci), std::move(v))};
   });
 }
 

@@ -26,6 +26,7 @@ EXPORTS = [
     "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_stream", "sk_ctx_stream",
     "sk_ctx_synchronize", "sk_ctx_set_timing", "sk_ctx_kernel_times",
     "sk_ctx_layer_stamps", "sk_ctx_layer_paths", "sk_ctx_set_density_switch",
+    "sk_ctx_set_tuning", "sk_ctx_get_tuning", "sk_ctx_last_exact",
     "sk_host_register", "sk_host_unregister",
     "sk_dense_create", "sk_dense_upload", "sk_dense_write", "sk_dense_download",
     "sk_dense_download_async", "sk_dense_shape", "sk_dense_device_ptr",
@@ -50,6 +51,17 @@ EXPORTS = [
 
 class FwdOpts(C.Structure):
     _fields_ = [("workers", C.c_int), ("materialize_bias", C.c_int), ("clip", C.c_float)]
+
+
+class Tuning(C.Structure):  # sk_tuning
+    _fields_ = [("exact", C.c_int), ("exact_kernel", C.c_int), ("exact_group", C.c_int),
+                ("exact_records", C.c_int), ("window_log2", C.c_int),
+                ("exact_window_log2", C.c_int), ("esc", C.c_int), ("esc_ratio", C.c_double)]
+
+
+class ExactInfo(C.Structure):  # sk_exact_info
+    _fields_ = [("launches", C.c_uint64), ("kernel", C.c_int), ("group", C.c_int),
+                ("records", C.c_int), ("window_log2", C.c_int), ("fields", C.c_int)]
 
 
 _lib = None
@@ -80,9 +92,14 @@ def load() -> C.CDLL:
     L.sk_ctx_set_stream.argtypes = [vp, vp]
     L.sk_ctx_set_timing.argtypes = [vp, C.c_int]
     L.sk_ctx_kernel_times.argtypes = [vp, f32p, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.sk_ctx_kernel_times_tagged.argtypes = [vp, f32p, C.POINTER(C.c_int), C.c_size_t,
+                                             C.POINTER(C.c_size_t)]
     L.sk_ctx_layer_stamps.argtypes = [vp, C.POINTER(C.c_longlong), C.c_size_t]
     L.sk_ctx_layer_paths.argtypes = [vp, C.POINTER(C.c_ubyte), C.c_size_t]
     L.sk_ctx_set_density_switch.argtypes = [vp, C.c_double, C.c_double]
+    L.sk_ctx_set_tuning.argtypes = [vp, C.POINTER(Tuning)]
+    L.sk_ctx_get_tuning.argtypes = [vp, C.POINTER(Tuning)]
+    L.sk_ctx_last_exact.argtypes = [vp, C.POINTER(ExactInfo)]
     L.sk_host_register.argtypes = [vp, C.c_size_t]
     L.sk_host_unregister.argtypes = [vp]
     L.sk_dense_create.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_float, C.POINTER(vp)]

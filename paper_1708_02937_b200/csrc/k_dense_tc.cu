@@ -569,31 +569,7 @@ __global__ void __launch_bounds__(6 * 32, 1)
 void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t M, uint32_t K,
                           uint32_t N, const float* bias, int relu, float* c) {
   if (M == 0 || N == 0) return;
-  static bool attr = false;
-  if (!attr) {
-    SK_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32x3<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Cfg<32>::kSmemBytes));
-    SK_CUDA(cudaFuncSetAttribute(tc::k_gemm_tf32x3<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Cfg<16>::kSmemBytes));
-    attr = true;
-  }
-  static const int bk = [] {
-    const char* e = getenv("SK_TC_BK");
-    return (e && atoi(e) == 32) ? 32 : 16;
-  }();
-  dim3 grid(ceil_div(N, tc::BN), ceil_div(M, tc::BM));
-  tc::TcParams tp{tc::kA_LBO, tc::kA_SBO, tc::kB_LBO, tc::kB_SBO,
-                  tc::idesc_tf32(tc::BM, tc::BN), 0};
-  if (const char* e = getenv("SK_TC_DBG")) {  // "a_lbo,a_sbo,b_lbo,b_sbo,idesc_hex,mode"
-    unsigned v[6] = {0, 0, 0, 0, 0, 0};
-    if (sscanf(e, "%u,%u,%u,%u,%x,%u", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]) >= 5)
-      tp = tc::TcParams{v[0], v[1], v[2], v[3], v[4], v[5]};
-  }
-  static const int ver = [] {
-    const char* e = getenv("SK_TC_VER");
-    return e ? atoi(e) : 3;
-  }();
-  if (ver == 3 && !getenv("SK_TC_DBG")) {
+  {
     // v3 kernel: pack (split once) + bulk-copy pipeline
     constexpr int BNp = 256, NSp = 4;
     using G = tc::Cfg3<BNp, NSp>;
@@ -604,13 +580,8 @@ void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t 
     float* alo = ahi + size_t(Mp) * Kp;
     float* bhi = alo + size_t(Mp) * Kp;
     float* blo = bhi + size_t(Np) * Kp;
-    static bool a3 = false;
-    if (!a3) {
-      SK_CUDA(cudaFuncSetAttribute(tc::k_gemm_packed<BNp, NSp>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
-      a3 = true;
-    }
-    timing_mark(ctx);
+    smem_attr(ctx, tc::k_gemm_packed<BNp, NSp>, int(G::kSmem));
+    timing_mark(ctx, SK_KT_GEMM_TC);
     const uint64_t wa = uint64_t(Mp / 32) * (Kp / tc::kPK), wb = uint64_t(Np / 32) * (Kp / tc::kPK);
     SK_LAUNCH(tc::k_pack_split,
               unsigned(std::min<uint64_t>((wa + 7) / 8, uint64_t(ctx->num_sms) * 16)), 256, 0,
@@ -623,16 +594,7 @@ void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t 
               bhi, blo, M, N, Kp / tc::kPK, bias, relu, c);
     timing_mark(ctx);
     dfree(ctx, buf);
-    return;
   }
-  timing_mark(ctx);
-  if (bk == 32)
-    SK_LAUNCH(tc::k_gemm_tf32x3<32>, grid, tc::kThreads, tc::Cfg<32>::kSmemBytes, ctx->stream, a,
-              b, M, K, N, bias, relu, c, tp);
-  else
-    SK_LAUNCH(tc::k_gemm_tf32x3<16>, grid, tc::kThreads, tc::Cfg<16>::kSmemBytes, ctx->stream, a,
-              b, M, K, N, bias, relu, c, tp);
-  timing_mark(ctx);
 }
 
 }  // namespace sk

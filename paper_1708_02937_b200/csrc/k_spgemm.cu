@@ -1290,7 +1290,7 @@ struct EngineArgs {
   int debug_phases;                // record g_phase_ts for layer 0
   const ValueStats* wstats;        // per layer
   const ValueStats* y0stats;       // of Y0's values
-  int exact_ok;                    // layer 0 may use the order-free path (SK_NO_EXACT unset)
+  int exact_ok;                    // layer 0 may use the order-free path (sk_tuning.exact >= 0)
   unsigned long long stop_above;   // stop after a layer with more entries (0 = never)
   int* layers_done;                // written when stopping early
   // Frontier path for near-empty inputs (bias_nonpos layers): bitmap of input
@@ -1621,15 +1621,10 @@ struct WinGeom {
   uint32_t S, nW;
 };
 
-static WinGeom geometry(uint32_t n) {
-  // 1024-sample windows by default (SK_WINDOW_LOG2 overrides, 8..12, for tuning);
+static WinGeom geometry(const sk_ctx* ctx, uint32_t n) {
+  // 1024-sample windows by default (sk_tuning.window_log2 selects 8..12);
   // small batches use one smaller window
-  static const int env_sh = [] {
-    const char* e = getenv("SK_WINDOW_LOG2");
-    const int v = e ? atoi(e) : 10;
-    return (v >= 8 && v <= 12) ? v : 10;
-  }();
-  int sh = env_sh;
+  int sh = ctx->tune.window_log2 ? ctx->tune.window_log2 : 10;
   while (sh > 7 && (1u << (sh - 1)) >= n) --sh;
   WinGeom g;
   g.sh = sh;
@@ -1655,21 +1650,10 @@ static uint32_t* build_wp(sk_ctx* ctx, const sk_csr* b, const WinGeom& g, bool a
   return wp;
 }
 
-template <typename K>
-static void set_smem_attr(K kernel) {
-  SK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-}
-
 template <typename Ops, bool kLayer>
 static void launch_rows(sk_ctx* ctx, const RowArgs& p, uint32_t m, size_t smem) {
-  static bool attr = false;
-  if (!attr) {
-    set_smem_attr(k_spgemm_rows<Ops, kLayer>);
-    attr = true;
-  }
-  int per_sm = 1;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spgemm_rows<Ops, kLayer>,
-                                                        kWarps * 32, smem));
+  smem_attr(ctx, k_spgemm_rows<Ops, kLayer>);
+  const int per_sm = occupancy(ctx, k_spgemm_rows<Ops, kLayer>, kWarps * 32, smem);
   const unsigned grid = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>((m + kWarps - 1) / kWarps, uint64_t(ctx->num_sms) * std::max(1, per_sm))));
   SK_LAUNCH((k_spgemm_rows<Ops, kLayer>), grid, kWarps * 32, smem, ctx->stream, p, m);
@@ -1685,7 +1669,7 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
     SK_CUDA(cudaMemsetAsync(o->rp, 0, (size_t(m) + 1) * 4, ctx->stream));
     return o;
   }
-  const WinGeom g = geometry(n);
+  const WinGeom g = geometry(ctx, n);
   arena_begin(ctx);  // temporaries from the context arena; the output is right-sized
   struct ArenaScope {
     sk_ctx* c;
@@ -1751,7 +1735,7 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   p.q_cval = 0;
   const size_t smem = block_smem(g);
   if (d_bias) {
-    timing_mark(ctx);  // the dominant kernel of a sparse layer (column-sharded forward)
+    timing_mark(ctx, SK_KT_SPGEMM);  // the dominant kernel of a sparse layer (column-sharded forward)
     launch_rows<OpArith, true>(ctx, p, m, smem);
     timing_mark(ctx);
   } else {
@@ -1808,7 +1792,7 @@ sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, con
     SK_CUDA(cudaMemsetAsync(o->rp, 0, (size_t(w->rows) + 1) * 4, ctx->stream));
     return o;
   }
-  if (!getenv("SK_NO_EXACT") && y->nnz && w->rows && y->cols) {
+  if (ctx->tune.exact >= 0 && y->nnz && w->rows && y->cols) {
     const ValueStats ws = weight_stats(ctx, w);
     const ValueStats ys = host_value_stats(ctx, y);
     if (products_exact(ws, ys)) {
@@ -1892,16 +1876,15 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
                               unsigned long long* trace_out, uint32_t* done,
                               const uint32_t* wp_in = nullptr) {
   const uint32_t m = md->neurons, n = y0->cols, Lm = md->layers, L = Lm - k0;
-  const WinGeom g = geometry(n);
+  const WinGeom g = geometry(ctx, n);
   const uint64_t items = uint64_t(m) * g.nW;
   const uint64_t full = uint64_t(m) * n;
   auto* mm = const_cast<sk_model*>(md);
 
   // Layer 0 may take the order-free path when its products are provably exact
-  // (decided on the device from the value statistics); SK_NO_EXACT=1 disables
-  // it for A/B measurements.
-  static const int exact_env = getenv("SK_NO_EXACT") ? 0 : 1;
-  const int exact_ok = exact_env;
+  // (decided on the device from the value statistics); sk_tuning.exact = -1 disables
+  // it (sk_tuning.exact = -1).
+  const int exact_ok = ctx->tune.exact >= 0 ? 1 : 0;
   ValueStats* y0stats = aalloc<ValueStats>(ctx, 1);
   {
     const ValueStats init SK_VALUESTATS_INIT;
@@ -1924,15 +1907,9 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
   // An early stop must leave a complete CSR, so the capacity covers the threshold.
   if (stop_above) cap = clamp_cap(std::max<unsigned long long>(cap, 2 * stop_above));
 
-  static bool attr = false;
-  if (!attr) {
-    set_smem_attr(k_sparse_engine);
-    attr = true;
-  }
+  smem_attr(ctx, k_sparse_engine);
   const size_t smem = block_smem(g);
-  int per_sm = 0;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sparse_engine, kWarps * 32,
-                                                        smem));
+  const int per_sm = occupancy(ctx, k_sparse_engine, kWarps * 32, smem);
   if (per_sm < 1) fail(SK_ERR_CUDA, "sparse engine does not fit on an SM");
   const unsigned grid = unsigned(ctx->num_sms * per_sm);
 
@@ -1987,7 +1964,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     p.overflow = flags;
     p.err = ctx->d_err;
     p.stamps = (ctx->stamps && k0 + L < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
-    p.debug_phases = getenv("SK_DEBUG_PHASES") ? 1 : 0;
+    p.debug_phases = 0;
     p.wstats = static_cast<const ValueStats*>(mm->d_wstats) + k0;
     p.y0stats = y0stats;
     p.exact_ok = exact_ok;
@@ -1998,11 +1975,10 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
     p.frontier = frontier;
     p.nfront = nfront;
     void* args[] = {&p};
-    timing_mark(ctx);
+    timing_mark(ctx, SK_KT_ENGINE);
     SK_CUDA(cudaLaunchCooperativeKernel((void*)k_sparse_engine, dim3(grid), dim3(kWarps * 32),
                                         args, smem, ctx->stream));
-    static const int dbg_phases = getenv("SK_DEBUG_PHASES") ? 1 : 0;
-    if (dbg_phases) {
+    if (p.debug_phases) {
       long long ts[16];
       SK_CUDA(cudaMemcpyFromSymbolAsync(ts, g_phase_ts, sizeof(ts), 0, cudaMemcpyDeviceToHost,
                                         ctx->stream));
@@ -2109,14 +2085,9 @@ static ValueStats weight_stats(sk_ctx* ctx, const sk_csr* w) {
 // Layer k0 on the order-free path as a standalone kernel (k_exact_layer), then
 // the count scan and the gather: the output CSR and its window table (for the
 // engine that continues from layer k0 + 1).
-static WinGeom exact_geometry(uint32_t n) {
-  // the exact layer's own window (SK_EXACT_WINDOW_LOG2 overrides, 8..12)
-  static const int env_sh = [] {
-    const char* e = getenv("SK_EXACT_WINDOW_LOG2");
-    const int v = e ? atoi(e) : 10;
-    return (v >= 8 && v <= 12) ? v : 10;
-  }();
-  int sh = env_sh;
+static WinGeom exact_geometry(const sk_ctx* ctx, uint32_t n) {
+  // the exact layer's own window (sk_tuning.exact_window_log2 selects 8..12)
+  int sh = ctx->tune.exact_window_log2 ? ctx->tune.exact_window_log2 : 10;
   while (sh > 7 && (1u << (sh - 1)) >= n) --sh;
   WinGeom g;
   g.sh = sh;
@@ -2145,8 +2116,8 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   const sk_csr* w = L_.w;
   const uint32_t m = w->rows, n = y0->cols;
   const uint32_t k0 = L_.stamp_layer;
-  const WinGeom g = exact_geometry(n);
-  const bool same_geometry = g.sh == geometry(n).sh;
+  const WinGeom g = exact_geometry(ctx, n);
+  const bool same_geometry = g.sh == geometry(ctx, n).sh;
   const uint64_t items = uint64_t(m) * g.nW;
   const uint64_t full = uint64_t(m) * n;
   // products per accumulator pass (mean in-degree x mean input row x P*S/n)
@@ -2173,41 +2144,21 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   const double per_pass = double(w->nnz) / double(std::max<uint32_t>(1, m)) *
                           double(y0->nnz) / double(std::max<uint32_t>(1, y0->rows)) *
                           double(probe.fx_pack) * double(g.S) / double(std::max<uint32_t>(1, n));
-  const bool big = per_pass > 200.0;
-  static bool attr = false;
-  if (!attr) {
-    set_smem_attr(k_exact_layer<kEngineRecCap>);
-    set_smem_attr(k_exact_layer<kExactRecCap>);
-    set_smem_attr(k_exact_layer<kEngineRecCap, true>);
-    set_smem_attr(k_exact_layer<kExactRecCap, true>);
-    attr = true;
-  }
+  const bool big = ctx->tune.exact_records ? ctx->tune.exact_records == kExactRecCap
+                                            : per_pass > 200.0;
   const size_t smem = size_t(kWarps) * exact_warp_bytes(g.S, big ? kExactRecCap : kEngineRecCap);
-  // occupancy per (variant, shared memory): a driver query, cached (host time
-  // between launches is GPU idle time)
-  static std::mutex occ_mu;
-  static std::map<std::pair<int, size_t>, int> occ;
-  int per_sm = 0;
-  {
-    std::lock_guard<std::mutex> lk(occ_mu);
-    auto it = occ.find({big ? 1 : 0, smem});
-    if (it != occ.end()) {
-      per_sm = it->second;
-    } else {
-      if (big)
-        SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, k_exact_layer<kExactRecCap>, kWarps * 32, smem));
-      else
-        SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, k_exact_layer<kEngineRecCap>, kWarps * 32, smem));
-      occ[{big ? 1 : 0, smem}] = per_sm;
-    }
-  }
-  const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
   // the specialised kernel (same block shape and shared memory) applies when the
-  // host knows the whole layer takes its one path
+  // host knows the whole layer takes its one path (sk_tuning.exact_kernel = 1
+  // keeps the generic kernel)
   const bool fast = g.sh == 10 && coarse && probe.q_const && probe.fx_pack == 4 &&
-                    !getenv("SK_EXACT_GENERIC");
+                    ctx->tune.exact_kernel != 1;
+  const void* kern =
+      big ? (fast ? (const void*)k_exact_layer<kExactRecCap, true> : (const void*)k_exact_layer<kExactRecCap>)
+          : (fast ? (const void*)k_exact_layer<kEngineRecCap, true> : (const void*)k_exact_layer<kEngineRecCap>);
+  kernel_smem_attr(ctx, kern, 200 * 1024);
+  // occupancy per (variant, shared memory): a driver query, cached per device
+  const int per_sm = kernel_occupancy(ctx, kern, kWarps * 32, smem);
+  const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
   unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
   auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
     c = std::min<unsigned long long>(c, full);
@@ -2252,14 +2203,16 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     p.wpc = wpc;
     p.nWc = gc.nW;
     p.wpc_lp = plp;
-    static const uint32_t env_group = [] {  // SK_EXACT_GROUP=4|8|16|32|64 (A/B measurements)
-      const char* e = getenv("SK_EXACT_GROUP");
-      const int v = e ? atoi(e) : 0;
-      return (v == 4 || v == 8 || v == 16 || v == 32 || v == 64) ? uint32_t(v) : 0u;
-    }();
-    p.xgroup = env_group ? env_group : exact_group(m, g.nW, uint64_t(grid) * kWarps);
+    p.xgroup = ctx->tune.exact_group ? uint32_t(ctx->tune.exact_group)
+                                     : exact_group(m, g.nW, uint64_t(grid) * kWarps);
+    ctx->last_exact.launches += 1;
+    ctx->last_exact.kernel = fast ? 2 : 1;
+    ctx->last_exact.group = int(p.xgroup);
+    ctx->last_exact.records = big ? kExactRecCap : kEngineRecCap;
+    ctx->last_exact.window_log2 = g.sh;
+    ctx->last_exact.fields = int(p.fx_pack);
     long long* stamp = (ctx->stamps && k0 < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
-    timing_mark(ctx);
+    timing_mark(ctx, SK_KT_EXACT);
     if (big && fast)
       SK_LAUNCH((k_exact_layer<kExactRecCap, true>), grid, kWarps * 32, smem, ctx->stream, p,
                 stamp);
@@ -2344,17 +2297,11 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
   unsigned long long* counts = nullptr;
   uint32_t k = 0;
   uint32_t* pending_wp = nullptr;  // window table of cur from the exact layer (arena)
-  static const int exact_env = getenv("SK_NO_EXACT") ? 0 : 1;
-  // expand-sort-compress for thin layers (SK_ESC=0 disables, SK_ESC_RATIO sets the
-  // products-per-item limit; A/B measurements)
-  static const int esc_env = [] {
-    const char* e = getenv("SK_ESC");
-    return e && atoi(e) == 0 ? 0 : 1;
-  }();
-  static const double esc_ratio = [] {
-    const char* e = getenv("SK_ESC_RATIO");
-    return e ? atof(e) : 8.0;
-  }();
+  const int exact_env = ctx->tune.exact >= 0 ? 1 : 0;
+  // expand-sort-compress for thin layers (sk_tuning.esc = -1 disables, esc_ratio
+  // sets the products-per-item limit)
+  const int esc_env = ctx->tune.esc >= 0 ? 1 : 0;
+  const double esc_ratio = ctx->tune.esc_ratio > 0 ? ctx->tune.esc_ratio : 8.0;
   arena_begin(ctx);  // every temporary of this call comes from the context's arena
   auto cleanup = [&] { arena_end(ctx); };
   try {

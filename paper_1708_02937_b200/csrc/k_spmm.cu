@@ -197,13 +197,12 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
   p.layers_done = d_done;
   const bool vec = (n % 4) == 0;
   const void* fn = vec ? (const void*)k_dense_engine<true> : (const void*)k_dense_engine<false>;
-  int per_sm = 0;
-  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+  const int per_sm = kernel_occupancy(ctx, fn, 256, 0);  // cached per device
   const uint64_t warps = uint64_t((n + 127) / 128) * m;
   const unsigned grid = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>((warps + 7) / 8, uint64_t(ctx->num_sms) * std::max(per_sm, 1))));
   void* args[] = {&p};
-  timing_mark(ctx);
+  timing_mark(ctx, SK_KT_DENSE_ENGINE);
   SK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, ctx->stream));
   g_launches.fetch_add(1);
   timing_mark(ctx);

@@ -5,7 +5,10 @@
 #include <cub/cub.cuh>
 
 #include <cstring>
+#include <initializer_list>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "sk_common.cuh"
 
@@ -93,12 +96,41 @@ void csr_release(sk_csr* a) {
 
 void sync(sk_ctx* ctx) { SK_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
-void timing_mark(sk_ctx* ctx) {
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_attr;                        // smem bytes set
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;           // blocks per SM
+}  // namespace
+
+void kernel_smem_attr(sk_ctx* ctx, const void* kernel, int bytes) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  int& have = g_attr[{kernel, ctx->device}];
+  if (have >= bytes) return;
+  SK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+}
+
+int kernel_occupancy(sk_ctx* ctx, const void* kernel, int threads, size_t smem) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  const auto key = std::make_tuple(kernel, ctx->device, threads, smem);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) return it->second;
+  int per_sm = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  g_occ[key] = per_sm;
+  return per_sm;
+}
+
+void timing_mark(sk_ctx* ctx, int tag) {
   if (!ctx->timing) return;
   if (ctx->ev_used == ctx->ev.size()) {
     cudaEvent_t e;
     SK_CUDA(cudaEventCreate(&e));
     ctx->ev.push_back(e);
+  }
+  if (ctx->ev_used % 2 == 0) {
+    if (ctx->ev_tag.size() <= ctx->ev_used / 2) ctx->ev_tag.resize(ctx->ev_used / 2 + 1);
+    ctx->ev_tag[ctx->ev_used / 2] = tag;
   }
   SK_CUDA(cudaEventRecord(ctx->ev[ctx->ev_used++], ctx->stream));
 }
@@ -249,6 +281,46 @@ extern "C" sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above,
   });
 }
 
+extern "C" sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!t) fail(SK_ERR_INVALID_ARGUMENT, "null tuning");
+    auto in = [](int v, std::initializer_list<int> ok) {
+      for (int o : ok)
+        if (v == o) return true;
+      return false;
+    };
+    if (!in(t->exact, {-1, 0, 1}) || !in(t->esc, {-1, 0, 1}))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact / esc must be -1, 0 or 1");
+    if (!in(t->exact_kernel, {0, 1, 2}))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_kernel must be 0, 1 or 2");
+    if (!in(t->exact_group, {0, 4, 8, 16, 32, 64}))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_group must be 0, 4, 8, 16, 32 or 64");
+    if (!in(t->exact_records, {0, 64, 192}))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_records must be 0, 64 or 192");
+    auto wl = [](int v) { return v == 0 || (v >= 8 && v <= 12); };
+    if (!wl(t->window_log2) || !wl(t->exact_window_log2))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: window log2 must be 0 or 8..12");
+    if (!(t->esc_ratio == t->esc_ratio))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: esc_ratio is NaN");
+    ctx->tune = *t;
+  });
+}
+
+extern "C" sk_status sk_ctx_get_tuning(const sk_ctx* ctx, sk_tuning* t) {
+  return guarded([&] {
+    if (!ctx || !t) fail(SK_ERR_INVALID_ARGUMENT, "null context or tuning");
+    *t = ctx->tune;
+  });
+}
+
+extern "C" sk_status sk_ctx_last_exact(const sk_ctx* ctx, sk_exact_info* info) {
+  return guarded([&] {
+    if (!ctx || !info) fail(SK_ERR_INVALID_ARGUMENT, "null context or info");
+    *info = ctx->last_exact;
+  });
+}
+
 extern "C" sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable) {
   return guarded([&] {
     require_ctx(ctx);
@@ -295,6 +367,21 @@ extern "C" sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, siz
     *count = pairs;
     for (size_t i = 0; i < pairs && i < cap; ++i)
       SK_CUDA(cudaEventElapsedTime(&ms[i], ctx->ev[2 * i], ctx->ev[2 * i + 1]));
+    ctx->ev_used = 0;
+  });
+}
+
+extern "C" sk_status sk_ctx_kernel_times_tagged(sk_ctx* ctx, float* ms, int* tags, size_t cap,
+                                                size_t* count) {
+  return guarded([&] {
+    require_ctx(ctx);
+    sync(ctx);
+    const size_t pairs = ctx->ev_used / 2;
+    *count = pairs;
+    for (size_t i = 0; i < pairs && i < cap; ++i) {
+      SK_CUDA(cudaEventElapsedTime(&ms[i], ctx->ev[2 * i], ctx->ev[2 * i + 1]));
+      tags[i] = ctx->ev_tag[i];
+    }
     ctx->ev_used = 0;
   });
 }
@@ -527,7 +614,7 @@ extern "C" sk_status sk_layer_step(sk_ctx* ctx, const sk_csr* w, const float* bi
     SK_CUDA(cudaMemcpyAsync(db, bias, size_t(w->rows) * 4, cudaMemcpyHostToDevice,
                             ctx->stream));
     sk_dense* o = new_dense(ctx, w->rows, y->cols);
-    timing_mark(ctx);  // K1 is the layer's only kernel (measurement hook)
+    timing_mark(ctx, SK_KT_SPMM);  // K1 is the layer's only kernel (measurement hook)
     launch_layer_dense(ctx, w, db, y->d, y->cols, opt_clip(opt), o->d);
     timing_mark(ctx);
     dfree(ctx, db);

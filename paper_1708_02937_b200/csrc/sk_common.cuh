@@ -102,6 +102,7 @@ struct sk_ctx {
   // this stream around each layer's SpGEMM launch); see sk_ctx_set_timing.
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // 2 per layer
+  std::vector<int> ev_tag;      // SK_KT_* per pair
   size_t ev_used = 0;
   // Optional per-layer %globaltimer stamps written by the sparse engine.
   long long* stamps = nullptr;
@@ -112,6 +113,10 @@ struct sk_ctx {
   // below sparse_below * m * n (sk_ctx_set_density_switch; dense_above <= 0 = off).
   double dense_above = 1.0 / 32;
   double sparse_below = 1.0 / 128;
+  // Kernel selection (sk_ctx_set_tuning; 0 = automatic) and what the last
+  // exact-layer launch ran (sk_ctx_last_exact).
+  sk_tuning tune = {0, 0, 0, 0, 0, 0, 0, 0.0};
+  sk_exact_info last_exact = {0, 0, 0, 0, 0, 0};
   // Grow-only scratch arena for the temporaries of one forward call (window
   // tables, item counts, scratch spans, ping-pong buffers): per-call pool
   // allocations of ~1 GB cost milliseconds of host time with the GPU idle.
@@ -219,11 +224,26 @@ inline void csr_ready(sk_ctx* ctx, const sk_csr* a) {
   if (ctx && a && a->ready) SK_CUDA(cudaStreamWaitEvent(ctx->stream, a->ready, 0));
 }
 
+// Kernel attributes are per device (each device's primary context holds its
+// own copy), so the "set once" state is keyed on (kernel, device) under a
+// lock; occupancy queries are driver calls and are cached on the same key.
+void kernel_smem_attr(sk_ctx* ctx, const void* kernel, int bytes);
+int kernel_occupancy(sk_ctx* ctx, const void* kernel, int threads, size_t smem);
+template <typename K>
+inline void smem_attr(sk_ctx* ctx, K* kernel, int bytes = 200 * 1024) {
+  kernel_smem_attr(ctx, reinterpret_cast<const void*>(kernel), bytes);
+}
+template <typename K>
+inline int occupancy(sk_ctx* ctx, K* kernel, int threads, size_t smem) {
+  return kernel_occupancy(ctx, reinterpret_cast<const void*>(kernel), threads, smem);
+}
+
 // Reads and clears the context's device error word (synchronising).
 void check_device_error(sk_ctx* ctx, const char* op);
 void sync(sk_ctx* ctx);
-// Record a timing event pair slot (no-op unless ctx->timing).
-void timing_mark(sk_ctx* ctx);
+// Record a timing event pair slot (no-op unless ctx->timing); the opening
+// mark of a pair carries the kernel's SK_KT_* tag.
+void timing_mark(sk_ctx* ctx, int tag = SK_KT_OTHER);
 void fill(sk_ctx* ctx, float* p, size_t n, float v);
 
 // device scan helpers (CUB, stream-ordered temp storage)

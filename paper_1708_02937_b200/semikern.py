@@ -164,6 +164,22 @@ class Context:
                                            C.byref(n)))
         return buf[: min(n.value, cap)].copy()
 
+    KERNEL_TAGS = {0: "other", 1: "k_exact_layer", 2: "k_sparse_engine", 3: "k_dense_engine",
+                   4: "k_spmm_rows", 5: "k_gemm_packed", 6: "k_spgemm_rows"}
+
+    def kernel_times_tagged(self):
+        """(durations ms, kernel names) of the timed launches since
+        set_timing(True) / the last call; resets the list."""
+        cap = 1 << 16
+        buf = np.zeros(cap, np.float32)
+        tags = np.zeros(cap, np.int32)
+        n = C.c_size_t()
+        _check(self._L.sk_ctx_kernel_times_tagged(self.h, buf.ctypes.data_as(_lib.f32p),
+                                                  tags.ctypes.data_as(C.POINTER(C.c_int)), cap,
+                                                  C.byref(n)))
+        k = min(n.value, cap)
+        return buf[:k].copy(), [self.KERNEL_TAGS.get(int(t), "other") for t in tags[:k]]
+
     def layer_stamps_ns(self, n: int) -> np.ndarray:
         """%globaltimer stamps of the last sparse forward: start + end of each layer."""
         buf = np.zeros(n, np.int64)
@@ -182,6 +198,39 @@ class Context:
         continues on the dense engine, and below which it returns to the sparse
         one.  dense_above <= 0 keeps the whole pass sparse.  Bitwise neutral."""
         _check(self._L.sk_ctx_set_density_switch(self.h, float(dense_above), float(sparse_below)))
+
+    TUNING_KEYS = ("exact", "exact_kernel", "exact_group", "exact_records", "window_log2",
+                   "exact_window_log2", "esc", "esc_ratio")
+
+    def tuning(self) -> dict:
+        """The context's kernel selection (sk_tuning; 0 = automatic)."""
+        t = _lib.Tuning()
+        _check(self._L.sk_ctx_get_tuning(self.h, C.byref(t)))
+        return {k: getattr(t, k) for k in self.TUNING_KEYS}
+
+    def set_tuning(self, **kw) -> dict:
+        """Select kernel variants (sk_ctx_set_tuning): keys not given keep their
+        value; returns the previous setting so callers can restore it.  Every
+        choice computes the same fold bit for bit."""
+        old = self.tuning()
+        for k in kw:
+            if k not in self.TUNING_KEYS:
+                raise InvalidArgument(f"unknown tuning key {k!r}")
+        new = dict(old, **kw)
+        t = _lib.Tuning(**{k: (float(v) if k == "esc_ratio" else int(v)) for k, v in new.items()})
+        _check(self._L.sk_ctx_set_tuning(self.h, C.byref(t)))
+        return old
+
+    def last_exact(self) -> dict:
+        """What the last exact-layer launch ran (sk_ctx_last_exact): kernel
+        ("generic" / "specialised"), windows per item, records per batch, window
+        log2, accumulator fields per word, and the launch count."""
+        e = _lib.ExactInfo()
+        _check(self._L.sk_ctx_last_exact(self.h, C.byref(e)))
+        return {"launches": int(e.launches),
+                "kernel": {0: None, 1: "generic", 2: "specialised"}[e.kernel],
+                "group": e.group, "records": e.records, "window_log2": e.window_log2,
+                "fields": e.fields}
 
     def set_stream(self, stream_ptr: int | None):
         _check(self._L.sk_ctx_set_stream(self.h, vp(stream_ptr) if stream_ptr else None))

@@ -279,10 +279,15 @@ def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None,
             peer.ensure(nnz)
             r0, _ = block_range(m, world, rank)
             peer.publish(local, k, r0, off, rank == world - 1)
-            if world > 1:  # every rank's stores land before anyone reads
+            # the publish kernel runs on the library context's stream: this rank's
+            # stores have landed once that stream is drained ...
+            local.ctx.synchronize()
+            if world > 1:
+                # ... and every rank's once the collective has completed on the host
+                # side (all ranks enter it only after their own publish finished)
                 flag = torch.zeros(1, device=device)
-                torch.cuda.current_stream(device).synchronize()
                 dist.all_reduce(flag, group=group)
+                flag.item()
             lrp, lci, lv = peer.local(k)
             y = skm.csr_from_device(m, n, nnz, lrp, lci, lv, ctx=y0.ctx)
             y.ctx.synchronize()
