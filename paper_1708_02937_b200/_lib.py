@@ -24,7 +24,7 @@ SK_OK = 0
 EXPORTS = [
     "sk_last_error", "sk_version", "sk_kernel_launch_count",
     "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_stream", "sk_ctx_stream",
-    "sk_ctx_synchronize", "sk_ctx_set_timing", "sk_ctx_kernel_times",
+    "sk_ctx_synchronize", "sk_ctx_set_timing", "sk_ctx_kernel_times", "sk_ctx_kernel_times_tagged",
     "sk_ctx_layer_stamps", "sk_ctx_layer_paths", "sk_ctx_set_density_switch",
     "sk_ctx_set_tuning", "sk_ctx_get_tuning", "sk_ctx_last_exact",
     "sk_host_register", "sk_host_unregister",
