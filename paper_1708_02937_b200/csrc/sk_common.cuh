@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -254,6 +255,7 @@ void exclusive_scan_u64(sk_ctx* ctx, const uint64_t* in, uint64_t* out, size_t n
 
 enum DevErr : int { kErrNone = 0, kErrGf2Domain = 1 };
 
+#ifdef __CUDACC__  // device op tables (host-only translation units skip them)
 struct OpArith {
   static constexpr int kind = SK_ARITHMETIC;
   __device__ static float zero() { return 0.0f; }
@@ -297,8 +299,11 @@ void dispatch_semiring(sk_semiring s, F&& f) {
   fail(SK_ERR_INVALID_ARGUMENT, "unknown semiring kind " + std::to_string(int(s)));
 }
 
+#endif  // __CUDACC__
+
 float semiring_zero_host(sk_semiring s);
 
+#ifdef __CUDACC__
 // ---- the layer epilogue (dnn.cpp:65-103 + optional clip) -----------------------
 // z = acc + b (max-plus "times"); z = z<0 ? 0 : z (max-plus "plus" with 0,
 // semiring.hpp:75 -- a select, so -0.0 and NaN pass through); clip by select.
@@ -309,6 +314,8 @@ __device__ __forceinline__ float layer_epilogue(float acc, float b, float clip) 
   return z;
 }
 
+#endif  // __CUDACC__
+
 // ---- SplitMix64 (rng.hpp:29-62), device side ------------------------------------
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -318,9 +325,11 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 __host__ __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t idx) {
   return mix64(seed + (idx + 1) * 0x9E3779B97F4A7C15ull);
 }
+#ifdef __CUDACC__
 __device__ __forceinline__ double to_unit(uint64_t bits) {
   return __dmul_rn((double)(bits >> 11), 0x1.0p-53);
 }
+#endif  // __CUDACC__
 
 // ---- internal entry points implemented in the .cu files ------------------------
 sk_csr* csr_from_device_triples(sk_ctx* ctx, uint32_t rows, uint32_t cols,
