@@ -28,10 +28,18 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "sk_async.cuh"
 #include "sk_common.cuh"
 
 namespace sk {
 namespace tc {
+
+using async::smem_u32;
+using async::mbar_init;
+using async::mbar_wait;
+using async::mbar_expect_tx;
+using async::bulk_g2s;
+
 
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 128;
@@ -48,10 +56,6 @@ struct Cfg {
   static constexpr uint32_t LBO = 128, SBO = KC * 128;
 };
 constexpr uint32_t kA_LBO = 128, kA_SBO = 1024, kB_LBO = 128, kB_SBO = 1024;  // BK = 32
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -86,22 +90,6 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    mbar)
                : "memory");
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n\t}\n" ::"r"(mbar),
-      "r"(parity)
-      : "memory");
 }
 
 __device__ __forceinline__ float rna_tf32(float x) {
@@ -410,18 +398,6 @@ __global__ void k_pack_split(const float* __restrict__ X, uint32_t rows, uint32_
       *reinterpret_cast<float4*>(lo + off + 4 * i) = make_float4(l[0], l[1], l[2], l[3]);
     }
   }
-}
-
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t mbar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(dst), "l"(src), "r"(bytes), "r"(mbar)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
-               : "memory");
 }
 
 template <int BN_, int NS>

@@ -15,6 +15,9 @@
 // touches it runs.
 #include <cooperative_groups.h>
 
+#include <vector>
+
+#include "sk_async.cuh"
 #include "sk_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -27,7 +30,17 @@ enum EpiMode { kEpiNone = 0, kEpiLayer = 1 };
 // (few stored entries) take kU = 4: the row's (k, w) pairs are loaded once for
 // 512 columns and every entry issues four independent float4 loads, so a task
 // is not a chain of dependent round trips per 128 columns.
-template <typename Ops, int kEpi, bool kVec4, int kU = 1>
+// kBatch: in-edges whose Y loads are in flight together (registers: 4 kU kBatch)
+// (light rows, kU = 4: the four chunks' loads are the batch).  Measured on
+// B200 (tools/prof_dense.py, tools/cfg2_sweep.py): 4 in-edges per batch with
+// 4 blocks of 256 per SM; 1, 2 and 8 were equal or slower.
+#ifndef SK_SPMM_BATCH
+#define SK_SPMM_BATCH 4
+#endif
+#ifndef SK_SPMM_MINB
+#define SK_SPMM_MINB 4
+#endif
+template <typename Ops, int kEpi, bool kVec4, int kU = 1, int kBatch = (kU == 1 ? SK_SPMM_BATCH : 1)>
 __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
                                            const uint32_t* __restrict__ ci,
                                            const float* __restrict__ wv,
@@ -41,8 +54,8 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
   const uint64_t tasks = uint64_t(chunks) * m;
   for (uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; task < tasks;
        task += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-    const uint32_t c = uint32_t(task / m);
-    const uint32_t i = uint32_t(task % m);
+    const uint32_t c = uint32_t(task / m);  // chunk-major: the live Y panel stays in L2
+    const uint32_t i = uint32_t(task - uint64_t(c) * m);
     float acc[kU][4];
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -57,26 +70,45 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
         kk = ci[e0 + lane];
         aa = wv[e0 + lane];
       }
-#pragma unroll 4
-      for (uint32_t t = 0; t < cnt; ++t) {
-        const uint32_t k = __shfl_sync(0xffffffffu, kk, t);
-        const float a = __shfl_sync(0xffffffffu, aa, t);
-        const float* yr = y + size_t(k) * n;
+      // Batches of kBatch in-edges: every Y load of the batch is issued before
+      // the first fold step consumes one, so kBatch (x kU) 512-byte row segments
+      // per warp are in flight instead of one (the fold itself stays strictly
+      // in ascending k).
+      for (uint32_t t0 = 0; t0 < cnt; t0 += kBatch) {
+        float4 v[kBatch][kU];
+        float a[kBatch];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const uint32_t col0 = (c * kU + u) * 128 + lane * 4;
-          if (kVec4) {
-            if (col0 < n) {
-              const float4 v = __ldg(reinterpret_cast<const float4*>(yr + col0));
-              acc[u][0] = Ops::add(acc[u][0], Ops::mul(a, v.x, err), err);
-              acc[u][1] = Ops::add(acc[u][1], Ops::mul(a, v.y, err), err);
-              acc[u][2] = Ops::add(acc[u][2], Ops::mul(a, v.z, err), err);
-              acc[u][3] = Ops::add(acc[u][3], Ops::mul(a, v.w, err), err);
+        for (int q = 0; q < kBatch; ++q) {
+          const uint32_t t = t0 + q;
+          const uint32_t k = __shfl_sync(0xffffffffu, kk, t & 31);
+          a[q] = __shfl_sync(0xffffffffu, aa, t & 31);
+          const float* yr = y + size_t(k) * n;
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const uint32_t col0 = (c * kU + u) * 128 + lane * 4;
+            v[q][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t < cnt) {
+              if (kVec4) {
+                if (col0 < n) v[q][u] = __ldg(reinterpret_cast<const float4*>(yr + col0));
+              } else {
+                if (col0 < n) v[q][u].x = yr[col0];
+                if (col0 + 1 < n) v[q][u].y = yr[col0 + 1];
+                if (col0 + 2 < n) v[q][u].z = yr[col0 + 2];
+                if (col0 + 3 < n) v[q][u].w = yr[col0 + 3];
+              }
             }
-          } else {
+          }
+        }
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (col0 + q < n) acc[u][q] = Ops::add(acc[u][q], Ops::mul(a, yr[col0 + q], err), err);
+        for (int q = 0; q < kBatch; ++q) {
+          if (t0 + q < cnt) {  // warp-uniform
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              acc[u][0] = Ops::add(acc[u][0], Ops::mul(a[q], v[q][u].x, err), err);
+              acc[u][1] = Ops::add(acc[u][1], Ops::mul(a[q], v[q][u].y, err), err);
+              acc[u][2] = Ops::add(acc[u][2], Ops::mul(a[q], v[q][u].z, err), err);
+              acc[u][3] = Ops::add(acc[u][3], Ops::mul(a[q], v[q][u].w, err), err);
+            }
           }
         }
       }
@@ -112,7 +144,7 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
 }
 
 template <typename Ops, int kEpi, bool kVec4, int kU = 1>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, SK_SPMM_MINB)
     k_spmm_rows(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                 const float* __restrict__ wv, const float* __restrict__ bias,
                 const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
@@ -145,11 +177,11 @@ struct DenseEngineArgs {
 };
 
 template <bool kVec4>
-__global__ void __launch_bounds__(256) k_dense_engine(DenseEngineArgs p) {
+__global__ void __launch_bounds__(256, SK_SPMM_MINB) k_dense_engine(DenseEngineArgs p) {
   cg::grid_group grid = cg::this_grid();
   for (uint32_t k = 0; k < p.L; ++k) {
-    const float* src = k == 0 ? p.y0 : p.buf[(k - 1) & 1];
-    float* dst = p.buf[k & 1];
+    const float* src = k == 0 ? p.y0 : (((k - 1) & 1) ? p.buf[1] : p.buf[0]);
+    float* dst = (k & 1) ? p.buf[1] : p.buf[0];
     spmm_tasks<OpArith, kEpiLayer, kVec4>(p.w_rp[k], p.w_ci[k], p.w_v[k], p.bias + size_t(k) * p.m,
                                           src, p.m, p.n, p.clip, dst, p.err,
                                           p.nnz ? p.nnz + k : nullptr);
@@ -161,6 +193,513 @@ __global__ void __launch_bounds__(256) k_dense_engine(DenseEngineArgs p) {
       }
     }
   }
+}
+
+// ---- K1t: register-tiled SpMM for weight rows with many entries ----------------------
+//
+// At high density (BASELINE cfg2, d >= 1/8) the row-per-warp K1 re-reads a
+// 512-byte Y segment from L2 for every stored weight; here a CTA owns a
+// (kWarps * kRW)-row x 256-column output tile and streams Y through shared memory
+// in 32-row k-chunks (cp.async.bulk, one 1 KB row segment per copy,
+// double-buffered on mbarriers).  A warp owns kRW rows x 256 columns (a lane:
+// 8 columns of each row, fp32 accumulators in registers): each Y chunk row is
+// read from shared memory once per warp and applied to every one of the warp's
+// rows that stores a weight at that k.  Presence comes from a 32-bit mask per
+// (row, chunk), so the fold is exactly the stored entries in ascending k (absent
+// weights are skipped, never multiplied as zeros): bit-identical to K1 and to
+// the reference's mxm_csr_dense (proj/src/matrix.cpp:403-424).
+//
+// The weights are repacked once per matrix (cached on the immutable handle)
+// into the tile order: for every (64-row tile, 32-k chunk) a 64 x 32 value
+// block (only present slots are written) and 64 masks, so each chunk's
+// weights arrive with one more bulk copy.
+namespace tile {
+constexpr int kPR = 64;                // rows per packed tile
+constexpr int kTC = 256;               // columns per CTA (lane: 2 x float4)
+constexpr int kKC = 32;                // k per chunk
+constexpr int kStages = 2;
+constexpr uint32_t kYBytes = uint32_t(kKC) * kTC * 4;      // 32 KB
+constexpr uint32_t kWBytes = uint32_t(kPR) * kKC * 4;      // 8 KB
+constexpr uint32_t kMBytes = uint32_t(kPR) * 4;            // 256 B
+constexpr uint32_t kStageBytes = kYBytes + kWBytes + kMBytes;
+constexpr size_t kSmem = size_t(kStages) * kStageBytes + 64;
+}  // namespace tile
+
+// Pack (once per weight matrix): masks zeroed by the caller, then a thread per
+// stored entry writes its value into its (tile, chunk) block and ORs its bit.
+__global__ void k_tile_pack(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                            const float* __restrict__ v, uint32_t m, uint32_t nK,
+                            float* __restrict__ vals, uint32_t* __restrict__ mask) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t rt = i / tile::kPR, r = i % tile::kPR;
+    for (uint32_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
+      const uint32_t k = ci[e], kc = k / tile::kKC, kk = k % tile::kKC;
+      const size_t blk = size_t(rt) * nK + kc;
+      vals[blk * (tile::kPR * tile::kKC) + r * tile::kKC + kk] = v[e];
+      atomicOr(&mask[blk * tile::kPR + r], 1u << kk);
+    }
+  }
+}
+
+// kRW rows per warp, 64 / kRW warps per CTA (one packed tile per CTA)
+template <int kEpi, int kRW>
+__global__ void __launch_bounds__(tile::kPR / kRW * 32, kRW == 4 ? 3 : 2)
+    k_spmm_tile(const __grid_constant__ CUtensorMap ymap, const float* __restrict__ wvals,
+                const uint32_t* __restrict__ wmask, const float* __restrict__ bias, uint32_t m,
+                uint32_t K, uint32_t n, float clip, float* __restrict__ out) {
+  using namespace tile;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t rt = blockIdx.y, c0 = blockIdx.x * kTC;
+  const uint32_t nK = (K + kKC - 1) / kKC;
+  const uint32_t ncols = min(uint32_t(kTC), n - c0);  // a multiple of 4 (n % 4 == 0)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  auto stage = [&](uint32_t s) { return smem + size_t(s) * kStageBytes; };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) async::mbar_init(async::smem_u32(mbar + s), 1);
+    async::fence_mbar_init();
+  }
+  __syncthreads();
+  // producer (thread 0): chunk j's 32 x 256 Y box (one 2-D tensor copy; rows
+  // past K and columns past n arrive as zeros and are never used) and its weight
+  // block + masks into stage j % kStages
+  auto issue = [&](uint32_t j) {
+    const uint32_t s = j % kStages;
+    const uint32_t mb = async::smem_u32(mbar + s);
+    uint8_t* st = stage(s);
+    async::mbar_expect_tx(mb, kYBytes + kWBytes + kMBytes);
+    const size_t blk = size_t(rt) * nK + j;
+    async::tma_2d_g2s(async::smem_u32(st), &ymap, int(c0), int(j * kKC), mb);
+    async::bulk_g2s(async::smem_u32(st + kYBytes), wvals + blk * (kPR * kKC), kWBytes, mb);
+    async::bulk_g2s(async::smem_u32(st + kYBytes + kWBytes), wmask + blk * kPR, kMBytes, mb);
+  };
+  if (threadIdx.x == 0)
+    for (uint32_t j = 0; j < min(uint32_t(kStages), nK); ++j) issue(j);
+
+  float acc[kRW][8];
+#pragma unroll
+  for (int r = 0; r < kRW; ++r)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[r][q] = 0.0f;
+  for (uint32_t j = 0; j < nK; ++j) {
+    const uint32_t s = j % kStages;
+    async::mbar_wait(async::smem_u32(mbar + s), (j / kStages) & 1u);
+    const float* Yc = reinterpret_cast<const float*>(stage(s));
+    const float* Wc = reinterpret_cast<const float*>(stage(s) + kYBytes) + warp * kRW * kKC;
+    const uint32_t* Mc =
+        reinterpret_cast<const uint32_t*>(stage(s) + kYBytes + kWBytes) + warp * kRW;
+    uint32_t mask[kRW];
+#pragma unroll
+    for (int r = 0; r < kRW; ++r) mask[r] = Mc[r];  // warp-uniform (broadcast)
+#pragma unroll 4
+    for (int kk = 0; kk < kKC; ++kk) {
+      const float4 y0 = *reinterpret_cast<const float4*>(Yc + kk * kTC + lane * 4);
+      const float4 y1 = *reinterpret_cast<const float4*>(Yc + kk * kTC + 128 + lane * 4);
+#pragma unroll
+      for (int r = 0; r < kRW; ++r) {
+        if (mask[r] & (1u << kk)) {  // warp-uniform: the warp's lanes share the rows
+          const float w = Wc[r * kKC + kk];
+          acc[r][0] = __fadd_rn(acc[r][0], __fmul_rn(w, y0.x));
+          acc[r][1] = __fadd_rn(acc[r][1], __fmul_rn(w, y0.y));
+          acc[r][2] = __fadd_rn(acc[r][2], __fmul_rn(w, y0.z));
+          acc[r][3] = __fadd_rn(acc[r][3], __fmul_rn(w, y0.w));
+          acc[r][4] = __fadd_rn(acc[r][4], __fmul_rn(w, y1.x));
+          acc[r][5] = __fadd_rn(acc[r][5], __fmul_rn(w, y1.y));
+          acc[r][6] = __fadd_rn(acc[r][6], __fmul_rn(w, y1.z));
+          acc[r][7] = __fadd_rn(acc[r][7], __fmul_rn(w, y1.w));
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && j + kStages < nK) issue(j + kStages);
+  }
+  // epilogue: bias + ReLU select (+ clip), two float4 stores per row
+#pragma unroll
+  for (int r = 0; r < kRW; ++r) {
+    const uint32_t i = rt * kPR + warp * kRW + r;
+    if (i >= m) continue;
+    const float b = kEpi == kEpiLayer ? bias[i] : 0.0f;
+    float z[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z[q] = kEpi == kEpiLayer ? layer_epilogue(acc[r][q], b, clip) : acc[r][q];
+    float* orow = out + size_t(i) * n + c0;
+    if (uint32_t(lane) * 4 < ncols)
+      *reinterpret_cast<float4*>(orow + lane * 4) = make_float4(z[0], z[1], z[2], z[3]);
+    if (128 + uint32_t(lane) * 4 < ncols)
+      *reinterpret_cast<float4*>(orow + 128 + lane * 4) = make_float4(z[4], z[5], z[6], z[7]);
+  }
+}
+
+// The tile-packed copy of W (built on first use, cached on the handle).
+static void ensure_tile_pack(sk_ctx* ctx, const sk_csr* w) {
+  auto* ww = const_cast<sk_csr*>(w);
+  if (ww->tile_vals) return;
+  const uint32_t nrt = (w->rows + tile::kPR - 1) / tile::kPR;
+  const uint32_t nK = (w->cols + tile::kKC - 1) / tile::kKC;
+  const size_t blocks = size_t(nrt) * nK;
+  ww->tile_vals = dalloc<float>(ctx, blocks * tile::kPR * tile::kKC);
+  ww->tile_mask = dalloc<uint32_t>(ctx, blocks * tile::kPR);
+  SK_CUDA(cudaMemsetAsync(ww->tile_mask, 0, blocks * tile::kPR * 4, ctx->stream));
+  const unsigned grid = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((uint64_t(w->rows) + 7) / 8, uint64_t(ctx->num_sms) * 16)));
+  SK_LAUNCH(k_tile_pack, grid, 256, 0, ctx->stream, w->rp, w->ci, w->v, w->rows, nK,
+            ww->tile_vals, ww->tile_mask);
+}
+
+#ifndef SK_TILE_RW
+#define SK_TILE_RW 8
+#endif
+
+// K1t applies when rows are heavy enough that a warp's rows share most k
+// (mean stored entries per row >= cols / 8), the activations are 16-byte
+// aligned rows (n % 4 == 0) and wide enough for the 256-column tiles, and the
+// packed copy (dense-tile sized) stays small against the device.
+static bool tile_applies(sk_ctx* ctx, const sk_csr* w, uint32_t n) {
+  if (n % 4 != 0 || n < 128 || w->rows == 0 || w->cols == 0) return false;
+  if (double(w->nnz) * 8.0 < double(w->rows) * double(w->cols)) return false;
+  const double packed = double((w->rows + 63) / 64) * 64.0 * double((w->cols + 31) / 32) * 32.0 * 4.0;
+  return packed < 0.05 * double(ctx->total_mem);
+}
+
+static void launch_tile(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const float* y,
+                        uint32_t n, float clip, float* out, bool layer) {
+  constexpr int kRW = SK_TILE_RW;
+  ensure_tile_pack(ctx, w);
+  CUtensorMap ymap;
+  if (!async::make_tmap_2d_f32(&ymap, y, w->cols, n, n, tile::kKC, tile::kTC))
+    fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed for the activation tile map");
+  dim3 grid(ceil_div(n, tile::kTC), ceil_div(w->rows, tile::kPR));
+  const int threads = tile::kPR / kRW * 32;
+  if (layer) {
+    smem_attr(ctx, k_spmm_tile<kEpiLayer, kRW>, int(tile::kSmem));
+    SK_LAUNCH((k_spmm_tile<kEpiLayer, kRW>), grid, threads, tile::kSmem, ctx->stream,
+              ymap, w->tile_vals, w->tile_mask, d_bias, w->rows, w->cols, n, clip, out);
+  } else {
+    smem_attr(ctx, k_spmm_tile<kEpiNone, kRW>, int(tile::kSmem));
+    SK_LAUNCH((k_spmm_tile<kEpiNone, kRW>), grid, threads, tile::kSmem, ctx->stream,
+              ymap, w->tile_vals, w->tile_mask, nullptr, w->rows, w->cols, n, 0.0f, out);
+  }
+}
+
+// ---- K1c: the whole forward of a small model, one thread-block cluster per ----------
+//      32-sample column block, layers separated by cluster barriers
+//
+// Output column j of layer k+1 depends only on column j of layer k, so sample
+// column blocks never need each other: a cluster of kCS CTAs owns 32 columns
+// and runs EVERY layer on them, its CTAs splitting the output rows; no
+// grid-wide barrier and no per-layer launch.  Per CTA:
+//  * at start, every layer's weight rows of the CTA (row pointers, columns,
+//    values) are copied into shared memory once;
+//  * per layer, Y_k's 32-column panel (all m rows, 128 B per row) arrives in
+//    shared memory by 2-D tensor copies (TMA), a warp folds one output row at a
+//    time with lane = column (conflict-free shared loads, the row's (k, w)
+//    broadcast), strictly in ascending k -- the reference's fold
+//    (proj/src/matrix.cpp:403-424) -- and writes Y_{k+1} to global memory;
+//  * a proxy fence + hardware cluster barrier (release / acquire) orders every
+//    CTA's writes before the next layer's tensor copies read them.
+// BASELINE cfg1 (m = 1024, 4 layers, 256 samples): 8 clusters x 8 CTAs.  (The
+// clusters of one launch are placed on one die -- measured: 16 clusters of 8
+// ran as two waves -- so the launch is kept to <= 9 clusters of 8.)
+namespace clu {
+constexpr int kCS = 8;        // CTAs per cluster
+constexpr int kWarps = 32;    // warps per CTA
+constexpr int kCols = 32;     // columns per cluster (kCols lanes fold one row)
+constexpr int kRows = 2;      // rows per lane group folded together
+constexpr int kBoxRows = 256; // tensor-copy box: 256 rows x kCols columns
+}  // namespace clu
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+struct ClusterMaps {
+  CUtensorMap y0, b0, b1;  // Y_0 and the two ping-pong buffers, box 256 x kCols
+};
+
+#ifdef SK_CLU_DEBUG
+__device__ long long g_clu_ts[64];
+#define CLU_TS(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_clu_ts[i] = t_; } } while (0)
+__device__ unsigned long long g_clu_start[2];  // min / max CTA start
+__device__ unsigned long long g_clu_end[2];
+#else
+#define CLU_TS(i) do {} while (0)
+#endif
+__global__ void __launch_bounds__(clu::kWarps * 32, 1)
+    k_dense_cluster(const __grid_constant__ ClusterMaps maps, DenseEngineArgs p,
+                    float* __restrict__ last, uint32_t wslice_entries) {
+  using namespace clu;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t crank = cluster_ctarank();
+  constexpr int kGroups = 32 / kCols;  // row groups per warp
+  const int h = lane / kCols, cl = lane % kCols;  // lane group, column within the block
+  const uint32_t c0 = (blockIdx.x / kCS) * kCols, col = c0 + cl;
+  const bool live = col < p.n;
+  const uint32_t r0 = uint32_t(uint64_t(p.m) * crank / kCS);
+  const uint32_t r1 = uint32_t(uint64_t(p.m) * (crank + 1) / kCS);
+  const uint32_t nr = r1 - r0;
+  // shared layout: Y panel (m x kCols floats, box-padded) | per layer: row
+  // offsets (nr + 1) | (k, w) pairs (wslice_entries)
+  const uint32_t mpad = (p.m + kBoxRows - 1) / kBoxRows * kBoxRows;
+  float* Ys = reinterpret_cast<float*>(smem);
+  uint32_t* roff = reinterpret_cast<uint32_t*>(Ys + size_t(mpad) * kCols);
+  uint2* kw = reinterpret_cast<uint2*>(roff + ((size_t(p.L) * (nr + 1) + 1) & ~size_t(1)));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(kw + size_t(wslice_entries));
+  CLU_TS(0);
+#ifdef SK_CLU_DEBUG
+  if (threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    atomicMin(&g_clu_start[0], t_);
+    atomicMax(&g_clu_start[1], t_);
+  }
+#endif
+  if (threadIdx.x == 0) {
+    async::mbar_init(async::smem_u32(mbar), 1);
+    async::fence_mbar_init();
+  }
+  // the CTA's weight rows of every layer in shared memory: slice bounds of all
+  // layers first (one load each, in parallel); layer 0's entries before the
+  // first fold, layer k+1's while the cluster waits at layer k's barrier
+  uint32_t* bnd = reinterpret_cast<uint32_t*>(mbar + 1);  // 2 L + 1 words
+  for (uint32_t q = threadIdx.x; q < 2 * p.L; q += blockDim.x)
+    bnd[q] = p.w_rp[q >> 1][(q & 1) ? r1 : r0];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t base = 0;
+    for (uint32_t k = 0; k < p.L; ++k) {
+      const uint32_t eb = bnd[2 * k], ee = bnd[2 * k + 1];
+      bnd[2 * k] = base;       // slice start in kw
+      bnd[2 * k + 1] = eb;     // the layer's first entry in global memory
+      base += ee - eb;
+    }
+    bnd[2 * p.L] = base;
+  }
+  __syncthreads();
+  for (uint32_t k = 0; k < p.L; ++k) {
+    const uint32_t* rp = p.w_rp[k];
+    for (uint32_t q = threadIdx.x; q <= nr; q += blockDim.x)
+      roff[k * (nr + 1) + q] = bnd[2 * k] + rp[r0 + q] - bnd[2 * k + 1];
+  }
+  float* bsh = reinterpret_cast<float*>(bnd + ((2 * p.L + 2) & ~1u));  // L x nr biases
+  auto load_slice = [&](uint32_t k) {
+    for (uint32_t q = threadIdx.x; q < nr; q += blockDim.x)
+      bsh[k * nr + q] = p.bias[size_t(k) * p.m + r0 + q];
+    const uint32_t* ci = p.w_ci[k];
+    const float* wv = p.w_v[k];
+    const uint32_t s0 = bnd[2 * k], cnt = bnd[2 * k + 2] - s0, g0 = bnd[2 * k + 1];
+    constexpr int kU = 4;  // loads in flight per thread
+    for (uint32_t t0 = threadIdx.x; t0 < cnt; t0 += blockDim.x * kU) {
+      uint32_t cc[kU];
+      float vv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t t = t0 + u * blockDim.x;
+        if (t < cnt) {
+          cc[u] = ci[g0 + t];
+          vv[u] = wv[g0 + t];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t t = t0 + u * blockDim.x;
+        if (t < cnt) kw[s0 + t] = make_uint2(cc[u], __float_as_uint(vv[u]));
+      }
+    }
+  };
+  load_slice(0);
+  __syncthreads();
+  const uint32_t nbox = mpad / kBoxRows;
+  CLU_TS(1);
+  for (uint32_t k = 0; k < p.L; ++k) {
+    const CUtensorMap* src = k == 0 ? &maps.y0 : (((k - 1) & 1) ? &maps.b1 : &maps.b0);
+    float* dst = k + 1 == p.L ? last : ((k & 1) ? p.buf[1] : p.buf[0]);
+    if (threadIdx.x == 0) {
+      const uint32_t mb = async::smem_u32(mbar);
+      async::mbar_expect_tx(mb, nbox * kBoxRows * kCols * 4);
+      for (uint32_t b = 0; b < nbox; ++b)
+        async::tma_2d_g2s(async::smem_u32(Ys + size_t(b) * kBoxRows * kCols), src, int(c0),
+                          int(b * kBoxRows), mb);
+    }
+    async::mbar_wait(async::smem_u32(mbar), k & 1u);
+    CLU_TS(2 + 3 * k);
+    const uint32_t* ro = roff + k * (nr + 1);
+    const float* bias = bsh + size_t(k) * nr - r0;  // indexed by the global row
+    // a lane group folds kRows rows at a time (independent chains in flight)
+    const uint32_t vw = uint32_t(warp) * kGroups + h, nvw = kGroups * kWarps;
+    for (uint32_t rb = vw; rb < nr; rb += nvw * kRows) {
+      float acc[kRows];
+      uint32_t e0[kRows], e1[kRows], len = 0;
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) {
+        const uint32_t r = rb + q * nvw;
+        acc[q] = 0.0f;
+        e0[q] = r < nr ? ro[r] : 0u;
+        e1[q] = r < nr ? ro[r + 1] : 0u;
+        len = max(len, e1[q] - e0[q]);
+      }
+      bool same = true;  // every row of the group has len entries: no guards
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) same &= e1[q] - e0[q] == len;
+      if (same && (len & 3u) == 0) {
+        for (uint32_t t0 = 0; t0 < len; t0 += 4) {
+          float yv[kRows][4], wv4[kRows][4];
+#pragma unroll
+          for (int q = 0; q < kRows; ++q)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint2 kv = kw[e0[q] + t0 + u];  // broadcast within the lane group
+              wv4[q][u] = __uint_as_float(kv.y);
+              yv[q][u] = Ys[kv.x * kCols + cl];
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < kRows; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wv4[q][u], yv[q][u]));
+        }
+        len = 0;  // done
+      }
+      // 4 steps at a time: the (k, w) and Y loads of all of them issued first
+      // (indices clamped into the slice; a step past a row's end is not folded)
+      for (uint32_t t0 = 0; t0 < len; t0 += 4) {
+        float yv[kRows][4], wv4[kRows][4];
+#pragma unroll
+        for (int q = 0; q < kRows; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t e = min(e0[q] + t0 + u, max(e1[q], 1u) - 1);
+            const uint2 kv = kw[e];  // broadcast within the half-warp
+            wv4[q][u] = __uint_as_float(kv.y);
+            yv[q][u] = Ys[kv.x * kCols + cl];
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < kRows; ++q)
+            if (e0[q] + t0 + u < e1[q]) acc[q] = __fadd_rn(acc[q], __fmul_rn(wv4[q][u], yv[q][u]));
+      }
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) {
+        const uint32_t r = rb + q * nvw;
+        if (r < nr && live) {
+          const uint32_t i = r0 + r;
+          dst[size_t(i) * p.n + col] = layer_epilogue(acc[q], bias[i], p.clip);
+        }
+      }
+    }
+    CLU_TS(3 + 3 * k);
+    if (k + 1 < p.L) {
+      // the generic-proxy stores above are read by the next layer's tensor copies
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      load_slice(k + 1);  // overlaps the wait for the slowest CTA of the cluster
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    CLU_TS(4 + 3 * k);
+  }
+#ifdef SK_CLU_DEBUG
+  if (threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    atomicMin(&g_clu_end[0], t_);
+    atomicMax(&g_clu_end[1], t_);
+  }
+#endif
+}
+
+// Shared memory K1c needs for a model and batch (0 = does not apply).
+static size_t cluster_smem(sk_ctx* ctx, const sk_model* md, uint32_t n, uint32_t* wslice) {
+  const uint32_t m = md->neurons;
+  if (md->layers < 1 || m < clu::kCS || n % 4 != 0 ||
+      size_t(m) * clu::kCols * 4 > 160 * 1024)
+    return 0;
+  auto* mm = const_cast<sk_model*>(md);
+  if (mm->clu_worst == SIZE_MAX) {
+    // the largest per-CTA weight slice over the cluster's row blocks (row
+    // pointers at the block bounds; once per model)
+    std::vector<uint32_t> bnd(size_t(md->layers) * (clu::kCS + 1));
+    for (uint32_t k = 0; k < md->layers; ++k)
+      for (uint32_t c = 0; c <= uint32_t(clu::kCS); ++c)
+        SK_CUDA(cudaMemcpyAsync(&bnd[size_t(k) * (clu::kCS + 1) + c],
+                                md->w[k]->rp + uint64_t(m) * c / clu::kCS, 4,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    size_t worst = 0;
+    for (uint32_t c = 0; c < uint32_t(clu::kCS); ++c) {
+      size_t tot = 0;
+      for (uint32_t k = 0; k < md->layers; ++k)
+        tot += bnd[size_t(k) * (clu::kCS + 1) + c + 1] - bnd[size_t(k) * (clu::kCS + 1) + c];
+      worst = std::max(worst, tot);
+    }
+    mm->clu_worst = worst;
+  }
+  const size_t worst = mm->clu_worst;
+  const size_t mpad = (m + clu::kBoxRows - 1) / clu::kBoxRows * clu::kBoxRows;
+  const size_t nr = (m + clu::kCS - 1) / clu::kCS + 1;
+  const size_t bytes = mpad * clu::kCols * 4 + ((size_t(md->layers) * (nr + 1) + 1) & ~size_t(1)) * 4 +
+                       worst * 8 + 16 + (2 * size_t(md->layers) + 2) * 4 +
+                       size_t(md->layers) * nr * 4;
+  *wslice = uint32_t(worst);
+  return bytes <= 200 * 1024 ? bytes : 0;
+}
+
+static void launch_cluster_forward(sk_ctx* ctx, const DenseEngineArgs& p, float* last,
+                                   size_t smem, uint32_t wslice) {
+  ClusterMaps maps;
+  const uint64_t m = p.m, n = p.n;
+  if (!async::make_tmap_2d_f32(&maps.y0, p.y0, m, n, n, clu::kBoxRows, clu::kCols) ||
+      !async::make_tmap_2d_f32(&maps.b0, p.buf[0] ? p.buf[0] : last, m, n, n, clu::kBoxRows,
+                               clu::kCols) ||
+      !async::make_tmap_2d_f32(&maps.b1, p.buf[1] ? p.buf[1] : last, m, n, n, clu::kBoxRows,
+                               clu::kCols))
+    fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed for the dense forward");
+  smem_attr(ctx, k_dense_cluster, int(smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(((p.n + clu::kCols - 1) / clu::kCols) * clu::kCS));
+  cfg.blockDim = dim3(clu::kWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = clu::kCS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  timing_mark(ctx, SK_KT_DENSE_ENGINE);  // (after the host-side map encoding)
+  SK_CUDA(cudaLaunchKernelEx(&cfg, k_dense_cluster, maps, p, last, wslice));
+  timing_mark(ctx);
+  g_launches.fetch_add(1);
+#ifdef SK_CLU_DEBUG
+  {
+    unsigned long long init[2] = {~0ull, 0ull};
+    // (for the next call)
+    unsigned long long st[2], en[2];
+    SK_CUDA(cudaMemcpyFromSymbolAsync(st, g_clu_start, 16, 0, cudaMemcpyDeviceToHost, ctx->stream));
+    SK_CUDA(cudaMemcpyFromSymbolAsync(en, g_clu_end, 16, 0, cudaMemcpyDeviceToHost, ctx->stream));
+    SK_CUDA(cudaStreamSynchronize(ctx->stream));
+    fprintf(stderr, "[clu] CTA starts spread %.2f us, ends spread %.2f us, first start -> last end %.2f us\n",
+            (st[1] - st[0]) / 1e3, (en[1] - en[0]) / 1e3, (en[1] - st[0]) / 1e3);
+    SK_CUDA(cudaMemcpyToSymbolAsync(g_clu_start, init, 16, 0, cudaMemcpyHostToDevice, ctx->stream));
+    SK_CUDA(cudaMemcpyToSymbolAsync(g_clu_end, init, 16, 0, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  long long ts[64];
+  SK_CUDA(cudaMemcpyFromSymbolAsync(ts, g_clu_ts, sizeof(ts), 0, cudaMemcpyDeviceToHost, ctx->stream));
+  SK_CUDA(cudaStreamSynchronize(ctx->stream));
+  fprintf(stderr, "[clu] prologue %.2f us |", (ts[1] - ts[0]) / 1e3);
+  for (uint32_t k = 0; k < p.L; ++k)
+    fprintf(stderr, " L%u tma %.2f fold %.2f bar %.2f |", k, (ts[2 + 3 * k] - (k ? ts[1 + 3 * k] : ts[1])) / 1e3,
+            (ts[3 + 3 * k] - ts[2 + 3 * k]) / 1e3, (ts[4 + 3 * k] - ts[3 + 3 * k]) / 1e3);
+  fprintf(stderr, "\n");
+#endif
 }
 
 static unsigned spmm_grid(sk_ctx* ctx, uint32_t m, uint32_t n, int U = 1) {
@@ -195,6 +734,16 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
   p.nnz = nnz;
   p.stop_below = nnz ? stop_below : 0;
   p.layers_done = d_done;
+  uint32_t wslice = 0;
+  const size_t csmem = (!nnz && k0 == 0 &&
+                        uint64_t((n + clu::kCols - 1) / clu::kCols) * clu::kCS <= uint64_t(ctx->num_sms) / 2)
+                           ? cluster_smem(ctx, md, n, &wslice) : 0;
+  if (csmem) {
+    // small model: one cluster-pipelined launch; the last layer writes the
+    // buffer the caller reads ((L - 1) & 1), the others ping-pong as usual
+    launch_cluster_forward(ctx, p, p.buf[(p.L - 1) & 1], csmem, wslice);
+    return;
+  }
   const bool vec = (n % 4) == 0;
   const void* fn = vec ? (const void*)k_dense_engine<true> : (const void*)k_dense_engine<false>;
   const int per_sm = kernel_occupancy(ctx, fn, 256, 0);  // cached per device
@@ -211,6 +760,10 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
 void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const float* y,
                         uint32_t n, float clip, float* out) {
   if (w->rows == 0 || n == 0) return;
+  if (tile_applies(ctx, w, n)) {
+    launch_tile(ctx, w, d_bias, y, n, clip, out, true);
+    return;
+  }
   const bool vec = (n % 4 == 0);
   // light rows (<= 16 stored entries on average) and wide activations: four
   // 128-column chunks per task
@@ -229,6 +782,10 @@ void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const
 void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b, uint32_t n,
                           sk_semiring s, float* out) {
   if (a->rows == 0 || n == 0) return;
+  if (s == SK_ARITHMETIC && tile_applies(ctx, a, n)) {
+    launch_tile(ctx, a, nullptr, b, n, 0.0f, out, false);
+    return;
+  }
   dispatch_semiring(s, [&](auto ops) {
     using Ops = decltype(ops);
     if (n % 4 == 0)

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <tuple>
 
+#include "sk_async.cuh"
 #include "sk_common.cuh"
 
 namespace sk {
@@ -90,6 +91,8 @@ void csr_release(sk_csr* a) {
     dfree(a->ctx, a->rp);
     dfree(a->ctx, a->ci);
     dfree(a->ctx, a->v);
+    if (a->tile_vals) dfree(a->ctx, a->tile_vals);
+    if (a->tile_mask) dfree(a->ctx, a->tile_mask);
     delete a;
   }
 }
@@ -109,6 +112,30 @@ void kernel_smem_attr(sk_ctx* ctx, const void* kernel, int bytes) {
   SK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   have = bytes;
 }
+
+namespace async {
+bool make_tmap_2d_f32(CUtensorMap* map, const float* base, uint64_t rows, uint64_t cols,
+                      uint64_t pitch_elems, uint32_t box_rows, uint32_t box_cols) {
+  static PFN_cuTensorMapEncodeTiled encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }();
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {pitch_elems * 4};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace async
 
 int kernel_occupancy(sk_ctx* ctx, const void* kernel, int threads, size_t smem) {
   std::lock_guard<std::mutex> lk(g_attr_mu);

@@ -172,6 +172,10 @@ struct sk_csr {
   // set by the stream-asynchronous constructor: the arrays are complete once
   // this event has fired (every consumer orders its stream after it)
   cudaEvent_t ready = nullptr;
+  // K1t's chunk-tiled copy of the weights (values in 64 x 32 tiles + presence
+  // masks), built on first use and cached like the statistics (k_spmm.cu)
+  float* tile_vals = nullptr;
+  uint32_t* tile_mask = nullptr;
 };
 
 
@@ -191,6 +195,7 @@ struct sk_model {
   int weights_finite = -1;           // every weight finite (-1 = not computed yet)
   std::vector<ValueStats> wstats_host;  // host copy of d_wstats
   std::vector<sk_csr*> wT;              // per layer W^T (out-edges), built on first ESC use
+  size_t clu_worst = SIZE_MAX;          // K1c: largest per-CTA weight slice (SIZE_MAX: not yet)
   std::vector<uint32_t> wT_maxdeg;      // longest W^T row
 };
 
