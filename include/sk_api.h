@@ -90,7 +90,7 @@ sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable);
 sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count);
 /* Same, plus which kernel each timed launch was (SK_KT_*). */
 enum { SK_KT_OTHER = 0, SK_KT_EXACT = 1, SK_KT_ENGINE = 2, SK_KT_DENSE_ENGINE = 3,
-       SK_KT_SPMM = 4, SK_KT_GEMM_TC = 5, SK_KT_SPGEMM = 6 };
+       SK_KT_SPMM = 4, SK_KT_GEMM_TC = 5, SK_KT_SPGEMM = 6, SK_KT_PUSH = 7 };
 sk_status sk_ctx_kernel_times_tagged(sk_ctx* ctx, float* ms, int* tags, size_t cap,
                                      size_t* count);
 /* With timing enabled, the sparse engine writes %globaltimer (ns) at the start
@@ -121,7 +121,13 @@ sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double spar
  *   exact_kernel   1 the generic k_exact_layer; 2 the specialised kernel
  *                  (taken only where its preconditions hold: 1024-sample
  *                  windows, constant increment, four 8-bit fields, every bias
- *                  <= 0 -- otherwise the generic kernel runs)
+ *                  <= 0 -- otherwise the generic kernel runs); 3 the
+ *                  sample-major push kernel k_push_layer (where it applies:
+ *                  constant positive products, every bias <= 0, 8-bit
+ *                  counters of all out-neurons within 64 KB, a model layer;
+ *                  measured slower than the windowed kernels, so never
+ *                  automatic); 0 = the specialised kernel where it applies,
+ *                  else the generic one
  *   exact_group    4, 8, 16, 32 or 64 windows per exact-layer work item
  *   exact_records  64 or 192 piece records per batch
  *   window_log2    8..12: sample window of the windowed engine (default 10)
@@ -143,7 +149,7 @@ sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t);
 sk_status sk_ctx_get_tuning(const sk_ctx* ctx, sk_tuning* t);
 /* What the last exact-layer launch on this context ran (introspection for the
  * parity tests): launches = exact-layer launches since the context was created;
- * kernel 1 generic / 2 specialised; group = windows per item; records = piece
+ * kernel 1 generic / 2 specialised / 3 push; group = windows per item; records = piece
  * records per batch; window_log2; fields = accumulator fields per word. */
 typedef struct sk_exact_info {
   uint64_t launches;

@@ -344,7 +344,7 @@ __global__ void k_esc_max_row(const uint32_t* rp, uint32_t rows, unsigned int* o
 
 // W^T of layer k (out-edges of every neuron) and its longest row, built on
 // first use and cached with the model.
-static const sk_csr* layer_transpose(sk_ctx* ctx, sk_model* mm, uint32_t k) {
+const sk_csr* model_layer_transpose(sk_ctx* ctx, sk_model* mm, uint32_t k) {
   if (mm->wT.size() != mm->layers) {
     mm->wT.assign(mm->layers, nullptr);
     mm->wT_maxdeg.assign(mm->layers, 0);
@@ -375,13 +375,13 @@ bool esc_applicable(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y
   const double items = m * double((uint64_t(y->cols) + 1023) / 1024);
   if (est > ratio * items || est > double(1u << 28)) return false;
   auto* mm = const_cast<sk_model*>(md);
-  layer_transpose(ctx, mm, k);
+  model_layer_transpose(ctx, mm, k);
   return double(y->nnz) * double(mm->wT_maxdeg[k]) < double(1u << 31);
 }
 
 sk_csr* esc_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y, uint32_t k, float clip) {
   auto* mm = const_cast<sk_model*>(md);
-  const sk_csr* wt = layer_transpose(ctx, mm, k);
+  const sk_csr* wt = model_layer_transpose(ctx, mm, k);
   const float* bias = md->bias + size_t(k) * md->neurons;
   const uint32_t maxdeg = mm->wT_maxdeg[k];
   return uint64_t(md->neurons) * y->cols <= 0xFFFFFFFFull

@@ -1771,6 +1771,7 @@ struct ExactLayerIn {
   bool nonpos;
   double negmin;
   uint32_t stamp_layer;  // %globaltimer slot (ctx->stamps)
+  const sk_csr* wT = nullptr;  // W^T (cached with a model) -- enables the push kernel
 };
 
 // Weight statistics of a bare CSR (value statistics + row bounds), cached on the
@@ -2108,6 +2109,8 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
   in.nonpos = md->bias_nonpos[k0] != 0;
   in.negmin = md->bias_negmin[k0];
   in.stamp_layer = k0;
+  if (md->bias_nonpos[k0] && ctx->tune.exact_kernel == 3)
+    in.wT = model_layer_transpose(ctx, const_cast<sk_model*>(md), k0);
   return exact_layer_w(ctx, in, y0, clip, ystats, wp_out_ptr);
 }
 
@@ -2133,6 +2136,39 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   // the order-free kernel only needs one entry per accumulator pass (P windows):
   // a table P times smaller, two adjacent words per in-edge and pass.
   const bool coarse = L_.nonpos;
+  // Sample-major push (K6, k_push.cu): every product is the same positive
+  // constant, every bias <= 0, the out-neurons' 8-bit counters fit shared
+  // memory and no in-degree can overflow them.  Selected with
+  // sk_tuning.exact_kernel = 3 only: measured slower than the windowed kernel
+  // (cfg4 1.40 vs 1.09 ms, cfg3 1.09 vs 0.76 ms -- its random counter
+  // increments meet ~3.5-way shared-memory bank conflicts per atomic, where the
+  // windowed kernel's lanes update consecutive samples; DESIGN.md §4 K6).
+  if (L_.wT && coarse && probe.q_const && ctx->tune.exact_kernel == 3 &&
+      L_.wstats.maxdeg <= 255 && push_smem(m) <= 64 * 1024) {
+    union {
+      uint32_t u;
+      float f;
+    } wc{L_.wstats.vmin}, yc{ystats.vmin};
+    const float v = wc.f * yc.f;  // the constant product (exact: products_exact)
+    if (v > 0.0f && std::isfinite(L_.negmin)) {
+      // the smallest count any row's threshold admits: c v > -b_i for some row
+      double c = std::floor(L_.negmin / double(v)) + 1.0;
+      while (c > 1.0 && (c - 1.0) * double(v) > L_.negmin) c -= 1.0;
+      while (c * double(v) <= L_.negmin) c += 1.0;
+      const uint32_t cmin = c > 256.0 ? 256u : uint32_t(c);
+      sk_csr* o = push_layer(ctx, L_.wT, y0, m, L_.bias, clip, v, cmin);
+      if (o) {
+        ctx->last_exact.launches += 1;
+        ctx->last_exact.kernel = 3;
+        ctx->last_exact.group = 0;
+        ctx->last_exact.records = 0;
+        ctx->last_exact.window_log2 = 0;
+        ctx->last_exact.fields = 4;
+        *wp_out_ptr = nullptr;
+        return o;
+      }
+    }
+  }
   int plp = 0;
   while ((1u << plp) < probe.fx_pack) ++plp;
   WinGeom gc = g;

@@ -363,6 +363,12 @@ sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, con
                           float clip, uint64_t dense_rows, double negmin = INFINITY);
 sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* m, const sk_csr* y0,
                             float clip, uint64_t* nnz_trace);
+// W^T of a model layer (out-edges), built on first use and cached (k_esc.cu).
+const sk_csr* model_layer_transpose(sk_ctx* ctx, sk_model* mm, uint32_t k);
+// K6 (k_push.cu): the sample-major push layer; nullptr when the counters do not fit.
+size_t push_smem(uint32_t m);
+sk_csr* push_layer(sk_ctx* ctx, const sk_csr* wT, const sk_csr* y, uint32_t m, const float* bias,
+                   float clip, float v, uint32_t cmin);
 void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b,
                           uint32_t M, uint32_t K, uint32_t N, const float* bias,
                           int relu, float* c);
