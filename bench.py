@@ -541,8 +541,10 @@ def run_ours(args, w):
         bblocks = [np.full(r1 - r0, w["bias"], np.float32)] * L
         Y0 = sk.gen_input_binary(m, Bg, kY_of(w), SEED)
         peer = shard.PeerExchange(m, ctx=ctx) if args.exchange == "peer" else None
+        plan = shard.ColShardPlan(blocks, bblocks, device=dev)  # device biases, agreed flags
         run = lambda y: shard.relu_forward_sparse_colsharded(  # noqa
-            blocks, bblocks, y, w["clip"], device=dev, exchange=args.exchange, peer=peer)
+            blocks, bblocks, y, w["clip"], device=dev, exchange=args.exchange, peer=peer,
+            plan=plan)
         host_rp, host_ci, host_v = (np.array(a) for a in Y0.extract())
         nnz0 = int(host_rp[-1])
     elif w["y0"] == "binary":

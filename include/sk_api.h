@@ -283,6 +283,15 @@ sk_status sk_relu_forward_sparse(sk_ctx* ctx, const sk_model* m,
  * Bitwise the same either way. */
 sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* bias,
                           const sk_csr* y, float clip, sk_csr** out);
+/* sk_sparse_layer for callers that run the same weight block many times (the
+ * column-sharded forward): the bias is already on the device (w->rows floats)
+ * and its two summaries are precomputed -- dense_rows = the number of rows with
+ * !(b_i <= 0) (their untouched positions survive), negmin = min over b_i <= 0
+ * of -b_i (+inf when there is none).  Does not synchronise beyond what the
+ * layer itself needs. */
+sk_status sk_sparse_layer_dev(sk_ctx* ctx, const sk_csr* w, const float* d_bias,
+                              uint64_t dense_rows, double negmin, const sk_csr* y, float clip,
+                              sk_csr** out);
 /* Column-sharded exchange over peer memory (no reference counterpart).
  * sk_ipc_alloc: a cudaMalloc'd buffer of `bytes` and its 64-byte CUDA IPC
  * handle; sk_ipc_open maps a peer's handle (peer access over NVLink);

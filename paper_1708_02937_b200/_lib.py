@@ -40,7 +40,7 @@ EXPORTS = [
     "sk_model_create", "sk_model_shape", "sk_model_free",
     "sk_layer_step", "sk_relu_forward", "sk_relu_forward_host", "sk_relu_forward_sparse",
     "sk_categories_csr", "sk_categories_dense",
-    "sk_sparse_layer", "sk_csr_device_arrays", "sk_csr_from_device", "sk_memcpy_d2d",
+    "sk_sparse_layer", "sk_sparse_layer_dev", "sk_csr_device_arrays", "sk_csr_from_device", "sk_memcpy_d2d",
     "sk_ipc_alloc", "sk_ipc_open", "sk_ipc_close", "sk_ipc_free", "sk_csr_publish",
     "sk_dense_layer_step", "sk_dense_relu_forward",
     "sk_gen_layer_fixed", "sk_gen_layer_density", "sk_gen_weight",
@@ -137,6 +137,8 @@ def load() -> C.CDLL:
     L.sk_relu_forward_host.argtypes = [vp, vp, C.c_uint32, vp, C.POINTER(FwdOpts), vp]
     L.sk_relu_forward_sparse.argtypes = [vp, vp, vp, C.POINTER(FwdOpts), C.POINTER(vp), vp]
     L.sk_sparse_layer.argtypes = [vp, vp, vp, vp, C.c_float, C.POINTER(vp)]
+    L.sk_sparse_layer_dev.argtypes = [vp, vp, vp, C.c_uint64, C.c_double, vp, C.c_float,
+                                      C.POINTER(vp)]
     L.sk_csr_device_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
     L.sk_csr_from_device.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_size_t, vp, vp, vp,
                                      C.POINTER(vp)]

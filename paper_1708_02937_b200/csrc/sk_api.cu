@@ -736,6 +736,23 @@ extern "C" sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* 
   });
 }
 
+extern "C" sk_status sk_sparse_layer_dev(sk_ctx* ctx, const sk_csr* w, const float* d_bias,
+                                         uint64_t dense_rows, double negmin, const sk_csr* y,
+                                         float clip, sk_csr** out) {
+  return guarded([&] {
+    csr_ready(ctx, w);
+    csr_ready(ctx, y);
+    require_ctx(ctx);
+    if (w->cols != y->rows)
+      fail(SK_ERR_DIMENSION, "weight is " + dim_string(w->rows, w->cols) + " but input has " +
+                                 std::to_string(y->rows) + " rows");
+    if (!d_bias && w->rows)
+      fail(SK_ERR_DIMENSION, "bias length 0 does not match " + std::to_string(w->rows) +
+                                 " output rows");
+    *out = sparse_layer_impl(ctx, w, d_bias, y, clip, dense_rows, negmin);
+  });
+}
+
 extern "C" sk_status sk_csr_device_arrays(const sk_csr* a, uint32_t** rp, uint32_t** ci,
                                           float** v) {
   return guarded([&] {

@@ -904,6 +904,26 @@ def sparse_layer(w: CsrMatrix, bias, y: CsrMatrix, clip: float = 0.0) -> CsrMatr
     return CsrMatrix(w.rows(), y.cols(), ctx=y.ctx, _handle=h)
 
 
+def sparse_layer_dev(w: CsrMatrix, d_bias: int, dense_rows: int, negmin: float, y: CsrMatrix,
+                     clip: float = 0.0) -> CsrMatrix:
+    """sparse_layer with a device-resident bias (pointer to w.rows() floats) and
+    its summaries precomputed (sk_sparse_layer_dev): dense_rows = rows with
+    !(b <= 0), negmin = min of -b over b <= 0 (inf if none)."""
+    h = vp()
+    _check(y.ctx._L.sk_sparse_layer_dev(y.ctx.h, w.h, vp(d_bias), int(dense_rows), float(negmin),
+                                        y.h, float(clip), C.byref(h)))
+    return CsrMatrix(w.rows(), y.cols(), ctx=y.ctx, _handle=h)
+
+
+def bias_summaries(bias) -> tuple[int, float]:
+    """(dense_rows, negmin) of a bias vector, as sk_sparse_layer_dev expects."""
+    b = _f32(bias)
+    nonpos = b <= 0.0
+    dense_rows = int(b.size - np.count_nonzero(nonpos))
+    negmin = float(np.min(-b[nonpos].astype(np.float64))) if np.any(nonpos) else math.inf
+    return dense_rows, negmin
+
+
 def csr_device_arrays(a: CsrMatrix):
     """(row_ptr, col_idx, values) device pointers of a handle (zero-copy)."""
     rp, ci, v = vp(), vp(), vp()

@@ -171,6 +171,16 @@ class PeerExchange:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.cap = 0
         self.sets = [None, None]
+        self.layers = 0  # exchanged layers so far (all calls): picks the ping-pong set
+
+    def next_set(self) -> int:
+        """The buffer set of the next exchanged layer.  The count runs across
+        calls, so consecutive exchanges always alternate: a rank writes a set
+        again only after every rank passed the barrier of the exchange that read
+        it (no end-of-call barrier needed)."""
+        s = self.layers % 2
+        self.layers += 1
+        return s
 
     def _free_all(self):
         # every rank unmaps its peers' buffers before any owner frees its own
@@ -228,67 +238,89 @@ class PeerExchange:
         self._free_all()
 
 
+class ColShardPlan:
+    """Per-model state of the column-sharded forward, built once and reused by
+    every call: each layer block's bias on the device with its two summaries
+    (sk_sparse_layer_dev), and the per-layer "every bias <= 0 on every rank"
+    flags agreed with ONE all-reduce."""
+
+    def __init__(self, w_blocks, b_blocks, device=None, group=None):
+        import torch
+        from . import semikern as skm
+        dist = _dist()
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.w_blocks = list(w_blocks)
+        self.d_bias = [torch.as_tensor(np.ascontiguousarray(b, np.float32), device=device)
+                       for b in b_blocks]
+        self.summ = [skm.bias_summaries(b) for b in b_blocks]
+        flags = torch.tensor([1 if np.all(np.asarray(b, np.float32) <= 0.0) else 0
+                              for b in b_blocks], dtype=torch.int32, device=device)
+        if dist.is_initialized() and len(b_blocks):
+            dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=group)
+        self.nonpos = [bool(x) for x in flags.cpu().tolist()]
+        torch.cuda.synchronize(device)
+
+
 def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None, device=None,
-                                   exchange="peer", peer=None):
+                                   exchange="peer", peer=None, plan=None, exchange_single=False):
     """Column-sharded sparse forward pass.  `w_blocks[k]` is this rank's block
     of output-neuron rows of W_ref[k] (a CsrMatrix m_g x m), `b_blocks[k]` its
     bias slice, `y0` the full m x n input (replicated).  Returns (Y_L, trace).
-    Per layer: local block SpGEMM + epilogue on the GPU (sk_sparse_layer: the
-    order-free kernel when the layer's partial sums are provably exact), then
-    one exchange of the sparse row blocks; runs of layers with an empty input
-    and every bias <= 0 are skipped on every rank at once.  exchange="peer": the
-    block counts go through one tiny NCCL all-gather, then ONE kernel per rank
-    stores its block into every rank's next-layer buffers over NVLink (CUDA
+    Per layer: local block SpGEMM + epilogue on the GPU (sk_sparse_layer_dev:
+    the order-free kernel when the layer's partial sums are provably exact),
+    then one exchange of the sparse row blocks; runs of layers with an empty
+    input and every bias <= 0 are skipped on every rank at once.  exchange="peer":
+    the block counts go through one tiny NCCL all-gather, then ONE kernel per
+    rank stores its block into every rank's next-layer buffers over NVLink (CUDA
     IPC, PeerExchange; pass `peer` to reuse its buffers across calls);
-    exchange="nccl": padded NCCL all-gathers of the blocks."""
+    exchange="nccl": padded NCCL all-gathers of the blocks.  With one rank the
+    exchange is the identity and is skipped (exchange_single=True runs it anyway,
+    for tests).  Pass `plan` (ColShardPlan) to reuse the per-layer device biases
+    and flags across calls."""
     import torch
     from . import semikern as skm
     dist = _dist()
     if device is None:
         device = torch.device("cuda", torch.cuda.current_device())
+    if plan is None:
+        plan = ColShardPlan(w_blocks, b_blocks, device=device, group=group)
     m, n = y0.rows(), y0.cols()
-    L = len(w_blocks)
-    # Per layer, is every bias <= 0 on every rank?  Then an empty input stays
-    # empty (untouched positions give epilogue(0 + b) = 0): those layers need no
-    # work and no exchange.  Every rank holds the same full Y_k, so all ranks
-    # take the same decision.
-    flags = torch.tensor([1 if np.all(np.asarray(b, np.float32) <= 0.0) else 0 for b in b_blocks],
-                         dtype=torch.int32, device=device)
-    if dist.is_initialized() and L:
-        dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=group)
-    nonpos = [bool(x) for x in flags.cpu().tolist()]
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
     y = y0
     trace = [y.nnz()]
     own_peer = None
-    for k, (w, b) in enumerate(zip(w_blocks, b_blocks)):
-        if y.nnz() == 0 and nonpos[k]:
+    for k, w in enumerate(plan.w_blocks):
+        if y.nnz() == 0 and plan.nonpos[k]:
             trace.append(0)
             continue
-        local = skm.sparse_layer(w, b, y, clip)
+        dense_rows, negmin = plan.summ[k]
+        local = skm.sparse_layer_dev(w, plan.d_bias[k].data_ptr(), dense_rows, negmin, y, clip)
+        if world == 1 and not exchange_single:  # one block: the exchange is the identity
+            y = local
+            trace.append(y.nnz())
+            continue
         if exchange == "peer":
-            rank = dist.get_rank(group) if dist.is_initialized() else 0
-            world = dist.get_world_size(group) if dist.is_initialized() else 1
             cnt = torch.tensor([local.nnz()], dtype=torch.int64, device=device)
-            cnts = [cnt]
-            if world > 1:
-                cnts = [torch.zeros_like(cnt) for _ in range(world)]
-                dist.all_gather(cnts, cnt, group=group)
+            cnts = [torch.zeros_like(cnt) for _ in range(world)]
+            dist.all_gather(cnts, cnt, group=group)
             off, nnz = exchange_plan([int(c.item()) for c in cnts], rank)
             if peer is None:
                 peer = own_peer = PeerExchange(m, group=group, ctx=y0.ctx)
             peer.ensure(nnz)
             r0, _ = block_range(m, world, rank)
-            peer.publish(local, k, r0, off, rank == world - 1)
+            s = peer.next_set()
+            peer.publish(local, s, r0, off, rank == world - 1)
             # the publish kernel runs on the library context's stream: this rank's
             # stores have landed once that stream is drained ...
             local.ctx.synchronize()
-            if world > 1:
-                # ... and every rank's once the collective has completed on the host
-                # side (all ranks enter it only after their own publish finished)
-                flag = torch.zeros(1, device=device)
-                dist.all_reduce(flag, group=group)
-                flag.item()
-            lrp, lci, lv = peer.local(k)
+            # ... and every rank's once the collective has completed on the host
+            # side (all ranks enter it only after their own publish finished)
+            flag = torch.zeros(1, device=device)
+            dist.all_reduce(flag, group=group)
+            flag.item()
+            lrp, lci, lv = peer.local(s)
             y = skm.csr_from_device(m, n, nnz, lrp, lci, lv, ctx=y0.ctx)
             y.ctx.synchronize()
         else:
@@ -301,8 +333,6 @@ def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None,
                                     ctx=y0.ctx)
             y.ctx.synchronize()
         trace.append(nnz)
-    if dist.is_initialized():
-        dist.barrier(group=group)
     if own_peer is not None:  # y is an owned copy: the exchange buffers can go
         own_peer.close()
     return y, trace

@@ -766,7 +766,7 @@ def test_column_sharded_forward_single_rank_nccl(sk, port, exchange):
         y, trace = relu_forward_sparse_colsharded([dev_csr(sk, w) for w in hW], bs,
                                                   dev_csr(sk, hY), clip=32.0,
                                                   device=torch.device("cuda", 0),
-                                                  exchange=exchange)
+                                                  exchange=exchange, exchange_single=True)
         want, want_trace = hY, [hY.nnz]
         for w, b in zip(hW, bs):
             want = port.layer_sparse(w, b, want, 32.0)
