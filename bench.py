@@ -502,6 +502,20 @@ def ctx_fma_peak(sk):
     return p.multi_processor_count * 128 * clk / 2
 
 
+def sample_plan(Bg, world, rank, cols, strong):
+    """(first sample, samples on this rank, samples of the whole job).  Column
+    sharding: every rank holds the whole batch.  Strong batch-row scaling: the one
+    global batch split by the reference's count*w/nw rule
+    (proj/src/detail/parallel.hpp:29-43).  Weak: every rank its own Bg samples."""
+    from paper_1708_02937_b200 import shard
+    if cols:
+        return 0, Bg, Bg
+    if strong:
+        b0, Bl = shard.batch_shard(Bg, world, rank)
+        return b0, Bl, Bg
+    return rank * Bg, Bg, Bg * world
+
+
 def run_ours(args, w):
     import torch
     R = Rank(args)
@@ -519,13 +533,7 @@ def run_ours(args, w):
     m, L, Bg = w["m"], w["L"], w["B"]
     cols = args.shard == "cols" and w["y0"] == "binary"
     strong = args.scaling == "strong"
-    if cols:
-        b0, Bl = 0, Bg
-    elif strong:
-        b0, Bl = shard.batch_shard(Bg, world, rank)
-    else:
-        b0, Bl = rank * Bg, Bg
-    job_batch = Bg if (cols or strong) else Bg * world
+    b0, Bl, job_batch = sample_plan(Bg, world, rank, cols, strong)
     layer1 = None
     if cols:
         # column sharding: this rank owns output neurons [r0, r1) of every W_ref and

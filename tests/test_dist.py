@@ -172,3 +172,35 @@ def test_grown_capacity_rule():
     assert grown_capacity(10, 0) == 1 << 16
     assert grown_capacity(70000, 1 << 16) == 1 << 17
     assert grown_capacity(100, 1 << 17) == 1 << 17
+
+
+def _w_strong_plan(rank, world):
+    """bench.py's strong-scaling plan for BASELINE cfg4 (one batch of 60000
+    samples split over the ranks): the shards tile the global batch exactly, the
+    job counts the global batch once, and each rank's generated input shard is
+    bitwise the matching slice of the single-process input (reduced width)."""
+    import bench
+    from oracle.oracle import Port
+    plans = [None] * world
+    mine = bench.sample_plan(60000, world, rank, cols=False, strong=True)
+    dist.all_gather_object(plans, mine)
+    spans = sorted((b, b + n) for b, n, _ in plans)
+    assert spans[0][0] == 0 and spans[-1][1] == 60000
+    assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+    assert {j for _, _, j in plans} == {60000}
+    assert bench.sample_plan(60000, world, rank, cols=False, strong=False) == \
+        (rank * 60000, 60000, 60000 * world)
+    P = Port.get()
+    m, kY = 2048, 9
+    b0, Bl, _ = mine
+    shard_y = P.gen_input_binary(m, Bl, kY, bench.SEED, sample_offset=b0)
+    full = P.gen_input_binary(m, 60000, kY, bench.SEED)
+    for k in range(0, m, 97):  # sampled rows: the shard is the global row's slice
+        row = full.col_idx[full.row_ptr[k]:full.row_ptr[k + 1]]
+        want = row[(row >= b0) & (row < b0 + Bl)] - b0
+        got = shard_y.col_idx[shard_y.row_ptr[k]:shard_y.row_ptr[k + 1]]
+        assert np.array_equal(got, want)
+
+
+def test_strong_scaling_plan_tiles_the_global_batch():
+    run_world(_w_strong_plan)
