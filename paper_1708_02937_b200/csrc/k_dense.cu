@@ -23,7 +23,8 @@ extern "C" sk_status sk_dense_mxm_baseline(sk_ctx* ctx, const sk_dense* a, const
       fail(SK_ERR_DIMENSION, "dense_mxm_baseline: inner dimensions " + std::to_string(a->cols) +
                                  " and " + std::to_string(b->rows) + " do not match");
     sk_dense* o = new_dense(ctx, a->rows, b->cols);
-    launch_dense_gemm_tc(ctx, a->d, b->d, a->rows, a->cols, b->cols, nullptr, 0, o->d);
+    launch_dense_gemm_tc(ctx, a->d, b->d, a->rows, a->cols, b->cols, nullptr, 0, o->d,
+                         const_cast<PackCache*>(&a->pack), a->version);
     *out = o;
   });
 }
@@ -41,7 +42,8 @@ extern "C" sk_status sk_dense_layer_step(sk_ctx* ctx, const sk_dense* w, const f
     float* db = dalloc<float>(ctx, w->rows);
     SK_CUDA(cudaMemcpyAsync(db, bias, size_t(w->rows) * 4, cudaMemcpyHostToDevice, ctx->stream));
     sk_dense* o = new_dense(ctx, w->rows, y->cols);
-    launch_dense_gemm_tc(ctx, w->d, y->d, w->rows, w->cols, y->cols, db, 1, o->d);
+    launch_dense_gemm_tc(ctx, w->d, y->d, w->rows, w->cols, y->cols, db, 1, o->d,
+                         const_cast<PackCache*>(&w->pack), w->version);
     dfree(ctx, db);
     sync(ctx);
     *out = o;
@@ -63,10 +65,18 @@ extern "C" sk_status sk_dense_relu_forward(sk_ctx* ctx, const sk_model* m, const
     const float* src = y0->d;
     int cur = 0;
     for (uint32_t k = 0; k < m->layers; ++k) {
-      sk_status st = sk_to_dense(ctx, m->w[k], 0.0f, &wd);
-      if (st != SK_OK) fail(st, sk_last_error());
-      launch_dense_gemm_tc(ctx, wd->d, src, nn, nn, n, m->bias + size_t(k) * nn, 1, bufs[cur]->d);
-      sk_dense_free(wd);
+      // the densified weights are only needed to (re)build the packed copy cached
+      // on the immutable CSR handle (dnn.cpp:145 re-densifies every layer; the
+      // split / pack of a layer's weights happens once per model here)
+      PackCache* pc = &const_cast<sk_csr*>(m->w[k])->pack;
+      const bool cached = pc->buf && pc->version == 0;
+      if (!cached) {
+        sk_status st = sk_to_dense(ctx, m->w[k], 0.0f, &wd);
+        if (st != SK_OK) fail(st, sk_last_error());
+      }
+      launch_dense_gemm_tc(ctx, cached ? nullptr : wd->d, src, nn, nn, n,
+                           m->bias + size_t(k) * nn, 1, bufs[cur]->d, pc, 0);
+      if (!cached) sk_dense_free(wd);
       src = bufs[cur]->d;
       cur ^= 1;
     }

@@ -543,7 +543,8 @@ __global__ void __launch_bounds__(6 * 32, 1)
 }  // namespace tc
 
 void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t M, uint32_t K,
-                          uint32_t N, const float* bias, int relu, float* c) {
+                          uint32_t N, const float* bias, int relu, float* c, PackCache* cache,
+                          uint64_t version) {
   if (M == 0 || N == 0) return;
   {
     // v3 kernel: pack (split once) + bulk-copy pipeline
@@ -551,17 +552,30 @@ void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t 
     using G = tc::Cfg3<BNp, NSp>;
     const uint32_t Mp = ceil_div(M, tc::BM) * tc::BM, Np = ceil_div(N, BNp) * BNp;
     const uint32_t Kp = ceil_div(K, tc::kPK) * tc::kPK;
-    float* buf = dalloc<float>(ctx, 2 * (size_t(Mp) + Np) * Kp);
-    float* ahi = buf;
+    // A's packed halves: from the owner's cache when it is current, else packed
+    // here (and kept in the cache when there is one)
+    const bool hit = cache && cache->buf && cache->version == version;
+    if (cache && !hit && cache->buf) {
+      dfree(ctx, cache->buf);
+      cache->buf = nullptr;
+    }
+    float* abuf = hit ? cache->buf : dalloc<float>(ctx, 2 * size_t(Mp) * Kp);
+    float* buf = dalloc<float>(ctx, 2 * size_t(Np) * Kp);
+    float* ahi = abuf;
     float* alo = ahi + size_t(Mp) * Kp;
-    float* bhi = alo + size_t(Mp) * Kp;
+    float* bhi = buf;
     float* blo = bhi + size_t(Np) * Kp;
     smem_attr(ctx, tc::k_gemm_packed<BNp, NSp>, int(G::kSmem));
     timing_mark(ctx, SK_KT_GEMM_TC);
     const uint64_t wa = uint64_t(Mp / 32) * (Kp / tc::kPK), wb = uint64_t(Np / 32) * (Kp / tc::kPK);
-    SK_LAUNCH(tc::k_pack_split,
-              unsigned(std::min<uint64_t>((wa + 7) / 8, uint64_t(ctx->num_sms) * 16)), 256, 0,
-              ctx->stream, a, M, K, K, 0, tc::BM, Mp, Kp, ahi, alo);
+    if (!hit)
+      SK_LAUNCH(tc::k_pack_split,
+                unsigned(std::min<uint64_t>((wa + 7) / 8, uint64_t(ctx->num_sms) * 16)), 256, 0,
+                ctx->stream, a, M, K, K, 0, tc::BM, Mp, Kp, ahi, alo);
+    if (cache && !hit) {
+      cache->buf = abuf;
+      cache->version = version;
+    }
     SK_LAUNCH(tc::k_pack_split,
               unsigned(std::min<uint64_t>((wb + 7) / 8, uint64_t(ctx->num_sms) * 16)), 256, 0,
               ctx->stream, b, N, K, N, 1, uint32_t(BNp), Np, Kp, bhi, blo);
@@ -570,6 +584,7 @@ void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b, uint32_t 
               bhi, blo, M, N, Kp / tc::kPK, bias, relu, c);
     timing_mark(ctx);
     dfree(ctx, buf);
+    if (!cache) dfree(ctx, abuf);
   }
 }
 

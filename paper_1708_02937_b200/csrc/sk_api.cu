@@ -92,6 +92,7 @@ void csr_release(sk_csr* a) {
     dfree(a->ctx, a->ci);
     dfree(a->ctx, a->v);
     if (a->tile_vals) dfree(a->ctx, a->tile_vals);
+    if (a->pack.buf) dfree(a->ctx, a->pack.buf);
     if (a->tile_mask) dfree(a->ctx, a->tile_mask);
     delete a;
   }
@@ -455,6 +456,7 @@ extern "C" sk_status sk_dense_upload(sk_ctx* ctx, uint32_t rows, uint32_t cols,
 extern "C" sk_status sk_dense_write(sk_ctx* ctx, sk_dense* d, const float* host) {
   return guarded([&] {
     require_ctx(ctx);
+    d->version += 1;  // invalidates derived copies (K4's packed operand)
     if (d->elems())
       SK_CUDA(cudaMemcpyAsync(d->d, host, d->elems() * sizeof(float),
                               cudaMemcpyHostToDevice, ctx->stream));
@@ -503,6 +505,7 @@ extern "C" sk_status sk_dense_free(sk_dense* d) {
   return guarded([&] {
     if (!d) return;
     dfree(d->ctx, d->d);
+    if (d->pack.buf) dfree(d->ctx, d->pack.buf);
     delete d;
   });
 }

@@ -128,11 +128,20 @@ struct sk_ctx {
   std::vector<void*> arena_spill;  // overflow allocations of the current call
 };
 
+// K4's split-and-packed copy of a weight operand (tf32 hi / lo halves in the
+// UMMA K-major tile layout), cached on the handle it was made from.
+struct PackCache {
+  float* buf = nullptr;      // hi then lo
+  uint64_t version = ~0ull;  // the owner's version it was made from
+};
+
 struct sk_dense {
   sk_ctx* ctx = nullptr;
   uint32_t rows = 0, cols = 0;
   float* d = nullptr;
   size_t elems() const { return size_t(rows) * cols; }
+  uint64_t version = 0;  // bumped by every in-place write (sk_dense_write)
+  PackCache pack;        // as K4's A operand (dense_mxm_baseline / dense_layer_step)
 };
 
 // Per-matrix value statistics (the exactness test of the sparse engine): the
@@ -176,6 +185,8 @@ struct sk_csr {
   // masks), built on first use and cached like the statistics (k_spmm.cu)
   float* tile_vals = nullptr;
   uint32_t* tile_mask = nullptr;
+  // K4's packed copy of the densified weights (dense_relu_forward)
+  PackCache pack;
 };
 
 
@@ -369,8 +380,10 @@ const sk_csr* model_layer_transpose(sk_ctx* ctx, sk_model* mm, uint32_t k);
 size_t push_smem(uint32_t m);
 sk_csr* push_layer(sk_ctx* ctx, const sk_csr* wT, const sk_csr* y, uint32_t m, const float* bias,
                    float clip, float v, uint32_t cmin);
+// C = A.B (+ bias, ReLU) on tcgen05 (3xTF32).  With `cache` (owned by A's
+// handle, current for `version`), A's split/pack is reused across calls.
 void launch_dense_gemm_tc(sk_ctx* ctx, const float* a, const float* b,
                           uint32_t M, uint32_t K, uint32_t N, const float* bias,
-                          int relu, float* c);
+                          int relu, float* c, PackCache* cache = nullptr, uint64_t version = 0);
 
 }  // namespace sk

@@ -337,6 +337,15 @@ class DenseMatrix:
     def __call__(self, i: int, j: int) -> float:
         return float(self.numpy()[i, j])
 
+    def write(self, a):
+        """Overwrite the values in place from a host array of the same shape
+        (sk_dense_write; stream-ordered).  Invalidates derived device copies."""
+        a = np.ascontiguousarray(a, np.float32)
+        if a.shape != (self.rows(), self.cols()):
+            raise DimensionError(f"write of {a.shape} into {self.rows()}x{self.cols()}")
+        _check(self.ctx._L.sk_dense_write(self.ctx.h, self.h, a.ctypes.data))
+        self.ctx.synchronize()  # the host array is borrowed
+
     def device_ptr(self) -> int:
         return int(self.ctx._L.sk_dense_device_ptr(self.h) or 0)
 

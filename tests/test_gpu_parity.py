@@ -817,3 +817,32 @@ def test_dense_layer_step_cfg2_density_matches_reference(sk, ref, port):
     pre = (wd.astype(np.float64) @ y.astype(np.float64)) + b[:, None]
     near = np.abs(pre) <= 1e-5 * scale + 1e-6
     assert ((got != 0) == (want != 0))[~near].all()
+
+
+def test_dense_leg_packed_weights_cache(sk, ref, port):
+    """K4 keeps the split/packed weights on the handle: repeated calls reuse it,
+    an in-place write invalidates it, and dense_relu_forward's per-model copy
+    gives the same result on every call (tolerance of approx_equal_scaled)."""
+    m, n = 512, 128
+    W = port.gen_layer_density(m, 0.1, port.layer_seed(11, 0))
+    wd = W.to_dense()
+    y = port.gen_input_dense(m, n, 11)
+    b = np.full(m, -0.05, np.float32)
+    Wd = sk.DenseMatrix.from_numpy(wd)
+    yd = sk.DenseMatrix.from_numpy(y)
+
+    def check(got, wmat):
+        want = ref.dense_layer_step(wmat, b, y, workers=8)
+        scale = np.abs(wmat).astype(np.float64) @ np.abs(y).astype(np.float64)
+        assert (np.abs(got.astype(np.float64) - want) <= np.maximum(1e-6, 1e-5 * scale)).all()
+
+    first = sk.dense_layer_step(Wd, b, yd).numpy()
+    check(first, wd)
+    assert np.array_equal(sk.dense_layer_step(Wd, b, yd).numpy(), first)  # cached pack
+    wd2 = (wd * -0.5).astype(np.float32)
+    Wd.write(wd2)  # invalidates the cached pack
+    check(sk.dense_layer_step(Wd, b, yd).numpy(), wd2)
+    model = sk.DnnModel([dev_csr(sk, W)] * 2, [b, b])
+    r1 = sk.dense_relu_forward(model, yd).numpy()
+    r2 = sk.dense_relu_forward(model, yd).numpy()
+    assert np.array_equal(r1, r2)
