@@ -202,7 +202,13 @@ sk_status sk_csr_from_pattern(sk_ctx* ctx, uint32_t rows, uint32_t cols,
  * the copies run there, overlapping work queued on the context's stream, and
  * every later use of the handle is ordered after them (an event on the handle).
  * The host arrays must stay valid (and should be page-locked) until then.  For
- * double-buffered input uploads.  No reference counterpart. */
+ * double-buffered input uploads.  No reference counterpart.
+ * TRUSTED INPUT ONLY: nothing checks that row_ptr is non-decreasing with
+ * row_ptr[rows] = nnz, or that each row's columns are strictly increasing and
+ * below `cols` (the invariants of the reference's validating CsrMatrix
+ * constructor, matrix.cpp:89-119).  The kernels index shared memory by column,
+ * so a violating pattern is undefined behaviour -- validate it once with
+ * sk_csr_from_pattern(..., validate = 1) when its origin is not trusted. */
 sk_status sk_csr_from_pattern_async(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                                     const uint32_t* row_ptr, const uint32_t* col_idx,
                                     float value, void* stream, sk_csr** out);
