@@ -592,8 +592,10 @@ def run_ours(args, w):
         out, res["trace"] = run(Y0)
         del out
 
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ (launch lists)
     with sampler as clocks:
         ms_max = timed_steps(R, stream, args.steps, step)
+    torch.cuda.nvtx.range_pop()
     trace = res.get("trace", trace)
     launches = sk._lib.launches() - launches0
     ktimes, ktags = ctx.kernel_times_tagged()
