@@ -363,7 +363,7 @@ extern "C" sk_status sk_csr_from_pattern_async(sk_ctx* ctx, uint32_t rows, uint3
     void* p = nullptr;
     SK_CUDA(cudaMallocAsync(&p, (size_t(rows) + 1) * 4, s));
     a->rp = static_cast<uint32_t*>(p);
-    SK_CUDA(cudaMallocAsync(&p, std::max<size_t>(nnz, 1) * 4, s));
+    SK_CUDA(cudaMallocAsync(&p, (nnz + kCiPad) * 4, s));
     a->ci = static_cast<uint32_t*>(p);
     SK_CUDA(cudaMallocAsync(&p, std::max<size_t>(nnz, 1) * 4, s));
     a->v = static_cast<float*>(p);

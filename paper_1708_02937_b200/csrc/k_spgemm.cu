@@ -2008,7 +2008,7 @@ static sk_csr* sparse_segment(sk_ctx* ctx, const sk_model* md, const sk_csr* y0,
       o->cols = n;
       o->nnz = nnz;
       o->rp = dalloc<uint32_t>(ctx, size_t(m) + 1);
-      o->ci = dalloc<uint32_t>(ctx, nnz);
+      o->ci = dalloc<uint32_t>(ctx, nnz + kCiPad);
       o->v = dalloc<float>(ctx, nnz);
       if (res == -1 || nnz == 0) {
         SK_CUDA(cudaMemsetAsync(o->rp, 0, (size_t(m) + 1) * 4, ctx->stream));

@@ -76,7 +76,7 @@ sk_csr* new_csr(sk_ctx* ctx, uint32_t rows, uint32_t cols, size_t nnz) {
   a->cols = cols;
   a->nnz = nnz;
   a->rp = dalloc<uint32_t>(ctx, size_t(rows) + 1);
-  a->ci = dalloc<uint32_t>(ctx, nnz);
+  a->ci = dalloc<uint32_t>(ctx, nnz + kCiPad);
   a->v = dalloc<float>(ctx, nnz);
   return a;
 }

@@ -163,6 +163,13 @@ struct ValueStats {
 // is c), on the host: the same rules as the device reduction (k_value_stats).
 ValueStats const_value_stats(float c, size_t nnz);
 
+// Every CSR column array carries kCiPad words of slack after its nnz entries,
+// so a kernel may read the aligned 16-byte block holding its last entries
+// without leaving the allocation.  (Measured for the exact layer's piece
+// gathers -- two 16-byte loads per 4-entry piece instead of four scalar ones:
+// cfg4 1.085 -> 1.131 ms, cfg5 2.36 -> 2.52 ms; not used there.)
+constexpr size_t kCiPad = 8;
+
 struct sk_csr {
   sk_ctx* ctx = nullptr;
   uint32_t rows = 0, cols = 0;
