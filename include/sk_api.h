@@ -298,6 +298,26 @@ sk_status sk_sparse_layer(sk_ctx* ctx, const sk_csr* w, const float* bias,
 sk_status sk_sparse_layer_dev(sk_ctx* ctx, const sk_csr* w, const float* d_bias,
                               uint64_t dense_rows, double negmin, const sk_csr* y, float clip,
                               sk_csr** out);
+/* The column-sharded layer with its exchange fused into the output gather (no
+ * reference counterpart; the boundary is dnn.cpp:117-119, where one layer's
+ * output becomes the next one's input).  sk_sparse_layer_stage computes the
+ * layer (sk_sparse_layer_dev semantics) up to its output count (*nnz) and
+ * keeps the block in the context's scratch; sk_staged_publish then writes it
+ * straight into `ndst` (<= 8) destinations -- entries at nnz_off, row pointers
+ * at row_off shifted by nnz_off, the closing pointer when write_last -- with
+ * the layer's own gather kernel (stores over NVLink into the peers' buffers),
+ * and releases the staged layer; sk_staged_free releases it unpublished.  No
+ * other call on the context may run between the two.  Layers that do not take
+ * the order-free exact path are finished in the stage call and published from
+ * the finished block. */
+typedef struct sk_staged sk_staged;
+sk_status sk_sparse_layer_stage(sk_ctx* ctx, const sk_csr* w, const float* d_bias,
+                                uint64_t dense_rows, double negmin, const sk_csr* y, float clip,
+                                sk_staged** out, uint64_t* nnz);
+sk_status sk_staged_publish(sk_ctx* ctx, sk_staged* st, uint32_t ndst, uint32_t* const* dst_rp,
+                            uint32_t* const* dst_ci, float* const* dst_v, uint32_t row_off,
+                            uint64_t nnz_off, int write_last);
+sk_status sk_staged_free(sk_staged* st);
 /* Column-sharded exchange over peer memory (no reference counterpart).
  * sk_ipc_alloc: a cudaMalloc'd buffer of `bytes` and its 64-byte CUDA IPC
  * handle; sk_ipc_open maps a peer's handle (peer access over NVLink);

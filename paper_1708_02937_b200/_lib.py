@@ -40,7 +40,8 @@ EXPORTS = [
     "sk_model_create", "sk_model_shape", "sk_model_free",
     "sk_layer_step", "sk_relu_forward", "sk_relu_forward_host", "sk_relu_forward_sparse",
     "sk_categories_csr", "sk_categories_dense",
-    "sk_sparse_layer", "sk_sparse_layer_dev", "sk_csr_device_arrays", "sk_csr_from_device", "sk_memcpy_d2d",
+    "sk_sparse_layer", "sk_sparse_layer_dev", "sk_sparse_layer_stage", "sk_staged_publish",
+    "sk_staged_free", "sk_csr_device_arrays", "sk_csr_from_device", "sk_memcpy_d2d",
     "sk_ipc_alloc", "sk_ipc_open", "sk_ipc_close", "sk_ipc_free", "sk_csr_publish",
     "sk_dense_layer_step", "sk_dense_relu_forward",
     "sk_gen_layer_fixed", "sk_gen_layer_density", "sk_gen_weight",
@@ -139,6 +140,11 @@ def load() -> C.CDLL:
     L.sk_sparse_layer.argtypes = [vp, vp, vp, vp, C.c_float, C.POINTER(vp)]
     L.sk_sparse_layer_dev.argtypes = [vp, vp, vp, C.c_uint64, C.c_double, vp, C.c_float,
                                       C.POINTER(vp)]
+    L.sk_sparse_layer_stage.argtypes = [vp, vp, vp, C.c_uint64, C.c_double, vp, C.c_float,
+                                        C.POINTER(vp), C.POINTER(C.c_uint64)]
+    L.sk_staged_publish.argtypes = [vp, vp, C.c_uint32, C.POINTER(vp), C.POINTER(vp),
+                                    C.POINTER(vp), C.c_uint32, C.c_uint64, C.c_int]
+    L.sk_staged_free.argtypes = [vp]
     L.sk_csr_device_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
     L.sk_csr_from_device.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_size_t, vp, vp, vp,
                                      C.POINTER(vp)]

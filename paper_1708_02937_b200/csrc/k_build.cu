@@ -1107,26 +1107,34 @@ extern "C" sk_status sk_ipc_free(void* dptr) {
   });
 }
 
+namespace sk {
+void csr_publish_impl(sk_ctx* ctx, const sk_csr* blk, uint32_t ndst, uint32_t* const* dst_rp,
+                      uint32_t* const* dst_ci, float* const* dst_v, uint32_t row_off,
+                      uint64_t nnz_off, int write_last) {
+  csr_ready(ctx, blk);
+  if (ndst > 8) fail(SK_ERR_INVALID_ARGUMENT, "at most 8 destinations (one NVLink box)");
+  if (nnz_off + blk->nnz > 0xFFFFFFFFull)
+    fail(SK_ERR_INVALID_ARGUMENT, "exchange exceeds the 32-bit index range");
+  PublishDst d{};
+  for (uint32_t r = 0; r < ndst; ++r) {
+    d.rp[r] = dst_rp[r];
+    d.ci[r] = dst_ci[r];
+    d.v[r] = dst_v[r];
+  }
+  const uint64_t work = std::max<uint64_t>(blk->nnz, blk->rows);
+  const unsigned grid = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((work + 255) / 256, uint64_t(ctx->num_sms) * 8)));
+  SK_LAUNCH(k_csr_publish, grid, 256, 0, ctx->stream, blk->rp, blk->ci, blk->v, blk->rows,
+            blk->nnz, d, ndst, row_off, uint32_t(nnz_off), write_last);
+}
+}  // namespace sk
+
 extern "C" sk_status sk_csr_publish(sk_ctx* ctx, const sk_csr* blk, uint32_t ndst,
                                     uint32_t* const* dst_rp, uint32_t* const* dst_ci,
                                     float* const* dst_v, uint32_t row_off, uint64_t nnz_off,
                                     int write_last) {
   return guarded([&] {
     ipc_ctx(ctx);
-    csr_ready(ctx, blk);
-    if (ndst > 8) fail(SK_ERR_INVALID_ARGUMENT, "at most 8 destinations (one NVLink box)");
-    if (nnz_off + blk->nnz > 0xFFFFFFFFull)
-      fail(SK_ERR_INVALID_ARGUMENT, "exchange exceeds the 32-bit index range");
-    PublishDst d{};
-    for (uint32_t r = 0; r < ndst; ++r) {
-      d.rp[r] = dst_rp[r];
-      d.ci[r] = dst_ci[r];
-      d.v[r] = dst_v[r];
-    }
-    const uint64_t work = std::max<uint64_t>(blk->nnz, blk->rows);
-    const unsigned grid = unsigned(std::max<uint64_t>(
-        1, std::min<uint64_t>((work + 255) / 256, uint64_t(ctx->num_sms) * 8)));
-    SK_LAUNCH(k_csr_publish, grid, 256, 0, ctx->stream, blk->rp, blk->ci, blk->v, blk->rows,
-              blk->nnz, d, ndst, row_off, uint32_t(nnz_off), write_last);
+    csr_publish_impl(ctx, blk, ndst, dst_rp, dst_ci, dst_v, row_off, nnz_off, write_last);
   });
 }

@@ -1246,6 +1246,52 @@ __global__ void k_rp_from_wp(const uint32_t* wp, uint32_t rows, uint32_t nW, uin
     rp[i] = wp[size_t(i) * nW];
 }
 
+// The exact layer's gather fused with the column-sharded exchange: the output
+// block goes straight from the layer's scratch spans into every destination
+// (the peers' next-layer input buffers, over NVLink): entries at nnz_off + the
+// item's offset, row pointers at row_off shifted by nnz_off, and the closing
+// pointer when write_last -- no local copy of the block and no second pass.
+struct GatherDst {
+  uint32_t* rp[8];
+  uint32_t* ci[8];
+  float* v[8];
+};
+
+__global__ void k_gather_publish(const uint32_t* __restrict__ item_cnt,
+                                 const unsigned long long* __restrict__ item_off,
+                                 const uint32_t* __restrict__ wp_out, uint64_t items, uint32_t m,
+                                 uint32_t nW, const uint32_t* __restrict__ sc_c,
+                                 const float* __restrict__ sc_v, GatherDst dst, uint32_t nd,
+                                 uint32_t row_off, uint32_t nnz_off, int write_last) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t it0 = gw * 32; it0 < items; it0 += nw * 32) {
+    const uint32_t c = it0 + lane < items ? item_cnt[it0 + lane] : 0u;
+    uint32_t nz = __ballot_sync(0xffffffffu, c != 0);
+    while (nz) {
+      const int l = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t cl = __shfl_sync(0xffffffffu, c, l);
+      const unsigned long long src = item_off[it0 + l];
+      const size_t o = size_t(nnz_off) + wp_out[it0 + l];
+      for (uint32_t t = lane; t < cl; t += 32) {
+        const uint32_t cc = sc_c[src + t];
+        const float vv = sc_v[src + t];
+        for (uint32_t d = 0; d < nd; ++d) {
+          dst.ci[d][o + t] = cc;
+          dst.v[d][o + t] = vv;
+        }
+      }
+    }
+  }
+  const uint32_t rows = write_last ? m + 1 : m;
+  for (uint32_t i = uint32_t(gw) * 32 + lane; i < rows; i += uint32_t(nw) * 32) {
+    const uint32_t r = wp_out[size_t(i) * nW] + nnz_off;
+    for (uint32_t d = 0; d < nd; ++d) dst.rp[d][row_off + i] = r;
+  }
+}
+
 __global__ void k_count_products(const uint32_t* arp, const uint32_t* aci, uint32_t m,
                                  const uint32_t* brp, unsigned long long* total) {
   unsigned long long c = 0;
@@ -1764,6 +1810,24 @@ sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_semir
 // One layer on the order-free path for a weight block w (rows = output neurons,
 // possibly a row block of a layer), its device bias, its statistics and the
 // bias summary (nonpos: every b <= 0; negmin: min of -b_i over b_i <= 0).
+// A layer computed up to its output count, its block still in the scratch
+// spans (arena memory, kept open until published): the column-sharded exchange
+// learns every rank's count, then k_gather_publish writes the block straight
+// into the peers' buffers.  Layers that did not take the exact path keep their
+// finished block in `csr` and are published with k_csr_publish.
+struct StagedLayer {
+  sk_ctx* ctx = nullptr;
+  uint32_t m = 0, n = 0, nW = 0;
+  uint64_t items = 0, nnz = 0;
+  uint32_t* item_cnt = nullptr;
+  unsigned long long* item_off = nullptr;
+  uint32_t* wp_out = nullptr;
+  uint32_t* sc_c = nullptr;
+  float* sc_v = nullptr;
+  sk_csr* csr = nullptr;  // the non-exact fallback
+  bool arena_open = false;
+};
+
 struct ExactLayerIn {
   const sk_csr* w;
   const float* bias;  // device, w->rows
@@ -1772,6 +1836,7 @@ struct ExactLayerIn {
   double negmin;
   uint32_t stamp_layer;  // %globaltimer slot (ctx->stamps)
   const sk_csr* wT = nullptr;  // W^T (cached with a model) -- enables the push kernel
+  StagedLayer* stage = nullptr;  // stop before the gather (the exchange publishes it)
 };
 
 // Weight statistics of a bare CSR (value statistics + row bounds), cached on the
@@ -1787,11 +1852,17 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
 // everything else the windowed SpGEMM + epilogue.  All three are the ascending
 // fold of the reference bit for bit.
 sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const sk_csr* y,
-                          float clip, uint64_t dense_rows, double negmin) {
+                          float clip, uint64_t dense_rows, double negmin, StagedLayer* stage) {
+  auto finish = [&](sk_csr* o) {
+    if (!stage) return o;
+    stage->csr = o;  // published from the finished block
+    stage->nnz = o->nnz;
+    return static_cast<sk_csr*>(nullptr);
+  };
   if (y->nnz == 0 && dense_rows == 0) {
     sk_csr* o = new_csr(ctx, w->rows, y->cols, 0);
     SK_CUDA(cudaMemsetAsync(o->rp, 0, (size_t(w->rows) + 1) * 4, ctx->stream));
-    return o;
+    return finish(o);
   }
   if (ctx->tune.exact >= 0 && y->nnz && w->rows && y->cols) {
     const ValueStats ws = weight_stats(ctx, w);
@@ -1804,19 +1875,58 @@ sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, con
       in.nonpos = dense_rows == 0;
       in.negmin = negmin;
       in.stamp_layer = 0;
+      in.stage = stage;
       arena_begin(ctx);
       try {
         uint32_t* wp = nullptr;
         sk_csr* o = exact_layer_w(ctx, in, y, clip, ys, &wp);
+        if (stage && !o) {
+          stage->arena_open = true;  // the spans live until the publish
+          return nullptr;
+        }
         arena_end(ctx);
-        return o;
+        return finish(o);
       } catch (...) {
         arena_end(ctx);
         throw;
       }
     }
   }
-  return spgemm_impl(ctx, w, y, SK_ARITHMETIC, d_bias, clip, dense_rows);
+  return finish(spgemm_impl(ctx, w, y, SK_ARITHMETIC, d_bias, clip, dense_rows));
+}
+
+StagedLayer* stage_new(sk_ctx* ctx) {
+  auto* st = new StagedLayer;
+  st->ctx = ctx;
+  return st;
+}
+
+uint64_t stage_nnz(const StagedLayer* st) { return st->nnz; }
+
+void stage_publish(StagedLayer* st, uint32_t nd, uint32_t* const* rp, uint32_t* const* ci,
+                   float* const* v, uint32_t row_off, uint64_t nnz_off, int write_last) {
+  sk_ctx* ctx = st->ctx;
+  if (st->csr) {
+    csr_publish_impl(ctx, st->csr, nd, rp, ci, v, row_off, nnz_off, write_last);
+    return;
+  }
+  GatherDst d{};
+  for (uint32_t r = 0; r < nd; ++r) {
+    d.rp[r] = rp[r];
+    d.ci[r] = ci[r];
+    d.v[r] = v[r];
+  }
+  const uint64_t work = std::max<uint64_t>(st->items, uint64_t(st->m) + 1);
+  SK_LAUNCH(k_gather_publish, grid_warps(ctx, (work + 31) / 32 * 32), 256, 0, ctx->stream,
+            st->item_cnt, st->item_off, st->wp_out, st->items, st->m, st->nW, st->sc_c, st->sc_v,
+            d, nd, row_off, uint32_t(nnz_off), write_last);
+}
+
+void stage_free(StagedLayer* st) {
+  if (!st) return;
+  if (st->csr) csr_release(st->csr);
+  if (st->arena_open) arena_end(st->ctx);
+  delete st;
 }
 
 // ---- the sparse-activation forward pass -----------------------------------------
@@ -2268,6 +2378,21 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     sync(ctx);
     const uint32_t nnz = hp[0];
     const int ovf = int(hp[1]);
+    if (!ovf && L_.stage) {
+      StagedLayer* st = L_.stage;
+      st->m = m;
+      st->n = n;
+      st->nW = g.nW;
+      st->items = items;
+      st->nnz = nnz;
+      st->item_cnt = item_cnt;
+      st->item_off = item_off;
+      st->wp_out = wp_out;
+      st->sc_c = sc_c;
+      st->sc_v = sc_v;
+      *wp_out_ptr = nullptr;
+      return nullptr;
+    }
     if (!ovf) {
       // the layer's output, right-sized (an owned CSR: the caller releases it)
       sk_csr* o = new_csr(ctx, m, n, nnz);

@@ -756,6 +756,65 @@ extern "C" sk_status sk_sparse_layer_dev(sk_ctx* ctx, const sk_csr* w, const flo
   });
 }
 
+struct sk_staged {
+  sk::StagedLayer* st;
+};
+
+extern "C" sk_status sk_sparse_layer_stage(sk_ctx* ctx, const sk_csr* w, const float* d_bias,
+                                           uint64_t dense_rows, double negmin, const sk_csr* y,
+                                           float clip, sk_staged** out, uint64_t* nnz) {
+  return guarded([&] {
+    csr_ready(ctx, w);
+    csr_ready(ctx, y);
+    require_ctx(ctx);
+    if (w->cols != y->rows)
+      fail(SK_ERR_DIMENSION, "weight is " + dim_string(w->rows, w->cols) + " but input has " +
+                                 std::to_string(y->rows) + " rows");
+    if (!d_bias && w->rows)
+      fail(SK_ERR_DIMENSION, "bias length 0 does not match " + std::to_string(w->rows) +
+                                 " output rows");
+    StagedLayer* st = stage_new(ctx);
+    try {
+      sparse_layer_impl(ctx, w, d_bias, y, clip, dense_rows, negmin, st);
+    } catch (...) {
+      stage_free(st);
+      throw;
+    }
+    *nnz = stage_nnz(st);
+    *out = new sk_staged{st};
+  });
+}
+
+extern "C" sk_status sk_staged_publish(sk_ctx* ctx, sk_staged* st, uint32_t ndst,
+                                       uint32_t* const* dst_rp, uint32_t* const* dst_ci,
+                                       float* const* dst_v, uint32_t row_off, uint64_t nnz_off,
+                                       int write_last) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!st) fail(SK_ERR_INVALID_ARGUMENT, "null staged layer");
+    if (ndst > 8) fail(SK_ERR_INVALID_ARGUMENT, "at most 8 destinations (one NVLink box)");
+    if (nnz_off + stage_nnz(st->st) > 0xFFFFFFFFull)
+      fail(SK_ERR_INVALID_ARGUMENT, "exchange exceeds the 32-bit index range");
+    try {
+      stage_publish(st->st, ndst, dst_rp, dst_ci, dst_v, row_off, nnz_off, write_last);
+    } catch (...) {
+      stage_free(st->st);
+      delete st;
+      throw;
+    }
+    stage_free(st->st);  // (stream-ordered: the spans are reused only by later work)
+    delete st;
+  });
+}
+
+extern "C" sk_status sk_staged_free(sk_staged* st) {
+  return guarded([&] {
+    if (!st) return;
+    stage_free(st->st);
+    delete st;
+  });
+}
+
 extern "C" sk_status sk_csr_device_arrays(const sk_csr* a, uint32_t** rp, uint32_t** ci,
                                           float** v) {
   return guarded([&] {

@@ -377,8 +377,20 @@ void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b,
                           uint32_t n, sk_semiring s, float* out);
 sk_csr* mxm_csr_csr_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b,
                          sk_semiring s);
+// A staged column-shard layer (k_spgemm.cu): sparse_layer_impl with `stage`
+// returns nullptr and leaves the block to stage_publish.
+struct StagedLayer;
 sk_csr* sparse_layer_impl(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const sk_csr* y,
-                          float clip, uint64_t dense_rows, double negmin = INFINITY);
+                          float clip, uint64_t dense_rows, double negmin = INFINITY,
+                          StagedLayer* stage = nullptr);
+StagedLayer* stage_new(sk_ctx* ctx);
+uint64_t stage_nnz(const StagedLayer* st);
+void stage_publish(StagedLayer* st, uint32_t nd, uint32_t* const* rp, uint32_t* const* ci,
+                   float* const* v, uint32_t row_off, uint64_t nnz_off, int write_last);
+void stage_free(StagedLayer* st);
+void csr_publish_impl(sk_ctx* ctx, const sk_csr* blk, uint32_t nd, uint32_t* const* rp,
+                      uint32_t* const* ci, float* const* v, uint32_t row_off, uint64_t nnz_off,
+                      int write_last);
 sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* m, const sk_csr* y0,
                             float clip, uint64_t* nnz_trace);
 // W^T of a model layer (out-edges), built on first use and cached (k_esc.cu).

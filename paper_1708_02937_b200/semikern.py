@@ -924,6 +924,39 @@ def sparse_layer_dev(w: CsrMatrix, d_bias: int, dense_rows: int, negmin: float, 
     return CsrMatrix(w.rows(), y.cols(), ctx=y.ctx, _handle=h)
 
 
+class StagedLayer:
+    """A column-shard layer computed up to its output count (sk_sparse_layer_stage);
+    publish() writes the block into the exchange destinations with the layer's
+    own gather kernel and releases it."""
+
+    def __init__(self, ctx, h, nnz: int):
+        self.ctx, self.h, self.nnz = ctx, h, nnz
+
+    def publish(self, dst_rp, dst_ci, dst_v, row_off: int, nnz_off: int, write_last: bool):
+        nd = len(dst_rp)
+        arr = lambda xs: (vp * nd)(*[vp(x) for x in xs])  # noqa: E731
+        h, self.h = self.h, None
+        _check(self.ctx._L.sk_staged_publish(self.ctx.h, h, nd, arr(dst_rp), arr(dst_ci),
+                                             arr(dst_v), row_off, nnz_off, int(write_last)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx._L.sk_staged_free(self.h)
+        except Exception:
+            pass
+
+
+def sparse_layer_stage(w: CsrMatrix, d_bias: int, dense_rows: int, negmin: float, y: CsrMatrix,
+                       clip: float = 0.0) -> StagedLayer:
+    h = vp()
+    nnz = C.c_uint64()
+    _check(y.ctx._L.sk_sparse_layer_stage(y.ctx.h, w.h, vp(d_bias), int(dense_rows),
+                                          float(negmin), y.h, float(clip), C.byref(h),
+                                          C.byref(nnz)))
+    return StagedLayer(y.ctx, h, int(nnz.value))
+
+
 def bias_summaries(bias) -> tuple[int, float]:
     """(dense_rows, negmin) of a bias vector, as sk_sparse_layer_dev expects."""
     b = _f32(bias)

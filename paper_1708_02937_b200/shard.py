@@ -228,6 +228,12 @@ class PeerExchange:
         self.skm.csr_publish(blk, s["rp"][1], s["ci"][1], s["v"][1], row_off, nnz_off,
                              write_last)
 
+    def publish_staged(self, st, k: int, row_off: int, nnz_off: int, write_last: bool):
+        """Write a staged layer's block into every rank's set k % 2 with the
+        layer's own gather kernel (the exchange fused into the output gather)."""
+        s = self.sets[k % 2]
+        st.publish(s["rp"][1], s["ci"][1], s["v"][1], row_off, nnz_off, write_last)
+
     def local(self, k: int):
         s = self.sets[k % 2]
         return s["rp"][0], s["ci"][0], s["v"][0]
@@ -273,7 +279,9 @@ def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None,
     input and every bias <= 0 are skipped on every rank at once.  exchange="peer":
     the block counts go through one tiny NCCL all-gather, then ONE kernel per
     rank stores its block into every rank's next-layer buffers over NVLink (CUDA
-    IPC, PeerExchange; pass `peer` to reuse its buffers across calls);
+    IPC, PeerExchange; pass `peer` to reuse its buffers across calls) -- with
+    the exact path that kernel IS the layer's output gather (sk_sparse_layer_stage
+    / sk_staged_publish: the block never lands in a local buffer first);
     exchange="nccl": padded NCCL all-gathers of the blocks.  With one rank the
     exchange is the identity and is skipped (exchange_single=True runs it anyway,
     for tests).  Pass `plan` (ColShardPlan) to reuse the per-layer device biases
@@ -296,34 +304,40 @@ def relu_forward_sparse_colsharded(w_blocks, b_blocks, y0, clip=0.0, group=None,
             trace.append(0)
             continue
         dense_rows, negmin = plan.summ[k]
-        local = skm.sparse_layer_dev(w, plan.d_bias[k].data_ptr(), dense_rows, negmin, y, clip)
         if world == 1 and not exchange_single:  # one block: the exchange is the identity
-            y = local
+            y = skm.sparse_layer_dev(w, plan.d_bias[k].data_ptr(), dense_rows, negmin, y, clip)
             trace.append(y.nnz())
             continue
         if exchange == "peer":
-            cnt = torch.tensor([local.nnz()], dtype=torch.int64, device=device)
-            cnts = [torch.zeros_like(cnt) for _ in range(world)]
-            dist.all_gather(cnts, cnt, group=group)
+            # the layer up to its block's count; the block itself is written into
+            # every rank's buffers by the layer's own gather (sk_staged_publish)
+            st = skm.sparse_layer_stage(w, plan.d_bias[k].data_ptr(), dense_rows, negmin, y, clip)
+            cnt = torch.tensor([st.nnz], dtype=torch.int64, device=device)
+            cnts = [cnt]
+            if world > 1:
+                cnts = [torch.zeros_like(cnt) for _ in range(world)]
+                dist.all_gather(cnts, cnt, group=group)
             off, nnz = exchange_plan([int(c.item()) for c in cnts], rank)
             if peer is None:
                 peer = own_peer = PeerExchange(m, group=group, ctx=y0.ctx)
             peer.ensure(nnz)
             r0, _ = block_range(m, world, rank)
             s = peer.next_set()
-            peer.publish(local, s, r0, off, rank == world - 1)
-            # the publish kernel runs on the library context's stream: this rank's
-            # stores have landed once that stream is drained ...
-            local.ctx.synchronize()
+            peer.publish_staged(st, s, r0, off, rank == world - 1)
+            # the gather runs on the library context's stream: this rank's stores
+            # have landed once that stream is drained ...
+            y0.ctx.synchronize()
             # ... and every rank's once the collective has completed on the host
             # side (all ranks enter it only after their own publish finished)
-            flag = torch.zeros(1, device=device)
-            dist.all_reduce(flag, group=group)
-            flag.item()
+            if world > 1:
+                flag = torch.zeros(1, device=device)
+                dist.all_reduce(flag, group=group)
+                flag.item()
             lrp, lci, lv = peer.local(s)
             y = skm.csr_from_device(m, n, nnz, lrp, lci, lv, ctx=y0.ctx)
             y.ctx.synchronize()
         else:
+            local = skm.sparse_layer_dev(w, plan.d_bias[k].data_ptr(), dense_rows, negmin, y, clip)
             rp, ci, v = csr_to_torch(local, device)
             frp, fci, fv = allgather_csr_rows(rp, ci, v, group=group)
             nnz = int(frp[-1].item())

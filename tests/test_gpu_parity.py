@@ -744,6 +744,50 @@ def test_csr_publish_to_several_destinations(sk, port):
             assert np.all(ci[:nnz_off] == 9)
 
 
+@pytest.mark.parametrize("kind", ["exact", "engine"])
+def test_staged_layer_publishes_from_its_gather(sk, port, kind):
+    """sk_sparse_layer_stage + sk_staged_publish: a row block's layer written by
+    its own gather kernel into several destinations (entries at nnz_off, row
+    pointers shifted) equals sk_sparse_layer_dev's block, bit for bit.  "exact":
+    the order-free path (the fused gather); "engine": a layer that is not
+    provably exact (finished first, published from the block)."""
+    import torch
+    from paper_1708_02937_b200 import semikern as skm
+    m, n, rows, r0 = 4096, 1500, 700, 1000
+    val = 1.0 / 16 if kind == "exact" else float("nan")
+    W = port.gen_layer_fixed(m, 32, port.layer_seed(5, 0), val)
+    blk_h = hcsr(rows, m, (W.row_ptr[r0:r0 + rows + 1] - W.row_ptr[r0]).astype(np.uint32),
+                 W.col_idx[W.row_ptr[r0]:W.row_ptr[r0 + rows]],
+                 W.values[W.row_ptr[r0]:W.row_ptr[r0 + rows]])
+    blk = dev_csr(sk, blk_h)
+    b = np.full(rows, -0.2, np.float32)
+    Y = dev_csr(sk, port.gen_input_binary(m, n, 300, 5))
+    dev = torch.device("cuda", 0)
+    db = torch.as_tensor(b, device=dev)
+    torch.cuda.synchronize()
+    dense_rows, negmin = skm.bias_summaries(b)
+    want = host_csr(skm.sparse_layer_dev(blk, db.data_ptr(), dense_rows, negmin, Y, 32.0))
+    assert want.nnz > 0
+    st = skm.sparse_layer_stage(blk, db.data_ptr(), dense_rows, negmin, Y, 32.0)
+    assert st.nnz == want.nnz
+    nnz_off, row_off = 3000, r0
+    total = nnz_off + want.nnz
+    bufs = [(torch.full((m + 1,), 7, dtype=torch.int32, device=dev),
+             torch.full((total,), 9, dtype=torch.int32, device=dev),
+             torch.full((total,), -1.0, dtype=torch.float32, device=dev)) for _ in range(3)]
+    st.publish([x[0].data_ptr() for x in bufs], [x[1].data_ptr() for x in bufs],
+               [x[2].data_ptr() for x in bufs], row_off, nnz_off, True)
+    sk.default_context().synchronize()
+    for rp, ci, v in bufs:
+        rp, ci, v = rp.cpu().numpy(), ci.cpu().numpy(), v.cpu().numpy()
+        assert np.array_equal(rp[row_off:row_off + rows + 1],
+                              want.row_ptr.astype(np.int64) + nnz_off)
+        assert rp[row_off - 1] == 7 and rp[row_off + rows + 1] == 7
+        assert np.array_equal(ci[nnz_off:], want.col_idx.astype(np.int32))
+        assert np.array_equal(bits(v[nnz_off:]), bits(want.values))
+        assert np.all(ci[:nnz_off] == 9)
+
+
 @pytest.mark.parametrize("exchange", ["peer", "nccl"])
 def test_column_sharded_forward_single_rank_nccl(sk, port, exchange):
     import socket
