@@ -406,7 +406,6 @@ namespace clu {
 constexpr int kCS = 8;        // CTAs per cluster
 constexpr int kWarps = 32;    // warps per CTA
 constexpr int kCols = 32;     // columns per cluster (kCols lanes fold one row)
-constexpr int kRows = 2;      // rows per lane group folded together
 constexpr int kBoxRows = 256; // tensor-copy box: 256 rows x kCols columns
 }  // namespace clu
 
@@ -533,66 +532,33 @@ __global__ void __launch_bounds__(clu::kWarps * 32, 1)
     CLU_TS(2 + 3 * k);
     const uint32_t* ro = roff + k * (nr + 1);
     const float* bias = bsh + size_t(k) * nr - r0;  // indexed by the global row
-    // a lane group folds kRows rows at a time (independent chains in flight)
+    // a lane group folds one row at a time: the row's entries in steps of 4
+    // with every (k, w) and Y load of a step issued first, then the fold in
+    // order; rows differ in length (W_ref's rows are W's columns), so there is
+    // no guard inside a step -- the 0..3 leftover entries fold one by one
     const uint32_t vw = uint32_t(warp) * kGroups + h, nvw = kGroups * kWarps;
-    for (uint32_t rb = vw; rb < nr; rb += nvw * kRows) {
-      float acc[kRows];
-      uint32_t e0[kRows], e1[kRows], len = 0;
+    for (uint32_t r = vw; r < nr; r += nvw) {
+      float acc = 0.0f;
+      const uint32_t e0 = ro[r], e1 = ro[r + 1];
+      uint32_t e = e0;
+      for (; e + 4 <= e1; e += 4) {
+        float yv[4], wv4[4];
 #pragma unroll
-      for (int q = 0; q < kRows; ++q) {
-        const uint32_t r = rb + q * nvw;
-        acc[q] = 0.0f;
-        e0[q] = r < nr ? ro[r] : 0u;
-        e1[q] = r < nr ? ro[r + 1] : 0u;
-        len = max(len, e1[q] - e0[q]);
-      }
-      bool same = true;  // every row of the group has len entries: no guards
-#pragma unroll
-      for (int q = 0; q < kRows; ++q) same &= e1[q] - e0[q] == len;
-      if (same && (len & 3u) == 0) {
-        for (uint32_t t0 = 0; t0 < len; t0 += 4) {
-          float yv[kRows][4], wv4[kRows][4];
-#pragma unroll
-          for (int q = 0; q < kRows; ++q)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint2 kv = kw[e0[q] + t0 + u];  // broadcast within the lane group
-              wv4[q][u] = __uint_as_float(kv.y);
-              yv[q][u] = Ys[kv.x * kCols + cl];
-            }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int q = 0; q < kRows; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wv4[q][u], yv[q][u]));
+        for (int u = 0; u < 4; ++u) {
+          const uint2 kv = kw[e + u];  // broadcast within the lane group
+          wv4[u] = __uint_as_float(kv.y);
+          yv[u] = Ys[kv.x * kCols + cl];
         }
-        len = 0;  // done
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = __fadd_rn(acc, __fmul_rn(wv4[u], yv[u]));
       }
-      // 4 steps at a time: the (k, w) and Y loads of all of them issued first
-      // (indices clamped into the slice; a step past a row's end is not folded)
-      for (uint32_t t0 = 0; t0 < len; t0 += 4) {
-        float yv[kRows][4], wv4[kRows][4];
-#pragma unroll
-        for (int q = 0; q < kRows; ++q)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t e = min(e0[q] + t0 + u, max(e1[q], 1u) - 1);
-            const uint2 kv = kw[e];  // broadcast within the half-warp
-            wv4[q][u] = __uint_as_float(kv.y);
-            yv[q][u] = Ys[kv.x * kCols + cl];
-          }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int q = 0; q < kRows; ++q)
-            if (e0[q] + t0 + u < e1[q]) acc[q] = __fadd_rn(acc[q], __fmul_rn(wv4[q][u], yv[q][u]));
+      for (; e < e1; ++e) {
+        const uint2 kv = kw[e];
+        acc = __fadd_rn(acc, __fmul_rn(__uint_as_float(kv.y), Ys[kv.x * kCols + cl]));
       }
-#pragma unroll
-      for (int q = 0; q < kRows; ++q) {
-        const uint32_t r = rb + q * nvw;
-        if (r < nr && live) {
-          const uint32_t i = r0 + r;
-          dst[size_t(i) * p.n + col] = layer_epilogue(acc[q], bias[i], p.clip);
-        }
+      if (live) {
+        const uint32_t i = r0 + r;
+        dst[size_t(i) * p.n + col] = layer_epilogue(acc, bias[i], p.clip);
       }
     }
     CLU_TS(3 + 3 * k);
