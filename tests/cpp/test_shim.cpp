@@ -139,13 +139,14 @@ int main() {
          const DnnModel ok({Matrix(w2)}, {{0.0f, 0.0f}});
          CHECK(ok.num_layers() == 1 && ok.neurons() == 2);
        }},
-      {"semiring path equals the dense reference on random models (test_dnn.cpp:153-172)",
+      {"semiring path equals the dense reference on 50 random models (acceptance.cpp:60-90 "
+       "criterion 1; test_dnn.cpp:153-172)",
        // The dense leg runs on tensor cores (3xTF32), so it is compared with the
        // reference's magnitude-scaled criterion (approx_equal_scaled,
        // semiring.hpp:50-55), scale = sum_k |w||y| propagated layer by layer.
        [] {
          Rng r{101};
-         for (int trial = 0; trial < 12; ++trial) {
+         for (int trial = 0; trial < 50; ++trial) {
            const index_t m = 4 + r.next() % 61, layers = 1 + r.next() % 4, n = 1 + r.next() % 8;
            const double density = std::vector<double>{1.0, 0.25, 1.0 / 64}[r.next() % 3];
            std::vector<Matrix> ws;
@@ -180,6 +181,58 @@ int main() {
            for (Scalar v : a) CHECK(v >= 0.0f);
          }
        }},
+      {"stored semiring zeros never change results, 20 instances x 4 semirings "
+       "(acceptance.cpp:147-180 criterion 4)",
+       [] {
+         Rng r{11};
+         const Semiring all[] = {arithmetic_semiring(), max_plus_semiring(), min_max_semiring(),
+                                 gf2_semiring()};
+         auto rnd = [&](index_t rows, index_t cols, const Semiring& s) {
+           std::vector<Triple> t;
+           for (index_t i = 0; i < rows; ++i)
+             for (index_t j = 0; j < cols; ++j)
+               if (r.unit() < 0.35) {
+                 float v = s.kind == SemiringKind::gf2 ? 1.0f : float(-4.0 + 8.0 * r.unit());
+                 t.push_back({i, j, v});
+               }
+           return csr_from_triples(rows, cols, t);
+         };
+         auto inject = [&](const CsrMatrix& a, Scalar zero) {  // validating ctor, zeros kept
+           std::vector<index_t> rp{0}, ci;
+           std::vector<Scalar> v;
+           for (index_t i = 0; i < a.rows(); ++i) {
+             const auto cols = a.row_cols(i);
+             const auto vals = a.row_values(i);
+             size_t k = 0;
+             for (index_t j = 0; j < a.cols(); ++j) {
+               if (k < cols.size() && cols[k] == j) {
+                 ci.push_back(j);
+                 v.push_back(vals[k++]);
+               } else if (r.unit() < 0.4) {
+                 ci.push_back(j);
+                 v.push_back(zero);
+               }
+             }
+             rp.push_back(index_t(ci.size()));
+           }
+           return CsrMatrix(a.rows(), a.cols(), rp, ci, v);
+         };
+         auto same = [](const DenseMatrix& x, const DenseMatrix& y) {
+           return x.rows() == y.rows() && x.cols() == y.cols() && bitwise(x.data(), y.data());
+         };
+         for (int trial = 0; trial < 20; ++trial) {
+           const Semiring& s = all[trial % 4];
+           const index_t m = 2 + r.next() % 8, l = 2 + r.next() % 8, n = 2 + r.next() % 8;
+           const CsrMatrix a = rnd(m, l, s), b = rnd(l, n, s), e = rnd(m, l, s);
+           const CsrMatrix az = inject(a, s.zero), bz = inject(b, s.zero), ez = inject(e, s.zero);
+           CHECK(same(to_dense(mxm(a, b, s), s.zero), to_dense(mxm(az, bz, s), s.zero)));
+           CHECK(same(mxm(a, to_dense(b, s.zero), s), mxm(az, to_dense(b, s.zero), s)));
+           CHECK(same(to_dense(ewise_add(Matrix(a), Matrix(e), s), s.zero),
+                      to_dense(ewise_add(Matrix(az), Matrix(ez), s), s.zero)));
+           CHECK(same(to_dense(ewise_mul(Matrix(a), Matrix(e), s), s.zero),
+                      to_dense(ewise_mul(Matrix(az), Matrix(ez), s), s.zero)));
+         }
+       }},
       {"zero bias reduces the layer to max(W*Y, 0) exactly (test_dnn.cpp:174-185)",
        [] {
          Rng r{31};
@@ -189,7 +242,8 @@ int main() {
          const auto prod = mxm(w, y, arithmetic_semiring()).data();
          for (size_t i = 0; i < got.size(); ++i) CHECK(got[i] == std::max(prod[i], 0.0f));
        }},
-      {"forward output is bitwise identical across worker counts (test_dnn.cpp:197-204)",
+      {"forward output is bitwise identical across worker counts (acceptance.cpp:318-349 "
+       "criterion 10; test_dnn.cpp:197-204)",
        [] {
          Rng r{1234};
          std::vector<Matrix> ws;

@@ -31,4 +31,4 @@ def test_reference_cases_pass_through_the_shim(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "0 of 13 cases failed" in r.stdout
+    assert "0 of 14 cases failed" in r.stdout
