@@ -657,6 +657,20 @@ def run_ours(args, w):
     e2e_wall = R.max_over_ranks((time.perf_counter() - t0) * 1e3)
     e2e_step_ms = max(e2e_ms, e2e_wall) / args.steps
     e2e_value = edges / (e2e_step_ms / 1e3)
+    # the host link alone: the same per-step input uploads back to back (what the
+    # overlapped e2e step cannot go below)
+    h2d_ms = None
+    if w["y0"] == "binary":
+        ups = []
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(copy_stream)
+        for _ in range(args.steps):
+            ups.append(upload())
+        ev1.record(copy_stream)
+        torch.cuda.synchronize()
+        h2d_ms = ev0.elapsed_time(ev1) / args.steps
+        del ups
 
     # ---- roofline of the dominant kernel ---------------------------------------------
     pk, pk_kind = peaks()
@@ -756,6 +770,7 @@ def run_ours(args, w):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h[0]), "ms_per_step": e2e_step_ms,
+                    "h2d_ms_per_step_alone": h2d_ms,
                     "input_upload": ("double-buffered: step s+1's pattern upload (copy stream, "
                                      "sk_csr_from_pattern_async) overlaps step s's forward; "
                                      "every step's upload and result read inside the timed "
