@@ -213,6 +213,9 @@ __global__ void __launch_bounds__(256, SK_SPMM_MINB) k_dense_engine(DenseEngineA
 // into the tile order: for every (64-row tile, 32-k chunk) a 64 x 32 value
 // block (only present slots are written) and 64 masks, so each chunk's
 // weights arrive with one more bulk copy.
+#ifndef SK_TILE_PRED
+#define SK_TILE_PRED 0
+#endif
 namespace tile {
 constexpr int kPR = 64;                // rows per packed tile
 constexpr int kTC = 256;               // columns per CTA (lane: 2 x float4)
@@ -245,7 +248,7 @@ __global__ void k_tile_pack(const uint32_t* __restrict__ rp, const uint32_t* __r
 
 // kRW rows per warp, 64 / kRW warps per CTA (one packed tile per CTA)
 template <int kEpi, int kRW>
-__global__ void __launch_bounds__(tile::kPR / kRW * 32, kRW == 4 ? 3 : 2)
+__global__ void __launch_bounds__(tile::kPR / kRW * 32, 2)
     k_spmm_tile(const __grid_constant__ CUtensorMap ymap, const float* __restrict__ wvals,
                 const uint32_t* __restrict__ wmask, const float* __restrict__ bias, uint32_t m,
                 uint32_t K, uint32_t n, float clip, float* __restrict__ out) {
@@ -299,6 +302,20 @@ __global__ void __launch_bounds__(tile::kPR / kRW * 32, kRW == 4 ? 3 : 2)
       const float4 y1 = *reinterpret_cast<const float4*>(Yc + kk * kTC + 128 + lane * 4);
 #pragma unroll
       for (int r = 0; r < kRW; ++r) {
+#if SK_TILE_PRED
+        // predicated (no branch): an absent weight leaves the accumulators as
+        // they are -- the fold still skips it, it is never multiplied as a zero
+        const bool pres = mask[r] & (1u << kk);
+        const float w = Wc[r * kKC + kk];
+        acc[r][0] = pres ? __fadd_rn(acc[r][0], __fmul_rn(w, y0.x)) : acc[r][0];
+        acc[r][1] = pres ? __fadd_rn(acc[r][1], __fmul_rn(w, y0.y)) : acc[r][1];
+        acc[r][2] = pres ? __fadd_rn(acc[r][2], __fmul_rn(w, y0.z)) : acc[r][2];
+        acc[r][3] = pres ? __fadd_rn(acc[r][3], __fmul_rn(w, y0.w)) : acc[r][3];
+        acc[r][4] = pres ? __fadd_rn(acc[r][4], __fmul_rn(w, y1.x)) : acc[r][4];
+        acc[r][5] = pres ? __fadd_rn(acc[r][5], __fmul_rn(w, y1.y)) : acc[r][5];
+        acc[r][6] = pres ? __fadd_rn(acc[r][6], __fmul_rn(w, y1.z)) : acc[r][6];
+        acc[r][7] = pres ? __fadd_rn(acc[r][7], __fmul_rn(w, y1.w)) : acc[r][7];
+#else
         if (mask[r] & (1u << kk)) {  // warp-uniform: the warp's lanes share the rows
           const float w = Wc[r * kKC + kk];
           acc[r][0] = __fadd_rn(acc[r][0], __fmul_rn(w, y0.x));
@@ -310,6 +327,7 @@ __global__ void __launch_bounds__(tile::kPR / kRW * 32, kRW == 4 ? 3 : 2)
           acc[r][6] = __fadd_rn(acc[r][6], __fmul_rn(w, y1.z));
           acc[r][7] = __fadd_rn(acc[r][7], __fmul_rn(w, y1.w));
         }
+#endif
       }
     }
     __syncthreads();  // every warp is done with stage s
@@ -349,7 +367,10 @@ static void ensure_tile_pack(sk_ctx* ctx, const sk_csr* w) {
 }
 
 #ifndef SK_TILE_RW
-#define SK_TILE_RW 8
+#define SK_TILE_RW 4
+#endif
+#ifndef SK_TILE_PRED
+#define SK_TILE_PRED 0
 #endif
 
 // K1t applies when rows are heavy enough that a warp's rows share most k
