@@ -126,8 +126,10 @@ sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double spar
  *                  constant positive products, every bias <= 0, 8-bit
  *                  counters of all out-neurons within 64 KB, a model layer;
  *                  measured slower than the windowed kernels, so never
- *                  automatic); 0 = the specialised kernel where it applies,
- *                  else the generic one
+ *                  automatic); 4 the specialised kernel with flattened
+ *                  products instead of piece records (measured slower; where
+ *                  the specialised kernel applies); 0 = the specialised kernel
+ *                  where it applies, else the generic one
  *   exact_group    4, 8, 16, 32 or 64 windows per exact-layer work item
  *   exact_records  64 or 192 piece records per batch
  *   window_log2    8..12: sample window of the windowed engine (default 10)
@@ -149,7 +151,7 @@ sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t);
 sk_status sk_ctx_get_tuning(const sk_ctx* ctx, sk_tuning* t);
 /* What the last exact-layer launch on this context ran (introspection for the
  * parity tests): launches = exact-layer launches since the context was created;
- * kernel 1 generic / 2 specialised / 3 push; group = windows per item; records = piece
+ * kernel 1 generic / 2 specialised / 3 push / 4 flat; group = windows per item; records = piece
  * records per batch; window_log2; fields = accumulator fields per word. */
 typedef struct sk_exact_info {
   uint64_t launches;

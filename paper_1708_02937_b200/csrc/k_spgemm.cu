@@ -633,7 +633,8 @@ constexpr int kEngineRecCap = 64, kExactRecCap = 192;
 
 // kSh: compile-time log2 window (0 = runtime p.sh); kYC: Y is constant-valued
 // kP: compile-time fields per word (0 = runtime p.fx_pack)
-template <bool kLayer, int kSh, bool kYC, int kCap, bool kQC = false, int kP = 0>
+template <bool kLayer, int kSh, bool kYC, int kCap, bool kQC = false, int kP = 0,
+          bool kFlat = false>
 __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, const WarpSmem& ws,
                                    int lane) {
   const int sh = kSh ? kSh : p.sh;
@@ -676,7 +677,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
     // (a constant increment needs no owner: on sparse passes two chunks of
     // in-edges share one record batch, so rows with 33-64 in-edges fill their
     // rounds; dense passes keep one chunk per batch)
-    constexpr bool kPair = kQC && kCap == kEngineRecCap;
+    constexpr bool kPair = kQC && kCap == kEngineRecCap && !kFlat;
     for (uint32_t c = 0; c < nchunks; c += kPair ? 2 : 1) {
       auto slice = [&](uint32_t kk, uint32_t& beg, uint32_t& cnt) {
         if (p.wpc) {  // one entry per pass: two adjacent words
@@ -698,6 +699,57 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
         slice(kk, beg, cnt);
       }
       if (kPair && e + 32 < ee) slice(p.aci[e + 32], beg2, cnt2);
+      if constexpr (kFlat) {
+        // Flattened products (constant increment): the chunk's slices laid end
+        // to end; lane l takes product b + l of each 32-product window, so a
+        // load instruction reads consecutive entries of one or two slices (a
+        // line or two, not one per lane) and no piece records are written.  The
+        // owner of a window's first product is the last nonempty slice starting
+        // at or before it; the slices starting inside the window (usually one or
+        // two) move the owner for the lanes at or after their start.
+        if (!__any_sync(0xffffffffu, cnt != 0)) continue;
+        any = true;
+        const uint32_t incl = warp_incl_scan(cnt, lane);
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t pre = incl - cnt;
+        constexpr int kU = 4;  // windows of 32 products in flight
+#pragma unroll 1
+        for (uint32_t b0 = 0; b0 < tot; b0 += 32 * kU) {
+          uint32_t smp[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const uint32_t wb = b0 + 32u * u;
+            smp[u] = 0xFFFFFFFFu;
+            if (wb < tot) {  // warp-uniform
+              const uint32_t ne = __ballot_sync(0xffffffffu, cnt != 0 && pre <= wb);
+              uint32_t own = 31 - __clz(ne);
+              uint32_t mk = __ballot_sync(0xffffffffu, cnt != 0 && pre > wb && pre < wb + 32);
+              for (; mk; mk &= mk - 1) {
+                const uint32_t o = __ffs(mk) - 1;
+                const uint32_t st = __shfl_sync(0xffffffffu, pre, o) - wb;
+                if (st <= uint32_t(lane)) own = o;
+              }
+              const uint32_t bo = __shfl_sync(0xffffffffu, beg, own);
+              const uint32_t po = __shfl_sync(0xffffffffu, pre, own);
+              if (wb + lane < tot) smp[u] = __ldg(&p.bci[bo + wb + lane - po]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            if (smp[u] != 0xFFFFFFFFu) {
+              const uint32_t sl = smp[u] - wbase;
+              const uint32_t sub = sl >> sh, wl = sl & (S - 1);
+              const uint32_t delta = uint32_t(p.q_cval) << (B * sub);
+              const uint32_t old = atomicAdd(acc + wl, delta);
+              if ((old + delta) & ~old & topb) {
+                atomicOr(cand + sub * SW + (wl >> 5), 1u << (wl & 31));
+                cflag |= 1u << sub;
+              }
+            }
+          }
+        }
+        continue;
+      }
       if (!__any_sync(0xffffffffu, (cnt | cnt2) != 0)) continue;
       any = true;
       // this lane's slice as pieces of <= 4 consecutive products; a piece record
@@ -859,7 +911,7 @@ __device__ void process_item_exact(const RowArgs& p, uint32_t i, uint32_t g, con
 // 1024-sample windows, a constant increment, four 8-bit fields, no dense rows --
 // compiled alone so its registers are not shared with the other paths
 template <typename Ops, bool kLayer, bool kExact, int kSh = 0, int kCap = kEngineRecCap,
-          bool kFast = false, bool kDyn = false>
+          bool kFast = false, bool kDyn = false, bool kFlat = false>
 __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, int lane,
                                         uint64_t gw, uint64_t nwarps,
                                         const uint32_t* rows = nullptr, uint32_t nrows = 0) {
@@ -869,7 +921,7 @@ __device__ __forceinline__ void phase_a(const RowArgs& p, const WarpSmem& ws, in
   if (nr == 0) return;
   auto item = [&](uint32_t i, uint64_t g) {
     if (kFast) {
-      process_item_exact<kLayer, 10, true, kCap, true, 4>(p, i, uint32_t(g), ws, lane);
+      process_item_exact<kLayer, 10, true, kCap, true, 4, kFlat>(p, i, uint32_t(g), ws, lane);
     } else if (kExact) {
       // rows whose untouched positions survive (epilogue(0 + b) != 0) need the
       // dense sweep of the float exact path
@@ -1125,7 +1177,7 @@ __host__ __device__ constexpr size_t exact_warp_bytes(uint32_t S, int cap) {
   return (size_t(S) + S / 32 + 2 * size_t(cap) + 4 * (S / 32)) * 4;
 }
 
-template <int kSh, int kCap, bool kFast = false>  // kSh 0: runtime p.sh
+template <int kSh, int kCap, bool kFast = false, bool kFlat = false>  // kSh 0: runtime p.sh
 __device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1145,17 +1197,17 @@ __device__ __forceinline__ void exact_layer_body(const RowArgs& p) {
   __syncwarp();
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  phase_a<OpArith, true, true, kSh, kCap, kFast, true>(p, ws, lane, gw, nw);
+  phase_a<OpArith, true, true, kSh, kCap, kFast, true, kFlat>(p, ws, lane, gw, nw);
 }
 
 // kCap: piece records per batch -- 192 when an accumulator pass holds many
 // products (one batch), 64 otherwise (the smaller area leaves L1 to the
 // gathered loads of wide, thin layers)
-template <int kCap, bool kFast = false>
+template <int kCap, bool kFast = false, bool kFlat = false>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_exact_layer(RowArgs p, long long* stamp) {
   if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer();
   if (kFast)
-    exact_layer_body<10, kCap, true>(p);
+    exact_layer_body<10, kCap, true, kFlat>(p);
   else if (p.sh == 10)
     exact_layer_body<10, kCap>(p);
   else
@@ -2298,8 +2350,12 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   // keeps the generic kernel)
   const bool fast = g.sh == 10 && coarse && probe.q_const && probe.fx_pack == 4 &&
                     ctx->tune.exact_kernel != 1;
+  // flattened products instead of piece records (sk_tuning.exact_kernel = 4)
+  const bool flat = fast && ctx->tune.exact_kernel == 4;
   const void* kern =
-      big ? (fast ? (const void*)k_exact_layer<kExactRecCap, true> : (const void*)k_exact_layer<kExactRecCap>)
+      flat ? (big ? (const void*)k_exact_layer<kExactRecCap, true, true>
+                  : (const void*)k_exact_layer<kEngineRecCap, true, true>)
+      : big ? (fast ? (const void*)k_exact_layer<kExactRecCap, true> : (const void*)k_exact_layer<kExactRecCap>)
           : (fast ? (const void*)k_exact_layer<kEngineRecCap, true> : (const void*)k_exact_layer<kEngineRecCap>);
   kernel_smem_attr(ctx, kern, 200 * 1024);
   // occupancy per (variant, shared memory): a driver query, cached per device
@@ -2352,14 +2408,20 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     p.xgroup = ctx->tune.exact_group ? uint32_t(ctx->tune.exact_group)
                                      : exact_group(m, g.nW, uint64_t(grid) * kWarps);
     ctx->last_exact.launches += 1;
-    ctx->last_exact.kernel = fast ? 2 : 1;
+    ctx->last_exact.kernel = flat ? 4 : (fast ? 2 : 1);
     ctx->last_exact.group = int(p.xgroup);
     ctx->last_exact.records = big ? kExactRecCap : kEngineRecCap;
     ctx->last_exact.window_log2 = g.sh;
     ctx->last_exact.fields = int(p.fx_pack);
     long long* stamp = (ctx->stamps && k0 < ctx->stamps_cap) ? ctx->stamps + k0 : nullptr;
     timing_mark(ctx, SK_KT_EXACT);
-    if (big && fast)
+    if (flat && big)
+      SK_LAUNCH((k_exact_layer<kExactRecCap, true, true>), grid, kWarps * 32, smem, ctx->stream,
+                p, stamp);
+    else if (flat)
+      SK_LAUNCH((k_exact_layer<kEngineRecCap, true, true>), grid, kWarps * 32, smem, ctx->stream,
+                p, stamp);
+    else if (big && fast)
       SK_LAUNCH((k_exact_layer<kExactRecCap, true>), grid, kWarps * 32, smem, ctx->stream, p,
                 stamp);
     else if (fast)

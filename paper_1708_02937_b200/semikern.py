@@ -228,7 +228,8 @@ class Context:
         e = _lib.ExactInfo()
         _check(self._L.sk_ctx_last_exact(self.h, C.byref(e)))
         return {"launches": int(e.launches),
-                "kernel": {0: None, 1: "generic", 2: "specialised", 3: "push"}[e.kernel],
+                "kernel": {0: None, 1: "generic", 2: "specialised", 3: "push",
+                           4: "flat"}[e.kernel],
                 "group": e.group, "records": e.records, "window_log2": e.window_log2,
                 "fields": e.fields}
 

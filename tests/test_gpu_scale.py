@@ -134,7 +134,7 @@ def test_exact_layer_every_variant_full_scale(sk, port, ctx, cfg, which):
     combos = [dict(exact_kernel=k, exact_records=r, exact_group=g)
               for k in (1, 2) for r in (64, 192) for g in (4, 8, 16, 32, 64)]
     combos += [dict(exact_kernel=1, exact_window_log2=s) for s in (8, 9, 11, 12)]
-    combos += [dict(exact_kernel=3)]
+    combos += [dict(exact_kernel=3), dict(exact_kernel=4)]
     for c in combos:
         ctx.set_tuning(**dict(dict(exact_kernel=0, exact_records=0, exact_group=0,
                                    exact_window_log2=0), **c))
@@ -144,6 +144,9 @@ def test_exact_layer_every_variant_full_scale(sk, port, ctx, cfg, which):
         assert_same(out, want, f"{cfg} bias {bias} {c}")
         if c["exact_kernel"] == 3:  # push where the counters fit, else the windowed kernel
             assert info["kernel"] == ("push" if m <= 65536 else "specialised"), (c, info)
+            continue
+        if c["exact_kernel"] == 4:  # flattened products (the specialised kernel's shape)
+            assert info["kernel"] == "flat", (c, info)
             continue
         assert info["kernel"] == {1: "generic", 2: "specialised"}[c["exact_kernel"]], (c, info)
         if "exact_records" in c:
