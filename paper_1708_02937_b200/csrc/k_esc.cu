@@ -268,11 +268,367 @@ sk_csr* esc_small(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* b
   return out;
 }
 
+// ---- sample-major ESC: one warp accumulates one sample ---------------------------
+//
+// The global ESC sorts ALL products by (i, j) (cfg3 layer 2: 4.4 M products, four
+// 8-bit onesweep passes, ~0.2 ms).  Seen per sample j the products are few (cfg3
+// layer 2: ~73 from ~2.3 active inputs), so one warp owns one sample: it walks the
+// sample's active inputs k in ASCENDING order (a counting transpose of Y gives
+// the entries; the warp ranks them) and adds each W^T row's products into a
+// per-warp shared-memory hash table keyed by output row i.  The i of one W^T row
+// are distinct, so within a step every slot sees one add, and across steps the
+// adds arrive in ascending k: each slot folds acc = +0, acc += w_ik y_kj exactly
+// as the reference's merge does (matrix.cpp:452-521 + dnn.cpp:65-103).  Then
+// z = epilogue(acc + b_i) per occupied slot; survivors are appended as
+// (i n + j, z) and sorted into CSR.  A sample with more than 32 active inputs
+// or more distinct rows than the small table holds is queued for a one-warp
+// block with a 16 K-slot table that sorts the entries first; beyond that the
+// layer falls back to the global sort.
+constexpr uint32_t kEmptySlot = 0xFFFFFFFFu;
+constexpr int kSampWarps = 8;
+constexpr uint32_t kSampSlots = 256, kSampBudget = 192;  // small kernel, per warp
+constexpr uint32_t kBigSlots = 4096, kBigBudget = 3072;  // big kernel, one warp per block
+constexpr uint32_t kBigEntries = 1024;                   // active inputs per sample, big kernel
+constexpr size_t kBigSmem = size_t(kBigSlots) * 8 + size_t(kBigBudget) * 2 + size_t(kBigEntries) * 8;
+
+__global__ void k_tv_count(const uint32_t* __restrict__ ci, size_t nnz, uint32_t* __restrict__ cnt) {
+  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+       e += size_t(gridDim.x) * blockDim.x)
+    atomicAdd(&cnt[ci[e]], 1u);
+}
+
+// entries of input row k -> their sample's list (k and the value; list order free)
+__global__ void k_tv_scatter(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                             const float* __restrict__ v, uint32_t rows,
+                             uint32_t* __restrict__ cursor, uint2* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < rows;
+       k += (gridDim.x * blockDim.x) >> 5)
+    for (uint32_t e = rp[k] + lane; e < rp[k + 1]; e += 32)
+      out[atomicAdd(&cursor[ci[e]], 1u)] = make_uint2(k, __float_as_uint(v[e]));
+}
+
+struct SampArgs {
+  const uint32_t* yt_rp;
+  const uint2* yt;
+  uint32_t n;
+  const uint32_t* trp;
+  const uint32_t* tci;
+  const float* tv;
+  const float* bias;
+  float clip;
+  unsigned long long* okey;
+  float* oval;
+  unsigned long long cap;
+  unsigned long long* ctr;  // [0] survivors, [1] overflow flag, [2] queued samples
+  uint32_t* queue;
+};
+
+// One product per lane into the warp's table (keys/acc of H slots; list holds
+// the occupied slots from index `used`).  Returns the slots newly occupied.
+template <uint32_t H>
+__device__ __forceinline__ uint32_t tab_add(uint32_t* keys, float* acc, uint16_t* list,
+                                            uint32_t used, bool live, uint32_t i, float p,
+                                            int lane) {
+  bool fresh = false;
+  uint32_t s = (i * 2654435761u) & (H - 1);
+  if (live) {
+    for (;;) {
+      const uint32_t prev = atomicCAS(&keys[s], kEmptySlot, i);
+      if (prev == kEmptySlot) {
+        fresh = true;
+        break;
+      }
+      if (prev == i) break;
+      s = (s + 1) & (H - 1);
+    }
+    acc[s] = __fadd_rn(acc[s], p);  // fresh slots hold +0
+  }
+  const unsigned b = __ballot_sync(0xffffffffu, fresh);
+  if (fresh) list[used + __popc(b & ((1u << lane) - 1u))] = uint16_t(s);
+  return __popc(b);
+}
+
+// W^T row entries [t0, te) of one input (activation y) into the table.
+template <uint32_t H>
+__device__ __forceinline__ uint32_t tab_add_range(const SampArgs& a, uint32_t* keys, float* acc,
+                                                  uint16_t* list, uint32_t used, uint32_t t0,
+                                                  uint32_t te, float y, int lane) {
+  uint32_t added = 0;
+  for (uint32_t base = t0; base < te; base += 32) {
+    const uint32_t t = base + lane;
+    const bool live = t < te;
+    const uint32_t i = live ? a.tci[t] : 0u;
+    const float w = live ? a.tv[t] : 0.0f;
+    added += tab_add<H>(keys, acc, list, used + added, live, i, __fmul_rn(w, y), lane);
+  }
+  return added;
+}
+
+// Occupied slots: epilogue, survivors appended, slots reset for the next sample.
+__device__ __forceinline__ void tab_flush(const SampArgs& a, uint32_t* keys, float* acc,
+                                          const uint16_t* list, uint32_t used, uint32_t j,
+                                          int lane, bool emit) {
+  __syncwarp();
+  for (uint32_t t = lane; t < used; t += 32) {
+    const uint32_t s = list[t], i = keys[s];
+    if (emit) {
+      const float z = layer_epilogue(acc[s], a.bias[i], a.clip);
+      if (z != 0.0f) {
+        const unsigned long long pos = atomicAdd(&a.ctr[0], 1ull);
+        if (pos < a.cap) {
+          a.okey[pos] = (unsigned long long)i * a.n + j;
+          a.oval[pos] = z;
+        }
+      }
+    }
+    keys[s] = kEmptySlot;
+    acc[s] = 0.0f;
+  }
+  __syncwarp();
+}
+
+// One warp per sample with at most 32 active inputs: inputs ranked by k in
+// registers, each input's first 32 W^T entries loaded one input ahead.
+__global__ void __launch_bounds__(kSampWarps * 32) k_esc_sample(SampArgs a) {
+  __shared__ uint32_t skeys[kSampWarps][kSampSlots];
+  __shared__ float sacc[kSampWarps][kSampSlots];
+  __shared__ uint16_t slist[kSampWarps][kSampBudget];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* const keys = skeys[wid];
+  float* const acc = sacc[wid];
+  uint16_t* const list = slist[wid];
+  for (uint32_t s = lane; s < kSampSlots; s += 32) {
+    keys[s] = kEmptySlot;
+    acc[s] = 0.0f;
+  }
+  __syncwarp();
+  const uint32_t stride = (gridDim.x * blockDim.x) >> 5;
+  uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint32_t nb0 = 0, nb1 = 0;
+  if (j < a.n) {
+    nb0 = a.yt_rp[j];
+    nb1 = a.yt_rp[j + 1];
+  }
+  for (; j < a.n; j += stride) {
+    const uint32_t e0 = nb0, E = nb1 - nb0;
+    if (j + stride < a.n) {  // next sample's bounds, one sample ahead
+      nb0 = a.yt_rp[j + stride];
+      nb1 = a.yt_rp[j + stride + 1];
+    }
+    if (E == 0) continue;
+    if (E > 32) {  // warp-uniform
+      if (lane == 0) a.queue[atomicAdd(&a.ctr[2], 1ull)] = j;
+      continue;
+    }
+    const bool mine = uint32_t(lane) < E;
+    uint2 ent = make_uint2(kEmptySlot, 0u);
+    uint32_t tb = 0, te = 0;
+    if (mine) {
+      ent = a.yt[e0 + lane];
+      tb = a.trp[ent.x];
+      te = a.trp[ent.x + 1];
+    }
+    uint32_t rank = 0;  // position of this lane's input in ascending k (k distinct)
+    for (uint32_t q = 0; q < E; ++q) rank += __shfl_sync(0xffffffffu, ent.x, q) < ent.x;
+    int src = __ffs(__ballot_sync(0xffffffffu, mine && rank == 0)) - 1;
+    uint32_t ctb = __shfl_sync(0xffffffffu, tb, src), cte = __shfl_sync(0xffffffffu, te, src);
+    float cy = __uint_as_float(__shfl_sync(0xffffffffu, ent.y, src));
+    bool cl = ctb + lane < cte;
+    uint32_t ci = cl ? a.tci[ctb + lane] : 0u;
+    float cw = cl ? a.tv[ctb + lane] : 0.0f;
+    uint32_t used = 0;
+    bool over = false;
+    for (uint32_t q = 0; q < E; ++q) {
+      uint32_t ntb = 0, nte = 0, ni = 0;
+      float ny = 0.0f, nw = 0.0f;
+      bool nl = false;
+      if (q + 1 < E) {
+        src = __ffs(__ballot_sync(0xffffffffu, mine && rank == q + 1)) - 1;
+        ntb = __shfl_sync(0xffffffffu, tb, src);
+        nte = __shfl_sync(0xffffffffu, te, src);
+        ny = __uint_as_float(__shfl_sync(0xffffffffu, ent.y, src));
+        nl = ntb + lane < nte;
+        if (nl) {
+          ni = a.tci[ntb + lane];
+          nw = a.tv[ntb + lane];
+        }
+      }
+      if (used + (cte - ctb) > kSampBudget) {
+        over = true;
+        break;
+      }
+      used += tab_add<kSampSlots>(keys, acc, list, used, cl, ci, __fmul_rn(cw, cy), lane);
+      if (cte - ctb > 32)
+        used += tab_add_range<kSampSlots>(a, keys, acc, list, used, ctb + 32, cte, cy, lane);
+      __syncwarp();
+      ctb = ntb;
+      cte = nte;
+      cy = ny;
+      ci = ni;
+      cw = nw;
+      cl = nl;
+    }
+    if (over && lane == 0) a.queue[atomicAdd(&a.ctr[2], 1ull)] = j;
+    tab_flush(a, keys, acc, list, used, j, lane, !over);
+  }
+}
+
+// One warp per queued sample: inputs sorted by k in shared memory (bitonic),
+// then the same ascending-k accumulation into a 4 K-slot table.
+__global__ void __launch_bounds__(32) k_esc_sample_big(SampArgs a) {
+  extern __shared__ __align__(16) uint32_t big_smem[];
+  uint32_t* const keys = big_smem;
+  float* const acc = reinterpret_cast<float*>(keys + kBigSlots);
+  uint32_t* const ek = reinterpret_cast<uint32_t*>(acc + kBigSlots);
+  float* const ev = reinterpret_cast<float*>(ek + kBigEntries);
+  uint16_t* const list = reinterpret_cast<uint16_t*>(ev + kBigEntries);
+  const int lane = threadIdx.x;
+  const uint32_t nq = uint32_t(a.ctr[2]);
+  if (blockIdx.x >= nq) return;
+  for (uint32_t s = lane; s < kBigSlots; s += 32) {
+    keys[s] = kEmptySlot;
+    acc[s] = 0.0f;
+  }
+  __syncwarp();
+  for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    const uint32_t j = a.queue[q];
+    const uint32_t e0 = a.yt_rp[j], E = a.yt_rp[j + 1] - e0;
+    if (E > kBigEntries) {
+      if (lane == 0) a.ctr[1] = 1;
+      continue;
+    }
+    uint32_t n2 = 32;
+    while (n2 < E) n2 <<= 1;
+    for (uint32_t t = lane; t < n2; t += 32) {
+      const uint2 e = t < E ? a.yt[e0 + t] : make_uint2(kEmptySlot, 0u);
+      ek[t] = e.x;
+      ev[t] = __uint_as_float(e.y);
+    }
+    __syncwarp();
+    for (uint32_t size = 2; size <= n2; size <<= 1)
+      for (uint32_t half = size >> 1; half; half >>= 1) {
+        for (uint32_t t = lane; t < (n2 >> 1); t += 32) {
+          const uint32_t x = 2 * t - (t & (half - 1)), z = x + half;
+          const uint32_t kx = ek[x], kz = ek[z];
+          if ((kx > kz) == ((x & size) == 0)) {
+            const float vx = ev[x];
+            ek[x] = kz;
+            ek[z] = kx;
+            ev[x] = ev[z];
+            ev[z] = vx;
+          }
+        }
+        __syncwarp();
+      }
+    uint32_t used = 0;
+    bool over = false;
+    for (uint32_t e = 0; e < E; ++e) {
+      const uint32_t k = ek[e], tb = a.trp[k], te = a.trp[k + 1];
+      if (used + (te - tb) > kBigBudget) {
+        over = true;
+        break;
+      }
+      used += tab_add_range<kBigSlots>(a, keys, acc, list, used, tb, te, ev[e], lane);
+      __syncwarp();
+    }
+    if (over && lane == 0) a.ctr[1] = 1;
+    tab_flush(a, keys, acc, list, used, j, lane, !over);
+  }
+}
+
+__global__ void k_samp_csr(const unsigned long long* __restrict__ key, const float* __restrict__ val,
+                           size_t cnt, uint32_t n, uint32_t* __restrict__ rows_cnt,
+                           uint32_t* __restrict__ ci, float* __restrict__ v) {
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < cnt;
+       q += size_t(gridDim.x) * blockDim.x) {
+    const unsigned long long k = key[q];
+    const uint32_t i = uint32_t(k / n);
+    ci[q] = uint32_t(k - (unsigned long long)i * n);
+    v[q] = val[q];
+    atomicAdd(&rows_cnt[i], 1u);
+  }
+}
+
+// nullptr when a sample exceeds the big table (the caller falls back)
+sk_csr* esc_sample(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias,
+                   float clip) {
+  const uint32_t m = wt->cols, n = y->cols, rows = y->rows;
+  // Y^T with values (counting transpose; per-sample order is fixed by the warp)
+  uint32_t* yt_rp = aalloc<uint32_t>(ctx, size_t(n) + 1);
+  uint32_t* cur = aalloc<uint32_t>(ctx, size_t(n) + 1);
+  uint2* yt = aalloc<uint2>(ctx, std::max<size_t>(y->nnz, 1));
+  uint32_t* queue = aalloc<uint32_t>(ctx, std::max<uint32_t>(n, 1));
+  SK_CUDA(cudaMemsetAsync(cur, 0, (size_t(n) + 1) * 4, ctx->stream));
+  SK_LAUNCH(k_tv_count, grid_of(ctx, y->nnz), 256, 0, ctx->stream, y->ci, y->nnz, cur);
+  exclusive_scan_u32(ctx, cur, yt_rp, size_t(n) + 1);
+  SK_CUDA(cudaMemcpyAsync(cur, yt_rp, size_t(n) * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  SK_LAUNCH(k_tv_scatter, grid_of(ctx, uint64_t(rows) * 32), 256, 0, ctx->stream, y->rp, y->ci,
+            y->v, rows, cur, yt);
+  smem_attr(ctx, k_esc_sample_big, int(kBigSmem));
+  const int occ = occupancy(ctx, k_esc_sample, kSampWarps * 32, 0);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ctx->d_u64);
+  unsigned long long cap = std::max<unsigned long long>(1u << 16, y->nnz);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    SampArgs a{yt_rp, yt, n, wt->rp, wt->ci, wt->v, bias, clip, nullptr, nullptr, cap, ctr, queue};
+    a.okey = aalloc<unsigned long long>(ctx, cap);
+    a.oval = aalloc<float>(ctx, cap);
+    SK_CUDA(cudaMemsetAsync(ctr, 0, 24, ctx->stream));
+    const unsigned grid = unsigned(std::min<uint64_t>((uint64_t(n) + kSampWarps - 1) / kSampWarps,
+                                                      uint64_t(ctx->num_sms) * occ));
+    SK_LAUNCH(k_esc_sample, grid, kSampWarps * 32, 0, ctx->stream, a);
+    SK_LAUNCH(k_esc_sample_big, unsigned(ctx->num_sms) * 4, 32, kBigSmem, ctx->stream, a);
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(ctx->h_u64 + 6);
+    SK_CUDA(cudaMemcpyAsync(h, ctr, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (getenv("SK_ESC_DEBUG")) {
+      unsigned long long qd = 0;
+      SK_CUDA(cudaMemcpy(&qd, ctr + 2, 8, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "esc_sample: n=%u nnz=%llu queued=%llu survivors=%llu overflow=%llu\n", n,
+              (unsigned long long)y->nnz, qd, h[0], h[1]);
+    }
+    if (h[1]) return nullptr;  // a sample beyond the big table
+    const unsigned long long cnt = h[0];
+    if (cnt > cap) {
+      cap = cnt;
+      continue;
+    }
+    unsigned long long* k2 = aalloc<unsigned long long>(ctx, std::max<unsigned long long>(cnt, 1));
+    float* v2 = aalloc<float>(ctx, std::max<unsigned long long>(cnt, 1));
+    if (cnt) {
+      const int end_bit = bits_for(uint64_t(m) * n);
+      size_t tmp = 0;
+      SK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, a.okey, k2, a.oval, v2, cnt, 0,
+                                              end_bit, ctx->stream));
+      void* t = aalloc<char>(ctx, tmp);
+      SK_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, a.okey, k2, a.oval, v2, cnt, 0, end_bit,
+                                              ctx->stream));
+      g_launches.fetch_add(1);
+    }
+    sk_csr* o = new_csr(ctx, m, n, cnt);
+    uint32_t* rc = aalloc<uint32_t>(ctx, size_t(m) + 1);
+    SK_CUDA(cudaMemsetAsync(rc, 0, (size_t(m) + 1) * 4, ctx->stream));
+    if (cnt)
+      SK_LAUNCH(k_samp_csr, grid_of(ctx, cnt), 256, 0, ctx->stream, k2, v2, cnt, n, rc, o->ci,
+                o->v);
+    exclusive_scan_u32(ctx, rc, o->rp, size_t(m) + 1);
+    return o;
+  }
+  fail(SK_ERR, "sample-major ESC: survivor count changed between attempts");
+}
+
 template <typename K>
 sk_csr* esc_run(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip,
                 uint32_t maxdeg) {
   if (y->nnz <= kSmallEntries && double(y->nnz) * double(maxdeg) <= double(kSmallCap))
     return esc_small<K>(ctx, y, wt, bias, clip);
+  // sample-major (per-warp tables) when a sample holds few products on average;
+  // a sample beyond the big table sends the layer to the global sort below
+  const double per_sample = double(y->nnz) * double(wt->nnz) / double(std::max<uint32_t>(1, wt->rows)) /
+                            double(std::max<uint32_t>(1, y->cols));
+  if (per_sample <= 128.0 && ctx->tune.esc >= 0) {
+    if (sk_csr* o = esc_sample(ctx, y, wt, bias, clip)) return o;
+  }
   const uint32_t m = wt->cols, n = y->cols, rows = y->rows;
   const size_t nnz = y->nnz;
   // 1. per-entry product counts, scanned (sentinel entry -> total)

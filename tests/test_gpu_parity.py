@@ -620,6 +620,42 @@ def test_esc_thin_layers_bitwise(sk, port, m, n, L, entries):
     assert paths[0] == "esc", paths
 
 
+@pytest.mark.parametrize("case", ["crowded_sample", "survivor_regrow"])
+def test_sample_major_esc_fallback_and_regrow(sk, port, case):
+    # The sample-major ESC sorts each sample's products in one warp's shared
+    # buffer (512 products).  "crowded_sample": one sample holds 640 products,
+    # so the layer must fall back to the global sort; "survivor_regrow": more
+    # survivors than the first output allocation (65536), so the kernel reruns
+    # with the exact count.  Both bitwise against the oracle.
+    rng = np.random.default_rng(7 if case == "crowded_sample" else 8)
+    m, n, L = 4096, 3000, 2
+    hW = _thin_model(port, m, L, 8, 17, rng, special=False)
+    entries = 2000 if case == "crowded_sample" else 24000
+    flat = rng.choice(m * n, size=entries, replace=False)
+    r, c = (flat // n).astype(np.uint32), (flat % n).astype(np.uint32)
+    if case == "crowded_sample":
+        extra = rng.choice(m, size=80, replace=False).astype(np.uint32)
+        keep = c != 17
+        r = np.concatenate([r[keep], extra])
+        c = np.concatenate([c[keep], np.full(80, 17, np.uint32)])
+    v = rng.uniform(0.2, 3.0, r.size).astype(np.float32)
+    Y = sk.csr_from_triples(m, n, (r, c, v))
+    hY = host_csr(Y)
+    b = (-rng.uniform(0.0, 0.3, m)).astype(np.float32)
+    if case == "survivor_regrow":
+        b[:] = 0.0
+    model = sk.DnnModel([dev_csr(sk, w) for w in hW], [b] * L)
+    out, trace = sk.relu_forward_sparse(model, Y, sk.ForwardOptions(clip=32.0))
+    y, want_trace = hY, [hY.nnz]
+    for k in range(L):
+        y = port.layer_sparse(hW[k], b, y, 32.0)
+        want_trace.append(y.nnz)
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, y)
+    if case == "survivor_regrow":
+        assert want_trace[1] > 65536, want_trace
+
+
 def test_empty_input_runs_and_positive_bias_after(sk, port):
     # an empty input stays empty through the layers with every bias <= 0 (no
     # work at all), then a layer with positive biases makes dense rows
