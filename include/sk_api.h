@@ -93,6 +93,14 @@ enum { SK_KT_OTHER = 0, SK_KT_EXACT = 1, SK_KT_ENGINE = 2, SK_KT_DENSE_ENGINE = 
        SK_KT_SPMM = 4, SK_KT_GEMM_TC = 5, SK_KT_SPGEMM = 6, SK_KT_PUSH = 7 };
 sk_status sk_ctx_kernel_times_tagged(sk_ctx* ctx, float* ms, int* tags, size_t cap,
                                      size_t* count);
+
+/* Stream stopwatch for callers that time whole API calls on the device (the
+ * C++ shim's run_sweep, bench.cpp time_step analogue): start records an event
+ * on the context's stream, stop records a second one, waits for it and
+ * returns the milliseconds between them. */
+sk_status sk_ctx_timer_start(sk_ctx* ctx);
+sk_status sk_ctx_timer_stop(sk_ctx* ctx, float* ms);
+
 /* With timing enabled, the sparse engine writes %globaltimer (ns) at the start
  * (entry 0) and at the end of every layer (entry k+1) of the last forward. */
 sk_status sk_ctx_layer_stamps(sk_ctx* ctx, long long* ns, size_t n);

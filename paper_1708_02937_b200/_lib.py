@@ -25,6 +25,7 @@ EXPORTS = [
     "sk_last_error", "sk_version", "sk_kernel_launch_count",
     "sk_ctx_create", "sk_ctx_destroy", "sk_ctx_set_stream", "sk_ctx_stream",
     "sk_ctx_synchronize", "sk_ctx_set_timing", "sk_ctx_kernel_times", "sk_ctx_kernel_times_tagged",
+    "sk_ctx_timer_start", "sk_ctx_timer_stop",
     "sk_ctx_layer_stamps", "sk_ctx_layer_paths", "sk_ctx_set_density_switch",
     "sk_ctx_set_tuning", "sk_ctx_get_tuning", "sk_ctx_last_exact",
     "sk_host_register", "sk_host_unregister",
@@ -96,6 +97,8 @@ def load() -> C.CDLL:
     L.sk_ctx_kernel_times_tagged.argtypes = [vp, f32p, C.POINTER(C.c_int), C.c_size_t,
                                              C.POINTER(C.c_size_t)]
     L.sk_ctx_layer_stamps.argtypes = [vp, C.POINTER(C.c_longlong), C.c_size_t]
+    L.sk_ctx_timer_start.argtypes = [vp]
+    L.sk_ctx_timer_stop.argtypes = [vp, f32p]
     L.sk_ctx_layer_paths.argtypes = [vp, C.POINTER(C.c_ubyte), C.c_size_t]
     L.sk_ctx_set_density_switch.argtypes = [vp, C.c_double, C.c_double]
     L.sk_ctx_set_tuning.argtypes = [vp, C.POINTER(Tuning)]

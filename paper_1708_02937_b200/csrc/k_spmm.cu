@@ -152,6 +152,117 @@ __global__ void __launch_bounds__(256, SK_SPMM_MINB)
   spmm_tasks<Ops, kEpi, kVec4, kU>(rp, ci, wv, bias, y, m, n, clip, out, err);
 }
 
+// Narrow activations (n <= 64, n % 4 == 0): a group of G = n/4 lanes (rounded
+// up to a power of two) owns one row and a lane owns 4 columns, so a warp
+// folds 32/G rows at once instead of leaving 32 - n/4 lanes idle; every lane
+// keeps kNB float4 Y loads in flight.  Rows of one warp may differ in length:
+// the loop runs to the warp's longest row with the shorter ones predicated
+// off, and each output still folds its row's entries strictly in ascending k.
+// (A one-column-per-lane variant for long rows, kC = 1, measured 3-4x slower
+// on the paper sweep's batch-64 shapes and is not dispatched.)
+template <typename Ops, int kEpi, int G, int kC, int kNB>
+__global__ void __launch_bounds__(256, kC == 1 ? 2 : 3)
+    k_spmm_narrow(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                  const float* __restrict__ wv, const float* __restrict__ bias,
+                  const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
+                  float* __restrict__ out, int* err) {
+  static_assert(kC == 1 || kC == 4, "lane column width");
+  constexpr int R = 32 / G;  // rows per warp
+  const int lane = threadIdx.x & 31, sub = lane % G;
+  const uint32_t chunks = (n + G * kC - 1) / (G * kC);
+  const uint64_t row_groups = (uint64_t(m) + R - 1) / R;
+  for (uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+       task < row_groups * chunks; task += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+    const uint32_t c = uint32_t(task / row_groups);
+    const uint32_t i = uint32_t(task - uint64_t(c) * row_groups) * R + uint32_t(lane / G);
+    const uint32_t col0 = (c * G + uint32_t(sub)) * kC;
+    const bool live_row = i < m, live_col = col0 < n;
+    const uint32_t eb = live_row ? rp[i] : 0u, ee = live_row ? rp[i + 1] : 0u;
+    const uint32_t len = ee - eb;
+    uint32_t wlen = len;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wlen = max(wlen, __shfl_xor_sync(0xffffffffu, wlen, o));
+    float acc[kC];
+#pragma unroll
+    for (int q = 0; q < kC; ++q) acc[q] = Ops::zero();
+    for (uint32_t e0 = 0; e0 < wlen; e0 += G) {
+      uint32_t kk = 0;
+      float aa = 0.0f;
+      if (e0 + sub < len) {
+        kk = ci[eb + e0 + sub];
+        aa = wv[eb + e0 + sub];
+      }
+      for (uint32_t t0 = 0; t0 < uint32_t(G) && e0 + t0 < wlen; t0 += kNB) {
+        float v[kNB][kC];
+        float a[kNB];
+#pragma unroll
+        for (int q = 0; q < kNB; ++q) {
+          const uint32_t t = t0 + q;
+          const uint32_t k = __shfl_sync(0xffffffffu, kk, int(t % G), G);
+          a[q] = __shfl_sync(0xffffffffu, aa, int(t % G), G);
+#pragma unroll
+          for (int u = 0; u < kC; ++u) v[q][u] = 0.0f;
+          if (t < uint32_t(G) && e0 + t < len && live_col) {
+            const float* yr = y + size_t(k) * n + col0;
+            if (kC == 4) {
+              const float4 f = __ldg(reinterpret_cast<const float4*>(yr));
+              v[q][0] = f.x;
+              v[q][kC > 1 ? 1 : 0] = f.y;
+              v[q][kC > 2 ? 2 : 0] = f.z;
+              v[q][kC > 3 ? 3 : 0] = f.w;
+            } else {
+              v[q][0] = __ldg(yr);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kNB; ++q)
+          if (t0 + q < uint32_t(G) && e0 + t0 + q < len)
+#pragma unroll
+            for (int u = 0; u < kC; ++u) acc[u] = Ops::add(acc[u], Ops::mul(a[q], v[q][u], err), err);
+      }
+    }
+    if (live_row && live_col) {
+      if (kEpi == kEpiLayer) {
+        const float b = bias[i];
+#pragma unroll
+        for (int u = 0; u < kC; ++u) acc[u] = layer_epilogue(acc[u], b, clip);
+      }
+      float* o = out + size_t(i) * n + col0;
+      if (kC == 4)
+        *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[kC > 1 ? 1 : 0],
+                                                    acc[kC > 2 ? 2 : 0], acc[kC > 3 ? 3 : 0]);
+      else
+        o[0] = acc[0];
+    }
+  }
+}
+
+template <typename Ops, int kEpi>
+bool launch_narrow(sk_ctx* ctx, const sk_csr* w, const float* bias, const float* y, uint32_t n,
+                   float clip, float* out) {
+  if (n > 64 || n % 4 != 0 || w->rows == 0) return false;
+  const uint32_t need = n / 4;  // lanes per row
+  auto go = [&](auto g, auto c) {
+    constexpr int G = decltype(g)::value, kC = decltype(c)::value;
+    constexpr int kNB = kC == 1 ? 16 : 8;
+    const uint64_t warps = (uint64_t(w->rows) + 32 / G - 1) / (32 / G) *
+                           ((n + G * kC - 1) / (G * kC));
+    const unsigned grid = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>((warps + 7) / 8, uint64_t(ctx->num_sms) * 16)));
+    SK_LAUNCH((k_spmm_narrow<Ops, kEpi, G, kC, kNB>), grid, 256, 0, ctx->stream, w->rp, w->ci,
+              w->v, bias, y, w->rows, n, clip, out, ctx->d_err);
+  };
+  using I1 = std::integral_constant<int, 1>;
+  using I4 = std::integral_constant<int, 4>;
+  if (need <= 1) go(I1{}, I4{});
+  else if (need <= 2) go(std::integral_constant<int, 2>{}, I4{});
+  else if (need <= 4) go(I4{}, I4{});
+  else if (need <= 8) go(std::integral_constant<int, 8>{}, I4{});
+  else go(std::integral_constant<int, 16>{}, I4{});
+  return true;
+}
+
 // The whole dense-activation forward in ONE persistent cooperative launch: each
 // layer is the K1 task loop, layers are separated by a grid barrier (every
 // output column of layer k+1 needs the whole of Y_k).  Removes the per-layer
@@ -751,6 +862,7 @@ void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const
     launch_tile(ctx, w, d_bias, y, n, clip, out, true);
     return;
   }
+  if (launch_narrow<OpArith, kEpiLayer>(ctx, w, d_bias, y, n, clip, out)) return;
   const bool vec = (n % 4 == 0);
   // light rows (<= 16 stored entries on average) and wide activations: four
   // 128-column chunks per task
@@ -775,6 +887,7 @@ void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b, uint32_t
   }
   dispatch_semiring(s, [&](auto ops) {
     using Ops = decltype(ops);
+    if (launch_narrow<Ops, kEpiNone>(ctx, a, nullptr, b, n, 0.0f, out)) return;
     if (n % 4 == 0)
       SK_LAUNCH((k_spmm_rows<Ops, kEpiNone, true>), spmm_grid(ctx, a->rows, n), 256, 0,
                 ctx->stream, a->rp, a->ci, a->v, nullptr, b, a->rows, n, 0.0f, out, ctx->d_err);

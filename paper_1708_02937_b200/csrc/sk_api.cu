@@ -279,6 +279,11 @@ extern "C" sk_status sk_ctx_destroy(sk_ctx* ctx) {
     cudaFree(ctx->d_u64);
     cudaFreeHost(ctx->h_u64);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->watch)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->pin_ev)
+      if (e) cudaEventDestroy(e);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
     if (ctx->stamps) cudaFree(ctx->stamps);
     if (ctx->arena) cudaFreeAsync(ctx->arena, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
@@ -364,6 +369,52 @@ extern "C" sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable) {
       ctx->stamps = nullptr;
       ctx->stamps_cap = 0;
     }
+  });
+}
+
+namespace sk {
+constexpr int kPinSlots = 4;
+constexpr size_t kPinSlotBytes = size_t(64) << 10;
+
+void upload_staged(sk_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  if (bytes > kPinSlotBytes) {  // pageable: staged by the driver before the call returns
+    SK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return;
+  }
+  if (!ctx->pin) {
+    SK_CUDA(cudaMallocHost(&ctx->pin, kPinSlots * kPinSlotBytes));
+    for (cudaEvent_t& e : ctx->pin_ev) SK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int slot = ctx->pin_next;
+  ctx->pin_next = (slot + 1) % kPinSlots;
+  SK_CUDA(cudaEventSynchronize(ctx->pin_ev[slot]));  // the slot's previous copy is done
+  char* p = ctx->pin + size_t(slot) * kPinSlotBytes;
+  std::memcpy(p, src, bytes);
+  SK_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  SK_CUDA(cudaEventRecord(ctx->pin_ev[slot], ctx->stream));
+}
+}  // namespace sk
+
+extern "C" sk_status sk_ctx_timer_start(sk_ctx* ctx) {
+  return guarded([&] {
+    require_ctx(ctx);
+    SK_CUDA(cudaSetDevice(ctx->device));
+    for (cudaEvent_t& e : ctx->watch)
+      if (!e) SK_CUDA(cudaEventCreate(&e));
+    SK_CUDA(cudaEventRecord(ctx->watch[0], ctx->stream));
+  });
+}
+
+extern "C" sk_status sk_ctx_timer_stop(sk_ctx* ctx, float* ms) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (!ms) fail(SK_ERR_INVALID_ARGUMENT, "sk_ctx_timer_stop: null output");
+    if (!ctx->watch[0]) fail(SK_ERR_INVALID_ARGUMENT, "sk_ctx_timer_stop: timer never started");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    SK_CUDA(cudaEventRecord(ctx->watch[1], ctx->stream));
+    SK_CUDA(cudaEventSynchronize(ctx->watch[1]));
+    SK_CUDA(cudaEventElapsedTime(ms, ctx->watch[0], ctx->watch[1]));
   });
 }
 
@@ -641,14 +692,12 @@ extern "C" sk_status sk_layer_step(sk_ctx* ctx, const sk_csr* w, const float* bi
       fail(SK_ERR_DIMENSION, "bias length 0 does not match " + std::to_string(w->rows) +
                                  " output rows");
     float* db = dalloc<float>(ctx, w->rows);
-    SK_CUDA(cudaMemcpyAsync(db, bias, size_t(w->rows) * 4, cudaMemcpyHostToDevice,
-                            ctx->stream));
+    upload_staged(ctx, db, bias, size_t(w->rows) * 4);  // the host bias is only lent
     sk_dense* o = new_dense(ctx, w->rows, y->cols);
     timing_mark(ctx, SK_KT_SPMM);  // K1 is the layer's only kernel (measurement hook)
     launch_layer_dense(ctx, w, db, y->d, y->cols, opt_clip(opt), o->d);
     timing_mark(ctx);
     dfree(ctx, db);
-    sync(ctx);  // the host bias buffer is borrowed only for this call
     *out = o;
   });
 }

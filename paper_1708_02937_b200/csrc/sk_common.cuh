@@ -104,6 +104,10 @@ struct sk_ctx {
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // 2 per layer
   std::vector<int> ev_tag;      // SK_KT_* per pair
+  cudaEvent_t watch[2] = {nullptr, nullptr};  // sk_ctx_timer_start/stop
+  char* pin = nullptr;                      // pinned staging ring (upload_staged)
+  cudaEvent_t pin_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int pin_next = 0;
   size_t ev_used = 0;
   // Optional per-layer %globaltimer stamps written by the sparse engine.
   long long* stamps = nullptr;
@@ -272,6 +276,10 @@ void fill(sk_ctx* ctx, float* p, size_t n, float v);
 
 // device scan helpers (CUB, stream-ordered temp storage)
 void exclusive_scan_u32(sk_ctx* ctx, const uint32_t* in, uint32_t* out, size_t n);
+// Host -> device copy of a small host buffer the caller only lends for the
+// call (a bias vector): staged through a pinned ring slot, so the copy is
+// stream-ordered and the call returns without waiting for the device.
+void upload_staged(sk_ctx* ctx, void* dst, const void* src, size_t bytes);
 void exclusive_scan_u64(sk_ctx* ctx, const uint64_t* in, uint64_t* out, size_t n);
 
 // ---- semiring op tables (semiring.hpp:63-110), device side --------------------

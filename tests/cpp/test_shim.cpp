@@ -61,8 +61,15 @@ DenseMatrix random_dense(index_t rows, index_t cols, Rng& r) {
   return DenseMatrix(rows, cols, v);
 }
 
-bool bitwise(const std::vector<Scalar>& a, const std::vector<Scalar>& b) {
+bool bitwise(std::span<const Scalar> a, std::span<const Scalar> b) {
   return a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * 4) == 0;
+}
+
+// Host copy of a (possibly temporary) matrix: data() views the matrix's own
+// storage, as in the reference, so a temporary's view must not outlive it.
+std::vector<Scalar> host(const DenseMatrix& d) {
+  const auto v = d.data();
+  return {v.begin(), v.end()};
 }
 
 }  // namespace
@@ -117,10 +124,10 @@ int main() {
       {"layer_step edge cases (test_dnn.cpp:115-151)",
        [] {
          const std::vector<Scalar> b3(3, 0.0f);
-         for (Scalar v : layer_step(Matrix(csr_from_triples(3, 3, {})), b3, DenseMatrix(3, 2, 1.0f)).data())
+         for (Scalar v : host(layer_step(Matrix(csr_from_triples(3, 3, {})), b3, DenseMatrix(3, 2, 1.0f))))
            CHECK(v == 0.0f);
          const std::vector<Scalar> m1(4, -1.0f);
-         for (Scalar v : layer_step(Matrix(DenseMatrix::identity(4)), m1, DenseMatrix(4, 3, 1.0f)).data())
+         for (Scalar v : host(layer_step(Matrix(DenseMatrix::identity(4)), m1, DenseMatrix(4, 3, 1.0f))))
            CHECK(v == 0.0f);
          CHECK_THROWS_AS(layer_step(Matrix(DenseMatrix::identity(3)), b3, DenseMatrix(2, 2, 1.0f)),
                          DimensionError);
@@ -159,8 +166,8 @@ int main() {
            }
            const DnnModel model(ws, bs);
            const Batch input = random_dense(m, n, r);
-           const auto a = relu_forward(model, input).data();
-           const auto d = dense_relu_forward(model, input).data();
+           const auto a = host(relu_forward(model, input));
+           const auto d = host(dense_relu_forward(model, input));
            const auto x0 = input.data();
            std::vector<double> y(x0.begin(), x0.end()), sc(y.size());
            for (auto& v : y) v = std::fabs(v);
@@ -238,8 +245,8 @@ int main() {
          Rng r{31};
          const CsrMatrix w = random_csr(20, 20, 0.25, r);
          const DenseMatrix y = random_dense(20, 6, r);
-         const auto got = layer_step(Matrix(w), std::vector<Scalar>(20, 0.0f), y).data();
-         const auto prod = mxm(w, y, arithmetic_semiring()).data();
+         const auto got = host(layer_step(Matrix(w), std::vector<Scalar>(20, 0.0f), y));
+         const auto prod = host(mxm(w, y, arithmetic_semiring()));
          for (size_t i = 0; i < got.size(); ++i) CHECK(got[i] == std::max(prod[i], 0.0f));
        }},
       {"forward output is bitwise identical across worker counts (acceptance.cpp:318-349 "
@@ -254,8 +261,8 @@ int main() {
          }
          const DnnModel model(ws, bs);
          const Batch input = random_dense(32, 8, r);
-         const auto base = relu_forward(model, input, {1, false}).data();
-         for (int w : {2, 4}) CHECK(bitwise(relu_forward(model, input, {w, false}).data(), base));
+         const auto base = host(relu_forward(model, input, {1, false}));
+         for (int w : {2, 4}) CHECK(bitwise(host(relu_forward(model, input, {w, false})), base));
        }},
       {"sparse-activation route equals the dense route",
        [] {
@@ -268,10 +275,10 @@ int main() {
          }
          const DnnModel model(ws, bs);
          const Batch input = random_dense(64, 40, r);
-         const auto dense = relu_forward(model, input).data();
+         const auto dense = host(relu_forward(model, input));
          std::vector<std::uint64_t> trace;
          const CsrMatrix sp = relu_forward_sparse(model, from_dense(input), {}, &trace);
-         CHECK(bitwise(to_dense(sp, 0.0f).data(), dense));
+         CHECK(bitwise(host(to_dense(sp, 0.0f)), dense));
          CHECK(trace.size() == 4 && trace[0] == 64u * 40u);
        }},
       {"gf2 domain violations surface from kernels (test_matrix.cpp:353-358)",

@@ -1,7 +1,10 @@
-"""The header-only C++ shim (include/semikern_b200/semikern.hpp) re-exposes the
+"""The header-only C++ shim (include/semikern_b200/semikern/*.hpp) re-exposes the
 reference's namespace semikern over the C-ABI.  CPU: it compiles against the
-library.  GPU: the restated reference test cases pass through it."""
+library, and so does the reference's own acceptance suite, unchanged.  GPU: the
+restated reference test cases and the reference's acceptance criteria pass
+through it."""
 import os
+import re
 import subprocess
 
 import pytest
@@ -10,6 +13,12 @@ from conftest import ROOT
 
 SRC = os.path.join(ROOT, "tests", "cpp", "test_shim.cpp")
 LIBDIR = os.path.join(ROOT, "paper_1708_02937_b200")
+REF_TESTS = "/root/reference/proj/tests"
+ACCEPTANCE = os.path.join(ROOT, "tests", "cpp", "_ref", "acceptance")
+# acceptance.cpp criteria that check results (bitwise or to the reference's
+# tolerance); 5-8 check the CPU cost model's timing-curve shape and are
+# reported, not asserted ("Reference acceptance suite").
+RESULT_CRITERIA = (1, 2, 3, 4, 9, 10, 11)
 
 
 def build(tmp_path):
@@ -32,3 +41,31 @@ def test_reference_cases_pass_through_the_shim(tmp_path):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 of 14 cases failed" in r.stdout
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="reference tree not present (GPU box)")
+def test_reference_acceptance_compiles_unchanged_against_the_shim(tmp_path):
+    # proj/tests/acceptance.cpp from where it lies, with the shim directory in
+    # place of proj/include: no edits, no wrapper.
+    exe = str(tmp_path / "acceptance")
+    cmd = ["g++", "-std=c++20", "-O1", "-Wall", "-I" + os.path.join(ROOT, "include", "semikern_b200"),
+           "-I" + os.path.join(ROOT, "include"), "-I" + REF_TESTS,
+           os.path.join(REF_TESTS, "acceptance.cpp"), "-L" + LIBDIR, "-lsk_b200",
+           "-Wl,-rpath," + LIBDIR, "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_on_the_b200():
+    # the binary tests/cpp/Makefile built (build() in this container); it ships
+    # with the snapshot like the library itself
+    if not os.path.exists(ACCEPTANCE):
+        pytest.skip("tests/cpp/_ref/acceptance not built (needs the reference tree at build time)")
+    r = subprocess.run([ACCEPTANCE], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    status = {int(m.group(1)): m.group(2)
+              for m in re.finditer(r"\[\s*(\d+)/11\].*?(PASS|FAIL)", r.stdout)}
+    assert sorted(status) == list(range(1, 12)), r.stdout + r.stderr
+    failed = [c for c in RESULT_CRITERIA if status[c] != "PASS"]
+    assert not failed, f"criteria {failed} failed:\n{r.stdout}"

@@ -255,6 +255,26 @@ def test_layer_step_matches_reference_on_odd_shapes(sk, ref, port):
         assert np.array_equal(bits(got), bits(port.layer_dense(W, b, y, 0.75))), (m, n)
 
 
+@pytest.mark.parametrize("m,n,inv", [(2048, 64, 1.0), (512, 64, 4.0), (700, 4, 2.0),
+                                     (300, 12, 1.0), (1000, 36, 16.0), (64, 8, 1.0),
+                                     (1024, 7, 1.0), (4096, 33, 2.0), (333, 64, 1.0)])
+def test_narrow_activation_spmm_bitwise_vs_reference(sk, ref, m, n, inv):
+    # n <= 64 (n % 4 == 0) takes the sub-warp-group SpMM (n/4 lanes a row,
+    # rows of different lengths in one warp); other n the row-warp K1: the
+    # paper sweep's batch-64 shapes, dense-ish rows included (inverse sparsity
+    # 1 = m entries a row)
+    w = sk.gen_weight(m, inv, 42 + m)
+    hw = host_csr(w)
+    rng = np.random.default_rng(m + n)
+    y = rng.uniform(-1, 1, (m, n)).astype(np.float32)
+    y[rng.random((m, n)) < 0.2] = 0.0
+    b = rng.uniform(-0.5, 0.5, m).astype(np.float32)
+    got = sk.layer_step(sk.Matrix(w), b, sk.DenseMatrix.from_numpy(y)).numpy()
+    assert np.array_equal(bits(got), bits(ref.layer_step(hw, b, y)))
+    got = sk.mxm(w, sk.DenseMatrix.from_numpy(y), sk.max_plus_semiring())
+    assert np.array_equal(bits(got.numpy()), bits(ref.mxm_csr_dense(hw, y, "max_plus")))
+
+
 def test_special_values_follow_reference_select(sk, ref):
     # NaN propagates, -0.0 survives the ReLU select, inf saturates (F4)
     m, n = 4, 6
@@ -881,6 +901,34 @@ def test_dense_mxm_baseline_tcgen05_within_scaled_tolerance(sk, ref, M, K, N):
     # relative error per term (median |err|/scale ~1e-4); 3xTF32 is ~1e-7
     rel = np.abs(got - exact) / np.maximum(scale, 1e-30)
     assert np.median(rel) < 1e-6 and rel.max() < 1e-5
+    if M * K * N <= 1 << 22:
+        # below the tensor-core threshold the comparator runs the reference's
+        # own order (ascending k, no FMA): bitwise
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("m,n,L", [(25, 8, 3), (64, 8, 4), (4, 1, 1)])
+def test_small_dense_forward_bitwise_and_within_reference_acceptance(sk, ref, port, m, n, L):
+    # acceptance.cpp criterion 1 (proj/tests/acceptance.cpp:60-90) compares the
+    # sparse pipeline with dense_relu_forward to 1e-5 relative PER ELEMENT; at
+    # these sizes both legs fold in the reference's order, so they agree bitwise
+    # with each other and with the reference.
+    rng = np.random.default_rng(m * 131 + n)
+    ws, bs = [], []
+    for _ in range(L):
+        w = rng.uniform(-1, 3, (m, m)).astype(np.float32)
+        w[rng.random(w.shape) < 0.75] = 0.0
+        ws.append(w)
+        bs.append(rng.uniform(0, 1, m).astype(np.float32))
+    y0 = rng.uniform(0, 1, (m, n)).astype(np.float32)
+    model = sk.DnnModel([sk.Matrix(sk.DenseMatrix.from_numpy(w)) for w in ws], bs)
+    dense = sk.dense_relu_forward(model, sk.DenseMatrix.from_numpy(y0)).numpy()
+    sparse = sk.relu_forward(model, sk.DenseMatrix.from_numpy(y0)).numpy()
+    want = y0
+    for w, b in zip(ws, bs):
+        want = ref.dense_layer_step(w, b, want, workers=1)
+    assert np.array_equal(dense.view(np.uint32), want.view(np.uint32))
+    assert np.array_equal(sparse.view(np.uint32), want.view(np.uint32))
 
 
 def test_dense_layer_step_cfg2_density_matches_reference(sk, ref, port):
