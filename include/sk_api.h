@@ -90,7 +90,8 @@ sk_status sk_ctx_set_timing(sk_ctx* ctx, int enable);
 sk_status sk_ctx_kernel_times(sk_ctx* ctx, float* ms, size_t cap, size_t* count);
 /* Same, plus which kernel each timed launch was (SK_KT_*). */
 enum { SK_KT_OTHER = 0, SK_KT_EXACT = 1, SK_KT_ENGINE = 2, SK_KT_DENSE_ENGINE = 3,
-       SK_KT_SPMM = 4, SK_KT_GEMM_TC = 5, SK_KT_SPGEMM = 6, SK_KT_PUSH = 7 };
+       SK_KT_SPMM = 4, SK_KT_GEMM_TC = 5, SK_KT_SPGEMM = 6, SK_KT_PUSH = 7,
+       SK_KT_STREAM = 8 };
 sk_status sk_ctx_kernel_times_tagged(sk_ctx* ctx, float* ms, int* tags, size_t cap,
                                      size_t* count);
 
@@ -136,10 +137,15 @@ sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double spar
  *                  measured slower than the windowed kernels, so never
  *                  automatic); 4 the specialised kernel with flattened
  *                  products instead of piece records (measured slower; where
- *                  the specialised kernel applies); 0 = the specialised kernel
- *                  where it applies, else the generic one
- *   exact_group    4, 8, 16, 32 or 64 windows per exact-layer work item
- *   exact_records  64 or 192 piece records per batch
+ *                  the specialised kernel applies); 5 the stream kernel
+ *                  k_exact_stream (K7: a row's in-edge slices bulk-copied into
+ *                  shared memory per pass, where the specialised kernel's
+ *                  preconditions hold and Y's column array is 16-byte aligned);
+ *                  0 = the stream kernel where it applies, else the generic one
+ *   exact_group    4, 8, 16, 32 or 64 windows per exact-layer work item (the
+ *                  stream kernel: 4, 8, 16 or 32 windows per pass)
+ *   exact_records  64 or 192 piece records per batch (the stream kernel: a
+ *                  staging buffer of 4x that many 16-byte units)
  *   window_log2    8..12: sample window of the windowed engine (default 10)
  *   exact_window_log2  8..12: sample window of the exact layer (default 10)
  *   esc            1 (default) thin layers take expand-sort-compress; -1 never
@@ -159,8 +165,8 @@ sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t);
 sk_status sk_ctx_get_tuning(const sk_ctx* ctx, sk_tuning* t);
 /* What the last exact-layer launch on this context ran (introspection for the
  * parity tests): launches = exact-layer launches since the context was created;
- * kernel 1 generic / 2 specialised / 3 push / 4 flat; group = windows per item; records = piece
- * records per batch; window_log2; fields = accumulator fields per word. */
+ * kernel 1 generic / 2 specialised / 3 push / 4 flat / 5 stream; group = windows per item
+ * (stream: per pass); records = piece records per batch (stream: 16-byte staging units); window_log2; fields = accumulator fields per word. */
 typedef struct sk_exact_info {
   uint64_t launches;
   int kernel;

@@ -1,0 +1,45 @@
+// K7 (k_exact_stream.cu): the exact layer, one output row at a time, its in-edge
+// slices streamed through registers with coalesced 16-byte loads.
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+struct sk_ctx;
+
+namespace sk {
+
+struct StreamArgs {
+  const uint32_t* arp;  // W_ref row pointers (row i = in-edges of output neuron i)
+  const uint32_t* aci;  // W_ref columns
+  const uint32_t* bci;  // Y columns, padded copy (launch_pad_passes)
+  const uint32_t* wpc;  // pass table: wpc[k*nP + j] = first padded entry of Y row k with sample >= j*SP
+  uint32_t m, n, nP, nW;  // output rows, samples, passes, 1024-sample output windows
+  const float* bias;
+  float clip;
+  uint32_t q;             // the constant fixed-point increment
+  uint32_t foff, clearw;  // field offset (sum + foff in each 8-bit field), cleared word
+  float fx_scale, fx_unscale;
+  uint32_t* item_cnt;     // per (row, output window)
+  unsigned long long* item_off;
+  uint32_t* sc_c;
+  float* sc_v;
+  unsigned long long* bump;
+  unsigned long long* work;
+  unsigned long long cap;
+  int* overflow;
+};
+
+// shared memory of one warp / one block for field log2 fl; threads per block
+size_t stream_warp_bytes(int fl);
+size_t stream_block_bytes(int fl);
+int stream_block_threads();
+const void* stream_kernel(int fl);
+// The padded copy of an activation CSR's columns (rows 16-byte aligned, sentinel
+// gaps; padded_size words) and its pass table (rows * nP + 1 words).
+size_t padded_size(uint32_t rows, size_t nnz);
+void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
+                       uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc);
+void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, unsigned grid, size_t smem);
+
+}  // namespace sk

@@ -51,6 +51,7 @@
 #include <mutex>
 
 #include "sk_common.cuh"
+#include "k_exact_stream.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -2337,6 +2338,137 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   gc.sh = g.sh + plp;
   gc.S = g.S << plp;
   gc.nW = std::max<uint32_t>(1, uint32_t((uint64_t(n) + gc.S - 1) >> gc.sh));
+  // K7 (k_exact_stream.cu): the specialised path's layer as a stream of
+  // bulk-copied slices, one row at a time (sk_tuning.exact_kernel = 5 forces it
+  // where it applies; 0 takes it automatically)
+  const bool fast0 = g.sh == 10 && coarse && probe.q_const && probe.fx_pack == 4;
+  const bool stream = fast0 && ctx->tune.exact_kernel == 5 &&
+                      probe.q_cval > 0 && n <= 0xFFFFF000u &&
+                      padded_size(y0->rows, y0->nnz) < 0xFFFFFFF0ull;
+  if (stream) {
+    const double erow = double(y0->nnz) / double(std::max<uint32_t>(1, y0->rows));
+    const double deg = double(w->nnz) / double(std::max<uint32_t>(1, m));
+    // entries per (row, pass): the pass widens while they stay few (fewer
+    // passes = fewer window-table reads and slice ends), up to 2^13 words
+    auto per_pass = [&](int fl) {
+      return deg * erow * double(4u << fl) / double(std::max<uint32_t>(1, n));
+    };
+    int fl = 10;
+    if (ctx->tune.exact_group) {
+      fl = ctx->tune.exact_group == 4 ? 10 : ctx->tune.exact_group == 8 ? 11
+         : ctx->tune.exact_group == 16 ? 12 : 13;
+    } else {
+      for (int f = 12; f > 10; --f)
+        if (per_pass(f) <= 2500.0) { fl = f; break; }
+    }
+    // no pass wider than the batch needs
+    while (fl > 10 && (4u << (fl - 1)) >= n) --fl;
+    WinGeom gs;
+    gs.sh = fl + 2;
+    gs.S = 4u << fl;
+    gs.nW = std::max<uint32_t>(1, uint32_t((uint64_t(n) + gs.S - 1) >> gs.sh));
+    // the padded copy of Y's columns and its pass table
+    uint32_t* pci = aalloc<uint32_t>(ctx, padded_size(y0->rows, y0->nnz));
+    uint32_t* wps = aalloc<uint32_t>(ctx, size_t(y0->rows) * gs.nW + 1);
+    launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps);
+    const size_t smem = stream_block_bytes(fl);
+    const void* kern = stream_kernel(fl);
+    kernel_smem_attr(ctx, kern, int(smem));
+    const int per_sm = kernel_occupancy(ctx, kern, stream_block_threads(), smem);
+    const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
+    auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
+      c = std::min<unsigned long long>(c, full);
+      c = std::min<unsigned long long>(c, mem_cap);
+      c = std::min<unsigned long long>(c, 0xFFFFFFFFull);
+      return std::max<unsigned long long>(c, 1);
+    };
+    unsigned long long cap = clamp_cap(std::max<unsigned long long>(4ull * y0->nnz, 1ull << 24),
+                                       (unsigned long long)(ctx->total_mem * 0.3 / 24.0));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      uint32_t* item_cnt = aalloc<uint32_t>(ctx, items + 1);
+      unsigned long long* item_off =
+          reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, items));
+      uint32_t* sc_c = aalloc<uint32_t>(ctx, cap);
+      float* sc_v = aalloc<float>(ctx, cap);
+      uint32_t* wp_out = aalloc<uint32_t>(ctx, items + 1);
+      SK_CUDA(cudaMemsetAsync(d, 0, 24, ctx->stream));  // d[0] bump, d[1] overflow, d[2] work
+      StreamArgs sa;
+      sa.arp = w->rp;
+      sa.aci = w->ci;
+      sa.bci = pci;
+      sa.wpc = wps;
+      sa.m = m;
+      sa.n = n;
+      sa.nP = gs.nW;
+      sa.nW = g.nW;
+      sa.bias = L_.bias;
+      sa.clip = clip;
+      sa.q = uint32_t(probe.q_cval);
+      RowArgs pr;
+      exact_params(L_.wstats, ystats, g.S, pr, thr);
+      sa.foff = pr.fx_off;
+      sa.clearw = pr.fx_clearw;
+      sa.fx_scale = pr.fx_scale;
+      sa.fx_unscale = pr.fx_unscale;
+      sa.item_cnt = item_cnt;
+      sa.item_off = item_off;
+      sa.sc_c = sc_c;
+      sa.sc_v = sc_v;
+      sa.bump = d;
+      sa.work = d + 2;
+      sa.cap = cap;
+      sa.overflow = reinterpret_cast<int*>(d + 1);
+      ctx->last_exact.launches += 1;
+      ctx->last_exact.kernel = 5;
+      ctx->last_exact.group = int(gs.S >> 10);
+      ctx->last_exact.records = 0;
+      ctx->last_exact.window_log2 = g.sh;
+      ctx->last_exact.fields = 4;
+      timing_mark(ctx, SK_KT_STREAM);
+      launch_exact_stream(ctx, sa, fl, grid, smem);
+      timing_mark(ctx);
+      SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
+      exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
+      uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
+      SK_CUDA(cudaMemcpyAsync(hp, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      SK_CUDA(cudaMemcpyAsync(hp + 1, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+      const uint32_t nnz = hp[0];
+      const int ovf = int(hp[1]);
+      if (!ovf && L_.stage) {
+        StagedLayer* st = L_.stage;
+        st->m = m;
+        st->n = n;
+        st->nW = g.nW;
+        st->items = items;
+        st->nnz = nnz;
+        st->item_cnt = item_cnt;
+        st->item_off = item_off;
+        st->wp_out = wp_out;
+        st->sc_c = sc_c;
+        st->sc_v = sc_v;
+        *wp_out_ptr = nullptr;
+        return nullptr;
+      }
+      if (!ovf) {
+        sk_csr* o = new_csr(ctx, m, n, nnz);
+        SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, item_cnt,
+                  item_off, wp_out, items, sc_c, sc_v, o->ci, o->v, sa.overflow);
+        SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, g.nW,
+                  o->rp);
+        *wp_out_ptr = same_geometry ? wp_out : nullptr;
+        return o;
+      }
+      size_t free_b = 0, total_b = 0;
+      SK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const unsigned long long bigger =
+          clamp_cap(full, (unsigned long long)(free_b * 0.6 / 24.0));
+      if (bigger <= cap) break;
+      cap = bigger;
+    }
+    fail(SK_ERR_OOM, "sparse forward: activation nnz exceeds the device capacity");
+  }
   uint32_t* wp0 = coarse ? nullptr : build_wp(ctx, y0, g, true);
   uint32_t* wpc = coarse ? build_wp(ctx, y0, gc, true) : nullptr;
   const double per_pass = double(w->nnz) / double(std::max<uint32_t>(1, m)) *

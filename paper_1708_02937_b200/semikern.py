@@ -165,7 +165,8 @@ class Context:
         return buf[: min(n.value, cap)].copy()
 
     KERNEL_TAGS = {0: "other", 1: "k_exact_layer", 2: "k_sparse_engine", 3: "k_dense_engine",
-                   4: "k_spmm_rows", 5: "k_gemm_packed", 6: "k_spgemm_rows", 7: "k_push_layer"}
+                   4: "k_spmm_rows", 5: "k_gemm_packed", 6: "k_spgemm_rows", 7: "k_push_layer",
+                   8: "k_exact_stream"}
 
     def kernel_times_tagged(self):
         """(durations ms, kernel names) of the timed launches since
@@ -229,7 +230,7 @@ class Context:
         _check(self._L.sk_ctx_last_exact(self.h, C.byref(e)))
         return {"launches": int(e.launches),
                 "kernel": {0: None, 1: "generic", 2: "specialised", 3: "push",
-                           4: "flat"}[e.kernel],
+                           4: "flat", 5: "stream"}[e.kernel],
                 "group": e.group, "records": e.records, "window_log2": e.window_log2,
                 "fields": e.fields}
 
