@@ -690,11 +690,15 @@ def run_ours(args, w):
             byts = sum(sparse_layer_bytes(tr[k], tr[k + 1] * mg // m, Bl, mg, nnzb[k])
                        for k in range(L) if tr[k] > 0)
             desc = "this rank's output-neuron block per layer (k_exact_layer / k_spgemm_rows)"
-        elif dom == "k_exact_layer":
+        elif dom in ("k_exact_layer", "k_exact_stream"):
             byts = sum(sparse_layer_bytes(tr[k], tr[k + 1], Bl, m, nnzW[k])
                        for k in range(L) if paths[k] == "exact")
             desc = ("k_exact_layer (order-free fixed-point windowed SpGEMM + bias/ReLU/clip + "
-                    "prune; its partial sums provably exact)")
+                    "prune; its partial sums provably exact)" if dom == "k_exact_layer" else
+                    "k_exact_stream (K7: order-free fixed-point SpGEMM, one output row per "
+                    "warp, in-edge slices of a padded Y streamed as coalesced 16-byte units "
+                    "into shared-memory 8-bit counters + bias/ReLU/clip + prune; partial sums "
+                    "provably exact)")
         elif dom == "k_dense_engine":
             byts = sum(dense_layer_bytes(Bl, m, nnzW[k]) for k in range(L)
                        if w["y0"] == "dense" or paths[k] == "dense")

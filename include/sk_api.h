@@ -143,7 +143,7 @@ sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double spar
  *                  preconditions hold and Y's column array is 16-byte aligned);
  *                  0 = the stream kernel where it applies, else the generic one
  *   exact_group    4, 8, 16, 32 or 64 windows per exact-layer work item (the
- *                  stream kernel: 4, 8, 16 or 32 windows per pass)
+ *                  stream kernel: 1, 2, 4, 8 or 16 windows per pass)
  *   exact_records  64 or 192 piece records per batch (the stream kernel: a
  *                  staging buffer of 4x that many 16-byte units)
  *   window_log2    8..12: sample window of the windowed engine (default 10)

@@ -45,12 +45,13 @@ namespace sk {
 namespace {
 
 constexpr int kSW = 1;  // warps per block (the accumulator base is then block-uniform)
-constexpr int kU = 4;   // 16-byte units per lane and step (two steps in flight)
+constexpr int kU = 4;   // 16-byte units per lane and step
+constexpr uint32_t kNone = 0xFFFFFFFFu;
 
-// accumulator (2^fl words) + candidate bitmap (4 * 2^fl bits) + unit records
-__host__ __device__ constexpr uint32_t rec_cap(int fl) { return fl >= 12 ? 1024u : 512u; }
+// accumulator (2^fl words) + candidate bitmap (4 * 2^fl bits) + 2 x unit records
+__host__ __device__ constexpr uint32_t rec_cap(int fl) { return fl <= 10 ? 1024u : 512u; }
 __host__ __device__ constexpr size_t warp_bytes(int fl) {
-  return (size_t(4) << fl) + ((size_t(4) << fl) / 8) + size_t(4) * rec_cap(fl);
+  return (size_t(4) << fl) + ((size_t(4) << fl) / 8) + size_t(8) * rec_cap(fl);
 }
 
 __device__ __forceinline__ uint32_t incl_scan(uint32_t v, int lane) {
@@ -79,18 +80,19 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-template <int FL>
+template <int FL, int NS>
 __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   extern __shared__ __align__(16) uint8_t smraw[];
   constexpr uint32_t Wd = 1u << FL;  // accumulator words
   constexpr uint32_t SP = 4u << FL;  // samples per pass
   constexpr uint32_t NWP = SP >> 10; // output windows per pass
   constexpr uint32_t RC = rec_cap(FL);
+  constexpr uint32_t STEP = 32 * kU; // units per step
   const int lane = threadIdx.x & 31;
   uint32_t* const acc =
       reinterpret_cast<uint32_t*>(smraw + (threadIdx.x >> 5) * warp_bytes(FL));
-  uint32_t* const cand = acc + Wd;     // SP bits
-  uint32_t* const rec = cand + SP / 32;  // RC unit records
+  uint32_t* const cand = acc + Wd;          // SP bits
+  uint32_t* const recs = cand + SP / 32;    // two buffers of RC unit records
   const uint32_t acc_s = async::smem_u32(acc);
 
   const uint32_t cw = p.clearw;
@@ -99,35 +101,42 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   for (uint32_t t = lane; t < SP / 32; t += 32) cand[t] = 0u;
   __syncwarp();
 
-  const uint32_t nP = p.nP, q = p.q;
+  const uint32_t nP = p.nP, q = p.q, m = p.m;
   const uint4* const bq = reinterpret_cast<const uint4*>(p.bci);
 
-  // A record per 16-byte unit of the pass's slices, laid end to end: the unit's
-  // index in the padded column array.  Lane c writes the records of in-edge c's
-  // slice that fall into the batch [b0, b0 + RC) of the flattened units.
-  auto write_recs = [&](uint32_t u0, uint32_t pre, uint32_t nu, uint32_t b0) {
-    const uint32_t lo = max(pre, b0), hi = min(pre + nu, b0 + RC);
-    uint32_t u = u0 + (lo - pre);
-    for (uint32_t t = lo; t < hi; ++t, ++u) rec[t - b0] = u;
+  // A record per 16-byte unit of a pass's slices, laid end to end: the unit's
+  // index in the padded column array.  Lane c owns in-edges c, c + 32, ...
+  // (in-degree <= 32 NS, host-checked) and writes the records of their slices
+  // that fall into the batch [b0, b0 + RC) of the flattened units.
+  auto units = [](uint32_t b, uint32_t e) { return e > b ? ((e + 3) >> 2) - (b >> 2) : 0u; };
+  auto write_recs = [&](uint32_t* rec, const uint32_t (&bg)[NS], const uint32_t (&en)[NS],
+                        uint32_t pre, uint32_t b0) {
+#pragma unroll
+    for (int q2 = 0; q2 < NS; ++q2) {
+      const uint32_t nu = units(bg[q2], en[q2]);
+      const uint32_t lo = max(pre, b0), hi = min(pre + nu, b0 + RC);
+      uint32_t u = (bg[q2] >> 2) + (lo - pre);
+      for (uint32_t t = lo; t < hi; ++t, ++u) rec[t - b0] = u;
+      pre += nu;
+    }
   };
-  // Units [base, n) of the current batch, kU per lane and step (the next step's
-  // loads are issued before this step's atomics).
-  auto load = [&](uint32_t base, uint32_t n, bool (&ok)[kU], uint4 (&x)[kU]) {
+  // Units [base, n) of a batch, kU per lane (records base + lane, + 32, ...)
+  auto load = [&](const uint32_t* rec, uint32_t base, uint32_t n, uint4 (&x)[kU]) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint32_t t = base + 32 * u + lane;
-      ok[u] = t < n;
-      x[u] = ok[u] ? __ldg(bq + rec[t]) : make_uint4(0u, 0u, 0u, 0u);
+      x[u] = t < n ? __ldg(bq + rec[t]) : make_uint4(0u, 0u, 0u, 0u);
     }
   };
   // Every entry of a loaded unit: its sample is inside this pass exactly when
   // it is one of the slice's entries (the rest are the row's own entries of
   // other passes or sentinels), and the increment's shift runs past 31 --
   // a zero increment -- for every other one.  cr collects top-bit transitions.
-  auto apply = [&](const bool (&ok)[kU], const uint4 (&x)[kU], uint32_t pbase, uint32_t& cr) {
+  auto apply = [&](uint32_t base, uint32_t n, const uint4 (&x)[kU], uint32_t pbase,
+                   uint32_t& cr) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      if (!ok[u]) continue;  // past the batch's end (last step only)
+      if (base + 32 * u + lane >= n) continue;
       const uint32_t v[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -139,11 +148,11 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   };
   // the candidates among a step's units (rare): every entry of the pass whose
   // field is past the smallest threshold is marked (re-marking is idempotent)
-  auto mark = [&](const bool (&ok)[kU], const uint4 (&x)[kU], uint32_t pbase,
+  auto mark = [&](uint32_t base, uint32_t n, const uint4 (&x)[kU], uint32_t pbase,
                   uint32_t& cflag) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      if (!ok[u]) continue;
+      if (base + 32 * u + lane >= n) continue;
       const uint32_t v[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -156,155 +165,255 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
       }
     }
   };
-
-  uint32_t nxt = 0;
-  if (lane == 0) nxt = uint32_t(atomicAdd(p.work, 1ull));
-  nxt = __shfl_sync(0xffffffffu, nxt, 0);
-#pragma unroll 1
-  while (nxt < p.m) {
-    const uint32_t row = nxt;
-    if (lane == 0) nxt = uint32_t(atomicAdd(p.work, 1ull));  // claimed one row ahead
-    const uint32_t eb = __ldg(p.arp + row), ee = __ldg(p.arp + row + 1);
-    const uint32_t nch = ee > eb ? (ee - eb + 31) / 32 : 1u;
-    uint32_t k = 0;
-    bool kok = false;
-    uint32_t beg = 0, end = 0, nend = 0;
-#pragma unroll 1
-    for (uint32_t pass = 0; pass < nP; ++pass) {
-      const uint32_t pbase = pass * SP;
-      uint32_t cflag = 0, ntot = 0, T = 0;
-#pragma unroll 1
-      for (uint32_t ch = 0; ch < nch; ++ch) {
-        // this lane's in-edge and its slice of the pass; the next pass's end is
-        // prefetched (a pass starts where the previous one ended)
-        if (pass == 0 || nch > 1) {
-          const uint32_t e = eb + 32 * ch + lane;
-          kok = e < ee;
-          k = kok ? __ldg(p.aci + e) : 0u;
-          beg = end = 0;
-          if (kok) {
-            beg = __ldg(p.wpc + size_t(k) * nP + pass);
-            end = __ldg(p.wpc + size_t(k) * nP + pass + 1);
-          }
-        } else {
-          beg = end;
-          end = nend;
-        }
-        nend = kok && pass + 1 < nP ? __ldg(p.wpc + size_t(k) * nP + pass + 2) : 0u;
-        ntot += __reduce_add_sync(0xffffffffu, end - beg);
-        const uint32_t nu = end > beg ? ((end + 3) >> 2) - (beg >> 2) : 0u;
-        const uint32_t incl = incl_scan(nu, lane);
-        T = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t pre = incl - nu;
-#pragma unroll 1
-        for (uint32_t b0 = 0; b0 < T; b0 += RC) {
-          __syncwarp();  // the previous batch's records are consumed
-          write_recs(beg >> 2, pre, nu, b0);
-          __syncwarp();
-          const uint32_t n = min(RC, T - b0);
-          bool ok[kU];
-          uint4 x[kU];
-          load(0, n, ok, x);
-#pragma unroll 1
-          for (uint32_t base = 0; base < n; base += 32 * kU) {
-            bool okn[kU];
-            uint4 xn[kU];
-            const bool more = base + 32 * kU < n;
-            if (more) load(base + 32 * kU, n, okn, xn);
-            uint32_t cr = 0;
-            apply(ok, x, pbase, cr);
-            if (cr) mark(ok, x, pbase, cflag);
-            if (more) {
+  // the per-lane slice geometry of a unit (row, pass): prefix and total units
+  auto geometry = [&](const uint32_t (&bg)[NS], const uint32_t (&en)[NS], uint32_t& pre,
+                      uint32_t& T) {
+    uint32_t nu = 0;
 #pragma unroll
-              for (int u = 0; u < kU; ++u) {
-                ok[u] = okn[u];
-                x[u] = xn[u];
-              }
-            }
-          }
-        }
-      }
-      __syncwarp();
-
-      // ---- emit the pass's windows --------------------------------------------------
-      const uint32_t w0 = pass * NWP;
-      const uint32_t nwp = min(NWP, p.nW - w0);
-      uint32_t cmask = __reduce_or_sync(0xffffffffu, cflag);
-      if (uint32_t(lane) < nwp && !((cmask >> lane) & 1u))
-        p.item_cnt[uint64_t(row) * p.nW + w0 + lane] = 0u;
-      if (cmask) {
-        const float b = __ldg(p.bias + row);
-        const float thr = __fmul_rn(-b, p.fx_scale);
-#pragma unroll 1
-        for (; cmask; cmask &= cmask - 1) {
-          const uint32_t wsub = __ffs(cmask) - 1;
-          const uint64_t it = uint64_t(row) * p.nW + w0 + wsub;
-          const uint32_t slw = wsub * 1024 + lane * 32;  // this lane's 32 samples
-          const uint32_t fs = 8 * (slw >> FL);
-          const uint32_t* const aw = acc + (slw & (Wd - 1));
-          const uint32_t t = cand[slw >> 5];
-          uint32_t keep = 0;
-          cand[slw >> 5] = 0u;
-          for (uint32_t tt = t; tt; tt &= tt - 1) {
-            const uint32_t bt = __ffs(tt) - 1;
-            const int ai = int(((aw[bt] >> fs) & 0xFFu) - p.foff);
-            if (__int2float_rn(ai) > thr) {
-              const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
-              if (layer_epilogue(x, b, p.clip) != 0.0f) keep |= 1u << bt;
-            }
-          }
-          const uint32_t mine = __popc(keep);
-          const uint32_t incl = incl_scan(mine, lane);
-          const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-          unsigned long long off = 0;
-          if (lane == 0) {
-            if (tot) {
-              off = atomicAdd(p.bump, (unsigned long long)tot);
-              if (off + tot > p.cap) atomicExch(p.overflow, 1);
-            }
-            p.item_cnt[it] = tot;
-            p.item_off[it] = off;
-          }
-          off = __shfl_sync(0xffffffffu, off, 0);
-          if (tot && off + tot <= p.cap) {
-            unsigned long long pos = off + (incl - mine);
-            for (; keep; keep &= keep - 1) {
-              const uint32_t bt = __ffs(keep) - 1;
-              const int ai = int(((aw[bt] >> fs) & 0xFFu) - p.foff);
-              const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
-              p.sc_c[pos] = pbase + slw + bt;
-              p.sc_v[pos] = layer_epilogue(x, b, p.clip);
-              ++pos;
-            }
-          }
-        }
-      }
-      __syncwarp();
-      // ---- clear the accumulator ------------------------------------------------------
-      if (ntot) {
-        if (nch == 1 && T <= RC && ntot * 5 < Wd) {
-          // sparse pass, its records all still in place: clear only the words its
-          // units touched (every word of a loaded unit -- the neighbours' entries
-          // too -- is either touched or already clear)
-#pragma unroll 1
-          for (uint32_t t = lane; t < T; t += 32) {
-            const uint4 x = __ldg(bq + rec[t]);
-            sts_u32(acc_s + ((x.x & (Wd - 1)) << 2), cw);
-            sts_u32(acc_s + ((x.y & (Wd - 1)) << 2), cw);
-            sts_u32(acc_s + ((x.z & (Wd - 1)) << 2), cw);
-            sts_u32(acc_s + ((x.w & (Wd - 1)) << 2), cw);
-          }
-        } else {
-          for (uint32_t t = lane * 4; t < Wd; t += 128)
-            *reinterpret_cast<uint4*>(acc + t) = make_uint4(cw, cw, cw, cw);
-        }
-      }
-      __syncwarp();
+    for (int q2 = 0; q2 < NS; ++q2) nu += units(bg[q2], en[q2]);
+    const uint32_t incl = incl_scan(nu, lane);
+    T = __shfl_sync(0xffffffffu, incl, 31);
+    pre = incl - nu;
+  };
+  // this lane's in-edges of a row (kNone: none) and their first pass bounds
+  auto row_edges = [&](uint32_t eb, uint32_t ee, uint32_t (&kk)[NS]) {
+#pragma unroll
+    for (int q2 = 0; q2 < NS; ++q2) {
+      const uint32_t e = eb + 32 * q2 + lane;
+      kk[q2] = e < ee ? __ldg(p.aci + e) : kNone;
     }
-    nxt = __shfl_sync(0xffffffffu, nxt, 0);
+  };
+  auto first_bounds = [&](const uint32_t (&kk)[NS], uint32_t (&bg)[NS], uint32_t (&en)[NS],
+                          uint32_t (&ea)[NS]) {
+#pragma unroll
+    for (int q2 = 0; q2 < NS; ++q2) {
+      bg[q2] = en[q2] = ea[q2] = 0;
+      if (kk[q2] != kNone) {
+        const uint32_t* wk = p.wpc + size_t(kk[q2]) * nP;
+        bg[q2] = __ldg(wk);
+        en[q2] = __ldg(wk + 1);
+        if (nP > 1) ea[q2] = __ldg(wk + 2);
+      }
+    }
+  };
+
+  // ---- the step pipeline: (row, pass) units in order, each a sequence of steps
+  // of <= STEP units; the next step's loads (the next unit's records first when
+  // the unit ends) are issued before the current step is applied, and the row
+  // after the current one is claimed and its in-edges and first pass bounds
+  // fetched in stages over the current row's passes.
+  uint32_t c_row = 0;
+  if (lane == 0) c_row = uint32_t(atomicAdd(p.work, 1ull));
+  c_row = __shfl_sync(0xffffffffu, c_row, 0);
+  if (c_row >= m) return;
+  // this lane's in-edges, their slices of the current pass, the ends of the next
+  uint32_t k[NS], c_beg[NS], c_end[NS], eA[NS];
+  row_edges(__ldg(p.arp + c_row), __ldg(p.arp + c_row + 1), k);
+  first_bounds(k, c_beg, c_end, eA);
+  uint32_t c_pass = 0, cb = 0, c_pre, c_T;
+  geometry(c_beg, c_end, c_pre, c_T);
+  write_recs(recs, c_beg, c_end, c_pre, 0);
+  __syncwarp();
+  uint4 xc[kU];
+  load(recs, 0, min(RC, c_T), xc);
+  uint32_t s_b0 = 0, s_base = 0;  // the current step within the current unit
+  uint32_t cflag = 0;             // windows of the current unit holding candidates (this lane)
+  // next-row prefetch state (stages 0..4 over the current row's passes)
+  uint32_t st = 0, n_row = kNone, n_eb = 0, n_ee = 0;
+  uint32_t n_k[NS], n_b[NS], n_e[NS], n_e2[NS];
+#pragma unroll
+  for (int q2 = 0; q2 < NS; ++q2) n_k[q2] = kNone, n_b[q2] = n_e[q2] = n_e2[q2] = 0;
+  auto stage = [&] {
+    if (st == 0) {
+      if (lane == 0) n_row = uint32_t(atomicAdd(p.work, 1ull));
+    } else if (st == 1) {
+      n_row = __shfl_sync(0xffffffffu, n_row, 0);
+      if (n_row < m) {
+        n_eb = __ldg(p.arp + n_row);
+        n_ee = __ldg(p.arp + n_row + 1);
+      }
+    } else if (st == 2) {
+      if (n_row < m) {
+        row_edges(n_eb, n_ee, n_k);
+      } else {
+#pragma unroll
+        for (int q2 = 0; q2 < NS; ++q2) n_k[q2] = kNone;
+      }
+    } else if (st == 3) {
+      first_bounds(n_k, n_b, n_e, n_e2);
+    }
+    if (st < 4) ++st;
+  };
+
+#pragma unroll 1
+  for (;;) {
+    const uint32_t c_pbase = c_pass * SP;
+    const uint32_t s_n = min(RC, c_T - min(c_T, s_b0));  // units in the current batch
+    // ---- the next step --------------------------------------------------------------
+    uint32_t n_b0 = s_b0, n_base = s_base + STEP;
+    if (n_base >= s_n) {
+      n_base = 0;
+      n_b0 = s_b0 + RC;
+    }
+    const bool same_unit = n_b0 < c_T;
+    bool more = true;
+    uint32_t x_row = 0, x_pass = 0, x_pre = 0, x_T = 0;
+    uint32_t x_beg[NS], x_end[NS], x_eA[NS], x_k[NS];
+    uint4 xn[kU];
+    if (same_unit) {
+      uint32_t* const rec = recs + cb * RC;
+      if (n_b0 != s_b0) {  // the unit's next batch of records (this step's units are loaded)
+        __syncwarp();
+        write_recs(rec, c_beg, c_end, c_pre, n_b0);
+        __syncwarp();
+      }
+      load(rec, n_base, min(RC, c_T - n_b0), xn);
+    } else {
+      if (c_pass + 1 < nP) {
+        x_row = c_row;
+        x_pass = c_pass + 1;
+#pragma unroll
+        for (int q2 = 0; q2 < NS; ++q2) {
+          x_k[q2] = k[q2];
+          x_beg[q2] = c_end[q2];
+          x_end[q2] = eA[q2];
+          x_eA[q2] = k[q2] != kNone && x_pass + 1 < nP
+                         ? __ldg(p.wpc + size_t(k[q2]) * nP + x_pass + 2) : 0u;
+        }
+      } else {
+        while (st < 4) stage();
+        x_row = n_row;
+        x_pass = 0;
+#pragma unroll
+        for (int q2 = 0; q2 < NS; ++q2) {
+          x_k[q2] = n_k[q2];
+          x_beg[q2] = n_b[q2];
+          x_end[q2] = n_e[q2];
+          x_eA[q2] = n_e2[q2];
+        }
+        more = n_row < m;
+      }
+      if (more) {
+        geometry(x_beg, x_end, x_pre, x_T);
+        write_recs(recs + (cb ^ 1) * RC, x_beg, x_end, x_pre, 0);
+        __syncwarp();
+        load(recs + (cb ^ 1) * RC, 0, min(RC, x_T), xn);
+      }
+      stage();
+    }
+
+    // ---- apply the current step -------------------------------------------------------
+    {
+      uint32_t cr = 0;
+      apply(s_base, s_n, xc, c_pbase, cr);
+      if (cr) mark(s_base, s_n, xc, c_pbase, cflag);
+    }
+    if (same_unit) {
+      s_b0 = n_b0;
+      s_base = n_base;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) xc[u] = xn[u];
+      continue;
+    }
+    __syncwarp();
+    uint32_t* const rec = recs + cb * RC;
+
+    // ---- emit the pass's windows --------------------------------------------------
+    const uint32_t w0 = c_pass * NWP;
+    const uint32_t nwp = min(NWP, p.nW - w0);
+    uint32_t cmask = __reduce_or_sync(0xffffffffu, cflag);
+    if (uint32_t(lane) < nwp && !((cmask >> lane) & 1u))
+      p.item_cnt[uint64_t(c_row) * p.nW + w0 + lane] = 0u;
+    if (cmask) {
+      const float b = __ldg(p.bias + c_row);
+      const float thr = __fmul_rn(-b, p.fx_scale);
+#pragma unroll 1
+      for (; cmask; cmask &= cmask - 1) {
+        const uint32_t wsub = __ffs(cmask) - 1;
+        const uint64_t it = uint64_t(c_row) * p.nW + w0 + wsub;
+        const uint32_t slw = wsub * 1024 + lane * 32;  // this lane's 32 samples
+        const uint32_t fs = 8 * (slw >> FL);
+        const uint32_t* const aw = acc + (slw & (Wd - 1));
+        const uint32_t t = cand[slw >> 5];
+        uint32_t keep = 0;
+        cand[slw >> 5] = 0u;
+        for (uint32_t tt = t; tt; tt &= tt - 1) {
+          const uint32_t bt = __ffs(tt) - 1;
+          const int ai = int(((aw[bt] >> fs) & 0xFFu) - p.foff);
+          if (__int2float_rn(ai) > thr) {
+            const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
+            if (layer_epilogue(x, b, p.clip) != 0.0f) keep |= 1u << bt;
+          }
+        }
+        const uint32_t mine = __popc(keep);
+        const uint32_t incl = incl_scan(mine, lane);
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long off = 0;
+        if (lane == 0) {
+          if (tot) {
+            off = atomicAdd(p.bump, (unsigned long long)tot);
+            if (off + tot > p.cap) atomicExch(p.overflow, 1);
+          }
+          p.item_cnt[it] = tot;
+          p.item_off[it] = off;
+        }
+        off = __shfl_sync(0xffffffffu, off, 0);
+        if (tot && off + tot <= p.cap) {
+          unsigned long long pos = off + (incl - mine);
+          for (; keep; keep &= keep - 1) {
+            const uint32_t bt = __ffs(keep) - 1;
+            const int ai = int(((aw[bt] >> fs) & 0xFFu) - p.foff);
+            const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
+            p.sc_c[pos] = c_pbase + slw + bt;
+            p.sc_v[pos] = layer_epilogue(x, b, p.clip);
+            ++pos;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    cflag = 0;
+    // ---- clear the accumulator ----------------------------------------------------
+    if (c_T) {
+      if (c_T <= RC && c_T * 20 < Wd) {
+        // sparse pass, its records in place: clear only the words its units
+        // touched (every word of a loaded unit -- the row's other entries and
+        // sentinels too -- is either touched or already clear)
+#pragma unroll 1
+        for (uint32_t t = lane; t < c_T; t += 32) {
+          const uint4 x = __ldg(bq + rec[t]);
+          sts_u32(acc_s + ((x.x & (Wd - 1)) << 2), cw);
+          sts_u32(acc_s + ((x.y & (Wd - 1)) << 2), cw);
+          sts_u32(acc_s + ((x.z & (Wd - 1)) << 2), cw);
+          sts_u32(acc_s + ((x.w & (Wd - 1)) << 2), cw);
+        }
+      } else {
+        for (uint32_t t = lane * 4; t < Wd; t += 128)
+          *reinterpret_cast<uint4*>(acc + t) = make_uint4(cw, cw, cw, cw);
+      }
+    }
+    __syncwarp();
+
+    // ---- rotate to the next unit ------------------------------------------------------
+    if (!more) break;
+    if (x_pass == 0) st = 0;  // a new row: start claiming the one after it
+    c_row = x_row;
+    c_pass = x_pass;
+#pragma unroll
+    for (int q2 = 0; q2 < NS; ++q2) {
+      k[q2] = x_k[q2];
+      c_beg[q2] = x_beg[q2];
+      c_end[q2] = x_end[q2];
+      eA[q2] = x_eA[q2];
+    }
+    c_pre = x_pre;
+    c_T = x_T;
+    cb ^= 1u;
+    s_b0 = s_base = 0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xc[u] = xn[u];
   }
 }
-
 
 // The padded copy of an activation CSR that K7 streams, and its pass table.
 // Row k starts at pk = 4k + (rp[k] & ~3) (16-byte aligned, and pk + len_k <=
@@ -360,14 +469,25 @@ size_t stream_block_bytes(int fl) { return size_t(kSW) * stream_warp_bytes(fl); 
 
 int stream_block_threads() { return 32 * kSW; }
 
-const void* stream_kernel(int fl) {
+template <int NS>
+static const void* stream_kernel_ns(int fl) {
   switch (fl) {
-    case 10: return reinterpret_cast<const void*>(k_exact_stream<10>);
-    case 11: return reinterpret_cast<const void*>(k_exact_stream<11>);
-    case 12: return reinterpret_cast<const void*>(k_exact_stream<12>);
-    case 13: return reinterpret_cast<const void*>(k_exact_stream<13>);
+    case 8: return reinterpret_cast<const void*>(k_exact_stream<8, NS>);
+    case 9: return reinterpret_cast<const void*>(k_exact_stream<9, NS>);
+    case 10: return reinterpret_cast<const void*>(k_exact_stream<10, NS>);
+    case 11: return reinterpret_cast<const void*>(k_exact_stream<11, NS>);
+    case 12: return reinterpret_cast<const void*>(k_exact_stream<12, NS>);
   }
-  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: field log2 must be 10..13");
+  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: field log2 must be 8..12");
+}
+
+const void* stream_kernel(int fl, int ns) {
+  switch (ns) {
+    case 1: return stream_kernel_ns<1>(fl);
+    case 2: return stream_kernel_ns<2>(fl);
+    case 3: return stream_kernel_ns<3>(fl);
+  }
+  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: in-edge slots must be 1..3");
 }
 
 size_t padded_size(uint32_t rows, size_t nnz) { return 4 * size_t(rows) + (nnz & ~size_t(3)) + 8; }
@@ -379,15 +499,12 @@ void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint
   SK_LAUNCH(k_pad_passes, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
 }
 
-void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, unsigned grid, size_t smem) {
-  const int th = 32 * kSW;
-  switch (fl) {
-    case 10: SK_LAUNCH(k_exact_stream<10>, grid, th, smem, ctx->stream, p); return;
-    case 11: SK_LAUNCH(k_exact_stream<11>, grid, th, smem, ctx->stream, p); return;
-    case 12: SK_LAUNCH(k_exact_stream<12>, grid, th, smem, ctx->stream, p); return;
-    case 13: SK_LAUNCH(k_exact_stream<13>, grid, th, smem, ctx->stream, p); return;
-  }
-  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: field log2 must be 10..13");
+void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, unsigned grid,
+                         size_t smem) {
+  const void* kern = stream_kernel(fl, ns);
+  void* args[] = {const_cast<StreamArgs*>(&p)};
+  SK_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(32 * kSW), args, smem, ctx->stream));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 }  // namespace sk

@@ -34,12 +34,14 @@ struct StreamArgs {
 size_t stream_warp_bytes(int fl);
 size_t stream_block_bytes(int fl);
 int stream_block_threads();
-const void* stream_kernel(int fl);
+// the kernel for field log2 fl (8..12) and ns in-edge slots per lane (in-degree <= 32 ns)
+const void* stream_kernel(int fl, int ns);
 // The padded copy of an activation CSR's columns (rows 16-byte aligned, sentinel
 // gaps; padded_size words) and its pass table (rows * nP + 1 words).
 size_t padded_size(uint32_t rows, size_t nnz);
 void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
                        uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc);
-void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, unsigned grid, size_t smem);
+void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, unsigned grid,
+                         size_t smem);
 
 }  // namespace sk

@@ -2342,27 +2342,34 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   // bulk-copied slices, one row at a time (sk_tuning.exact_kernel = 5 forces it
   // where it applies; 0 takes it automatically)
   const bool fast0 = g.sh == 10 && coarse && probe.q_const && probe.fx_pack == 4;
-  const bool stream = fast0 && ctx->tune.exact_kernel == 5 &&
-                      probe.q_cval > 0 && n <= 0xFFFFF000u &&
-                      padded_size(y0->rows, y0->nnz) < 0xFFFFFFF0ull;
+  // K7 applies where the specialised kernel's preconditions hold, every product
+  // is a positive increment, in-degrees are <= 96 and the padded copy of Y fits
+  // 32-bit unit indices; automatically (exact_kernel 0) where a pass of 8192
+  // samples holds >= 500 entries per row (cfg3 / cfg4: measured faster than the
+  // specialised kernel; cfg5's ~260 per pass: the specialised kernel is as fast)
+  const double erow0 = double(y0->nnz) / double(std::max<uint32_t>(1, y0->rows));
+  const double deg0 = double(w->nnz) / double(std::max<uint32_t>(1, m));
+  auto stream_pass = [&](int fl) {
+    return deg0 * erow0 * double(4u << fl) / double(std::max<uint32_t>(1, n));
+  };
+  const bool stream_ok = fast0 && probe.q_cval > 0 && n <= 0xFFFFF000u &&
+                         L_.wstats.maxdeg <= 96 &&
+                         padded_size(y0->rows, y0->nnz) < 0xFFFFFFF0ull;
+  const bool stream = stream_ok && (ctx->tune.exact_kernel == 5 ||
+                                    (ctx->tune.exact_kernel == 0 && stream_pass(11) >= 500.0));
   if (stream) {
-    const double erow = double(y0->nnz) / double(std::max<uint32_t>(1, y0->rows));
-    const double deg = double(w->nnz) / double(std::max<uint32_t>(1, m));
-    // entries per (row, pass): the pass widens while they stay few (fewer
-    // passes = fewer window-table reads and slice ends), up to 2^13 words
-    auto per_pass = [&](int fl) {
-      return deg * erow * double(4u << fl) / double(std::max<uint32_t>(1, n));
-    };
-    int fl = 10;
+    // The largest pass up to 2^11 accumulator words (8 KB: ~17 warps per SM
+    // with the records; 16 KB halves that) holding <= 2000 entries per row.
+    int fl = 8;
     if (ctx->tune.exact_group) {
-      fl = ctx->tune.exact_group == 4 ? 10 : ctx->tune.exact_group == 8 ? 11
-         : ctx->tune.exact_group == 16 ? 12 : 13;
+      const int g = ctx->tune.exact_group;  // windows per pass
+      fl = g == 1 ? 8 : g == 2 ? 9 : g == 4 ? 10 : g == 8 ? 11 : 12;
     } else {
-      for (int f = 12; f > 10; --f)
-        if (per_pass(f) <= 2500.0) { fl = f; break; }
+      for (int f = 11; f > 8; --f)
+        if (stream_pass(f) <= 2000.0) { fl = f; break; }
     }
     // no pass wider than the batch needs
-    while (fl > 10 && (4u << (fl - 1)) >= n) --fl;
+    while (fl > 8 && (4u << (fl - 1)) >= n) --fl;
     WinGeom gs;
     gs.sh = fl + 2;
     gs.S = 4u << fl;
@@ -2371,8 +2378,9 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     uint32_t* pci = aalloc<uint32_t>(ctx, padded_size(y0->rows, y0->nnz));
     uint32_t* wps = aalloc<uint32_t>(ctx, size_t(y0->rows) * gs.nW + 1);
     launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps);
+    const int ns = std::max(1, (L_.wstats.maxdeg + 31) / 32);  // in-edge slots per lane
     const size_t smem = stream_block_bytes(fl);
-    const void* kern = stream_kernel(fl);
+    const void* kern = stream_kernel(fl, ns);
     kernel_smem_attr(ctx, kern, int(smem));
     const int per_sm = kernel_occupancy(ctx, kern, stream_block_threads(), smem);
     const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
@@ -2426,7 +2434,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       ctx->last_exact.window_log2 = g.sh;
       ctx->last_exact.fields = 4;
       timing_mark(ctx, SK_KT_STREAM);
-      launch_exact_stream(ctx, sa, fl, grid, smem);
+      launch_exact_stream(ctx, sa, fl, ns, grid, smem);
       timing_mark(ctx);
       SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
       exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);

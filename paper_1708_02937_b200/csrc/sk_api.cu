@@ -327,8 +327,8 @@ extern "C" sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t) {
       fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact / esc must be -1, 0 or 1");
     if (!in(t->exact_kernel, {0, 1, 2, 3, 4, 5}))
       fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_kernel must be 0..5");
-    if (!in(t->exact_group, {0, 4, 8, 16, 32, 64}))
-      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_group must be 0, 4, 8, 16, 32 or 64");
+    if (!in(t->exact_group, {0, 1, 2, 4, 8, 16, 32, 64}))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_group must be 0, 1, 2, 4, 8, 16, 32 or 64");
     if (!in(t->exact_records, {0, 64, 192}))
       fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_records must be 0, 64 or 192");
     auto wl = [](int v) { return v == 0 || (v >= 8 && v <= 12); };

@@ -4,9 +4,12 @@
   bench's seeds: the whole L-layer forward (nnz trace, output CSR, category
   set) bitwise against the C restatement of the reference's sparse layer
   (oracle/sk_oracle.c, pinned to proj/src/matrix.cpp:452-521 + dnn.cpp:86-121),
-  and the kernel the bench runs asserted (sk_ctx_last_exact).
+  and the kernel the bench runs asserted (sk_ctx_last_exact): K7 (the row
+  stream, k_exact_stream.cu) on cfg3/cfg4, the specialised windowed kernel on
+  cfg5.
 * Layer 1 of each at full scale with EVERY exact-layer variant forced through
-  the per-context tuning (generic / specialised kernel x 64 / 192 records x
+  the per-context tuning (K7 at 1 / 2 / 4 / 8 / 16 windows per pass;
+  generic / specialised kernel x 64 / 192 records x
   4..64 windows per item, i.e. 1..16 accumulator passes per item, plus the
   other window sizes), at the bench bias and at a less negative bias whose
   output holds millions of entries -- so the multi-pass items, the candidate
@@ -31,7 +34,7 @@ CFG = {
     "cfg5": (262144, 120, 262, -0.45, -0.1),
 }
 # the records / kernel the bench takes on layer 1 (profiles/r01 launch lists)
-BENCH_KERNEL = {"cfg3": (192, "specialised"), "cfg4": (192, "specialised"),
+BENCH_KERNEL = {"cfg3": (0, "stream"), "cfg4": (0, "stream"),
                 "cfg5": (64, "specialised")}
 
 
@@ -135,6 +138,7 @@ def test_exact_layer_every_variant_full_scale(sk, port, ctx, cfg, which):
               for k in (1, 2) for r in (64, 192) for g in (4, 8, 16, 32, 64)]
     combos += [dict(exact_kernel=1, exact_window_log2=s) for s in (8, 9, 11, 12)]
     combos += [dict(exact_kernel=3), dict(exact_kernel=4)]
+    combos += [dict(exact_kernel=5, exact_group=g) for g in (1, 2, 4, 8, 16)]
     for c in combos:
         ctx.set_tuning(**dict(dict(exact_kernel=0, exact_records=0, exact_group=0,
                                    exact_window_log2=0), **c))
@@ -147,6 +151,9 @@ def test_exact_layer_every_variant_full_scale(sk, port, ctx, cfg, which):
             continue
         if c["exact_kernel"] == 4:  # flattened products (the specialised kernel's shape)
             assert info["kernel"] == "flat", (c, info)
+            continue
+        if c["exact_kernel"] == 5:  # K7: windows per pass as asked
+            assert (info["kernel"], info["group"]) == ("stream", c["exact_group"]), (c, info)
             continue
         assert info["kernel"] == {1: "generic", 2: "specialised"}[c["exact_kernel"]], (c, info)
         if "exact_records" in c:

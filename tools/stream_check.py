@@ -27,7 +27,7 @@ def run(ctx, model, Y0, opt, reps=5):
     return out, round(float(np.sum(ex)) / reps, 4), ctx.last_exact()
 
 
-GROUPS = [int(x) for x in os.environ.get("SC_GROUPS", "0,4,8,16,32").split(",")]
+GROUPS = [int(x) for x in os.environ.get("SC_GROUPS", "0,1,2,4,8,16").split(",")]
 RECS = [int(x) for x in os.environ.get("SC_RECS", "0,192").split(",")]
 
 
