@@ -150,7 +150,10 @@ sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double spar
  *   exact_window_log2  8..12: sample window of the exact layer (default 10)
  *   esc            1 (default) thin layers take expand-sort-compress; -1 never
  *   esc_ratio      products per (row, window) below which ESC applies
- *                  (<= 0: default 8) */
+ *                  (<= 0: default 8)
+ *   exact_fields   the stream kernel's counter width: 4 or 8 bits (0: 4 where
+ *                  the threshold and increment allow it; a 4-bit counter that
+ *                  wraps makes the layer rerun with 8-bit ones) */
 typedef struct sk_tuning {
   int exact;
   int exact_kernel;
@@ -160,6 +163,7 @@ typedef struct sk_tuning {
   int exact_window_log2;
   int esc;
   double esc_ratio;
+  int exact_fields;
 } sk_tuning;
 sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t);
 sk_status sk_ctx_get_tuning(const sk_ctx* ctx, sk_tuning* t);
@@ -174,6 +178,7 @@ typedef struct sk_exact_info {
   int records;
   int window_log2;
   int fields;
+  int wraps;  /* stream kernel: launches rerun with 8-bit fields after a 4-bit one wrapped */
 } sk_exact_info;
 sk_status sk_ctx_last_exact(const sk_ctx* ctx, sk_exact_info* info);
 /* Page-lock / unlock a caller host buffer for async copies. */

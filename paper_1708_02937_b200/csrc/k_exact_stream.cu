@@ -48,10 +48,14 @@ constexpr int kSW = 1;  // warps per block (the accumulator base is then block-u
 constexpr int kU = 4;   // 16-byte units per lane and step
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
-// accumulator (2^fl words) + candidate bitmap (4 * 2^fl bits) + 2 x unit records
-__host__ __device__ constexpr uint32_t rec_cap(int fl) { return fl <= 10 ? 1024u : 512u; }
-__host__ __device__ constexpr size_t warp_bytes(int fl) {
-  return (size_t(4) << fl) + ((size_t(4) << fl) / 8) + size_t(8) * rec_cap(fl);
+// accumulator (2^fl words of 32 / fb fields) + candidate bitmap (a bit per
+// sample of the pass) + 2 x unit records
+__host__ __device__ constexpr uint32_t pass_samples(int fl, int fb) { return (32u / fb) << fl; }
+__host__ __device__ constexpr uint32_t rec_cap(int fl, int fb) {
+  return pass_samples(fl, fb) <= 4096 ? 1024u : 512u;
+}
+__host__ __device__ constexpr size_t warp_bytes(int fl, int fb) {
+  return (size_t(4) << fl) + pass_samples(fl, fb) / 8 + size_t(8) * rec_cap(fl, fb);
 }
 
 __device__ __forceinline__ uint32_t incl_scan(uint32_t v, int lane) {
@@ -80,17 +84,24 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-template <int FL, int NS>
+// FB: bits per field (8, or 4 when the offset threshold and the increment are
+// small: twice the samples per accumulator byte; a field that wraps is detected
+// -- its top bit goes from set to clear -- and the host reruns the layer with
+// 8-bit fields)
+template <int FL, int NS, int FB>
 __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   extern __shared__ __align__(16) uint8_t smraw[];
-  constexpr uint32_t Wd = 1u << FL;  // accumulator words
-  constexpr uint32_t SP = 4u << FL;  // samples per pass
-  constexpr uint32_t NWP = SP >> 10; // output windows per pass
-  constexpr uint32_t RC = rec_cap(FL);
+  constexpr uint32_t Wd = 1u << FL;                 // accumulator words
+  constexpr uint32_t SP = pass_samples(FL, FB);     // samples per pass
+  constexpr uint32_t NWP = SP >> 10;                // output windows per pass
+  constexpr uint32_t RC = rec_cap(FL, FB);
+  constexpr int LB = FB == 8 ? 3 : 2;               // log2(FB)
+  constexpr uint32_t TOP = FB == 8 ? 0x80808080u : 0x88888888u;  // field top bits
+  constexpr uint32_t FMASK = (1u << FB) - 1u;
   constexpr uint32_t STEP = 32 * kU; // units per step
   const int lane = threadIdx.x & 31;
   uint32_t* const acc =
-      reinterpret_cast<uint32_t*>(smraw + (threadIdx.x >> 5) * warp_bytes(FL));
+      reinterpret_cast<uint32_t*>(smraw + (threadIdx.x >> 5) * warp_bytes(FL, FB));
   uint32_t* const cand = acc + Wd;          // SP bits
   uint32_t* const recs = cand + SP / 32;    // two buffers of RC unit records
   const uint32_t acc_s = async::smem_u32(acc);
@@ -131,18 +142,22 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   // Every entry of a loaded unit: its sample is inside this pass exactly when
   // it is one of the slice's entries (the rest are the row's own entries of
   // other passes or sentinels), and the increment's shift runs past 31 --
-  // a zero increment -- for every other one.  cr collects top-bit transitions.
+  // a zero increment -- for every other one.  cr collects bits newly set, wr
+  // bits cleared (masked to the fields' top bits by the caller: a top bit set is
+  // a field passing the smallest threshold, a top bit cleared a field wrapping).
   auto apply = [&](uint32_t base, uint32_t n, const uint4 (&x)[kU], uint32_t pbase,
-                   uint32_t& cr) {
+                   uint32_t& cr, uint32_t& wr) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       if (base + 32 * u + lane >= n) continue;
       const uint32_t v[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint32_t delta = shl_clamp(q, ((v[j] - pbase) >> (FL - 3)) & ~7u);
+        const uint32_t delta = shl_clamp(q, ((v[j] - pbase) >> (FL - LB)) & ~(FB - 1u));
         const uint32_t old = atoms_add(acc_s + ((v[j] & (Wd - 1)) << 2), delta);
-        cr |= (old + delta) & ~old & 0x80808080u;
+        const uint32_t sum = old + delta;
+        cr |= sum & ~old;
+        if (FB == 4) wr |= old & ~sum;
       }
     }
   };
@@ -158,7 +173,7 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
       for (int j = 0; j < 4; ++j) {
         const uint32_t sl = v[j] - pbase;
         if (sl >= SP) continue;
-        if (((acc[v[j] & (Wd - 1)] >> (8 * (sl >> FL))) & 0xFFu) >= 0x80u) {
+        if (((acc[v[j] & (Wd - 1)] >> (FB * (sl >> FL))) & FMASK) > (FMASK >> 1)) {
           atomicOr(cand + (sl >> 5), 1u << (sl & 31));
           cflag |= 1u << (sl >> 10);
         }
@@ -304,9 +319,10 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
 
     // ---- apply the current step -------------------------------------------------------
     {
-      uint32_t cr = 0;
-      apply(s_base, s_n, xc, c_pbase, cr);
-      if (cr) mark(s_base, s_n, xc, c_pbase, cflag);
+      uint32_t cr = 0, wr = 0;
+      apply(s_base, s_n, xc, c_pbase, cr, wr);
+      if (cr & TOP) mark(s_base, s_n, xc, c_pbase, cflag);
+      if (FB == 4 && (wr & TOP)) atomicExch(p.wrap, 1);
     }
     if (same_unit) {
       s_b0 = n_b0;
@@ -332,14 +348,14 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
         const uint32_t wsub = __ffs(cmask) - 1;
         const uint64_t it = uint64_t(c_row) * p.nW + w0 + wsub;
         const uint32_t slw = wsub * 1024 + lane * 32;  // this lane's 32 samples
-        const uint32_t fs = 8 * (slw >> FL);
+        const uint32_t fs = FB * (slw >> FL);
         const uint32_t* const aw = acc + (slw & (Wd - 1));
         const uint32_t t = cand[slw >> 5];
         uint32_t keep = 0;
         cand[slw >> 5] = 0u;
         for (uint32_t tt = t; tt; tt &= tt - 1) {
           const uint32_t bt = __ffs(tt) - 1;
-          const int ai = int(((aw[bt] >> fs) & 0xFFu) - p.foff);
+          const int ai = int(((aw[bt] >> fs) & FMASK) - p.foff);
           if (__int2float_rn(ai) > thr) {
             const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
             if (layer_epilogue(x, b, p.clip) != 0.0f) keep |= 1u << bt;
@@ -362,7 +378,7 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
           unsigned long long pos = off + (incl - mine);
           for (; keep; keep &= keep - 1) {
             const uint32_t bt = __ffs(keep) - 1;
-            const int ai = int(((aw[bt] >> fs) & 0xFFu) - p.foff);
+            const int ai = int(((aw[bt] >> fs) & FMASK) - p.foff);
             const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
             p.sc_c[pos] = c_pbase + slw + bt;
             p.sc_v[pos] = layer_epilogue(x, b, p.clip);
@@ -463,31 +479,33 @@ __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __
 
 }  // namespace
 
-size_t stream_warp_bytes(int fl) { return warp_bytes(fl); }
-
-size_t stream_block_bytes(int fl) { return size_t(kSW) * stream_warp_bytes(fl); }
+size_t stream_block_bytes(int fl, int fb) { return size_t(kSW) * warp_bytes(fl, fb); }
 
 int stream_block_threads() { return 32 * kSW; }
 
-template <int NS>
+template <int NS, int FB>
 static const void* stream_kernel_ns(int fl) {
   switch (fl) {
-    case 8: return reinterpret_cast<const void*>(k_exact_stream<8, NS>);
-    case 9: return reinterpret_cast<const void*>(k_exact_stream<9, NS>);
-    case 10: return reinterpret_cast<const void*>(k_exact_stream<10, NS>);
-    case 11: return reinterpret_cast<const void*>(k_exact_stream<11, NS>);
-    case 12: return reinterpret_cast<const void*>(k_exact_stream<12, NS>);
+    case 8: return reinterpret_cast<const void*>(k_exact_stream<8, NS, FB>);
+    case 9: return reinterpret_cast<const void*>(k_exact_stream<9, NS, FB>);
+    case 10: return reinterpret_cast<const void*>(k_exact_stream<10, NS, FB>);
+    case 11: return reinterpret_cast<const void*>(k_exact_stream<11, NS, FB>);
   }
-  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: field log2 must be 8..12");
+  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: field log2 must be 8..11");
 }
 
-const void* stream_kernel(int fl, int ns) {
-  switch (ns) {
-    case 1: return stream_kernel_ns<1>(fl);
-    case 2: return stream_kernel_ns<2>(fl);
-    case 3: return stream_kernel_ns<3>(fl);
-  }
-  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: in-edge slots must be 1..3");
+const void* stream_kernel(int fl, int ns, int fb) {
+  if (fb == 8) switch (ns) {
+      case 1: return stream_kernel_ns<1, 8>(fl);
+      case 2: return stream_kernel_ns<2, 8>(fl);
+      case 3: return stream_kernel_ns<3, 8>(fl);
+    }
+  if (fb == 4) switch (ns) {
+      case 1: return stream_kernel_ns<1, 4>(fl);
+      case 2: return stream_kernel_ns<2, 4>(fl);
+      case 3: return stream_kernel_ns<3, 4>(fl);
+    }
+  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: in-edge slots 1..3, fields of 4 or 8 bits");
 }
 
 size_t padded_size(uint32_t rows, size_t nnz) { return 4 * size_t(rows) + (nnz & ~size_t(3)) + 8; }
@@ -499,9 +517,9 @@ void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint
   SK_LAUNCH(k_pad_passes, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
 }
 
-void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, unsigned grid,
-                         size_t smem) {
-  const void* kern = stream_kernel(fl, ns);
+void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb,
+                         unsigned grid, size_t smem) {
+  const void* kern = stream_kernel(fl, ns, fb);
   void* args[] = {const_cast<StreamArgs*>(&p)};
   SK_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(32 * kSW), args, smem, ctx->stream));
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -28,20 +28,22 @@ struct StreamArgs {
   unsigned long long* work;
   unsigned long long cap;
   int* overflow;
+  int* wrap;              // 4-bit fields: a field wrapped (the layer is rerun with 8-bit ones)
 };
 
-// shared memory of one warp / one block for field log2 fl; threads per block
-size_t stream_warp_bytes(int fl);
-size_t stream_block_bytes(int fl);
+// shared memory of one block for 2^fl accumulator words of fb-bit fields;
+// threads per block
+size_t stream_block_bytes(int fl, int fb);
 int stream_block_threads();
-// the kernel for field log2 fl (8..12) and ns in-edge slots per lane (in-degree <= 32 ns)
-const void* stream_kernel(int fl, int ns);
+// the kernel for 2^fl accumulator words (fl 8..11; 8..10 with 4-bit fields),
+// ns in-edge slots per lane (in-degree <= 32 ns) and fb-bit fields (8 or 4)
+const void* stream_kernel(int fl, int ns, int fb);
 // The padded copy of an activation CSR's columns (rows 16-byte aligned, sentinel
 // gaps; padded_size words) and its pass table (rows * nP + 1 words).
 size_t padded_size(uint32_t rows, size_t nnz);
 void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
                        uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc);
-void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, unsigned grid,
-                         size_t smem);
+void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb,
+                         unsigned grid, size_t smem);
 
 }  // namespace sk

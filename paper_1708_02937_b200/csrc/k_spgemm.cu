@@ -2344,9 +2344,8 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   const bool fast0 = g.sh == 10 && coarse && probe.q_const && probe.fx_pack == 4;
   // K7 applies where the specialised kernel's preconditions hold, every product
   // is a positive increment, in-degrees are <= 96 and the padded copy of Y fits
-  // 32-bit unit indices; automatically (exact_kernel 0) where a pass of 8192
-  // samples holds >= 500 entries per row (cfg3 / cfg4: measured faster than the
-  // specialised kernel; cfg5's ~260 per pass: the specialised kernel is as fast)
+  // 32-bit unit indices (measured faster than the specialised kernel on cfg3,
+  // cfg4 and cfg5: 0.65 / 0.71 / 1.89 ms against 0.76 / 1.09 / 2.36)
   const double erow0 = double(y0->nnz) / double(std::max<uint32_t>(1, y0->rows));
   const double deg0 = double(w->nnz) / double(std::max<uint32_t>(1, m));
   auto stream_pass = [&](int fl) {
@@ -2355,35 +2354,41 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   const bool stream_ok = fast0 && probe.q_cval > 0 && n <= 0xFFFFF000u &&
                          L_.wstats.maxdeg <= 96 &&
                          padded_size(y0->rows, y0->nnz) < 0xFFFFFFF0ull;
-  const bool stream = stream_ok && (ctx->tune.exact_kernel == 5 ||
-                                    (ctx->tune.exact_kernel == 0 && stream_pass(11) >= 500.0));
+  const bool stream = stream_ok && (ctx->tune.exact_kernel == 5 || ctx->tune.exact_kernel == 0);
   if (stream) {
-    // The largest pass up to 2^11 accumulator words (8 KB: ~17 warps per SM
-    // with the records; 16 KB halves that) holding <= 2000 entries per row.
-    int fl = 8;
+    // 4-bit fields: the smallest threshold t' (count units) <= 7 and an
+    // increment <= 8, so a field below its top bit cannot wrap in one step
+    RowArgs pr0;
+    exact_params(L_.wstats, ystats, g.S, pr0, thr);
+    const uint32_t tmin = 127u - pr0.fx_off;
+    // The pass: 16384 samples (4-bit fields, 8 KB of accumulator) when a row
+    // holds <= 2500 entries in it, else the largest of 8192..1024 holding <= 4000
+    // (measured: cfg4 16384 0.67 ms / 8192 0.71; cfg5 1.52 / 1.90; cfg3 (7900
+    // entries per 16384) 0.72 / 0.64)
+    const bool nib_ok = tmin <= 7 && probe.q_cval <= 8 && ctx->tune.exact_fields != 8;
+    int sp_lg = 10;
     if (ctx->tune.exact_group) {
       const int g = ctx->tune.exact_group;  // windows per pass
-      fl = g == 1 ? 8 : g == 2 ? 9 : g == 4 ? 10 : g == 8 ? 11 : 12;
+      sp_lg = g == 1 ? 10 : g == 2 ? 11 : g == 4 ? 12 : g == 8 ? 13 : 14;
+    } else if (nib_ok && stream_pass(12) <= 2500.0) {
+      sp_lg = 14;
     } else {
-      for (int f = 11; f > 8; --f)
-        if (stream_pass(f) <= 2000.0) { fl = f; break; }
+      for (int f = 13; f > 10; --f)
+        if (stream_pass(f - 2) <= 4000.0) { sp_lg = f; break; }
     }
-    // no pass wider than the batch needs
-    while (fl > 8 && (4u << (fl - 1)) >= n) --fl;
+    while (sp_lg > 10 && (1u << (sp_lg - 1)) >= n) --sp_lg;  // no wider than the batch
+    const bool nib = nib_ok && sp_lg >= 11;
+    int fb = nib ? 4 : 8;
+    if (fb == 8 && sp_lg == 14) sp_lg = 13;  // 8-bit fields: at most 2^11 words
     WinGeom gs;
-    gs.sh = fl + 2;
-    gs.S = 4u << fl;
+    gs.sh = sp_lg;
+    gs.S = 1u << sp_lg;
     gs.nW = std::max<uint32_t>(1, uint32_t((uint64_t(n) + gs.S - 1) >> gs.sh));
     // the padded copy of Y's columns and its pass table
     uint32_t* pci = aalloc<uint32_t>(ctx, padded_size(y0->rows, y0->nnz));
     uint32_t* wps = aalloc<uint32_t>(ctx, size_t(y0->rows) * gs.nW + 1);
     launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps);
     const int ns = std::max(1, (L_.wstats.maxdeg + 31) / 32);  // in-edge slots per lane
-    const size_t smem = stream_block_bytes(fl);
-    const void* kern = stream_kernel(fl, ns);
-    kernel_smem_attr(ctx, kern, int(smem));
-    const int per_sm = kernel_occupancy(ctx, kern, stream_block_threads(), smem);
-    const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
     auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
       c = std::min<unsigned long long>(c, full);
@@ -2394,13 +2399,20 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     unsigned long long cap = clamp_cap(std::max<unsigned long long>(4ull * y0->nnz, 1ull << 24),
                                        (unsigned long long)(ctx->total_mem * 0.3 / 24.0));
     for (int attempt = 0; attempt < 2; ++attempt) {
+      const int fl = sp_lg - (fb == 4 ? 3 : 2);
+      const size_t smem = stream_block_bytes(fl, fb);
+      const void* kern = stream_kernel(fl, ns, fb);
+      kernel_smem_attr(ctx, kern, int(smem));
+      const int per_sm = kernel_occupancy(ctx, kern, stream_block_threads(), smem);
+      const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
       uint32_t* item_cnt = aalloc<uint32_t>(ctx, items + 1);
       unsigned long long* item_off =
           reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, items));
       uint32_t* sc_c = aalloc<uint32_t>(ctx, cap);
       float* sc_v = aalloc<float>(ctx, cap);
       uint32_t* wp_out = aalloc<uint32_t>(ctx, items + 1);
-      SK_CUDA(cudaMemsetAsync(d, 0, 24, ctx->stream));  // d[0] bump, d[1] overflow, d[2] work
+      // d[0] bump, d[1] overflow, d[2] work, d[3] wrap
+      SK_CUDA(cudaMemsetAsync(d, 0, 32, ctx->stream));
       StreamArgs sa;
       sa.arp = w->rp;
       sa.aci = w->ci;
@@ -2415,8 +2427,8 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       sa.q = uint32_t(probe.q_cval);
       RowArgs pr;
       exact_params(L_.wstats, ystats, g.S, pr, thr);
-      sa.foff = pr.fx_off;
-      sa.clearw = pr.fx_clearw;
+      sa.foff = fb == 4 ? 7u - tmin : pr.fx_off;
+      sa.clearw = fb == 4 ? sa.foff * 0x11111111u : pr.fx_clearw;
       sa.fx_scale = pr.fx_scale;
       sa.fx_unscale = pr.fx_unscale;
       sa.item_cnt = item_cnt;
@@ -2427,21 +2439,29 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       sa.work = d + 2;
       sa.cap = cap;
       sa.overflow = reinterpret_cast<int*>(d + 1);
+      sa.wrap = reinterpret_cast<int*>(d + 3);
       ctx->last_exact.launches += 1;
       ctx->last_exact.kernel = 5;
       ctx->last_exact.group = int(gs.S >> 10);
       ctx->last_exact.records = 0;
       ctx->last_exact.window_log2 = g.sh;
-      ctx->last_exact.fields = 4;
+      ctx->last_exact.fields = 32 / fb;
       timing_mark(ctx, SK_KT_STREAM);
-      launch_exact_stream(ctx, sa, fl, ns, grid, smem);
+      launch_exact_stream(ctx, sa, fl, ns, fb, grid, smem);
       timing_mark(ctx);
       SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
       exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
       uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
       SK_CUDA(cudaMemcpyAsync(hp, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
       SK_CUDA(cudaMemcpyAsync(hp + 1, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      SK_CUDA(cudaMemcpyAsync(hp + 2, d + 3, 4, cudaMemcpyDeviceToHost, ctx->stream));
       sync(ctx);
+      if (hp[2]) {  // a 4-bit field wrapped: rerun with 8-bit fields
+        fb = 8;
+        ctx->last_exact.wraps += 1;
+        --attempt;
+        continue;
+      }
       const uint32_t nnz = hp[0];
       const int ovf = int(hp[1]);
       if (!ovf && L_.stage) {

@@ -334,6 +334,8 @@ extern "C" sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t) {
     auto wl = [](int v) { return v == 0 || (v >= 8 && v <= 12); };
     if (!wl(t->window_log2) || !wl(t->exact_window_log2))
       fail(SK_ERR_INVALID_ARGUMENT, "tuning: window log2 must be 0 or 8..12");
+    if (!in(t->exact_fields, {0, 4, 8}))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_fields must be 0, 4 or 8");
     if (!(t->esc_ratio == t->esc_ratio))
       fail(SK_ERR_INVALID_ARGUMENT, "tuning: esc_ratio is NaN");
     ctx->tune = *t;

@@ -974,3 +974,65 @@ def test_dense_leg_packed_weights_cache(sk, ref, port):
     r1 = sk.dense_relu_forward(model, yd).numpy()
     r2 = sk.dense_relu_forward(model, yd).numpy()
     assert np.array_equal(r1, r2)
+
+
+def _in_degree_weights(m, maxdeg, seed):
+    """W_ref with in-degrees 0..maxdeg (row i: (37 i) mod (maxdeg + 1) in-edges at
+    distinct random inputs), every value 1/16: a constant increment."""
+    from oracle.oracle import Csr
+    rng = np.random.default_rng(seed)
+    rp, ci = [0], []
+    for i in range(m):
+        d = (37 * i) % (maxdeg + 1)
+        ci.extend(sorted(rng.choice(m, size=d, replace=False).tolist()))
+        rp.append(len(ci))
+    return Csr(m, m, np.array(rp, np.uint32), np.array(ci, np.uint32),
+               np.full(len(ci), 1.0 / 16, np.float32))
+
+
+# (m, samples, active inputs per sample, bias, clip, max in-degree, counter width)
+STREAM_CASES = [
+    (8192, 5000, 120, -0.3, 32.0, 64, 0),     # 4-bit counters, 8192-sample passes + a partial one
+    (8192, 5000, 120, -0.3, 32.0, 64, 8),     # the same with 8-bit counters
+    (4096, 700, 200, -0.45, 32.0, 40, 0),     # a batch narrower than one pass (t' = 7: 4-bit edge)
+    (4096, 3000, 400, -0.5, 0.0, 96, 0),      # t' = 8: 8-bit counters; three in-edge slots
+    (16384, 3000, 3000, -0.1, 2.0, 70, 0),    # 4-bit counters wrap (counts >= 10): the rerun;
+                                              # clip 2 is active
+    (2048, 20000, 4, -0.05, 32.0, 33, 0),     # 16384-sample passes, sparse passes (touched clear)
+]
+
+
+@pytest.mark.parametrize("case", STREAM_CASES)
+def test_stream_kernel_regimes(sk, port, case):
+    """K7 (k_exact_stream, the order-free row stream) against the oracle's sparse
+    layer (matrix.cpp:452-521 + dnn.cpp:86-103 restated) in the regimes its
+    host logic chooses between: 4- vs 8-bit counters, a 4-bit counter wrapping
+    (the layer is rerun with 8-bit ones), in-degrees up to 96 (one to three
+    in-edge slots per lane, rows with none), a batch narrower than one pass,
+    passes that end past the batch, the touched-word clear of sparse passes."""
+    m, n, kY, bias, clip, maxdeg, fields = case
+    hW = _in_degree_weights(m, maxdeg, m + n)
+    hY = port.gen_input_binary(m, n, kY, 7)
+    b = np.full(m, bias, np.float32)
+    want = port.layer_sparse(hW, b, hY, clip)
+    ctx = sk.default_context()
+    # the wrapping case: 2048-sample passes (the widest that take 4-bit counters
+    # is chosen narrower for this density)
+    old = ctx.set_tuning(exact_kernel=5, exact_fields=fields,
+                         exact_group=2 if bias == -0.1 else 0)
+    ctx.set_density_switch(0.0, 0.0)  # keep the activations sparse
+    try:
+        n0 = ctx.last_exact()["wraps"]
+        model = sk.DnnModel([dev_csr(sk, hW)], [b])
+        out, trace = sk.relu_forward_sparse(model, dev_csr(sk, hY), sk.ForwardOptions(clip=clip))
+        info = ctx.last_exact()
+    finally:
+        ctx.set_tuning(**old)
+        ctx.set_density_switch()
+    assert ctx.layer_paths(1) == ["exact"] and info["kernel"] == "stream", info
+    assert list(trace) == [hY.nnz, want.nnz]
+    assert_csr_bitwise(out, want)
+    if fields == 8 or bias == -0.5:
+        assert info["fields"] == 4, info  # 8-bit counters: four per word
+    if bias == -0.1:
+        assert want.nnz > 100000 and info["wraps"] > n0, info  # the 4-bit pass wrapped

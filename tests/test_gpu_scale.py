@@ -5,10 +5,10 @@
   set) bitwise against the C restatement of the reference's sparse layer
   (oracle/sk_oracle.c, pinned to proj/src/matrix.cpp:452-521 + dnn.cpp:86-121),
   and the kernel the bench runs asserted (sk_ctx_last_exact): K7 (the row
-  stream, k_exact_stream.cu) on cfg3/cfg4, the specialised windowed kernel on
-  cfg5.
+  stream, k_exact_stream.cu).
 * Layer 1 of each at full scale with EVERY exact-layer variant forced through
-  the per-context tuning (K7 at 1 / 2 / 4 / 8 / 16 windows per pass;
+  the per-context tuning (K7 at 1 / 2 / 4 / 8 / 16 windows per pass x 4-bit
+  (where the threshold allows) / 8-bit counters;
   generic / specialised kernel x 64 / 192 records x
   4..64 windows per item, i.e. 1..16 accumulator passes per item, plus the
   other window sizes), at the bench bias and at a less negative bias whose
@@ -34,8 +34,7 @@ CFG = {
     "cfg5": (262144, 120, 262, -0.45, -0.1),
 }
 # the records / kernel the bench takes on layer 1 (profiles/r01 launch lists)
-BENCH_KERNEL = {"cfg3": (0, "stream"), "cfg4": (0, "stream"),
-                "cfg5": (64, "specialised")}
+BENCH_KERNEL = {"cfg3": (0, "stream"), "cfg4": (0, "stream"), "cfg5": (0, "stream")}
 
 
 def bits(a):
@@ -138,10 +137,11 @@ def test_exact_layer_every_variant_full_scale(sk, port, ctx, cfg, which):
               for k in (1, 2) for r in (64, 192) for g in (4, 8, 16, 32, 64)]
     combos += [dict(exact_kernel=1, exact_window_log2=s) for s in (8, 9, 11, 12)]
     combos += [dict(exact_kernel=3), dict(exact_kernel=4)]
-    combos += [dict(exact_kernel=5, exact_group=g) for g in (1, 2, 4, 8, 16)]
+    combos += [dict(exact_kernel=5, exact_group=g, exact_fields=f)
+               for g in (1, 2, 4, 8, 16) for f in (0, 8)]
     for c in combos:
         ctx.set_tuning(**dict(dict(exact_kernel=0, exact_records=0, exact_group=0,
-                                   exact_window_log2=0), **c))
+                                   exact_window_log2=0, exact_fields=0), **c))
         out, trace = sk.relu_forward_sparse(model, Y0, sk.ForwardOptions(clip=32.0))
         info = ctx.last_exact()
         assert ctx.layer_paths(1) == ["exact"], c
@@ -152,8 +152,11 @@ def test_exact_layer_every_variant_full_scale(sk, port, ctx, cfg, which):
         if c["exact_kernel"] == 4:  # flattened products (the specialised kernel's shape)
             assert info["kernel"] == "flat", (c, info)
             continue
-        if c["exact_kernel"] == 5:  # K7: windows per pass as asked
-            assert (info["kernel"], info["group"]) == ("stream", c["exact_group"]), (c, info)
+        if c["exact_kernel"] == 5:  # K7: windows per pass as asked (8-bit: at most 8)
+            g = min(c["exact_group"], 8) if c["exact_fields"] == 8 else c["exact_group"]
+            assert (info["kernel"], info["group"]) == ("stream", g), (c, info)
+            if c["exact_fields"] == 8:
+                assert info["fields"] == 4, (c, info)
             continue
         assert info["kernel"] == {1: "generic", 2: "specialised"}[c["exact_kernel"]], (c, info)
         if "exact_records" in c:

@@ -28,7 +28,8 @@ def run(ctx, model, Y0, opt, reps=5):
 
 
 GROUPS = [int(x) for x in os.environ.get("SC_GROUPS", "0,1,2,4,8,16").split(",")]
-RECS = [int(x) for x in os.environ.get("SC_RECS", "0,192").split(",")]
+RECS = [int(x) for x in os.environ.get("SC_RECS", "0").split(",")]
+FIELDS = [int(x) for x in os.environ.get("SC_FIELDS", "0,8").split(",")]
 
 
 def main():
@@ -47,15 +48,15 @@ def main():
             rr = ref.extract()
             res = {"specialised": t_ref, "nnz": int(ref.nnz())}
             for grp in GROUPS:
-                for rec in RECS:
-                    ctx.set_tuning(exact_kernel=5, exact_group=grp, exact_records=rec)
+                for fb in FIELDS:
+                    ctx.set_tuning(exact_kernel=5, exact_group=grp, exact_fields=fb)
                     out, t, info = run(ctx, model, Y0, opt)
                     oo = out.extract()
                     same = all(np.array_equal(a.view(np.uint32), b.view(np.uint32))
                                for a, b in zip(oo, rr))
-                    res[f"g{grp}r{rec}"] = [t, info["kernel"], info["group"], info["records"],
-                                           "OK" if same else "DIFF"]
-            ctx.set_tuning(exact_kernel=0, exact_group=0, exact_records=0)
+                    res[f"g{grp}f{fb}"] = [t, info["kernel"], info["group"], info["fields"],
+                                          "OK" if same else "DIFF", info["wraps"]]
+            ctx.set_tuning(exact_kernel=0, exact_group=0, exact_fields=0)
             print(json.dumps({name: {str(bias): res}}), flush=True)
 
 
