@@ -25,10 +25,11 @@
 //    atomic still runs, on an arbitrary word, and changes nothing), so the
 //    update loop has no per-entry branch; the next step's loads are issued
 //    before the current step's atomics.
-//  * Per pass: emit the windows (1024 samples, the output window table's unit)
-//    holding candidates -- each candidate evaluated with the row's own
-//    threshold and epilogue -- into scratch spans (item counts per (row,
-//    window), scanned and gathered by the host code as for k_exact_layer), then
+//  * Per pass: emit the survivors -- each candidate evaluated with the row's own
+//    threshold and epilogue -- into a scratch span (one item per (row, pass):
+//    count and offset, scanned and gathered by the host code as for
+//    k_exact_layer; per-window items would write m * n / 1024 counts, 62 MB on
+//    cfg5, almost all zero), then
 //    clear the accumulator: all of it, or when the pass is sparse only the words
 //    its entries touched (cfg5: a full clear per pass would write m * n bytes of
 //    shared memory, 15.7 GB per layer).
@@ -334,26 +335,26 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
     __syncwarp();
     uint32_t* const rec = recs + cb * RC;
 
-    // ---- emit the pass's windows --------------------------------------------------
-    const uint32_t w0 = c_pass * NWP;
-    const uint32_t nwp = min(NWP, p.nW - w0);
+    // ---- emit the pass: one item per (row, pass) ------------------------------------
+    // Candidates of the windows that hold any are evaluated with the row's own
+    // threshold and epilogue (keep masks replace the candidate words); one
+    // reservation per pass; survivors are written window by window, lane by
+    // lane: sample order.
+    const uint64_t it = uint64_t(c_row) * nP + c_pass;
     uint32_t cmask = __reduce_or_sync(0xffffffffu, cflag);
-    if (uint32_t(lane) < nwp && !((cmask >> lane) & 1u))
-      p.item_cnt[uint64_t(c_row) * p.nW + w0 + lane] = 0u;
-    if (cmask) {
+    if (!cmask) {
+      if (lane == 0) p.item_cnt[it] = 0u;
+    } else {
       const float b = __ldg(p.bias + c_row);
       const float thr = __fmul_rn(-b, p.fx_scale);
+      uint32_t tot = 0;
 #pragma unroll 1
-      for (; cmask; cmask &= cmask - 1) {
-        const uint32_t wsub = __ffs(cmask) - 1;
-        const uint64_t it = uint64_t(c_row) * p.nW + w0 + wsub;
-        const uint32_t slw = wsub * 1024 + lane * 32;  // this lane's 32 samples
+      for (uint32_t cm = cmask; cm; cm &= cm - 1) {
+        const uint32_t slw = (__ffs(cm) - 1) * 1024 + lane * 32;  // this lane's 32 samples
         const uint32_t fs = FB * (slw >> FL);
         const uint32_t* const aw = acc + (slw & (Wd - 1));
-        const uint32_t t = cand[slw >> 5];
         uint32_t keep = 0;
-        cand[slw >> 5] = 0u;
-        for (uint32_t tt = t; tt; tt &= tt - 1) {
+        for (uint32_t tt = cand[slw >> 5]; tt; tt &= tt - 1) {
           const uint32_t bt = __ffs(tt) - 1;
           const int ai = int(((aw[bt] >> fs) & FMASK) - p.foff);
           if (__int2float_rn(ai) > thr) {
@@ -361,21 +362,32 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
             if (layer_epilogue(x, b, p.clip) != 0.0f) keep |= 1u << bt;
           }
         }
+        cand[slw >> 5] = keep;
+        tot += __reduce_add_sync(0xffffffffu, __popc(keep));
+      }
+      unsigned long long off = 0;
+      if (lane == 0) {
+        if (tot) {
+          off = atomicAdd(p.bump, (unsigned long long)tot);
+          if (off + tot > p.cap) atomicExch(p.overflow, 1);
+        }
+        p.item_cnt[it] = tot;
+        p.item_off[it] = off;
+      }
+      off = __shfl_sync(0xffffffffu, off, 0);
+      const bool can = tot && off + tot <= p.cap;
+#pragma unroll 1
+      for (uint32_t cm = cmask; cm; cm &= cm - 1) {
+        const uint32_t slw = (__ffs(cm) - 1) * 1024 + lane * 32;
+        const uint32_t fs = FB * (slw >> FL);
+        const uint32_t* const aw = acc + (slw & (Wd - 1));
+        uint32_t keep = cand[slw >> 5];
+        cand[slw >> 5] = 0u;
         const uint32_t mine = __popc(keep);
         const uint32_t incl = incl_scan(mine, lane);
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned long long off = 0;
-        if (lane == 0) {
-          if (tot) {
-            off = atomicAdd(p.bump, (unsigned long long)tot);
-            if (off + tot > p.cap) atomicExch(p.overflow, 1);
-          }
-          p.item_cnt[it] = tot;
-          p.item_off[it] = off;
-        }
-        off = __shfl_sync(0xffffffffu, off, 0);
-        if (tot && off + tot <= p.cap) {
-          unsigned long long pos = off + (incl - mine);
+        unsigned long long pos = off + (incl - mine);
+        off += __shfl_sync(0xffffffffu, incl, 31);
+        if (can) {
           for (; keep; keep &= keep - 1) {
             const uint32_t bt = __ffs(keep) - 1;
             const int ai = int(((aw[bt] >> fs) & FMASK) - p.foff);
@@ -440,39 +452,53 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
 __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                              uint32_t rows, uint32_t nP, int sh, uint32_t* __restrict__ pci,
                              uint32_t* __restrict__ wpc) {
+  constexpr int kC = 8;  // entries per lane in flight (256 per warp)
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  uint32_t rb = 0, re = 0;
+  if (gw < rows) {
+    rb = __ldg(rp + gw);
+    re = __ldg(rp + gw + 1);
+  }
   for (uint32_t k = gw; k < rows; k += nw) {
-    const uint32_t rb = rp[k], re = rp[k + 1];
+    // the next row's bounds are fetched while this one is copied
+    const uint32_t kn = k + nw;
+    uint32_t nb = 0, ne = 0;
+    if (kn < rows) {
+      nb = __ldg(rp + kn);
+      ne = __ldg(rp + kn + 1);
+    }
     const uint32_t pb = 4 * k + (rb & ~3u), pn = 4 * (k + 1) + (re & ~3u);
     uint32_t* const out = wpc + size_t(k) * nP;
     int carry = -1;  // pass of the entry before this chunk (-1: none)
-    for (uint32_t e0 = rb; e0 < re; e0 += 128) {
-      uint32_t sv[4];
-      int we[4];
+    for (uint32_t e0 = rb; e0 < re; e0 += 32 * kC) {
+      uint32_t sv[kC];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kC; ++u) {
         const uint32_t e = e0 + 32 * u + lane;
         sv[u] = e < re ? __ldg(ci + e) : 0u;
-        we[u] = e < re ? int(sv[u] >> sh) : int(nP);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kC; ++u) {
         const uint32_t e = e0 + 32 * u + lane;
+        const int we = e < re ? int(sv[u] >> sh) : int(nP);
         if (e < re) pci[pb + (e - rb)] = sv[u];
-        int prev = __shfl_up_sync(0xffffffffu, we[u], 1);
+        int prev = __shfl_up_sync(0xffffffffu, we, 1);
         if (lane == 0) prev = carry;
         if (e < re)
-          for (int w = prev + 1; w <= we[u]; ++w) out[w] = pb + (e - rb);
-        carry = __shfl_sync(0xffffffffu, we[u], 31);
+          for (int w = prev + 1; w <= we; ++w) out[w] = pb + (e - rb);
+        carry = __shfl_sync(0xffffffffu, we, 31);
       }
     }
-    const int last = re > rb ? int(ci[re - 1] >> sh) : -1;
+    // passes after the row's last entry (all of them for an empty row)
+    const int last = re > rb ? int(__ldg(ci + re - 1) >> sh) : -1;
     for (int w = last + 1 + lane; w < int(nP); w += 32) out[w] = pb + (re - rb);
     // the gap up to the next row (and the slack after the last row)
     const uint32_t gend = k + 1 == rows ? pn + 8 : pn;
     for (uint32_t t = pb + (re - rb) + lane; t < gend; t += 32) pci[t] = 0xFFFFFFE0u | (t & 31u);
+    rb = nb;
+    re = ne;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) wpc[size_t(rows) * nP] = 4 * rows + (rp[rows] & ~3u);
 }
@@ -512,8 +538,10 @@ size_t padded_size(uint32_t rows, size_t nnz) { return 4 * size_t(rows) + (nnz &
 
 void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
                        uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc) {
+  // one resident wave (8 blocks of 8 warps per SM), each warp walking rows with
+  // the next row's bounds prefetched
   const unsigned blocks = unsigned(std::max<uint64_t>(
-      1, std::min<uint64_t>((uint64_t(rows) + 7) / 8, uint64_t(ctx->num_sms) * 64)));
+      1, std::min<uint64_t>((uint64_t(rows) + 7) / 8, uint64_t(ctx->num_sms) * 8)));
   SK_LAUNCH(k_pad_passes, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
 }
 

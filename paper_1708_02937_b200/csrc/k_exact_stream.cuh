@@ -14,13 +14,14 @@ struct StreamArgs {
   const uint32_t* aci;  // W_ref columns
   const uint32_t* bci;  // Y columns, padded copy (launch_pad_passes)
   const uint32_t* wpc;  // pass table: wpc[k*nP + j] = first padded entry of Y row k with sample >= j*SP
-  uint32_t m, n, nP, nW;  // output rows, samples, passes, 1024-sample output windows
+  uint32_t m, n, nP, nW;  // output rows, samples, passes, 1024-sample windows
+                          // (items: one per (row, pass), item_cnt[row * nP + pass])
   const float* bias;
   float clip;
   uint32_t q;             // the constant fixed-point increment
   uint32_t foff, clearw;  // field offset (sum + foff in each 8-bit field), cleared word
   float fx_scale, fx_unscale;
-  uint32_t* item_cnt;     // per (row, output window)
+  uint32_t* item_cnt;     // per (row, pass)
   unsigned long long* item_off;
   uint32_t* sc_c;
   float* sc_v;

@@ -2398,6 +2398,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     };
     unsigned long long cap = clamp_cap(std::max<unsigned long long>(4ull * y0->nnz, 1ull << 24),
                                        (unsigned long long)(ctx->total_mem * 0.3 / 24.0));
+    const uint64_t sitems = uint64_t(m) * gs.nW;  // one output item per (row, pass)
     for (int attempt = 0; attempt < 2; ++attempt) {
       const int fl = sp_lg - (fb == 4 ? 3 : 2);
       const size_t smem = stream_block_bytes(fl, fb);
@@ -2405,12 +2406,12 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       kernel_smem_attr(ctx, kern, int(smem));
       const int per_sm = kernel_occupancy(ctx, kern, stream_block_threads(), smem);
       const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
-      uint32_t* item_cnt = aalloc<uint32_t>(ctx, items + 1);
+      uint32_t* item_cnt = aalloc<uint32_t>(ctx, sitems + 1);
       unsigned long long* item_off =
-          reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, items));
+          reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, sitems));
       uint32_t* sc_c = aalloc<uint32_t>(ctx, cap);
       float* sc_v = aalloc<float>(ctx, cap);
-      uint32_t* wp_out = aalloc<uint32_t>(ctx, items + 1);
+      uint32_t* wp_out = aalloc<uint32_t>(ctx, sitems + 1);
       // d[0] bump, d[1] overflow, d[2] work, d[3] wrap
       SK_CUDA(cudaMemsetAsync(d, 0, 32, ctx->stream));
       StreamArgs sa;
@@ -2449,10 +2450,10 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       timing_mark(ctx, SK_KT_STREAM);
       launch_exact_stream(ctx, sa, fl, ns, fb, grid, smem);
       timing_mark(ctx);
-      SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
-      exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
+      SK_CUDA(cudaMemsetAsync(item_cnt + sitems, 0, 4, ctx->stream));
+      exclusive_scan_u32(ctx, item_cnt, wp_out, sitems + 1);
       uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
-      SK_CUDA(cudaMemcpyAsync(hp, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      SK_CUDA(cudaMemcpyAsync(hp, wp_out + sitems, 4, cudaMemcpyDeviceToHost, ctx->stream));
       SK_CUDA(cudaMemcpyAsync(hp + 1, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
       SK_CUDA(cudaMemcpyAsync(hp + 2, d + 3, 4, cudaMemcpyDeviceToHost, ctx->stream));
       sync(ctx);
@@ -2468,8 +2469,8 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
         StagedLayer* st = L_.stage;
         st->m = m;
         st->n = n;
-        st->nW = g.nW;
-        st->items = items;
+        st->nW = gs.nW;
+        st->items = sitems;
         st->nnz = nnz;
         st->item_cnt = item_cnt;
         st->item_off = item_off;
@@ -2481,11 +2482,11 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       }
       if (!ovf) {
         sk_csr* o = new_csr(ctx, m, n, nnz);
-        SK_LAUNCH(k_gather_items, grid_warps(ctx, items), 256, 0, ctx->stream, item_cnt,
-                  item_off, wp_out, items, sc_c, sc_v, o->ci, o->v, sa.overflow);
-        SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, g.nW,
+        SK_LAUNCH(k_gather_items, grid_warps(ctx, sitems), 256, 0, ctx->stream, item_cnt,
+                  item_off, wp_out, sitems, sc_c, sc_v, o->ci, o->v, sa.overflow);
+        SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, gs.nW,
                   o->rp);
-        *wp_out_ptr = same_geometry ? wp_out : nullptr;
+        *wp_out_ptr = nullptr;  // items per pass: not the engine's window table
         return o;
       }
       size_t free_b = 0, total_b = 0;
