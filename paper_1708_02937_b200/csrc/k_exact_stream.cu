@@ -46,7 +46,6 @@ namespace sk {
 namespace {
 
 constexpr int kSW = 1;  // warps per block (the accumulator base is then block-uniform)
-constexpr int kU = 4;   // 16-byte units per lane and step
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 // accumulator (2^fl words of 32 / fb fields) + candidate bitmap (a bit per
@@ -89,7 +88,8 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
 // small: twice the samples per accumulator byte; a field that wraps is detected
 // -- its top bit goes from set to clear -- and the host reruns the layer with
 // 8-bit fields)
-template <int FL, int NS, int FB>
+// KU: 16-byte units per lane and step (4 for long passes, 6 for short ones)
+template <int FL, int NS, int FB, int kU>
 __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   extern __shared__ __align__(16) uint8_t smraw[];
   constexpr uint32_t Wd = 1u << FL;                 // accumulator words
@@ -470,8 +470,7 @@ __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __
       ne = __ldg(rp + kn + 1);
     }
     const uint32_t pb = 4 * k + (rb & ~3u), pn = 4 * (k + 1) + (re & ~3u);
-    uint32_t* const out = wpc + size_t(k) * nP;
-    int carry = -1;  // pass of the entry before this chunk (-1: none)
+    uint32_t* const dst = pci + pb - rb;  // entry e of the row goes to dst[e]
     for (uint32_t e0 = rb; e0 < re; e0 += 32 * kC) {
       uint32_t sv[kC];
 #pragma unroll
@@ -482,18 +481,21 @@ __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __
 #pragma unroll
       for (int u = 0; u < kC; ++u) {
         const uint32_t e = e0 + 32 * u + lane;
-        const int we = e < re ? int(sv[u] >> sh) : int(nP);
-        if (e < re) pci[pb + (e - rb)] = sv[u];
-        int prev = __shfl_up_sync(0xffffffffu, we, 1);
-        if (lane == 0) prev = carry;
-        if (e < re)
-          for (int w = prev + 1; w <= we; ++w) out[w] = pb + (e - rb);
-        carry = __shfl_sync(0xffffffffu, we, 31);
+        if (e < re) dst[e] = sv[u];
       }
     }
-    // passes after the row's last entry (all of them for an empty row)
-    const int last = re > rb ? int(__ldg(ci + re - 1) >> sh) : -1;
-    for (int w = last + 1 + lane; w < int(nP); w += 32) out[w] = pb + (re - rb);
+    // pass table: lane j finds the first entry of pass j by a binary search of the
+    // (sorted) row -- passes are few, the row is in L1/L2 from the copy
+    uint32_t* const out = wpc + size_t(k) * nP;
+    for (uint32_t j = lane; j < nP; j += 32) {
+      const uint32_t key = j << sh;
+      uint32_t lo = rb, hi = re;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(ci + mid) < key) lo = mid + 1; else hi = mid;
+      }
+      out[j] = pb + (lo - rb);
+    }
     // the gap up to the next row (and the slack after the last row)
     const uint32_t gend = k + 1 == rows ? pn + 8 : pn;
     for (uint32_t t = pb + (re - rb) + lane; t < gend; t += 32) pci[t] = 0xFFFFFFE0u | (t & 31u);
@@ -509,29 +511,28 @@ size_t stream_block_bytes(int fl, int fb) { return size_t(kSW) * warp_bytes(fl, 
 
 int stream_block_threads() { return 32 * kSW; }
 
-template <int NS, int FB>
+template <int NS, int FB, int KU>
 static const void* stream_kernel_ns(int fl) {
   switch (fl) {
-    case 8: return reinterpret_cast<const void*>(k_exact_stream<8, NS, FB>);
-    case 9: return reinterpret_cast<const void*>(k_exact_stream<9, NS, FB>);
-    case 10: return reinterpret_cast<const void*>(k_exact_stream<10, NS, FB>);
-    case 11: return reinterpret_cast<const void*>(k_exact_stream<11, NS, FB>);
+    case 8: return reinterpret_cast<const void*>(k_exact_stream<8, NS, FB, KU>);
+    case 9: return reinterpret_cast<const void*>(k_exact_stream<9, NS, FB, KU>);
+    case 10: return reinterpret_cast<const void*>(k_exact_stream<10, NS, FB, KU>);
+    case 11: return reinterpret_cast<const void*>(k_exact_stream<11, NS, FB, KU>);
   }
   fail(SK_ERR_INVALID_ARGUMENT, "exact stream: field log2 must be 8..11");
 }
 
-const void* stream_kernel(int fl, int ns, int fb) {
-  if (fb == 8) switch (ns) {
-      case 1: return stream_kernel_ns<1, 8>(fl);
-      case 2: return stream_kernel_ns<2, 8>(fl);
-      case 3: return stream_kernel_ns<3, 8>(fl);
-    }
-  if (fb == 4) switch (ns) {
-      case 1: return stream_kernel_ns<1, 4>(fl);
-      case 2: return stream_kernel_ns<2, 4>(fl);
-      case 3: return stream_kernel_ns<3, 4>(fl);
-    }
-  fail(SK_ERR_INVALID_ARGUMENT, "exact stream: in-edge slots 1..3, fields of 4 or 8 bits");
+template <int NS, int FB>
+static const void* stream_kernel_ku(int fl, int ku) {
+  return ku == 6 ? stream_kernel_ns<NS, FB, 6>(fl) : stream_kernel_ns<NS, FB, 4>(fl);
+}
+
+const void* stream_kernel(int fl, int ns, int fb, int ku) {
+  if (ns < 1 || ns > 3 || (fb != 4 && fb != 8))
+    fail(SK_ERR_INVALID_ARGUMENT, "exact stream: in-edge slots 1..3, fields of 4 or 8 bits");
+  // in-degree <= 32 takes the two-slot kernel (its second slot stays empty)
+  if (ns <= 2) return fb == 8 ? stream_kernel_ku<2, 8>(fl, ku) : stream_kernel_ku<2, 4>(fl, ku);
+  return fb == 8 ? stream_kernel_ku<3, 8>(fl, ku) : stream_kernel_ku<3, 4>(fl, ku);
 }
 
 size_t padded_size(uint32_t rows, size_t nnz) { return 4 * size_t(rows) + (nnz & ~size_t(3)) + 8; }
@@ -545,9 +546,9 @@ void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint
   SK_LAUNCH(k_pad_passes, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
 }
 
-void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb,
+void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb, int ku,
                          unsigned grid, size_t smem) {
-  const void* kern = stream_kernel(fl, ns, fb);
+  const void* kern = stream_kernel(fl, ns, fb, ku);
   void* args[] = {const_cast<StreamArgs*>(&p)};
   SK_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(32 * kSW), args, smem, ctx->stream));
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -36,15 +36,16 @@ struct StreamArgs {
 // threads per block
 size_t stream_block_bytes(int fl, int fb);
 int stream_block_threads();
-// the kernel for 2^fl accumulator words (fl 8..11; 8..10 with 4-bit fields),
-// ns in-edge slots per lane (in-degree <= 32 ns) and fb-bit fields (8 or 4)
-const void* stream_kernel(int fl, int ns, int fb);
+// the kernel for 2^fl accumulator words (fl 8..11), ns in-edge slots per lane
+// (in-degree <= 32 ns), fb-bit fields (8 or 4) and ku 16-byte units per lane
+// and step (4 or 6)
+const void* stream_kernel(int fl, int ns, int fb, int ku);
 // The padded copy of an activation CSR's columns (rows 16-byte aligned, sentinel
 // gaps; padded_size words) and its pass table (rows * nP + 1 words).
 size_t padded_size(uint32_t rows, size_t nnz);
 void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
                        uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc);
-void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb,
+void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb, int ku,
                          unsigned grid, size_t smem);
 
 }  // namespace sk

@@ -2399,10 +2399,16 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     unsigned long long cap = clamp_cap(std::max<unsigned long long>(4ull * y0->nnz, 1ull << 24),
                                        (unsigned long long)(ctx->total_mem * 0.3 / 24.0));
     const uint64_t sitems = uint64_t(m) * gs.nW;  // one output item per (row, pass)
+    // units per lane and step: 6 when a pass has <= ~700 16-byte units (cfg4 /
+    // cfg5: 0.65 / 1.27 ms against 0.67 / 1.45 with 4), else 4 (cfg3's ~1000:
+    // 0.64 ms against 0.70)
+    const double units = deg0 * (erow0 * double(1u << sp_lg) / double(std::max<uint32_t>(1, n)) /
+                                 4.0 + 1.2);
+    const int ku = units <= 700.0 ? 6 : 4;
     for (int attempt = 0; attempt < 2; ++attempt) {
       const int fl = sp_lg - (fb == 4 ? 3 : 2);
       const size_t smem = stream_block_bytes(fl, fb);
-      const void* kern = stream_kernel(fl, ns, fb);
+      const void* kern = stream_kernel(fl, ns, fb, ku);
       kernel_smem_attr(ctx, kern, int(smem));
       const int per_sm = kernel_occupancy(ctx, kern, stream_block_threads(), smem);
       const unsigned grid = unsigned(ctx->num_sms * std::max(1, per_sm));
@@ -2448,7 +2454,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       ctx->last_exact.window_log2 = g.sh;
       ctx->last_exact.fields = 32 / fb;
       timing_mark(ctx, SK_KT_STREAM);
-      launch_exact_stream(ctx, sa, fl, ns, fb, grid, smem);
+      launch_exact_stream(ctx, sa, fl, ns, fb, ku, grid, smem);
       timing_mark(ctx);
       SK_CUDA(cudaMemsetAsync(item_cnt + sitems, 0, 4, ctx->stream));
       exclusive_scan_u32(ctx, item_cnt, wp_out, sitems + 1);

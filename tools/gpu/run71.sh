@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests/ -q -m gpu -x > gpurun_out/tests71.log 2>&1
+echo "tests rc=$?" >> gpurun_out/tests71.log
+for w in cfg4 cfg3 cfg5; do python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --no-sustained > gpurun_out/b71_$w.json 2>&1; done

@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_gemm_packed", "k_pack_split", "k_exact_layer", "k_spmm_tile", "k_dense_cluster",
+KERNELS = ["k_gemm_packed", "k_pack_split", "k_exact_stream", "k_pad_passes", "k_exact_layer", "k_spmm_tile", "k_dense_cluster",
            "k_dense_engine", "k_spmm_rows", "k_push_layer", "k_sparse_engine"]
 # mnemonics worth calling out (B200_PROFILING.md): tcgen05 / TMA / TMEM / atomics
 MARK = ("UTCHMMA", "UTCQMMA", "UTCBAR", "UBLKCP", "UTMALDG", "LDTM", "STTM", "ATOMS", "REDUX",
