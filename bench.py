@@ -606,17 +606,24 @@ def run_ours(args, w):
 
     # ---- e2e: host buffers in, result read back, through the public API ---------------
     if w["y0"] == "binary":
-        # Y0 is binary: only its pattern crosses the host link (sk_csr_from_pattern)
+        # Y0 is binary: only its pattern crosses the host link (sk_csr_from_pattern);
+        # with <= 65536 samples its column indices travel as 16-bit words
+        # (sk_csr_from_pattern16_async: half the bytes, widened on the device)
         assert np.all(host_v == 1.0), "pattern upload needs a binary Y0"
-        for a in (host_rp, host_ci):
-            sk._lib.load().sk_host_register(a.ctypes.data, a.nbytes)
-        h2d = host_rp.nbytes + host_ci.nbytes
-        copy_stream = torch.cuda.Stream(device=local)
         ncols = Y0.cols()
+        narrow = ncols <= 65536
+        up_ci = host_ci.astype(np.uint16) if narrow else host_ci
+        for a in (host_rp, up_ci):
+            sk._lib.load().sk_host_register(a.ctypes.data, a.nbytes)
+        h2d = host_rp.nbytes + up_ci.nbytes
+        copy_stream = torch.cuda.Stream(device=local)
 
         def upload():
             # on a copy stream: overlaps the forward already queued on the compute stream
-            return sk.CsrMatrix.from_pattern_async(m, ncols, host_rp, host_ci, 1.0,
+            if narrow:
+                return sk.CsrMatrix.from_pattern16_async(m, ncols, host_rp, up_ci, 1.0,
+                                                         stream=copy_stream.cuda_stream)
+            return sk.CsrMatrix.from_pattern_async(m, ncols, host_rp, up_ci, 1.0,
                                                    stream=copy_stream.cuda_stream)
 
         pending, left = [], [0]  # left: steps still to run after this one
@@ -776,9 +783,10 @@ def run_ours(args, w):
                     "d2h_bytes_per_step": int(d2h[0]), "ms_per_step": e2e_step_ms,
                     "h2d_ms_per_step_alone": h2d_ms,
                     "input_upload": ("double-buffered: step s+1's pattern upload (copy stream, "
-                                     "sk_csr_from_pattern_async) overlaps step s's forward; "
-                                     "every step's upload and result read inside the timed "
-                                     "region" if w["y0"] == "binary" else
+                                     "sk_csr_from_pattern16_async: row_ptr + 16-bit column "
+                                     "indices, widened on the device) overlaps step s's "
+                                     "forward; every step's upload and result read inside "
+                                     "the timed region" if w["y0"] == "binary" else
                                      "synchronous per step (sk_relu_forward_host)")},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),

@@ -33,6 +33,7 @@ EXPORTS = [
     "sk_dense_download_async", "sk_dense_shape", "sk_dense_device_ptr",
     "sk_dense_identity", "sk_dense_free",
     "sk_csr_from_triples", "sk_csr_from_parts", "sk_csr_from_pattern", "sk_csr_from_pattern_async",
+    "sk_csr_from_pattern16_async",
     "sk_csr_shape",
     "sk_csr_extract",
     "sk_csr_free", "sk_to_dense", "sk_from_dense", "sk_dense_nnz",
@@ -123,6 +124,8 @@ def load() -> C.CDLL:
                                       C.POINTER(vp)]
     L.sk_csr_from_pattern_async.argtypes = [vp, C.c_uint32, C.c_uint32, vp, vp, C.c_float, vp,
                                             C.POINTER(vp)]
+    L.sk_csr_from_pattern16_async.argtypes = [vp, C.c_uint32, C.c_uint32, vp, vp, C.c_float, vp,
+                                              C.POINTER(vp)]
     L.sk_csr_shape.argtypes = [vp, u32p, u32p, C.POINTER(C.c_size_t)]
     L.sk_csr_extract.argtypes = [vp, vp, vp, vp, vp]
     L.sk_to_dense.argtypes = [vp, vp, C.c_float, C.POINTER(vp)]

@@ -380,6 +380,63 @@ extern "C" sk_status sk_csr_from_pattern_async(sk_ctx* ctx, uint32_t rows, uint3
   });
 }
 
+namespace sk {
+// 16-bit column indices widened to the handle's 32-bit array (8 per thread-step)
+__global__ void k_widen_u16(const uint16_t* __restrict__ in, size_t n, uint32_t* __restrict__ out) {
+  const size_t n8 = n / 8;
+  const size_t tid = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const size_t nth = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = tid; i < n8; i += nth) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(in) + i);
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    uint4* o = reinterpret_cast<uint4*>(out) + 2 * i;
+    o[0] = make_uint4(w[0] & 0xFFFFu, w[0] >> 16, w[1] & 0xFFFFu, w[1] >> 16);
+    o[1] = make_uint4(w[2] & 0xFFFFu, w[2] >> 16, w[3] & 0xFFFFu, w[3] >> 16);
+  }
+  for (size_t i = n8 * 8 + tid; i < n; i += nth) out[i] = in[i];
+}
+}  // namespace sk
+
+extern "C" sk_status sk_csr_from_pattern16_async(sk_ctx* ctx, uint32_t rows, uint32_t cols,
+                                                 const uint32_t* rp, const uint16_t* ci,
+                                                 float value, void* stream, sk_csr** out) {
+  return guarded([&] {
+    if (!ctx) fail(SK_ERR_INVALID_ARGUMENT, "null context");
+    if (cols > 65536u)
+      fail(SK_ERR_INVALID_ARGUMENT, "16-bit column indices need cols <= 65536");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t nnz = rp[rows];
+    auto* a = new sk_csr;
+    a->ctx = ctx;
+    a->rows = rows;
+    a->cols = cols;
+    a->nnz = nnz;
+    void* p = nullptr;
+    SK_CUDA(cudaMallocAsync(&p, (size_t(rows) + 1) * 4, s));
+    a->rp = static_cast<uint32_t*>(p);
+    SK_CUDA(cudaMallocAsync(&p, (nnz + kCiPad) * 4, s));
+    a->ci = static_cast<uint32_t*>(p);
+    SK_CUDA(cudaMallocAsync(&p, std::max<size_t>(nnz, 1) * 4, s));
+    a->v = static_cast<float*>(p);
+    SK_CUDA(cudaMemcpyAsync(a->rp, rp, (size_t(rows) + 1) * 4, cudaMemcpyHostToDevice, s));
+    if (nnz) {
+      void* t = nullptr;  // the 16-bit staging copy (16-byte aligned: cudaMallocAsync)
+      SK_CUDA(cudaMallocAsync(&t, nnz * 2, s));
+      SK_CUDA(cudaMemcpyAsync(t, ci, nnz * 2, cudaMemcpyHostToDevice, s));
+      SK_LAUNCH(k_widen_u16, grid_for(ctx, (nnz + 7) / 8), 256, 0, s,
+                static_cast<const uint16_t*>(t), nnz, a->ci);
+      SK_CUDA(cudaFreeAsync(t, s));
+      SK_LAUNCH(k_fill_f32, grid_for(ctx, nnz), 256, 0, s, a->v, nnz, value);
+    }
+    a->stats = const_value_stats(value, nnz);
+    a->stats_valid = true;
+    SK_CUDA(cudaEventCreateWithFlags(&a->ready, cudaEventDisableTiming));
+    SK_CUDA(cudaEventRecord(a->ready, s));
+    *out = a;
+  });
+}
+
 extern "C" sk_status sk_csr_from_pattern(sk_ctx* ctx, uint32_t rows, uint32_t cols,
                                          const uint32_t* rp, const uint32_t* ci, float value,
                                          int validate, sk_csr** out) {

@@ -431,6 +431,23 @@ class CsrMatrix:
         m._host_refs = (rp, ci)
         return m
 
+    @staticmethod
+    def from_pattern16_async(rows, cols, row_ptr, col_idx16, value: float = 1.0, *, stream: int,
+                             ctx=None) -> "CsrMatrix":
+        """from_pattern_async with 16-bit column indices (cols <= 65536): half the
+        bytes over the host link; widened on the device (sk_csr_from_pattern16_async)."""
+        c = _ctx(ctx)
+        rp = _u32(row_ptr)
+        ci = np.ascontiguousarray(col_idx16, dtype=np.uint16)
+        if rp.size != rows + 1:
+            raise InvalidArgument("row_ptr length must be rows+1")
+        h = vp()
+        _check(c._L.sk_csr_from_pattern16_async(c.h, rows, cols, rp.ctypes.data, ci.ctypes.data,
+                                                float(value), vp(stream), C.byref(h)))
+        m = CsrMatrix(rows, cols, ctx=c, _handle=h)
+        m._host_refs = (rp, ci)
+        return m
+
     def rows(self) -> int:
         return self._rows
 

@@ -1036,3 +1036,29 @@ def test_stream_kernel_regimes(sk, port, case):
         assert info["fields"] == 4, info  # 8-bit counters: four per word
     if bias == -0.1:
         assert want.nnz > 100000 and info["wraps"] > n0, info  # the 4-bit pass wrapped
+
+
+def test_pattern16_upload_matches_pattern(sk, port):
+    """sk_csr_from_pattern16_async (16-bit column indices widened on the device,
+    the bench's end-to-end upload) gives the same CSR as the 32-bit upload:
+    odd nnz (the widening kernel's tail), the largest column 65535, empty rows."""
+    import torch
+    m, n = 3000, 65536
+    Y = port.gen_input_binary(m, n, 7, 3)
+    rp = Y.row_ptr.copy()
+    ci = Y.col_idx.copy()
+    ci[rp[5]:rp[6]] = np.arange(65536 - (rp[6] - rp[5]), 65536, dtype=np.uint32)  # top columns
+    rp2 = np.concatenate([rp[:11], rp[11:] - (rp[11] - rp[10])]).astype(np.uint32)
+    ci2 = np.concatenate([ci[:rp[10]], ci[rp[11]:]]).astype(np.uint32)   # row 10 emptied
+    ci2 = ci2[:-1]                                                        # odd nnz
+    rp2[-1] -= 1
+    rp2 = np.minimum(rp2, rp2[-1])
+    s = torch.cuda.Stream()
+    a = sk.CsrMatrix.from_pattern16_async(m, n, rp2, ci2.astype(np.uint16), 1.0,
+                                          stream=s.cuda_stream)
+    b = sk.CsrMatrix.from_pattern(m, n, rp2, ci2, 1.0, validate=True)
+    for x, y in zip(a.extract(), b.extract()):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    with pytest.raises(Exception):
+        sk.CsrMatrix.from_pattern16_async(m, n + 1, rp2, ci2.astype(np.uint16), 1.0,
+                                          stream=s.cuda_stream)
