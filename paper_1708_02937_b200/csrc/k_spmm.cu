@@ -327,12 +327,22 @@ __global__ void __launch_bounds__(256, SK_SPMM_MINB) k_dense_engine(DenseEngineA
 #ifndef SK_TILE_PRED
 #define SK_TILE_PRED 0
 #endif
+#ifndef SK_TILE_CB
+#define SK_TILE_CB 2
+#endif
+#ifndef SK_TILE_PR
+#define SK_TILE_PR 64
+#endif
+#ifndef SK_TILE_KC
+#define SK_TILE_KC 32
+#endif
 namespace tile {
-constexpr int kPR = 64;                // rows per packed tile
-constexpr int kTC = 256;               // columns per CTA (lane: 2 x float4)
-constexpr int kKC = 32;                // k per chunk
+constexpr int kPR = SK_TILE_PR;        // rows per packed tile
+constexpr int kCB = SK_TILE_CB;        // 256-column blocks per CTA (one 2-D TMA box each)
+constexpr int kTC = 256 * kCB;         // columns per CTA (lane: 2 kCB x float4)
+constexpr int kKC = SK_TILE_KC;        // k per chunk
 constexpr int kStages = 2;
-constexpr uint32_t kYBytes = uint32_t(kKC) * kTC * 4;      // 32 KB
+constexpr uint32_t kYBytes = uint32_t(kKC) * kTC * 4;      // 32 KB per column block
 constexpr uint32_t kWBytes = uint32_t(kPR) * kKC * 4;      // 8 KB
 constexpr uint32_t kMBytes = uint32_t(kPR) * 4;            // 256 B
 constexpr uint32_t kStageBytes = kYBytes + kWBytes + kMBytes;
@@ -359,7 +369,8 @@ __global__ void k_tile_pack(const uint32_t* __restrict__ rp, const uint32_t* __r
 
 // kRW rows per warp, 64 / kRW warps per CTA (one packed tile per CTA)
 template <int kEpi, int kRW>
-__global__ void __launch_bounds__(tile::kPR / kRW * 32, 2)
+__global__ void __launch_bounds__(tile::kPR / kRW * 32,
+                                  tile::kCB * tile::kKC * tile::kStages <= 64 ? 2 : 1)
     k_spmm_tile(const __grid_constant__ CUtensorMap ymap, const float* __restrict__ wvals,
                 const uint32_t* __restrict__ wmask, const float* __restrict__ bias, uint32_t m,
                 uint32_t K, uint32_t n, float clip, float* __restrict__ out) {
@@ -385,18 +396,22 @@ __global__ void __launch_bounds__(tile::kPR / kRW * 32, 2)
     uint8_t* st = stage(s);
     async::mbar_expect_tx(mb, kYBytes + kWBytes + kMBytes);
     const size_t blk = size_t(rt) * nK + j;
-    async::tma_2d_g2s(async::smem_u32(st), &ymap, int(c0), int(j * kKC), mb);
+#pragma unroll
+    for (int h = 0; h < kCB; ++h)  // [kCB][kKC][256] in shared memory
+      async::tma_2d_g2s(async::smem_u32(st + h * (kYBytes / kCB)), &ymap, int(c0 + 256 * h),
+                        int(j * kKC), mb);
     async::bulk_g2s(async::smem_u32(st + kYBytes), wvals + blk * (kPR * kKC), kWBytes, mb);
     async::bulk_g2s(async::smem_u32(st + kYBytes + kWBytes), wmask + blk * kPR, kMBytes, mb);
   };
   if (threadIdx.x == 0)
     for (uint32_t j = 0; j < min(uint32_t(kStages), nK); ++j) issue(j);
 
-  float acc[kRW][8];
+  constexpr int kQ = 8 * kCB;  // columns per lane
+  float acc[kRW][kQ];
 #pragma unroll
   for (int r = 0; r < kRW; ++r)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[r][q] = 0.0f;
+    for (int q = 0; q < kQ; ++q) acc[r][q] = 0.0f;
   for (uint32_t j = 0; j < nK; ++j) {
     const uint32_t s = j % kStages;
     async::mbar_wait(async::smem_u32(mbar + s), (j / kStages) & 1u);
@@ -409,55 +424,47 @@ __global__ void __launch_bounds__(tile::kPR / kRW * 32, 2)
     for (int r = 0; r < kRW; ++r) mask[r] = Mc[r];  // warp-uniform (broadcast)
 #pragma unroll 4
     for (int kk = 0; kk < kKC; ++kk) {
-      const float4 y0 = *reinterpret_cast<const float4*>(Yc + kk * kTC + lane * 4);
-      const float4 y1 = *reinterpret_cast<const float4*>(Yc + kk * kTC + 128 + lane * 4);
+      float yv[kQ];
+#pragma unroll
+      for (int h = 0; h < kCB; ++h) {
+        const float* yr = Yc + h * (kKC * 256) + kk * 256;
+        const float4 a = *reinterpret_cast<const float4*>(yr + lane * 4);
+        const float4 b4 = *reinterpret_cast<const float4*>(yr + 128 + lane * 4);
+        yv[8 * h + 0] = a.x, yv[8 * h + 1] = a.y, yv[8 * h + 2] = a.z, yv[8 * h + 3] = a.w;
+        yv[8 * h + 4] = b4.x, yv[8 * h + 5] = b4.y, yv[8 * h + 6] = b4.z, yv[8 * h + 7] = b4.w;
+      }
 #pragma unroll
       for (int r = 0; r < kRW; ++r) {
-#if SK_TILE_PRED
-        // predicated (no branch): an absent weight leaves the accumulators as
-        // they are -- the fold still skips it, it is never multiplied as a zero
-        const bool pres = mask[r] & (1u << kk);
-        const float w = Wc[r * kKC + kk];
-        acc[r][0] = pres ? __fadd_rn(acc[r][0], __fmul_rn(w, y0.x)) : acc[r][0];
-        acc[r][1] = pres ? __fadd_rn(acc[r][1], __fmul_rn(w, y0.y)) : acc[r][1];
-        acc[r][2] = pres ? __fadd_rn(acc[r][2], __fmul_rn(w, y0.z)) : acc[r][2];
-        acc[r][3] = pres ? __fadd_rn(acc[r][3], __fmul_rn(w, y0.w)) : acc[r][3];
-        acc[r][4] = pres ? __fadd_rn(acc[r][4], __fmul_rn(w, y1.x)) : acc[r][4];
-        acc[r][5] = pres ? __fadd_rn(acc[r][5], __fmul_rn(w, y1.y)) : acc[r][5];
-        acc[r][6] = pres ? __fadd_rn(acc[r][6], __fmul_rn(w, y1.z)) : acc[r][6];
-        acc[r][7] = pres ? __fadd_rn(acc[r][7], __fmul_rn(w, y1.w)) : acc[r][7];
-#else
         if (mask[r] & (1u << kk)) {  // warp-uniform: the warp's lanes share the rows
           const float w = Wc[r * kKC + kk];
-          acc[r][0] = __fadd_rn(acc[r][0], __fmul_rn(w, y0.x));
-          acc[r][1] = __fadd_rn(acc[r][1], __fmul_rn(w, y0.y));
-          acc[r][2] = __fadd_rn(acc[r][2], __fmul_rn(w, y0.z));
-          acc[r][3] = __fadd_rn(acc[r][3], __fmul_rn(w, y0.w));
-          acc[r][4] = __fadd_rn(acc[r][4], __fmul_rn(w, y1.x));
-          acc[r][5] = __fadd_rn(acc[r][5], __fmul_rn(w, y1.y));
-          acc[r][6] = __fadd_rn(acc[r][6], __fmul_rn(w, y1.z));
-          acc[r][7] = __fadd_rn(acc[r][7], __fmul_rn(w, y1.w));
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) acc[r][q] = __fadd_rn(acc[r][q], __fmul_rn(w, yv[q]));
         }
-#endif
       }
     }
     __syncthreads();  // every warp is done with stage s
     if (threadIdx.x == 0 && j + kStages < nK) issue(j + kStages);
   }
-  // epilogue: bias + ReLU select (+ clip), two float4 stores per row
+  // epilogue: bias + ReLU select (+ clip), 2 kCB float4 stores per row
 #pragma unroll
   for (int r = 0; r < kRW; ++r) {
     const uint32_t i = rt * kPR + warp * kRW + r;
     if (i >= m) continue;
     const float b = kEpi == kEpiLayer ? bias[i] : 0.0f;
-    float z[8];
+    float z[kQ];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) z[q] = kEpi == kEpiLayer ? layer_epilogue(acc[r][q], b, clip) : acc[r][q];
+    for (int q = 0; q < kQ; ++q) z[q] = kEpi == kEpiLayer ? layer_epilogue(acc[r][q], b, clip) : acc[r][q];
     float* orow = out + size_t(i) * n + c0;
-    if (uint32_t(lane) * 4 < ncols)
-      *reinterpret_cast<float4*>(orow + lane * 4) = make_float4(z[0], z[1], z[2], z[3]);
-    if (128 + uint32_t(lane) * 4 < ncols)
-      *reinterpret_cast<float4*>(orow + 128 + lane * 4) = make_float4(z[4], z[5], z[6], z[7]);
+#pragma unroll
+    for (int h = 0; h < kCB; ++h) {
+      const uint32_t ca = 256 * h + uint32_t(lane) * 4, cb = ca + 128;
+      if (ca < ncols)
+        *reinterpret_cast<float4*>(orow + ca) =
+            make_float4(z[8 * h + 0], z[8 * h + 1], z[8 * h + 2], z[8 * h + 3]);
+      if (cb < ncols)
+        *reinterpret_cast<float4*>(orow + cb) =
+            make_float4(z[8 * h + 4], z[8 * h + 5], z[8 * h + 6], z[8 * h + 7]);
+    }
   }
 }
 
@@ -500,7 +507,7 @@ static void launch_tile(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const
   constexpr int kRW = SK_TILE_RW;
   ensure_tile_pack(ctx, w);
   CUtensorMap ymap;
-  if (!async::make_tmap_2d_f32(&ymap, y, w->cols, n, n, tile::kKC, tile::kTC))
+  if (!async::make_tmap_2d_f32(&ymap, y, w->cols, n, n, tile::kKC, 256))
     fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed for the activation tile map");
   dim3 grid(ceil_div(n, tile::kTC), ceil_div(w->rows, tile::kPR));
   const int threads = tile::kPR / kRW * 32;
