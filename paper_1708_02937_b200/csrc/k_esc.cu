@@ -108,128 +108,11 @@ __global__ void k_esc_row_ptr(const K* okey, uint32_t S, uint32_t rows, uint32_t
 }
 
 // ---- small layers: one block does everything in shared memory ------------------
-// (products <= kSmallCap: expand, stable block radix sort, run fold, compaction)
+// (products <= kSmallCap: expand, bitonic sort, run fold, compaction, CSR)
 constexpr int kSmallThreads = 1024, kSmallItems = 2;
 constexpr uint32_t kSmallCap = uint32_t(kSmallThreads) * kSmallItems;  // products
 constexpr uint32_t kSmallEntries = 512;                                 // input entries
 
-// row id of every input entry (warp per row; only the small path needs it)
-__global__ void k_esc_entry_rows(const uint32_t* yrp, uint32_t rows, uint32_t* erow) {
-  const int lane = threadIdx.x & 31;
-  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < rows;
-       k += (gridDim.x * blockDim.x) >> 5)
-    for (uint32_t e = yrp[k] + lane; e < yrp[k + 1]; e += 32) erow[e] = k;
-}
-
-template <typename K>
-__global__ void __launch_bounds__(kSmallThreads)
-    k_esc_small(const uint32_t* erow, const uint32_t* yci, const float* yv, uint32_t nnz,
-                uint32_t n, const uint32_t* trp, const uint32_t* tci, const float* tv,
-                const float* bias, float clip, int end_bit, K* okey, float* ov,
-                uint32_t* count) {
-  using Sort = cub::BlockRadixSort<K, kSmallThreads, kSmallItems, float>;
-  using Scan = cub::BlockScan<uint32_t, kSmallThreads>;
-  // the staging arrays share storage with the block primitives' temporaries
-  // (every hand-off is separated by a barrier)
-  __shared__ union {
-    typename Sort::TempStorage sort;
-    typename Scan::TempStorage scan;
-    struct {
-      K key[kSmallCap];
-      float val[kSmallCap];
-    } buf;
-  } tmp;
-  __shared__ uint32_t s_off[kSmallEntries + 1];  // entry -> first product
-  __shared__ uint32_t s_tb[kSmallEntries];       // entry -> its W^T row start
-  K* const skey = tmp.buf.key;
-  float* const sval = tmp.buf.val;
-  const uint32_t tid = threadIdx.x;
-  // 1. product offsets of the thread's entries (blocked)
-  uint32_t ed[kSmallItems], eo[kSmallItems];
-#pragma unroll
-  for (int u = 0; u < kSmallItems; ++u) {
-    const uint32_t e = tid * kSmallItems + u;
-    ed[u] = 0;
-    if (e < nnz) {
-      const uint32_t k = erow[e], tb = trp[k];
-      s_tb[e] = tb;
-      ed[u] = trp[k + 1] - tb;
-    }
-  }
-  uint32_t P;
-  Scan(tmp.scan).ExclusiveSum(ed, eo, P);
-#pragma unroll
-  for (int u = 0; u < kSmallItems; ++u) {
-    const uint32_t e = tid * kSmallItems + u;
-    if (e < nnz) s_off[e] = eo[u];
-  }
-  if (tid == 0) s_off[nnz] = P;
-  __syncthreads();
-  // 2. expand, a product per thread (entry found in the offsets); input order
-  //    (ascending k) is the product index order
-  for (uint32_t q = tid; q < P; q += kSmallThreads) {
-    uint32_t lo = 0, hi = nnz;  // last entry with s_off[e] <= q
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (s_off[mid] <= q) lo = mid;
-      else hi = mid;
-    }
-    const uint32_t t = s_tb[lo] + (q - s_off[lo]);
-    skey[q] = K(tci[t]) * K(n) + K(yci[lo]);
-    sval[q] = __fmul_rn(tv[t], yv[lo]);
-  }
-  __syncthreads();
-  // 3. stable sort; padding sorts after every product (largest key, last in order)
-  K keys[kSmallItems];
-  float vals[kSmallItems];
-#pragma unroll
-  for (int u = 0; u < kSmallItems; ++u) {
-    const uint32_t q = tid * kSmallItems + u;
-    keys[u] = q < P ? skey[q] : ~K(0);
-    vals[u] = q < P ? sval[q] : 0.0f;
-  }
-  __syncthreads();
-  Sort(tmp.sort).Sort(keys, vals, 0, end_bit);
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kSmallItems; ++u) {
-    skey[tid * kSmallItems + u] = keys[u];
-    sval[tid * kSmallItems + u] = vals[u];
-  }
-  __syncthreads();
-  // 4. run heads fold ascending k, epilogue, 5. compaction in key order
-  uint32_t keep[kSmallItems], pos[kSmallItems];
-  float z[kSmallItems];
-#pragma unroll
-  for (int u = 0; u < kSmallItems; ++u) {
-    const uint32_t q = tid * kSmallItems + u;
-    keep[u] = 0;
-    z[u] = 0.0f;
-    keys[u] = skey[q];
-    if (q < P && (q == 0 || skey[q - 1] != skey[q])) {
-      float acc = 0.0f;
-      for (uint32_t r = q; r < P && skey[r] == skey[q]; ++r) acc = __fadd_rn(acc, sval[r]);
-      z[u] = layer_epilogue(acc, bias[uint32_t(skey[q] / K(n))], clip);
-      keep[u] = z[u] != 0.0f ? 1u : 0u;
-    }
-  }
-  uint32_t S;
-  __syncthreads();
-  Scan(tmp.scan).ExclusiveSum(keep, pos, S);
-#pragma unroll
-  for (int u = 0; u < kSmallItems; ++u)
-    if (keep[u]) {
-      okey[pos[u]] = keys[u];
-      ov[pos[u]] = z[u];
-    }
-  if (tid == 0) *count = S;
-}
-
-template <typename K>
-__global__ void k_esc_cols(const K* okey, uint32_t S, uint32_t n, uint32_t* oci) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < S; t += gridDim.x * blockDim.x)
-    oci[t] = uint32_t(okey[t] % K(n));
-}
 
 unsigned grid_of(sk_ctx* ctx, uint64_t threads) {
   return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((threads + 255) / 256,
@@ -242,29 +125,225 @@ int bits_for(uint64_t v) {  // smallest b with v <= 2^b
   return b;
 }
 
-template <typename K>
-sk_csr* esc_small(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip) {
+// The whole tiny layer in one CTA (<= kSmallEntries inputs, <= kSmallCap
+// products): input rows by binary search, products expanded, a bitonic sort of
+// (i n + j) << 11 | product index in shared memory (the product index breaks
+// ties, so a run lists its products in input order = ascending k), run folds
+// + epilogue, compaction, and the output CSR written directly (column, value
+// and all m + 1 row pointers, each by a binary search of the survivors' rows);
+// the host reads back only the count.  Replaces a row-id kernel, a block radix
+// sort over every key bit and three finishing launches (cfg4 layer 2, 24
+// inputs: ~30 -> ~6 us).
+__global__ void __launch_bounds__(kSmallThreads)
+    k_esc_tiny(const uint32_t* __restrict__ yrp, uint32_t rows, const uint32_t* __restrict__ yci,
+               const float* __restrict__ yv, uint32_t nnz, uint32_t n,
+               const uint32_t* __restrict__ trp, const uint32_t* __restrict__ tci,
+               const float* __restrict__ tv, uint32_t m, const float* __restrict__ bias,
+               float clip, uint32_t* __restrict__ orp, uint32_t* __restrict__ oci,
+               float* __restrict__ ov, uint32_t* __restrict__ count) {
+  __shared__ unsigned long long skey[kSmallCap];
+  __shared__ float sval[kSmallCap];
+  __shared__ uint32_t s_off[kSmallEntries + 1];
+  __shared__ uint32_t s_tb[kSmallEntries];
+  __shared__ uint32_t s_row[kSmallCap];  // input entries' rows, later the survivors' rows
+  __shared__ uint32_t s_wsum[kSmallThreads / 32];
+  constexpr uint32_t kIdx = 2049;
+  __shared__ uint32_t s_idx[kIdx];        // row pointers of every 2^lst-th row
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // block-wide exclusive sum of one value per thread
+  auto block_excl = [&](uint32_t v, uint32_t& total) {
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= uint32_t(o)) x += t;
+    }
+    if (lane == 31) s_wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t w = s_wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= uint32_t(o)) w += t;
+      }
+      s_wsum[lane] = w;
+    }
+    __syncthreads();
+    total = s_wsum[31];
+    const uint32_t ex = x - v + (wid ? s_wsum[wid - 1] : 0u);
+    __syncthreads();
+    return ex;
+  };
+  // 1. each input entry's row: the row pointers sampled every `st` rows into
+  //    shared memory (one coalesced load per thread), then per entry a binary
+  //    search there and one of <= log2(st) global steps inside its block -- not
+  //    ~17 dependent L2 round trips, and not a walk over every row
+  constexpr uint32_t kRB = 64;  // rows per thread and round (step 6)
+  uint32_t lst = 6;
+  while ((uint32_t(kIdx - 1) << lst) < rows) ++lst;
+  const uint32_t nb = (rows + (1u << lst) - 1) >> lst;  // blocks (<= kIdx - 1)
+  for (uint32_t b = tid; b <= nb; b += kSmallThreads) s_idx[b] = yrp[min(b << lst, rows)];
+  __syncthreads();
+  if (tid < nnz) {
+    uint32_t lo = 0, hi = nb;  // last block with s_idx[b] <= tid
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_idx[mid] <= tid) lo = mid; else hi = mid;
+    }
+    uint32_t rlo = lo << lst, rhi = min(rows, (lo + 1) << lst);  // last row with yrp <= tid
+    while (rhi - rlo > 1) {
+      const uint32_t mid = (rlo + rhi) >> 1;
+      if (yrp[mid] <= tid) rlo = mid; else rhi = mid;
+    }
+    s_row[tid] = rlo;
+  }
+  __syncthreads();
+  uint32_t deg = 0;
+  if (tid < nnz) {
+    const uint32_t k = s_row[tid];
+    const uint32_t tb = trp[k];
+    s_tb[tid] = tb;
+    deg = trp[k + 1] - tb;
+  }
+  uint32_t P;
+  const uint32_t eo = block_excl(deg, P);
+  if (tid < nnz) s_off[tid] = eo;
+  if (tid == 0) s_off[nnz] = P;
+  __syncthreads();
+  uint32_t P2 = 1;
+  while (P2 < P) P2 <<= 1;
+  // 2. expand: product q of entry e = (W^T row entry, input entry)
+  for (uint32_t q = tid; q < P2; q += kSmallThreads) {
+    if (q < P) {
+      uint32_t lo = 0, hi = nnz;  // last entry with s_off[e] <= q
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_off[mid] <= q) lo = mid; else hi = mid;
+      }
+      const uint32_t t = s_tb[lo] + (q - s_off[lo]);
+      skey[q] = ((unsigned long long)tci[t] * n + yci[lo]) << 11 | q;
+      sval[q] = __fmul_rn(tv[t], yv[lo]);
+    } else {
+      skey[q] = ~0ull;  // padding sorts last
+    }
+  }
+  __syncthreads();
+  // 3. bitonic sort of the P2 keys, two per thread (indices tid, tid + 1024) in
+  //    registers: partners closer than 32 are in the same warp (shuffles, no
+  //    barrier); the farther ones go through shared memory, one barrier each
+  {
+    unsigned long long v[2];
+    v[0] = skey[tid];
+    v[1] = tid + kSmallThreads < P2 ? skey[tid + kSmallThreads] : ~0ull;
+    const bool two = P2 > kSmallThreads;
+    for (uint32_t k = 2; k <= P2; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        if (j >= 32) {
+          __syncthreads();  // the previous round's reads are done
+          skey[tid] = v[0];
+          if (two) skey[tid + kSmallThreads] = v[1];
+          __syncthreads();
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !two) break;
+          const uint32_t i = tid + h * kSmallThreads;
+          unsigned long long o;
+          if (j >= 32) {
+            o = skey[i ^ j];
+          } else {
+            const uint32_t lo32 = __shfl_xor_sync(0xffffffffu, uint32_t(v[h]), j);
+            const uint32_t hi32 = __shfl_xor_sync(0xffffffffu, uint32_t(v[h] >> 32), j);
+            o = (unsigned long long)hi32 << 32 | lo32;
+          }
+          // the lower index of an ascending pair keeps the minimum
+          const bool lower = (i & j) == 0, up = (i & k) == 0;
+          const bool take_min = lower == up;
+          v[h] = take_min ? (o < v[h] ? o : v[h]) : (o > v[h] ? o : v[h]);
+        }
+      }
+    }
+    __syncthreads();
+    skey[tid] = v[0];
+    if (two) skey[tid + kSmallThreads] = v[1];
+    __syncthreads();
+  }
+  // 4. run heads fold their products in order, epilogue; 5. compaction
+  float z[kSmallItems];
+  uint32_t keep[kSmallItems];
+  uint32_t mine = 0;
+#pragma unroll
+  for (int u = 0; u < kSmallItems; ++u) {
+    const uint32_t q = tid * kSmallItems + u;
+    keep[u] = 0;
+    z[u] = 0.0f;
+    if (q < P) {
+      const unsigned long long key = skey[q] >> 11;
+      if (q == 0 || (skey[q - 1] >> 11) != key) {
+        float acc = 0.0f;
+        for (uint32_t r = q; r < P && (skey[r] >> 11) == key; ++r)
+          acc = __fadd_rn(acc, sval[uint32_t(skey[r] & 2047u)]);
+        z[u] = layer_epilogue(acc, bias[uint32_t(key / n)], clip);
+        keep[u] = z[u] != 0.0f ? 1u : 0u;
+      }
+    }
+    mine += keep[u];
+  }
+  uint32_t S;
+  uint32_t pos = block_excl(mine, S);
+#pragma unroll
+  for (int u = 0; u < kSmallItems; ++u)
+    if (keep[u]) {
+      const unsigned long long key = skey[tid * kSmallItems + u] >> 11;
+      const uint32_t i = uint32_t(key / n);
+      oci[pos] = uint32_t(key - (unsigned long long)i * n);
+      ov[pos] = z[u];
+      s_row[pos] = i;
+      ++pos;
+    }
+  __syncthreads();
+  // 6. row pointers: rp[r] = survivors in rows < r; thread t owns a block of
+  //    rows: two binary searches give its ends, a block with no survivor is a
+  //    constant fill, the others are walked
+  for (uint32_t r0 = tid * kRB; r0 <= m; r0 += kSmallThreads * kRB) {
+    const uint32_t r1 = min(m + 1, r0 + kRB);
+    auto lower = [&](uint32_t r) {
+      uint32_t lo = 0, hi = S;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_row[mid] < r) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    uint32_t lo = lower(r0);
+    const uint32_t hi = lower(r1);
+    if (lo == hi && (r0 & 3) == 0 && (r1 & 3) == 0) {
+      for (uint32_t r = r0; r < r1; r += 4)
+        *reinterpret_cast<uint4*>(orp + r) = make_uint4(lo, lo, lo, lo);
+      continue;
+    }
+    for (uint32_t r = r0; r < r1; ++r) {
+      while (lo < S && s_row[lo] < r) ++lo;
+      orp[r] = lo;
+    }
+  }
+  if (tid == 0) *count = S;
+}
+
+sk_csr* esc_tiny(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip,
+                 uint32_t maxdeg) {
   const uint32_t m = wt->cols, n = y->cols;
-  K* okey = aalloc<K>(ctx, kSmallCap);
-  float* ov = aalloc<float>(ctx, kSmallCap);
+  const size_t capn = std::max<size_t>(1, size_t(y->nnz) * maxdeg);  // <= kSmallCap
+  sk_csr* out = new_csr(ctx, m, n, capn);
   uint32_t* cnt = aalloc<uint32_t>(ctx, 1);
-  uint32_t* erow = aalloc<uint32_t>(ctx, y->nnz);
-  SK_LAUNCH(k_esc_entry_rows, grid_of(ctx, uint64_t(y->rows) * 32), 256, 0, ctx->stream, y->rp,
-            y->rows, erow);
-  SK_LAUNCH(k_esc_small<K>, 1, kSmallThreads, 0, ctx->stream, erow, y->ci, y->v,
-            uint32_t(y->nnz), n, wt->rp, wt->ci, wt->v, bias, clip, bits_for(uint64_t(m) * n),
-            okey, ov, cnt);
+  SK_LAUNCH(k_esc_tiny, 1, kSmallThreads, 0, ctx->stream, y->rp, y->rows, y->ci, y->v,
+            uint32_t(y->nnz), n, wt->rp, wt->ci, wt->v, m, bias, clip, out->rp, out->ci, out->v,
+            cnt);
   uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: an async copy
   SK_CUDA(cudaMemcpyAsync(hp, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
-  const uint32_t S = hp[0];
-  sk_csr* out = new_csr(ctx, m, n, S);
-  if (S) {
-    SK_CUDA(cudaMemcpyAsync(out->v, ov, size_t(S) * 4, cudaMemcpyDeviceToDevice, ctx->stream));
-    SK_LAUNCH(k_esc_cols<K>, grid_of(ctx, S), 256, 0, ctx->stream, okey, S, n, out->ci);
-  }
-  SK_LAUNCH(k_esc_row_ptr<K>, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, okey, S, m, n,
-            out->rp);
+  out->nnz = hp[0];  // the arrays keep their capacity
   return out;
 }
 
@@ -620,8 +699,9 @@ sk_csr* esc_sample(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* 
 template <typename K>
 sk_csr* esc_run(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip,
                 uint32_t maxdeg) {
-  if (y->nnz <= kSmallEntries && double(y->nnz) * double(maxdeg) <= double(kSmallCap))
-    return esc_small<K>(ctx, y, wt, bias, clip);
+  if (y->nnz <= kSmallEntries && double(y->nnz) * double(maxdeg) <= double(kSmallCap) &&
+      y->rows >= 1 && double(wt->cols) * double(y->cols) < 9.0e15)  // (i n + j) << 11 in 64 bits
+    return esc_tiny(ctx, y, wt, bias, clip, maxdeg);
   // sample-major (per-warp tables) when a sample holds few products on average;
   // a sample beyond the big table sends the layer to the global sort below
   const double per_sample = double(y->nnz) * double(wt->nnz) / double(std::max<uint32_t>(1, wt->rows)) /

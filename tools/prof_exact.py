@@ -18,7 +18,9 @@ def main():
     w = bench.WORKLOADS[name]
     W0 = sk.gen_layer_fixed(w["m"], w["kW"], sk.layer_seed(bench.SEED, 0), w["value"])
     Y0 = sk.gen_input_binary(w["m"], w["B"], bench.kY_of(w), bench.SEED)
-    model = sk.DnnModel([W0], [np.full(w["m"], w["bias"], np.float32)])
+    L = int(os.environ.get("PE_LAYERS", "1"))
+    Ws = [W0] + [sk.gen_layer_fixed(w["m"], w["kW"], sk.layer_seed(bench.SEED, k), w["value"]) for k in range(1, L)]
+    model = sk.DnnModel(Ws, [np.full(w["m"], w["bias"], np.float32)] * L)
     ctx.set_tuning(**tune)
     for _ in range(3):
         out, _ = sk.relu_forward_sparse(model, Y0, sk.ForwardOptions(clip=w["clip"]))
