@@ -21,7 +21,8 @@ def main():
     ctx.set_stream(s.cuda_stream)
     Ws = [sk.gen_layer_fixed(w["m"], w["kW"], sk.layer_seed(bench.SEED, k), w["value"])
           for k in range(3)]
-    Y0 = sk.gen_input_binary(w["m"], w["B"], bench.kY_of(w), bench.SEED)
+    B = int(os.environ.get("SB_BATCH", w["B"]))  # e.g. 7500: one GPU's share at N = 8
+    Y0 = sk.gen_input_binary(w["m"], B, bench.kY_of(w), bench.SEED)
     opt = sk.ForwardOptions(clip=w["clip"])
     b = np.full(w["m"], w["bias"], np.float32)
     res = {}
@@ -44,7 +45,7 @@ def main():
         kt, tags = ctx.kernel_times_tagged()
         ctx.set_timing(False)
         res[f"{L}_kernels"] = {t: round(float(x), 4) for x, t in zip(kt, tags)}
-    print(json.dumps({name: res}))
+    print(json.dumps({name: res, "batch": B}))
 
 
 if __name__ == "__main__":
