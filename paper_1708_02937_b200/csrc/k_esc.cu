@@ -139,8 +139,10 @@ __global__ void __launch_bounds__(kSmallThreads)
                const float* __restrict__ yv, uint32_t nnz, uint32_t n,
                const uint32_t* __restrict__ trp, const uint32_t* __restrict__ tci,
                const float* __restrict__ tv, uint32_t m, const float* __restrict__ bias,
-               float clip, uint32_t* __restrict__ orp, uint32_t* __restrict__ oci,
-               float* __restrict__ ov, uint32_t* __restrict__ count) {
+               float clip, uint32_t* __restrict__ oci,
+               float* __restrict__ ov, uint32_t* __restrict__ count,
+               const uint32_t* __restrict__ nnz_dev, uint32_t* __restrict__ handled,
+               uint32_t* __restrict__ orow) {
   __shared__ unsigned long long skey[kSmallCap];
   __shared__ float sval[kSmallCap];
   __shared__ uint32_t s_off[kSmallEntries + 1];
@@ -175,6 +177,15 @@ __global__ void __launch_bounds__(kSmallThreads)
     __syncthreads();
     return ex;
   };
+  // deferred launch (the input's entry count is only on the device): a layer
+  // beyond the tiny limits is left to the host (handled = 0, nothing written)
+  if (nnz_dev) {
+    nnz = *nnz_dev;
+    if (nnz > kSmallEntries) {
+      if (tid == 0) *handled = 0u, *count = 0u;
+      return;
+    }
+  }
   // 1. each input entry's row: the row pointers sampled every `st` rows into
   //    shared memory (one coalesced load per thread), then per entry a binary
   //    search there and one of <= log2(st) global steps inside its block -- not
@@ -208,6 +219,10 @@ __global__ void __launch_bounds__(kSmallThreads)
   }
   uint32_t P;
   const uint32_t eo = block_excl(deg, P);
+  if (handled && P > kSmallCap) {  // block-uniform
+    if (tid == 0) *handled = 0u, *count = 0u;
+    return;
+  }
   if (tid < nnz) s_off[tid] = eo;
   if (tid == 0) s_off[nnz] = P;
   __syncthreads();
@@ -303,32 +318,26 @@ __global__ void __launch_bounds__(kSmallThreads)
       ++pos;
     }
   __syncthreads();
-  // 6. row pointers: rp[r] = survivors in rows < r; thread t owns a block of
-  //    rows: two binary searches give its ends, a block with no survivor is a
-  //    constant fill, the others are walked
-  for (uint32_t r0 = tid * kRB; r0 <= m; r0 += kSmallThreads * kRB) {
-    const uint32_t r1 = min(m + 1, r0 + kRB);
-    auto lower = [&](uint32_t r) {
-      uint32_t lo = 0, hi = S;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_row[mid] < r) lo = mid + 1; else hi = mid;
-      }
-      return lo;
-    };
-    uint32_t lo = lower(r0);
-    const uint32_t hi = lower(r1);
-    if (lo == hi && (r0 & 3) == 0 && (r1 & 3) == 0) {
-      for (uint32_t r = r0; r < r1; r += 4)
-        *reinterpret_cast<uint4*>(orp + r) = make_uint4(lo, lo, lo, lo);
-      continue;
-    }
-    for (uint32_t r = r0; r < r1; ++r) {
-      while (lo < S && s_row[lo] < r) ++lo;
-      orp[r] = lo;
-    }
+  // 6. the survivors' rows (sorted) for the row-pointer kernel that follows
+  for (uint32_t t = tid; t < S; t += kSmallThreads) orow[t] = s_row[t];
+  if (tid == 0) {
+    *count = S;
+    if (handled) *handled = 1u;
   }
-  if (tid == 0) *count = S;
+}
+
+// rp[r] = survivors in rows < r (the survivors' rows sorted, count on the device)
+__global__ void k_esc_fill_rp(const uint32_t* __restrict__ orow, const uint32_t* __restrict__ count,
+                              uint32_t m, uint32_t* __restrict__ rp) {
+  const uint32_t S = *count;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= m; r += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = S;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(orow + mid) < r) lo = mid + 1; else hi = mid;
+    }
+    rp[r] = lo;
+  }
 }
 
 sk_csr* esc_tiny(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bias, float clip,
@@ -337,9 +346,12 @@ sk_csr* esc_tiny(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bi
   const size_t capn = std::max<size_t>(1, size_t(y->nnz) * maxdeg);  // <= kSmallCap
   sk_csr* out = new_csr(ctx, m, n, capn);
   uint32_t* cnt = aalloc<uint32_t>(ctx, 1);
+  uint32_t* orow = aalloc<uint32_t>(ctx, kSmallCap);
   SK_LAUNCH(k_esc_tiny, 1, kSmallThreads, 0, ctx->stream, y->rp, y->rows, y->ci, y->v,
-            uint32_t(y->nnz), n, wt->rp, wt->ci, wt->v, m, bias, clip, out->rp, out->ci, out->v,
-            cnt);
+            uint32_t(y->nnz), n, wt->rp, wt->ci, wt->v, m, bias, clip, out->ci, out->v,
+            cnt, nullptr, nullptr, orow);
+  SK_LAUNCH(k_esc_fill_rp, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, orow, cnt, m,
+            out->rp);
   uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: an async copy
   SK_CUDA(cudaMemcpyAsync(hp, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
   sync(ctx);
@@ -813,6 +825,32 @@ bool esc_applicable(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y
   auto* mm = const_cast<sk_model*>(md);
   model_layer_transpose(ctx, mm, k);
   return double(y->nnz) * double(mm->wT_maxdeg[k]) < double(1u << 31);
+}
+
+// Layer k on the tiny ESC kernel launched before the input's entry count is
+// known on the host (it is read from *d_nnz on the device): the output has the
+// kernel's full capacity; d_cnt[0] receives its entry count and d_cnt[1] 1 when
+// the kernel handled the layer (0: too many inputs or products -- nothing was
+// written, the host takes the layer its usual way).  Every bias of layer k <= 0.
+sk_csr* esc_tiny_deferred(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y,
+                          const uint32_t* d_nnz, float clip, uint32_t* d_cnt) {
+  auto* mm = const_cast<sk_model*>(md);
+  const sk_csr* wt = model_layer_transpose(ctx, mm, k);
+  const uint32_t m = wt->cols, n = y->cols;
+  sk_csr* out = new_csr(ctx, m, n, kSmallCap);
+  uint32_t* orow = aalloc<uint32_t>(ctx, kSmallCap);
+  SK_LAUNCH(k_esc_tiny, 1, kSmallThreads, 0, ctx->stream, y->rp, y->rows, y->ci, y->v, 0u, n,
+            wt->rp, wt->ci, wt->v, m, md->bias + size_t(k) * md->neurons, clip, out->ci,
+            out->v, d_cnt, d_nnz, d_cnt + 1, orow);
+  // (a layer the kernel left to the host has count 0 here: rp is rewritten then)
+  SK_LAUNCH(k_esc_fill_rp, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, orow, d_cnt, m,
+            out->rp);
+  return out;
+}
+
+bool esc_tiny_possible(const sk_model* md, uint32_t k, const sk_csr* y) {
+  return md->bias_nonpos[k] && y->rows >= 1 &&
+         double(md->neurons) * double(y->cols) < 9.0e15;  // (i n + j) << 11 in 64 bits
 }
 
 sk_csr* esc_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y, uint32_t k, float clip) {

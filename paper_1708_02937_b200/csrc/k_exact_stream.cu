@@ -471,30 +471,47 @@ __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __
     }
     const uint32_t pb = 4 * k + (rb & ~3u), pn = 4 * (k + 1) + (re & ~3u);
     uint32_t* const dst = pci + pb - rb;  // entry e of the row goes to dst[e]
+    // pass table from the copied entries themselves: lane j (and j + 32) counts
+    // the row's entries below j SP (<= 64 passes; more take a binary search per
+    // pass -- dependent loads, the slow way on rows as short as cfg5's)
+    uint32_t below0 = 0, below1 = 0;
+    const bool count = nP <= 64;
     for (uint32_t e0 = rb; e0 < re; e0 += 32 * kC) {
       uint32_t sv[kC];
 #pragma unroll
       for (int u = 0; u < kC; ++u) {
         const uint32_t e = e0 + 32 * u + lane;
-        sv[u] = e < re ? __ldg(ci + e) : 0u;
+        sv[u] = e < re ? __ldg(ci + e) : 0xFFFFFFFFu;
       }
 #pragma unroll
       for (int u = 0; u < kC; ++u) {
         const uint32_t e = e0 + 32 * u + lane;
         if (e < re) dst[e] = sv[u];
       }
-    }
-    // pass table: lane j finds the first entry of pass j by a binary search of the
-    // (sorted) row -- passes are few, the row is in L1/L2 from the copy
-    uint32_t* const out = wpc + size_t(k) * nP;
-    for (uint32_t j = lane; j < nP; j += 32) {
-      const uint32_t key = j << sh;
-      uint32_t lo = rb, hi = re;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(ci + mid) < key) lo = mid + 1; else hi = mid;
+      if (count) {
+        for (uint32_t j = 1; j < nP; ++j) {
+          uint32_t c = 0;
+#pragma unroll
+          for (int u = 0; u < kC; ++u) c += sv[u] < (j << sh) ? 1u : 0u;
+          c = __reduce_add_sync(0xffffffffu, c);
+          if (uint32_t(lane) == (j & 31)) (j < 32 ? below0 : below1) += c;
+        }
       }
-      out[j] = pb + (lo - rb);
+    }
+    uint32_t* const out = wpc + size_t(k) * nP;
+    if (count) {
+      if (uint32_t(lane) < nP) out[lane] = pb + below0;
+      if (uint32_t(lane) + 32 < nP) out[lane + 32] = pb + below1;
+    } else {
+      for (uint32_t j = lane; j < nP; j += 32) {
+        const uint32_t key = j << sh;
+        uint32_t lo = rb, hi = re;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (__ldg(ci + mid) < key) lo = mid + 1; else hi = mid;
+        }
+        out[j] = pb + (lo - rb);
+      }
     }
     // the gap up to the next row (and the slack after the last row)
     const uint32_t gend = k + 1 == rows ? pn + 8 : pn;

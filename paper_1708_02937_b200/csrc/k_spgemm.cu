@@ -1890,6 +1890,10 @@ struct ExactLayerIn {
   uint32_t stamp_layer;  // %globaltimer slot (ctx->stamps)
   const sk_csr* wT = nullptr;  // W^T (cached with a model) -- enables the push kernel
   StagedLayer* stage = nullptr;  // stop before the gather (the exchange publishes it)
+  // K7 only: no host round trip -- the output gets the scratch capacity, its
+  // entry count stays on the device (*defer_nnz), and the caller reads it with
+  // the overflow / wrap flags (ctx->d_u64 slots 1 and 3) after its own next step
+  const uint32_t** defer_nnz = nullptr;
 };
 
 // Weight statistics of a bare CSR (value statistics + row bounds), cached on the
@@ -2264,8 +2268,10 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
                              const ValueStats& ystats, uint32_t** wp_out_ptr);
 
 static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, uint32_t k0,
-                           float clip, const ValueStats& ystats, uint32_t** wp_out_ptr) {
+                           float clip, const ValueStats& ystats, uint32_t** wp_out_ptr,
+                           const uint32_t** defer_nnz = nullptr) {
   ExactLayerIn in;
+  in.defer_nnz = defer_nnz;
   in.w = md->w[k0];
   in.bias = md->bias + size_t(k0) * md->neurons;
   in.wstats = md->wstats_host[k0];
@@ -2458,6 +2464,18 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       timing_mark(ctx);
       SK_CUDA(cudaMemsetAsync(item_cnt + sitems, 0, 4, ctx->stream));
       exclusive_scan_u32(ctx, item_cnt, wp_out, sitems + 1);
+      if (L_.defer_nnz && !L_.stage) {
+        // no round trip: the output at the scratch capacity, gathered and
+        // row-pointed on the device (the gather reads the total itself)
+        sk_csr* o = new_csr(ctx, m, n, cap);
+        SK_LAUNCH(k_gather_items, grid_warps(ctx, sitems), 256, 0, ctx->stream, item_cnt,
+                  item_off, wp_out, sitems, sc_c, sc_v, o->ci, o->v, sa.overflow);
+        SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, gs.nW,
+                  o->rp);
+        *L_.defer_nnz = wp_out + sitems;
+        *wp_out_ptr = nullptr;
+        return o;
+      }
       uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
       SK_CUDA(cudaMemcpyAsync(hp, wp_out + sitems, 4, cudaMemcpyDeviceToHost, ctx->stream));
       SK_CUDA(cudaMemcpyAsync(hp + 1, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -2706,6 +2724,63 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
           const ValueStats ys = host_value_stats(ctx, cur);
           if (products_exact(md->wstats_host[k], ys)) {
             uint32_t* wp1 = nullptr;
+            // the exact layer and the tiny ESC of layer k + 1 behind it with ONE host
+            // round trip (the collapse of cfg3-5: layer 2's input is a few entries)
+            if (esc_env && k + 1 < L && esc_tiny_possible(md, k + 1, cur)) {
+              const uint32_t* d_nnz = nullptr;
+              model_layer_transpose(ctx, const_cast<sk_model*>(md), k + 1);  // cached
+              sk_csr* r = exact_layer(ctx, md, cur, k, clip, ys, &wp1, &d_nnz);
+              if (d_nnz) {
+                uint32_t* dc = aalloc<uint32_t>(ctx, 2);
+                sk_csr* r2 = esc_tiny_deferred(ctx, md, k + 1, r, d_nnz, clip, dc);
+                uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 16);  // pinned
+                const uint32_t* dflags = reinterpret_cast<const uint32_t*>(ctx->d_u64);
+                SK_CUDA(cudaMemcpyAsync(hp, d_nnz, 4, cudaMemcpyDeviceToHost, ctx->stream));
+                SK_CUDA(cudaMemcpyAsync(hp + 1, dflags + 2, 4, cudaMemcpyDeviceToHost,
+                                        ctx->stream));  // overflow (slot 1)
+                SK_CUDA(cudaMemcpyAsync(hp + 2, dflags + 6, 4, cudaMemcpyDeviceToHost,
+                                        ctx->stream));  // wrap (slot 3)
+                SK_CUDA(cudaMemcpyAsync(hp + 3, dc, 8, cudaMemcpyDeviceToHost, ctx->stream));
+                sync(ctx);
+                if (!hp[1] && !hp[2]) {
+                  r->nnz = hp[0];  // the arrays keep the scratch capacity
+                  if (owned) csr_release(owned);
+                  trace[k + 1] = hp[0];
+                  set_paths(k, 1, SK_PATH_EXACT);
+                  pending_wp = nullptr;
+                  if (hp[4]) {  // the tiny ESC took layer k + 1
+                    r2->nnz = hp[3];
+                    csr_release(r);
+                    owned = r2;
+                    cur = r2;
+                    trace[k + 2] = hp[3];
+                    set_paths(k + 1, 1, SK_PATH_ESC);
+                    k += 2;
+                  } else {
+                    csr_release(r2);
+                    owned = r;
+                    cur = r;
+                    k += 1;
+                  }
+                  if (k >= L) break;
+                  continue;
+                }
+                // an overflow or a wrapped 4-bit counter: the layer again, with its
+                // own round trips (it grows the scratch / takes 8-bit counters)
+                csr_release(r2);
+                csr_release(r);
+              } else {
+                if (owned) csr_release(owned);
+                owned = r;
+                cur = r;
+                trace[k + 1] = r->nnz;
+                set_paths(k, 1, SK_PATH_EXACT);
+                k += 1;
+                pending_wp = wp1;
+                if (k >= L) break;
+                continue;
+              }
+            }
             sk_csr* r = exact_layer(ctx, md, cur, k, clip, ys, &wp1);
             if (owned) csr_release(owned);
             owned = r;
