@@ -1062,3 +1062,48 @@ def test_pattern16_upload_matches_pattern(sk, port):
     with pytest.raises(Exception):
         sk.CsrMatrix.from_pattern16_async(m, n + 1, rp2, ci2.astype(np.uint16), 1.0,
                                           stream=s.cuda_stream)
+
+
+# (m, samples, active inputs per sample, bias, max in-degree, 4-bit wrap expected)
+CHAIN_CASES = [
+    (8192, 5000, 120, -0.45, 64, False),   # layer 1 leaves a few entries: the tiny ESC takes layer 2
+    (8192, 5000, 120, -0.2, 64, False),    # layer 1 leaves thousands: the tiny ESC declines
+    (16384, 3000, 3000, -0.1, 70, True),   # a 4-bit counter wraps: the synchronous fallback
+]
+
+
+@pytest.mark.parametrize("case", CHAIN_CASES)
+def test_exact_layer_chained_with_tiny_esc(sk, port, case):
+    """The exact layer and the tiny ESC of the next layer issued with one host
+    round trip (the layer-1 count stays on the device): both outcomes of the
+    tiny kernel (it takes the layer / declines and the host goes on its usual
+    way) and the fallback when a 4-bit counter wraps -- three layers against
+    the oracle's sparse layer, layer by layer."""
+    m, n, kY, bias, maxdeg, wraps = case
+    L = 3
+    hW = [_in_degree_weights(m, maxdeg, m + n + 7 * k) for k in range(L)]
+    hY = port.gen_input_binary(m, n, kY, 11)
+    b = np.full(m, bias, np.float32)
+    y, want_trace = hY, [hY.nnz]
+    for k in range(L):
+        y = port.layer_sparse(hW[k], b, y, 32.0)
+        want_trace.append(y.nnz)
+    ctx = sk.default_context()
+    old = ctx.set_tuning(exact_kernel=5, exact_group=2 if wraps else 0)
+    ctx.set_density_switch(0.0, 0.0)
+    try:
+        w0 = ctx.last_exact()["wraps"]
+        model = sk.DnnModel([dev_csr(sk, w) for w in hW], [b] * L)
+        out, trace = sk.relu_forward_sparse(model, dev_csr(sk, hY), sk.ForwardOptions(clip=32.0))
+        paths = ctx.layer_paths(L)
+        info = ctx.last_exact()
+    finally:
+        ctx.set_tuning(**old)
+        ctx.set_density_switch()
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, y)
+    assert paths[0] == "exact", paths
+    if want_trace[1] <= 512 and want_trace[1] * maxdeg <= 2048:
+        assert paths[1] == "esc", (paths, want_trace)
+    if wraps:
+        assert info["wraps"] > w0, info
