@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kSmallThreads)
                float clip, uint32_t* __restrict__ oci,
                float* __restrict__ ov, uint32_t* __restrict__ count,
                const uint32_t* __restrict__ nnz_dev, uint32_t* __restrict__ handled,
-               uint32_t* __restrict__ orow) {
+               uint32_t* __restrict__ orow, const uint32_t* __restrict__ erow_dev) {
   __shared__ unsigned long long skey[kSmallCap];
   __shared__ float sval[kSmallCap];
   __shared__ uint32_t s_off[kSmallEntries + 1];
@@ -186,28 +186,32 @@ __global__ void __launch_bounds__(kSmallThreads)
       return;
     }
   }
-  // 1. each input entry's row: the row pointers sampled every `st` rows into
-  //    shared memory (one coalesced load per thread), then per entry a binary
-  //    search there and one of <= log2(st) global steps inside its block -- not
-  //    ~17 dependent L2 round trips, and not a walk over every row
-  constexpr uint32_t kRB = 64;  // rows per thread and round (step 6)
-  uint32_t lst = 6;
-  while ((uint32_t(kIdx - 1) << lst) < rows) ++lst;
-  const uint32_t nb = (rows + (1u << lst) - 1) >> lst;  // blocks (<= kIdx - 1)
-  for (uint32_t b = tid; b <= nb; b += kSmallThreads) s_idx[b] = yrp[min(b << lst, rows)];
-  __syncthreads();
-  if (tid < nnz) {
-    uint32_t lo = 0, hi = nb;  // last block with s_idx[b] <= tid
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (s_idx[mid] <= tid) lo = mid; else hi = mid;
+  // 1. each input entry's row: given by the producer (erow_dev), or from the
+  //    row pointers sampled every 2^lst rows into shared memory (one coalesced
+  //    load per thread), then per entry a binary search there and one of
+  //    <= log2(2^lst) global steps inside its block -- not ~17 dependent L2 round
+  //    trips, and not a walk over every row
+  if (erow_dev) {
+    if (tid < nnz) s_row[tid] = erow_dev[tid];
+  } else {
+    uint32_t lst = 6;
+    while ((uint32_t(kIdx - 1) << lst) < rows) ++lst;
+    const uint32_t nb = (rows + (1u << lst) - 1) >> lst;  // blocks (<= kIdx - 1)
+    for (uint32_t b = tid; b <= nb; b += kSmallThreads) s_idx[b] = yrp[min(b << lst, rows)];
+    __syncthreads();
+    if (tid < nnz) {
+      uint32_t lo = 0, hi = nb;  // last block with s_idx[b] <= tid
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_idx[mid] <= tid) lo = mid; else hi = mid;
+      }
+      uint32_t rlo = lo << lst, rhi = min(rows, (lo + 1) << lst);  // last row with yrp <= tid
+      while (rhi - rlo > 1) {
+        const uint32_t mid = (rlo + rhi) >> 1;
+        if (yrp[mid] <= tid) rlo = mid; else rhi = mid;
+      }
+      s_row[tid] = rlo;
     }
-    uint32_t rlo = lo << lst, rhi = min(rows, (lo + 1) << lst);  // last row with yrp <= tid
-    while (rhi - rlo > 1) {
-      const uint32_t mid = (rlo + rhi) >> 1;
-      if (yrp[mid] <= tid) rlo = mid; else rhi = mid;
-    }
-    s_row[tid] = rlo;
   }
   __syncthreads();
   uint32_t deg = 0;
@@ -349,7 +353,7 @@ sk_csr* esc_tiny(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bi
   uint32_t* orow = aalloc<uint32_t>(ctx, kSmallCap);
   SK_LAUNCH(k_esc_tiny, 1, kSmallThreads, 0, ctx->stream, y->rp, y->rows, y->ci, y->v,
             uint32_t(y->nnz), n, wt->rp, wt->ci, wt->v, m, bias, clip, out->ci, out->v,
-            cnt, nullptr, nullptr, orow);
+            cnt, nullptr, nullptr, orow, nullptr);
   SK_LAUNCH(k_esc_fill_rp, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, orow, cnt, m,
             out->rp);
   uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: an async copy
@@ -833,7 +837,8 @@ bool esc_applicable(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y
 // the kernel handled the layer (0: too many inputs or products -- nothing was
 // written, the host takes the layer its usual way).  Every bias of layer k <= 0.
 sk_csr* esc_tiny_deferred(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y,
-                          const uint32_t* d_nnz, float clip, uint32_t* d_cnt) {
+                          const uint32_t* d_nnz, const uint32_t* d_erow, float clip,
+                          uint32_t* d_cnt) {
   auto* mm = const_cast<sk_model*>(md);
   const sk_csr* wt = model_layer_transpose(ctx, mm, k);
   const uint32_t m = wt->cols, n = y->cols;
@@ -841,7 +846,7 @@ sk_csr* esc_tiny_deferred(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_
   uint32_t* orow = aalloc<uint32_t>(ctx, kSmallCap);
   SK_LAUNCH(k_esc_tiny, 1, kSmallThreads, 0, ctx->stream, y->rp, y->rows, y->ci, y->v, 0u, n,
             wt->rp, wt->ci, wt->v, m, md->bias + size_t(k) * md->neurons, clip, out->ci,
-            out->v, d_cnt, d_nnz, d_cnt + 1, orow);
+            out->v, d_cnt, d_nnz, d_cnt + 1, orow, d_erow);
   // (a layer the kernel left to the host has count 0 here: rp is rewritten then)
   SK_LAUNCH(k_esc_fill_rp, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, orow, d_cnt, m,
             out->rp);

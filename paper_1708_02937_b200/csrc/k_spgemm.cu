@@ -1229,12 +1229,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_spgemm_rows(RowArgs p, uint32_t
   phase_a<Ops, kLayer, false>(p, ws, lane, gw, nw);
 }
 
+// erow (optional): the row of each of the first erow_cap output entries (items
+// per_row to a row), for the tiny ESC that follows without a host round trip
 __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
                                const unsigned long long* __restrict__ item_off,
                                const uint32_t* __restrict__ wp_out, uint64_t items,
                                const uint32_t* __restrict__ sc_c, const float* __restrict__ sc_v,
                                uint32_t* __restrict__ oc, float* __restrict__ ov,
-                               const int* overflow) {
+                               const int* overflow, uint32_t per_row = 1,
+                               uint32_t* __restrict__ erow = nullptr, uint32_t erow_cap = 0) {
   if (*overflow || wp_out[items] == 0) return;
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1251,6 +1254,7 @@ __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
       for (uint32_t t = lane; t < cl; t += 32) {
         oc[size_t(dst) + t] = sc_c[src + t];
         ov[size_t(dst) + t] = sc_v[src + t];
+        if (erow && dst + t < erow_cap) erow[dst + t] = uint32_t((it0 + l) / per_row);
       }
     }
   }
@@ -1894,6 +1898,7 @@ struct ExactLayerIn {
   // entry count stays on the device (*defer_nnz), and the caller reads it with
   // the overflow / wrap flags (ctx->d_u64 slots 1 and 3) after its own next step
   const uint32_t** defer_nnz = nullptr;
+  uint32_t* defer_erow = nullptr;  // with defer_nnz: rows of the first 512 output entries
 };
 
 // Weight statistics of a bare CSR (value statistics + row bounds), cached on the
@@ -2269,9 +2274,11 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
 
 static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, uint32_t k0,
                            float clip, const ValueStats& ystats, uint32_t** wp_out_ptr,
-                           const uint32_t** defer_nnz = nullptr) {
+                           const uint32_t** defer_nnz = nullptr,
+                           uint32_t* defer_erow = nullptr) {
   ExactLayerIn in;
   in.defer_nnz = defer_nnz;
+  in.defer_erow = defer_erow;
   in.w = md->w[k0];
   in.bias = md->bias + size_t(k0) * md->neurons;
   in.wstats = md->wstats_host[k0];
@@ -2469,7 +2476,8 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
         // row-pointed on the device (the gather reads the total itself)
         sk_csr* o = new_csr(ctx, m, n, cap);
         SK_LAUNCH(k_gather_items, grid_warps(ctx, sitems), 256, 0, ctx->stream, item_cnt,
-                  item_off, wp_out, sitems, sc_c, sc_v, o->ci, o->v, sa.overflow);
+                  item_off, wp_out, sitems, sc_c, sc_v, o->ci, o->v, sa.overflow, gs.nW,
+                  L_.defer_erow, L_.defer_erow ? 512u : 0u);
         SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, gs.nW,
                   o->rp);
         *L_.defer_nnz = wp_out + sitems;
@@ -2729,10 +2737,11 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
             if (esc_env && k + 1 < L && esc_tiny_possible(md, k + 1, cur)) {
               const uint32_t* d_nnz = nullptr;
               model_layer_transpose(ctx, const_cast<sk_model*>(md), k + 1);  // cached
-              sk_csr* r = exact_layer(ctx, md, cur, k, clip, ys, &wp1, &d_nnz);
+              uint32_t* erow = aalloc<uint32_t>(ctx, 512);
+              sk_csr* r = exact_layer(ctx, md, cur, k, clip, ys, &wp1, &d_nnz, erow);
               if (d_nnz) {
                 uint32_t* dc = aalloc<uint32_t>(ctx, 2);
-                sk_csr* r2 = esc_tiny_deferred(ctx, md, k + 1, r, d_nnz, clip, dc);
+                sk_csr* r2 = esc_tiny_deferred(ctx, md, k + 1, r, d_nnz, erow, clip, dc);
                 uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 16);  // pinned
                 const uint32_t* dflags = reinterpret_cast<const uint32_t*>(ctx->d_u64);
                 SK_CUDA(cudaMemcpyAsync(hp, d_nnz, 4, cudaMemcpyDeviceToHost, ctx->stream));

@@ -376,7 +376,8 @@ sk_csr* esc_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y, uint32_t k, 
 // count is read from *d_nnz; d_cnt[0] = output entries, d_cnt[1] = 1 if handled.
 bool esc_tiny_possible(const sk_model* md, uint32_t k, const sk_csr* y);
 sk_csr* esc_tiny_deferred(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y,
-                          const uint32_t* d_nnz, float clip, uint32_t* d_cnt);
+                          const uint32_t* d_nnz, const uint32_t* d_erow, float clip,
+                          uint32_t* d_cnt);
 void ensure_model_tables(sk_ctx* ctx, sk_model* md);
 void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const float* y0,
                           uint32_t n, float clip, float* buf0, float* buf1,
