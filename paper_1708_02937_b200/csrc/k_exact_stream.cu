@@ -449,40 +449,50 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
 // pass contains, low bits varied so their zero-increment atomics spread over
 // the banks).  wpc[k*nP + j] = pk + (first entry of row k with sample >= j SP)
 // - rp[k]; wpc[rows*nP] = p_rows.  Warp per row, the row's samples read once.
+// kC entries per lane and chunk (32 kC per warp): 8 for long rows, 2 for short
+// ones (cfg5's ~60 entries: a 256-entry chunk was ~360 instructions per row)
+template <int kC>
 __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                              uint32_t rows, uint32_t nP, int sh, uint32_t* __restrict__ pci,
                              uint32_t* __restrict__ wpc) {
-  constexpr int kC = 8;  // entries per lane in flight (256 per warp)
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  uint32_t rb = 0, re = 0;
-  if (gw < rows) {
-    rb = __ldg(rp + gw);
-    re = __ldg(rp + gw + 1);
-  }
-  for (uint32_t k = gw; k < rows; k += nw) {
-    // the next row's bounds are fetched while this one is copied
-    const uint32_t kn = k + nw;
-    uint32_t nb = 0, ne = 0;
-    if (kn < rows) {
-      nb = __ldg(rp + kn);
-      ne = __ldg(rp + kn + 1);
+  // software pipeline over the warp's rows: bounds two rows ahead, the first
+  // 256 entries one row ahead, so a short row (cfg5: ~60 entries) does not wait
+  // a full memory round trip per row
+  auto bounds = [&](uint32_t k, uint32_t& b, uint32_t& e) {
+    b = e = 0;
+    if (k < rows) {
+      b = __ldg(rp + k);
+      e = __ldg(rp + k + 1);
     }
+  };
+  auto chunk = [&](uint32_t e0, uint32_t re, uint32_t (&sv)[kC]) {
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+      const uint32_t e = e0 + 32 * u + lane;
+      sv[u] = e < re ? __ldg(ci + e) : 0xFFFFFFFFu;
+    }
+  };
+  uint32_t rb, re, nb, ne;
+  bounds(gw, rb, re);
+  bounds(gw + nw, nb, ne);
+  uint32_t sv[kC];
+  chunk(rb, re, sv);
+  const bool count = nP <= 64;
+  for (uint32_t k = gw; k < rows; k += nw) {
+    uint32_t nnb, nne, svn[kC];
+    bounds(k + 2 * nw, nnb, nne);
+    chunk(nb, ne, svn);
     const uint32_t pb = 4 * k + (rb & ~3u), pn = 4 * (k + 1) + (re & ~3u);
     uint32_t* const dst = pci + pb - rb;  // entry e of the row goes to dst[e]
     // pass table from the copied entries themselves: lane j (and j + 32) counts
     // the row's entries below j SP (<= 64 passes; more take a binary search per
     // pass -- dependent loads, the slow way on rows as short as cfg5's)
     uint32_t below0 = 0, below1 = 0;
-    const bool count = nP <= 64;
     for (uint32_t e0 = rb; e0 < re; e0 += 32 * kC) {
-      uint32_t sv[kC];
-#pragma unroll
-      for (int u = 0; u < kC; ++u) {
-        const uint32_t e = e0 + 32 * u + lane;
-        sv[u] = e < re ? __ldg(ci + e) : 0xFFFFFFFFu;
-      }
+      if (e0 != rb) chunk(e0, re, sv);
 #pragma unroll
       for (int u = 0; u < kC; ++u) {
         const uint32_t e = e0 + 32 * u + lane;
@@ -518,6 +528,10 @@ __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __
     for (uint32_t t = pb + (re - rb) + lane; t < gend; t += 32) pci[t] = 0xFFFFFFE0u | (t & 31u);
     rb = nb;
     re = ne;
+    nb = nnb;
+    ne = nne;
+#pragma unroll
+    for (int u = 0; u < kC; ++u) sv[u] = svn[u];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) wpc[size_t(rows) * nP] = 4 * rows + (rp[rows] & ~3u);
 }
@@ -555,12 +569,15 @@ const void* stream_kernel(int fl, int ns, int fb, int ku) {
 size_t padded_size(uint32_t rows, size_t nnz) { return 4 * size_t(rows) + (nnz & ~size_t(3)) + 8; }
 
 void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
-                       uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc) {
+                       uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc, bool short_rows) {
   // one resident wave (8 blocks of 8 warps per SM), each warp walking rows with
   // the next row's bounds prefetched
   const unsigned blocks = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>((uint64_t(rows) + 7) / 8, uint64_t(ctx->num_sms) * 8)));
-  SK_LAUNCH(k_pad_passes, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
+  if (short_rows)
+    SK_LAUNCH(k_pad_passes<2>, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
+  else
+    SK_LAUNCH(k_pad_passes<8>, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
 }
 
 void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb, int ku,

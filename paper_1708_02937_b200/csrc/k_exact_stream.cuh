@@ -43,8 +43,9 @@ const void* stream_kernel(int fl, int ns, int fb, int ku);
 // The padded copy of an activation CSR's columns (rows 16-byte aligned, sentinel
 // gaps; padded_size words) and its pass table (rows * nP + 1 words).
 size_t padded_size(uint32_t rows, size_t nnz);
+// short_rows: the mean row holds <= 96 entries (narrower chunks per warp)
 void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
-                       uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc);
+                       uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc, bool short_rows);
 void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb, int ku,
                          unsigned grid, size_t smem);
 

@@ -2400,7 +2400,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     // the padded copy of Y's columns and its pass table
     uint32_t* pci = aalloc<uint32_t>(ctx, padded_size(y0->rows, y0->nnz));
     uint32_t* wps = aalloc<uint32_t>(ctx, size_t(y0->rows) * gs.nW + 1);
-    launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps);
+    launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps, erow0 <= 96.0);
     const int ns = std::max(1, (L_.wstats.maxdeg + 31) / 32);  // in-edge slots per lane
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
     auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
