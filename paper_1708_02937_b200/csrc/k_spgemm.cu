@@ -1885,6 +1885,8 @@ struct StagedLayer {
   bool arena_open = false;
 };
 
+void host_prof_mark(int i);  // SK_HOST_PROF (sparse_forward_impl)
+
 struct ExactLayerIn {
   const sk_csr* w;
   const float* bias;  // device, w->rows
@@ -2400,6 +2402,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     // the padded copy of Y's columns and its pass table
     uint32_t* pci = aalloc<uint32_t>(ctx, padded_size(y0->rows, y0->nnz));
     uint32_t* wps = aalloc<uint32_t>(ctx, size_t(y0->rows) * gs.nW + 1);
+    host_prof_mark(1);
     launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps, erow0 <= 96.0);
     const int ns = std::max(1, (L_.wstats.maxdeg + 31) / 32);  // in-edge slots per lane
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
@@ -2678,8 +2681,47 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
 // nnz <= dense_above * m * n, dense engine (K1) above it, back to sparse below
 // sparse_below * m * n.  Non-finite weights, tiny batches or too little memory
 // for two dense buffers keep the whole pass on the sparse engine.
+// SK_HOST_PROF=1: host-side time split of the sparse forward (debug aid), printed
+// every 20 calls: entry -> first launch, -> the round trip's sync, sync wait, rest
+namespace {
+struct HostProf {
+  bool on = getenv("SK_HOST_PROF") != nullptr;
+  double acc[4] = {0, 0, 0, 0};
+  int calls = 0;
+  std::chrono::steady_clock::time_point t0, t1, t2, t3;
+};
+HostProf g_hprof;
+inline double us_between(std::chrono::steady_clock::time_point a,
+                         std::chrono::steady_clock::time_point b) {
+  return std::chrono::duration<double, std::micro>(b - a).count();
+}
+}  // namespace
+void host_prof_mark(int i) {
+  if (!g_hprof.on) return;
+  const auto now = std::chrono::steady_clock::now();
+  if (i == 1) g_hprof.t1 = now;
+  if (i == 2) g_hprof.t2 = now;
+  if (i == 3) g_hprof.t3 = now;
+}
+
 sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, float clip,
                             uint64_t* nnz_trace) {
+  if (g_hprof.on) g_hprof.t0 = g_hprof.t1 = g_hprof.t2 = g_hprof.t3 = std::chrono::steady_clock::now();
+  struct ProfEnd {
+    ~ProfEnd() {
+      if (!g_hprof.on) return;
+      const auto t4 = std::chrono::steady_clock::now();
+      g_hprof.acc[0] += us_between(g_hprof.t0, g_hprof.t1);
+      g_hprof.acc[1] += us_between(g_hprof.t1, g_hprof.t2);
+      g_hprof.acc[2] += us_between(g_hprof.t2, g_hprof.t3);
+      g_hprof.acc[3] += us_between(g_hprof.t3, t4);
+      if (++g_hprof.calls % 20 == 0) {
+        fprintf(stderr, "[host] entry->launch %.1f us, launches->sync %.1f, sync %.1f, rest %.1f\n",
+                g_hprof.acc[0] / 20, g_hprof.acc[1] / 20, g_hprof.acc[2] / 20, g_hprof.acc[3] / 20);
+        for (double& a : g_hprof.acc) a = 0;
+      }
+    }
+  } prof_end;
   const uint32_t m = md->neurons, n = y0->cols, L = md->layers;
   const uint64_t full = uint64_t(m) * n;
   auto* mm = const_cast<sk_model*>(md);
@@ -2750,7 +2792,9 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
                 SK_CUDA(cudaMemcpyAsync(hp + 2, dflags + 6, 4, cudaMemcpyDeviceToHost,
                                         ctx->stream));  // wrap (slot 3)
                 SK_CUDA(cudaMemcpyAsync(hp + 3, dc, 8, cudaMemcpyDeviceToHost, ctx->stream));
+                host_prof_mark(2);
                 sync(ctx);
+                host_prof_mark(3);
                 if (!hp[1] && !hp[2]) {
                   r->nnz = hp[0];  // the arrays keep the scratch capacity
                   if (owned) csr_release(owned);
