@@ -30,6 +30,7 @@ def run(ctx, model, Y0, opt, reps=5):
 GROUPS = [int(x) for x in os.environ.get("SC_GROUPS", "0,1,2,4,8,16").split(",")]
 RECS = [int(x) for x in os.environ.get("SC_RECS", "0").split(",")]
 FIELDS = [int(x) for x in os.environ.get("SC_FIELDS", "0,8").split(",")]
+KERNEL = int(os.environ.get("SC_KERNEL", "5"))
 
 
 def main():
@@ -49,7 +50,7 @@ def main():
             res = {"specialised": t_ref, "nnz": int(ref.nnz())}
             for grp in GROUPS:
                 for fb in FIELDS:
-                    ctx.set_tuning(exact_kernel=5, exact_group=grp, exact_fields=fb)
+                    ctx.set_tuning(exact_kernel=KERNEL, exact_group=grp, exact_fields=fb)
                     out, t, info = run(ctx, model, Y0, opt)
                     oo = out.extract()
                     same = all(np.array_equal(a.view(np.uint32), b.view(np.uint32))
