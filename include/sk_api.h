@@ -153,7 +153,12 @@ sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double spar
  *                  (<= 0: default 8)
  *   exact_fields   the stream kernel's counter width: 4 or 8 bits (0: 4 where
  *                  the threshold and increment allow it; a 4-bit counter that
- *                  wraps makes the layer rerun with 8-bit ones) */
+ *                  wraps makes the layer rerun with 8-bit ones)
+ *   exact_layout   the stream kernel's view of Y: 1 a padded copy (rows
+ *                  16-byte aligned); 2 its own column array where that is
+ *                  16-byte aligned (a pass table and two side units per row are
+ *                  built; else the copy); 0 = 2 for rows of > 96 entries on
+ *                  average, else 1 */
 typedef struct sk_tuning {
   int exact;
   int exact_kernel;
@@ -164,6 +169,7 @@ typedef struct sk_tuning {
   int esc;
   double esc_ratio;
   int exact_fields;
+  int exact_layout;
 } sk_tuning;
 sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t);
 sk_status sk_ctx_get_tuning(const sk_ctx* ctx, sk_tuning* t);
@@ -179,6 +185,7 @@ typedef struct sk_exact_info {
   int window_log2;
   int fields;
   int wraps;  /* stream kernel: launches rerun with 8-bit fields after a 4-bit one wrapped */
+  int layout; /* stream kernel: 0 Y read in place, 1 the padded copy */
 } sk_exact_info;
 sk_status sk_ctx_last_exact(const sk_ctx* ctx, sk_exact_info* info);
 /* Page-lock / unlock a caller host buffer for async copies. */

@@ -60,13 +60,13 @@ class Tuning(C.Structure):  # sk_tuning
     _fields_ = [("exact", C.c_int), ("exact_kernel", C.c_int), ("exact_group", C.c_int),
                 ("exact_records", C.c_int), ("window_log2", C.c_int),
                 ("exact_window_log2", C.c_int), ("esc", C.c_int), ("esc_ratio", C.c_double),
-                ("exact_fields", C.c_int)]
+                ("exact_fields", C.c_int), ("exact_layout", C.c_int)]
 
 
 class ExactInfo(C.Structure):  # sk_exact_info
     _fields_ = [("launches", C.c_uint64), ("kernel", C.c_int), ("group", C.c_int),
                 ("records", C.c_int), ("window_log2", C.c_int), ("fields", C.c_int),
-                ("wraps", C.c_int)]
+                ("wraps", C.c_int), ("layout", C.c_int)]
 
 
 _lib = None

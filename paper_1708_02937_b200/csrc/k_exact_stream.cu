@@ -47,15 +47,23 @@ namespace {
 
 constexpr int kSW = 1;  // warps per block (the accumulator base is then block-uniform)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+// pass-table values: entry position (bits 0-29) + two flags (stream_table_flags)
+constexpr uint32_t kPos = 0x3FFFFFFFu, kHeadF = 0x80000000u, kTailF = 0x40000000u;
 
+#ifndef SK_K7_RC6
+#define SK_K7_RC6 384
+#endif
 // accumulator (2^fl words of 32 / fb fields) + candidate bitmap (a bit per
-// sample of the pass) + 2 x unit records
+// sample of the pass) + 2 x unit records.  A batch of records is a whole number
+// of steps (32 ku units): a batch ending inside a step would leave the step's
+// other lanes idle.
 __host__ __device__ constexpr uint32_t pass_samples(int fl, int fb) { return (32u / fb) << fl; }
-__host__ __device__ constexpr uint32_t rec_cap(int fl, int fb) {
-  return pass_samples(fl, fb) <= 4096 ? 1024u : 512u;
+__host__ __device__ constexpr uint32_t rec_cap(int fl, int fb, int ku) {
+  return pass_samples(fl, fb) <= 4096 ? (ku == 6 ? 960u : 1024u)
+                                      : (ku == 6 ? uint32_t(SK_K7_RC6) : 512u);
 }
-__host__ __device__ constexpr size_t warp_bytes(int fl, int fb) {
-  return (size_t(4) << fl) + pass_samples(fl, fb) / 8 + size_t(8) * rec_cap(fl, fb);
+__host__ __device__ constexpr size_t warp_bytes(int fl, int fb, int ku) {
+  return (size_t(4) << fl) + pass_samples(fl, fb) / 8 + size_t(8) * rec_cap(fl, fb, ku);
 }
 
 __device__ __forceinline__ uint32_t incl_scan(uint32_t v, int lane) {
@@ -95,14 +103,14 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   constexpr uint32_t Wd = 1u << FL;                 // accumulator words
   constexpr uint32_t SP = pass_samples(FL, FB);     // samples per pass
   constexpr uint32_t NWP = SP >> 10;                // output windows per pass
-  constexpr uint32_t RC = rec_cap(FL, FB);
+  constexpr uint32_t RC = rec_cap(FL, FB, kU);
   constexpr int LB = FB == 8 ? 3 : 2;               // log2(FB)
   constexpr uint32_t TOP = FB == 8 ? 0x80808080u : 0x88888888u;  // field top bits
   constexpr uint32_t FMASK = (1u << FB) - 1u;
   constexpr uint32_t STEP = 32 * kU; // units per step
   const int lane = threadIdx.x & 31;
   uint32_t* const acc =
-      reinterpret_cast<uint32_t*>(smraw + (threadIdx.x >> 5) * warp_bytes(FL, FB));
+      reinterpret_cast<uint32_t*>(smraw + (threadIdx.x >> 5) * warp_bytes(FL, FB, kU));
   uint32_t* const cand = acc + Wd;          // SP bits
   uint32_t* const recs = cand + SP / 32;    // two buffers of RC unit records
   const uint32_t acc_s = async::smem_u32(acc);
@@ -117,18 +125,33 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   const uint4* const bq = reinterpret_cast<const uint4*>(p.bci);
 
   // A record per 16-byte unit of a pass's slices, laid end to end: the unit's
-  // index in the padded column array.  Lane c owns in-edges c, c + 32, ...
-  // (in-degree <= 32 NS, host-checked) and writes the records of their slices
-  // that fall into the batch [b0, b0 + RC) of the flattened units.
-  auto units = [](uint32_t b, uint32_t e) { return e > b ? ((e + 3) >> 2) - (b >> 2) : 0u; };
-  auto write_recs = [&](uint32_t* rec, const uint32_t (&bg)[NS], const uint32_t (&en)[NS],
-                        uint32_t pre, uint32_t b0) {
+  // index relative to bci (signed: the side units may lie below it).  Lane c
+  // owns in-edges c, c + 32, ... (in-degree <= 32 NS, host-checked) and writes
+  // the records of their slices that fall into the batch [b0, b0 + RC) of the
+  // flattened units.  A slice whose first (last) unit is its row's first (last)
+  // unit and holds another row's entries (the table value's head / tail flag)
+  // reads the row's side unit there instead: the same unit with every entry
+  // outside the row replaced by a sentinel (launch_pass_table).
+  auto units = [](uint32_t b, uint32_t e) {
+    b &= kPos;
+    e &= kPos;
+    return e > b ? ((e + 3) >> 2) - (b >> 2) : 0u;
+  };
+  const uint32_t side = p.side;
+  auto write_recs = [&](uint32_t* rec, const uint32_t (&kk)[NS], const uint32_t (&bg)[NS],
+                        const uint32_t (&en)[NS], uint32_t pre, uint32_t b0) {
 #pragma unroll
     for (int q2 = 0; q2 < NS; ++q2) {
       const uint32_t nu = units(bg[q2], en[q2]);
       const uint32_t lo = max(pre, b0), hi = min(pre + nu, b0 + RC);
-      uint32_t u = (bg[q2] >> 2) + (lo - pre);
+      uint32_t u = ((bg[q2] & kPos) >> 2) + (lo - pre);
       for (uint32_t t = lo; t < hi; ++t, ++u) rec[t - b0] = u;
+      if (nu) {
+        if ((bg[q2] & kHeadF) && pre >= b0 && pre < b0 + RC) rec[pre - b0] = side + 2 * kk[q2];
+        const uint32_t last = pre + nu - 1;
+        if ((en[q2] & kTailF) && last >= b0 && last < b0 + RC)
+          rec[last - b0] = side + 2 * kk[q2] + 1;
+      }
       pre += nu;
     }
   };
@@ -137,7 +160,7 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint32_t t = base + 32 * u + lane;
-      x[u] = t < n ? __ldg(bq + rec[t]) : make_uint4(0u, 0u, 0u, 0u);
+      x[u] = t < n ? __ldg(bq + int32_t(rec[t])) : make_uint4(0u, 0u, 0u, 0u);
     }
   };
   // Every entry of a loaded unit: its sample is inside this pass exactly when
@@ -228,7 +251,7 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
   first_bounds(k, c_beg, c_end, eA);
   uint32_t c_pass = 0, cb = 0, c_pre, c_T;
   geometry(c_beg, c_end, c_pre, c_T);
-  write_recs(recs, c_beg, c_end, c_pre, 0);
+  write_recs(recs, k, c_beg, c_end, c_pre, 0);
   __syncwarp();
   uint4 xc[kU];
   load(recs, 0, min(RC, c_T), xc);
@@ -280,7 +303,7 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
       uint32_t* const rec = recs + cb * RC;
       if (n_b0 != s_b0) {  // the unit's next batch of records (this step's units are loaded)
         __syncwarp();
-        write_recs(rec, c_beg, c_end, c_pre, n_b0);
+        write_recs(rec, k, c_beg, c_end, c_pre, n_b0);
         __syncwarp();
       }
       load(rec, n_base, min(RC, c_T - n_b0), xn);
@@ -311,7 +334,7 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
       }
       if (more) {
         geometry(x_beg, x_end, x_pre, x_T);
-        write_recs(recs + (cb ^ 1) * RC, x_beg, x_end, x_pre, 0);
+        write_recs(recs + (cb ^ 1) * RC, x_k, x_beg, x_end, x_pre, 0);
         __syncwarp();
         load(recs + (cb ^ 1) * RC, 0, min(RC, x_T), xn);
       }
@@ -409,7 +432,7 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
         // sentinels too -- is either touched or already clear)
 #pragma unroll 1
         for (uint32_t t = lane; t < c_T; t += 32) {
-          const uint4 x = __ldg(bq + rec[t]);
+          const uint4 x = __ldg(bq + int32_t(rec[t]));
           sts_u32(acc_s + ((x.x & (Wd - 1)) << 2), cw);
           sts_u32(acc_s + ((x.y & (Wd - 1)) << 2), cw);
           sts_u32(acc_s + ((x.z & (Wd - 1)) << 2), cw);
@@ -536,9 +559,150 @@ __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __
   if (blockIdx.x == 0 && threadIdx.x == 0) wpc[size_t(rows) * nP] = 4 * rows + (rp[rows] & ~3u);
 }
 
+// The padded copy for short rows (mean <= 96 entries, <= 64 passes): a warp
+// takes 32 consecutive rows (their row pointers in one coalesced load), then
+// kB rows at a time with all their first 64 entries loaded before any is
+// stored -- the per-row latency chain of a warp-per-row walk (cfg5's 262144
+// rows of ~60 entries: 100 us) becomes kB rows per memory round trip.  The pass
+// table from ballots over the loaded entries; longer rows continue in 32-entry
+// chunks.  Same output as k_pad_passes.
+__global__ void k_pad_rows(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                           uint32_t rows, uint32_t nP, int sh, uint32_t* __restrict__ pci,
+                           uint32_t* __restrict__ wpc) {
+  constexpr int kB = 4;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k0 = gw * 32; k0 < rows; k0 += nw * 32) {
+    const uint32_t nr = min(32u, rows - k0);
+    const uint32_t rpv = __ldg(rp + k0 + min(lane, nr));
+    const uint32_t rend = __ldg(rp + k0 + nr);
+    for (uint32_t r0 = 0; r0 < nr; r0 += kB) {
+      uint32_t rb[kB], re[kB], v[kB][2];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const uint32_t r = r0 + i;
+        rb[i] = __shfl_sync(0xffffffffu, rpv, r & 31);
+        const uint32_t nx = __shfl_sync(0xffffffffu, rpv, (r + 1) & 31);
+        re[i] = r + 1 < nr ? nx : rend;
+        if (r >= nr) re[i] = rb[i];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const uint32_t e = rb[i] + 32 * c + lane;
+          v[i][c] = e < re[i] ? __ldg(ci + e) : 0xFFFFFFFFu;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const uint32_t r = r0 + i;
+        if (r >= nr) break;
+        const uint32_t k = k0 + r, len = re[i] - rb[i];
+        const uint32_t pb = 4 * k + (rb[i] & ~3u);
+        uint32_t* const dst = pci + pb;
+        uint32_t mine0 = 0, mine1 = 0;  // entries below pass lane / lane + 32
+        auto count = [&](uint32_t x) {
+          for (uint32_t j = 1; j < nP; ++j) {
+            const uint32_t c = __popc(__ballot_sync(0xffffffffu, x < (j << sh)));
+            if (lane == (j & 31)) (j < 32 ? mine0 : mine1) += c;
+          }
+        };
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (32 * c + lane < len) dst[32 * c + lane] = v[i][c];
+          count(v[i][c]);
+        }
+        for (uint32_t e0 = 64; e0 < len; e0 += 32) {  // long rows: the rest in chunks
+          const uint32_t x = e0 + lane < len ? __ldg(ci + rb[i] + e0 + lane) : 0xFFFFFFFFu;
+          if (e0 + lane < len) dst[e0 + lane] = x;
+          count(x);
+        }
+        uint32_t* const out = wpc + size_t(k) * nP;
+        if (lane < nP) out[lane] = pb + mine0;
+        if (lane + 32 < nP) out[lane + 32] = pb + mine1;
+        // the gap up to the next row (1..7 words; the last row: 8 more)
+        const uint32_t gap = 4 - (re[i] & 3u) + (rb[i] & 3u) + (k + 1 == rows ? 8u : 0u);
+        if (lane < gap) {
+          const uint32_t t = pb + len + lane;
+          pci[t] = 0xFFFFFFE0u | (t & 31u);
+        }
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) wpc[size_t(rows) * nP] = 4 * rows + (rp[rows] & ~3u);
+}
+
+// The pass table of an activation CSR that K7 reads in place (Y's own column
+// array, 16-byte units), and each row's two side units.  Thread per row; the
+// row's pass boundaries by binary searches, up to kS of them interleaved (their
+// dependent loads overlap): no pass over the entries themselves (the padded
+// copy wrote every entry: 100 us on cfg5's 262144 short rows).
+//   wpc[k*nP + j] = (first entry of row k with sample >= j SP)
+//                   | kHeadF when a slice starting there has its first unit in
+//                     the row's first unit and the row starts inside a unit
+//                   | kTailF when a slice ending there has its last unit in the
+//                     row's last unit and the row ends inside a unit
+//   (j = 0: rb, both flags when rb is not a multiple of 4 -- the value also
+//   ends row k - 1's last slice); wpc[rows*nP] = nnz (+ kTailF).
+//   side[2k] / side[2k+1]: the row's first / last unit with every entry outside
+//   the row replaced by a sentinel (a sample no pass contains, low bits varied).
+__global__ void k_pass_table(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                             uint32_t rows, uint32_t nP, int sh, uint32_t* __restrict__ wpc,
+                             uint4* __restrict__ side) {
+  constexpr int kS = 8;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < rows; k += stride) {
+    const uint32_t rb = __ldg(rp + k), re = __ldg(rp + k + 1);
+    auto side_unit = [&](uint32_t u) {
+      uint32_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t e = 4 * u + j;
+        v[j] = e >= rb && e < re ? __ldg(ci + e) : 0xFFFFFFE0u | ((4 * k + j) & 31u);
+      }
+      return make_uint4(v[0], v[1], v[2], v[3]);
+    };
+    const uint4 h = side_unit(rb >> 2), t = side_unit(re > rb ? (re - 1) >> 2 : rb >> 2);
+    side[2 * size_t(k)] = h;
+    side[2 * size_t(k) + 1] = t;
+    const bool hmis = (rb & 3u) != 0, tmis = (re & 3u) != 0;
+    uint32_t* const out = wpc + size_t(k) * nP;
+    out[0] = rb | (hmis ? kHeadF | kTailF : 0u);
+    for (uint32_t j0 = 1; j0 < nP; j0 += kS) {
+      uint32_t lo[kS], hi[kS];
+#pragma unroll
+      for (int s = 0; s < kS; ++s) {
+        lo[s] = rb;
+        hi[s] = j0 + s < nP ? re : rb;
+      }
+      for (bool any = true; any;) {
+        any = false;
+#pragma unroll
+        for (int s = 0; s < kS; ++s)
+          if (lo[s] < hi[s]) {
+            const uint32_t mid = (lo[s] + hi[s]) >> 1;
+            if (__ldg(ci + mid) < ((j0 + s) << sh)) lo[s] = mid + 1; else hi[s] = mid;
+            any = true;
+          }
+      }
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        if (j0 + s < nP) {
+          const uint32_t v = lo[s];
+          const bool hf = hmis && (v >> 2) == (rb >> 2);
+          const bool tf = tmis && v > rb && ((v - 1) >> 2) == ((re - 1) >> 2);
+          out[j0 + s] = v | (hf ? kHeadF : 0u) | (tf ? kTailF : 0u);
+        }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t e = rp[rows];
+    wpc[size_t(rows) * nP] = e | ((e & 3u) ? kTailF : 0u);
+  }
+}
+
 }  // namespace
 
-size_t stream_block_bytes(int fl, int fb) { return size_t(kSW) * warp_bytes(fl, fb); }
+size_t stream_block_bytes(int fl, int fb, int ku) { return size_t(kSW) * warp_bytes(fl, fb, ku); }
 
 int stream_block_threads() { return 32 * kSW; }
 
@@ -574,10 +738,22 @@ void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint
   // the next row's bounds prefetched
   const unsigned blocks = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>((uint64_t(rows) + 7) / 8, uint64_t(ctx->num_sms) * 8)));
-  if (short_rows)
+  if (short_rows && nP <= 64) {
+    const unsigned rb = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t(rows) + 255) / 256, uint64_t(ctx->num_sms) * 8)));
+    SK_LAUNCH(k_pad_rows, rb, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
+  } else if (short_rows)
     SK_LAUNCH(k_pad_passes<2>, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
   else
     SK_LAUNCH(k_pad_passes<8>, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
+}
+
+void launch_pass_table(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
+                       uint32_t nP, int sh, uint32_t* wpc, void* side) {
+  const unsigned blocks = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((uint64_t(rows) + 255) / 256, uint64_t(ctx->num_sms) * 8)));
+  SK_LAUNCH(k_pass_table, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, wpc,
+            static_cast<uint4*>(side));
 }
 
 void launch_exact_stream(sk_ctx* ctx, const StreamArgs& p, int fl, int ns, int fb, int ku,

@@ -2366,9 +2366,11 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
   auto stream_pass = [&](int fl) {
     return deg0 * erow0 * double(4u << fl) / double(std::max<uint32_t>(1, n));
   };
-  const bool stream_ok = fast0 && probe.q_cval > 0 && n <= 0xFFFFF000u &&
+  // (samples <= 0xFFF00000: a sentinel is never inside a pass; table positions
+  // < 2^30: the top two bits carry flags)
+  const bool stream_ok = fast0 && probe.q_cval > 0 && n <= 0xFFF00000u &&
                          L_.wstats.maxdeg <= 96 &&
-                         padded_size(y0->rows, y0->nnz) < 0xFFFFFFF0ull;
+                         padded_size(y0->rows, y0->nnz) < (1ull << 30);
   const bool stream = stream_ok && (ctx->tune.exact_kernel == 5 || ctx->tune.exact_kernel == 0);
   if (stream) {
     // 4-bit fields: the smallest threshold t' (count units) <= 7 and an
@@ -2400,10 +2402,37 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     gs.S = 1u << sp_lg;
     gs.nW = std::max<uint32_t>(1, uint32_t((uint64_t(n) + gs.S - 1) >> gs.sh));
     // the padded copy of Y's columns and its pass table
-    uint32_t* pci = aalloc<uint32_t>(ctx, padded_size(y0->rows, y0->nnz));
+    // Y's own column array for rows of > 96 entries (a pass table + two side
+    // units per row; cfg4 / cfg3: the padded copy's 35 us saved, the kernel
+    // unchanged), when it is 16-byte aligned and the side units lie within
+    // signed 32-bit unit offsets of it; else the padded copy (short rows: their
+    // slices are a few units, and a side unit is one more line per slice --
+    // cfg5's kernel 1.28 -> 1.37 ms read in place).  sk_tuning.exact_layout
+    // 1 / 2 forces the padded copy / the in-place read.
     uint32_t* wps = aalloc<uint32_t>(ctx, size_t(y0->rows) * gs.nW + 1);
-    host_prof_mark(1);
-    launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps, erow0 <= 96.0);
+    const uint32_t* bci = y0->ci;
+    uint32_t side_off = 0;
+    const int lay = ctx->tune.exact_layout;
+    bool direct = (lay == 2 || (lay == 0 && erow0 > 96.0)) &&
+                  (reinterpret_cast<uintptr_t>(y0->ci) & 15u) == 0;
+    if (direct) {
+      void* side = aalloc<uint4>(ctx, 2 * size_t(std::max<uint32_t>(1, y0->rows)));
+      const long long off = (reinterpret_cast<long long>(side) -
+                             reinterpret_cast<long long>(y0->ci)) / 16;
+      direct = off >= -(1ll << 31) && off + 2ll * y0->rows < (1ll << 31);
+      if (direct) {
+        side_off = uint32_t(int32_t(off));
+        host_prof_mark(1);
+        launch_pass_table(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, wps, side);
+      }
+    }
+    if (!direct) {
+      uint32_t* pci = aalloc<uint32_t>(ctx, padded_size(y0->rows, y0->nnz));
+      host_prof_mark(1);
+      launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps, erow0 <= 96.0);
+      bci = pci;
+    }
+    ctx->last_exact.layout = direct ? 0 : 1;
     const int ns = std::max(1, (L_.wstats.maxdeg + 31) / 32);  // in-edge slots per lane
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
     auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {
@@ -2423,7 +2452,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     const int ku = units <= 700.0 ? 6 : 4;
     for (int attempt = 0; attempt < 2; ++attempt) {
       const int fl = sp_lg - (fb == 4 ? 3 : 2);
-      const size_t smem = stream_block_bytes(fl, fb);
+      const size_t smem = stream_block_bytes(fl, fb, ku);
       const void* kern = stream_kernel(fl, ns, fb, ku);
       kernel_smem_attr(ctx, kern, int(smem));
       const int per_sm = kernel_occupancy(ctx, kern, stream_block_threads(), smem);
@@ -2439,7 +2468,8 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       StreamArgs sa;
       sa.arp = w->rp;
       sa.aci = w->ci;
-      sa.bci = pci;
+      sa.bci = bci;
+      sa.side = side_off;
       sa.wpc = wps;
       sa.m = m;
       sa.n = n;

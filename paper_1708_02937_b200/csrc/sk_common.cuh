@@ -120,8 +120,8 @@ struct sk_ctx {
   double sparse_below = 1.0 / 128;
   // Kernel selection (sk_ctx_set_tuning; 0 = automatic) and what the last
   // exact-layer launch ran (sk_ctx_last_exact).
-  sk_tuning tune = {0, 0, 0, 0, 0, 0, 0, 0.0, 0};
-  sk_exact_info last_exact = {0, 0, 0, 0, 0, 0, 0};
+  sk_tuning tune = {0, 0, 0, 0, 0, 0, 0, 0.0, 0, 0};
+  sk_exact_info last_exact = {0, 0, 0, 0, 0, 0, 0, 0};
   // Grow-only scratch arena for the temporaries of one forward call (window
   // tables, item counts, scratch spans, ping-pong buffers): per-call pool
   // allocations of ~1 GB cost milliseconds of host time with the GPU idle.

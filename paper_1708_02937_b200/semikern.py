@@ -201,7 +201,7 @@ class Context:
         _check(self._L.sk_ctx_set_density_switch(self.h, float(dense_above), float(sparse_below)))
 
     TUNING_KEYS = ("exact", "exact_kernel", "exact_group", "exact_records", "window_log2",
-                   "exact_window_log2", "esc", "esc_ratio", "exact_fields")
+                   "exact_window_log2", "esc", "esc_ratio", "exact_fields", "exact_layout")
 
     def tuning(self) -> dict:
         """The context's kernel selection (sk_tuning; 0 = automatic)."""
@@ -232,7 +232,8 @@ class Context:
                 "kernel": {0: None, 1: "generic", 2: "specialised", 3: "push",
                            4: "flat", 5: "stream"}[e.kernel],
                 "group": e.group, "records": e.records, "window_log2": e.window_log2,
-                "fields": e.fields, "wraps": e.wraps}
+                "fields": e.fields, "wraps": e.wraps,
+                "layout": {0: "direct", 1: "padded"}[e.layout]}
 
     def set_stream(self, stream_ptr: int | None):
         _check(self._L.sk_ctx_set_stream(self.h, vp(stream_ptr) if stream_ptr else None))

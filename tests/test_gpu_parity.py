@@ -1002,14 +1002,16 @@ STREAM_CASES = [
 ]
 
 
+@pytest.mark.parametrize("layout", [2, 1])
 @pytest.mark.parametrize("case", STREAM_CASES)
-def test_stream_kernel_regimes(sk, port, case):
+def test_stream_kernel_regimes(sk, port, case, layout):
     """K7 (k_exact_stream, the order-free row stream) against the oracle's sparse
     layer (matrix.cpp:452-521 + dnn.cpp:86-103 restated) in the regimes its
     host logic chooses between: 4- vs 8-bit counters, a 4-bit counter wrapping
     (the layer is rerun with 8-bit ones), in-degrees up to 96 (one to three
     in-edge slots per lane, rows with none), a batch narrower than one pass,
-    passes that end past the batch, the touched-word clear of sparse passes."""
+    passes that end past the batch, the touched-word clear of sparse passes --
+    each with Y read in place (layout 2) and through the padded copy (1)."""
     m, n, kY, bias, clip, maxdeg, fields = case
     hW = _in_degree_weights(m, maxdeg, m + n)
     hY = port.gen_input_binary(m, n, kY, 7)
@@ -1018,7 +1020,7 @@ def test_stream_kernel_regimes(sk, port, case):
     ctx = sk.default_context()
     # the wrapping case: 2048-sample passes (the widest that take 4-bit counters
     # is chosen narrower for this density)
-    old = ctx.set_tuning(exact_kernel=5, exact_fields=fields,
+    old = ctx.set_tuning(exact_kernel=5, exact_fields=fields, exact_layout=layout,
                          exact_group=2 if bias == -0.1 else 0)
     ctx.set_density_switch(0.0, 0.0)  # keep the activations sparse
     try:
@@ -1030,12 +1032,56 @@ def test_stream_kernel_regimes(sk, port, case):
         ctx.set_tuning(**old)
         ctx.set_density_switch()
     assert ctx.layer_paths(1) == ["exact"] and info["kernel"] == "stream", info
+    assert info["layout"] == {2: "direct", 1: "padded"}[layout], info
     assert list(trace) == [hY.nnz, want.nnz]
     assert_csr_bitwise(out, want)
     if fields == 8 or bias == -0.5:
         assert info["fields"] == 4, info  # 8-bit counters: four per word
     if bias == -0.1:
         assert want.nnz > 100000 and info["wraps"] > n0, info  # the 4-bit pass wrapped
+
+
+@pytest.mark.parametrize("n,group", [(20000, 0), (40000, 0), (9000, 1), (3000, 0)])
+def test_stream_in_place_row_boundaries(sk, port, n, group):
+    """K7 reading Y in place: a 16-byte unit at a row's start or end also holds
+    entries of the neighbouring rows, and those must not count (the slice's side
+    unit replaces it -- the pass table's head / tail flags).  Rows of 0..9
+    entries at random samples (most rows start and end inside a unit, many
+    consist of one unit, neighbours' samples fall into the same pass), 2 / 3 /
+    9 / 1 passes; bitwise against the oracle's sparse layer and against the
+    padded copy."""
+    from oracle.oracle import Csr
+    m = 3001
+    rng = np.random.default_rng(n + group)
+    lens = rng.integers(0, 10, size=m)
+    lens[::97] = 0
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+    ci = np.concatenate([np.sort(rng.choice(n, size=int(c), replace=False)) for c in lens]
+                        ).astype(np.uint32)
+    hY = Csr(m, n, rp, ci, np.ones(len(ci), np.float32))
+    hW = _in_degree_weights(m, 64, 11)
+    b = np.full(m, -0.05, np.float32)
+    want = port.layer_sparse(hW, b, hY, 32.0)
+    ctx = sk.default_context()
+    outs = []
+    for layout in (2, 1):
+        old = ctx.set_tuning(exact_kernel=5, exact_layout=layout, esc=-1,
+                             exact_group=group)
+        ctx.set_density_switch(0.0, 0.0)
+        try:
+            model = sk.DnnModel([dev_csr(sk, hW)], [b])
+            out, trace = sk.relu_forward_sparse(model, dev_csr(sk, hY),
+                                                sk.ForwardOptions(clip=32.0))
+            info = ctx.last_exact()
+        finally:
+            ctx.set_tuning(**old)
+            ctx.set_density_switch()
+        assert info["kernel"] == "stream", info
+        assert info["layout"] == {2: "direct", 1: "padded"}[layout], info
+        assert list(trace) == [hY.nnz, want.nnz]
+        assert_csr_bitwise(out, want)
+        outs.append(out)
+    assert want.nnz > 1000
 
 
 def test_pattern16_upload_matches_pattern(sk, port):
