@@ -126,7 +126,9 @@ int bits_for(uint64_t v) {  // smallest b with v <= 2^b
 }
 
 // The whole tiny layer in one CTA (<= kSmallEntries inputs, <= kSmallCap
-// products): input rows by binary search, products expanded, a bitonic sort of
+// products): input rows by binary search (or, for K7's unsorted output read
+// straight from its scratch, given per entry and the inputs sorted by (row,
+// column) first), products expanded, a bitonic sort of
 // (i n + j) << 11 | product index in shared memory (the product index breaks
 // ties, so a run lists its products in input order = ascending k), run folds
 // + epilogue, compaction, and the output CSR written directly (column, value
@@ -142,15 +144,18 @@ __global__ void __launch_bounds__(kSmallThreads)
                float clip, uint32_t* __restrict__ oci,
                float* __restrict__ ov, uint32_t* __restrict__ count,
                const uint32_t* __restrict__ nnz_dev, uint32_t* __restrict__ handled,
-               uint32_t* __restrict__ orow, const uint32_t* __restrict__ erow_dev) {
+               uint32_t* __restrict__ orow, const uint32_t* __restrict__ in_row) {
   __shared__ unsigned long long skey[kSmallCap];
   __shared__ float sval[kSmallCap];
   __shared__ uint32_t s_off[kSmallEntries + 1];
   __shared__ uint32_t s_tb[kSmallEntries];
   __shared__ uint32_t s_row[kSmallCap];  // input entries' rows, later the survivors' rows
+  __shared__ uint32_t s_col[kSmallEntries];  // input entries' columns and values
+  __shared__ float s_val[kSmallEntries];
   __shared__ uint32_t s_wsum[kSmallThreads / 32];
   constexpr uint32_t kIdx = 2049;
-  __shared__ uint32_t s_idx[kIdx];        // row pointers of every 2^lst-th row
+  static_assert(kIdx * 4 <= sizeof(skey), "the row-pointer samples live in skey");
+  uint32_t* const s_idx = reinterpret_cast<uint32_t*>(skey);  // every 2^lst-th row pointer
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // block-wide exclusive sum of one value per thread
   auto block_excl = [&](uint32_t v, uint32_t& total) {
@@ -177,81 +182,10 @@ __global__ void __launch_bounds__(kSmallThreads)
     __syncthreads();
     return ex;
   };
-  // deferred launch (the input's entry count is only on the device): a layer
-  // beyond the tiny limits is left to the host (handled = 0, nothing written)
-  if (nnz_dev) {
-    nnz = *nnz_dev;
-    if (nnz > kSmallEntries) {
-      if (tid == 0) *handled = 0u, *count = 0u;
-      return;
-    }
-  }
-  // 1. each input entry's row: given by the producer (erow_dev), or from the
-  //    row pointers sampled every 2^lst rows into shared memory (one coalesced
-  //    load per thread), then per entry a binary search there and one of
-  //    <= log2(2^lst) global steps inside its block -- not ~17 dependent L2 round
-  //    trips, and not a walk over every row
-  if (erow_dev) {
-    if (tid < nnz) s_row[tid] = erow_dev[tid];
-  } else {
-    uint32_t lst = 6;
-    while ((uint32_t(kIdx - 1) << lst) < rows) ++lst;
-    const uint32_t nb = (rows + (1u << lst) - 1) >> lst;  // blocks (<= kIdx - 1)
-    for (uint32_t b = tid; b <= nb; b += kSmallThreads) s_idx[b] = yrp[min(b << lst, rows)];
-    __syncthreads();
-    if (tid < nnz) {
-      uint32_t lo = 0, hi = nb;  // last block with s_idx[b] <= tid
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_idx[mid] <= tid) lo = mid; else hi = mid;
-      }
-      uint32_t rlo = lo << lst, rhi = min(rows, (lo + 1) << lst);  // last row with yrp <= tid
-      while (rhi - rlo > 1) {
-        const uint32_t mid = (rlo + rhi) >> 1;
-        if (yrp[mid] <= tid) rlo = mid; else rhi = mid;
-      }
-      s_row[tid] = rlo;
-    }
-  }
-  __syncthreads();
-  uint32_t deg = 0;
-  if (tid < nnz) {
-    const uint32_t k = s_row[tid];
-    const uint32_t tb = trp[k];
-    s_tb[tid] = tb;
-    deg = trp[k + 1] - tb;
-  }
-  uint32_t P;
-  const uint32_t eo = block_excl(deg, P);
-  if (handled && P > kSmallCap) {  // block-uniform
-    if (tid == 0) *handled = 0u, *count = 0u;
-    return;
-  }
-  if (tid < nnz) s_off[tid] = eo;
-  if (tid == 0) s_off[nnz] = P;
-  __syncthreads();
-  uint32_t P2 = 1;
-  while (P2 < P) P2 <<= 1;
-  // 2. expand: product q of entry e = (W^T row entry, input entry)
-  for (uint32_t q = tid; q < P2; q += kSmallThreads) {
-    if (q < P) {
-      uint32_t lo = 0, hi = nnz;  // last entry with s_off[e] <= q
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_off[mid] <= q) lo = mid; else hi = mid;
-      }
-      const uint32_t t = s_tb[lo] + (q - s_off[lo]);
-      skey[q] = ((unsigned long long)tci[t] * n + yci[lo]) << 11 | q;
-      sval[q] = __fmul_rn(tv[t], yv[lo]);
-    } else {
-      skey[q] = ~0ull;  // padding sorts last
-    }
-  }
-  __syncthreads();
-  // 3. bitonic sort of the P2 keys, two per thread (indices tid, tid + 1024) in
-  //    registers: partners closer than 32 are in the same warp (shuffles, no
-  //    barrier); the farther ones go through shared memory, one barrier each
-  {
+  // bitonic sort of skey[0, P2), two keys per thread (indices tid, tid + 1024)
+  // in registers: partners closer than 32 are in the same warp (shuffles, no
+  // barrier); the farther ones go through shared memory, one barrier each
+  auto sort_keys = [&](uint32_t P2) {
     unsigned long long v[2];
     v[0] = skey[tid];
     v[1] = tid + kSmallThreads < P2 ? skey[tid + kSmallThreads] : ~0ull;
@@ -287,7 +221,95 @@ __global__ void __launch_bounds__(kSmallThreads)
     skey[tid] = v[0];
     if (two) skey[tid + kSmallThreads] = v[1];
     __syncthreads();
+  };
+  // deferred launch (the input's entry count is only on the device): a layer
+  // beyond the tiny limits is left to the host (handled = 0, nothing written)
+  if (nnz_dev) {
+    nnz = *nnz_dev;
+    if (nnz > kSmallEntries) {
+      if (tid == 0) *handled = 0u, *count = 0u;
+      return;
+    }
   }
+  // 1. each input entry's row: given by the producer (in_row), or from the
+  //    row pointers sampled every 2^lst rows into shared memory (one coalesced
+  //    load per thread), then per entry a binary search there and one of
+  //    <= log2(2^lst) global steps inside its block -- not ~17 dependent L2 round
+  //    trips, and not a walk over every row
+  if (in_row) {
+    // unsorted inputs (K7's scratch): sorted by (row, column) -- a run's
+    // products then fold in ascending k, as the reference's mxm does
+    uint32_t P2 = 1;
+    while (P2 < nnz) P2 <<= 1;
+    for (uint32_t q = tid; q < P2; q += kSmallThreads)
+      skey[q] = q < nnz ? ((unsigned long long)in_row[q] * n + yci[q]) << 9 | q : ~0ull;
+    __syncthreads();
+    sort_keys(P2);
+    if (tid < nnz) {
+      const uint32_t e = uint32_t(skey[tid] & 511u);
+      s_row[tid] = in_row[e];
+      s_col[tid] = yci[e];
+      s_val[tid] = yv[e];
+    }
+  } else {
+    uint32_t lst = 6;
+    while ((uint32_t(kIdx - 1) << lst) < rows) ++lst;
+    const uint32_t nb = (rows + (1u << lst) - 1) >> lst;  // blocks (<= kIdx - 1)
+    for (uint32_t b = tid; b <= nb; b += kSmallThreads) s_idx[b] = yrp[min(b << lst, rows)];
+    __syncthreads();
+    if (tid < nnz) {
+      uint32_t lo = 0, hi = nb;  // last block with s_idx[b] <= tid
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_idx[mid] <= tid) lo = mid; else hi = mid;
+      }
+      uint32_t rlo = lo << lst, rhi = min(rows, (lo + 1) << lst);  // last row with yrp <= tid
+      while (rhi - rlo > 1) {
+        const uint32_t mid = (rlo + rhi) >> 1;
+        if (yrp[mid] <= tid) rlo = mid; else rhi = mid;
+      }
+      s_row[tid] = rlo;
+      s_col[tid] = yci[tid];
+      s_val[tid] = yv[tid];
+    }
+  }
+  __syncthreads();
+  uint32_t deg = 0;
+  if (tid < nnz) {
+    const uint32_t k = s_row[tid];
+    const uint32_t tb = trp[k];
+    s_tb[tid] = tb;
+    deg = trp[k + 1] - tb;
+  }
+  uint32_t P;
+  const uint32_t eo = block_excl(deg, P);
+  if (handled && P > kSmallCap) {  // block-uniform
+    if (tid == 0) *handled = 0u, *count = 0u;
+    return;
+  }
+  if (tid < nnz) s_off[tid] = eo;
+  if (tid == 0) s_off[nnz] = P;
+  __syncthreads();
+  uint32_t P2 = 1;
+  while (P2 < P) P2 <<= 1;
+  // 2. expand: product q of entry e = (W^T row entry, input entry)
+  for (uint32_t q = tid; q < P2; q += kSmallThreads) {
+    if (q < P) {
+      uint32_t lo = 0, hi = nnz;  // last entry with s_off[e] <= q
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_off[mid] <= q) lo = mid; else hi = mid;
+      }
+      const uint32_t t = s_tb[lo] + (q - s_off[lo]);
+      skey[q] = ((unsigned long long)tci[t] * n + s_col[lo]) << 11 | q;
+      sval[q] = __fmul_rn(tv[t], s_val[lo]);
+    } else {
+      skey[q] = ~0ull;  // padding sorts last
+    }
+  }
+  __syncthreads();
+  // 3. bitonic sort of the P2 product keys
+  sort_keys(P2);
   // 4. run heads fold their products in order, epilogue; 5. compaction
   float z[kSmallItems];
   uint32_t keep[kSmallItems];
@@ -832,21 +854,23 @@ bool esc_applicable(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y
 }
 
 // Layer k on the tiny ESC kernel launched before the input's entry count is
-// known on the host (it is read from *d_nnz on the device): the output has the
-// kernel's full capacity; d_cnt[0] receives its entry count and d_cnt[1] 1 when
-// the kernel handled the layer (0: too many inputs or products -- nothing was
-// written, the host takes the layer its usual way).  Every bias of layer k <= 0.
-sk_csr* esc_tiny_deferred(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y,
-                          const uint32_t* d_nnz, const uint32_t* d_erow, float clip,
-                          uint32_t* d_cnt) {
+// known on the host (it is read from *d_nnz on the device), its input the
+// entries (in_row, in_col, in_val) in any order (K7's scratch, before the
+// gather): the output has the kernel's full capacity; d_cnt[0] receives its
+// entry count and d_cnt[1] 1 when the kernel handled the layer (0: too many
+// inputs or products -- nothing was written, the host takes the layer its
+// usual way).  Every bias of layer k <= 0.
+sk_csr* esc_tiny_deferred(sk_ctx* ctx, const sk_model* md, uint32_t k, uint32_t n,
+                          const uint32_t* in_row, const uint32_t* in_col, const float* in_val,
+                          const uint32_t* d_nnz, float clip, uint32_t* d_cnt) {
   auto* mm = const_cast<sk_model*>(md);
   const sk_csr* wt = model_layer_transpose(ctx, mm, k);
-  const uint32_t m = wt->cols, n = y->cols;
+  const uint32_t m = wt->cols;
   sk_csr* out = new_csr(ctx, m, n, kSmallCap);
   uint32_t* orow = aalloc<uint32_t>(ctx, kSmallCap);
-  SK_LAUNCH(k_esc_tiny, 1, kSmallThreads, 0, ctx->stream, y->rp, y->rows, y->ci, y->v, 0u, n,
+  SK_LAUNCH(k_esc_tiny, 1, kSmallThreads, 0, ctx->stream, nullptr, 0u, in_col, in_val, 0u, n,
             wt->rp, wt->ci, wt->v, m, md->bias + size_t(k) * md->neurons, clip, out->ci,
-            out->v, d_cnt, d_nnz, d_cnt + 1, orow, d_erow);
+            out->v, d_cnt, d_nnz, d_cnt + 1, orow, in_row);
   // (a layer the kernel left to the host has count 0 here: rp is rewritten then)
   SK_LAUNCH(k_esc_fill_rp, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, orow, d_cnt, m,
             out->rp);

@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(32 * kSW) k_exact_stream(StreamArgs p) {
             const float x = __fmul_rn(__int2float_rn(ai), p.fx_unscale);
             p.sc_c[pos] = c_pbase + slw + bt;
             p.sc_v[pos] = layer_epilogue(x, b, p.clip);
+            if (p.sc_r && pos < 512) p.sc_r[pos] = c_row;
             ++pos;
           }
         }

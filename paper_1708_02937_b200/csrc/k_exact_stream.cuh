@@ -28,6 +28,7 @@ struct StreamArgs {
   unsigned long long* item_off;
   uint32_t* sc_c;
   float* sc_v;
+  uint32_t* sc_r;         // nullable: the row of each of the first 512 scratch entries
   unsigned long long* bump;
   unsigned long long* work;
   unsigned long long cap;

@@ -1229,15 +1229,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_spgemm_rows(RowArgs p, uint32_t
   phase_a<Ops, kLayer, false>(p, ws, lane, gw, nw);
 }
 
-// erow (optional): the row of each of the first erow_cap output entries (items
-// per_row to a row), for the tiny ESC that follows without a host round trip
 __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
                                const unsigned long long* __restrict__ item_off,
                                const uint32_t* __restrict__ wp_out, uint64_t items,
                                const uint32_t* __restrict__ sc_c, const float* __restrict__ sc_v,
                                uint32_t* __restrict__ oc, float* __restrict__ ov,
-                               const int* overflow, uint32_t per_row = 1,
-                               uint32_t* __restrict__ erow = nullptr, uint32_t erow_cap = 0) {
+                               const int* overflow) {
   if (*overflow || wp_out[items] == 0) return;
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1254,7 +1251,6 @@ __global__ void k_gather_items(const uint32_t* __restrict__ item_cnt,
       for (uint32_t t = lane; t < cl; t += 32) {
         oc[size_t(dst) + t] = sc_c[src + t];
         ov[size_t(dst) + t] = sc_v[src + t];
-        if (erow && dst + t < erow_cap) erow[dst + t] = uint32_t((it0 + l) / per_row);
       }
     }
   }
@@ -1887,6 +1883,22 @@ struct StagedLayer {
 
 void host_prof_mark(int i);  // SK_HOST_PROF (sparse_forward_impl)
 
+// K7's output left in its scratch (deferred chaining): the survivors of each
+// (row, pass) item at item_off, unordered across items; the rows of the first
+// 512 entries in sc_r; the entry count at *d_nnz (the bump counter's low word)
+struct StreamPending {
+  bool ok = false;
+  uint32_t m = 0, n = 0, nP = 0;
+  uint64_t sitems = 0;
+  uint32_t* item_cnt = nullptr;
+  unsigned long long* item_off = nullptr;
+  uint32_t* sc_c = nullptr;
+  float* sc_v = nullptr;
+  uint32_t* sc_r = nullptr;
+  int* overflow = nullptr;
+  const uint32_t* d_nnz = nullptr;
+};
+
 struct ExactLayerIn {
   const sk_csr* w;
   const float* bias;  // device, w->rows
@@ -1896,11 +1908,11 @@ struct ExactLayerIn {
   uint32_t stamp_layer;  // %globaltimer slot (ctx->stamps)
   const sk_csr* wT = nullptr;  // W^T (cached with a model) -- enables the push kernel
   StagedLayer* stage = nullptr;  // stop before the gather (the exchange publishes it)
-  // K7 only: no host round trip -- the output gets the scratch capacity, its
-  // entry count stays on the device (*defer_nnz), and the caller reads it with
-  // the overflow / wrap flags (ctx->d_u64 slots 1 and 3) after its own next step
-  const uint32_t** defer_nnz = nullptr;
-  uint32_t* defer_erow = nullptr;  // with defer_nnz: rows of the first 512 output entries
+  // K7 only: no host round trip -- the output stays in the kernel's scratch
+  // (*defer filled, nullptr returned), its entry count on the device; the
+  // caller reads it with the overflow / wrap flags (ctx->d_u64 slots 1 and 3)
+  // after its own next step, and gathers it (stream_finish) only if needed
+  StreamPending* defer = nullptr;
 };
 
 // Weight statistics of a bare CSR (value statistics + row bounds), cached on the
@@ -2276,11 +2288,9 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
 
 static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, uint32_t k0,
                            float clip, const ValueStats& ystats, uint32_t** wp_out_ptr,
-                           const uint32_t** defer_nnz = nullptr,
-                           uint32_t* defer_erow = nullptr) {
+                           StreamPending* defer = nullptr) {
   ExactLayerIn in;
-  in.defer_nnz = defer_nnz;
-  in.defer_erow = defer_erow;
+  in.defer = defer;
   in.w = md->w[k0];
   in.bias = md->bias + size_t(k0) * md->neurons;
   in.wstats = md->wstats_host[k0];
@@ -2290,6 +2300,20 @@ static sk_csr* exact_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, ui
   if (md->bias_nonpos[k0] && ctx->tune.exact_kernel == 3)
     in.wT = model_layer_transpose(ctx, const_cast<sk_model*>(md), k0);
   return exact_layer_w(ctx, in, y0, clip, ystats, wp_out_ptr);
+}
+
+// A deferred K7 output (StreamPending) as a CSR of nnz entries: the items'
+// scan, the gather in (row, sample) order, the row pointers.
+static sk_csr* stream_finish(sk_ctx* ctx, const StreamPending& sp, uint32_t nnz) {
+  uint32_t* wp_out = aalloc<uint32_t>(ctx, sp.sitems + 1);
+  SK_CUDA(cudaMemsetAsync(sp.item_cnt + sp.sitems, 0, 4, ctx->stream));
+  exclusive_scan_u32(ctx, sp.item_cnt, wp_out, sp.sitems + 1);
+  sk_csr* o = new_csr(ctx, sp.m, sp.n, nnz);
+  SK_LAUNCH(k_gather_items, grid_warps(ctx, sp.sitems), 256, 0, ctx->stream, sp.item_cnt,
+            sp.item_off, wp_out, sp.sitems, sp.sc_c, sp.sc_v, o->ci, o->v, sp.overflow);
+  SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, sp.m + 1), 256, 0, ctx->stream, wp_out, sp.m, sp.nP,
+            o->rp);
+  return o;
 }
 
 static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* y0, float clip,
@@ -2488,6 +2512,7 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       sa.item_off = item_off;
       sa.sc_c = sc_c;
       sa.sc_v = sc_v;
+      sa.sc_r = L_.defer && !L_.stage ? aalloc<uint32_t>(ctx, 512) : nullptr;
       sa.bump = d;
       sa.work = d + 2;
       sa.cap = cap;
@@ -2502,21 +2527,26 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       timing_mark(ctx, SK_KT_STREAM);
       launch_exact_stream(ctx, sa, fl, ns, fb, ku, grid, smem);
       timing_mark(ctx);
+      if (L_.defer && !L_.stage) {
+        // no round trip and no gather yet: the output stays in the scratch
+        StreamPending& dp = *L_.defer;
+        dp.ok = true;
+        dp.m = m;
+        dp.n = n;
+        dp.nP = gs.nW;
+        dp.sitems = sitems;
+        dp.item_cnt = item_cnt;
+        dp.item_off = item_off;
+        dp.sc_c = sc_c;
+        dp.sc_v = sc_v;
+        dp.sc_r = sa.sc_r;
+        dp.overflow = sa.overflow;
+        dp.d_nnz = reinterpret_cast<const uint32_t*>(d);  // bump, low word
+        *wp_out_ptr = nullptr;
+        return nullptr;
+      }
       SK_CUDA(cudaMemsetAsync(item_cnt + sitems, 0, 4, ctx->stream));
       exclusive_scan_u32(ctx, item_cnt, wp_out, sitems + 1);
-      if (L_.defer_nnz && !L_.stage) {
-        // no round trip: the output at the scratch capacity, gathered and
-        // row-pointed on the device (the gather reads the total itself)
-        sk_csr* o = new_csr(ctx, m, n, cap);
-        SK_LAUNCH(k_gather_items, grid_warps(ctx, sitems), 256, 0, ctx->stream, item_cnt,
-                  item_off, wp_out, sitems, sc_c, sc_v, o->ci, o->v, sa.overflow, gs.nW,
-                  L_.defer_erow, L_.defer_erow ? 512u : 0u);
-        SK_LAUNCH(k_rp_from_wp, grid_warps(ctx, m + 1), 256, 0, ctx->stream, wp_out, m, gs.nW,
-                  o->rp);
-        *L_.defer_nnz = wp_out + sitems;
-        *wp_out_ptr = nullptr;
-        return o;
-      }
       uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
       SK_CUDA(cudaMemcpyAsync(hp, wp_out + sitems, 4, cudaMemcpyDeviceToHost, ctx->stream));
       SK_CUDA(cudaMemcpyAsync(hp + 1, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -2807,16 +2837,18 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
             // the exact layer and the tiny ESC of layer k + 1 behind it with ONE host
             // round trip (the collapse of cfg3-5: layer 2's input is a few entries)
             if (esc_env && k + 1 < L && esc_tiny_possible(md, k + 1, cur)) {
-              const uint32_t* d_nnz = nullptr;
+              StreamPending sp;
               model_layer_transpose(ctx, const_cast<sk_model*>(md), k + 1);  // cached
-              uint32_t* erow = aalloc<uint32_t>(ctx, 512);
-              sk_csr* r = exact_layer(ctx, md, cur, k, clip, ys, &wp1, &d_nnz, erow);
-              if (d_nnz) {
+              sk_csr* r = exact_layer(ctx, md, cur, k, clip, ys, &wp1, &sp);
+              if (sp.ok) {
+                // the tiny ESC reads K7's scratch directly; the gather into a CSR
+                // runs only when it declines the layer
                 uint32_t* dc = aalloc<uint32_t>(ctx, 2);
-                sk_csr* r2 = esc_tiny_deferred(ctx, md, k + 1, r, d_nnz, erow, clip, dc);
+                sk_csr* r2 = esc_tiny_deferred(ctx, md, k + 1, sp.n, sp.sc_r, sp.sc_c, sp.sc_v,
+                                               sp.d_nnz, clip, dc);
                 uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 16);  // pinned
                 const uint32_t* dflags = reinterpret_cast<const uint32_t*>(ctx->d_u64);
-                SK_CUDA(cudaMemcpyAsync(hp, d_nnz, 4, cudaMemcpyDeviceToHost, ctx->stream));
+                SK_CUDA(cudaMemcpyAsync(hp, sp.d_nnz, 4, cudaMemcpyDeviceToHost, ctx->stream));
                 SK_CUDA(cudaMemcpyAsync(hp + 1, dflags + 2, 4, cudaMemcpyDeviceToHost,
                                         ctx->stream));  // overflow (slot 1)
                 SK_CUDA(cudaMemcpyAsync(hp + 2, dflags + 6, 4, cudaMemcpyDeviceToHost,
@@ -2826,14 +2858,12 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
                 sync(ctx);
                 host_prof_mark(3);
                 if (!hp[1] && !hp[2]) {
-                  r->nnz = hp[0];  // the arrays keep the scratch capacity
                   if (owned) csr_release(owned);
                   trace[k + 1] = hp[0];
                   set_paths(k, 1, SK_PATH_EXACT);
                   pending_wp = nullptr;
                   if (hp[4]) {  // the tiny ESC took layer k + 1
                     r2->nnz = hp[3];
-                    csr_release(r);
                     owned = r2;
                     cur = r2;
                     trace[k + 2] = hp[3];
@@ -2841,8 +2871,9 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
                     k += 2;
                   } else {
                     csr_release(r2);
-                    owned = r;
-                    cur = r;
+                    sk_csr* r1 = stream_finish(ctx, sp, hp[0]);
+                    owned = r1;
+                    cur = r1;
                     k += 1;
                   }
                   if (k >= L) break;
@@ -2851,7 +2882,6 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
                 // an overflow or a wrapped 4-bit counter: the layer again, with its
                 // own round trips (it grows the scratch / takes 8-bit counters)
                 csr_release(r2);
-                csr_release(r);
               } else {
                 if (owned) csr_release(owned);
                 owned = r;

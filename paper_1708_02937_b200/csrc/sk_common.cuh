@@ -372,12 +372,13 @@ sk_csr* csr_transpose(sk_ctx* ctx, const sk_csr* a);
 // Thin layers by expand-sort-compress (k_esc.cu); every bias of layer k <= 0.
 bool esc_applicable(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y, double ratio);
 sk_csr* esc_layer(sk_ctx* ctx, const sk_model* md, const sk_csr* y, uint32_t k, float clip);
-// The tiny ESC launched before y's entry count reaches the host (k_esc.cu): the
-// count is read from *d_nnz; d_cnt[0] = output entries, d_cnt[1] = 1 if handled.
+// The tiny ESC launched before its input's entry count reaches the host
+// (k_esc.cu): the count is read from *d_nnz, the entries (in any order) from
+// in_row / in_col / in_val; d_cnt[0] = output entries, d_cnt[1] = 1 if handled.
 bool esc_tiny_possible(const sk_model* md, uint32_t k, const sk_csr* y);
-sk_csr* esc_tiny_deferred(sk_ctx* ctx, const sk_model* md, uint32_t k, const sk_csr* y,
-                          const uint32_t* d_nnz, const uint32_t* d_erow, float clip,
-                          uint32_t* d_cnt);
+sk_csr* esc_tiny_deferred(sk_ctx* ctx, const sk_model* md, uint32_t k, uint32_t n,
+                          const uint32_t* in_row, const uint32_t* in_col, const float* in_val,
+                          const uint32_t* d_nnz, float clip, uint32_t* d_cnt);
 void ensure_model_tables(sk_ctx* ctx, sk_model* md);
 void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const float* y0,
                           uint32_t n, float clip, float* buf0, float* buf1,
