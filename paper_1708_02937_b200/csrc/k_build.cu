@@ -795,6 +795,17 @@ __global__ void k_flag_cols_dense(const float* d, uint32_t rows, uint32_t cols,
     if (d[i] != 0.0f) flags[i % cols] = 1;
 }
 
+__global__ void k_post_list(const int* nsel, const uint32_t* list, volatile uint32_t* box,
+                            uint32_t cap, uint32_t seq) {
+  const uint32_t n = uint32_t(*nsel);
+  if (threadIdx.x == 0) box[kMboxHdr] = n;
+  if (n <= cap)
+    for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) box[kMboxHdr + 1 + j] = list[j];
+  __threadfence_system();  // every thread's stores before the flag
+  __syncthreads();
+  if (threadIdx.x == 0) box[0] = seq;
+}
+
 void categories_from_flags(sk_ctx* ctx, uint8_t* flags, uint32_t n, uint32_t* idx,
                            size_t cap, size_t* count) {
   uint32_t* out = dalloc<uint32_t>(ctx, n);
@@ -805,14 +816,22 @@ void categories_from_flags(sk_ctx* ctx, uint8_t* flags, uint32_t n, uint32_t* id
   void* t = dalloc<char>(ctx, tmp);
   SK_CUDA(cub::DeviceSelect::Flagged(t, tmp, it, flags, out, nsel, n, ctx->stream));
   g_launches.fetch_add(1);
-  int h = 0;
-  SK_CUDA(cudaMemcpyAsync(&h, nsel, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
+  // count + (when it fits) the list itself through the mailbox: no device->host
+  // copies, no stream synchronise (both stall beside a bulk upload on another stream)
+  const uint32_t seq = ++ctx->mbox_seq;
+  SK_LAUNCH(k_post_list, 1, 256, 0, ctx->stream, nsel, out, ctx->mbox_dev, kMboxWords - 1, seq);
+  mbox_wait(ctx, seq);
+  const uint32_t h = ctx->mbox[kMboxHdr];
   *count = size_t(h);
-  if (idx && h)
-    SK_CUDA(cudaMemcpyAsync(idx, out, std::min<size_t>(cap, h) * 4, cudaMemcpyDeviceToHost,
-                            ctx->stream));
-  sync(ctx);
+  if (idx && h) {
+    const size_t take = std::min<size_t>(cap, h);
+    if (h <= kMboxWords - 1) {
+      std::memcpy(idx, ctx->mbox + kMboxHdr + 1, take * 4);
+    } else {
+      SK_CUDA(cudaMemcpyAsync(idx, out, take * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      sync(ctx);
+    }
+  }
   dfree(ctx, t);
   dfree(ctx, out);
 }
@@ -823,6 +842,10 @@ extern "C" sk_status sk_categories_csr(sk_ctx* ctx, const sk_csr* y, uint32_t* i
   return guarded([&] {
     csr_ready(ctx, y);
     SK_CUDA(cudaSetDevice(ctx->device));
+    if (y->nnz == 0) {  // no stored entry, no category: nothing to launch or read back
+      *count = 0;
+      return;
+    }
     uint8_t* flags = dalloc<uint8_t>(ctx, y->cols);
     SK_CUDA(cudaMemsetAsync(flags, 0, y->cols, ctx->stream));
     if (y->nnz)

@@ -16,6 +16,8 @@
 // gives epilogue(0 + b) == 0, so outputs exist only where products exist.
 #include <cub/cub.cuh>
 
+#include <cstring>
+
 #include "sk_common.cuh"
 
 namespace sk {
@@ -378,10 +380,7 @@ sk_csr* esc_tiny(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bi
             cnt, nullptr, nullptr, orow, nullptr);
   SK_LAUNCH(k_esc_fill_rp, grid_of(ctx, uint64_t(m) + 1), 256, 0, ctx->stream, orow, cnt, m,
             out->rp);
-  uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: an async copy
-  SK_CUDA(cudaMemcpyAsync(hp, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
-  out->nnz = hp[0];  // the arrays keep their capacity
+  out->nnz = Fetch(ctx).add(cnt, 1).run()[0];  // mailbox; the arrays keep their capacity
   return out;
 }
 
@@ -695,9 +694,8 @@ sk_csr* esc_sample(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* 
                                                       uint64_t(ctx->num_sms) * occ));
     SK_LAUNCH(k_esc_sample, grid, kSampWarps * 32, 0, ctx->stream, a);
     SK_LAUNCH(k_esc_sample_big, unsigned(ctx->num_sms) * 4, 32, kBigSmem, ctx->stream, a);
-    unsigned long long* h = reinterpret_cast<unsigned long long*>(ctx->h_u64 + 6);
-    SK_CUDA(cudaMemcpyAsync(h, ctr, 16, cudaMemcpyDeviceToHost, ctx->stream));
-    sync(ctx);
+    unsigned long long h[2];  // survivors, overflow: through the mailbox
+    std::memcpy(h, Fetch(ctx).add(ctr, 4).run(), sizeof(h));
     if (getenv("SK_ESC_DEBUG")) {
       unsigned long long qd = 0;
       SK_CUDA(cudaMemcpy(&qd, ctr + 2, 8, cudaMemcpyDeviceToHost));
@@ -759,9 +757,7 @@ sk_csr* esc_run(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bia
   void* t0 = aalloc<char>(ctx, tmp);
   SK_CUDA(cub::DeviceScan::ExclusiveSum(t0, tmp, deg, off, nnz + 1, ctx->stream));
   g_launches.fetch_add(1);
-  uint32_t P = 0;
-  SK_CUDA(cudaMemcpyAsync(&P, off + nnz, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
+  const uint32_t P = Fetch(ctx).add(off + nnz, 1).run()[0];
   sk_csr* out = nullptr;
   if (P == 0) {
     out = new_csr(ctx, m, n, 0);
@@ -793,9 +789,7 @@ sk_csr* esc_run(sk_ctx* ctx, const sk_csr* y, const sk_csr* wt, const float* bia
   void* t2 = aalloc<char>(ctx, tmp);
   SK_CUDA(cub::DeviceScan::ExclusiveSum(t2, tmp, keep, pos, size_t(P) + 1, ctx->stream));
   g_launches.fetch_add(1);
-  uint32_t S = 0;
-  SK_CUDA(cudaMemcpyAsync(&S, pos + P, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
+  const uint32_t S = Fetch(ctx).add(pos + P, 1).run()[0];
   out = new_csr(ctx, m, n, S);
   K* okey = k0;  // free after the sort
   if (S)

@@ -1842,10 +1842,8 @@ static sk_csr* spgemm_impl(sk_ctx* ctx, const sk_csr* a, const sk_csr* b, sk_sem
   }
   SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
   exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
-  uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
-  SK_CUDA(cudaMemcpyAsync(hp, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  SK_CUDA(cudaMemcpyAsync(hp + 1, overflow, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  sync(ctx);
+  uint32_t hp[2];  // through the mailbox
+  std::memcpy(hp, Fetch(ctx).add(wp_out + items, 1).add(overflow, 1).run(), sizeof(hp));
   const uint32_t nnz = hp[0];
   const int ovf = int(hp[1]);
   if (ovf) fail(SK_ERR_INVALID_ARGUMENT, "mxm scratch capacity exceeded");
@@ -2547,11 +2545,9 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
       }
       SK_CUDA(cudaMemsetAsync(item_cnt + sitems, 0, 4, ctx->stream));
       exclusive_scan_u32(ctx, item_cnt, wp_out, sitems + 1);
-      uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
-      SK_CUDA(cudaMemcpyAsync(hp, wp_out + sitems, 4, cudaMemcpyDeviceToHost, ctx->stream));
-      SK_CUDA(cudaMemcpyAsync(hp + 1, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
-      SK_CUDA(cudaMemcpyAsync(hp + 2, d + 3, 4, cudaMemcpyDeviceToHost, ctx->stream));
-      sync(ctx);
+      uint32_t hp[3];  // through the mailbox (no device->host copies, no stream sync)
+      std::memcpy(hp, Fetch(ctx).add(wp_out + sitems, 1).add(d + 1, 1).add(d + 3, 1).run(),
+                  sizeof(hp));
       if (hp[2]) {  // a 4-bit field wrapped: rerun with 8-bit fields
         fb = 8;
         ctx->last_exact.wraps += 1;
@@ -2690,10 +2686,8 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     timing_mark(ctx);
     SK_CUDA(cudaMemsetAsync(item_cnt + items, 0, 4, ctx->stream));
     exclusive_scan_u32(ctx, item_cnt, wp_out, items + 1);
-    uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 4);  // pinned: async copies
-    SK_CUDA(cudaMemcpyAsync(hp, wp_out + items, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    SK_CUDA(cudaMemcpyAsync(hp + 1, d + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    sync(ctx);
+    uint32_t hp[2];  // through the mailbox
+    std::memcpy(hp, Fetch(ctx).add(wp_out + items, 1).add(d + 1, 1).run(), sizeof(hp));
     const uint32_t nnz = hp[0];
     const int ovf = int(hp[1]);
     if (!ovf && L_.stage) {
@@ -2846,16 +2840,12 @@ sk_csr* sparse_forward_impl(sk_ctx* ctx, const sk_model* md, const sk_csr* y0, f
                 uint32_t* dc = aalloc<uint32_t>(ctx, 2);
                 sk_csr* r2 = esc_tiny_deferred(ctx, md, k + 1, sp.n, sp.sc_r, sp.sc_c, sp.sc_v,
                                                sp.d_nnz, clip, dc);
-                uint32_t* hp = reinterpret_cast<uint32_t*>(ctx->h_u64 + 16);  // pinned
                 const uint32_t* dflags = reinterpret_cast<const uint32_t*>(ctx->d_u64);
-                SK_CUDA(cudaMemcpyAsync(hp, sp.d_nnz, 4, cudaMemcpyDeviceToHost, ctx->stream));
-                SK_CUDA(cudaMemcpyAsync(hp + 1, dflags + 2, 4, cudaMemcpyDeviceToHost,
-                                        ctx->stream));  // overflow (slot 1)
-                SK_CUDA(cudaMemcpyAsync(hp + 2, dflags + 6, 4, cudaMemcpyDeviceToHost,
-                                        ctx->stream));  // wrap (slot 3)
-                SK_CUDA(cudaMemcpyAsync(hp + 3, dc, 8, cudaMemcpyDeviceToHost, ctx->stream));
                 host_prof_mark(2);
-                sync(ctx);
+                // count, overflow (slot 1), wrap (slot 3), the tiny ESC's count + verdict
+                uint32_t hp[5];
+                std::memcpy(hp, Fetch(ctx).add(sp.d_nnz, 1).add(dflags + 2, 1)
+                                    .add(dflags + 6, 1).add(dc, 2).run(), sizeof(hp));
                 host_prof_mark(3);
                 if (!hp[1] && !hp[2]) {
                   if (owned) csr_release(owned);

@@ -100,6 +100,52 @@ void csr_release(sk_csr* a) {
 
 void sync(sk_ctx* ctx) { SK_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
+__global__ void k_post_words(PostSrc s, volatile uint32_t* box, uint32_t seq) {
+  const uint32_t lane = threadIdx.x;
+  uint32_t o = kMboxHdr;
+  for (int i = 0; i < s.cnt; ++i) {
+    for (uint32_t j = lane; j < s.n[i]; j += 32) box[o + j] = s.p[i][j];
+    o += s.n[i];
+  }
+  __threadfence_system();  // each lane's payload stores before the flag
+  __syncwarp();
+  if (lane == 0) box[0] = seq;
+}
+
+Fetch& Fetch::add(const void* dev, uint32_t words) {
+  if (s.cnt >= 8) fail(SK_ERR_INVALID_ARGUMENT, "fetch: too many sources");
+  s.p[s.cnt] = static_cast<const uint32_t*>(dev);
+  s.n[s.cnt] = words;
+  ++s.cnt;
+  return *this;
+}
+
+void mbox_wait(sk_ctx* ctx, uint32_t seq) {
+  volatile uint32_t* flag = ctx->mbox;
+  for (unsigned spins = 1;; ++spins) {
+    if (*flag == seq) return;
+    if ((spins & 0x3FF) == 0) {  // a faulted or drained stream must not spin forever
+      const cudaError_t q = cudaStreamQuery(ctx->stream);
+      if (q == cudaSuccess) {
+        if (*flag == seq) return;
+        fail(SK_ERR_CUDA, "mailbox: the stream drained without posting");
+      }
+      if (q != cudaErrorNotReady) SK_CUDA(q);
+    }
+    __builtin_ia32_pause();
+  }
+}
+
+const uint32_t* Fetch::run() {
+  uint32_t total = 0;
+  for (int i = 0; i < s.cnt; ++i) total += s.n[i];
+  if (total > kMboxWords) fail(SK_ERR_INVALID_ARGUMENT, "fetch: payload exceeds the mailbox");
+  const uint32_t seq = ++ctx->mbox_seq;
+  SK_LAUNCH(k_post_words, 1, 32, 0, ctx->stream, s, ctx->mbox_dev, seq);
+  mbox_wait(ctx, seq);
+  return ctx->mbox + kMboxHdr;
+}
+
 namespace {
 std::mutex g_attr_mu;
 std::map<std::pair<const void*, int>, int> g_attr;                        // smem bytes set
@@ -266,6 +312,10 @@ extern "C" sk_status sk_ctx_create(int device, sk_ctx** out) {
     SK_CUDA(cudaMalloc(&c->d_u64, 64 * sizeof(uint64_t)));
     SK_CUDA(cudaMemset(c->d_u64, 0, 64 * sizeof(uint64_t)));
     SK_CUDA(cudaMallocHost(&c->h_u64, 64 * sizeof(uint64_t)));
+    SK_CUDA(cudaHostAlloc(&c->mbox, (kMboxHdr + kMboxWords) * sizeof(uint32_t),
+                          cudaHostAllocMapped));
+    std::memset(c->mbox, 0, (kMboxHdr + kMboxWords) * sizeof(uint32_t));
+    SK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->mbox_dev), c->mbox, 0));
     *out = c;
   });
 }
@@ -278,6 +328,7 @@ extern "C" sk_status sk_ctx_destroy(sk_ctx* ctx) {
     cudaFree(ctx->d_err);
     cudaFree(ctx->d_u64);
     cudaFreeHost(ctx->h_u64);
+    cudaFreeHost(ctx->mbox);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->watch)
       if (e) cudaEventDestroy(e);

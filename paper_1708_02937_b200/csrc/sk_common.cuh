@@ -99,6 +99,12 @@ struct sk_ctx {
   int* d_err = nullptr;      // device error word (0 = ok)
   uint64_t* d_u64 = nullptr; // small device scratch for counters/flags (64 slots)
   uint64_t* h_u64 = nullptr; // pinned mirror of d_u64
+  // Mailbox: mapped pinned host memory a one-warp kernel posts a few words into
+  // (word 0 = sequence flag, payload from word kMboxHdr); the host polls the flag
+  // instead of issuing device->host copies + a stream synchronise (see Fetch).
+  uint32_t* mbox = nullptr;    // host address
+  uint32_t* mbox_dev = nullptr;  // the same memory as the device sees it
+  uint32_t mbox_seq = 0;
   // Optional per-layer timing of the dominant kernel (CUDA events recorded on
   // this stream around each layer's SpGEMM launch); see sk_ctx_set_timing.
   bool timing = false;
@@ -269,6 +275,32 @@ inline int occupancy(sk_ctx* ctx, K* kernel, int threads, size_t smem) {
 // Reads and clears the context's device error word (synchronising).
 void check_device_error(sk_ctx* ctx, const char* op);
 void sync(sk_ctx* ctx);
+
+// Small device results read back through the context's mailbox.  A bulk
+// host->device copy in flight on another stream delays every small
+// device->host cudaMemcpyAsync by tens of microseconds each (measured with
+// tools/micro/copy_interference.py: four 4-byte copies + a synchronise 36 -> 147 us
+// beside a 32 MB upload), and cudaStreamSynchronize itself by ~20 us; a store into
+// mapped host memory followed by a polled flag is not.  Stream-ordered like the
+// copies it replaces: the post kernel runs after everything queued before it.
+constexpr uint32_t kMboxHdr = 16;        // payload offset (words)
+constexpr uint32_t kMboxWords = 1 << 15; // payload capacity (words)
+struct PostSrc {
+  const uint32_t* p[8];
+  uint32_t n[8];
+  int cnt;
+};
+struct Fetch {
+  sk_ctx* ctx;
+  PostSrc s;
+  explicit Fetch(sk_ctx* c) : ctx(c) { s.cnt = 0; }
+  Fetch& add(const void* dev, uint32_t words);
+  // launches the post kernel, waits for it, returns the payload (words in add()
+  // order; valid until the context's next fetch)
+  const uint32_t* run();
+};
+// waits until the mailbox flag shows `seq` (a failed stream raises instead of spinning)
+void mbox_wait(sk_ctx* ctx, uint32_t seq);
 // Record a timing event pair slot (no-op unless ctx->timing); the opening
 // mark of a pair carries the kernel's SK_KT_* tag.
 void timing_mark(sk_ctx* ctx, int tag = SK_KT_OTHER);
