@@ -157,8 +157,11 @@ sk_status sk_ctx_set_density_switch(sk_ctx* ctx, double dense_above, double spar
  *   exact_layout   the stream kernel's view of Y: 1 a padded copy (rows
  *                  16-byte aligned); 2 its own column array where that is
  *                  16-byte aligned (a pass table and two side units per row are
- *                  built; else the copy); 0 = 2 for rows of > 96 entries on
- *                  average, else 1 */
+ *                  built; else the copy); 3 the padded copy with every pass
+ *                  slice's entries in accumulator-bank order (<= 8 passes, else
+ *                  1; fewer shared-memory bank conflicts in the counter
+ *                  atomics, measured not worth the sort: DESIGN.md K7);
+ *                  0 = 2 for rows of > 96 entries on average, else 1 */
 typedef struct sk_tuning {
   int exact;
   int exact_kernel;

@@ -560,6 +560,100 @@ __global__ void k_pad_passes(const uint32_t* __restrict__ rp, const uint32_t* __
   if (blockIdx.x == 0 && threadIdx.x == 0) wpc[size_t(rows) * nP] = 4 * rows + (rp[rows] & ~3u);
 }
 
+// The padded copy with every pass slice in BANK ORDER (<= 8 passes).  K7 counts
+// order-free, so the entries of a slice may come in any order; its lanes take
+// consecutive 16-byte units of a slice, and the accumulator word of sample s is
+// s mod 2^FL -- bank s mod 32.  With a slice sorted by (s + 13 k) mod 32 (k the
+// row: the rotation decorrelates the slices that share a 32-unit step), the
+// j-th entries of neighbouring units fall into different banks: an ATOMS.ADD
+// then meets the 2-3 slices of its step, not 32 random banks
+// (tools/micro/atoms_vs_red.cu: 3.6 cycles per instruction at random words,
+// 1.7 conflict-free).  Warp per row: a shared-memory histogram over
+// (pass, bank), its exclusive scan (also the pass table), then a counting-sort
+// scatter; the order inside a bank is whatever the atomics give.
+template <int kC>
+__global__ void __launch_bounds__(256) k_pad_banked(const uint32_t* __restrict__ rp,
+                                                    const uint32_t* __restrict__ ci,
+                                                    uint32_t rows, uint32_t nP, int sh,
+                                                    uint32_t* __restrict__ pci,
+                                                    uint32_t* __restrict__ wpc) {
+  __shared__ uint32_t hist_all[8][256];
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* const hist = hist_all[threadIdx.x >> 5];
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  auto bounds = [&](uint32_t k, uint32_t& b, uint32_t& e) {
+    b = e = 0;
+    if (k < rows) {
+      b = __ldg(rp + k);
+      e = __ldg(rp + k + 1);
+    }
+  };
+  auto chunk = [&](uint32_t e0, uint32_t re, uint32_t (&sv)[kC]) {
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+      const uint32_t e = e0 + 32 * u + lane;
+      sv[u] = e < re ? __ldg(ci + e) : 0xFFFFFFFFu;
+    }
+  };
+  uint32_t rb, re, nb, ne;
+  bounds(gw, rb, re);
+  bounds(gw + nw, nb, ne);
+  uint32_t sv[kC];
+  chunk(rb, re, sv);
+  for (uint32_t k = gw; k < rows; k += nw) {
+    uint32_t nnb, nne, svn[kC];
+    bounds(k + 2 * nw, nnb, nne);
+    chunk(nb, ne, svn);  // the next row's first chunk, in flight over this row's sort
+    const uint32_t pb = 4 * k + (rb & ~3u), pn = 4 * (k + 1) + (re & ~3u);
+    const uint32_t rot = 13u * k;
+    auto key = [&](uint32_t s) { return ((s >> sh) << 5) | ((s + rot) & 31u); };
+    *reinterpret_cast<uint4*>(hist + 8 * lane) = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(hist + 8 * lane + 4) = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
+    const bool one = re - rb <= 32 * kC;  // the whole row is in registers
+    for (uint32_t e0 = rb; e0 < re; e0 += 32 * kC) {
+      if (e0 != rb) chunk(e0, re, sv);
+#pragma unroll
+      for (int u = 0; u < kC; ++u)
+        if (e0 + 32 * u + lane < re) atomicAdd(hist + key(sv[u]), 1u);
+    }
+    __syncwarp();
+    // exclusive scan of the 256 counters: 8 consecutive per lane (4 lanes per pass)
+    uint32_t c[8], tot = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = hist[8 * lane + j];
+      tot += c[j];
+    }
+    uint32_t run = incl_scan(tot, int(lane)) - tot;
+    if ((lane & 3u) == 0 && (lane >> 2) < nP) wpc[size_t(k) * nP + (lane >> 2)] = pb + run;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hist[8 * lane + j] = run;
+      run += c[j];
+    }
+    __syncwarp();
+    uint32_t* const dst = pci + pb;
+    for (uint32_t e0 = rb; e0 < re; e0 += 32 * kC) {
+      if (!one) chunk(e0, re, sv);
+#pragma unroll
+      for (int u = 0; u < kC; ++u)
+        if (e0 + 32 * u + lane < re) dst[atomicAdd(hist + key(sv[u]), 1u)] = sv[u];
+    }
+    __syncwarp();
+    const uint32_t gend = k + 1 == rows ? pn + 8 : pn;
+    for (uint32_t t = pb + (re - rb) + lane; t < gend; t += 32) pci[t] = 0xFFFFFFE0u | (t & 31u);
+    rb = nb;
+    re = ne;
+    nb = nnb;
+    ne = nne;
+#pragma unroll
+    for (int u = 0; u < kC; ++u) sv[u] = svn[u];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) wpc[size_t(rows) * nP] = 4 * rows + (rp[rows] & ~3u);
+}
+
 // The padded copy for short rows (mean <= 96 entries, <= 64 passes): a warp
 // takes 32 consecutive rows (their row pointers in one coalesced load), then
 // kB rows at a time with all their first 64 entries loaded before any is
@@ -732,6 +826,17 @@ const void* stream_kernel(int fl, int ns, int fb, int ku) {
 }
 
 size_t padded_size(uint32_t rows, size_t nnz) { return 4 * size_t(rows) + (nnz & ~size_t(3)) + 8; }
+
+void launch_pad_banked(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
+                       uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc, bool short_rows) {
+  if (nP > 8) fail(SK_ERR_INVALID_ARGUMENT, "bank-ordered padded copy: at most 8 passes");
+  const unsigned blocks = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((uint64_t(rows) + 7) / 8, uint64_t(ctx->num_sms) * 8)));
+  if (short_rows)
+    SK_LAUNCH(k_pad_banked<2>, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
+  else
+    SK_LAUNCH(k_pad_banked<8>, blocks, 256, 0, ctx->stream, rp, ci, rows, nP, sh, pci, wpc);
+}
 
 void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
                        uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc, bool short_rows) {

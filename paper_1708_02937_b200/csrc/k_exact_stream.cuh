@@ -50,6 +50,10 @@ size_t padded_size(uint32_t rows, size_t nnz);
 // short_rows: the mean row holds <= 96 entries (narrower chunks per warp)
 void launch_pad_passes(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
                        uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc, bool short_rows);
+// The same padded copy with every pass slice's entries in bank order ((sample +
+// 13 row) mod 32; <= 8 passes): K7's counter atomics meet fewer bank conflicts.
+void launch_pad_banked(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,
+                       uint32_t nP, int sh, uint32_t* pci, uint32_t* wpc, bool short_rows);
 // The pass table of an activation CSR read in place (16-byte aligned column
 // array, nnz < 2^30) and the rows' side units (2 * rows 16-byte units).
 void launch_pass_table(sk_ctx* ctx, const uint32_t* rp, const uint32_t* ci, uint32_t rows,

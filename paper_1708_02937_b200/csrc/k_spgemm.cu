@@ -2451,10 +2451,13 @@ static sk_csr* exact_layer_w(sk_ctx* ctx, const ExactLayerIn& L_, const sk_csr* 
     if (!direct) {
       uint32_t* pci = aalloc<uint32_t>(ctx, padded_size(y0->rows, y0->nnz));
       host_prof_mark(1);
-      launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps, erow0 <= 96.0);
+      if (lay == 3 && gs.nW <= 8)
+        launch_pad_banked(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps, erow0 <= 96.0);
+      else
+        launch_pad_passes(ctx, y0->rp, y0->ci, y0->rows, gs.nW, gs.sh, pci, wps, erow0 <= 96.0);
       bci = pci;
     }
-    ctx->last_exact.layout = direct ? 0 : 1;
+    ctx->last_exact.layout = direct ? 0 : (lay == 3 && gs.nW <= 8) ? 3 : 1;
     const int ns = std::max(1, (L_.wstats.maxdeg + 31) / 32);  // in-edge slots per lane
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_u64);
     auto clamp_cap = [&](unsigned long long c, unsigned long long mem_cap) {

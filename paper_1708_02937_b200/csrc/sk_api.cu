@@ -387,8 +387,8 @@ extern "C" sk_status sk_ctx_set_tuning(sk_ctx* ctx, const sk_tuning* t) {
       fail(SK_ERR_INVALID_ARGUMENT, "tuning: window log2 must be 0 or 8..12");
     if (!in(t->exact_fields, {0, 4, 8}))
       fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_fields must be 0, 4 or 8");
-    if (!in(t->exact_layout, {0, 1, 2}))
-      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_layout must be 0, 1 or 2");
+    if (!in(t->exact_layout, {0, 1, 2, 3}))
+      fail(SK_ERR_INVALID_ARGUMENT, "tuning: exact_layout must be 0, 1, 2 or 3");
     if (!(t->esc_ratio == t->esc_ratio))
       fail(SK_ERR_INVALID_ARGUMENT, "tuning: esc_ratio is NaN");
     ctx->tune = *t;

@@ -233,7 +233,7 @@ class Context:
                            4: "flat", 5: "stream"}[e.kernel],
                 "group": e.group, "records": e.records, "window_log2": e.window_log2,
                 "fields": e.fields, "wraps": e.wraps,
-                "layout": {0: "direct", 1: "padded"}[e.layout]}
+                "layout": {0: "direct", 1: "padded", 3: "banked"}[e.layout]}
 
     def set_stream(self, stream_ptr: int | None):
         _check(self._L.sk_ctx_set_stream(self.h, vp(stream_ptr) if stream_ptr else None))

@@ -1002,7 +1002,7 @@ STREAM_CASES = [
 ]
 
 
-@pytest.mark.parametrize("layout", [2, 1])
+@pytest.mark.parametrize("layout", [2, 1, 3])
 @pytest.mark.parametrize("case", STREAM_CASES)
 def test_stream_kernel_regimes(sk, port, case, layout):
     """K7 (k_exact_stream, the order-free row stream) against the oracle's sparse
@@ -1011,7 +1011,8 @@ def test_stream_kernel_regimes(sk, port, case, layout):
     (the layer is rerun with 8-bit ones), in-degrees up to 96 (one to three
     in-edge slots per lane, rows with none), a batch narrower than one pass,
     passes that end past the batch, the touched-word clear of sparse passes --
-    each with Y read in place (layout 2) and through the padded copy (1)."""
+    each with Y read in place (layout 2), through the padded copy (1) and through
+    the padded copy with bank-ordered pass slices (3: <= 8 passes, else 1)."""
     m, n, kY, bias, clip, maxdeg, fields = case
     hW = _in_degree_weights(m, maxdeg, m + n)
     hY = port.gen_input_binary(m, n, kY, 7)
@@ -1032,7 +1033,7 @@ def test_stream_kernel_regimes(sk, port, case, layout):
         ctx.set_tuning(**old)
         ctx.set_density_switch()
     assert ctx.layer_paths(1) == ["exact"] and info["kernel"] == "stream", info
-    assert info["layout"] == {2: "direct", 1: "padded"}[layout], info
+    assert info["layout"] in {2: ("direct",), 1: ("padded",), 3: ("banked", "padded")}[layout], info
     assert list(trace) == [hY.nnz, want.nnz]
     assert_csr_bitwise(out, want)
     if fields == 8 or bias == -0.5:
