@@ -54,8 +54,16 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
   const uint64_t tasks = uint64_t(chunks) * m;
   for (uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; task < tasks;
        task += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-    const uint32_t c = uint32_t(task / m);  // chunk-major: the live Y panel stays in L2
-    const uint32_t i = uint32_t(task - uint64_t(c) * m);
+    // chunk-major: the live Y panel stays in L2 (a 32-bit divide where the
+    // task count allows: the 64-bit one is ~100 instructions per task)
+    uint32_t c, i;
+    if (tasks <= 0xFFFFFFFFull) {
+      c = uint32_t(task) / m;
+      i = uint32_t(task) - c * m;
+    } else {
+      c = uint32_t(task / m);
+      i = uint32_t(task - uint64_t(c) * m);
+    }
     float acc[kU][4];
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -287,15 +295,34 @@ struct DenseEngineArgs {
   int* layers_done;                // written when stopping early
 };
 
-template <bool kVec4>
-__global__ void __launch_bounds__(256, SK_SPMM_MINB) k_dense_engine(DenseEngineArgs p) {
+// kU = 2 (wide batches, n >= 1024): a task is a row x 256 columns, so the (k, w)
+// broadcasts, the row address and the loop overhead of an in-edge are paid once
+// per two 16-byte loads (the saturated cfg3 layer ran ~36 instructions per
+// in-edge and 128 columns, 8 of them the multiply-adds), and 4 in-edges x 2
+// loads are in flight per lane at 3 blocks per SM.  Measured per saturated
+// 16384 x 60000 layer (tools/prof_dense.py): 17.5 -> 15.0 ms; kU = 4 x batch 2
+// 15.2, kU = 2 x batch 8 at 2 blocks 14.7 (15000 samples: 3.4 against 3.3),
+// batch 2 at 4 blocks 16.2; L1::no_allocate loads 20.0 and an L2 bulk prefetch
+// of the next column panel 16.7 -- both slower, removed.
+#ifndef SK_ENG_KU
+#define SK_ENG_KU 2
+#endif
+#ifndef SK_ENG_BATCH
+#define SK_ENG_BATCH 4
+#endif
+#ifndef SK_ENG_MINB
+#define SK_ENG_MINB 3
+#endif
+template <bool kVec4, int kU = 1>
+__global__ void __launch_bounds__(256, kU == 1 ? SK_SPMM_MINB : SK_ENG_MINB)
+    k_dense_engine(DenseEngineArgs p) {
   cg::grid_group grid = cg::this_grid();
   for (uint32_t k = 0; k < p.L; ++k) {
     const float* src = k == 0 ? p.y0 : (((k - 1) & 1) ? p.buf[1] : p.buf[0]);
     float* dst = (k & 1) ? p.buf[1] : p.buf[0];
-    spmm_tasks<OpArith, kEpiLayer, kVec4>(p.w_rp[k], p.w_ci[k], p.w_v[k], p.bias + size_t(k) * p.m,
-                                          src, p.m, p.n, p.clip, dst, p.err,
-                                          p.nnz ? p.nnz + k : nullptr);
+    spmm_tasks<OpArith, kEpiLayer, kVec4, kU, (kU == 1 ? SK_SPMM_BATCH : SK_ENG_BATCH)>(
+        p.w_rp[k], p.w_ci[k], p.w_v[k], p.bias + size_t(k) * p.m, src, p.m, p.n, p.clip, dst,
+        p.err, p.nnz ? p.nnz + k : nullptr);
     if (k + 1 < p.L) {
       grid.sync();
       if (p.stop_below && *(volatile unsigned long long*)(p.nnz + k) < p.stop_below) {
@@ -850,9 +877,12 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
     return;
   }
   const bool vec = (n % 4) == 0;
-  const void* fn = vec ? (const void*)k_dense_engine<true> : (const void*)k_dense_engine<false>;
+  const bool wide = vec && n >= 1024 && SK_ENG_KU > 1;
+  const void* fn = wide ? (const void*)k_dense_engine<true, SK_ENG_KU>
+                   : vec ? (const void*)k_dense_engine<true> : (const void*)k_dense_engine<false>;
   const int per_sm = kernel_occupancy(ctx, fn, 256, 0);  // cached per device
-  const uint64_t warps = uint64_t((n + 127) / 128) * m;
+  const uint32_t tcols = wide ? 128u * SK_ENG_KU : 128u;
+  const uint64_t warps = uint64_t((n + tcols - 1) / tcols) * m;
   const unsigned grid = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>((warps + 7) / 8, uint64_t(ctx->num_sms) * std::max(per_sm, 1))));
   void* args[] = {&p};

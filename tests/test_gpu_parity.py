@@ -255,6 +255,37 @@ def test_layer_step_matches_reference_on_odd_shapes(sk, ref, port):
         assert np.array_equal(bits(got), bits(port.layer_dense(W, b, y, 0.75))), (m, n)
 
 
+@pytest.mark.parametrize("m,n", [(300, 1024), (257, 1500), (64, 2052)])
+def test_wide_batch_forward_matches_reference(sk, ref, port, m, n):
+    """The dense engine's wide-batch variant (n >= 1024: a task is a row x 256
+    columns, two 16-byte loads per in-edge and lane) against the reference's
+    relu_forward (dnn.cpp:86-121 over matrix.cpp:403-424): rows of 0..70 stored
+    entries (more than one 32-entry batch, leftovers of every size), a ragged
+    last chunk (1500 = 5 x 256 + 220, 2052 = 8 x 256 + 4), three layers; and one
+    clipped layer against the restated epilogue."""
+    rng = np.random.default_rng(m + n)
+    Ws, bs = [], []
+    for k in range(3):
+        lens = rng.integers(0, 71, size=m)
+        lens[::13] = 0
+        lens = np.minimum(lens, m)
+        rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+        ci = np.concatenate([np.sort(rng.choice(m, size=int(c), replace=False)) for c in lens]
+                            + [np.zeros(0, np.int64)]).astype(np.uint32)
+        v = rng.uniform(-1, 1, len(ci)).astype(np.float32)
+        Ws.append(hcsr(m, m, rp, ci, v))
+        bs.append(rng.uniform(-0.2, 0.2, m).astype(np.float32))
+    y0 = rng.uniform(0, 1, (m, n)).astype(np.float32)
+    y0[rng.random((m, n)) < 0.3] = 0.0
+    model = sk.DnnModel([dev_csr(sk, w) for w in Ws], bs)
+    got = sk.relu_forward(model, sk.DenseMatrix.from_numpy(y0)).numpy()
+    assert np.array_equal(bits(got), bits(ref.relu_forward(Ws, bs, y0, workers=2)))
+    clipped = sk.relu_forward(sk.DnnModel([dev_csr(sk, Ws[0])] * 2, bs[:2]),
+                              sk.DenseMatrix.from_numpy(y0), sk.ForwardOptions(clip=0.5)).numpy()
+    want = port.layer_dense(Ws[0], bs[1], port.layer_dense(Ws[0], bs[0], y0, 0.5), 0.5)
+    assert np.array_equal(bits(clipped), bits(want))
+
+
 @pytest.mark.parametrize("m,n,inv", [(2048, 64, 1.0), (512, 64, 4.0), (700, 4, 2.0),
                                      (300, 12, 1.0), (1000, 36, 16.0), (64, 8, 1.0),
                                      (1024, 7, 1.0), (4096, 33, 2.0), (333, 64, 1.0)])
