@@ -160,6 +160,17 @@ __global__ void __launch_bounds__(256, SK_SPMM_MINB)
   spmm_tasks<Ops, kEpi, kVec4, kU>(rp, ci, wv, bias, y, m, n, clip, out, err);
 }
 
+// Wide batches, rows of more than 16 entries: the engine's wide task (a row x
+// 256 columns, 4 in-edges x 2 loads in flight per lane, 3 blocks per SM).
+template <typename Ops, int kEpi>
+__global__ void __launch_bounds__(256, 3)
+    k_spmm_rows_wide(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                     const float* __restrict__ wv, const float* __restrict__ bias,
+                     const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
+                     float* __restrict__ out, int* err) {
+  spmm_tasks<Ops, kEpi, true, 2, 4>(rp, ci, wv, bias, y, m, n, clip, out, err);
+}
+
 // Narrow activations (n <= 64, n % 4 == 0): a group of G = n/4 lanes (rounded
 // up to a power of two) owns one row and a lane owns 4 columns, so a warp
 // folds 32/G rows at once instead of leaving 32 - n/4 lanes idle; every lane
@@ -892,6 +903,9 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
   timing_mark(ctx);
 }
 
+#ifndef SK_ROWS_WIDE_MIN
+#define SK_ROWS_WIDE_MIN 1024
+#endif
 void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const float* y,
                         uint32_t n, float clip, float* out) {
   if (w->rows == 0 || n == 0) return;
@@ -906,6 +920,9 @@ void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const
   const bool light = vec && n >= 512 && w->nnz <= size_t(16) * w->rows;
   if (light)
     SK_LAUNCH((k_spmm_rows<OpArith, kEpiLayer, true, 4>), spmm_grid(ctx, w->rows, n, 4), 256, 0,
+              ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n, clip, out, ctx->d_err);
+  else if (vec && n >= SK_ROWS_WIDE_MIN)
+    SK_LAUNCH((k_spmm_rows_wide<OpArith, kEpiLayer>), spmm_grid(ctx, w->rows, n, 2), 256, 0,
               ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n, clip, out, ctx->d_err);
   else if (vec)
     SK_LAUNCH((k_spmm_rows<OpArith, kEpiLayer, true>), spmm_grid(ctx, w->rows, n), 256, 0,
@@ -925,7 +942,10 @@ void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b, uint32_t
   dispatch_semiring(s, [&](auto ops) {
     using Ops = decltype(ops);
     if (launch_narrow<Ops, kEpiNone>(ctx, a, nullptr, b, n, 0.0f, out)) return;
-    if (n % 4 == 0)
+    if (n % 4 == 0 && n >= SK_ROWS_WIDE_MIN && a->nnz > size_t(16) * a->rows)
+      SK_LAUNCH((k_spmm_rows_wide<Ops, kEpiNone>), spmm_grid(ctx, a->rows, n, 2), 256, 0,
+                ctx->stream, a->rp, a->ci, a->v, nullptr, b, a->rows, n, 0.0f, out, ctx->d_err);
+    else if (n % 4 == 0)
       SK_LAUNCH((k_spmm_rows<Ops, kEpiNone, true>), spmm_grid(ctx, a->rows, n), 256, 0,
                 ctx->stream, a->rp, a->ci, a->v, nullptr, b, a->rows, n, 0.0f, out, ctx->d_err);
     else

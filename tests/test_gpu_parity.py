@@ -364,6 +364,23 @@ def rand_csr(rng, rows, cols, density, kind):
     return hcsr(rows, cols, rp, ci, vals[mask])
 
 
+def test_mxm_wide_batch_all_semirings_match_reference(sk, ref):
+    """mxm(CsrMatrix, DenseMatrix) at n >= 1024 with rows of more than 16 entries
+    takes the wide row kernel (a row x 256 columns per task) under every
+    semiring: bitwise against the reference (matrix.cpp:403-424), ragged last
+    chunk (1028 = 4 x 256 + 4)."""
+    rng = np.random.default_rng(29)
+    for kind in SEMIRINGS:
+        s = getattr(sk, {"arithmetic": "arithmetic_semiring", "max_plus": "max_plus_semiring",
+                         "min_max": "min_max_semiring", "gf2": "gf2_semiring"}[kind])()
+        a = rand_csr(rng, 37, 90, 0.5, kind)
+        assert a.nnz > 16 * 37
+        b = rand_csr(rng, 90, 1028, 0.6, kind)
+        bd = ref.to_dense(b, s.zero)
+        got = sk.mxm(dev_csr(sk, a), sk.DenseMatrix.from_numpy(bd), s).numpy()
+        assert np.array_equal(bits(got), bits(ref.mxm_csr_dense(a, bd, kind))), kind
+
+
 def test_mxm_all_semirings_match_reference(sk, ref):
     rng = np.random.default_rng(13)
     for kind in SEMIRINGS:
