@@ -469,6 +469,20 @@ def run_sustained(sk, ctx, stream, R, args, pk, b0, Bl, Bg):
     fma_peak = ctx_fma_peak(sk)
     edges = edges_per_inference(w, Bg)
     useful = useful_products(tr, paths, w["m"], Bl, nnzW, None)
+    # per-layer DRAM traffic of the engine from the committed ncu capture (one
+    # saturated 60000-sample layer), scaled to this rank's batch
+    tb, trep, _ = measured_traffic("cfg3_saturated_wide")
+    if tb is not None:
+        tb = int(tb * Bl / 60000)
+    sustained_extra = {
+        "traffic_per_layer": tb, "traffic_source": trep,
+        "algorithmic_bytes_per_layer": dense_layer_bytes(Bl, w["m"], nnzW[0]),
+        "l2_to_sm_gbs": 4.0 * macs / (dense_ms / 1e3) / 1e9 if dense_ms > 0 else 0.0,
+        "measured_limiter": "latency of gathered 512-byte activation segments from L2 (4 B per "
+                            "MAC, no on-chip reuse for a random W): L2 35 %, L1/TEX 47 %, issue "
+                            "52 % busy, 40 % of cycles no eligible warp "
+                            "(profiles/r02/engine_wide_b60000_brief.txt)",
+    }
     return {
         "workload": w["desc"], "value": edges / (ms / 1e3), "unit": "edges/s",
         "ms_per_step": ms, "steps": steps, "warmup": 3,
@@ -485,7 +499,8 @@ def run_sustained(sk, ctx, stream, R, args, pk, b0, Bl, Bg):
                      "fp32_frac": (macs / (dense_ms / 1e3)) / fma_peak if dense_ms > 0 else 0.0,
                      "fp32_peak_macs_per_s": fma_peak,
                      "fp32_note": "non-fused mul + add (bitwise parity): 2 FP32 pipe ops per "
-                                  "MAC; peak = SMs x 128 lanes x max SM clock / 2"},
+                                  "MAC; peak = SMs x 128 lanes x max SM clock / 2",
+                     **sustained_extra},
     }
 
 
