@@ -151,6 +151,168 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
   }
 }
 
+// ---- K1b: the wide task with its activation segments staged through shared memory -----
+// The register-staged wide task waits on its gathered loads with no unit busy
+// (ncu: L2 36 %, 40 % of cycles without an eligible warp): what a warp keeps in
+// flight is bounded by its registers (4 in-edges x 2 x 16 bytes per lane).  Here
+// a lane copies its two 16-byte pieces of every in-edge's 1 KB segment (256
+// columns of row k of Y) with cp.async into a warp-private ring of kS stages
+// and reads back exactly the bytes it copied, so the pipeline is lane-local: one
+// commit group per in-edge, cp.async.wait_group kS - 1 before the fold, no
+// barrier and no cross-lane visibility to wait for; kS KB per warp are in flight
+// whatever the register budget.  (The bulk-copy engine, one cp.async.bulk per
+// segment on an mbarrier ring, measured 43 ms per saturated layer against 15:
+// ~100 cycles per 1 KB copy and SM.)  n % 4 == 0 (16-byte aligned segments).
+#ifndef SK_BULK_STAGES
+#define SK_BULK_STAGES 8
+#endif
+namespace bulk {
+constexpr int kS = SK_BULK_STAGES;
+constexpr int kWarps = 8;
+constexpr size_t kSmem = size_t(kWarps) * kS * 1024;
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void wait_pending() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace bulk
+
+template <typename Ops, int kEpi>
+__device__ __forceinline__ void spmm_tasks_bulk(const uint32_t* __restrict__ rp,
+                                                const uint32_t* __restrict__ ci,
+                                                const float* __restrict__ wv,
+                                                const float* __restrict__ bias,
+                                                const float* __restrict__ y, uint32_t m,
+                                                uint32_t n, float clip, float* __restrict__ out,
+                                                int* err, unsigned long long* nz_count,
+                                                uint8_t* smem, bool src_blk = false,
+                                                bool dst_blk = false,
+                                                unsigned long long* work = nullptr) {
+  // work (a zeroed counter): tasks are claimed in order, one ahead, instead of
+  // strided statically.  A column panel is only m / (warps in flight) ~ 5 tasks
+  // per warp, so statically strided warps drift panels apart within a layer
+  // and the L2 stops holding "the" panel: ncu measured 351 GB of DRAM reads for
+  // 15.7 GB of activations on four saturated 16384 x 60000 layers (5.8 TB/s:
+  // DRAM-bound), 34 GB for 3.9 GB at 15000 samples.  Claimed in order, the
+  // tasks in flight are always ~3500 consecutive rows of one panel.
+  // src_blk / dst_blk: the activations in PANEL-MAJOR layout -- element (row r,
+  // column j) at ((j / 256) * m + r) * 256 + j % 256 -- so the 256-column panel
+  // a task sweep gathers from is one contiguous m KB instead of m segments a row
+  // pitch apart (16384 x 60000: 3.9 GB spanned per panel, and the gathers' rate
+  // fell from 12.8 to 8.8 TB/s between 15000 and 60000 samples).  Square layers
+  // only (Y has m rows); the engine keeps its intermediate activations this way.
+  using namespace bulk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // this lane's 16 bytes of the two halves of every stage
+  const float* const mine = reinterpret_cast<const float*>(smem + size_t(warp) * kS * 1024) + lane * 4;
+  const uint32_t mine_s = async::smem_u32(mine);
+  uint32_t nz = 0;
+  const uint32_t chunks = (n + 255) / 256;
+  const uint64_t tasks = uint64_t(chunks) * m;
+  const uint64_t stride = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (work) {
+    if (lane == 0) task = atomicAdd(work, 1ull);
+    task = __shfl_sync(0xffffffffu, task, 0);
+  }
+  while (task < tasks) {
+    unsigned long long claimed = 0;
+    if (work && lane == 0) claimed = atomicAdd(work, 1ull);  // consumed after this task
+    uint32_t c, i;
+    if (tasks <= 0xFFFFFFFFull) {
+      c = uint32_t(task) / m;
+      i = uint32_t(task) - c * m;
+    } else {
+      c = uint32_t(task / m);
+      i = uint32_t(task - uint64_t(c) * m);
+    }
+    const uint32_t col0 = c * 256 + lane * 4;
+    const bool in0 = col0 < n, in1 = col0 + 128 < n;  // the last chunk may be ragged
+    float acc[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[u][q] = Ops::zero();
+    const uint32_t eb = rp[i], ee = rp[i + 1];
+    for (uint32_t e0 = eb; e0 < ee; e0 += 32) {
+      const uint32_t cnt = min(32u, ee - e0);
+      uint32_t kk = 0;
+      float aa = 0.0f;
+      if (uint32_t(lane) < cnt) {
+        kk = ci[e0 + lane];
+        aa = wv[e0 + lane];
+      }
+      auto issue = [&](uint32_t t) {  // in-edge t of the group into stage t % kS
+        if (t < cnt) {
+          const uint32_t k = __shfl_sync(0xffffffffu, kk, t & 31);
+          const float* src = src_blk ? y + (size_t(c) * m + k) * 256 + lane * 4
+                                     : y + size_t(k) * n + col0;
+          const uint32_t dst = mine_s + (t % kS) * 1024;
+          if (in0) cp16(dst, src);
+          if (in1) cp16(dst + 512, src + 128);
+        }
+        commit();  // one group per step, empty past the end: the wait count stays fixed
+      };
+#pragma unroll
+      for (int j = 0; j < kS; ++j) issue(j);
+      for (uint32_t t = 0; t < cnt; ++t) {
+        wait_pending<kS - 1>();
+        const float* const seg = mine + (t % kS) * 256;
+        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+        if (in0) v0 = *reinterpret_cast<const float4*>(seg);
+        if (in1) v1 = *reinterpret_cast<const float4*>(seg + 128);
+        const float a = __shfl_sync(0xffffffffu, aa, t);
+        acc[0][0] = Ops::add(acc[0][0], Ops::mul(a, v0.x, err), err);
+        acc[0][1] = Ops::add(acc[0][1], Ops::mul(a, v0.y, err), err);
+        acc[0][2] = Ops::add(acc[0][2], Ops::mul(a, v0.z, err), err);
+        acc[0][3] = Ops::add(acc[0][3], Ops::mul(a, v0.w, err), err);
+        acc[1][0] = Ops::add(acc[1][0], Ops::mul(a, v1.x, err), err);
+        acc[1][1] = Ops::add(acc[1][1], Ops::mul(a, v1.y, err), err);
+        acc[1][2] = Ops::add(acc[1][2], Ops::mul(a, v1.z, err), err);
+        acc[1][3] = Ops::add(acc[1][3], Ops::mul(a, v1.w, err), err);
+        issue(t + kS);  // refills the stage just read (the values are in registers)
+      }
+    }
+    float b = 0.0f;
+    if (kEpi == kEpiLayer) b = bias[i];
+    float* const orow = dst_blk ? out + (size_t(c) * m + i) * 256 - size_t(c) * 256
+                                : out + size_t(i) * n;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t cu = col0 + u * 128;
+      if (kEpi == kEpiLayer)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[u][q] = layer_epilogue(acc[u][q], b, clip);
+      if (nz_count)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nz += (cu + q < n && acc[u][q] != 0.0f) ? 1u : 0u;
+      if (cu < n)
+        *reinterpret_cast<float4*>(orow + cu) =
+            make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+    }
+    task = work ? __shfl_sync(0xffffffffu, claimed, 0) : task + stride;
+  }
+  if (nz_count) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    if (lane == 0 && nz) atomicAdd(nz_count, (unsigned long long)nz);
+  }
+}
+
+template <typename Ops, int kEpi>
+__global__ void __launch_bounds__(256, 3)
+    k_spmm_rows_bulk(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                     const float* __restrict__ wv, const float* __restrict__ bias,
+                     const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
+                     float* __restrict__ out, int* err) {
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  spmm_tasks_bulk<Ops, kEpi>(rp, ci, wv, bias, y, m, n, clip, out, err, nullptr, bulk_smem);
+}
+
 template <typename Ops, int kEpi, bool kVec4, int kU = 1>
 __global__ void __launch_bounds__(256, SK_SPMM_MINB)
     k_spmm_rows(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
@@ -304,6 +466,8 @@ struct DenseEngineArgs {
   unsigned long long* nnz;         // L counters, zeroed (optional)
   unsigned long long stop_below;   // 0 = never stop early
   int* layers_done;                // written when stopping early
+  float* blk[2];                   // K1b: panel-major scratch of the intermediate layers (or null)
+  unsigned long long* work;        // K1b: L zeroed task counters (or null: static striding)
 };
 
 // kU = 2 (wide batches, n >= 1024): a task is a row x 256 columns, so the (k, w)
@@ -324,6 +488,15 @@ struct DenseEngineArgs {
 #ifndef SK_ENG_MINB
 #define SK_ENG_MINB 3
 #endif
+#ifndef SK_ENG_BULK
+#define SK_ENG_BULK 1
+#endif
+#ifndef SK_ENG_BLOCKED
+#define SK_ENG_BLOCKED 1
+#endif
+#ifndef SK_ENG_CLAIM
+#define SK_ENG_CLAIM 1
+#endif
 template <bool kVec4, int kU = 1>
 __global__ void __launch_bounds__(256, kU == 1 ? SK_SPMM_MINB : SK_ENG_MINB)
     k_dense_engine(DenseEngineArgs p) {
@@ -337,6 +510,48 @@ __global__ void __launch_bounds__(256, kU == 1 ? SK_SPMM_MINB : SK_ENG_MINB)
     if (k + 1 < p.L) {
       grid.sync();
       if (p.stop_below && *(volatile unsigned long long*)(p.nnz + k) < p.stop_below) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *p.layers_done = int(k + 1);
+        return;
+      }
+    }
+  }
+}
+
+// The engine over the shared-memory-staged wide task (K1b).  With p.blk the
+// intermediate activations live in panel-major scratch: layer 0 reads the
+// caller's row-major Y_0, the last layer writes the caller's row-major buffer;
+// a density stop after layer k copies that layer's panels back into the
+// row-major buffer the caller expects before the engine returns.
+__global__ void __launch_bounds__(256, 3) k_dense_engine_bulk(DenseEngineArgs p) {
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  cg::grid_group grid = cg::this_grid();
+  const bool blk = p.blk[0] != nullptr;
+  for (uint32_t k = 0; k < p.L; ++k) {
+    const bool last = k + 1 == p.L;
+    const bool sb = blk && k > 0, db = blk && !last;
+    const float* src = k == 0 ? p.y0 : sb ? p.blk[(k - 1) & 1] : p.buf[(k - 1) & 1];
+    float* dst = db ? p.blk[k & 1] : p.buf[k & 1];
+    spmm_tasks_bulk<OpArith, kEpiLayer>(p.w_rp[k], p.w_ci[k], p.w_v[k],
+                                        p.bias + size_t(k) * p.m, src, p.m, p.n, p.clip, dst,
+                                        p.err, p.nnz ? p.nnz + k : nullptr, bulk_smem, sb, db,
+                                        p.work ? p.work + k : nullptr);
+    if (!last) {
+      grid.sync();
+      if (p.stop_below && *(volatile unsigned long long*)(p.nnz + k) < p.stop_below) {
+        if (db) {  // 16-byte units of the panels back to rows
+          const uint32_t chunks = (p.n + 255) / 256;
+          const uint64_t units = uint64_t(chunks) * p.m * 64;
+          for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < units;
+               t += uint64_t(gridDim.x) * blockDim.x) {
+            const uint32_t q = uint32_t(t & 63);
+            const uint64_t cr = t >> 6;  // c * m + row
+            const uint32_t c = uint32_t(cr / p.m), r = uint32_t(cr - uint64_t(c) * p.m);
+            const uint32_t col = c * 256 + q * 4;
+            if (col < p.n)
+              *reinterpret_cast<float4*>(p.buf[k & 1] + size_t(r) * p.n + col) =
+                  *reinterpret_cast<const float4*>(dst + t * 4);
+          }
+        }
         if (blockIdx.x == 0 && threadIdx.x == 0) *p.layers_done = int(k + 1);
         return;
       }
@@ -877,6 +1092,8 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
   p.nnz = nnz;
   p.stop_below = nnz ? stop_below : 0;
   p.layers_done = d_done;
+  p.blk[0] = p.blk[1] = nullptr;
+  p.work = nullptr;
   uint32_t wslice = 0;
   const size_t csmem = (!nnz && k0 == 0 &&
                         uint64_t((n + clu::kCols - 1) / clu::kCols) * clu::kCS <= uint64_t(ctx->num_sms) / 2)
@@ -889,18 +1106,40 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
   }
   const bool vec = (n % 4) == 0;
   const bool wide = vec && n >= 1024 && SK_ENG_KU > 1;
-  const void* fn = wide ? (const void*)k_dense_engine<true, SK_ENG_KU>
+  const bool staged = wide && SK_ENG_BULK != 0;
+  const void* fn = staged ? (const void*)k_dense_engine_bulk
+                   : wide ? (const void*)k_dense_engine<true, SK_ENG_KU>
                    : vec ? (const void*)k_dense_engine<true> : (const void*)k_dense_engine<false>;
-  const int per_sm = kernel_occupancy(ctx, fn, 256, 0);  // cached per device
+  const size_t esmem = staged ? bulk::kSmem : 0;
+  if (staged) smem_attr(ctx, k_dense_engine_bulk, int(bulk::kSmem));
+  // panel-major scratch for the intermediate layers (three layers or more: the
+  // first reads and the last writes the caller's row-major buffers anyway)
+  p.blk[0] = p.blk[1] = nullptr;
+  p.work = nullptr;
+  const bool blocked = staged && p.L >= 3 && SK_ENG_BLOCKED != 0;
+  if (staged) {
+    arena_begin(ctx);
+    if (SK_ENG_CLAIM) {
+      p.work = reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, p.L));
+      SK_CUDA(cudaMemsetAsync(p.work, 0, size_t(p.L) * 8, ctx->stream));
+    }
+  }
+  if (blocked) {
+    const size_t padded = size_t((n + 255) / 256) * 256 * m;
+    p.blk[0] = aalloc<float>(ctx, padded);
+    p.blk[1] = aalloc<float>(ctx, padded);
+  }
+  const int per_sm = kernel_occupancy(ctx, fn, 256, esmem);  // cached per device
   const uint32_t tcols = wide ? 128u * SK_ENG_KU : 128u;
   const uint64_t warps = uint64_t((n + tcols - 1) / tcols) * m;
   const unsigned grid = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>((warps + 7) / 8, uint64_t(ctx->num_sms) * std::max(per_sm, 1))));
   void* args[] = {&p};
   timing_mark(ctx, SK_KT_DENSE_ENGINE);
-  SK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, ctx->stream));
+  SK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, esmem, ctx->stream));
   g_launches.fetch_add(1);
   timing_mark(ctx);
+  if (staged) arena_end(ctx);  // stream-ordered: later arena users queue behind the engine
 }
 
 #ifndef SK_ROWS_WIDE_MIN

@@ -485,10 +485,10 @@ def test_sparse_forward_bitwise_vs_oracle(sk, port, m, n, kY, kW, value, bias, c
     assert_csr_bitwise(out, y)
 
 
-def _rise_and_fall(port, sk):
+def _rise_and_fall(port, sk, n=520):
     """A network whose activation density rises (positive bias) then decays
     (negative bias), so the density-adaptive forward switches both ways."""
-    m, n, seed = 2048, 520, 23
+    m, seed = 2048, 23
     hW = [port.gen_layer_fixed(m, 16, port.layer_seed(seed, k), float("nan")) for k in range(6)]
     bs = [np.full(m, b, np.float32) for b in (0.01, -0.2, -0.6, -0.9, -0.9, -0.9)]
     hY = port.gen_input_binary(m, n, 20, seed)
@@ -531,6 +531,32 @@ def test_density_switch_is_bitwise_neutral(sk, port, mode):
         assert segments == 2
     if mode == "pingpong":
         assert segments >= 3  # sparse -> dense -> sparse
+
+
+@pytest.mark.parametrize("mode", ["all_dense", "pingpong"])
+def test_density_switch_wide_batch(sk, port, mode):
+    """The same rise-and-fall network at 1300 samples (5 x 256 + 20): the dense
+    segments run the staged wide engine (K1b) with its intermediate activations
+    in panel-major scratch -- six layers in one launch (all_dense: the first
+    reads and the last writes row-major buffers), and a density stop mid-way
+    (pingpong: the stopping layer's panels are copied back to rows before the
+    sparse engine takes over); bitwise against the oracle's sparse layers."""
+    model, y0, want, want_trace, full = _rise_and_fall(port, sk, n=1300)
+    dens = np.array(want_trace[1:-1], np.float64) / full
+    ctx = sk.default_context()
+    try:
+        if mode == "all_dense":
+            ctx.set_density_switch(1e-9, 0.0)
+        else:
+            t = float(np.sqrt(dens.max() * max(dens.min(), 1e-9)))
+            ctx.set_density_switch(t, t)
+        out, trace = sk.relu_forward_sparse(model, y0)
+        paths = ctx.layer_paths(6)
+    finally:
+        ctx.set_density_switch()
+    assert list(trace) == want_trace
+    assert_csr_bitwise(out, want)
+    assert paths.count("dense") >= (6 if mode == "all_dense" else 2), paths
 
 
 def test_density_switch_not_taken_with_nonfinite_weights(sk, port):
