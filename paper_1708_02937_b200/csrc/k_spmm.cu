@@ -164,7 +164,10 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
 // segment on an mbarrier ring, measured 43 ms per saturated layer against 15:
 // ~100 cycles per 1 KB copy and SM.)  n % 4 == 0 (16-byte aligned segments).
 #ifndef SK_BULK_STAGES
-#define SK_BULK_STAGES 8
+#define SK_BULK_STAGES 4
+#endif
+#ifndef SK_BULK_MINB
+#define SK_BULK_MINB 4
 #endif
 namespace bulk {
 constexpr int kS = SK_BULK_STAGES;
@@ -246,35 +249,43 @@ __device__ __forceinline__ void spmm_tasks_bulk(const uint32_t* __restrict__ rp,
         kk = ci[e0 + lane];
         aa = wv[e0 + lane];
       }
-      auto issue = [&](uint32_t t) {  // in-edge t of the group into stage t % kS
+      // in-edge t of the group into stage j = t % kS (a compile-time index: the
+      // fold loop is unrolled by kS)
+      auto issue = [&](uint32_t t, int j) {
         if (t < cnt) {
           const uint32_t k = __shfl_sync(0xffffffffu, kk, t & 31);
           const float* src = src_blk ? y + (size_t(c) * m + k) * 256 + lane * 4
                                      : y + size_t(k) * n + col0;
-          const uint32_t dst = mine_s + (t % kS) * 1024;
+          const uint32_t dst = mine_s + j * 1024;
           if (in0) cp16(dst, src);
           if (in1) cp16(dst + 512, src + 128);
         }
         commit();  // one group per step, empty past the end: the wait count stays fixed
       };
 #pragma unroll
-      for (int j = 0; j < kS; ++j) issue(j);
-      for (uint32_t t = 0; t < cnt; ++t) {
-        wait_pending<kS - 1>();
-        const float* const seg = mine + (t % kS) * 256;
-        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-        if (in0) v0 = *reinterpret_cast<const float4*>(seg);
-        if (in1) v1 = *reinterpret_cast<const float4*>(seg + 128);
-        const float a = __shfl_sync(0xffffffffu, aa, t);
-        acc[0][0] = Ops::add(acc[0][0], Ops::mul(a, v0.x, err), err);
-        acc[0][1] = Ops::add(acc[0][1], Ops::mul(a, v0.y, err), err);
-        acc[0][2] = Ops::add(acc[0][2], Ops::mul(a, v0.z, err), err);
-        acc[0][3] = Ops::add(acc[0][3], Ops::mul(a, v0.w, err), err);
-        acc[1][0] = Ops::add(acc[1][0], Ops::mul(a, v1.x, err), err);
-        acc[1][1] = Ops::add(acc[1][1], Ops::mul(a, v1.y, err), err);
-        acc[1][2] = Ops::add(acc[1][2], Ops::mul(a, v1.z, err), err);
-        acc[1][3] = Ops::add(acc[1][3], Ops::mul(a, v1.w, err), err);
-        issue(t + kS);  // refills the stage just read (the values are in registers)
+      for (int j = 0; j < kS; ++j) issue(j, j);
+      for (uint32_t t0 = 0; t0 < cnt; t0 += kS) {
+#pragma unroll
+        for (int j = 0; j < kS; ++j) {
+          const uint32_t t = t0 + j;
+          if (t < cnt) {  // warp-uniform
+            wait_pending<kS - 1>();
+            const float* const seg = mine + j * 256;
+            float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+            if (in0) v0 = *reinterpret_cast<const float4*>(seg);
+            if (in1) v1 = *reinterpret_cast<const float4*>(seg + 128);
+            const float a = __shfl_sync(0xffffffffu, aa, t);
+            acc[0][0] = Ops::add(acc[0][0], Ops::mul(a, v0.x, err), err);
+            acc[0][1] = Ops::add(acc[0][1], Ops::mul(a, v0.y, err), err);
+            acc[0][2] = Ops::add(acc[0][2], Ops::mul(a, v0.z, err), err);
+            acc[0][3] = Ops::add(acc[0][3], Ops::mul(a, v0.w, err), err);
+            acc[1][0] = Ops::add(acc[1][0], Ops::mul(a, v1.x, err), err);
+            acc[1][1] = Ops::add(acc[1][1], Ops::mul(a, v1.y, err), err);
+            acc[1][2] = Ops::add(acc[1][2], Ops::mul(a, v1.z, err), err);
+            acc[1][3] = Ops::add(acc[1][3], Ops::mul(a, v1.w, err), err);
+            issue(t + kS, j);  // refills the stage just read (the values are in registers)
+          }
+        }
       }
     }
     float b = 0.0f;
@@ -304,13 +315,14 @@ __device__ __forceinline__ void spmm_tasks_bulk(const uint32_t* __restrict__ rp,
 }
 
 template <typename Ops, int kEpi>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, SK_BULK_MINB)
     k_spmm_rows_bulk(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                      const float* __restrict__ wv, const float* __restrict__ bias,
                      const float* __restrict__ y, uint32_t m, uint32_t n, float clip,
-                     float* __restrict__ out, int* err) {
+                     float* __restrict__ out, int* err, unsigned long long* work) {
   extern __shared__ __align__(128) uint8_t bulk_smem[];
-  spmm_tasks_bulk<Ops, kEpi>(rp, ci, wv, bias, y, m, n, clip, out, err, nullptr, bulk_smem);
+  spmm_tasks_bulk<Ops, kEpi>(rp, ci, wv, bias, y, m, n, clip, out, err, nullptr, bulk_smem, false,
+                             false, work);
 }
 
 template <typename Ops, int kEpi, bool kVec4, int kU = 1>
@@ -522,7 +534,7 @@ __global__ void __launch_bounds__(256, kU == 1 ? SK_SPMM_MINB : SK_ENG_MINB)
 // caller's row-major Y_0, the last layer writes the caller's row-major buffer;
 // a density stop after layer k copies that layer's panels back into the
 // row-major buffer the caller expects before the engine returns.
-__global__ void __launch_bounds__(256, 3) k_dense_engine_bulk(DenseEngineArgs p) {
+__global__ void __launch_bounds__(256, SK_BULK_MINB) k_dense_engine_bulk(DenseEngineArgs p) {
   extern __shared__ __align__(128) uint8_t bulk_smem[];
   cg::grid_group grid = cg::this_grid();
   const bool blk = p.blk[0] != nullptr;
@@ -1145,6 +1157,35 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
 #ifndef SK_ROWS_WIDE_MIN
 #define SK_ROWS_WIDE_MIN 1024
 #endif
+#ifndef SK_ROWS_BULK
+#define SK_ROWS_BULK 1
+#endif
+// K1b standalone applies when the activations do not fit the L2 comfortably
+// (> 48 MB): there the in-order claim keeps one column panel hot.  Smaller
+// problems stay on the register-staged wide task (cfg2, 16 MB of Y: d = 0.1
+// 0.39 ms against 0.44 staged).
+static bool rows_bulk_applies(const sk_csr* w, uint32_t n) {
+  return SK_ROWS_BULK && size_t(w->cols) * n * 4 > (size_t(48) << 20);
+}
+
+// The staged wide task (K1b) as a standalone layer / mxm: a zeroed task counter
+// from the arena, one resident wave.
+template <typename Ops, int kEpi>
+static void launch_rows_bulk(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const float* y,
+                             uint32_t n, float clip, float* out) {
+  auto* kern = k_spmm_rows_bulk<Ops, kEpi>;
+  smem_attr(ctx, kern, int(bulk::kSmem));
+  const int per_sm = std::max(1, occupancy(ctx, kern, 256, bulk::kSmem));
+  const uint64_t warps = uint64_t((n + 255) / 256) * w->rows;
+  const unsigned grid = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((warps + 7) / 8, uint64_t(ctx->num_sms) * per_sm)));
+  arena_begin(ctx);
+  auto* work = reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, 1));
+  SK_CUDA(cudaMemsetAsync(work, 0, 8, ctx->stream));
+  SK_LAUNCH(kern, grid, 256, bulk::kSmem, ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n,
+            clip, out, ctx->d_err, work);
+  arena_end(ctx);
+}
 void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const float* y,
                         uint32_t n, float clip, float* out) {
   if (w->rows == 0 || n == 0) return;
@@ -1160,6 +1201,8 @@ void launch_layer_dense(sk_ctx* ctx, const sk_csr* w, const float* d_bias, const
   if (light)
     SK_LAUNCH((k_spmm_rows<OpArith, kEpiLayer, true, 4>), spmm_grid(ctx, w->rows, n, 4), 256, 0,
               ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n, clip, out, ctx->d_err);
+  else if (vec && n >= SK_ROWS_WIDE_MIN && rows_bulk_applies(w, n))
+    launch_rows_bulk<OpArith, kEpiLayer>(ctx, w, d_bias, y, n, clip, out);
   else if (vec && n >= SK_ROWS_WIDE_MIN)
     SK_LAUNCH((k_spmm_rows_wide<OpArith, kEpiLayer>), spmm_grid(ctx, w->rows, n, 2), 256, 0,
               ctx->stream, w->rp, w->ci, w->v, d_bias, y, w->rows, n, clip, out, ctx->d_err);
@@ -1181,7 +1224,10 @@ void launch_mxm_csr_dense(sk_ctx* ctx, const sk_csr* a, const float* b, uint32_t
   dispatch_semiring(s, [&](auto ops) {
     using Ops = decltype(ops);
     if (launch_narrow<Ops, kEpiNone>(ctx, a, nullptr, b, n, 0.0f, out)) return;
-    if (n % 4 == 0 && n >= SK_ROWS_WIDE_MIN && a->nnz > size_t(16) * a->rows)
+    if (n % 4 == 0 && n >= SK_ROWS_WIDE_MIN && a->nnz > size_t(16) * a->rows &&
+        rows_bulk_applies(a, n))
+      launch_rows_bulk<Ops, kEpiNone>(ctx, a, nullptr, b, n, 0.0f, out);
+    else if (n % 4 == 0 && n >= SK_ROWS_WIDE_MIN && a->nnz > size_t(16) * a->rows)
       SK_LAUNCH((k_spmm_rows_wide<Ops, kEpiNone>), spmm_grid(ctx, a->rows, n, 2), 256, 0,
                 ctx->stream, a->rp, a->ci, a->v, nullptr, b, a->rows, n, 0.0f, out, ctx->d_err);
     else if (n % 4 == 0)

@@ -208,3 +208,45 @@ def test_cfg2_full_size_both_legs(sk, ref, port, d):
     scale = np.abs(wd).astype(np.float64) @ np.abs(y).astype(np.float64)
     tol = np.maximum(1e-6, 1e-5 * scale)
     assert (np.abs(got_d.astype(np.float64) - want.astype(np.float64)) <= tol).all()
+
+
+def test_staged_wide_task_standalone_and_saturated_forward(sk, ref, port):
+    """K1b (the shared-memory-staged wide task with in-order task claiming):
+    * standalone, where the activations exceed the L2 budget (4096 x 4100:
+      67 MB, ragged last chunk): layer_step bitwise against the reference
+      (dnn.cpp:86-103 over matrix.cpp:403-424) and mxm(CsrMatrix, DenseMatrix)
+      under max-plus against the reference's mxm;
+    * in the engine on a saturating network (cfg3's construction at 2048
+      neurons, 50 % binary inputs, 6000 samples, 5 layers: every layer dense,
+      intermediate activations in panel-major scratch): relu_forward_sparse
+      bitwise against the oracle's sparse layers."""
+    m, n, seed = 4096, 4100, 7
+    hW = port.gen_layer_fixed(m, 24, port.layer_seed(seed, 0), float("nan"))
+    rng = np.random.default_rng(seed)
+    y = rng.uniform(0, 1, (m, n)).astype(np.float32)
+    y[rng.random((m, n)) < 0.25] = 0.0
+    b = rng.uniform(-0.3, 0.1, m).astype(np.float32)
+    W = sk.CsrMatrix(m, m, hW.row_ptr, hW.col_idx, hW.values)
+    yd = sk.DenseMatrix.from_numpy(y)
+    got = sk.layer_step(sk.Matrix(W), b, yd).numpy()
+    assert np.array_equal(bits(got), bits(ref.layer_step(hW, b, y, workers=8)))
+    got = sk.mxm(W, yd, sk.max_plus_semiring()).numpy()
+    assert np.array_equal(bits(got), bits(ref.mxm_csr_dense(hW, y, "max_plus")))
+    del got, yd, y
+
+    m, n, L = 2048, 6000, 5
+    hWs = [port.gen_layer_fixed(m, 32, port.layer_seed(SEED, k), 1.0 / 16) for k in range(L)]
+    bs = [np.full(m, -0.3, np.float32)] * L
+    hY = port.gen_input_binary(m, n, m // 2, SEED)
+    want, trace = hY, [hY.nnz]
+    for k in range(L):
+        want = port.layer_sparse(hWs[k], bs[k], want, 32.0)
+        trace.append(want.nnz)
+    assert trace[-1] > 0.9 * m * n  # saturated
+    ctx = sk.default_context()
+    model = sk.DnnModel([sk.CsrMatrix(m, m, w.row_ptr, w.col_idx, w.values) for w in hWs], bs)
+    Y0 = sk.CsrMatrix(m, n, hY.row_ptr, hY.col_idx, hY.values)
+    out, tr = sk.relu_forward_sparse(model, Y0, sk.ForwardOptions(clip=32.0))
+    assert ctx.layer_paths(L).count("dense") >= L - 1
+    assert [int(x) for x in tr] == trace
+    assert_same(out, want, "saturated forward")
