@@ -184,7 +184,7 @@ __device__ __forceinline__ void wait_pending() {
 }
 }  // namespace bulk
 
-template <typename Ops, int kEpi>
+template <typename Ops, int kEpi, bool kSrcBlk = false>
 __device__ __forceinline__ void spmm_tasks_bulk(const uint32_t* __restrict__ rp,
                                                 const uint32_t* __restrict__ ci,
                                                 const float* __restrict__ wv,
@@ -192,8 +192,7 @@ __device__ __forceinline__ void spmm_tasks_bulk(const uint32_t* __restrict__ rp,
                                                 const float* __restrict__ y, uint32_t m,
                                                 uint32_t n, float clip, float* __restrict__ out,
                                                 int* err, unsigned long long* nz_count,
-                                                uint8_t* smem, bool src_blk = false,
-                                                bool dst_blk = false,
+                                                uint8_t* smem, bool dst_blk = false,
                                                 unsigned long long* work = nullptr) {
   // work (a zeroed counter): tasks are claimed in order, one ahead, instead of
   // strided statically.  A column panel is only m / (warps in flight) ~ 5 tasks
@@ -202,7 +201,7 @@ __device__ __forceinline__ void spmm_tasks_bulk(const uint32_t* __restrict__ rp,
   // 15.7 GB of activations on four saturated 16384 x 60000 layers (5.8 TB/s:
   // DRAM-bound), 34 GB for 3.9 GB at 15000 samples.  Claimed in order, the
   // tasks in flight are always ~3500 consecutive rows of one panel.
-  // src_blk / dst_blk: the activations in PANEL-MAJOR layout -- element (row r,
+  // kSrcBlk / dst_blk: the activations in PANEL-MAJOR layout -- element (row r,
   // column j) at ((j / 256) * m + r) * 256 + j % 256 -- so the 256-column panel
   // a task sweep gathers from is one contiguous m KB instead of m segments a row
   // pitch apart (16384 x 60000: 3.9 GB spanned per panel, and the gathers' rate
@@ -241,7 +240,13 @@ __device__ __forceinline__ void spmm_tasks_bulk(const uint32_t* __restrict__ rp,
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[u][q] = Ops::zero();
     const uint32_t eb = rp[i], ee = rp[i + 1];
-    for (uint32_t e0 = eb; e0 < ee; e0 += 32) {
+    // this lane's first piece of row 0 of the task's panel
+    const float* const ybase = kSrcBlk ? y + size_t(c) * m * 256 + lane * 4 : y + col0;
+    const size_t pitch = kSrcBlk ? 256 : n;
+    // One group of <= 32 in-edges.  kFull: the chunk has all 256 columns (no
+    // column predicates); a group of exactly 32 runs without per-edge bounds.
+    auto group = [&](auto full_tag, uint32_t e0) {
+      constexpr bool kFull = decltype(full_tag)::value;
       const uint32_t cnt = min(32u, ee - e0);
       uint32_t kk = 0;
       float aa = 0.0f;
@@ -249,44 +254,75 @@ __device__ __forceinline__ void spmm_tasks_bulk(const uint32_t* __restrict__ rp,
         kk = ci[e0 + lane];
         aa = wv[e0 + lane];
       }
-      // in-edge t of the group into stage j = t % kS (a compile-time index: the
-      // fold loop is unrolled by kS)
+      // in-edge t into stage j (a compile-time index: the loops are unrolled by kS)
       auto issue = [&](uint32_t t, int j) {
-        if (t < cnt) {
-          const uint32_t k = __shfl_sync(0xffffffffu, kk, t & 31);
-          const float* src = src_blk ? y + (size_t(c) * m + k) * 256 + lane * 4
-                                     : y + size_t(k) * n + col0;
-          const uint32_t dst = mine_s + j * 1024;
-          if (in0) cp16(dst, src);
-          if (in1) cp16(dst + 512, src + 128);
-        }
-        commit();  // one group per step, empty past the end: the wait count stays fixed
+        const uint32_t k = __shfl_sync(0xffffffffu, kk, t & 31);
+        const float* src = ybase + size_t(k) * pitch;
+        const uint32_t dst = mine_s + j * 1024;
+        if (kFull || in0) cp16(dst, src);
+        if (kFull || in1) cp16(dst + 512, src + 128);
       };
-#pragma unroll
-      for (int j = 0; j < kS; ++j) issue(j, j);
-      for (uint32_t t0 = 0; t0 < cnt; t0 += kS) {
+      auto fold = [&](uint32_t t, int j) {
+        wait_pending<kS - 1>();
+        const float* const seg = mine + j * 256;
+        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+        if (kFull || in0) v0 = *reinterpret_cast<const float4*>(seg);
+        if (kFull || in1) v1 = *reinterpret_cast<const float4*>(seg + 128);
+        const float a = __shfl_sync(0xffffffffu, aa, t);
+        acc[0][0] = Ops::add(acc[0][0], Ops::mul(a, v0.x, err), err);
+        acc[0][1] = Ops::add(acc[0][1], Ops::mul(a, v0.y, err), err);
+        acc[0][2] = Ops::add(acc[0][2], Ops::mul(a, v0.z, err), err);
+        acc[0][3] = Ops::add(acc[0][3], Ops::mul(a, v0.w, err), err);
+        acc[1][0] = Ops::add(acc[1][0], Ops::mul(a, v1.x, err), err);
+        acc[1][1] = Ops::add(acc[1][1], Ops::mul(a, v1.y, err), err);
+        acc[1][2] = Ops::add(acc[1][2], Ops::mul(a, v1.z, err), err);
+        acc[1][3] = Ops::add(acc[1][3], Ops::mul(a, v1.w, err), err);
+      };
+      // one commit group per step, empty past the end: the wait count stays fixed
+      if (cnt == 32) {
 #pragma unroll
         for (int j = 0; j < kS; ++j) {
-          const uint32_t t = t0 + j;
-          if (t < cnt) {  // warp-uniform
-            wait_pending<kS - 1>();
-            const float* const seg = mine + j * 256;
-            float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-            if (in0) v0 = *reinterpret_cast<const float4*>(seg);
-            if (in1) v1 = *reinterpret_cast<const float4*>(seg + 128);
-            const float a = __shfl_sync(0xffffffffu, aa, t);
-            acc[0][0] = Ops::add(acc[0][0], Ops::mul(a, v0.x, err), err);
-            acc[0][1] = Ops::add(acc[0][1], Ops::mul(a, v0.y, err), err);
-            acc[0][2] = Ops::add(acc[0][2], Ops::mul(a, v0.z, err), err);
-            acc[0][3] = Ops::add(acc[0][3], Ops::mul(a, v0.w, err), err);
-            acc[1][0] = Ops::add(acc[1][0], Ops::mul(a, v1.x, err), err);
-            acc[1][1] = Ops::add(acc[1][1], Ops::mul(a, v1.y, err), err);
-            acc[1][2] = Ops::add(acc[1][2], Ops::mul(a, v1.z, err), err);
-            acc[1][3] = Ops::add(acc[1][3], Ops::mul(a, v1.w, err), err);
-            issue(t + kS, j);  // refills the stage just read (the values are in registers)
+          issue(j, j);
+          commit();
+        }
+#pragma unroll 1
+        for (uint32_t t0 = 0; t0 < 32 - kS; t0 += kS) {
+#pragma unroll
+          for (int j = 0; j < kS; ++j) {
+            fold(t0 + j, j);
+            issue(t0 + j + kS, j);  // refills the stage just read (its values are in registers)
+            commit();
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kS; ++j) {
+          fold(32 - kS + j, j);
+          commit();
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kS; ++j) {
+          if (uint32_t(j) < cnt) issue(j, j);
+          commit();
+        }
+        for (uint32_t t0 = 0; t0 < cnt; t0 += kS) {
+#pragma unroll
+          for (int j = 0; j < kS; ++j) {
+            const uint32_t t = t0 + j;
+            if (t < cnt) {  // warp-uniform
+              fold(t, j);
+              if (t + kS < cnt) issue(t + kS, j);
+              commit();
+            }
           }
         }
       }
+    };
+    static_assert(32 % kS == 0, "the 32-edge path unrolls whole rings");
+    const bool full = c + 1 < chunks || (n & 255u) == 0;
+    for (uint32_t e0 = eb; e0 < ee; e0 += 32) {
+      if (full) group(std::true_type{}, e0);
+      else group(std::false_type{}, e0);
     }
     float b = 0.0f;
     if (kEpi == kEpiLayer) b = bias[i];
@@ -322,7 +358,7 @@ __global__ void __launch_bounds__(256, SK_BULK_MINB)
                      float* __restrict__ out, int* err, unsigned long long* work) {
   extern __shared__ __align__(128) uint8_t bulk_smem[];
   spmm_tasks_bulk<Ops, kEpi>(rp, ci, wv, bias, y, m, n, clip, out, err, nullptr, bulk_smem, false,
-                             false, work);
+                             work);
 }
 
 template <typename Ops, int kEpi, bool kVec4, int kU = 1>
@@ -543,10 +579,14 @@ __global__ void __launch_bounds__(256, SK_BULK_MINB) k_dense_engine_bulk(DenseEn
     const bool sb = blk && k > 0, db = blk && !last;
     const float* src = k == 0 ? p.y0 : sb ? p.blk[(k - 1) & 1] : p.buf[(k - 1) & 1];
     float* dst = db ? p.blk[k & 1] : p.buf[k & 1];
-    spmm_tasks_bulk<OpArith, kEpiLayer>(p.w_rp[k], p.w_ci[k], p.w_v[k],
-                                        p.bias + size_t(k) * p.m, src, p.m, p.n, p.clip, dst,
-                                        p.err, p.nnz ? p.nnz + k : nullptr, bulk_smem, sb, db,
-                                        p.work ? p.work + k : nullptr);
+    if (sb)
+      spmm_tasks_bulk<OpArith, kEpiLayer, true>(
+          p.w_rp[k], p.w_ci[k], p.w_v[k], p.bias + size_t(k) * p.m, src, p.m, p.n, p.clip, dst,
+          p.err, p.nnz ? p.nnz + k : nullptr, bulk_smem, db, p.work ? p.work + k : nullptr);
+    else
+      spmm_tasks_bulk<OpArith, kEpiLayer, false>(
+          p.w_rp[k], p.w_ci[k], p.w_v[k], p.bias + size_t(k) * p.m, src, p.m, p.n, p.clip, dst,
+          p.err, p.nnz ? p.nnz + k : nullptr, bulk_smem, db, p.work ? p.work + k : nullptr);
     if (!last) {
       grid.sync();
       if (p.stop_below && *(volatile unsigned long long*)(p.nnz + k) < p.stop_below) {
