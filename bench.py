@@ -478,10 +478,10 @@ def run_sustained(sk, ctx, stream, R, args, pk, b0, Bl, Bg):
         "traffic_per_layer": tb, "traffic_source": trep,
         "algorithmic_bytes_per_layer": dense_layer_bytes(Bl, w["m"], nnzW[0]),
         "l2_to_sm_gbs": 4.0 * macs / (dense_ms / 1e3) / 1e9 if dense_ms > 0 else 0.0,
-        "measured_limiter": "latency of gathered 512-byte activation segments from L2 (4 B per "
-                            "MAC, no on-chip reuse for a random W): L2 35 %, L1/TEX 47 %, issue "
-                            "52 % busy, 40 % of cycles no eligible warp "
-                            "(profiles/r02/engine_wide_b60000_brief.txt)",
+        "measured_limiter": "L1/TEX data pipe 85 % (cp.async writes + shared reads of the staged "
+                            "activation segments), L2 76 %, issue 67 %; 4 B per MAC cross "
+                            "L2 -> SM (no on-chip reuse for a random W), DRAM traffic 1.02x the "
+                            "algorithmic bytes (profiles/r02/engine_staged_b60000_brief.txt)",
     }
     return {
         "workload": w["desc"], "value": edges / (ms / 1e3), "unit": "edges/s",
@@ -491,8 +491,9 @@ def run_sustained(sk, ctx, stream, R, args, pk, b0, Bl, Bg):
         "layer_paths": {p_: paths.count(p_) for p_ in sorted(set(paths))},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                     "kernel": "k_dense_engine (dense-activation layers: fused SpMM + "
-                               "bias/ReLU/clip)",
+                     "kernel": "k_dense_engine_bulk (K1b, dense-activation layers: fused SpMM + "
+                               "bias/ReLU/clip; activation segments staged through shared "
+                               "memory by cp.async, tasks claimed in panel order)",
                      "algorithmic_bytes": byts, "launch_ms": dense_ms,
                      "kernel_share_of_step": dense_ms / ms,
                      "fp32_macs_per_s": macs / (dense_ms / 1e3) if dense_ms > 0 else 0.0,
