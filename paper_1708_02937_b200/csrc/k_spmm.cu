@@ -1168,7 +1168,9 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
   // first reads and the last writes the caller's row-major buffers anyway)
   p.blk[0] = p.blk[1] = nullptr;
   p.work = nullptr;
-  const bool blocked = staged && p.L >= 3 && SK_ENG_BLOCKED != 0;
+  // (only while the two scratch copies stay small against the device)
+  const bool blocked = staged && p.L >= 3 && SK_ENG_BLOCKED != 0 &&
+                       double((n + 255) / 256) * 256.0 * m * 8.0 < 0.2 * double(ctx->total_mem);
   if (staged) {
     arena_begin(ctx);
     if (SK_ENG_CLAIM) {
