@@ -203,14 +203,26 @@ def _time_step(y0, layers: int, warmup: int, repetitions: int, step, stream) -> 
 
 
 def run_sweep(config: BenchConfig, progress: IO | None = None) -> SweepResult:
-    """bench.cpp run_sweep on the GPU (CUDA events on torch's current stream,
-    which the library is pointed at)."""
+    """bench.cpp run_sweep on the GPU: CUDA events on a dedicated stream that the
+    library is pointed at (the legacy default stream has handle 0, which
+    set_stream reads as "the library's own stream": events recorded there would
+    not bracket the kernels)."""
     import torch
     config.validate()
     ctx = sk.default_context()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
     ctx.set_stream(stream.cuda_stream)
     res = SweepResult([], [])
+    try:
+        _sweep_into(res, config, stream, progress)
+    finally:
+        ctx.synchronize()
+        ctx.set_stream(None)  # back to the library's own stream before `stream` goes away
+    res.records.sort(key=BenchRecord.key)
+    return res
+
+
+def _sweep_into(res: SweepResult, config: BenchConfig, stream, progress) -> None:
     workers = sorted(set(config.workers))
     for m in sorted(set(config.sizes)):
         for s in sorted(set(config.inverse_sparsities)):
@@ -246,8 +258,6 @@ def run_sweep(config: BenchConfig, progress: IO | None = None) -> SweepResult:
                 res.records.append(BenchRecord(m, s, Impl.sparse, wk, mean, sd, nnz, sparse_bytes))
                 if progress:
                     print(f"m={m} is={s:g} sparse workers={wk} mean={mean:g}s", file=progress)
-    res.records.sort(key=BenchRecord.key)
-    return res
 
 
 # ---- analysis (bench.cpp analyze) ---------------------------------------------------------
