@@ -26,7 +26,7 @@ def main():
     a = ap.parse_args()
     import torch
     ctx = sk.default_context()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real handle: 0 would mean the library's own stream
     ctx.set_stream(stream.cuda_stream)
     m, n, seed = 4096, 1024, 42
     y = sk.gen_input_dense(m, n, seed)

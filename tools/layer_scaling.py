@@ -22,7 +22,7 @@ Ls = [int(x) for x in a.layers.split(",")]
 Ws = [sk.gen_layer_fixed(m, 32, sk.layer_seed(42, k), 1.0 / 16) for k in range(max(Ls))]
 Y0 = sk.gen_input_binary(m, 60000, int(round(dens * m)), 42)
 ctx = sk.default_context()
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()  # a real handle: 0 would mean the library's own stream
 ctx.set_stream(stream.cuda_stream)
 ctx.set_timing(bool(a.timing))
 for L in Ls:

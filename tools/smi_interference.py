@@ -19,7 +19,8 @@ def main():
     wl = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
     w = bench.WORKLOADS[wl]
     ctx = sk.default_context()
-    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    stream = torch.cuda.Stream()  # a real handle: 0 would mean the library's own stream
+    ctx.set_stream(stream.cuda_stream)
     model, _ = bench.build_model(sk, w)
     Y0 = sk.gen_input_binary(w["m"], w["B"], bench.kY_of(w), bench.SEED)
     opts = sk.ForwardOptions(clip=w["clip"])
