@@ -47,13 +47,22 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
                                            const float* __restrict__ bias,
                                            const float* __restrict__ y, uint32_t m, uint32_t n,
                                            float clip, float* __restrict__ out, int* err,
-                                           unsigned long long* nz_count = nullptr) {
+                                           unsigned long long* nz_count = nullptr,
+                                           unsigned long long* work = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t nz = 0;  // nonzero outputs written by this lane (only when nz_count)
   const uint32_t chunks = (n + 128 * kU - 1) / (128 * kU);
   const uint64_t tasks = uint64_t(chunks) * m;
-  for (uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; task < tasks;
-       task += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+  // work (a zeroed counter): tasks claimed in order, one ahead (see K1b)
+  const uint64_t stride = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  uint64_t task = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (work) {
+    if (lane == 0) task = atomicAdd(work, 1ull);
+    task = __shfl_sync(0xffffffffu, task, 0);
+  }
+  for (; task < tasks;) {
+    unsigned long long claimed = 0;
+    if (work && lane == 0) claimed = atomicAdd(work, 1ull);
     // chunk-major: the live Y panel stays in L2 (a 32-bit divide where the
     // task count allows: the 64-bit one is ~100 instructions per task)
     uint32_t c, i;
@@ -143,6 +152,7 @@ __device__ __forceinline__ void spmm_tasks(const uint32_t* __restrict__ rp,
           if (col0 + q < n) orow[col0 + q] = acc[u][q];
       }
     }
+    task = work ? __shfl_sync(0xffffffffu, claimed, 0) : task + stride;
   }
   if (nz_count) {  // warp-uniform: nz_count is a kernel argument
 #pragma unroll
@@ -545,6 +555,9 @@ struct DenseEngineArgs {
 #ifndef SK_ENG_CLAIM
 #define SK_ENG_CLAIM 1
 #endif
+#ifndef SK_ENG_CLAIM_REG
+#define SK_ENG_CLAIM_REG 1
+#endif
 template <bool kVec4, int kU = 1>
 __global__ void __launch_bounds__(256, kU == 1 ? SK_SPMM_MINB : SK_ENG_MINB)
     k_dense_engine(DenseEngineArgs p) {
@@ -554,7 +567,7 @@ __global__ void __launch_bounds__(256, kU == 1 ? SK_SPMM_MINB : SK_ENG_MINB)
     float* dst = (k & 1) ? p.buf[1] : p.buf[0];
     spmm_tasks<OpArith, kEpiLayer, kVec4, kU, (kU == 1 ? SK_SPMM_BATCH : SK_ENG_BATCH)>(
         p.w_rp[k], p.w_ci[k], p.w_v[k], p.bias + size_t(k) * p.m, src, p.m, p.n, p.clip, dst,
-        p.err, p.nnz ? p.nnz + k : nullptr);
+        p.err, p.nnz ? p.nnz + k : nullptr, p.work ? p.work + k : nullptr);
     if (k + 1 < p.L) {
       grid.sync();
       if (p.stop_below && *(volatile unsigned long long*)(p.nnz + k) < p.stop_below) {
@@ -1171,7 +1184,8 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
   // (only while the two scratch copies stay small against the device)
   const bool blocked = staged && p.L >= 3 && SK_ENG_BLOCKED != 0 &&
                        double((n + 255) / 256) * 256.0 * m * 8.0 < 0.2 * double(ctx->total_mem);
-  if (staged) {
+  const bool claim = staged || (wide && SK_ENG_CLAIM_REG != 0);
+  if (claim) {
     arena_begin(ctx);
     if (SK_ENG_CLAIM) {
       p.work = reinterpret_cast<unsigned long long*>(aalloc<uint64_t>(ctx, p.L));
@@ -1193,7 +1207,7 @@ void dense_forward_engine(sk_ctx* ctx, const sk_model* md, uint32_t k0, const fl
   SK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, esmem, ctx->stream));
   g_launches.fetch_add(1);
   timing_mark(ctx);
-  if (staged) arena_end(ctx);  // stream-ordered: later arena users queue behind the engine
+  if (claim) arena_end(ctx);  // stream-ordered: later arena users queue behind the engine
 }
 
 #ifndef SK_ROWS_WIDE_MIN
